@@ -1,0 +1,177 @@
+/*
+ * flashmp_b200.h -- C ABI of the B200-native FlashMP hot path (libflashmp_b200.so).
+ *
+ * The reference (arXiv 2508.07193 "FlashMP", pure Python package `flashmp`) has no
+ * native boundary: its hot path is the duck-typed Python interface
+ *     op.apply(list) -> list            ref: pkg/src/flashmp/schwarz.py:377-388
+ *     prec.apply(list) -> list          ref: pkg/src/flashmp/schwarz.py:320-339
+ *     bicgstab/gmres(op, prec, b, cfg)  ref: pkg/src/flashmp/krylov.py:146, 242
+ * backed by numpy/scipy calls.  Each entry point below replaces one of those calls;
+ * the Python package `paper_2508_07193_b200` binds them with ctypes and keeps the
+ * reference class names and signatures on top.
+ *
+ * Conventions
+ *  - All pointers are DEVICE pointers unless stated; all arithmetic is FP64.
+ *  - A field is component-major (3, bz, by, bx), x fastest: the reference layout
+ *    (ref: pkg/src/flashmp/grid.py:1-14) restricted to one GPU's block.
+ *  - `stream` is a cudaStream_t passed as void*; every call is asynchronous on it.
+ *  - Return value: 0 on success, negative on error; fmp_last_error() gives the text.
+ *    Nothing on an apply path allocates device memory; callers own every buffer.
+ *  - Reductions are deterministic: fixed-order two-level trees, no atomics.
+ */
+#ifndef FLASHMP_B200_H
+#define FLASHMP_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FMP_ABI_VERSION 1
+
+/* ---------------------------------------------------------------- geometry */
+
+/* One GPU's block of the global grid plus its ghost shell.
+ * A point (c,k,j,i) in block-local coordinates outside [0,b*) reads
+ *   0                       when it lies outside the global box (zero-ghost Dirichlet,
+ *                           ref: pkg/src/flashmp/operators.py:1-21), otherwise
+ *   ghost[0|1] (x-lo|hi)    shape (3, bz+2P, by+2P, P)   when i is outside,
+ *   ghost[2|3] (y-lo|hi)    shape (3, bz+2P, P, bx)      when only j/k are outside and j is,
+ *   ghost[4|5] (z-lo|hi)    shape (3, P, by, bx)         when only k is outside.
+ * Single-GPU blocks cover the global box and pass NULL ghosts. */
+typedef struct fmp_block {
+  int64_t bx, by, bz;          /* block extents */
+  int64_t gx0, gy0, gz0;       /* global coordinates of the block origin */
+  int64_t nx, ny, nz;          /* global extents */
+  int64_t halo;                /* ghost width P (>= 1 when any ghost is set) */
+  const double* ghost[6];
+} fmp_block;
+
+int fmp_abi_version(void);
+int fmp_last_error(char* buf, size_t len);
+/* Scratch (in doubles) every reduction entry point below needs. */
+int64_t fmp_reduce_scratch_doubles(void);
+
+/* ---------------------------------------------------------------- stencils (K7/K13)
+ * y = x + alpha*(C_b C_f x + Lambda x) with boundary=1, the corrected operator
+ *   ref: pkg/src/flashmp/operators.py:167-175 (apply_operator) and the CSR blocks of
+ *   DistributedOperator.apply, ref: pkg/src/flashmp/schwarz.py:377-388;
+ * boundary=0 drops Lambda (ref: operators.py:172-173, with_boundary=False).
+ * mode: 0 = y only; 1 = y and dots[0] = (y, w); 2 = y, dots[0] = (y, w), dots[1] = (y, y);
+ *       3 = no y: dots[0] = ||w - A x||^2   (the true-residual check, ref: krylov.py:139-143).
+ * dots is a device pointer to >= 2 doubles; scratch has fmp_reduce_scratch_doubles(). */
+int fmp_stencil_apply(const fmp_block* blk, double alpha, int boundary, int mode,
+                      const double* x, double* y, const double* w,
+                      double* dots, double* scratch, void* stream);
+
+/* out = curl_f(x) (kind 0) or curl_b(x) (kind 1)      ref: operators.py:119-125 */
+int fmp_curl(const fmp_block* blk, int kind, const double* x, double* out, void* stream);
+
+/* CN right-hand side R = E + dt*curl_b(H) - (dt^2/4)*C_b C_f E    ref: cn_driver.py:54-59.
+ * blkE / blkH carry the ghosts of E and H respectively. */
+int fmp_cn_rhs(const fmp_block* blkE, const fmp_block* blkH, double dt,
+               const double* E, const double* H, double* R, void* stream);
+
+/* H_new = H - dt/2 (curl_f(E_new) + curl_f(E_old))               ref: cn_driver.py:90-91 */
+int fmp_cn_h_update(const fmp_block* blkNew, const fmp_block* blkOld, double dt,
+                    const double* H, const double* E_new, const double* E_old,
+                    double* H_new, void* stream);
+
+/* ---------------------------------------------------------------- Krylov vectors (K8)
+ * n = number of doubles.  Elementwise results are rounded exactly as numpy evaluates
+ * the reference expressions (products and sums rounded separately, no FMA
+ * contraction), so they match the reference bit for bit on equal inputs.      */
+/* out = a*x + b*y                     ref: krylov.py:120-123 (_Dist.lincomb) */
+int fmp_vec_lincomb(int64_t n, double a, const double* x, double b, const double* y,
+                    double* out, void* stream);
+/* y += a*x                            ref: krylov.py:125-129 (_Dist.axpy_into) */
+int fmp_vec_axpy(int64_t n, double a, const double* x, double* y, void* stream);
+/* out = a*x                           ref: krylov.py:131-133 (_Dist.scale) */
+int fmp_vec_scale(int64_t n, double a, const double* x, double* out, void* stream);
+/* out[0] = (x, y)                     ref: krylov.py:108-112 (_Dist.dot) */
+int fmp_vec_dot(int64_t n, const double* x, const double* y, double* out,
+                double* scratch, void* stream);
+/* BiCGSTAB p-update, in place: p = r + beta*(p + (-omega)*v)   ref: krylov.py:181-182 */
+int fmp_bicg_p(int64_t n, const double* r, double* p, const double* v,
+               double beta, double omega, void* stream);
+/* BiCGSTAB tail: x += alpha*p_hat; x += omega*s_hat; r = s + (-omega)*t;
+ * then dots[0] = (r_shadow, r_new) -- the next iteration's rho. ref: krylov.py:213-216, 171 */
+int fmp_bicg_xr(int64_t n, double* x, const double* p_hat, const double* s_hat,
+                const double* s, const double* t, double* r, const double* r_shadow,
+                double alpha, double omega, double* dots, double* scratch, void* stream);
+
+/* ---------------------------------------------------------------- subdomain solves (K1-K5)
+ * A preconditioner plan batches every subdomain of one GPU block.  Subdomains are
+ * grouped by extended shape; each shape shares its SVD factors and its dense C^-1.
+ * Descriptors are plain int64 records in device memory (layout below). */
+
+typedef struct fmp_subdomain {   /* 16 x int64 */
+  int64_t ext[3];        /* extended box extents (ex, ey, ez) */
+  int64_t ext_lo[3];     /* extended box origin in block-local coordinates (may be < 0) */
+  int64_t own_off[3];    /* owned tile offset inside the extended box */
+  int64_t own[3];        /* owned tile extents */
+  int64_t shape;         /* index into the shape table */
+  int64_t column;        /* column of this subdomain in its shape's Y/Z matrices */
+  int64_t ws_off;        /* element offset of this subdomain's 3*V_ext workspace slot */
+  int64_t in_off;        /* element offset of this subdomain's input for compact inputs (mode FACES) */
+} fmp_subdomain;
+
+typedef struct fmp_shape {       /* 16 x int64 */
+  int64_t ext[3];
+  int64_t m;             /* boundary-correction size (ref: subdomain.py:235-238) */
+  int64_t m_comp[3];     /* rows per component */
+  int64_t ut_off[3];     /* offset (doubles) of U^T per axis in the factor buffer */
+  int64_t vt_off[3];     /* offset of V^T per axis */
+  int64_t s_off[3];      /* offset of the singular values per axis */
+} fmp_shape;
+#define FMP_SUBDOMAIN_WORDS 16
+#define FMP_SHAPE_WORDS 16
+
+typedef struct fmp_precond_desc {
+  double alpha;
+  int64_t n_sub, n_shape;
+  const fmp_subdomain* subs;     /* device, n_sub records, grouped by shape */
+  const fmp_shape* shapes;       /* device, n_shape records */
+  const fmp_subdomain* subs_host;/* host copy (launch geometry) */
+  const fmp_shape* shapes_host;  /* host copy */
+  const int64_t* shape_first;    /* host: first subdomain of each shape (n_shape+1 entries) */
+  const double* factors;         /* device: concatenated U^T, V^T, S blocks */
+  const double* const* cinv;     /* host array of n_shape device pointers to m x m C^-1 */
+  double* work_a;                /* device workspace, >= sum 3*V_ext (+ padding) doubles */
+  double* work_b;                /* device workspace, same size */
+  double* corr;                  /* device: n_sub * 6 * pmax^2 doubles (correction planes) */
+  double* const* ymat;           /* host array of n_shape device pointers, m x n_s each */
+  double* const* zmat;           /* host array of n_shape device pointers, m x n_s each */
+  int64_t pmax;                  /* max extent over all shapes */
+} fmp_precond_desc;
+
+typedef struct fmp_precond fmp_precond;
+
+int fmp_precond_create(const fmp_precond_desc* desc, fmp_precond** out);
+int fmp_precond_destroy(fmp_precond* p);
+
+/* Solve modes */
+#define FMP_SOLVE_WOODBURY 0  /* full RAS apply: z(owned) = A_i^-1 S_i r   (schwarz.py:320-339) */
+#define FMP_SOLVE_EXACT    1  /* (I + alpha M)^-1 only, no boundary correction (subdomain.py:255-262) */
+#define FMP_SOLVE_FACES    2  /* Y[:, col] = ((I + alpha M)^-1 r_i)[rows]: C assembly (subdomain.py:196-204) */
+
+/* RAS apply over every subdomain of the block.
+ * mode WOODBURY/EXACT: input r is a block field (ghosts in blk), output z is a block
+ *   field; each subdomain writes its owned tile (disjoint, so z is fully written when
+ *   the owned tiles cover the block).
+ * mode FACES: input r holds compact per-subdomain fields at in_off; output goes to
+ *   the shape's Y matrices (z unused). */
+int fmp_precond_apply(fmp_precond* p, const fmp_block* blk, int mode,
+                      const double* r, double* z, void* stream);
+
+/* Restriction only: out[ws_off(i) ...] = S_i^gamma r for every subdomain i, in the
+ * reference's extended-vector order (ref:schwarz.py:217-257).  out has the plan's
+ * workspace size.  Exposes the index maps of the fused solve for bit-exact tests. */
+int fmp_precond_restrict(fmp_precond* p, const fmp_block* blk, const double* r, double* out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FLASHMP_B200_H */

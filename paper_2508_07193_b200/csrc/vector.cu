@@ -1,0 +1,169 @@
+// Krylov vector kernels (K8) and the deterministic reduction tail (K9's on-device half).
+//
+// Elementwise updates reproduce numpy's evaluation of the reference expressions
+// (ref:krylov.py:114-136): every product and every sum is rounded on its own
+// (__dmul_rn/__dadd_rn forbid FMA contraction), so equal inputs give equal bits.
+// Roofline: HBM-bound; bytes per double = 8 x (vectors read + written).
+#include <cstdarg>
+#include <cstring>
+#include "common.cuh"
+
+namespace fmp {
+
+static thread_local char g_err[512] = "";
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof g_err, fmt, ap);
+  va_end(ap);
+}
+
+// ---------------------------------------------------------------- reduction tail
+template <int ND>
+__global__ void __launch_bounds__(1024) k_finish(const double* __restrict__ partials, int count, double* out) {
+  __shared__ double red[32];
+#pragma unroll
+  for (int q = 0; q < ND; ++q) {
+    double v = 0.0;
+    for (int b = threadIdx.x; b < count; b += blockDim.x) v += partials[q * count + b];
+    v = block_sum<1024>(v, red);
+    if (threadIdx.x == 0) out[q] = v;
+  }
+}
+
+int finish_reduce(const double* partials, int count, int nd, double* out, cudaStream_t st) {
+  if (nd == 1)
+    k_finish<1><<<1, 1024, 0, st>>>(partials, count, out);
+  else
+    k_finish<2><<<1, 1024, 0, st>>>(partials, count, out);
+  FMP_CHECK_LAUNCH();
+  return 0;
+}
+
+// ---------------------------------------------------------------- elementwise
+__global__ void k_lincomb(int64_t n, double a, const double* __restrict__ x, double b, const double* __restrict__ y,
+                          double* __restrict__ out) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x)
+    out[q] = add_rn(mul_rn(a, x[q]), mul_rn(b, y[q]));
+}
+
+__global__ void k_axpy(int64_t n, double a, const double* __restrict__ x, double* __restrict__ y) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x)
+    y[q] = add_rn(y[q], mul_rn(a, x[q]));
+}
+
+__global__ void k_scale(int64_t n, double a, const double* __restrict__ x, double* __restrict__ out) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x)
+    out[q] = mul_rn(a, x[q]);
+}
+
+__global__ void __launch_bounds__(kVecThreads) k_dot(int64_t n, const double* __restrict__ x,
+                                                     const double* __restrict__ y, double* __restrict__ partials) {
+  __shared__ double red[kVecThreads / 32];
+  double acc = 0.0;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x)
+    acc = fma(x[q], y[q], acc);
+  acc = block_sum<kVecThreads>(acc, red);
+  if (threadIdx.x == 0) partials[blockIdx.x] = acc;
+}
+
+// p = 1.0*r + beta*(1.0*p + (-omega)*v)     (ref:krylov.py:181-182)
+__global__ void k_bicg_p(int64_t n, const double* __restrict__ r, double* __restrict__ p,
+                         const double* __restrict__ v, double beta, double momega) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x) {
+    const double p1 = add_rn(p[q], mul_rn(momega, v[q]));
+    p[q] = add_rn(r[q], mul_rn(beta, p1));
+  }
+}
+
+// x += alpha*p_hat; x += omega*s_hat; r = 1.0*s + (-omega)*t; rho_next partial = (r_shadow, r)
+// (ref:krylov.py:213-215 and the next iteration's krylov.py:171)
+__global__ void __launch_bounds__(kVecThreads) k_bicg_xr(int64_t n, double* __restrict__ x,
+                                                         const double* __restrict__ ph,
+                                                         const double* __restrict__ sh,
+                                                         const double* __restrict__ s,
+                                                         const double* __restrict__ t, double* __restrict__ r,
+                                                         const double* __restrict__ rs, double alpha,
+                                                         double omega, double* __restrict__ partials) {
+  __shared__ double red[kVecThreads / 32];
+  double acc = 0.0;
+  const double momega = -omega;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x) {
+    double xv = add_rn(x[q], mul_rn(alpha, ph[q]));
+    x[q] = add_rn(xv, mul_rn(omega, sh[q]));
+    const double rv = add_rn(s[q], mul_rn(momega, t[q]));
+    r[q] = rv;
+    acc = fma(rs[q], rv, acc);
+  }
+  acc = block_sum<kVecThreads>(acc, red);
+  if (threadIdx.x == 0) partials[blockIdx.x] = acc;
+}
+
+static inline int vec_grid(int64_t n) {
+  const int64_t need = (n + kVecThreads - 1) / kVecThreads;
+  return (int)(need < kVecGrid ? (need > 0 ? need : 1) : kVecGrid);
+}
+
+}  // namespace fmp
+
+using namespace fmp;
+
+extern "C" int fmp_abi_version(void) { return FMP_ABI_VERSION; }
+
+extern "C" int fmp_last_error(char* buf, size_t len) {
+  if (!buf || !len) return -1;
+  strncpy(buf, g_err, len - 1);
+  buf[len - 1] = 0;
+  return 0;
+}
+
+extern "C" int64_t fmp_reduce_scratch_doubles(void) { return kScratchDoubles; }
+
+extern "C" int fmp_vec_lincomb(int64_t n, double a, const double* x, double b, const double* y, double* out,
+                               void* stream) {
+  if (n <= 0) return 0;
+  k_lincomb<<<vec_grid(n), kVecThreads, 0, as_stream(stream)>>>(n, a, x, b, y, out);
+  FMP_CHECK_LAUNCH();
+  return 0;
+}
+
+extern "C" int fmp_vec_axpy(int64_t n, double a, const double* x, double* y, void* stream) {
+  if (n <= 0) return 0;
+  k_axpy<<<vec_grid(n), kVecThreads, 0, as_stream(stream)>>>(n, a, x, y);
+  FMP_CHECK_LAUNCH();
+  return 0;
+}
+
+extern "C" int fmp_vec_scale(int64_t n, double a, const double* x, double* out, void* stream) {
+  if (n <= 0) return 0;
+  k_scale<<<vec_grid(n), kVecThreads, 0, as_stream(stream)>>>(n, a, x, out);
+  FMP_CHECK_LAUNCH();
+  return 0;
+}
+
+extern "C" int fmp_vec_dot(int64_t n, const double* x, const double* y, double* out, double* scratch, void* stream) {
+  const int grid = vec_grid(n);
+  cudaStream_t st = as_stream(stream);
+  k_dot<<<grid, kVecThreads, 0, st>>>(n, x, y, scratch);
+  FMP_CHECK_LAUNCH();
+  return finish_reduce(scratch, grid, 1, out, st);
+}
+
+extern "C" int fmp_bicg_p(int64_t n, const double* r, double* p, const double* v, double beta, double omega,
+                          void* stream) {
+  if (n <= 0) return 0;
+  k_bicg_p<<<vec_grid(n), kVecThreads, 0, as_stream(stream)>>>(n, r, p, v, beta, -omega);
+  FMP_CHECK_LAUNCH();
+  return 0;
+}
+
+extern "C" int fmp_bicg_xr(int64_t n, double* x, const double* p_hat, const double* s_hat, const double* s,
+                           const double* t, double* r, const double* r_shadow, double alpha, double omega,
+                           double* dots, double* scratch, void* stream) {
+  const int grid = vec_grid(n);
+  cudaStream_t st = as_stream(stream);
+  k_bicg_xr<<<grid, kVecThreads, 0, st>>>(n, x, p_hat, s_hat, s, t, r, r_shadow, alpha, omega, scratch);
+  FMP_CHECK_LAUNCH();
+  return finish_reduce(scratch, grid, 1, dots, st);
+}

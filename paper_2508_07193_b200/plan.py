@@ -1,0 +1,167 @@
+"""Host-side builder of a batched subdomain-solve plan (fmp_precond in the C ABI).
+
+A plan covers a list of subdomains that share one input field (a GPU block, or
+compact per-column inputs during precompute).  Subdomains are grouped by
+extended shape; every shape carries its SVD factors, its correction rows and
+(for Woodbury solves) its dense C^-1.  All buffers are torch CUDA tensors owned
+by the plan; the C library only sees their addresses.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .transform import svd_of_difference
+
+
+@dataclass(frozen=True)
+class SubSpec:
+    """One subdomain: extended box + owned tile, in block-local coordinates."""
+
+    ext: tuple[int, int, int]
+    ext_lo: tuple[int, int, int]
+    own_off: tuple[int, int, int]
+    own: tuple[int, int, int]
+    in_off: int = 0
+
+
+def correction_counts(ext) -> tuple[int, int, int]:
+    """Rows per component (ref:subdomain.py:235-238)."""
+    nx, ny, nz = ext
+    return (nx * (ny + nz - 1), ny * (nx + nz - 1), nz * (nx + ny - 1))
+
+
+class FactorTable:
+    """U^T, V^T (row-major) and S for every distinct axis extent, in one device buffer."""
+
+    def __init__(self, extents, device):
+        blocks, self.offsets, off = [], {}, 0
+        for n in sorted(set(extents)):
+            s = svd_of_difference(n)
+            ut, vt = np.ascontiguousarray(s.U.T), np.ascontiguousarray(s.Vt)
+            self.offsets[n] = (off, off + n * n, off + 2 * n * n)
+            blocks += [ut.ravel(), vt.ravel(), s.S.ravel()]
+            off += 2 * n * n + n
+            pad = (-off) % 8
+            if pad:
+                blocks.append(np.zeros(pad))
+                off += pad
+        self.host = np.concatenate(blocks) if blocks else np.zeros(1)
+        self.device = torch.from_numpy(self.host).to(device)
+
+
+class SolvePlan:
+    """Batched FlashMP subdomain solves over `subs` (see csrc/precond.cu)."""
+
+    def __init__(self, subs: list[SubSpec], alpha: float, device, cinv: dict | None = None,
+                 need_woodbury: bool = True):
+        _lib.lib()
+        self.device = torch.device(device)
+        self.alpha = float(alpha)
+        shapes: list[tuple[int, int, int]] = []
+        for s in subs:
+            if s.ext not in shapes:
+                shapes.append(s.ext)
+        order = sorted(range(len(subs)), key=lambda q: shapes.index(subs[q].ext))
+        self.subs = [subs[q] for q in order]
+        self.order = order
+        self.shapes = shapes
+        self.factors = FactorTable([n for e in shapes for n in e], self.device)
+        self.pmax = max(max(e) for e in shapes)
+        # ---- shape table
+        sh_rec = np.zeros((len(shapes), 16), dtype=np.int64)
+        self.m = []
+        for q, e in enumerate(shapes):
+            mc = correction_counts(e)
+            self.m.append(sum(mc))
+            offs = [self.factors.offsets[n] for n in e]
+            sh_rec[q] = [*e, sum(mc), *mc, *(o[0] for o in offs), *(o[1] for o in offs), *(o[2] for o in offs)]
+        # ---- subdomain table, workspace layout
+        sub_rec = np.zeros((len(self.subs), 16), dtype=np.int64)
+        first = np.zeros(len(shapes) + 1, dtype=np.int64)
+        col_of_shape = [0] * len(shapes)
+        ws = 0
+        for q, s in enumerate(self.subs):
+            sid = shapes.index(s.ext)
+            sub_rec[q] = [*s.ext, *s.ext_lo, *s.own_off, *s.own, sid, col_of_shape[sid], ws, s.in_off]
+            col_of_shape[sid] += 1
+            ws += (3 * int(np.prod(s.ext)) + 7) // 8 * 8
+        for q in range(len(shapes)):
+            first[q + 1] = first[q] + col_of_shape[q]
+        self.ncols = col_of_shape
+        self.ws_size = ws
+        self._sub_host, self._sh_host, self._first = sub_rec, sh_rec, first
+        self.sub_dev = torch.from_numpy(sub_rec).to(self.device)
+        self.sh_dev = torch.from_numpy(sh_rec).to(self.device)
+        f64 = dict(dtype=torch.float64, device=self.device)
+        self.work_a = torch.empty(ws, **f64)
+        self.work_b = torch.empty(ws, **f64)
+        self.corr = torch.zeros(len(self.subs) * 6 * self.pmax * self.pmax, **f64)
+        # per-shape Y/Z matrices (column-major m x ncols == row-major (ncols, m))
+        self.ymat = [torch.zeros((max(1, n), m), **f64) for n, m in zip(self.ncols, self.m)]
+        self.zmat = [torch.zeros((max(1, n), m), **f64) for n, m in zip(self.ncols, self.m)]
+        self.cinv = []
+        for e, m in zip(shapes, self.m):
+            t = (cinv or {}).get(e)
+            if t is None:
+                if need_woodbury:
+                    raise ValueError(f"missing C^-1 for shape {e}")
+                t = torch.zeros(1, **f64)
+            elif t.shape != (m, m) or t.dtype != torch.float64 or not t.is_contiguous():
+                raise ValueError(f"C^-1 for {e} must be a contiguous float64 ({m}, {m}) tensor")
+            self.cinv.append(t)
+        P = C.c_void_p
+        self._cinv_arr = (P * len(shapes))(*[t.data_ptr() for t in self.cinv])
+        self._y_arr = (P * len(shapes))(*[t.data_ptr() for t in self.ymat])
+        self._z_arr = (P * len(shapes))(*[t.data_ptr() for t in self.zmat])
+        desc = _lib.FmpPrecondDesc()
+        desc.alpha = self.alpha
+        desc.n_sub, desc.n_shape = len(self.subs), len(shapes)
+        desc.subs, desc.shapes = self.sub_dev.data_ptr(), self.sh_dev.data_ptr()
+        desc.subs_host, desc.shapes_host = sub_rec.ctypes.data, sh_rec.ctypes.data
+        desc.shape_first = first.ctypes.data
+        desc.factors = self.factors.device.data_ptr()
+        desc.cinv = C.cast(self._cinv_arr, P)
+        desc.work_a, desc.work_b = self.work_a.data_ptr(), self.work_b.data_ptr()
+        desc.corr = self.corr.data_ptr()
+        desc.ymat, desc.zmat = C.cast(self._y_arr, P), C.cast(self._z_arr, P)
+        desc.pmax = self.pmax
+        handle = C.c_void_p()
+        _lib.check(_lib.lib().fmp_precond_create(C.byref(desc), C.byref(handle)), "fmp_precond_create")
+        self._handle = handle
+
+    def apply(self, blk: _lib.FmpBlock, mode: int, r: torch.Tensor, z: torch.Tensor | None) -> None:
+        _lib.check(_lib.lib().fmp_precond_apply(self._handle, C.byref(blk), mode, _lib.ptr(r),
+                                                _lib.ptr(z) if z is not None else None, _lib.stream()),
+                   "fmp_precond_apply")
+
+    def restrict(self, blk: _lib.FmpBlock, r: torch.Tensor) -> torch.Tensor:
+        """Every subdomain's extended vector, concatenated in plan order at ws offsets."""
+        out = torch.empty_like(self.work_a)
+        _lib.check(_lib.lib().fmp_precond_restrict(self._handle, C.byref(blk), _lib.ptr(r), _lib.ptr(out),
+                                                   _lib.stream()), "fmp_precond_restrict")
+        return out
+
+    def __del__(self):
+        h = getattr(self, "_handle", None)
+        if h is not None and h.value and _lib._LIB is not None:
+            _lib._LIB.fmp_precond_destroy(h)
+            self._handle = None
+
+
+def block_struct(bx, by, bz, origin=(0, 0, 0), global_ext=None, halo=0, ghosts=None) -> _lib.FmpBlock:
+    """fmp_block for a field of extents (bx, by, bz) at `origin` inside `global_ext`."""
+    b = _lib.FmpBlock()
+    b.bx, b.by, b.bz = bx, by, bz
+    b.gx0, b.gy0, b.gz0 = origin
+    b.nx, b.ny, b.nz = global_ext if global_ext is not None else (bx, by, bz)
+    b.halo = halo
+    for q in range(6):
+        g = None if ghosts is None else ghosts[q]
+        b.ghost[q] = g.data_ptr() if g is not None else None
+    return b

@@ -1,0 +1,545 @@
+"""Domain decomposition, halo exchange and the RAS preconditioner (mirror of ref:schwarz.py).
+
+Two levels of decomposition:
+
+* the reference's subdomain partition (`make_partition`, identical geometry and rank
+  order, ref:schwarz.py:78-123): the preconditioner's mathematics depends only on it;
+* the GPU decomposition: one process per GPU owns a contiguous block of subdomain
+  tiles (`BlockLayout`, GPU grid = the reference CLI's `_proc_grid_for(N)`,
+  ref:cli.py:214-231).  Inside a GPU, a subdomain's overlap region is read straight
+  from the block field -- no halo copy at all; across GPUs the block's ghost shell is
+  filled by a three-phase (z, y, x) face exchange over NCCL, which also carries edges
+  and corners.
+
+Vectors are per-GPU block tensors (3, bz, by, bx) in the reference's component-major
+order.  The reference's list-of-rank-vectors form is accepted on a single GPU for
+drop-in use (converted at the boundary).
+"""
+
+from __future__ import annotations
+
+import os
+from dataclasses import dataclass
+from itertools import product
+
+import numpy as np
+import torch
+
+from . import _lib
+from .grid import Box, FieldVector
+from .instrument import NULL_TIMER
+from .operators import OperatorParams
+from .plan import SolvePlan, SubSpec, block_struct
+from . import subdomain
+
+Range3 = tuple[tuple[int, int], tuple[int, int], tuple[int, int]]
+
+
+class CommunicationError(RuntimeError):
+    """Mismatched collective participation or lost halo message (ref:schwarz.py:45)."""
+
+
+# ---------------------------------------------------------------------------- geometry
+@dataclass(frozen=True)
+class RankGeometry:
+    rank: int
+    coords: tuple[int, int, int]
+    owned_lo: tuple[int, int, int]
+    owned: Box
+    ext_lo: tuple[int, int, int]
+    ext: Box
+    neighbors: tuple[tuple[tuple[int, int, int], int], ...]
+
+    def owned_range(self) -> Range3:
+        return tuple((lo, lo + n) for lo, n in zip(self.owned_lo, self.owned.extents))
+
+    def ext_range(self) -> Range3:
+        return tuple((lo, lo + n) for lo, n in zip(self.ext_lo, self.ext.extents))
+
+
+@dataclass(frozen=True)
+class Partition:
+    global_box: Box
+    proc_grid: tuple[int, int, int]
+    overlap: int
+    ranks: tuple[RankGeometry, ...]
+
+    @property
+    def nranks(self) -> int:
+        return len(self.ranks)
+
+
+def make_partition(global_box: Box, proc_grid: tuple[int, int, int], overlap: int) -> Partition:
+    """Owned tiles + extended boxes clamped at the physical boundary, rank x-fastest
+    (ref:schwarz.py:78-123; same validation messages)."""
+    grid = tuple(int(p) for p in proc_grid)
+    if min(grid) < 1:
+        raise ValueError(f"process grid must be positive, got {proc_grid}")
+    if overlap < 0:
+        raise ValueError(f"overlap must be >= 0, got {overlap}")
+    for n, p, ax in zip(global_box.extents, grid, "xyz"):
+        if n % p:
+            raise ValueError(f"extent {n} along {ax} not divisible by grid {p}")
+    tile = tuple(n // p for n, p in zip(global_box.extents, grid))
+    if overlap > min(tile):
+        raise ValueError(f"overlap {overlap} exceeds smallest tile extent {min(tile)}")
+    px, py, pz = grid
+    rank_of = lambda c: c[0] + px * (c[1] + py * c[2])
+    ranks = []
+    for cz, cy, cx in product(range(pz), range(py), range(px)):
+        c = (cx, cy, cz)
+        lo = tuple(q * t for q, t in zip(c, tile))
+        elo = tuple(max(0, l - overlap) for l in lo)
+        ehi = tuple(min(n, l + t + overlap) for n, l, t in zip(global_box.extents, lo, tile))
+        nb = []
+        if overlap > 0:
+            for dz, dy, dx in product((-1, 0, 1), repeat=3):
+                q = (cx + dx, cy + dy, cz + dz)
+                if (dx, dy, dz) != (0, 0, 0) and all(0 <= a < b for a, b in zip(q, grid)):
+                    nb.append(((dx, dy, dz), rank_of(q)))
+        ranks.append(RankGeometry(rank_of(c), c, lo, Box(*tile), elo,
+                                  Box(*(h - l for l, h in zip(elo, ehi))), tuple(nb)))
+    return Partition(global_box, grid, int(overlap), tuple(ranks))
+
+
+def _intersect(a: Range3, b: Range3) -> Range3 | None:
+    out = tuple((max(a0, b0), min(a1, b1)) for (a0, a1), (b0, b1) in zip(a, b))
+    return None if any(lo >= hi for lo, hi in out) else out
+
+
+def _local_slices(region: Range3, origin):
+    (x0, x1), (y0, y1), (z0, z1) = region
+    ox, oy, oz = origin
+    return (slice(None), slice(z0 - oz, z1 - oz), slice(y0 - oy, y1 - oy), slice(x0 - ox, x1 - ox))
+
+
+def proc_grid_for(nranks: int) -> tuple[int, int, int]:
+    """Most cubic (px, py, pz), ties to the larger px (ref:cli.py:214-231)."""
+    if nranks < 1:
+        raise ValueError(f"rank count must be >= 1, got {nranks}")
+    best = None
+    for px in range(1, nranks + 1):
+        if nranks % px:
+            continue
+        for py in range(1, nranks // px + 1):
+            if (nranks // px) % py:
+                continue
+            pz = nranks // px // py
+            key = (max(px, py, pz) - min(px, py, pz), -px)
+            if best is None or key < best[0]:
+                best = (key, (px, py, pz))
+    return best[1]
+
+
+# ---------------------------------------------------------------------------- transports
+class DeviceTransport:
+    """One process, one GPU (stands in for the reference's serial/threads transports)."""
+
+    name = "cuda"
+    world = 1
+    rank = 0
+    distributed = False
+
+    def __init__(self, device=None):
+        self.device = _lib.require_cuda(device) if device is None or str(device) != "cpu" else torch.device("cpu")
+
+    def run_ranks(self, fns) -> None:
+        for fn in fns:
+            fn()
+
+    def allreduce_(self, t: torch.Tensor) -> torch.Tensor:
+        return t
+
+    def close(self) -> None:
+        pass
+
+
+class DistTransport:
+    """One process per GPU over torch.distributed (NCCL on GPUs, gloo for CPU tests)."""
+
+    name = "nccl"
+    distributed = True
+
+    def __init__(self, device=None, group=None):
+        import torch.distributed as dist
+        if not dist.is_initialized():
+            backend = "nccl" if torch.cuda.is_available() else "gloo"
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            dist.init_process_group(backend=backend)
+        self.dist = dist
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        if device is None:
+            if dist.get_backend(group) == "nccl":
+                device = torch.device("cuda", int(os.environ.get("LOCAL_RANK", self.rank)) % torch.cuda.device_count())
+                torch.cuda.set_device(device)
+            else:
+                device = torch.device("cpu")
+        self.device = torch.device(device)
+        self.name = dist.get_backend(group)
+
+    def run_ranks(self, fns) -> None:
+        for fn in fns:
+            fn()
+
+    def allreduce_(self, t: torch.Tensor) -> torch.Tensor:
+        self.dist.all_reduce(t, group=self.group)
+        return t
+
+    def exchange(self, sends: list[tuple[int, torch.Tensor]], recvs: list[tuple[int, torch.Tensor]]) -> None:
+        ops = [self.dist.P2POp(self.dist.isend, t, peer, self.group) for peer, t in sends]
+        ops += [self.dist.P2POp(self.dist.irecv, t, peer, self.group) for peer, t in recvs]
+        if ops:
+            for w in self.dist.batch_isend_irecv(ops):
+                w.wait()
+
+    def close(self) -> None:
+        pass
+
+
+def make_transport(name: str, nranks: int | None = None, device=None):
+    """'cuda' (aliases 'serial', 'threads': one GPU) or 'nccl' / 'gloo' (one process per
+    device under torch.distributed).  Unknown names raise ValueError (ref:schwarz.py:174-179)."""
+    if name in ("cuda", "serial", "threads"):
+        return DeviceTransport(device)
+    if name in ("nccl", "gloo", "dist"):
+        return DistTransport(device)
+    raise ValueError(f"unknown transport {name!r}")
+
+
+# ---------------------------------------------------------------------------- GPU blocks
+class BlockLayout:
+    """This process's block of the global grid and the subdomains it owns."""
+
+    def __init__(self, partition: Partition, transport):
+        self.partition = partition
+        self.transport = transport
+        self.world, self.rank = transport.world, transport.rank
+        self.device = transport.device
+        g = proc_grid_for(self.world)
+        for sp, gp, ax in zip(partition.proc_grid, g, "xyz"):
+            if sp % gp:
+                raise ValueError(f"subdomain grid {partition.proc_grid} not divisible by GPU grid {g} along {ax}")
+        self.gpu_grid = g
+        gx, gy, gz = g
+        self.coords = (self.rank % gx, (self.rank // gx) % gy, self.rank // (gx * gy))
+        gext = partition.global_box.extents
+        self.block = tuple(n // p for n, p in zip(gext, g))
+        self.origin = tuple(c * b for c, b in zip(self.coords, self.block))
+        self.box = Box(*self.block)
+        lo, hi = self.origin, tuple(o + b for o, b in zip(self.origin, self.block))
+        self.local_ranks = [r for r in partition.ranks
+                            if all(l <= o < h for o, l, h in zip(r.owned_lo, lo, hi))]
+        self.rank_of_gpu = lambda c: c[0] + gx * (c[1] + gy * c[2])
+
+    @property
+    def shape4(self):
+        return self.box.shape4
+
+    def neighbor(self, axis: int, side: int) -> int | None:
+        c = list(self.coords)
+        c[axis] += side
+        if not 0 <= c[axis] < self.gpu_grid[axis]:
+            return None
+        return self.rank_of_gpu(tuple(c))
+
+    def sub_specs(self) -> list[SubSpec]:
+        out = []
+        for r in self.local_ranks:
+            elo = tuple(e - o for e, o in zip(r.ext_lo, self.origin))
+            own_off = tuple(o - e for o, e in zip(r.owned_lo, r.ext_lo))
+            out.append(SubSpec(r.ext.extents, elo, own_off, r.owned.extents))
+        return out
+
+    def block_struct(self, ghosts=None, halo: int = 0) -> _lib.FmpBlock:
+        return block_struct(*self.block, origin=self.origin, global_ext=self.partition.global_box.extents,
+                            halo=halo, ghosts=ghosts)
+
+    # ---- conversions between the reference list form and block tensors (single GPU)
+    def from_list(self, dist: list) -> torch.Tensor:
+        if self.world != 1:
+            raise CommunicationError("list-form vectors are only supported on a single GPU")
+        full = gather_field(self.partition, [np.asarray(a) for a in dist])
+        return torch.from_numpy(full).to(self.device).view(self.shape4)
+
+    def to_list(self, x: torch.Tensor) -> list[np.ndarray]:
+        return scatter_field(self.partition, x.detach().cpu().numpy().ravel())
+
+    def as_block(self, v) -> tuple[torch.Tensor, bool]:
+        """(block tensor, was_list)."""
+        if isinstance(v, torch.Tensor):
+            if tuple(v.shape) != self.shape4:
+                v = v.reshape(self.shape4)
+            return v, False
+        return self.from_list(v), True
+
+
+class HaloExchanger:
+    """Fills the ghost shell (width P) of a block field from the neighbour GPUs.
+
+    Three phases: z faces, then y faces extended over the z ghosts, then x faces
+    extended over both, so edges and corners arrive without diagonal messages.  The
+    slab layout is the one fmp_block documents (include/flashmp_b200.h).
+    """
+
+    def __init__(self, layout: BlockLayout, width: int, record_trace: bool = False):
+        self.layout = layout
+        self.P = P = int(width)
+        self.epoch = 0
+        self.trace: list[tuple[int, int, int, int]] = []
+        self.record_trace = record_trace
+        bx, by, bz = layout.block
+        dev = layout.device
+        mk = lambda shape: torch.zeros(shape, dtype=torch.float64, device=dev)
+        nb = [layout.neighbor(a, s) for a in (0, 1, 2) for s in (-1, 1)]
+        self.nb = nb   # xlo, xhi, ylo, yhi, zlo, zhi
+        shapes = [(3, bz + 2 * P, by + 2 * P, P)] * 2 + [(3, bz + 2 * P, P, bx)] * 2 + [(3, P, by, bx)] * 2
+        self.ghosts = [mk(s) if (n is not None and P > 0) else None for s, n in zip(shapes, nb)]
+        self.active = any(n is not None for n in nb) and P > 0
+
+    def block_struct(self) -> _lib.FmpBlock:
+        return self.layout.block_struct(self.ghosts if self.active else None, self.P if self.active else 0)
+
+    def _swap(self, pairs):
+        """pairs: list of (peer, send_tensor, recv_tensor)."""
+        tr = self.layout.transport
+        sends = [(p, s.contiguous()) for p, s, _ in pairs]
+        recvs = [(p, r) for p, _, r in pairs]
+        if self.record_trace:
+            for p, s in sends:
+                self.trace.append((self.epoch, self.layout.rank, p, s.numel() * 8))
+        tmp = [(p, torch.empty_like(r)) for p, r in recvs]
+        tr.exchange(sends, tmp)
+        for (p, r), (_, t) in zip(recvs, tmp):
+            r.copy_(t)
+
+    def exchange(self, x: torch.Tensor) -> None:
+        if not self.active:
+            return
+        self.epoch += 1
+        P = self.P
+        bx, by, bz = self.layout.block
+        xlo, xhi, ylo, yhi, zlo, zhi = self.ghosts
+        nxl, nxh, nyl, nyh, nzl, nzh = self.nb
+        # phase z
+        pairs = []
+        if nzl is not None:
+            pairs.append((nzl, x[:, :P], zlo))
+        if nzh is not None:
+            pairs.append((nzh, x[:, bz - P:], zhi))
+        self._swap(pairs)
+
+        def zext(rows: slice):  # (3, bz+2P, |rows|, bx): block rows with the z ghosts around them
+            parts = [zlo[:, :, rows] if zlo is not None else x.new_zeros((3, P, rows.stop - rows.start, bx)),
+                     x[:, :, rows],
+                     zhi[:, :, rows] if zhi is not None else x.new_zeros((3, P, rows.stop - rows.start, bx))]
+            return torch.cat(parts, dim=1)
+
+        pairs = []
+        if nyl is not None:
+            pairs.append((nyl, zext(slice(0, P)), ylo))
+        if nyh is not None:
+            pairs.append((nyh, zext(slice(by - P, by)), yhi))
+        self._swap(pairs)
+
+        def padded_cols(c0: int, c1: int):  # (3, bz+2P, by+2P, c1-c0)
+            w = c1 - c0
+            out = x.new_zeros((3, bz + 2 * P, by + 2 * P, w))
+            out[:, P:P + bz, P:P + by] = x[..., c0:c1]
+            if ylo is not None:
+                out[:, :, :P] = ylo[..., c0:c1]
+            if yhi is not None:
+                out[:, :, P + by:] = yhi[..., c0:c1]
+            if zlo is not None:
+                out[:, :P, P:P + by] = zlo[..., c0:c1]
+            if zhi is not None:
+                out[:, P + bz:, P:P + by] = zhi[..., c0:c1]
+            return out
+
+        pairs = []
+        if nxl is not None:
+            pairs.append((nxl, padded_cols(0, P), xlo))
+        if nxh is not None:
+            pairs.append((nxh, padded_cols(bx - P, bx), xhi))
+        self._swap(pairs)
+
+    def write_trace_csv(self, path) -> None:
+        import csv
+        with open(path, "w", newline="") as f:
+            w = csv.writer(f)
+            w.writerow(["epoch", "src_rank", "dst_rank", "bytes"])
+            w.writerows(self.trace)
+
+
+# ---------------------------------------------------------------------------- host helpers
+def scatter_field(partition: Partition, global_data) -> list[np.ndarray]:
+    """Global component-major vector -> per-rank owned vectors (ref:schwarz.py:273-281)."""
+    g = partition.global_box
+    view = np.asarray(global_data).reshape(g.shape4)
+    return [np.ascontiguousarray(view[_local_slices(r.owned_range(), (0, 0, 0))]).ravel()
+            for r in partition.ranks]
+
+
+def gather_field(partition: Partition, dist) -> np.ndarray:
+    """Inverse of scatter_field (ref:schwarz.py:284-292)."""
+    g = partition.global_box
+    full = np.empty(g.shape4)
+    for r, arr in zip(partition.ranks, dist):
+        full[_local_slices(r.owned_range(), (0, 0, 0))] = np.asarray(arr).reshape(r.owned.shape4)
+    return full.ravel()
+
+
+_SOLVER_CACHE: dict = {}
+
+
+def solver_data_for(box: Box, alpha: float, device=None) -> subdomain.SubdomainSolverData:
+    """Shared precompute cache keyed by (extents, alpha) (ref:schwarz.py:295-305)."""
+    dev = _lib.require_cuda(device)
+    key = (box.extents, float(alpha), str(dev))
+    data = _SOLVER_CACHE.get(key)
+    if data is None:
+        data = subdomain.precompute(OperatorParams(box, alpha), dev)
+        _SOLVER_CACHE[key] = data
+    return data
+
+
+# ---------------------------------------------------------------------------- exchanger (API parity)
+class Exchanger:
+    """Reference-compatible halo gather: per-subdomain extended vectors (ref:schwarz.py:182-266).
+
+    The extended vectors are produced by the same device restriction the fused solve
+    uses (fmp_precond_restrict), so this doubles as the bit-exact index-map check."""
+
+    def __init__(self, partition: Partition, transport, record_trace: bool = False):
+        self.partition = partition
+        self.layout = BlockLayout(partition, transport)
+        self.halo = HaloExchanger(self.layout, max(1, partition.overlap), record_trace)
+        self.plan = SolvePlan(self.layout.sub_specs(), 0.0, self.layout.device, need_woodbury=False)
+        self.epoch = 0
+
+    @property
+    def trace(self):
+        return self.halo.trace
+
+    def exchange(self, locals_):
+        x, was_list = self.layout.as_block(locals_) if not isinstance(locals_, torch.Tensor) else (locals_, False)
+        if was_list and len(locals_) != self.partition.nranks:
+            raise CommunicationError(f"expected {self.partition.nranks} rank vectors, got {len(locals_)}")
+        self.epoch += 1
+        self.halo.exchange(x)
+        flat = self.plan.restrict(self.halo.block_struct(), x)
+        offs = self.plan._sub_host[:, 14]
+        sizes = 3 * self.plan._sub_host[:, 0] * self.plan._sub_host[:, 1] * self.plan._sub_host[:, 2]
+        exts = [None] * len(self.plan.subs)
+        host = flat.cpu().numpy() if was_list else None
+        for pos, orig in enumerate(self.plan.order):
+            seg = slice(int(offs[pos]), int(offs[pos] + sizes[pos]))
+            exts[orig] = host[seg].copy() if was_list else flat[seg]
+        return exts
+
+    def write_trace_csv(self, path) -> None:
+        self.halo.write_trace_csv(path)
+
+
+def exchange_halo(exchanger: Exchanger, locals_):
+    return exchanger.exchange(locals_)
+
+
+# ---------------------------------------------------------------------------- RAS preconditioner
+class RasPreconditioner:
+    """Restricted additive Schwarz with exact subdomain solves (ref:schwarz.py:308-339).
+
+    apply(r) = sum_i S_i^0T A_i^-1 S_i^gamma r over every subdomain of this GPU in one
+    batched launch sequence (csrc/precond.cu); the restriction reads the overlap
+    straight from the block field and its ghost shell, the prolongation writes the
+    owned tiles straight into the output block."""
+
+    def __init__(self, partition: Partition, alpha: float, transport, timer=NULL_TIMER,
+                 record_trace: bool = False):
+        self.partition = partition
+        self.alpha = float(alpha)
+        self.timer = timer
+        self.layout = BlockLayout(partition, transport)
+        self.exchanger = HaloExchanger(self.layout, partition.overlap, record_trace)
+        dev = self.layout.device
+        self.solvers = {}
+        specs = self.layout.sub_specs()
+        cinv = {}
+        if self.alpha != 0.0:
+            for s in specs:
+                if s.ext not in self.solvers:
+                    data = solver_data_for(Box(*s.ext), self.alpha, dev)
+                    self.solvers[s.ext] = data
+                    cinv[s.ext] = data.corr.inverse
+        self.plan = SolvePlan(specs, self.alpha, dev, cinv=cinv) if self.alpha != 0.0 else None
+
+    def apply_into(self, r: torch.Tensor, z: torch.Tensor) -> torch.Tensor:
+        with self.timer.phase("asm_comm"):
+            self.exchanger.exchange(r)
+        with self.timer.phase("fast_solve"):
+            if self.plan is None:
+                z.copy_(r)
+            else:
+                self.plan.apply(self.exchanger.block_struct(), _lib.FMP_SOLVE_WOODBURY, r, z)
+        return z
+
+    def apply(self, r_dist):
+        r, was_list = self.layout.as_block(r_dist)
+        z = self.apply_into(r, torch.empty_like(r))
+        return self.layout.to_list(z) if was_list else z
+
+
+def ras_apply(prec: RasPreconditioner, r_dist):
+    return prec.apply(r_dist)
+
+
+# ---------------------------------------------------------------------------- operator
+class DistributedOperator:
+    """y = A x over this GPU's block (ref:schwarz.py:347-388): a width-1 ghost exchange
+    (multi-GPU only) plus the matrix-free stencil kernel; optional fused dot products
+    feed the Krylov solvers."""
+
+    def __init__(self, partition: Partition, alpha: float, transport, timer=NULL_TIMER,
+                 with_boundary: bool = True):
+        self.partition = partition
+        self.alpha = float(alpha)
+        self.with_boundary = with_boundary
+        self.timer = timer
+        self.transport = transport
+        self.layout = BlockLayout(partition, transport)
+        self.exchanger = HaloExchanger(self.layout, 1)
+        dev = self.layout.device
+        self._dots = torch.zeros(2, dtype=torch.float64, device=dev)
+        self._scratch = torch.zeros(int(_lib.lib().fmp_reduce_scratch_doubles()), dtype=torch.float64, device=dev)
+
+    def _run(self, mode: int, x: torch.Tensor, y, w):
+        with self.timer.phase("p2p"):
+            self.exchanger.exchange(x)
+        blk = self.exchanger.block_struct()
+        with self.timer.phase("spmv"):
+            _lib.call("fmp_stencil_apply", _lib.ref(blk), self.alpha, int(self.with_boundary), mode,
+                      x.data_ptr(), _lib.ptr(y), _lib.ptr(w), self._dots.data_ptr(), self._scratch.data_ptr(),
+                      _lib.stream())
+
+    def apply_into(self, x: torch.Tensor, y: torch.Tensor) -> torch.Tensor:
+        self._run(0, x, y, None)
+        return y
+
+    def apply(self, x_dist):
+        x, was_list = self.layout.as_block(x_dist)
+        y = self.apply_into(x, torch.empty_like(x))
+        return self.layout.to_list(y) if was_list else y
+
+    def apply_dots(self, x: torch.Tensor, y: torch.Tensor, w: torch.Tensor, both: bool) -> torch.Tensor:
+        """y = A x; returns the device tensor [(y, w), (y, y)] (second entry only if both),
+        summed over GPUs."""
+        self._run(2 if both else 1, x, y, w)
+        with self.timer.phase("reduction"):
+            return self.transport.allreduce_(self._dots.clone())
+
+    def residual_norm2(self, x: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
+        """||b - A x||^2 over all GPUs, without materialising A x."""
+        self._run(3, x, None, b)
+        with self.timer.phase("reduction"):
+            return self.transport.allreduce_(self._dots[:1].clone())

@@ -1,0 +1,110 @@
+"""GPU parity: subdomain exact solve, Woodbury solve, GPU-built C^-1, RAS apply and the
+restriction index maps, against the reference goldens and the oracle."""
+
+import numpy as np
+import pytest
+import torch
+
+import flashmp_oracle as O
+from conftest import GOLDEN
+
+pytestmark = pytest.mark.gpu
+
+SUB_EXTS = [(1, 1, 1), (2, 2, 2), (3, 3, 3), (4, 5, 6), (6, 2, 4), (1, 3, 4), (5, 1, 2)]
+
+
+def rel(a, b):
+    a, b = np.ravel(np.asarray(a)), np.ravel(np.asarray(b))
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+@pytest.mark.parametrize("ext", SUB_EXTS)
+@pytest.mark.parametrize("alpha", [0.05, 0.25, 1.0])
+def test_subdomain_solves_match_reference(ext, alpha):
+    from paper_2508_07193_b200 import Box, FieldVector, OperatorParams, exact_solve, precompute, solve
+    g = np.load(GOLDEN / "subdomain.npz")
+    tag = "_".join(map(str, ext)) + f"_a{alpha}"
+    data = precompute(OperatorParams(Box(*ext), alpha))
+    r = FieldVector(Box(*ext), g[f"r_{tag}"])
+    assert rel(exact_solve(data, r).data, g[f"exact_{tag}"]) <= 1e-12
+    assert rel(solve(data, r).data, g[f"solve_{tag}"]) <= 1e-11
+    if f"rows_{tag}" in g:
+        assert np.array_equal(data.corr.rows, g[f"rows_{tag}"])
+        assert np.array_equal(data.corr.values, g[f"values_{tag}"])
+        assert np.abs(data.corr.inverse.cpu().numpy() - g[f"Cinv_{tag}"]).max() <= 1e-12
+
+
+def test_alpha_zero_is_identity():
+    from paper_2508_07193_b200 import Box, FieldVector, OperatorParams, exact_solve, precompute, solve
+    box = Box(3, 4, 5)
+    data = precompute(OperatorParams(box, 0.0))
+    v = FieldVector(box, np.random.default_rng(0).uniform(-1, 1, box.dof))
+    assert data.corr is None
+    assert np.array_equal(exact_solve(data, v).data, v.data)
+    assert np.array_equal(solve(data, v).data, v.data)
+
+
+@pytest.mark.parametrize("ext", [(17, 18, 17), (34, 34, 34), (33, 34, 33)])
+def test_solve_round_trip_against_stencil(ext):
+    """A (solve r) == r on the config-3/4 extended shapes (size-independent property)."""
+    from paper_2508_07193_b200 import Box, FieldVector, OperatorParams, precompute, solve
+    from paper_2508_07193_b200.operators import stencil_apply
+    box = Box(*ext)
+    data = precompute(OperatorParams(box, 0.25))
+    r = np.random.default_rng(5).uniform(-1, 1, box.dof)
+    e = solve(data, FieldVector(box, r)).data
+    back = stencil_apply(torch.from_numpy(e).cuda().view(box.shape4), 0.25, True).cpu().numpy().ravel()
+    assert rel(back, r) <= 1e-12
+    # and against the oracle's exact solve (no correction) on the same input
+    if ext == (17, 18, 17):
+        od = O.precompute(ext, 0.25)
+        assert rel(e, O.solve(od, r)) <= 1e-11
+
+
+def test_precompute_cinv_matches_oracle_34():
+    """GPU-assembled C^-1 on a 34^3-class shape vs the oracle (ref algorithm) -- 12x12x12 here
+    to keep the oracle's CPU precompute short."""
+    from paper_2508_07193_b200 import Box, OperatorParams, precompute
+    ext = (12, 11, 13)
+    data = precompute(OperatorParams(Box(*ext), 0.25))
+    od = O.precompute(ext, 0.25)
+    assert np.array_equal(data.corr.rows, od.rows)
+    assert np.abs(data.corr.inverse.cpu().numpy() - od.Cinv).max() <= 1e-12
+
+
+SCHWARZ = [((8, 8, 8), (2, 1, 1), 0), ((8, 8, 8), (2, 1, 1), 1), ((8, 8, 4), (2, 2, 1), 1),
+           ((12, 8, 8), (3, 2, 2), 2), ((8, 4, 6), (2, 2, 3), 1)]
+
+
+@pytest.mark.parametrize("gext,grid,ov", SCHWARZ)
+def test_ras_and_index_maps_match_reference(gext, grid, ov):
+    from paper_2508_07193_b200 import (Box, DistributedOperator, Exchanger, RasPreconditioner, gather_field,
+                                       make_partition, make_transport, scatter_field)
+    g = np.load(GOLDEN / "schwarz.npz")
+    tag = "_".join(map(str, gext)) + "_g" + "".join(map(str, grid)) + f"_o{ov}"
+    part = make_partition(Box(*gext), grid, ov)
+    tr = make_transport("serial", part.nranks)
+    r = g[f"r_{tag}"]
+    prec = RasPreconditioner(part, 0.25, tr)
+    got = gather_field(part, prec.apply(scatter_field(part, r)))
+    assert rel(got, g[f"ras_{tag}"]) <= 1e-11
+    op = DistributedOperator(part, 0.25, tr)
+    assert rel(gather_field(part, op.apply(scatter_field(part, r))), g[f"spmv_{tag}"]) <= 1e-14
+    ex = Exchanger(part, tr)
+    lin = np.arange(3 * int(np.prod(gext)), dtype=np.float64)
+    exts = ex.exchange(scatter_field(part, lin))
+    assert np.array_equal(np.concatenate(exts).astype(np.int64), g[f"extidx_{tag}"])
+
+
+def test_ras_device_tensor_path_and_no_aliasing():
+    from paper_2508_07193_b200 import Box, RasPreconditioner, make_partition, make_transport
+    part = make_partition(Box(16, 16, 16), (2, 2, 2), 1)
+    prec = RasPreconditioner(part, 0.25, make_transport("cuda"))
+    r = torch.from_numpy(np.random.default_rng(6).uniform(-1, 1, part.global_box.dof)).cuda().view(3, 16, 16, 16)
+    z1 = prec.apply(r)
+    z2 = prec.apply(r)
+    assert z1.data_ptr() != z2.data_ptr() and z1.data_ptr() != r.data_ptr()
+    assert torch.equal(z1, z2)   # deterministic
+    want = O.ras_apply((16, 16, 16), O.partition((16, 16, 16), (2, 2, 2), 1), 0.25, r.cpu().numpy().ravel())
+    assert rel(z1.cpu().numpy(), want) <= 1e-11
+    assert not prec.apply(torch.zeros_like(r)).any()

@@ -1,0 +1,135 @@
+"""GPU parity: matrix-free stencils and Krylov vector kernels vs the oracle / reference goldens."""
+
+import numpy as np
+import pytest
+import torch
+
+import flashmp_oracle as O
+from conftest import GOLDEN
+
+pytestmark = pytest.mark.gpu
+
+EXTS = [(3, 3, 3), (4, 5, 6), (1, 3, 4), (8, 8, 8), (2, 7, 3)]
+
+
+def rel(a, b):
+    a, b = np.ravel(np.asarray(a)), np.ravel(np.asarray(b))
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+def dev(x, ext):
+    return torch.from_numpy(np.ascontiguousarray(x)).cuda().view(3, ext[2], ext[1], ext[0])
+
+
+@pytest.mark.parametrize("ext", EXTS)
+def test_stencil_matches_reference(ext):
+    from paper_2508_07193_b200.operators import stencil_apply
+    from paper_2508_07193_b200 import apply_curl, apply_double_curl
+    g = np.load(GOLDEN / "operators.npz")
+    tag = "_".join(map(str, ext))
+    x = dev(g[f"x_{tag}"], ext)
+    assert rel(stencil_apply(x, 0.25, True).cpu(), g[f"A_{tag}"]) <= 1e-14
+    assert rel(stencil_apply(x, 0.25, True).cpu(), g[f"Acsr_{tag}"]) <= 1e-14
+    assert rel(stencil_apply(x, 0.25, False).cpu(), g[f"A0_{tag}"]) <= 1e-14
+    assert rel(apply_curl("forward", x).cpu(), g[f"curlf_{tag}"]) <= 1e-15
+    assert rel(apply_curl("backward", x).cpu(), g[f"curlb_{tag}"]) <= 1e-15
+    assert rel(apply_double_curl(x).cpu(), g[f"M_{tag}"]) <= 1e-14
+
+
+@pytest.mark.parametrize("ext", [(37, 9, 19), (64, 64, 64), (33, 34, 35)])
+@pytest.mark.parametrize("boundary", [True, False])
+def test_stencil_matches_oracle_larger(ext, boundary):
+    from paper_2508_07193_b200.operators import stencil_apply
+    x = np.random.default_rng(1).uniform(-1, 1, (3, ext[2], ext[1], ext[0]))
+    got = stencil_apply(dev(x, ext), 0.25, boundary).cpu().numpy()
+    want = O.apply_A(0.25, x, boundary)
+    assert np.abs(got - want).max() <= 1e-14 * np.abs(want).max()
+
+
+def test_stencil_fused_dots_and_residual():
+    from paper_2508_07193_b200 import _lib
+    from paper_2508_07193_b200.plan import block_struct
+    ext = (40, 24, 16)
+    rng = np.random.default_rng(2)
+    x, w = (rng.uniform(-1, 1, (3, ext[2], ext[1], ext[0])) for _ in range(2))
+    X, W = dev(x, ext), dev(w, ext)
+    Y = torch.empty_like(X)
+    dots = torch.zeros(2, dtype=torch.float64, device="cuda")
+    scratch = torch.zeros(int(_lib.lib().fmp_reduce_scratch_doubles()), dtype=torch.float64, device="cuda")
+    blk = block_struct(*ext)
+    y = O.apply_A(0.3, x, True)
+    for mode in (1, 2, 3):
+        _lib.call("fmp_stencil_apply", _lib.ref(blk), 0.3, 1, mode, X.data_ptr(),
+                  Y.data_ptr() if mode < 3 else None, W.data_ptr(), dots.data_ptr(), scratch.data_ptr(),
+                  _lib.stream())
+        d = dots.cpu().numpy()
+        if mode < 3:
+            assert rel(Y.cpu(), y) <= 1e-14
+            assert abs(d[0] - np.sum(y * w)) <= 1e-12 * np.sum(np.abs(y * w))
+        if mode == 2:
+            assert abs(d[1] - np.sum(y * y)) <= 1e-13 * np.sum(y * y)
+        if mode == 3:
+            assert abs(d[0] - np.sum((w - y) ** 2)) <= 1e-13 * np.sum((w - y) ** 2)
+
+
+def test_stencil_symmetric_and_deterministic():
+    """A is SPD: (Ax, y) == (x, Ay); repeated launches are bitwise equal."""
+    from paper_2508_07193_b200.operators import stencil_apply
+    ext = (48, 40, 32)
+    rng = np.random.default_rng(3)
+    x, y = (dev(rng.uniform(-1, 1, (3, ext[2], ext[1], ext[0])), ext) for _ in range(2))
+    ax, ay = stencil_apply(x, 0.25), stencil_apply(y, 0.25)
+    lhs, rhs = float((ax * y).sum()), float((x * ay).sum())
+    assert abs(lhs - rhs) <= 1e-12 * abs(lhs)
+    assert torch.equal(stencil_apply(x, 0.25), ax)
+
+
+def test_vector_kernels_bitwise_numpy():
+    from paper_2508_07193_b200 import _lib
+    n = 1_000_003
+    rng = np.random.default_rng(4)
+    a, b, c, d, e, f = (rng.uniform(-1, 1, n) for _ in range(6))
+    T = lambda v: torch.from_numpy(v.copy()).cuda()
+    st = _lib.stream()
+    out = torch.empty(n, dtype=torch.float64, device="cuda")
+    _lib.call("fmp_vec_lincomb", n, 0.7, T(a).data_ptr(), -1.3, T(b).data_ptr(), out.data_ptr(), st)
+    assert np.array_equal(out.cpu().numpy(), 0.7 * a + -1.3 * b)
+    y = T(b)
+    _lib.call("fmp_vec_axpy", n, 0.37, T(a).data_ptr(), y.data_ptr(), st)
+    bb = b.copy()
+    bb += 0.37 * a
+    assert np.array_equal(y.cpu().numpy(), bb)
+    _lib.call("fmp_vec_scale", n, 1.0 / 3.0, T(a).data_ptr(), out.data_ptr(), st)
+    assert np.array_equal(out.cpu().numpy(), (1.0 / 3.0) * a)
+    # BiCGSTAB p update: p = 1.0*r + beta*(1.0*p + (-omega)*v)   (ref:krylov.py:181-182)
+    p = T(b)
+    _lib.call("fmp_bicg_p", n, T(a).data_ptr(), p.data_ptr(), T(c).data_ptr(), 0.9, 0.4, st)
+    p1 = 1.0 * b + (-0.4) * c
+    assert np.array_equal(p.cpu().numpy(), 1.0 * a + 0.9 * p1)
+    # BiCGSTAB tail + next rho
+    x, r = T(a), T(b)
+    dots = torch.zeros(2, dtype=torch.float64, device="cuda")
+    scratch = torch.zeros(int(_lib.lib().fmp_reduce_scratch_doubles()), dtype=torch.float64, device="cuda")
+    _lib.call("fmp_bicg_xr", n, x.data_ptr(), T(c).data_ptr(), T(d).data_ptr(), T(e).data_ptr(), T(f).data_ptr(),
+              r.data_ptr(), T(c).data_ptr(), 0.3, 0.6, dots.data_ptr(), scratch.data_ptr(), st)
+    xx = a.copy()
+    xx += 0.3 * c
+    xx += 0.6 * d
+    rr = 1.0 * e + (-0.6) * f
+    assert np.array_equal(x.cpu().numpy(), xx)
+    assert np.array_equal(r.cpu().numpy(), rr)
+    assert abs(float(dots[0]) - float(c @ rr)) <= 1e-12 * np.sum(np.abs(c * rr))
+    _lib.call("fmp_vec_dot", n, T(a).data_ptr(), T(b).data_ptr(), dots.data_ptr(), scratch.data_ptr(), st)
+    assert abs(float(dots[0]) - float(a @ b)) <= 1e-12 * np.sum(np.abs(a * b))
+
+
+def test_cn_stencils_match_reference():
+    from paper_2508_07193_b200 import EmState, FieldVector, Box, build_rhs
+    g = np.load(GOLDEN / "cn.npz")
+    for gext, tag in [((8, 8, 8), "8_8_8_g111_o1"), ((16, 16, 16), "16_16_16_g222_o1")]:
+        rng = np.random.default_rng(42)
+        box = Box(*gext)
+        E = FieldVector(box, rng.uniform(-1, 1, box.dof))
+        H = FieldVector(box, rng.uniform(-1, 1, box.dof))
+        R = build_rhs(EmState(E, H, 0, 1.0))
+        assert rel(R.data, g[f"rhs_{tag}"]) <= 1e-14
