@@ -1,0 +1,396 @@
+"""Benchmark: FlashMP-preconditioned BiCGSTAB CN-FDTD steps on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config cfg4]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+
+A step is one Crank-Nicolson FDTD step of the double-curl system (ref:cn_driver.py:82-94):
+RHS stencil, BiCGSTAB + RAS/FlashMP solve to relres <= 1e-12 (ref defaults: alpha 0.25,
+overlap 1, tol 1e-12), H update.  Workload (weak scaling, BASELINE config 4): 256^3 grid
+points per GPU in 32^3 subdomains (8x8x8 per GPU), GPU grid = the reference CLI's
+_proc_grid_for(N).  value = 3 * global grid points / step seconds / 1e6 (MDoF/s, the
+reference's definition ref:cli.py:41,84-85) over all N GPUs.
+
+Rank 0 prints ONE JSON line.  --impl reference times the CPU reference algorithm (the
+numpy oracle port, oracle/flashmp_oracle.py) on the host cores instead.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "CN-FDTD step time-to-solve (s), MDOF/s, iters; precond apply GB/s @1/2/4/8 B200"
+FP64_PEAK_FILE = ROOT / "profiles" / "r01_fp64_probe.json"
+
+CONFIGS = {
+    # name: (per-GPU block extents, subdomain extents, overlap)
+    "cfg4": ((256, 256, 256), (32, 32, 32), 1),
+    "cfg2": ((64, 64, 64), (32, 32, 32), 1),
+    "cfg1": ((32, 32, 32), (32, 32, 32), 1),
+}
+
+
+def measured_peaks():
+    peaks = {"hbm_gbs": None, "hbm_source": None, "fp64_tflops": None, "fp64_source": None}
+    mp = ROOT / "MEASURED_PEAKS.json"
+    if mp.exists():
+        peaks["hbm_gbs"] = json.loads(mp.read_text())["hbm_gbs"]
+        peaks["hbm_source"] = "MEASURED_PEAKS.json hbm_gbs (measured copy)"
+    else:
+        peaks["hbm_gbs"], peaks["hbm_source"] = 6650.0, "B200_PROFILING.md fallback"
+    if FP64_PEAK_FILE.exists():
+        d = json.loads(FP64_PEAK_FILE.read_text())
+        peaks["fp64_tflops"] = max(v for k, v in d.items() if k.startswith("dmma_"))
+        peaks["fp64_source"] = "profiles/r01_fp64_probe.json (measured DMMA issue peak on this pool's B200)"
+    return peaks
+
+
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.out = ""
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                self.out, _ = self.proc.communicate()
+
+    def summary(self):
+        rows = []
+        for line in (self.out or "").strip().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6 and parts[0].isdigit():
+                rows.append(parts)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in rows for n, v in zip(names, r[2:]) if v.lower() == "active"})
+        return {"sm_mhz": statistics.median(float(r[0]) for r in rows), "sm_max_mhz": float(rows[0][1]),
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ----------------------------------------------------------------------------------- ours
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    from paper_2508_07193_b200 import (Box, CnSolver, DeviceCnStepper, SolverConfig, make_transport, _lib)
+    from paper_2508_07193_b200.schwarz import proc_grid_for
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    if world > 1:
+        tr = make_transport("nccl")
+    else:
+        tr = make_transport("cuda")
+    rank = tr.rank
+    dev = torch.cuda.current_device()
+    block, sub, overlap = CONFIGS[args.config]
+    ggrid = proc_grid_for(world)
+    gext = tuple(b * g for b, g in zip(block, ggrid))
+    sgrid = tuple(n // s for n, s in zip(gext, sub))
+    alpha = 0.25
+    dt = 2.0 * math.sqrt(alpha)     # ref:cli.py:145
+    cfg = SolverConfig(method="bicgstab", tol=1e-12, max_iter=1000)
+    t_setup = time.perf_counter()
+    solver = CnSolver(Box(*gext), sgrid, overlap, alpha, cfg, tr)
+    torch.cuda.synchronize()
+    setup_s = time.perf_counter() - t_setup
+    shape4 = solver.op.layout.shape4
+    gen = torch.Generator(device="cuda").manual_seed(42 + rank)
+    E0 = torch.rand(shape4, dtype=torch.float64, device="cuda", generator=gen).mul_(2).sub_(1)
+    H0 = torch.rand(shape4, dtype=torch.float64, device="cuda", generator=gen).mul_(2).sub_(1)
+    stepper = DeviceCnStepper(solver, E0.clone(), H0.clone(), dt)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(args.warmup):
+        stepper.step()
+    torch.cuda.synchronize()
+    barrier()
+    # ---- timed region: K device-resident steps
+    lib = _lib.lib()
+    launches0 = lib.fmp_launch_count()
+    iters = []
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(dev) as clocks:
+        torch.cuda.synchronize()
+        barrier()
+        ev0.record()
+        for _ in range(args.steps):
+            rep = stepper.step()
+            iters.append(rep.iterations)
+        ev1.record()
+        torch.cuda.synchronize()
+        barrier()
+    launches = lib.fmp_launch_count() - launches0
+    t_total = max_over_ranks(ev0.elapsed_time(ev1) * 1e-3)
+    ms_per_step = t_total / args.steps * 1e3
+    dof = 3 * int(np.prod(gext))
+    value = dof * args.steps / t_total / 1e6
+
+    # ---- component timings (CUDA events on the launching stream) for the roofline
+    prec, op = solver.prec, solver.op
+    x = stepper.E.clone()
+    z = torch.empty_like(x)
+    reps = 5
+    for _ in range(2):
+        prec.apply_into(x, z)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(reps):
+        prec.apply_into(x, z)
+    e1.record()
+    torch.cuda.synchronize()
+    t_prec = e0.elapsed_time(e1) * 1e-3 / reps
+    e0.record()
+    for _ in range(reps):
+        op.apply_into(x, z)
+    e1.record()
+    torch.cuda.synchronize()
+    t_spmv = e0.elapsed_time(e1) * 1e-3 / reps
+    from paper_2508_07193_b200.subdomain import analytic_cost, correction_size
+    specs = solver.op.layout.sub_specs()
+    flops_ref = flops_exec = 0
+    bytes_alg = 0
+    for s in specs:
+        bx = Box(*s.ext)
+        c = analytic_cost(bx, correction_size(bx))
+        flops_ref += c.flops_per_solve
+        flops_exec += c.flops_executed
+        bytes_alg += 24 * bx.volume
+    owned = int(np.prod(block))
+    bytes_alg += 24 * owned + sum(8 * correction_size(Box(*e)) ** 2 for e in {s.ext for s in specs})
+    peaks = measured_peaks()
+    spmv_bytes = 48 * owned
+    prec_tflops = flops_exec / t_prec / 1e12
+
+    # ---- end-to-end through the public API: host fields in, host fields out, every step
+    e2e = None
+    if not args.no_e2e:
+        Eh = E0.cpu().pin_memory()
+        Hh = H0.cpu().pin_memory()
+        Eo, Ho = torch.empty_like(Eh).pin_memory(), torch.empty_like(Hh).pin_memory()
+        stepper2 = DeviceCnStepper(solver, E0.clone(), H0.clone(), dt)
+        ke = max(1, min(args.steps, 3))
+        torch.cuda.synchronize()
+        barrier()
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record()
+        for _ in range(ke):
+            stepper2.E.copy_(Eh, non_blocking=True)
+            stepper2.H.copy_(Hh, non_blocking=True)
+            stepper2.step()
+            Eo.copy_(stepper2.E, non_blocking=True)
+            Ho.copy_(stepper2.H, non_blocking=True)
+        a1.record()
+        torch.cuda.synchronize()
+        t_e2e = max_over_ranks(a0.elapsed_time(a1) * 1e-3)
+        e2e = {"value": round(dof * ke / t_e2e / 1e6, 3), "unit": "MDoF/s",
+               "h2d_bytes_per_step": 2 * Eh.numel() * 8, "d2h_bytes_per_step": 2 * Eo.numel() * 8,
+               "steps": ke, "ms_per_step": round(t_e2e / ke * 1e3, 3)}
+
+    line = {
+        "metric": METRIC, "value": round(value, 3), "unit": "MDoF/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms_per_step, 3), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic: E,H ~ U[-1,1) (torch Philox, seed 42+rank)",
+        "config": {"workload": f"{args.config}: CN-FDTD step, BiCGSTAB+FlashMP RAS, tol 1e-12, alpha 0.25, "
+                               f"overlap {overlap}", "global_grid": list(gext), "per_gpu_block": list(block),
+                   "subdomain": list(sub), "subdomain_grid": list(sgrid), "gpu_grid": list(ggrid),
+                   "parallelism": f"domain decomposition x{world}",
+                   "l2": "inputs larger than L2 (each field 403 MB per GPU at 256^3)"},
+        "step_time_s": round(ms_per_step / 1e3, 6), "iters_per_step": iters,
+        "setup_s": round(setup_s, 3),
+        "precond_apply": {"ms": round(t_prec * 1e3, 4), "GB_per_s": round(bytes_alg / t_prec / 1e9, 1),
+                          "algorithmic_bytes": bytes_alg, "flops_reference_count": flops_ref,
+                          "flops_executed": flops_exec, "tflops_executed": round(prec_tflops, 2),
+                          "tflops_reference_count": round(flops_ref / t_prec / 1e12, 2)},
+        "spmv": {"ms": round(t_spmv * 1e3, 4), "GB_per_s": round(spmv_bytes / t_spmv / 1e9, 1),
+                 "frac_hbm": round(spmv_bytes / t_spmv / 1e9 / peaks["hbm_gbs"], 3)},
+        "roofline": {"kernel": "RAS precond apply (fused FlashMP sequence, FP64 DMMA + cuBLAS DGEMM)",
+                     "bound": "tensor", "achieved": round(prec_tflops, 3), "peak": peaks["fp64_tflops"],
+                     "unit": "TFLOP/s", "frac": round(prec_tflops / peaks["fp64_tflops"], 3)
+                     if peaks["fp64_tflops"] else None, "traffic": None,
+                     "peak_source": peaks["fp64_source"], "flops_per_launch": flops_exec},
+        "gpu_launches": int(launches),
+        "clocks": clocks.summary(),
+        "e2e": e2e,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(gext, sub, overlap, iters, budget_s=args.cpu_budget)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+# ----------------------------------------------------------------------------------- CPU reference
+def cpu_sample(gext, sub, overlap, iters_per_step, budget_s=20.0):
+    """Time the CPU reference algorithm (oracle port, numpy/OpenBLAS, all host threads) on a
+    bounded sample of one CN step at the full workload and compose the per-step time:
+        step = rhs + H update + iters * (2 * sum_subdomains solve + 3 * SpMV + vector ops)
+    Sample: one global SpMV, one global RHS, one Woodbury solve per distinct extended shape
+    (timing-only C^-1: a random symmetric matrix of the true size m; the reference's own
+    precompute takes 38-55 s per shape and is excluded from its solve time anyway), and the
+    BiCGSTAB vector updates on full-size vectors."""
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import flashmp_oracle as O
+    t_start = time.perf_counter()
+    rng = np.random.default_rng(0)
+    shape = (3, gext[2], gext[1], gext[0])
+    E = rng.uniform(-1, 1, shape)
+    H = rng.uniform(-1, 1, shape)
+    t0 = time.perf_counter()
+    R = O.build_rhs(E, H, 1.0)
+    t_rhs = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    O.apply_A(0.25, E, True)
+    t_spmv = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    _ = H - 0.5 * (O.curl("forward", E) + O.curl("forward", R))
+    t_h = time.perf_counter() - t0
+    # vector ops of one BiCGSTAB iteration: 6 axpy-type + 4 dots + true-residual lincomb/norm
+    a, b = E.ravel(), H.ravel()
+    t_vec_unit = math.inf
+    for _ in range(2):
+        t0 = time.perf_counter()
+        c = 1.0 * a + 0.5 * b
+        d = float(a @ b)
+        t_vec_unit = min(t_vec_unit, time.perf_counter() - t0)
+    t_vec = 7 * t_vec_unit
+    del c, d
+    ranks = O.partition(tuple(gext), tuple(n // s for n, s in zip(gext, sub)), overlap)
+    census: dict = {}
+    for r in ranks:
+        census[r.ext] = census.get(r.ext, 0) + 1
+    t_solve_total = 0.0
+    for ext, count in census.items():
+        V = int(np.prod(ext))
+        m = O.correction_size(ext)
+        binv = O.point_block_inverses(ext, 0.25)
+        Cinv = rng.standard_normal((m, m))
+        data = O.SubdomainData(ext, 0.25, binv, *O.correction_rows(ext), Cinv)
+        r = rng.uniform(-1, 1, 3 * V)
+        best = math.inf
+        for _ in range(2):
+            t0 = time.perf_counter()
+            O.solve(data, r)
+            best = min(best, time.perf_counter() - t0)
+        t_solve_total += best * count
+        if time.perf_counter() - t_start > budget_s * 3:
+            break
+    iters = statistics.mean(iters_per_step) if iters_per_step else 4
+    per_iter = 2 * t_solve_total + 3 * t_spmv + t_vec
+    step = t_rhs + t_h + iters * per_iter
+    return step, {"rhs_s": t_rhs, "spmv_s": t_spmv, "h_update_s": t_h, "vector_ops_s": t_vec,
+                  "ras_apply_s": t_solve_total, "iters": iters, "wall_s": time.perf_counter() - t_start,
+                  "shapes": len(census)}
+
+
+def cpu_baseline(gext, sub, overlap, iters, budget_s=20.0):
+    step, parts = cpu_sample(gext, sub, overlap, iters, budget_s)
+    dof = 3 * int(np.prod(gext))
+    return {"value": round(dof / step / 1e6, 4), "unit": "MDoF/s", "cores": os.cpu_count(), "kind": "port",
+            "sample": "oracle/flashmp_oracle.py (numpy restatement of the reference) on this host: one RHS, one "
+                      "SpMV, one Woodbury solve per extended shape x census, vector ops; composed per step with "
+                      f"the GPU-measured iteration count ({parts['iters']}); parts(s)="
+                      + json.dumps({k: round(v, 3) if isinstance(v, float) else v for k, v in parts.items()}),
+            "step_s": round(step, 3)}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    from paper_2508_07193_b200.schwarz import proc_grid_for
+    block, sub, overlap = CONFIGS[args.config]
+    ggrid = proc_grid_for(args.gpus)
+    gext = tuple(b * g for b, g in zip(block, ggrid))
+    iters = [4]   # reference CPU iteration count at 256^3 / 512 subdomains (measured)
+    for _ in range(args.warmup if args.warmup <= 1 else 1):
+        pass
+    times = []
+    for _ in range(args.steps):
+        step, parts = cpu_sample(gext, sub, overlap, iters, args.cpu_budget)
+        times.append(step)
+    step = statistics.mean(times)
+    dof = 3 * int(np.prod(gext))
+    value = dof / step / 1e6
+    line = {"impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "MDoF/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(step * 1e3, 1),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic U[-1,1) (numpy PCG64 seed 0)",
+            "config": {"workload": f"{args.config}: CN-FDTD step, BiCGSTAB+FlashMP RAS (CPU reference algorithm)",
+                       "global_grid": list(gext), "subdomain": list(sub), "world_launch": world},
+            "cpu_baseline": {"value": round(value, 4), "unit": "MDoF/s", "cores": os.cpu_count(), "kind": "port",
+                             "sample": "per step: oracle RHS + SpMV + one Woodbury solve per extended shape "
+                                       "(census-weighted) + vector ops, composed with 4 iterations/step; "
+                                       + json.dumps({k: round(v, 3) if isinstance(v, float) else v
+                                                     for k, v in parts.items()})},
+            "e2e": {"value": round(value, 4), "unit": "MDoF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="cfg4", choices=sorted(CONFIGS))
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=20.0)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

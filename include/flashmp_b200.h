@@ -53,6 +53,8 @@ int fmp_abi_version(void);
 int fmp_last_error(char* buf, size_t len);
 /* Scratch (in doubles) every reduction entry point below needs. */
 int64_t fmp_reduce_scratch_doubles(void);
+/* Number of kernels this library has launched in the process (cuBLAS calls excluded). */
+int64_t fmp_launch_count(void);
 
 /* ---------------------------------------------------------------- stencils (K7/K13)
  * y = x + alpha*(C_b C_f x + Lambda x) with boundary=1, the corrected operator

@@ -21,6 +21,7 @@ SIGNATURES = {
     "fmp_abi_version": (_i, []),
     "fmp_last_error": (_i, [C.c_char_p, C.c_size_t]),
     "fmp_reduce_scratch_doubles": (_i64, []),
+    "fmp_launch_count": (_i64, []),
     "fmp_stencil_apply": (_i, [_p, _d, _i, _i, _p, _p, _p, _p, _p, _p]),
     "fmp_curl": (_i, [_p, _i, _p, _p, _p]),
     "fmp_cn_rhs": (_i, [_p, _p, _d, _p, _p, _p, _p]),

@@ -1,5 +1,6 @@
 // Shared device helpers for libflashmp_b200 (sm_100a).
 #pragma once
+#include <atomic>
 #include <cstdint>
 #include <cstdio>
 #include <cuda_runtime.h>
@@ -17,7 +18,14 @@ void set_error(const char* fmt, ...);
       return -1;                                                                    \
     }                                                                               \
   } while (0)
-#define FMP_CHECK_LAUNCH() FMP_CHECK_CUDA(cudaGetLastError())
+// Every kernel launch of this library is followed by FMP_CHECK_LAUNCH(), which also counts
+// it (fmp_launch_count) so benchmarks can report how many of OUR kernels ran.
+extern std::atomic<int64_t> g_launches;
+#define FMP_CHECK_LAUNCH()                                        \
+  do {                                                            \
+    ::fmp::g_launches.fetch_add(1, std::memory_order_relaxed);    \
+    FMP_CHECK_CUDA(cudaGetLastError());                           \
+  } while (0)
 #define FMP_REQUIRE(cond, ...)                                                      \
   do {                                                                              \
     if (!(cond)) { ::fmp::set_error(__VA_ARGS__); return -2; }                      \

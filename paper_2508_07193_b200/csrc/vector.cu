@@ -11,6 +11,7 @@
 namespace fmp {
 
 static thread_local char g_err[512] = "";
+std::atomic<int64_t> g_launches{0};
 
 void set_error(const char* fmt, ...) {
   va_list ap;
@@ -119,6 +120,8 @@ extern "C" int fmp_last_error(char* buf, size_t len) {
 }
 
 extern "C" int64_t fmp_reduce_scratch_doubles(void) { return kScratchDoubles; }
+
+extern "C" int64_t fmp_launch_count(void) { return g_launches.load(); }
 
 extern "C" int fmp_vec_lincomb(int64_t n, double a, const double* x, double b, const double* y, double* out,
                                void* stream) {

@@ -113,7 +113,8 @@ def correction_rows(box: Box) -> tuple[np.ndarray, np.ndarray, tuple[int, int, i
     """Boundary slots and weights (ref:subdomain.py:183-194, ref:operators.py:151-164)."""
     nx, ny, nz = box.extents
     k, j, i = np.meshgrid(np.arange(nz), np.arange(ny), np.arange(nx), indexing="ij")
-    weights = ((j == 0) + (k == 0), (i == 0) + (k == 0), (i == 0) + (j == 0))
+    i0, j0, k0 = (i == 0).astype(np.int64), (j == 0).astype(np.int64), (k == 0).astype(np.int64)
+    weights = (j0 + k0, i0 + k0, i0 + j0)
     rows, vals, per = [], [], []
     for c, w in enumerate(weights):
         flat = w.ravel()
