@@ -89,7 +89,13 @@ def test_vector_kernels_bitwise_numpy():
     n = 1_000_003
     rng = np.random.default_rng(4)
     a, b, c, d, e, f = (rng.uniform(-1, 1, n) for _ in range(6))
-    T = lambda v: torch.from_numpy(v.copy()).cuda()
+    keep = []
+
+    def T(v):  # keep every device copy alive until the kernels have run (no allocator reuse)
+        t = torch.from_numpy(v.copy()).cuda()
+        keep.append(t)
+        return t
+
     st = _lib.stream()
     out = torch.empty(n, dtype=torch.float64, device="cuda")
     _lib.call("fmp_vec_lincomb", n, 0.7, T(a).data_ptr(), -1.3, T(b).data_ptr(), out.data_ptr(), st)
