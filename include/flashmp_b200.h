@@ -120,16 +120,19 @@ typedef struct fmp_subdomain {   /* 16 x int64 */
   int64_t in_off;        /* element offset of this subdomain's input for compact inputs (mode FACES) */
 } fmp_subdomain;
 
-typedef struct fmp_shape {       /* 16 x int64 */
+typedef struct fmp_shape {       /* 20 x int64 */
   int64_t ext[3];
   int64_t m;             /* boundary-correction size (ref: subdomain.py:235-238) */
   int64_t m_comp[3];     /* rows per component */
   int64_t ut_off[3];     /* offset (doubles) of U^T per axis in the factor buffer */
   int64_t vt_off[3];     /* offset of V^T per axis */
   int64_t s_off[3];      /* offset of the singular values per axis */
+  int64_t qw_off;        /* offset of the per-point block-inverse table: (q, w) pairs, point-major,
+                            q = 1/(1+alpha|s|^2), w = (1-q)/|s|^2  so  B^-1 y = q y + w s (s.y) */
+  int64_t reserved[3];
 } fmp_shape;
 #define FMP_SUBDOMAIN_WORDS 16
-#define FMP_SHAPE_WORDS 16
+#define FMP_SHAPE_WORDS 20
 
 typedef struct fmp_precond_desc {
   double alpha;

@@ -91,6 +91,46 @@ __device__ __forceinline__ double fetch(const Geo& g, const double* __restrict__
   return __ldg(s + ((((int64_t)c * P + kk) * g.by + j) * g.bx + i));
 }
 
+// Address of a block-local point for async copies: nullptr means "reads as zero"
+// (outside the global box, or a missing ghost slab).  Same rules as fetch().
+__device__ __forceinline__ const double* point_ptr(const Geo& g, const double* f, int c, int k, int j, int i) {
+  if ((unsigned)i < (unsigned)g.bx && (unsigned)j < (unsigned)g.by && (unsigned)k < (unsigned)g.bz)
+    return f + fidx(g, c, k, j, i);
+  const int gi = g.gx0 + i, gj = g.gy0 + j, gk = g.gz0 + k;
+  if ((unsigned)gi >= (unsigned)g.nx || (unsigned)gj >= (unsigned)g.ny || (unsigned)gk >= (unsigned)g.nz)
+    return nullptr;
+  const int P = g.P;
+  if (i < 0 || i >= g.bx) {
+    const double* s = i < 0 ? g.ghost[0] : g.ghost[1];
+    if (!s) return nullptr;
+    const int ii = i < 0 ? i + P : i - g.bx;
+    return s + ((((int64_t)c * (g.bz + 2 * P) + (k + P)) * (g.by + 2 * P) + (j + P)) * P + ii);
+  }
+  if (j < 0 || j >= g.by) {
+    const double* s = j < 0 ? g.ghost[2] : g.ghost[3];
+    if (!s) return nullptr;
+    const int jj = j < 0 ? j + P : j - g.by;
+    return s + ((((int64_t)c * (g.bz + 2 * P) + (k + P)) * P + jj) * g.bx + i);
+  }
+  const double* s = k < 0 ? g.ghost[4] : g.ghost[5];
+  if (!s) return nullptr;
+  const int kk = k < 0 ? k + P : k - g.bz;
+  return s + ((((int64_t)c * P + kk) * g.by + j) * g.bx + i);
+}
+
+// ---------------------------------------------------------------- cp.async (LDGSTS)
+// 8-byte async global->shared copy; src == nullptr zero-fills the destination (the copy then
+// reads 0 bytes from `valid`, any mapped global address).
+__device__ __forceinline__ void cp_async8(double* dst, const double* src, const double* valid) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  const int n = src ? 8 : 0;
+  const void* s = src ? (const void*)src : (const void*)valid;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(s), "r"(n));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
 // ---------------------------------------------------------------- numpy-faithful rounding
 __device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }

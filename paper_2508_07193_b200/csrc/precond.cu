@@ -52,294 +52,367 @@ __device__ __forceinline__ const double* fwd_factor(const double* factors, const
   return factors + (a == c ? sh.ut_off[a] : sh.vt_off[a]);
 }
 
-// C[m][n] = sum_k A(m,k) B(k,n) over 8x8 DMMA tiles distributed round-robin over warps.
-// A(m,k) = a[m*sa + k] (or a[k*sa + m] if AT); B(k,n) = b[k*sb + n] (or b[n*sb + k] if BT).
-template <bool AT, bool BT>
-__device__ __forceinline__ void smem_gemm(const double* __restrict__ a, int sa, const double* __restrict__ b, int sb,
-                                          double* __restrict__ c, int sc, int m8, int n8, int k4, int warp,
-                                          int nwarps, int lane) {
-  const int g = lane >> 2, t = lane & 3;
-  for (int tile = warp; tile < m8 * n8; tile += nwarps) {
-    const int mt = tile / n8, nt = tile - mt * n8;
-    const int m = mt * 8 + g, n = nt * 8 + g;
-    double d0 = 0.0, d1 = 0.0;
-#pragma unroll 4
-    for (int kk = 0; kk < k4; ++kk) {
-      const int k = kk * 4 + t;
-      const double av = AT ? a[k * sa + m] : a[m * sa + k];
-      const double bv = BT ? b[n * sb + k] : b[k * sb + n];
-      dmma884(d0, d1, av, bv);
-    }
-    double* cp = c + (mt * 8 + g) * sc + nt * 8 + 2 * t;
-    cp[0] = d0;
-    cp[1] = d1;
-  }
-}
-
-// ---------------------------------------------------------------- K1 / K4: plane passes
-struct PlaneArgs {
-  const fmp_subdomain* subs;
-  const fmp_shape* shapes;
-  const double* factors;
-  Geo g;
-  const double* src;
-  double* dst;
-  int mode;  // FMP_SOLVE_*
-  int ppc;   // planes per CTA
-};
-
-// Load an n x n factor (row-major, rows r < n) into smem with stride s, zero padded to pad8.
-__device__ __forceinline__ void load_factor(double* dst, int s, const double* __restrict__ f, int n) {
-  const int P = pad8(n);
-  for (int q = threadIdx.x; q < P * s; q += blockDim.x) {
-    const int r = q / s, c = q - r * s;
-    dst[q] = (r < n && c < n) ? __ldg(f + r * n + c) : 0.0;
-  }
-}
-
-// Restriction S_i^gamma: point (c, k, j, i) of the extended box read from the block field,
-// its ghost shell (neighbour GPUs) or the global zero ghost (ref:schwarz.py:237-250).
-__device__ __forceinline__ double restrict_point(const Geo& g, const double* __restrict__ src, const SubD& d,
-                                                 bool inside, int c, int k, int j, int i) {
-  if (inside) return __ldg(src + fidx(g, c, d.lz + k, d.ly + j, d.lx + i));
-  return fetch(g, src, c, d.lz + k, d.ly + j, d.lx + i);
-}
-
-__device__ __forceinline__ bool ext_inside(const Geo& g, const SubD& d) {
-  return d.lx >= 0 && d.ly >= 0 && d.lz >= 0 && d.lx + d.ex <= g.bx && d.ly + d.ey <= g.by && d.lz + d.ez <= g.bz;
-}
-
+// ---------------------------------------------------------------- restriction (index maps)
 // Extended vectors of every subdomain, [c][k][j][i] at ws_off: the reference Exchanger's
-// output (ref:schwarz.py:217-257), produced with the same addressing as K1.
+// output (ref:schwarz.py:217-257), read with the same addressing (point_ptr) as K1.
 __global__ void k_restrict(const fmp_subdomain* subs, Geo g, const double* __restrict__ src,
                            double* __restrict__ out) {
   const SubD d = load_sub(subs + blockIdx.z);
   const int c = blockIdx.y, k = blockIdx.x;
   if (k >= d.ez) return;
-  const bool inside = ext_inside(g, d);
   const int64_t P = (int64_t)d.ex * d.ey;
   double* o = out + d.ws_off + (c * d.ez + k) * P;
   for (int q = threadIdx.x; q < P; q += blockDim.x) {
     const int r = q / d.ex, col = q - r * d.ex;
-    o[q] = restrict_point(g, src, d, inside, c, k, r, col);
+    const double* sp = point_ptr(g, src, c, d.lz + k, d.ly + r, d.lx + col);
+    o[q] = sp ? __ldg(sp) : 0.0;
   }
 }
 
-// INV = false (K1): X = r restricted to plane k of the extended box; out = Fy X Fx^T -> work
-// INV = true  (K4): X = work plane k; out = Fy^T X Fx; owned part -> block field z
-template <bool INV>
-__global__ void __launch_bounds__(128) k_plane(PlaneArgs A) {
-  extern __shared__ double smem[];
-  const SubD d = load_sub(A.subs + blockIdx.z);
-  const fmp_shape sh = A.shapes[d.shape];
-  const int c = blockIdx.y;
-  const int nplanes = INV ? d.wz : d.ez;
-  const int kbeg = blockIdx.x * A.ppc;
-  if (kbeg >= nplanes) return;
-  const int kend = min(kbeg + A.ppc, nplanes);
-  const int ex = d.ex, ey = d.ey, PX = pad8(ex), PY = pad8(ey), SXs = sstride(ex), SYs = sstride(ey);
-  double* sFx = smem;               // [PX][SXs]
-  double* sFy = sFx + PX * SXs;     // [PY][SYs]
-  double* sX = sFy + PY * SYs;      // [PY][SXs]
-  double* sT = sX + PY * SXs;       // [PY][SXs]
-  load_factor(sFx, SXs, fwd_factor(A.factors, sh, c, 0), ex);
-  load_factor(sFy, SYs, fwd_factor(A.factors, sh, c, 1), ey);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  const int64_t P = (int64_t)ex * ey;
-  const int64_t V = P * d.ez;
-  // source addressing
-  const bool inside = ext_inside(A.g, d);
-  for (int kk = kbeg; kk < kend; ++kk) {
-    const int k = INV ? d.oz + kk : kk;
-    // ---- load plane into sX (zero padded)
-    for (int q = threadIdx.x; q < PY * SXs; q += blockDim.x) {
-      const int r = q / SXs, col = q - r * SXs;
-      double v = 0.0;
-      if (r < ey && col < ex) {
-        if (INV) {
-          v = A.src[d.ws_off + (c * d.ez + k) * P + r * ex + col];
-        } else if (A.mode == FMP_SOLVE_FACES) {
-          v = A.src[d.in_off + c * V + k * P + r * ex + col];
-        } else {
-          v = restrict_point(A.g, A.src, d, inside, c, k, r, col);
+// ---------------------------------------------------------------- K1 / K4: plane passes
+// Work item = (subdomain, component, slab of nk consecutive z-planes).  nk planes are stacked
+// so that both GEMMs of the 2-D transform have one combined dimension (nk*ey rows, then
+// nk*ex columns) of up to MAXR = 72 = 9 DMMA tiles, which keeps the 8-padding waste on one
+// side only.  One warp owns one 8-wide strip per GEMM and keeps NT independent accumulator
+// tiles (ILP).  CTAs are persistent over a contiguous item range; the next slab streams in
+// with cp.async (LDGSTS) while the current one is multiplied.
+constexpr int MAXR = 72;
+constexpr int PW = 9;                 // warps per plane CTA
+constexpr int TS = 76;                // stride of the step-1 result (>= MAXR, == 4 mod 8)
+__host__ __device__ constexpr int kstride(int n) { return (pad4(n) & 7) == 4 ? pad4(n) : pad4(n) + 4; }
+__host__ __device__ inline int slab_planes(int ex, int ey) {
+  const int a = MAXR / ex, b = MAXR / ey;
+  const int m = a < b ? a : b;
+  return m < 1 ? 1 : m;
+}
+
+struct PlaneArgs {
+  const fmp_subdomain* subs;
+  const fmp_shape* shapes;
+  const double* factors;
+  const int4* items;   // (sub, comp, k0, nk)
+  int n_items;
+  Geo g;
+  const double* src;
+  double* dst;
+  int mode;            // FMP_SOLVE_*
+  int fx_words, fy_words, xs;   // smem carve-out (max over shapes)
+};
+
+// Load an n x n factor (row-major) into smem rows of stride s, zero padded to pad8(n) x s.
+__device__ __forceinline__ void load_factor(double* dst, int s, const double* __restrict__ f, int n, int tid,
+                                            int nt) {
+  const int P = pad8(n);
+  for (int r = 0; r < P; ++r)
+    for (int c = tid; c < s; c += nt) dst[r * s + c] = (r < n && c < n) ? __ldg(f + r * n + c) : 0.0;
+}
+
+// INV = false (K1): slab of r restricted to the extended box -> Fy X Fx^T per plane -> work
+// INV = true  (K4): slab of work planes -> Fy^T X Fx -> owned tile of the block field z
+template <bool INV, int NTM>
+__global__ void __launch_bounds__(PW * 32, 2) k_plane(PlaneArgs A) {
+  extern __shared__ __align__(16) double smem[];
+  double* sFx = smem;
+  double* sFy = sFx + A.fx_words;
+  double* sXb = sFy + A.fy_words;       // 2 x [MAXR][xs]
+  double* sT = sXb + 2 * MAXR * A.xs;   // [pad8(ey)][TS]
+  int* sMap1 = reinterpret_cast<int*>(sT + MAXR * TS);
+  int* sMap2 = sMap1 + MAXR;
+  const int tid = threadIdx.x, nth = blockDim.x;
+  const int warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
+  const int per = (A.n_items + gridDim.x - 1) / gridDim.x;
+  const int beg = blockIdx.x * per, end = min(beg + per, A.n_items);
+  if (beg >= end) return;
+
+  auto issue = [&](int it, int buf) {
+    const int4 w = A.items[it];
+    const SubD d = load_sub(A.subs + w.x);
+    const int c = w.y, ex = d.ex, ey = d.ey, cols = pad4(ex), rows = w.w * ey;
+    const int64_t P = (int64_t)ex * ey, V = P * d.ez;
+    double* X = sXb + buf * MAXR * A.xs;
+    const bool inside = d.lx >= 0 && d.ly >= 0 && d.lz >= 0 && d.lx + ex <= A.g.bx && d.ly + ey <= A.g.by &&
+                        d.lz + d.ez <= A.g.bz;
+    const int rpp = nth / cols;  // rows per pass
+    const int col = tid % cols, r0 = tid / cols;
+    if (r0 < rpp) {
+      for (int r = r0; r < rows; r += rpp) {
+        const int kk = r / ey, j = r - kk * ey;
+        const double* src = nullptr;
+        if (col < ex) {
+          if (INV) {
+            src = A.src + d.ws_off + (c * d.ez + d.oz + w.z + kk) * P + j * ex + col;
+          } else if (A.mode == FMP_SOLVE_FACES) {
+            src = A.src + d.in_off + c * V + (w.z + kk) * P + j * ex + col;
+          } else if (inside) {
+            src = A.src + fidx(A.g, c, d.lz + w.z + kk, d.ly + j, d.lx + col);
+          } else {
+            src = point_ptr(A.g, A.src, c, d.lz + w.z + kk, d.ly + j, d.lx + col);
+          }
+        }
+        cp_async8(X + r * A.xs + col, src, A.factors);
+      }
+    }
+  };
+
+  int buf = 0, cur_shape = -1, cur_c = -1;
+  issue(beg, 0);
+  cp_async_commit();
+  for (int it = beg; it < end; ++it) {
+    if (it + 1 < end) issue(it + 1, buf ^ 1);
+    cp_async_commit();
+    cp_async_wait<1>();
+    const int4 w = A.items[it];
+    const SubD d = load_sub(A.subs + w.x);
+    const int c = w.y, ex = d.ex, ey = d.ey, nk = w.w;
+    const int fsx = pad8(ex) + 4, fsy = pad8(ey) + 4;
+    const int M1 = nk * ey, N2 = nk * ex;
+    __syncthreads();  // (a) slab `buf` landed for everyone; previous item fully consumed
+    if (d.shape != cur_shape || c != cur_c) {
+      const fmp_shape& sh = A.shapes[d.shape];
+      load_factor(sFx, fsx, fwd_factor(A.factors, sh, c, 0), ex, tid, nth);
+      load_factor(sFy, fsy, fwd_factor(A.factors, sh, c, 1), ey, tid, nth);
+      cur_shape = d.shape;
+      cur_c = c;
+    }
+    for (int q = tid; q < MAXR; q += nth) {
+      sMap1[q] = q < M1 ? ((q / ey) << 16) | (q % ey) : 0;
+      sMap2[q] = q < N2 ? ((q / ex) << 16) | (q % ex) : 0;
+    }
+    for (int q = tid; q < (pad4(ey) - ey) * TS; q += nth) sT[(ey + q / TS) * TS + q % TS] = 0.0;  // K pad of step 2
+    __syncthreads();  // (b)
+    const double* X = sXb + buf * MAXR * A.xs;
+    // ---- step 1: T[j][k*ex + a] = sum_i X[(k,j)][i] Fx[a][i]   (INV: sum_a X[(k,b)][a] Fx[a][i])
+    if (warp * 8 < M1) {
+      double acc[NTM][2];
+#pragma unroll
+      for (int n = 0; n < NTM; ++n) acc[n][0] = acc[n][1] = 0.0;
+      const int nt1 = pad8(ex) / 8, k4 = pad4(ex) / 4;
+      const double* xa = X + (warp * 8 + g) * A.xs + t;
+      for (int kk = 0; kk < k4; ++kk) {
+        const double av = xa[kk * 4];
+#pragma unroll
+        for (int n = 0; n < NTM; ++n)
+          if (n < nt1) {
+            const double bv = INV ? sFx[(kk * 4 + t) * fsx + n * 8 + g] : sFx[(n * 8 + g) * fsx + kk * 4 + t];
+            dmma884(acc[n][0], acc[n][1], av, bv);
+          }
+      }
+      const int r = warp * 8 + g;
+      if (r < M1) {
+        const int mp = sMap1[r], kk = mp >> 16, j = mp & 0xffff;
+        double* trow = sT + j * TS + kk * ex;
+#pragma unroll
+        for (int n = 0; n < NTM; ++n)
+          if (n < nt1) {
+            const int a = n * 8 + 2 * t;
+            if (a < ex) trow[a] = acc[n][0];
+            if (a + 1 < ex) trow[a + 1] = acc[n][1];
+          }
+      }
+    }
+    __syncthreads();  // (c)
+    // ---- step 2: O[b][(k,a)] = sum_j Fy[b][j] T[j][(k,a)]   (INV: sum_b Fy[b][j] T[b][(k,i)])
+    if (warp * 8 < N2) {
+      double acc[NTM][2];
+#pragma unroll
+      for (int m = 0; m < NTM; ++m) acc[m][0] = acc[m][1] = 0.0;
+      const int mt2 = pad8(ey) / 8, k4 = pad4(ey) / 4;
+      const double* tb = sT + t * TS + warp * 8 + g;
+      for (int kk = 0; kk < k4; ++kk) {
+        const double bv = tb[kk * 4 * TS];
+#pragma unroll
+        for (int m = 0; m < NTM; ++m)
+          if (m < mt2) {
+            const double av = INV ? sFy[(kk * 4 + t) * fsy + m * 8 + g] : sFy[(m * 8 + g) * fsy + kk * 4 + t];
+            dmma884(acc[m][0], acc[m][1], av, bv);
+          }
+      }
+      const int64_t P = (int64_t)ex * ey;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int n = warp * 8 + 2 * t + h;
+        if (n >= N2) continue;
+        const int mp = sMap2[n], kk = mp >> 16, a = mp & 0xffff;
+#pragma unroll
+        for (int m = 0; m < NTM; ++m) {
+          const int row = m * 8 + g;
+          if (m >= mt2 || row >= ey) continue;
+          if (!INV) {
+            A.dst[d.ws_off + (c * d.ez + w.z + kk) * P + row * ex + a] = acc[m][h];
+          } else {
+            const int jo = row - d.oy, io = a - d.ox;
+            if ((unsigned)jo < (unsigned)d.wy && (unsigned)io < (unsigned)d.wx)
+              A.dst[fidx(A.g, c, d.lz + d.oz + w.z + kk, d.ly + row, d.lx + a)] = acc[m][h];
+          }
         }
       }
-      sX[q] = v;
     }
-    __syncthreads();
-    if (!INV) {
-      // T[j][a] = sum_i X[j][i] Fx[a][i];   O[b][a] = sum_j Fy[b][j] T[j][a]
-      smem_gemm<false, true>(sX, SXs, sFx, SXs, sT, SXs, PY / 8, PX / 8, pad4(ex) / 4, warp, nw, lane);
-      __syncthreads();
-      smem_gemm<false, false>(sFy, SYs, sT, SXs, sX, SXs, PY / 8, PX / 8, pad4(ey) / 4, warp, nw, lane);
-    } else {
-      // T[b][i] = sum_a X[b][a] Fx[a][i];   O[j][i] = sum_b Fy[b][j] T[b][i]
-      smem_gemm<false, false>(sX, SXs, sFx, SXs, sT, SXs, PY / 8, PX / 8, pad4(ex) / 4, warp, nw, lane);
-      __syncthreads();
-      smem_gemm<true, false>(sFy, SYs, sT, SXs, sX, SXs, PY / 8, PX / 8, pad4(ey) / 4, warp, nw, lane);
-    }
-    __syncthreads();
-    if (!INV) {
-      double* out = A.dst + d.ws_off + (c * d.ez + k) * P;
-      for (int q = threadIdx.x; q < P; q += blockDim.x) {
-        const int r = q / ex, col = q - r * ex;
-        out[q] = sX[r * SXs + col];
-      }
-    } else {
-      for (int q = threadIdx.x; q < d.wy * d.wx; q += blockDim.x) {
-        const int r = q / d.wx, col = q - r * d.wx;
-        A.dst[fidx(A.g, c, d.lz + k, d.ly + d.oy + r, d.lx + d.ox + col)] = sX[(d.oy + r) * SXs + d.ox + col];
-      }
-    }
-    __syncthreads();
+    buf ^= 1;
   }
+  cp_async_wait<0>();
 }
 
 // ---------------------------------------------------------------- K2 / K3: column passes
-constexpr int TP = 64;  // columns (flattened (j,i) plane positions) per CTA
+// Work item = (subdomain, 32 consecutive columns p = j*ex + i of the plane), all three
+// components and all z.  The z contraction is the DMMA GEMM Fz (ez x ez) x X (ez x 32);
+// each warp owns 8 columns and keeps 3 components x MT row tiles of accumulators, so the
+// per-point 3x3 block solve happens in registers right after the GEMM (K2), and the
+// folded Woodbury correction is applied to the tile in shared memory before the inverse
+// GEMM (K3).  Persistent CTAs, cp.async double buffering as in the plane pass.
+constexpr int TP = 32;
+constexpr int CW = TP / 8;
+constexpr int SC = TP + 4;   // tile row stride (== 4 mod 8)
 
 struct ColArgs {
   const fmp_subdomain* subs;
   const fmp_shape* shapes;
   const double* factors;
+  const int2* items;   // (sub, p0)
+  int n_items;
   const double* src;
   double* dst;
   const double* corr;  // K3 only, may be null (no correction)
   int pmax;
-  double alpha;
+  int f_words, x_rows;   // smem carve-out: per-factor words, tile rows (pad8 of max ez)
 };
 
-// B^-1 y at a transformed point with singular-value triplet s (ref:subdomain.py:145-153):
-// B^-1 = q I + (1 - q) u u^T, q = 1/(1 + alpha |s|^2), u = s/|s|.
-__device__ __forceinline__ void block_solve(double sx, double sy, double sz, double alpha, double& y0, double& y1,
-                                            double& y2) {
-  const double s2 = sx * sx + sy * sy + sz * sz;
-  const double q = 1.0 / (1.0 + alpha * s2);
-  const double proj = (1.0 - q) * (sx * y0 + sy * y1 + sz * y2) / s2;
-  y0 = q * y0 + proj * sx;
-  y1 = q * y1 + proj * sy;
-  y2 = q * y2 + proj * sz;
-}
-
-// INV = false (K2): X[c][k][p] = work; y^ = B^-1 (Fz X) -> dst
-// INV = true  (K3): X[c][k~][p] = y^ (minus the folded Woodbury term); out = Fz^T X -> dst
 template <int MT, bool INV>
-__global__ void __launch_bounds__(256) k_column(ColArgs A) {
-  extern __shared__ double smem[];
-  const SubD d = load_sub(A.subs + blockIdx.y);
-  const fmp_shape sh = A.shapes[d.shape];
-  const int ex = d.ex, ey = d.ey, ez = d.ez;
-  const int P = ex * ey;
-  const int p0 = blockIdx.x * TP;
-  if (p0 >= P) return;
-  const int PZ = pad8(ez), SZs = sstride(ez), SC = TP + 4;
-  double* sX = smem;                   // [3][PZ][SC]
-  double* sF = sX + 3 * PZ * SC;       // [2][PZ][SZs]: V^T_z (components x, y), U^T_z (component z)
-  load_factor(sF, SZs, A.factors + sh.vt_off[2], ez);
-  load_factor(sF + PZ * SZs, SZs, A.factors + sh.ut_off[2], ez);
-  const int64_t V = (int64_t)P * ez;
-  const double* src = A.src + d.ws_off;
-  for (int q = threadIdx.x; q < 3 * PZ * SC; q += blockDim.x) {
-    const int cc = q / (PZ * SC), rem = q - cc * PZ * SC, r = rem / SC, col = rem - r * SC;
-    double v = 0.0;
-    if (r < ez && col < TP && p0 + col < P) v = src[cc * V + (int64_t)r * P + p0 + col];
-    sX[q] = v;
-  }
-  const double* Sx = A.factors + sh.s_off[0];
-  const double* Sy = A.factors + sh.s_off[1];
-  const double* Sz = A.factors + sh.s_off[2];
-  __syncthreads();
-  if (INV && A.corr) {
-    // y^ -= B^-1 (G Q Z): per component two rank-structured face terms (see K6)
-    const double* cb = A.corr + (int64_t)blockIdx.y * 6 * A.pmax * A.pmax;
-    const int pm = A.pmax, pm2 = pm * pm;
-    const double* Fx0 = A.factors + sh.ut_off[0];  // comp x on axis x uses U^T, others V^T
-    const double* Vx = A.factors + sh.vt_off[0];
-    const double* Uy = A.factors + sh.ut_off[1];
-    const double* Vy = A.factors + sh.vt_off[1];
-    const double* Uz = A.factors + sh.ut_off[2];
-    const double* Vz = A.factors + sh.vt_off[2];
-    (void)Fx0;
-    for (int q = threadIdx.x; q < ez * TP; q += blockDim.x) {
-      const int cz = q / TP, col = q - cz * TP;
-      const int p = p0 + col;
-      if (p >= P) continue;
-      const int b = p / ex, a = p - b * ex;
-      // comp x: Fz=V_z, Fy=V_y:  Fz[cz][0] * G_x[b][a] + Fy[b][0] * F_x[cz][a]
-      double dx = Vz[cz * ez] * cb[0 * pm2 + b * pm + a] + Vy[b * ey] * cb[1 * pm2 + cz * pm + a];
-      // comp y: Fz=V_z, Fx=V_x:  Fz[cz][0] * G_y[b][a] + Fx[a][0] * F_y[cz][b]
-      double dy = Vz[cz * ez] * cb[2 * pm2 + b * pm + a] + Vx[a * ex] * cb[3 * pm2 + cz * pm + b];
-      // comp z: Fy=V_y, Fx=V_x:  Fy[b][0] * G_z[cz][a] + Fx[a][0] * F_z[cz][b]
-      double dz = Vy[b * ey] * cb[4 * pm2 + cz * pm + a] + Vx[a * ex] * cb[5 * pm2 + cz * pm + b];
-      (void)Uy; (void)Uz;
-      block_solve(Sx[a], Sy[b], Sz[cz], A.alpha, dx, dy, dz);
-      sX[(0 * PZ + cz) * SC + col] -= dx;
-      sX[(1 * PZ + cz) * SC + col] -= dy;
-      sX[(2 * PZ + cz) * SC + col] -= dz;
+__global__ void __launch_bounds__(CW * 32, 2) k_column(ColArgs A) {
+  extern __shared__ __align__(16) double smem[];
+  double* sF = smem;                      // [2][pad8(ez)][pad8(ez)+4]: V^T_z (comps x,y), U^T_z (comp z)
+  double* sXb = sF + 2 * A.f_words;       // 2 x [3][x_rows][SC]
+  const int xbuf = 3 * A.x_rows * SC;
+  const int tid = threadIdx.x, nth = blockDim.x;
+  const int warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
+  const int per = (A.n_items + gridDim.x - 1) / gridDim.x;
+  const int beg = blockIdx.x * per, end = min(beg + per, A.n_items);
+  if (beg >= end) return;
+
+  auto issue = [&](int it, int buf) {
+    const int2 w = A.items[it];
+    const SubD d = load_sub(A.subs + w.x);
+    const int P = d.ex * d.ey, rows = pad4(d.ez);
+    const int64_t V = (int64_t)P * d.ez;
+    const double* src = A.src + d.ws_off;
+    double* X = sXb + buf * xbuf;
+    const int col = tid % TP;
+    const bool cval = w.y + col < P;
+    for (int r = tid / TP; r < 3 * rows; r += nth / TP) {
+      const int cc = r / rows, k = r - cc * rows;
+      cp_async8(X + (cc * A.x_rows + k) * SC + col,
+                (cval && k < d.ez) ? src + cc * V + (int64_t)k * P + w.y + col : nullptr, A.factors);
     }
-    __syncthreads();
-  }
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int g = lane >> 2, t = lane & 3;
-  const int nt = warp;  // 8 warps x 8 columns = TP
-  const int m8 = PZ / 8, k4 = pad4(ez) / 4;
-  double acc[3][MT][2];
-#pragma unroll
-  for (int cc = 0; cc < 3; ++cc)
-#pragma unroll
-    for (int mt = 0; mt < MT; ++mt) acc[cc][mt][0] = acc[cc][mt][1] = 0.0;
-  const double* Fv = sF;
-  const double* Fu = sF + PZ * SZs;
-  for (int kk = 0; kk < k4; ++kk) {
-    const int k = kk * 4 + t;
-    const double b0 = sX[(0 * PZ + k) * SC + nt * 8 + g];
-    const double b1 = sX[(1 * PZ + k) * SC + nt * 8 + g];
-    const double b2 = sX[(2 * PZ + k) * SC + nt * 8 + g];
-#pragma unroll
-    for (int mt = 0; mt < MT; ++mt) {
-      if (mt < m8) {
-        const int m = mt * 8 + g;
-        const double av = INV ? Fv[k * SZs + m] : Fv[m * SZs + k];
-        const double au = INV ? Fu[k * SZs + m] : Fu[m * SZs + k];
-        dmma884(acc[0][mt][0], acc[0][mt][1], av, b0);
-        dmma884(acc[1][mt][0], acc[1][mt][1], av, b1);
-        dmma884(acc[2][mt][0], acc[2][mt][1], au, b2);
+  };
+
+  int buf = 0, cur_shape = -1;
+  issue(beg, 0);
+  cp_async_commit();
+  for (int it = beg; it < end; ++it) {
+    if (it + 1 < end) issue(it + 1, buf ^ 1);
+    cp_async_commit();
+    cp_async_wait<1>();
+    const int2 w = A.items[it];
+    const SubD d = load_sub(A.subs + w.x);
+    const fmp_shape& sh = A.shapes[d.shape];
+    const int ex = d.ex, ey = d.ey, ez = d.ez, P = ex * ey, p0 = w.y;
+    const int fs = pad8(ez) + 4;
+    const int64_t V = (int64_t)P * ez;
+    double* X = sXb + buf * xbuf;
+    __syncthreads();  // (a)
+    if (d.shape != cur_shape) {
+      load_factor(sF, fs, A.factors + sh.vt_off[2], ez, tid, nth);
+      load_factor(sF + A.f_words, fs, A.factors + sh.ut_off[2], ez, tid, nth);
+      cur_shape = d.shape;
+      __syncthreads();
+    }
+    const double* Sx = A.factors + sh.s_off[0];
+    const double* Sy = A.factors + sh.s_off[1];
+    const double* Sz = A.factors + sh.s_off[2];
+    const double* QW = A.factors + sh.qw_off;
+    if (INV && A.corr) {
+      // y^ -= B^-1 (G Q Z): two rank-structured face terms per component (see K6)
+      const double* cb = A.corr + (int64_t)w.x * 6 * A.pmax * A.pmax;
+      const int pm = A.pmax, pm2 = pm * pm;
+      const double* Vx = A.factors + sh.vt_off[0];
+      const double* Vy = A.factors + sh.vt_off[1];
+      const int col = tid % TP, p = p0 + col;
+      if (p < P) {
+        const int b = p / ex, a = p - b * ex;
+        const double vy0 = __ldg(Vy + b * ey), vx0 = __ldg(Vx + a * ex), sx = __ldg(Sx + a), sy = __ldg(Sy + b);
+        for (int cz = tid / TP; cz < ez; cz += nth / TP) {
+          const double vz0 = sF[cz * fs];  // V^T_z[cz][0]
+          double dx = vz0 * cb[0 * pm2 + b * pm + a] + vy0 * cb[1 * pm2 + cz * pm + a];
+          double dy = vz0 * cb[2 * pm2 + b * pm + a] + vx0 * cb[3 * pm2 + cz * pm + b];
+          double dz = vy0 * cb[4 * pm2 + cz * pm + a] + vx0 * cb[5 * pm2 + cz * pm + b];
+          const double sz = __ldg(Sz + cz);
+          const double q = __ldg(QW + 2 * ((int64_t)cz * P + p)), wq = __ldg(QW + 2 * ((int64_t)cz * P + p) + 1);
+          const double pr = wq * (sx * dx + sy * dy + sz * dz);
+          X[(0 * A.x_rows + cz) * SC + col] -= q * dx + pr * sx;
+          X[(1 * A.x_rows + cz) * SC + col] -= q * dy + pr * sy;
+          X[(2 * A.x_rows + cz) * SC + col] -= q * dz + pr * sz;
+        }
       }
+      __syncthreads();
     }
-  }
-  if (!INV) {
+    const int m8 = pad8(ez) / 8, k4 = pad4(ez) / 4;
+    double acc[3][MT][2];
 #pragma unroll
-    for (int mt = 0; mt < MT; ++mt) {
-      if (mt < m8) {
-        const int cz = mt * 8 + g;
+    for (int cc = 0; cc < 3; ++cc)
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int p = p0 + nt * 8 + 2 * t + h;
-          if (cz < ez && p < P) {
-            const int b = p / ex, a = p - b * ex;
-            block_solve(Sx[a], Sy[b], Sz[cz], A.alpha, acc[0][mt][h], acc[1][mt][h], acc[2][mt][h]);
-          }
+      for (int m = 0; m < MT; ++m) acc[cc][m][0] = acc[cc][m][1] = 0.0;
+    const double* Fv = sF;
+    const double* Fu = sF + A.f_words;
+    const double* xb = X + t * SC + warp * 8 + g;
+    for (int kk = 0; kk < k4; ++kk) {
+      const int k = kk * 4 + t;
+      const double b0 = xb[(0 * A.x_rows + kk * 4) * SC];
+      const double b1 = xb[(1 * A.x_rows + kk * 4) * SC];
+      const double b2 = xb[(2 * A.x_rows + kk * 4) * SC];
+#pragma unroll
+      for (int m = 0; m < MT; ++m) {
+        if (m < m8) {
+          const int r = m * 8 + g;
+          const double av = INV ? Fv[k * fs + r] : Fv[r * fs + k];
+          const double au = INV ? Fu[k * fs + r] : Fu[r * fs + k];
+          dmma884(acc[0][m][0], acc[0][m][1], av, b0);
+          dmma884(acc[1][m][0], acc[1][m][1], av, b1);
+          dmma884(acc[2][m][0], acc[2][m][1], au, b2);
         }
       }
     }
-  }
-  __syncthreads();
+    double* dst = A.dst + d.ws_off;
 #pragma unroll
-  for (int cc = 0; cc < 3; ++cc)
-#pragma unroll
-    for (int mt = 0; mt < MT; ++mt)
-      if (mt < m8) {
-        double* o = sX + (cc * PZ + mt * 8 + g) * SC + nt * 8 + 2 * t;
-        o[0] = acc[cc][mt][0];
-        o[1] = acc[cc][mt][1];
+    for (int h = 0; h < 2; ++h) {
+      const int p = p0 + warp * 8 + 2 * t + h;
+      if (p >= P) continue;
+      double sx = 0.0, sy = 0.0;
+      if (!INV) {
+        const int b = p / ex, a = p - b * ex;
+        sx = __ldg(Sx + a);
+        sy = __ldg(Sy + b);
       }
-  __syncthreads();
-  double* dst = A.dst + d.ws_off;
-  const int ncol = min(TP, P - p0);
-  for (int q = threadIdx.x; q < 3 * ez * TP; q += blockDim.x) {
-    const int cc = q / (ez * TP), rem = q - cc * ez * TP, r = rem / TP, col = rem - r * TP;
-    if (col < ncol) dst[cc * V + (int64_t)r * P + p0 + col] = sX[(cc * PZ + r) * SC + col];
+#pragma unroll
+      for (int m = 0; m < MT; ++m) {
+        const int r = m * 8 + g;
+        if (m >= m8 || r >= ez) continue;
+        double y0 = acc[0][m][h], y1 = acc[1][m][h], y2 = acc[2][m][h];
+        if (!INV) {  // B^-1 y = q y + w s (s . y)   (ref:subdomain.py:145-153, table form)
+          const double sz = __ldg(Sz + r);
+          const double q = __ldg(QW + 2 * ((int64_t)r * P + p)), wq = __ldg(QW + 2 * ((int64_t)r * P + p) + 1);
+          const double pr = wq * (sx * y0 + sy * y1 + sz * y2);
+          y0 = q * y0 + pr * sx;
+          y1 = q * y1 + pr * sy;
+          y2 = q * y2 + pr * sz;
+        }
+        const int64_t o = (int64_t)r * P + p;
+        dst[o] = y0;
+        dst[V + o] = y1;
+        dst[2 * V + o] = y2;
+      }
+    }
+    buf ^= 1;
   }
+  cp_async_wait<0>();
 }
 
 // ---------------------------------------------------------------- K5 / K6: boundary faces
@@ -518,9 +591,56 @@ struct fmp_precond {
   std::vector<double*> ymat, zmat;
   double** d_ymat = nullptr;  // device copies of the pointer tables
   double** d_zmat = nullptr;
+  int4* d_fwd_items = nullptr;   // K1 work items
+  int4* d_inv_items = nullptr;   // K4 work items
+  int2* d_col_items = nullptr;   // K2/K3 work items
+  int n_fwd = 0, n_inv = 0, n_col = 0;
   cublasHandle_t blas = nullptr;
-  int max_ex = 1, max_ey = 1, max_ez = 1, max_p = 1, max_wz = 1;
+  int max_ex = 1, max_ey = 1, max_ez = 1, max_p = 1;
+  int sms = kNumSM;
 };
+
+template <class T>
+static int upload(const std::vector<T>& v, T** out) {
+  *out = nullptr;
+  if (v.empty()) return 0;
+  FMP_CHECK_CUDA(cudaMalloc(out, sizeof(T) * v.size()));
+  FMP_CHECK_CUDA(cudaMemcpy(*out, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice));
+  return 0;
+}
+
+static void free_plan(fmp_precond* p) {
+  if (!p) return;
+  if (p->blas) cublasDestroy(p->blas);
+  cudaFree(p->d_ymat);
+  cudaFree(p->d_zmat);
+  cudaFree(p->d_fwd_items);
+  cudaFree(p->d_inv_items);
+  cudaFree(p->d_col_items);
+  delete p;
+}
+
+// smem footprints (doubles) for the largest shape in the plan
+static size_t plane_smem(const fmp_precond* p, int* fxw, int* fyw, int* xs) {
+  *fxw = pad8(p->max_ex) * (pad8(p->max_ex) + 4);
+  *fyw = pad8(p->max_ey) * (pad8(p->max_ey) + 4);
+  *xs = kstride(p->max_ex);
+  return (size_t)(*fxw + *fyw + 2 * MAXR * *xs + MAXR * TS) * sizeof(double) + 2 * MAXR * sizeof(int);
+}
+static size_t column_smem(const fmp_precond* p, int* fw, int* xrows) {
+  *fw = pad8(p->max_ez) * (pad8(p->max_ez) + 4);
+  *xrows = pad8(p->max_ez);
+  return (size_t)(2 * *fw + 2 * 3 * *xrows * SC) * sizeof(double);
+}
+
+template <bool INV, int NTM>
+static void plane_attr(size_t smem) {
+  cudaFuncSetAttribute(k_plane<INV, NTM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+}
+template <int MT, bool INV>
+static void column_attr(size_t smem) {
+  cudaFuncSetAttribute(k_column<MT, INV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+}
 
 extern "C" int fmp_precond_create(const fmp_precond_desc* desc, fmp_precond** out) {
   FMP_REQUIRE(desc && out, "null argument");
@@ -533,104 +653,118 @@ extern "C" int fmp_precond_create(const fmp_precond_desc* desc, fmp_precond** ou
   p->cinv.assign(desc->cinv, desc->cinv + desc->n_shape);
   p->ymat.assign(desc->ymat, desc->ymat + desc->n_shape);
   p->zmat.assign(desc->zmat, desc->zmat + desc->n_shape);
-  for (const auto& s : p->subs) {
-    p->max_ex = std::max<int>(p->max_ex, (int)s.ext[0]);
-    p->max_ey = std::max<int>(p->max_ey, (int)s.ext[1]);
-    p->max_ez = std::max<int>(p->max_ez, (int)s.ext[2]);
-    p->max_p = std::max<int>(p->max_p, (int)(s.ext[0] * s.ext[1]));
-    p->max_wz = std::max<int>(p->max_wz, (int)s.own[2]);
+  std::vector<int4> fwd, inv;
+  std::vector<int2> col;
+  for (int64_t q = 0; q < desc->n_sub; ++q) {
+    const auto& s = p->subs[q];
+    const int ex = (int)s.ext[0], ey = (int)s.ext[1], ez = (int)s.ext[2], wz = (int)s.own[2];
+    p->max_ex = std::max(p->max_ex, ex);
+    p->max_ey = std::max(p->max_ey, ey);
+    p->max_ez = std::max(p->max_ez, ez);
+    p->max_p = std::max(p->max_p, ex * ey);
+    const int ns = slab_planes(ex, ey);
+    for (int c = 0; c < 3; ++c) {
+      for (int k0 = 0; k0 < ez; k0 += ns) fwd.push_back(make_int4((int)q, c, k0, std::min(ns, ez - k0)));
+      for (int k0 = 0; k0 < wz; k0 += ns) inv.push_back(make_int4((int)q, c, k0, std::min(ns, wz - k0)));
+    }
+    for (int p0 = 0; p0 < ex * ey; p0 += TP) col.push_back(make_int2((int)q, p0));
   }
   const int mx = std::max(p->max_ex, std::max(p->max_ey, p->max_ez));
-  if (mx > 72 || mx > desc->pmax) {
-    delete p;
-    FMP_REQUIRE(false, "extended extent %d exceeds the supported maximum 72 (or pmax %lld)", mx,
+  if (mx > MAXR || mx > desc->pmax) {
+    free_plan(p);
+    FMP_REQUIRE(false, "extended extent %d exceeds the supported maximum %d (or pmax %lld)", mx, MAXR,
                 (long long)desc->pmax);
   }
-  if (cudaMalloc(&p->d_ymat, sizeof(double*) * desc->n_shape) != cudaSuccess ||
-      cudaMalloc(&p->d_zmat, sizeof(double*) * desc->n_shape) != cudaSuccess) {
-    delete p;
-    FMP_REQUIRE(false, "cudaMalloc of pointer tables failed");
+  p->n_fwd = (int)fwd.size();
+  p->n_inv = (int)inv.size();
+  p->n_col = (int)col.size();
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&p->sms, cudaDevAttrMultiProcessorCount, dev);
+  if (upload(fwd, &p->d_fwd_items) || upload(inv, &p->d_inv_items) || upload(col, &p->d_col_items) ||
+      upload(p->ymat, &p->d_ymat) || upload(p->zmat, &p->d_zmat)) {
+    free_plan(p);
+    return -1;
   }
-  cudaMemcpy(p->d_ymat, p->ymat.data(), sizeof(double*) * desc->n_shape, cudaMemcpyHostToDevice);
-  cudaMemcpy(p->d_zmat, p->zmat.data(), sizeof(double*) * desc->n_shape, cudaMemcpyHostToDevice);
   if (cublasCreate(&p->blas) != CUBLAS_STATUS_SUCCESS) {
-    cudaFree(p->d_ymat);
-    cudaFree(p->d_zmat);
-    delete p;
+    free_plan(p);
     FMP_REQUIRE(false, "cublasCreate failed");
   }
   cublasSetMathMode(p->blas, CUBLAS_DEFAULT_MATH);
-  // shared-memory opt-in for the largest configuration we may launch
-  cudaFuncSetAttribute(k_plane<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-  cudaFuncSetAttribute(k_plane<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  int a, b, c2;
+  const size_t ps = plane_smem(p, &a, &b, &c2);
+  plane_attr<false, 5>(ps); plane_attr<true, 5>(ps); plane_attr<false, 9>(ps); plane_attr<true, 9>(ps);
+  const size_t cs = column_smem(p, &a, &b);
+  column_attr<1, false>(cs); column_attr<2, false>(cs); column_attr<3, false>(cs); column_attr<4, false>(cs);
+  column_attr<5, false>(cs); column_attr<6, false>(cs); column_attr<7, false>(cs); column_attr<8, false>(cs);
+  column_attr<9, false>(cs);
+  column_attr<1, true>(cs); column_attr<2, true>(cs); column_attr<3, true>(cs); column_attr<4, true>(cs);
+  column_attr<5, true>(cs); column_attr<6, true>(cs); column_attr<7, true>(cs); column_attr<8, true>(cs);
+  column_attr<9, true>(cs);
   cudaFuncSetAttribute(k_faces, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   cudaFuncSetAttribute(k_corr, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  FMP_CHECK_CUDA(cudaGetLastError());
   *out = p;
   return 0;
 }
 
 extern "C" int fmp_precond_destroy(fmp_precond* p) {
-  if (!p) return 0;
-  if (p->blas) cublasDestroy(p->blas);
-  cudaFree(p->d_ymat);
-  cudaFree(p->d_zmat);
-  delete p;
-  return 0;
-}
-
-template <int MT>
-static int launch_column(bool inv, dim3 grid, size_t smem, cudaStream_t st, const ColArgs& a) {
-  if (inv) {
-    cudaFuncSetAttribute(k_column<MT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_column<MT, true><<<grid, 256, smem, st>>>(a);
-  } else {
-    cudaFuncSetAttribute(k_column<MT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_column<MT, false><<<grid, 256, smem, st>>>(a);
-  }
-  FMP_CHECK_LAUNCH();
+  free_plan(p);
   return 0;
 }
 
 static int column_pass(fmp_precond* p, bool inv, const double* src, double* dst, const double* corr,
                        cudaStream_t st) {
-  ColArgs a{p->d.subs, p->d.shapes, p->d.factors, src, dst, corr, (int)p->d.pmax, p->d.alpha};
-  const int PZ = pad8(p->max_ez);
-  const size_t smem = (size_t)(3 * PZ * (TP + 4) + 2 * PZ * sstride(p->max_ez)) * sizeof(double);
-  dim3 grid((p->max_p + TP - 1) / TP, (unsigned)p->d.n_sub);
-  switch (PZ / 8) {
-    case 1: return launch_column<1>(inv, grid, smem, st, a);
-    case 2: return launch_column<2>(inv, grid, smem, st, a);
-    case 3: return launch_column<3>(inv, grid, smem, st, a);
-    case 4: return launch_column<4>(inv, grid, smem, st, a);
-    case 5: return launch_column<5>(inv, grid, smem, st, a);
-    case 6: return launch_column<6>(inv, grid, smem, st, a);
-    case 7: return launch_column<7>(inv, grid, smem, st, a);
-    case 8: return launch_column<8>(inv, grid, smem, st, a);
-    case 9: return launch_column<9>(inv, grid, smem, st, a);
+  ColArgs a{};
+  a.subs = p->d.subs;
+  a.shapes = p->d.shapes;
+  a.factors = p->d.factors;
+  a.items = p->d_col_items;
+  a.n_items = p->n_col;
+  a.src = src;
+  a.dst = dst;
+  a.corr = corr;
+  a.pmax = (int)p->d.pmax;
+  const size_t smem = column_smem(p, &a.f_words, &a.x_rows);
+  const int grid = std::min(p->n_col, 2 * p->sms);
+#define FMP_COL(MT)                                                                   \
+  case MT:                                                                            \
+    if (inv)                                                                          \
+      k_column<MT, true><<<grid, CW * 32, smem, st>>>(a);                             \
+    else                                                                              \
+      k_column<MT, false><<<grid, CW * 32, smem, st>>>(a);                            \
+    break;
+  switch (pad8(p->max_ez) / 8) {
+    FMP_COL(1) FMP_COL(2) FMP_COL(3) FMP_COL(4) FMP_COL(5) FMP_COL(6) FMP_COL(7) FMP_COL(8) FMP_COL(9)
+    default: FMP_REQUIRE(false, "unsupported z extent");
   }
-  FMP_REQUIRE(false, "unsupported z extent");
+#undef FMP_COL
+  FMP_CHECK_LAUNCH();
+  return 0;
 }
 
 static int plane_pass(fmp_precond* p, const fmp_block* blk, bool inv, int mode, const double* src, double* dst,
                       cudaStream_t st) {
-  PlaneArgs a;
+  PlaneArgs a{};
   a.subs = p->d.subs;
   a.shapes = p->d.shapes;
   a.factors = p->d.factors;
+  a.items = inv ? p->d_inv_items : p->d_fwd_items;
+  a.n_items = inv ? p->n_inv : p->n_fwd;
   a.g = make_geo(blk);
   a.src = src;
   a.dst = dst;
   a.mode = mode;
-  a.ppc = 2;
-  const int PX = pad8(p->max_ex), PY = pad8(p->max_ey);
-  const size_t smem =
-      (size_t)(PX * sstride(p->max_ex) + PY * sstride(p->max_ey) + 2 * PY * sstride(p->max_ex)) * sizeof(double);
-  const int planes = inv ? p->max_wz : p->max_ez;
-  dim3 grid((planes + a.ppc - 1) / a.ppc, 3, (unsigned)p->d.n_sub);
-  if (inv)
-    k_plane<true><<<grid, 128, smem, st>>>(a);
-  else
-    k_plane<false><<<grid, 128, smem, st>>>(a);
+  const size_t smem = plane_smem(p, &a.fx_words, &a.fy_words, &a.xs);
+  const int grid = std::min(a.n_items, 2 * p->sms);
+  const bool small = std::max(p->max_ex, p->max_ey) <= 40;
+  if (inv) {
+    if (small) k_plane<true, 5><<<grid, PW * 32, smem, st>>>(a);
+    else k_plane<true, 9><<<grid, PW * 32, smem, st>>>(a);
+  } else {
+    if (small) k_plane<false, 5><<<grid, PW * 32, smem, st>>>(a);
+    else k_plane<false, 9><<<grid, PW * 32, smem, st>>>(a);
+  }
   FMP_CHECK_LAUNCH();
   return 0;
 }

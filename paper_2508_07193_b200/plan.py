@@ -37,21 +37,36 @@ def correction_counts(ext) -> tuple[int, int, int]:
 
 
 class FactorTable:
-    """U^T, V^T (row-major) and S for every distinct axis extent, in one device buffer."""
+    """One device buffer with, per distinct axis extent, U^T, V^T (row-major) and S, and per
+    extended shape the block-inverse table: (q, w) per transformed point (c', b, a) with
+    q = 1/(1 + alpha |s|^2), w = (1 - q)/|s|^2, so B^-1 y = q y + w s (s . y)
+    (the closed form of ref:subdomain.py:137-153)."""
 
-    def __init__(self, extents, device):
-        blocks, self.offsets, off = [], {}, 0
-        for n in sorted(set(extents)):
-            s = svd_of_difference(n)
-            ut, vt = np.ascontiguousarray(s.U.T), np.ascontiguousarray(s.Vt)
-            self.offsets[n] = (off, off + n * n, off + 2 * n * n)
-            blocks += [ut.ravel(), vt.ravel(), s.S.ravel()]
-            off += 2 * n * n + n
+    def __init__(self, shapes, alpha: float, device):
+        blocks, self.offsets, self.qw, off = [], {}, {}, 0
+
+        def push(arr):
+            nonlocal off
+            start = off
+            blocks.append(np.ascontiguousarray(arr, dtype=np.float64).ravel())
+            off += blocks[-1].size
             pad = (-off) % 8
             if pad:
                 blocks.append(np.zeros(pad))
                 off += pad
-        self.host = np.concatenate(blocks) if blocks else np.zeros(1)
+            return start
+
+        for n in sorted({n for e in shapes for n in e}):
+            sv = svd_of_difference(n)
+            self.offsets[n] = (push(sv.U.T), push(sv.Vt), push(sv.S))
+        for e in shapes:
+            nx, ny, nz = e
+            S = [svd_of_difference(n).S for n in e]
+            s2 = S[2][:, None, None] ** 2 + S[1][None, :, None] ** 2 + S[0][None, None, :] ** 2
+            q = 1.0 / (1.0 + alpha * s2)
+            w = (1.0 - q) / s2
+            self.qw[e] = push(np.stack([q, w], axis=-1))
+        self.host = np.concatenate(blocks) if blocks else np.zeros(8)
         self.device = torch.from_numpy(self.host).to(device)
 
 
@@ -71,16 +86,17 @@ class SolvePlan:
         self.subs = [subs[q] for q in order]
         self.order = order
         self.shapes = shapes
-        self.factors = FactorTable([n for e in shapes for n in e], self.device)
+        self.factors = FactorTable(shapes, self.alpha, self.device)
         self.pmax = max(max(e) for e in shapes)
         # ---- shape table
-        sh_rec = np.zeros((len(shapes), 16), dtype=np.int64)
+        sh_rec = np.zeros((len(shapes), 20), dtype=np.int64)
         self.m = []
         for q, e in enumerate(shapes):
             mc = correction_counts(e)
             self.m.append(sum(mc))
             offs = [self.factors.offsets[n] for n in e]
-            sh_rec[q] = [*e, sum(mc), *mc, *(o[0] for o in offs), *(o[1] for o in offs), *(o[2] for o in offs)]
+            sh_rec[q] = [*e, sum(mc), *mc, *(o[0] for o in offs), *(o[1] for o in offs), *(o[2] for o in offs),
+                         self.factors.qw[e], 0, 0, 0]
         # ---- subdomain table, workspace layout
         sub_rec = np.zeros((len(self.subs), 16), dtype=np.int64)
         first = np.zeros(len(shapes) + 1, dtype=np.int64)
