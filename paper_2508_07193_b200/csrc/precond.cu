@@ -96,7 +96,6 @@ struct PlaneArgs {
   const double* src;
   double* dst;
   int mode;            // FMP_SOLVE_*
-  int fx_words, fy_words, xs;   // smem carve-out (max over shapes)
 };
 
 // Load an n x n factor (row-major) into smem rows of stride s, zero padded to pad8(n) x s.
@@ -109,27 +108,46 @@ __device__ __forceinline__ void load_factor(double* dst, int s, const double* __
 
 // INV = false (K1): slab of r restricted to the extended box -> Fy X Fx^T per plane -> work
 // INV = true  (K4): slab of work planes -> Fy^T X Fx -> owned tile of the block field z
-template <bool INV, int NTM>
+// NT = 8-wide tiles covering the largest x/y extent of the plan (5 for 33/34, 9 for <= 72):
+// all strides are compile-time, and tiles past the current extent compute on zero padding
+// instead of branching (mma.sync under a predicate costs a WARPSYNC per instruction).
+template <int NT>
+struct PlaneSmem {
+  static constexpr int FS = NT * 8 + 4;            // factor row stride (== 4 mod 8)
+  static constexpr int XS = NT * 8 + 4;            // slab row stride
+  static constexpr int F = NT * 8 * FS;            // one factor
+  static constexpr int X = MAXR * XS;              // one slab buffer
+  static constexpr int T = NT * 8 * TS;            // step-1 result
+  static constexpr size_t bytes = (size_t)(2 * F + 2 * X + T) * sizeof(double) + 2 * MAXR * sizeof(int);
+};
+
+template <bool INV, int NT>
 __global__ void __launch_bounds__(PW * 32, 2) k_plane(PlaneArgs A) {
+  using L = PlaneSmem<NT>;
+  constexpr int FS = L::FS, XS = L::XS;
   extern __shared__ __align__(16) double smem[];
   double* sFx = smem;
-  double* sFy = sFx + A.fx_words;
-  double* sXb = sFy + A.fy_words;       // 2 x [MAXR][xs]
-  double* sT = sXb + 2 * MAXR * A.xs;   // [pad8(ey)][TS]
-  int* sMap1 = reinterpret_cast<int*>(sT + MAXR * TS);
+  double* sFy = sFx + L::F;
+  double* sXb = sFy + L::F;       // 2 x [MAXR][XS]
+  double* sT = sXb + 2 * L::X;    // [NT*8][TS]
+  int* sMap1 = reinterpret_cast<int*>(sT + L::T);
   int* sMap2 = sMap1 + MAXR;
   const int tid = threadIdx.x, nth = blockDim.x;
   const int warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
   const int per = (A.n_items + gridDim.x - 1) / gridDim.x;
   const int beg = blockIdx.x * per, end = min(beg + per, A.n_items);
   if (beg >= end) return;
+  // zero the factor and result buffers once: padding rows/cols must read as 0 (K padding)
+  for (int q = tid; q < 2 * L::F; q += nth) smem[q] = 0.0;
+  for (int q = tid; q < L::T; q += nth) sT[q] = 0.0;
+  __syncthreads();
 
   auto issue = [&](int it, int buf) {
     const int4 w = A.items[it];
     const SubD d = load_sub(A.subs + w.x);
     const int c = w.y, ex = d.ex, ey = d.ey, cols = pad4(ex), rows = w.w * ey;
     const int64_t P = (int64_t)ex * ey, V = P * d.ez;
-    double* X = sXb + buf * MAXR * A.xs;
+    double* X = sXb + buf * L::X;
     const bool inside = d.lx >= 0 && d.ly >= 0 && d.lz >= 0 && d.lx + ex <= A.g.bx && d.ly + ey <= A.g.by &&
                         d.lz + d.ez <= A.g.bz;
     const int rpp = nth / cols;  // rows per pass
@@ -149,12 +167,12 @@ __global__ void __launch_bounds__(PW * 32, 2) k_plane(PlaneArgs A) {
             src = point_ptr(A.g, A.src, c, d.lz + w.z + kk, d.ly + j, d.lx + col);
           }
         }
-        cp_async8(X + r * A.xs + col, src, A.factors);
+        cp_async8(X + r * XS + col, src, A.factors);
       }
     }
   };
 
-  int buf = 0, cur_shape = -1, cur_c = -1;
+  int buf = 0, cur_shape = -1, cur_c = -1, cur_ey = NT * 8;
   issue(beg, 0);
   cp_async_commit();
   for (int it = beg; it < end; ++it) {
@@ -164,68 +182,70 @@ __global__ void __launch_bounds__(PW * 32, 2) k_plane(PlaneArgs A) {
     const int4 w = A.items[it];
     const SubD d = load_sub(A.subs + w.x);
     const int c = w.y, ex = d.ex, ey = d.ey, nk = w.w;
-    const int fsx = pad8(ex) + 4, fsy = pad8(ey) + 4;
     const int M1 = nk * ey, N2 = nk * ex;
     __syncthreads();  // (a) slab `buf` landed for everyone; previous item fully consumed
     if (d.shape != cur_shape || c != cur_c) {
       const fmp_shape& sh = A.shapes[d.shape];
-      load_factor(sFx, fsx, fwd_factor(A.factors, sh, c, 0), ex, tid, nth);
-      load_factor(sFy, fsy, fwd_factor(A.factors, sh, c, 1), ey, tid, nth);
+      const double* fx = fwd_factor(A.factors, sh, c, 0);
+      const double* fy = fwd_factor(A.factors, sh, c, 1);
+      for (int q = tid; q < ex * ex; q += nth) sFx[(q / ex) * FS + q % ex] = __ldg(fx + q);
+      for (int q = tid; q < ey * ey; q += nth) sFy[(q / ey) * FS + q % ey] = __ldg(fy + q);
+      if (ey < cur_ey)  // rows ey.. of T are the K padding of step 2: clear what a larger shape left
+        for (int q = tid; q < (cur_ey - ey) * TS; q += nth) sT[ey * TS + q] = 0.0;
       cur_shape = d.shape;
       cur_c = c;
+      cur_ey = ey;
     }
     for (int q = tid; q < MAXR; q += nth) {
       sMap1[q] = q < M1 ? ((q / ey) << 16) | (q % ey) : 0;
       sMap2[q] = q < N2 ? ((q / ex) << 16) | (q % ex) : 0;
     }
-    for (int q = tid; q < (pad4(ey) - ey) * TS; q += nth) sT[(ey + q / TS) * TS + q % TS] = 0.0;  // K pad of step 2
     __syncthreads();  // (b)
-    const double* X = sXb + buf * MAXR * A.xs;
+    const double* X = sXb + buf * L::X;
     // ---- step 1: T[j][k*ex + a] = sum_i X[(k,j)][i] Fx[a][i]   (INV: sum_a X[(k,b)][a] Fx[a][i])
     if (warp * 8 < M1) {
-      double acc[NTM][2];
+      double acc[NT][2];
 #pragma unroll
-      for (int n = 0; n < NTM; ++n) acc[n][0] = acc[n][1] = 0.0;
-      const int nt1 = pad8(ex) / 8, k4 = pad4(ex) / 4;
-      const double* xa = X + (warp * 8 + g) * A.xs + t;
+      for (int n = 0; n < NT; ++n) acc[n][0] = acc[n][1] = 0.0;
+      const int k4 = pad4(ex) / 4;
+      const double* xa = X + (warp * 8 + g) * XS + t;
+      const double* fb = INV ? sFx + t * FS + g : sFx + g * FS + t;
       for (int kk = 0; kk < k4; ++kk) {
         const double av = xa[kk * 4];
 #pragma unroll
-        for (int n = 0; n < NTM; ++n)
-          if (n < nt1) {
-            const double bv = INV ? sFx[(kk * 4 + t) * fsx + n * 8 + g] : sFx[(n * 8 + g) * fsx + kk * 4 + t];
-            dmma884(acc[n][0], acc[n][1], av, bv);
-          }
+        for (int n = 0; n < NT; ++n) {
+          const double bv = INV ? fb[kk * 4 * FS + n * 8] : fb[n * 8 * FS + kk * 4];
+          dmma884(acc[n][0], acc[n][1], av, bv);
+        }
       }
       const int r = warp * 8 + g;
       if (r < M1) {
         const int mp = sMap1[r], kk = mp >> 16, j = mp & 0xffff;
         double* trow = sT + j * TS + kk * ex;
 #pragma unroll
-        for (int n = 0; n < NTM; ++n)
-          if (n < nt1) {
-            const int a = n * 8 + 2 * t;
-            if (a < ex) trow[a] = acc[n][0];
-            if (a + 1 < ex) trow[a + 1] = acc[n][1];
-          }
+        for (int n = 0; n < NT; ++n) {
+          const int a = n * 8 + 2 * t;
+          if (a < ex) trow[a] = acc[n][0];
+          if (a + 1 < ex) trow[a + 1] = acc[n][1];
+        }
       }
     }
     __syncthreads();  // (c)
     // ---- step 2: O[b][(k,a)] = sum_j Fy[b][j] T[j][(k,a)]   (INV: sum_b Fy[b][j] T[b][(k,i)])
     if (warp * 8 < N2) {
-      double acc[NTM][2];
+      double acc[NT][2];
 #pragma unroll
-      for (int m = 0; m < NTM; ++m) acc[m][0] = acc[m][1] = 0.0;
-      const int mt2 = pad8(ey) / 8, k4 = pad4(ey) / 4;
+      for (int m = 0; m < NT; ++m) acc[m][0] = acc[m][1] = 0.0;
+      const int k4 = pad4(ey) / 4;
       const double* tb = sT + t * TS + warp * 8 + g;
+      const double* fa = INV ? sFy + t * FS + g : sFy + g * FS + t;
       for (int kk = 0; kk < k4; ++kk) {
         const double bv = tb[kk * 4 * TS];
 #pragma unroll
-        for (int m = 0; m < NTM; ++m)
-          if (m < mt2) {
-            const double av = INV ? sFy[(kk * 4 + t) * fsy + m * 8 + g] : sFy[(m * 8 + g) * fsy + kk * 4 + t];
-            dmma884(acc[m][0], acc[m][1], av, bv);
-          }
+        for (int m = 0; m < NT; ++m) {
+          const double av = INV ? fa[kk * 4 * FS + m * 8] : fa[m * 8 * FS + kk * 4];
+          dmma884(acc[m][0], acc[m][1], av, bv);
+        }
       }
       const int64_t P = (int64_t)ex * ey;
 #pragma unroll
@@ -234,9 +254,9 @@ __global__ void __launch_bounds__(PW * 32, 2) k_plane(PlaneArgs A) {
         if (n >= N2) continue;
         const int mp = sMap2[n], kk = mp >> 16, a = mp & 0xffff;
 #pragma unroll
-        for (int m = 0; m < NTM; ++m) {
+        for (int m = 0; m < NT; ++m) {
           const int row = m * 8 + g;
-          if (m >= mt2 || row >= ey) continue;
+          if (row >= ey) continue;
           if (!INV) {
             A.dst[d.ws_off + (c * d.ez + w.z + kk) * P + row * ex + a] = acc[m][h];
           } else {
@@ -273,20 +293,30 @@ struct ColArgs {
   double* dst;
   const double* corr;  // K3 only, may be null (no correction)
   int pmax;
-  int f_words, x_rows;   // smem carve-out: per-factor words, tile rows (pad8 of max ez)
+};
+
+template <int MT>
+struct ColSmem {
+  static constexpr int FS = MT * 8 + 4;      // factor row stride
+  static constexpr int XR = MT * 8;          // tile rows per component
+  static constexpr int F = MT * 8 * FS;
+  static constexpr int X = 3 * XR * SC;      // one tile buffer (3 components)
+  static constexpr size_t bytes = (size_t)(2 * F + 2 * X) * sizeof(double);
 };
 
 template <int MT, bool INV>
 __global__ void __launch_bounds__(CW * 32, 2) k_column(ColArgs A) {
+  using L = ColSmem<MT>;
+  constexpr int FS = L::FS, XR = L::XR;
   extern __shared__ __align__(16) double smem[];
-  double* sF = smem;                      // [2][pad8(ez)][pad8(ez)+4]: V^T_z (comps x,y), U^T_z (comp z)
-  double* sXb = sF + 2 * A.f_words;       // 2 x [3][x_rows][SC]
-  const int xbuf = 3 * A.x_rows * SC;
+  double* sF = smem;               // [2][MT*8][FS]: V^T_z (comps x,y), U^T_z (comp z)
+  double* sXb = sF + 2 * L::F;     // 2 x [3][XR][SC]
   const int tid = threadIdx.x, nth = blockDim.x;
   const int warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
   const int per = (A.n_items + gridDim.x - 1) / gridDim.x;
   const int beg = blockIdx.x * per, end = min(beg + per, A.n_items);
   if (beg >= end) return;
+  for (int q = tid; q < 2 * L::F; q += nth) sF[q] = 0.0;
 
   auto issue = [&](int it, int buf) {
     const int2 w = A.items[it];
@@ -294,12 +324,12 @@ __global__ void __launch_bounds__(CW * 32, 2) k_column(ColArgs A) {
     const int P = d.ex * d.ey, rows = pad4(d.ez);
     const int64_t V = (int64_t)P * d.ez;
     const double* src = A.src + d.ws_off;
-    double* X = sXb + buf * xbuf;
+    double* X = sXb + buf * L::X;
     const int col = tid % TP;
     const bool cval = w.y + col < P;
     for (int r = tid / TP; r < 3 * rows; r += nth / TP) {
       const int cc = r / rows, k = r - cc * rows;
-      cp_async8(X + (cc * A.x_rows + k) * SC + col,
+      cp_async8(X + (cc * XR + k) * SC + col,
                 (cval && k < d.ez) ? src + cc * V + (int64_t)k * P + w.y + col : nullptr, A.factors);
     }
   };
@@ -315,13 +345,17 @@ __global__ void __launch_bounds__(CW * 32, 2) k_column(ColArgs A) {
     const SubD d = load_sub(A.subs + w.x);
     const fmp_shape& sh = A.shapes[d.shape];
     const int ex = d.ex, ey = d.ey, ez = d.ez, P = ex * ey, p0 = w.y;
-    const int fs = pad8(ez) + 4;
     const int64_t V = (int64_t)P * ez;
-    double* X = sXb + buf * xbuf;
+    double* X = sXb + buf * L::X;
     __syncthreads();  // (a)
     if (d.shape != cur_shape) {
-      load_factor(sF, fs, A.factors + sh.vt_off[2], ez, tid, nth);
-      load_factor(sF + A.f_words, fs, A.factors + sh.ut_off[2], ez, tid, nth);
+      const double* fv = A.factors + sh.vt_off[2];
+      const double* fu = A.factors + sh.ut_off[2];
+      for (int q = tid; q < ez * ez; q += nth) {
+        const int r = q / ez, cc = q - r * ez;
+        sF[r * FS + cc] = __ldg(fv + q);
+        sF[L::F + r * FS + cc] = __ldg(fu + q);
+      }
       cur_shape = d.shape;
       __syncthreads();
     }
@@ -340,44 +374,39 @@ __global__ void __launch_bounds__(CW * 32, 2) k_column(ColArgs A) {
         const int b = p / ex, a = p - b * ex;
         const double vy0 = __ldg(Vy + b * ey), vx0 = __ldg(Vx + a * ex), sx = __ldg(Sx + a), sy = __ldg(Sy + b);
         for (int cz = tid / TP; cz < ez; cz += nth / TP) {
-          const double vz0 = sF[cz * fs];  // V^T_z[cz][0]
-          double dx = vz0 * cb[0 * pm2 + b * pm + a] + vy0 * cb[1 * pm2 + cz * pm + a];
-          double dy = vz0 * cb[2 * pm2 + b * pm + a] + vx0 * cb[3 * pm2 + cz * pm + b];
-          double dz = vy0 * cb[4 * pm2 + cz * pm + a] + vx0 * cb[5 * pm2 + cz * pm + b];
+          const double vz0 = sF[cz * FS];  // V^T_z[cz][0]
+          const double dx = vz0 * cb[0 * pm2 + b * pm + a] + vy0 * cb[1 * pm2 + cz * pm + a];
+          const double dy = vz0 * cb[2 * pm2 + b * pm + a] + vx0 * cb[3 * pm2 + cz * pm + b];
+          const double dz = vy0 * cb[4 * pm2 + cz * pm + a] + vx0 * cb[5 * pm2 + cz * pm + b];
           const double sz = __ldg(Sz + cz);
           const double q = __ldg(QW + 2 * ((int64_t)cz * P + p)), wq = __ldg(QW + 2 * ((int64_t)cz * P + p) + 1);
           const double pr = wq * (sx * dx + sy * dy + sz * dz);
-          X[(0 * A.x_rows + cz) * SC + col] -= q * dx + pr * sx;
-          X[(1 * A.x_rows + cz) * SC + col] -= q * dy + pr * sy;
-          X[(2 * A.x_rows + cz) * SC + col] -= q * dz + pr * sz;
+          X[(0 * XR + cz) * SC + col] -= q * dx + pr * sx;
+          X[(1 * XR + cz) * SC + col] -= q * dy + pr * sy;
+          X[(2 * XR + cz) * SC + col] -= q * dz + pr * sz;
         }
       }
       __syncthreads();
     }
-    const int m8 = pad8(ez) / 8, k4 = pad4(ez) / 4;
+    const int k4 = pad4(ez) / 4;
     double acc[3][MT][2];
 #pragma unroll
     for (int cc = 0; cc < 3; ++cc)
 #pragma unroll
       for (int m = 0; m < MT; ++m) acc[cc][m][0] = acc[cc][m][1] = 0.0;
-    const double* Fv = sF;
-    const double* Fu = sF + A.f_words;
     const double* xb = X + t * SC + warp * 8 + g;
+    const double* fa = INV ? sF + t * FS + g : sF + g * FS + t;
     for (int kk = 0; kk < k4; ++kk) {
-      const int k = kk * 4 + t;
-      const double b0 = xb[(0 * A.x_rows + kk * 4) * SC];
-      const double b1 = xb[(1 * A.x_rows + kk * 4) * SC];
-      const double b2 = xb[(2 * A.x_rows + kk * 4) * SC];
+      const double b0 = xb[(0 * XR + kk * 4) * SC];
+      const double b1 = xb[(1 * XR + kk * 4) * SC];
+      const double b2 = xb[(2 * XR + kk * 4) * SC];
 #pragma unroll
       for (int m = 0; m < MT; ++m) {
-        if (m < m8) {
-          const int r = m * 8 + g;
-          const double av = INV ? Fv[k * fs + r] : Fv[r * fs + k];
-          const double au = INV ? Fu[k * fs + r] : Fu[r * fs + k];
-          dmma884(acc[0][m][0], acc[0][m][1], av, b0);
-          dmma884(acc[1][m][0], acc[1][m][1], av, b1);
-          dmma884(acc[2][m][0], acc[2][m][1], au, b2);
-        }
+        const double av = INV ? fa[kk * 4 * FS + m * 8] : fa[m * 8 * FS + kk * 4];
+        const double au = INV ? fa[L::F + kk * 4 * FS + m * 8] : fa[L::F + m * 8 * FS + kk * 4];
+        dmma884(acc[0][m][0], acc[0][m][1], av, b0);
+        dmma884(acc[1][m][0], acc[1][m][1], av, b1);
+        dmma884(acc[2][m][0], acc[2][m][1], au, b2);
       }
     }
     double* dst = A.dst + d.ws_off;
@@ -394,7 +423,7 @@ __global__ void __launch_bounds__(CW * 32, 2) k_column(ColArgs A) {
 #pragma unroll
       for (int m = 0; m < MT; ++m) {
         const int r = m * 8 + g;
-        if (m >= m8 || r >= ez) continue;
+        if (r >= ez) continue;
         double y0 = acc[0][m][h], y1 = acc[1][m][h], y2 = acc[2][m][h];
         if (!INV) {  // B^-1 y = q y + w s (s . y)   (ref:subdomain.py:145-153, table form)
           const double sz = __ldg(Sz + r);
@@ -620,26 +649,17 @@ static void free_plan(fmp_precond* p) {
   delete p;
 }
 
-// smem footprints (doubles) for the largest shape in the plan
-static size_t plane_smem(const fmp_precond* p, int* fxw, int* fyw, int* xs) {
-  *fxw = pad8(p->max_ex) * (pad8(p->max_ex) + 4);
-  *fyw = pad8(p->max_ey) * (pad8(p->max_ey) + 4);
-  *xs = kstride(p->max_ex);
-  return (size_t)(*fxw + *fyw + 2 * MAXR * *xs + MAXR * TS) * sizeof(double) + 2 * MAXR * sizeof(int);
-}
-static size_t column_smem(const fmp_precond* p, int* fw, int* xrows) {
-  *fw = pad8(p->max_ez) * (pad8(p->max_ez) + 4);
-  *xrows = pad8(p->max_ez);
-  return (size_t)(2 * *fw + 2 * 3 * *xrows * SC) * sizeof(double);
-}
+static int plane_nt(const fmp_precond* p) { return std::max(p->max_ex, p->max_ey) <= 40 ? 5 : 9; }
+static int column_mt(const fmp_precond* p) { return pad8(p->max_ez) / 8; }
 
-template <bool INV, int NTM>
-static void plane_attr(size_t smem) {
-  cudaFuncSetAttribute(k_plane<INV, NTM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+template <bool INV, int NT>
+static void plane_attr() {
+  cudaFuncSetAttribute(k_plane<INV, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PlaneSmem<NT>::bytes);
 }
-template <int MT, bool INV>
-static void column_attr(size_t smem) {
-  cudaFuncSetAttribute(k_column<MT, INV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+template <int MT>
+static void column_attr() {
+  cudaFuncSetAttribute(k_column<MT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ColSmem<MT>::bytes);
+  cudaFuncSetAttribute(k_column<MT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ColSmem<MT>::bytes);
 }
 
 extern "C" int fmp_precond_create(const fmp_precond_desc* desc, fmp_precond** out) {
@@ -691,16 +711,9 @@ extern "C" int fmp_precond_create(const fmp_precond_desc* desc, fmp_precond** ou
     FMP_REQUIRE(false, "cublasCreate failed");
   }
   cublasSetMathMode(p->blas, CUBLAS_DEFAULT_MATH);
-  int a, b, c2;
-  const size_t ps = plane_smem(p, &a, &b, &c2);
-  plane_attr<false, 5>(ps); plane_attr<true, 5>(ps); plane_attr<false, 9>(ps); plane_attr<true, 9>(ps);
-  const size_t cs = column_smem(p, &a, &b);
-  column_attr<1, false>(cs); column_attr<2, false>(cs); column_attr<3, false>(cs); column_attr<4, false>(cs);
-  column_attr<5, false>(cs); column_attr<6, false>(cs); column_attr<7, false>(cs); column_attr<8, false>(cs);
-  column_attr<9, false>(cs);
-  column_attr<1, true>(cs); column_attr<2, true>(cs); column_attr<3, true>(cs); column_attr<4, true>(cs);
-  column_attr<5, true>(cs); column_attr<6, true>(cs); column_attr<7, true>(cs); column_attr<8, true>(cs);
-  column_attr<9, true>(cs);
+  plane_attr<false, 5>(); plane_attr<true, 5>(); plane_attr<false, 9>(); plane_attr<true, 9>();
+  column_attr<1>(); column_attr<2>(); column_attr<3>(); column_attr<4>(); column_attr<5>();
+  column_attr<6>(); column_attr<7>(); column_attr<8>(); column_attr<9>();
   cudaFuncSetAttribute(k_faces, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   cudaFuncSetAttribute(k_corr, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   FMP_CHECK_CUDA(cudaGetLastError());
@@ -725,16 +738,15 @@ static int column_pass(fmp_precond* p, bool inv, const double* src, double* dst,
   a.dst = dst;
   a.corr = corr;
   a.pmax = (int)p->d.pmax;
-  const size_t smem = column_smem(p, &a.f_words, &a.x_rows);
   const int grid = std::min(p->n_col, 2 * p->sms);
 #define FMP_COL(MT)                                                                   \
   case MT:                                                                            \
     if (inv)                                                                          \
-      k_column<MT, true><<<grid, CW * 32, smem, st>>>(a);                             \
+      k_column<MT, true><<<grid, CW * 32, ColSmem<MT>::bytes, st>>>(a);               \
     else                                                                              \
-      k_column<MT, false><<<grid, CW * 32, smem, st>>>(a);                            \
+      k_column<MT, false><<<grid, CW * 32, ColSmem<MT>::bytes, st>>>(a);              \
     break;
-  switch (pad8(p->max_ez) / 8) {
+  switch (column_mt(p)) {
     FMP_COL(1) FMP_COL(2) FMP_COL(3) FMP_COL(4) FMP_COL(5) FMP_COL(6) FMP_COL(7) FMP_COL(8) FMP_COL(9)
     default: FMP_REQUIRE(false, "unsupported z extent");
   }
@@ -755,15 +767,13 @@ static int plane_pass(fmp_precond* p, const fmp_block* blk, bool inv, int mode, 
   a.src = src;
   a.dst = dst;
   a.mode = mode;
-  const size_t smem = plane_smem(p, &a.fx_words, &a.fy_words, &a.xs);
   const int grid = std::min(a.n_items, 2 * p->sms);
-  const bool small = std::max(p->max_ex, p->max_ey) <= 40;
-  if (inv) {
-    if (small) k_plane<true, 5><<<grid, PW * 32, smem, st>>>(a);
-    else k_plane<true, 9><<<grid, PW * 32, smem, st>>>(a);
+  if (plane_nt(p) == 5) {
+    if (inv) k_plane<true, 5><<<grid, PW * 32, PlaneSmem<5>::bytes, st>>>(a);
+    else k_plane<false, 5><<<grid, PW * 32, PlaneSmem<5>::bytes, st>>>(a);
   } else {
-    if (small) k_plane<false, 5><<<grid, PW * 32, smem, st>>>(a);
-    else k_plane<false, 9><<<grid, PW * 32, smem, st>>>(a);
+    if (inv) k_plane<true, 9><<<grid, PW * 32, PlaneSmem<9>::bytes, st>>>(a);
+    else k_plane<false, 9><<<grid, PW * 32, PlaneSmem<9>::bytes, st>>>(a);
   }
   FMP_CHECK_LAUNCH();
   return 0;
