@@ -17,6 +17,8 @@
 // Axis contractions run on FP64 tensor cores (DMMA m8n8k4, mma.sync) from shared
 // memory.  Layout of every per-subdomain workspace slot: [c][k][j][i] for the three
 // components of the extended box (x fastest), i.e. the reference's own order.
+#include <algorithm>
+#include <cstdlib>
 #include <vector>
 #include <cublas_v2.h>
 #include "common.cuh"
@@ -29,9 +31,12 @@ __host__ __device__ constexpr int pad4(int n) { return (n + 3) & ~3; }
 // DMMA fragment loads (8 rows x 4 cols per warp) hit 16 distinct 8-byte banks.
 __host__ __device__ constexpr int sstride(int n) { return pad8(n) + 4; }
 
+// Workspace slots store each component as ez planes of stride ps = ex*ey rounded up to 4
+// doubles (32 B), so every plane and every 8-column tile starts 32-byte aligned.
 struct SubD {
-  int ex, ey, ez, lx, ly, lz, ox, oy, oz, wx, wy, wz, shape, column;
+  int ex, ey, ez, lx, ly, lz, ox, oy, oz, wx, wy, wz, shape, column, ps;
   int64_t ws_off, in_off;
+  __device__ __forceinline__ int64_t cstride() const { return (int64_t)ps * ez; }
 };
 
 __device__ __forceinline__ SubD load_sub(const fmp_subdomain* s) {
@@ -43,6 +48,7 @@ __device__ __forceinline__ SubD load_sub(const fmp_subdomain* s) {
   d.wx = (int)w[9]; d.wy = (int)w[10]; d.wz = (int)w[11];
   d.shape = (int)w[12]; d.column = (int)w[13];
   d.ws_off = w[14]; d.in_off = w[15];
+  d.ps = (d.ex * d.ey + 3) & ~3;
   return d;
 }
 
@@ -158,7 +164,7 @@ __global__ void __launch_bounds__(PW * 32, 2) k_plane(PlaneArgs A) {
         const double* src = nullptr;
         if (col < ex) {
           if (INV) {
-            src = A.src + d.ws_off + (c * d.ez + d.oz + w.z + kk) * P + j * ex + col;
+            src = A.src + d.ws_off + (int64_t)(c * d.ez + d.oz + w.z + kk) * d.ps + j * ex + col;
           } else if (A.mode == FMP_SOLVE_FACES) {
             src = A.src + d.in_off + c * V + (w.z + kk) * P + j * ex + col;
           } else if (inside) {
@@ -247,7 +253,6 @@ __global__ void __launch_bounds__(PW * 32, 2) k_plane(PlaneArgs A) {
           dmma884(acc[m][0], acc[m][1], av, bv);
         }
       }
-      const int64_t P = (int64_t)ex * ey;
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int n = warp * 8 + 2 * t + h;
@@ -258,7 +263,7 @@ __global__ void __launch_bounds__(PW * 32, 2) k_plane(PlaneArgs A) {
           const int row = m * 8 + g;
           if (row >= ey) continue;
           if (!INV) {
-            A.dst[d.ws_off + (c * d.ez + w.z + kk) * P + row * ex + a] = acc[m][h];
+            A.dst[d.ws_off + (int64_t)(c * d.ez + w.z + kk) * d.ps + row * ex + a] = acc[m][h];
           } else {
             const int jo = row - d.oy, io = a - d.ox;
             if ((unsigned)jo < (unsigned)d.wy && (unsigned)io < (unsigned)d.wx)
@@ -322,7 +327,7 @@ __global__ void __launch_bounds__(CW * 32, 2) k_column(ColArgs A) {
     const int2 w = A.items[it];
     const SubD d = load_sub(A.subs + w.x);
     const int P = d.ex * d.ey, rows = pad4(d.ez);
-    const int64_t V = (int64_t)P * d.ez;
+    const int64_t V = d.cstride();
     const double* src = A.src + d.ws_off;
     double* X = sXb + buf * L::X;
     const int col = tid % TP;
@@ -330,7 +335,7 @@ __global__ void __launch_bounds__(CW * 32, 2) k_column(ColArgs A) {
     for (int r = tid / TP; r < 3 * rows; r += nth / TP) {
       const int cc = r / rows, k = r - cc * rows;
       cp_async8(X + (cc * XR + k) * SC + col,
-                (cval && k < d.ez) ? src + cc * V + (int64_t)k * P + w.y + col : nullptr, A.factors);
+                (cval && k < d.ez) ? src + cc * V + (int64_t)k * d.ps + w.y + col : nullptr, A.factors);
     }
   };
 
@@ -345,7 +350,7 @@ __global__ void __launch_bounds__(CW * 32, 2) k_column(ColArgs A) {
     const SubD d = load_sub(A.subs + w.x);
     const fmp_shape& sh = A.shapes[d.shape];
     const int ex = d.ex, ey = d.ey, ez = d.ez, P = ex * ey, p0 = w.y;
-    const int64_t V = (int64_t)P * ez;
+    const int64_t V = d.cstride();
     double* X = sXb + buf * L::X;
     __syncthreads();  // (a)
     if (d.shape != cur_shape) {
@@ -433,12 +438,383 @@ __global__ void __launch_bounds__(CW * 32, 2) k_column(ColArgs A) {
           y1 = q * y1 + pr * sy;
           y2 = q * y2 + pr * sz;
         }
-        const int64_t o = (int64_t)r * P + p;
+        const int64_t o = (int64_t)r * d.ps + p;
         dst[o] = y0;
         dst[V + o] = y1;
         dst[2 * V + o] = y2;
       }
     }
+    buf ^= 1;
+  }
+  cp_async_wait<0>();
+}
+
+// ================================================================ fast path (extents <= 40)
+// Warp-independent variants of K1-K4.  Each warp owns whole work items (one z-plane of one
+// component, or 8 columns of one subdomain), double-buffers its own inputs with cp.async and
+// never waits on other warps: DMMA of one warp overlaps loads/epilogues of the others, which
+// is what keeps the per-SMSP DMMA pipe (1 issue / 16 cycles, 26-cycle latency, measured by
+// tools/dmma_latency.cu) busy.  The SVD factors of every distinct extent of the plan (at most
+// FX_MAXE) stay resident in shared memory for the whole launch.
+constexpr int FN = 40;               // padded extent (5 DMMA tiles)
+constexpr int FSM = 44;              // factor / T row stride (== 4 mod 8)
+constexpr int FMAT = FN * FSM;       // one padded factor matrix (doubles)
+constexpr int FX_MAXE = 2;           // distinct extents with resident factors
+constexpr int PXS = 36;              // plane slab row stride (== 4 mod 8)
+constexpr int PX_BUF = FN * PXS;     // one plane buffer
+constexpr int PW_WARPS = 4;          // warps per plane CTA (one per SMSP)
+constexpr int PW_PER_WARP = 2 * PX_BUF + FMAT;
+constexpr int CXS = 12;              // column tile row stride (8 columns + 4)
+constexpr int CXR = 36;              // column tile rows per component (pad4 of the max extent)
+constexpr int CX_BUF = 3 * CXR * CXS;  // one column tile (3 components)
+constexpr int CW_WARPS = 8;
+constexpr int FAST_MAX_EXT = CXR;    // the fast path serves plans whose extents are all <= 36
+
+struct ExtTable {
+  int n;
+  int ext[FX_MAXE];
+  int64_t ut[FX_MAXE], vt[FX_MAXE], sg[FX_MAXE];   // offsets in the factor buffer
+};
+
+// Resident factors: slot e holds [U^T_e, V^T_e] as zero-padded FN x FSM matrices + sigma_e.
+__device__ __forceinline__ void load_resident(double* sm, const ExtTable& et, const double* factors, int tid,
+                                              int nth) {
+  for (int e = 0; e < et.n; ++e) {
+    const int n = et.ext[e];
+    for (int h = 0; h < 2; ++h) {
+      const double* f = factors + (h == 0 ? et.ut[e] : et.vt[e]);
+      double* m = sm + (2 * e + h) * FMAT;
+      for (int q = tid; q < FMAT; q += nth) {
+        const int r = q / FSM, c = q - r * FSM;
+        m[q] = (r < n && c < n) ? __ldg(f + r * n + c) : 0.0;
+      }
+    }
+    double* sg = sm + 2 * FX_MAXE * FMAT + e * FN;
+    for (int q = tid; q < FN; q += nth) sg[q] = q < n ? __ldg(factors + et.sg[e] + q) : 0.0;
+  }
+}
+__device__ __forceinline__ int ext_slot(const ExtTable& et, int n) { return (et.n > 1 && et.ext[1] == n) ? 1 : 0; }
+// forward factor of component c on axis a for extent n: U^T on the own axis, V^T otherwise
+__device__ __forceinline__ const double* res_factor(const double* sm, const ExtTable& et, int c, int a, int n) {
+  return sm + (2 * ext_slot(et, n) + (a == c ? 0 : 1)) * FMAT;
+}
+__device__ __forceinline__ const double* res_sigma(const double* sm, const ExtTable& et, int n) {
+  return sm + 2 * FX_MAXE * FMAT + ext_slot(et, n) * FN;
+}
+constexpr int RES_WORDS = 2 * FX_MAXE * FMAT + FX_MAXE * FN;
+
+__device__ __forceinline__ void cp_async16(double* dst, const double* src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src));
+}
+
+struct FastPlaneArgs {
+  const fmp_subdomain* subs;
+  const int4* items;   // (sub, comp, plane, -)
+  int n_items;
+  Geo g;
+  const double* src;
+  double* dst;
+  const double* factors;
+  int mode;
+  ExtTable et;
+};
+
+// K1 (INV=false): plane k of S_i r -> Fy X Fx^T -> work;  K4 (INV=true): work plane -> Fy^T X Fx -> owned z
+template <bool INV>
+__global__ void __launch_bounds__(PW_WARPS * 32, 1) k_plane_fast(FastPlaneArgs A) {
+  extern __shared__ __align__(16) double smem[];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
+  load_resident(smem, A.et, A.factors, tid, blockDim.x);
+  double* wbase = smem + RES_WORDS + warp * PW_PER_WARP;
+  double* T = wbase + 2 * PX_BUF;
+  for (int q = lane; q < PW_PER_WARP; q += 32) wbase[q] = 0.0;   // K padding must read as finite zeros
+  __syncthreads();
+  const int gw = blockIdx.x * PW_WARPS + warp, nw = gridDim.x * PW_WARPS;
+  const int per = (A.n_items + nw - 1) / nw;
+  const int beg = gw * per, end = min(beg + per, A.n_items);
+  if (beg >= end) return;
+
+  // returns the column shift of the slab data inside the buffer (16-byte superset loads)
+  auto issue = [&](int it, int buf) -> int {
+    const int4 w = A.items[it];
+    const SubD d = load_sub(A.subs + w.x);
+    const int c = w.y, ex = d.ex, ey = d.ey;
+    double* X = wbase + buf * PX_BUF;
+    if (INV) {  // work plane (32-byte aligned, stride ex): rows of ex, start shift by row parity
+      const double* base = A.src + d.ws_off + (int64_t)(c * d.ez + d.oz + w.z) * d.ps;
+      // row j starts at base + j*ex; copy 8-byte elements (rows are not 16B aligned when ex is odd)
+      for (int q = lane; q < ey * ex; q += 32) {
+        const int j = q / ex, i = q - j * ex;
+        cp_async8(X + j * PXS + i, base + q, A.factors);
+      }
+      return 0;
+    }
+    if (A.mode == FMP_SOLVE_FACES) {
+      const int64_t P = (int64_t)ex * ey;
+      const double* base = A.src + d.in_off + c * P * d.ez + w.z * P;
+      for (int q = lane; q < ey * ex; q += 32) {
+        const int j = q / ex, i = q - j * ex;
+        cp_async8(X + j * PXS + i, base + q, A.factors);
+      }
+      return 0;
+    }
+    const bool inside = d.lx >= 0 && d.ly >= 0 && d.lz >= 0 && d.lx + ex <= A.g.bx && d.ly + ey <= A.g.by &&
+                        d.lz + d.ez <= A.g.bz;
+    if (inside && (A.g.bx & 1) == 0) {
+      const double* row0 = A.src + fidx(A.g, c, d.lz + w.z, d.ly, d.lx);
+      const int shift = (int)(((uintptr_t)row0 >> 3) & 1);
+      const int span = ex + shift, nch = (span + 1) >> 1;   // 16-byte chunks per row (last may be half)
+      const double* a0 = row0 - shift;
+      for (int q = lane; q < ey * nch; q += 32) {
+        const int j = q / nch, ch = q - j * nch;
+        const double* sp = a0 + (int64_t)j * A.g.bx + 2 * ch;
+        if (2 * ch + 1 < span)
+          cp_async16(X + j * PXS + 2 * ch, sp);
+        else
+          cp_async8(X + j * PXS + 2 * ch, sp, A.factors);   // never read past the row
+      }
+      return shift;
+    }
+    for (int q = lane; q < ey * ex; q += 32) {
+      const int j = q / ex, i = q - j * ex;
+      cp_async8(X + j * PXS + i, point_ptr(A.g, A.src, c, d.lz + w.z, d.ly + j, d.lx + i), A.factors);
+    }
+    return 0;
+  };
+
+  int buf = 0;
+  int shift_cur = issue(beg, 0);
+  cp_async_commit();
+  for (int it = beg; it < end; ++it) {
+    int shift_next = 0;
+    if (it + 1 < end) shift_next = issue(it + 1, buf ^ 1);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncwarp();
+    const int4 w = A.items[it];
+    const SubD d = load_sub(A.subs + w.x);
+    const int c = w.y, ex = d.ex, ey = d.ey;
+    const double* Fx = res_factor(smem, A.et, c, 0, ex);
+    const double* Fy = res_factor(smem, A.et, c, 1, ey);
+    const double* X = wbase + buf * PX_BUF + shift_cur;
+    // ---- step 1: T[j][a] = sum_i X[j][i] Fx[a][i]   (INV: T[b][i] = sum_a X[b][a] Fx[a][i])
+    {
+      const int k4 = pad4(ex) / 4;
+      const double* fb = INV ? Fx + t * FSM + g : Fx + g * FSM + t;
+#pragma unroll 1
+      for (int m = 0; m < 5; ++m) {
+        double acc[5][2];
+#pragma unroll
+        for (int n = 0; n < 5; ++n) acc[n][0] = acc[n][1] = 0.0;
+        const double* xa = X + (m * 8 + g) * PXS + t;
+        for (int kk = 0; kk < k4; ++kk) {
+          const double av = xa[kk * 4];
+#pragma unroll
+          for (int n = 0; n < 5; ++n) {
+            const double bv = INV ? fb[kk * 4 * FSM + n * 8] : fb[n * 8 * FSM + kk * 4];
+            dmma884(acc[n][0], acc[n][1], av, bv);
+          }
+        }
+        double* tr = T + (m * 8 + g) * FSM + 2 * t;
+#pragma unroll
+        for (int n = 0; n < 5; ++n) {
+          tr[n * 8] = acc[n][0];
+          tr[n * 8 + 1] = acc[n][1];
+        }
+      }
+    }
+    __syncwarp();
+    // ---- step 2: O[b][a] = sum_j Fy[b][j] T[j][a]   (INV: O[j][i] = sum_b Fy[b][j] T[b][i])
+    {
+      const int k4 = pad4(ey) / 4;
+      const double* fa = INV ? Fy + t * FSM + g : Fy + g * FSM + t;
+      const double* tb = T + t * FSM + g;
+      const int64_t obase = INV ? 0 : d.ws_off + (int64_t)(c * d.ez + w.z) * d.ps;
+#pragma unroll 1
+      for (int n = 0; n < 5; ++n) {
+        double acc[5][2];
+#pragma unroll
+        for (int m = 0; m < 5; ++m) acc[m][0] = acc[m][1] = 0.0;
+        for (int kk = 0; kk < k4; ++kk) {
+          const double bv = tb[kk * 4 * FSM + n * 8];
+#pragma unroll
+          for (int m = 0; m < 5; ++m) {
+            const double av = INV ? fa[kk * 4 * FSM + m * 8] : fa[m * 8 * FSM + kk * 4];
+            dmma884(acc[m][0], acc[m][1], av, bv);
+          }
+        }
+#pragma unroll
+        for (int m = 0; m < 5; ++m) {
+          const int row = m * 8 + g;
+          if (row >= ey) continue;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int col = n * 8 + 2 * t + h;
+            if (col >= ex) continue;
+            if (!INV) {
+              A.dst[obase + row * ex + col] = acc[m][h];
+            } else {
+              const int jo = row - d.oy, io = col - d.ox;
+              if ((unsigned)jo < (unsigned)d.wy && (unsigned)io < (unsigned)d.wx)
+                A.dst[fidx(A.g, c, d.lz + d.oz + w.z, d.ly + row, d.lx + col)] = acc[m][h];
+            }
+          }
+        }
+      }
+    }
+    __syncwarp();
+    shift_cur = shift_next;
+    buf ^= 1;
+  }
+  cp_async_wait<0>();
+}
+
+struct FastColArgs {
+  const fmp_subdomain* subs;
+  const int2* items;   // (sub, p0), 8 columns each
+  int n_items;
+  const double* src;
+  double* dst;
+  const double* factors;
+  const double* corr;  // K3 only (Woodbury), may be null
+  int pmax;
+  double alpha;
+  ExtTable et;
+};
+
+// K2 (INV=false): y^ = B^-1 (Fz X) over 8 columns x all z, 3 components;  K3 (INV=true): Fz^T (y^ - corr)
+template <bool INV>
+__global__ void __launch_bounds__(CW_WARPS * 32, 1) k_column_fast(FastColArgs A) {
+  extern __shared__ __align__(16) double smem[];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
+  load_resident(smem, A.et, A.factors, tid, blockDim.x);
+  double* wbase = smem + RES_WORDS + warp * 2 * CX_BUF;
+  for (int q = lane; q < 2 * CX_BUF; q += 32) wbase[q] = 0.0;
+  __syncthreads();
+  const int gw = blockIdx.x * CW_WARPS + warp, nw = gridDim.x * CW_WARPS;
+  const int per = (A.n_items + nw - 1) / nw;
+  const int beg = gw * per, end = min(beg + per, A.n_items);
+  if (beg >= end) return;
+
+  auto issue = [&](int it, int buf) {
+    const int2 w = A.items[it];
+    const SubD d = load_sub(A.subs + w.x);
+    const int P = d.ex * d.ey, ez = d.ez;
+    const int64_t V = d.cstride();
+    const double* src = A.src + d.ws_off + w.y;
+    double* X = wbase + buf * CX_BUF;
+    if (w.y + 8 <= d.ps) {   // 4 aligned 16-byte chunks per row (ps, ws_off, p0 all multiples of 4/8)
+      for (int q = lane; q < 3 * ez * 4; q += 32) {
+        const int r = q >> 2, ch = q & 3, cc = r / ez, k = r - cc * ez;
+        cp_async16(X + (cc * CXR + k) * CXS + 2 * ch, src + cc * V + (int64_t)k * d.ps + 2 * ch);
+      }
+    } else {
+      for (int q = lane; q < 3 * ez * 8; q += 32) {
+        const int r = q >> 3, col = q & 7, cc = r / ez, k = r - cc * ez;
+        cp_async8(X + (cc * CXR + k) * CXS + col, w.y + col < P ? src + cc * V + (int64_t)k * d.ps + col : nullptr,
+                  A.factors);
+      }
+    }
+  };
+
+  int buf = 0;
+  issue(beg, 0);
+  cp_async_commit();
+  for (int it = beg; it < end; ++it) {
+    if (it + 1 < end) issue(it + 1, buf ^ 1);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncwarp();
+    const int2 w = A.items[it];
+    const SubD d = load_sub(A.subs + w.x);
+    const int ex = d.ex, ey = d.ey, ez = d.ez, P = ex * ey, p0 = w.y;
+    const int64_t V = d.cstride();
+    double* X = wbase + buf * CX_BUF;
+    const double* Fv = res_factor(smem, A.et, 0, 2, ez);   // V^T_z (components x, y)
+    const double* Fu = res_factor(smem, A.et, 2, 2, ez);   // U^T_z (component z)
+    const double* Sx = res_sigma(smem, A.et, ex);
+    const double* Sy = res_sigma(smem, A.et, ey);
+    const double* Sz = res_sigma(smem, A.et, ez);
+    if (INV && A.corr) {
+      // y^ -= B^-1 (G Q Z): two rank-structured face terms per component (K6)
+      const double* cb = A.corr + (int64_t)w.x * 6 * A.pmax * A.pmax;
+      const int pm = A.pmax, pm2 = pm * pm;
+      const double* Vx = res_factor(smem, A.et, 1, 0, ex);   // V^T_x
+      const double* Vy = res_factor(smem, A.et, 0, 1, ey);   // V^T_y
+      const int col = lane & 7, p = p0 + col;
+      if (p < P) {
+        const int b = p / ex, a = p - b * ex;
+        const double vy0 = Vy[b * FSM], vx0 = Vx[a * FSM], sx = Sx[a], sy = Sy[b];
+        const double gx = cb[0 * pm2 + b * pm + a], gy = cb[2 * pm2 + b * pm + a];
+        for (int cz = lane >> 3; cz < ez; cz += 4) {
+          const double vz0 = Fv[cz * FSM];
+          const double dx = vz0 * gx + vy0 * cb[1 * pm2 + cz * pm + a];
+          const double dy = vz0 * gy + vx0 * cb[3 * pm2 + cz * pm + b];
+          const double dz = vy0 * cb[4 * pm2 + cz * pm + a] + vx0 * cb[5 * pm2 + cz * pm + b];
+          const double sz = Sz[cz];
+          const double q = __drcp_rn(1.0 + A.alpha * (sx * sx + sy * sy + sz * sz));
+          const double pr = A.alpha * (sx * dx + sy * dy + sz * dz);
+          X[(0 * CXR + cz) * CXS + col] -= q * (dx + pr * sx);
+          X[(1 * CXR + cz) * CXS + col] -= q * (dy + pr * sy);
+          X[(2 * CXR + cz) * CXS + col] -= q * (dz + pr * sz);
+        }
+      }
+      __syncwarp();
+    }
+    const int k4 = pad4(ez) / 4;
+    double acc[3][5][2];
+#pragma unroll
+    for (int cc = 0; cc < 3; ++cc)
+#pragma unroll
+      for (int m = 0; m < 5; ++m) acc[cc][m][0] = acc[cc][m][1] = 0.0;
+    const double* xb = X + t * CXS + g;
+    const double* fv = INV ? Fv + t * FSM + g : Fv + g * FSM + t;
+    const double* fu = INV ? Fu + t * FSM + g : Fu + g * FSM + t;
+    for (int kk = 0; kk < k4; ++kk) {
+      const double b0 = xb[(0 * CXR + kk * 4) * CXS];
+      const double b1 = xb[(1 * CXR + kk * 4) * CXS];
+      const double b2 = xb[(2 * CXR + kk * 4) * CXS];
+#pragma unroll
+      for (int m = 0; m < 5; ++m) {
+        const double av = INV ? fv[kk * 4 * FSM + m * 8] : fv[m * 8 * FSM + kk * 4];
+        const double au = INV ? fu[kk * 4 * FSM + m * 8] : fu[m * 8 * FSM + kk * 4];
+        dmma884(acc[0][m][0], acc[0][m][1], av, b0);
+        dmma884(acc[1][m][0], acc[1][m][1], av, b1);
+        dmma884(acc[2][m][0], acc[2][m][1], au, b2);
+      }
+    }
+    double* dst = A.dst + d.ws_off;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int p = p0 + 2 * t + h;
+      if (p >= P) continue;
+      double sx = 0.0, sy = 0.0;
+      if (!INV) {
+        const int b = p / ex, a = p - b * ex;
+        sx = Sx[a];
+        sy = Sy[b];
+      }
+#pragma unroll
+      for (int m = 0; m < 5; ++m) {
+        const int r = m * 8 + g;
+        if (r >= ez) continue;
+        double y0 = acc[0][m][h], y1 = acc[1][m][h], y2 = acc[2][m][h];
+        if (!INV) {  // B^-1 y = q (y + alpha s (s . y)), q = 1/(1 + alpha |s|^2)  (ref:subdomain.py:145-153)
+          const double sz = Sz[r];
+          const double q = __drcp_rn(1.0 + A.alpha * (sx * sx + sy * sy + sz * sz));
+          const double pr = A.alpha * (sx * y0 + sy * y1 + sz * y2);
+          y0 = q * (y0 + pr * sx);
+          y1 = q * (y1 + pr * sy);
+          y2 = q * (y2 + pr * sz);
+        }
+        const int64_t o = (int64_t)r * d.ps + p;
+        dst[o] = y0;
+        dst[V + o] = y1;
+        dst[2 * V + o] = y2;
+      }
+    }
+    __syncwarp();
     buf ^= 1;
   }
   cp_async_wait<0>();
@@ -501,11 +877,11 @@ __global__ void __launch_bounds__(256) k_faces(FaceArgs A) {
   const double* wn1 = fwd_factor(A.factors, sh, c, fg.n1);
   const double* wn2 = fwd_factor(A.factors, sh, c, fg.n2);
   const int nn1 = ext_of(d, fg.n1), nn2 = ext_of(d, fg.n2);
-  const double* src = A.yhat + d.ws_off + (int64_t)c * P * ez;
+  const double* src = A.yhat + d.ws_off + (int64_t)c * d.cstride();
   for (int q = threadIdx.x; q < pm2; q += blockDim.x) sA[q] = 0.0;
   for (int cz = 0; cz < ez; ++cz) {
     __syncthreads();
-    for (int q = threadIdx.x; q < P; q += blockDim.x) sPlane[q] = src[(int64_t)cz * P + q];
+    for (int q = threadIdx.x; q < P; q += blockDim.x) sPlane[q] = src[(int64_t)cz * d.ps + q];
     __syncthreads();
     // primary face
     if (fg.n1 == 2) {  // z-normal: sA[b][a] += w[cz] * plane[b][a]
@@ -624,6 +1000,13 @@ struct fmp_precond {
   int4* d_inv_items = nullptr;   // K4 work items
   int2* d_col_items = nullptr;   // K2/K3 work items
   int n_fwd = 0, n_inv = 0, n_col = 0;
+  // fast path (all extents <= FAST_MAX_EXT, at most FX_MAXE distinct): warp-independent kernels
+  bool fast = false;
+  ExtTable et{};
+  int4* d_ffwd = nullptr;
+  int4* d_finv = nullptr;
+  int2* d_fcol = nullptr;
+  int n_ffwd = 0, n_finv = 0, n_fcol = 0;
   cublasHandle_t blas = nullptr;
   int max_ex = 1, max_ey = 1, max_ez = 1, max_p = 1;
   int sms = kNumSM;
@@ -646,8 +1029,14 @@ static void free_plan(fmp_precond* p) {
   cudaFree(p->d_fwd_items);
   cudaFree(p->d_inv_items);
   cudaFree(p->d_col_items);
+  cudaFree(p->d_ffwd);
+  cudaFree(p->d_finv);
+  cudaFree(p->d_fcol);
   delete p;
 }
+
+constexpr int kPlaneFastSmem = (RES_WORDS + PW_WARPS * PW_PER_WARP) * (int)sizeof(double);
+constexpr int kColFastSmem = (RES_WORDS + CW_WARPS * 2 * CX_BUF) * (int)sizeof(double);
 
 static int plane_nt(const fmp_precond* p) { return std::max(p->max_ex, p->max_ey) <= 40 ? 5 : 9; }
 static int column_mt(const fmp_precond* p) { return pad8(p->max_ez) / 8; }
@@ -695,6 +1084,46 @@ extern "C" int fmp_precond_create(const fmp_precond_desc* desc, fmp_precond** ou
     FMP_REQUIRE(false, "extended extent %d exceeds the supported maximum %d (or pmax %lld)", mx, MAXR,
                 (long long)desc->pmax);
   }
+  // fast-path eligibility and its per-plane / per-8-column work items
+  {
+    std::vector<int> exts;
+    for (const auto& sh : p->shapes)
+      for (int a = 0; a < 3; ++a)
+        if (std::find(exts.begin(), exts.end(), (int)sh.ext[a]) == exts.end()) exts.push_back((int)sh.ext[a]);
+    const char* force = getenv("FMP_FORCE_GENERAL");
+    p->fast = (int)exts.size() <= FX_MAXE && mx <= FAST_MAX_EXT && !(force && force[0] == '1');
+    if (p->fast) {
+      p->et.n = (int)exts.size();
+      for (int e = 0; e < p->et.n; ++e) {
+        p->et.ext[e] = exts[e];
+        for (const auto& sh : p->shapes)
+          for (int a = 0; a < 3; ++a)
+            if ((int)sh.ext[a] == exts[e]) {
+              p->et.ut[e] = sh.ut_off[a];
+              p->et.vt[e] = sh.vt_off[a];
+              p->et.sg[e] = sh.s_off[a];
+            }
+      }
+      std::vector<int4> ff, fi;
+      std::vector<int2> fc;
+      for (int64_t q = 0; q < desc->n_sub; ++q) {
+        const auto& sd = p->subs[q];
+        const int ez = (int)sd.ext[2], wz = (int)sd.own[2], P = (int)(sd.ext[0] * sd.ext[1]);
+        for (int c = 0; c < 3; ++c) {
+          for (int k = 0; k < ez; ++k) ff.push_back(make_int4((int)q, c, k, 1));
+          for (int k = 0; k < wz; ++k) fi.push_back(make_int4((int)q, c, k, 1));
+        }
+        for (int p0 = 0; p0 < P; p0 += 8) fc.push_back(make_int2((int)q, p0));
+      }
+      p->n_ffwd = (int)ff.size();
+      p->n_finv = (int)fi.size();
+      p->n_fcol = (int)fc.size();
+      if (upload(ff, &p->d_ffwd) || upload(fi, &p->d_finv) || upload(fc, &p->d_fcol)) {
+        free_plan(p);
+        return -1;
+      }
+    }
+  }
   p->n_fwd = (int)fwd.size();
   p->n_inv = (int)inv.size();
   p->n_col = (int)col.size();
@@ -714,6 +1143,10 @@ extern "C" int fmp_precond_create(const fmp_precond_desc* desc, fmp_precond** ou
   plane_attr<false, 5>(); plane_attr<true, 5>(); plane_attr<false, 9>(); plane_attr<true, 9>();
   column_attr<1>(); column_attr<2>(); column_attr<3>(); column_attr<4>(); column_attr<5>();
   column_attr<6>(); column_attr<7>(); column_attr<8>(); column_attr<9>();
+  cudaFuncSetAttribute(k_plane_fast<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kPlaneFastSmem);
+  cudaFuncSetAttribute(k_plane_fast<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kPlaneFastSmem);
+  cudaFuncSetAttribute(k_column_fast<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kColFastSmem);
+  cudaFuncSetAttribute(k_column_fast<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kColFastSmem);
   cudaFuncSetAttribute(k_faces, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   cudaFuncSetAttribute(k_corr, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   FMP_CHECK_CUDA(cudaGetLastError());
@@ -728,6 +1161,26 @@ extern "C" int fmp_precond_destroy(fmp_precond* p) {
 
 static int column_pass(fmp_precond* p, bool inv, const double* src, double* dst, const double* corr,
                        cudaStream_t st) {
+  if (p->fast) {
+    FastColArgs a{};
+    a.subs = p->d.subs;
+    a.items = p->d_fcol;
+    a.n_items = p->n_fcol;
+    a.src = src;
+    a.dst = dst;
+    a.factors = p->d.factors;
+    a.corr = corr;
+    a.pmax = (int)p->d.pmax;
+    a.alpha = p->d.alpha;
+    a.et = p->et;
+    const int grid = std::min(p->sms, (p->n_fcol + CW_WARPS - 1) / CW_WARPS);
+    if (inv)
+      k_column_fast<true><<<grid, CW_WARPS * 32, kColFastSmem, st>>>(a);
+    else
+      k_column_fast<false><<<grid, CW_WARPS * 32, kColFastSmem, st>>>(a);
+    FMP_CHECK_LAUNCH();
+    return 0;
+  }
   ColArgs a{};
   a.subs = p->d.subs;
   a.shapes = p->d.shapes;
@@ -757,6 +1210,25 @@ static int column_pass(fmp_precond* p, bool inv, const double* src, double* dst,
 
 static int plane_pass(fmp_precond* p, const fmp_block* blk, bool inv, int mode, const double* src, double* dst,
                       cudaStream_t st) {
+  if (p->fast) {
+    FastPlaneArgs a{};
+    a.subs = p->d.subs;
+    a.items = inv ? p->d_finv : p->d_ffwd;
+    a.n_items = inv ? p->n_finv : p->n_ffwd;
+    a.g = make_geo(blk);
+    a.src = src;
+    a.dst = dst;
+    a.factors = p->d.factors;
+    a.mode = mode;
+    a.et = p->et;
+    const int grid = std::min(p->sms, (a.n_items + PW_WARPS - 1) / PW_WARPS);
+    if (inv)
+      k_plane_fast<true><<<grid, PW_WARPS * 32, kPlaneFastSmem, st>>>(a);
+    else
+      k_plane_fast<false><<<grid, PW_WARPS * 32, kPlaneFastSmem, st>>>(a);
+    FMP_CHECK_LAUNCH();
+    return 0;
+  }
   PlaneArgs a{};
   a.subs = p->d.subs;
   a.shapes = p->d.shapes;

@@ -106,7 +106,8 @@ class SolvePlan:
             sid = shapes.index(s.ext)
             sub_rec[q] = [*s.ext, *s.ext_lo, *s.own_off, *s.own, sid, col_of_shape[sid], ws, s.in_off]
             col_of_shape[sid] += 1
-            ws += (3 * int(np.prod(s.ext)) + 7) // 8 * 8
+            ps = (s.ext[0] * s.ext[1] + 3) // 4 * 4      # plane stride of a workspace slot (csrc SubD::ps)
+            ws += (3 * s.ext[2] * ps + 7) // 8 * 8
         for q in range(len(shapes)):
             first[q + 1] = first[q] + col_of_shape[q]
         self.ncols = col_of_shape
@@ -115,8 +116,10 @@ class SolvePlan:
         self.sub_dev = torch.from_numpy(sub_rec).to(self.device)
         self.sh_dev = torch.from_numpy(sh_rec).to(self.device)
         f64 = dict(dtype=torch.float64, device=self.device)
-        self.work_a = torch.empty(ws, **f64)
-        self.work_b = torch.empty(ws, **f64)
+        # zero-filled: the plane-stride padding of every slot must stay finite (it is read as
+        # DMMA operand padding and multiplied by zero factor entries)
+        self.work_a = torch.zeros(ws, **f64)
+        self.work_b = torch.zeros(ws, **f64)
         self.corr = torch.zeros(len(self.subs) * 6 * self.pmax * self.pmax, **f64)
         # per-shape Y/Z matrices (column-major m x ncols == row-major (ncols, m))
         self.ymat = [torch.zeros((max(1, n), m), **f64) for n, m in zip(self.ncols, self.m)]

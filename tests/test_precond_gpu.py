@@ -108,3 +108,22 @@ def test_ras_device_tensor_path_and_no_aliasing():
     want = O.ras_apply((16, 16, 16), O.partition((16, 16, 16), (2, 2, 2), 1), 0.25, r.cpu().numpy().ravel())
     assert rel(z1.cpu().numpy(), want) <= 1e-11
     assert not prec.apply(torch.zeros_like(r)).any()
+
+
+@pytest.mark.parametrize("gext,grid", [((32, 32, 32), (2, 2, 2)), ((48, 32, 32), (3, 2, 2)), ((16, 16, 16), (1, 1, 1))])
+def test_fast_and_general_paths_agree(gext, grid, monkeypatch):
+    """The warp-independent fast kernels (<= 2 distinct extents <= 36) and the general
+    CTA-synchronous kernels compute the same preconditioner."""
+    from paper_2508_07193_b200 import Box, RasPreconditioner, make_partition, make_transport
+    part = make_partition(Box(*gext), grid, 1)
+    tr = make_transport("cuda")
+    r = torch.from_numpy(np.random.default_rng(7).uniform(-1, 1, part.global_box.dof)).cuda().view(
+        part.global_box.shape4)
+    monkeypatch.setenv("FMP_FORCE_GENERAL", "0")
+    z_fast = RasPreconditioner(part, 0.25, tr).apply(r)
+    monkeypatch.setenv("FMP_FORCE_GENERAL", "1")
+    z_gen = RasPreconditioner(part, 0.25, tr).apply(r)
+    assert rel(z_fast.cpu().numpy(), z_gen.cpu().numpy()) <= 1e-13
+    if int(np.prod(gext)) <= 32 ** 3:
+        want = O.ras_apply(gext, O.partition(gext, grid, 1), 0.25, r.cpu().numpy().ravel())
+        assert rel(z_fast.cpu().numpy(), want) <= 1e-11
