@@ -462,8 +462,9 @@ constexpr int FMAT = FN * FSM;       // one padded factor matrix (doubles)
 constexpr int FX_MAXE = 2;           // distinct extents with resident factors
 constexpr int PXS = 36;              // plane slab row stride (== 4 mod 8)
 constexpr int PX_BUF = FN * PXS;     // one plane buffer
-constexpr int PW_WARPS = 4;          // warps per plane CTA (one per SMSP)
-constexpr int PW_PER_WARP = 2 * PX_BUF + FMAT;
+constexpr int PW_WARPS = 8;          // warps per plane CTA: 4 pairs, one plane item per pair
+constexpr int PW_PAIRS = PW_WARPS / 2;
+constexpr int PW_PER_WARP = 2 * PX_BUF + FMAT;   // per pair: double-buffered plane + step-1 result
 constexpr int CXS = 12;              // column tile row stride (8 columns + 4)
 constexpr int CXR = 36;              // column tile rows per component (pad4 of the max extent)
 constexpr int CX_BUF = 3 * CXR * CXS;  // one column tile (3 components)
@@ -521,39 +522,44 @@ struct FastPlaneArgs {
 };
 
 // K1 (INV=false): plane k of S_i r -> Fy X Fx^T -> work;  K4 (INV=true): work plane -> Fy^T X Fx -> owned z
+// A pair of warps owns a plane item: warp 0 of the pair takes DMMA tiles 0-2, warp 1 tiles 3-4
+// of each 5-tile GEMM, synchronising only with each other (named barrier).  The two warps of a
+// pair sit on different SM sub-partitions and every sub-partition hosts one "3-tile" and one
+// "2-tile" warp, so the DMMA pipes stay balanced.
+__device__ __forceinline__ void pair_sync(int pair) {
+  asm volatile("bar.sync %0, 64;\n" ::"r"(pair + 1) : "memory");
+}
+
 template <bool INV>
 __global__ void __launch_bounds__(PW_WARPS * 32, 1) k_plane_fast(FastPlaneArgs A) {
   extern __shared__ __align__(16) double smem[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
+  // pairs (0,5) (1,4) (2,7) (3,6): the members are on different SMSPs (warp % 4)
+  const int pair = warp < 4 ? warp : (warp == 4 ? 1 : warp == 5 ? 0 : warp == 6 ? 3 : 2);
+  const int half = warp < 4 ? 0 : 1;                      // 0: tiles 0..2, 1: tiles 3..4
+  const int tlo = half ? 3 : 0, thi = half ? 5 : 3;
+  const int ptid = half * 32 + lane;                       // thread index within the pair
   load_resident(smem, A.et, A.factors, tid, blockDim.x);
-  double* wbase = smem + RES_WORDS + warp * PW_PER_WARP;
+  double* wbase = smem + RES_WORDS + pair * PW_PER_WARP;
   double* T = wbase + 2 * PX_BUF;
-  for (int q = lane; q < PW_PER_WARP; q += 32) wbase[q] = 0.0;   // K padding must read as finite zeros
+  for (int q = tid; q < PW_PAIRS * PW_PER_WARP; q += blockDim.x) smem[RES_WORDS + q] = 0.0;
   __syncthreads();
-  const int gw = blockIdx.x * PW_WARPS + warp, nw = gridDim.x * PW_WARPS;
-  const int per = (A.n_items + nw - 1) / nw;
-  const int beg = gw * per, end = min(beg + per, A.n_items);
+  const int gp = blockIdx.x * PW_PAIRS + pair, np = gridDim.x * PW_PAIRS;
+  const int per = (A.n_items + np - 1) / np;
+  const int beg = gp * per, end = min(beg + per, A.n_items);
   if (beg >= end) return;
 
-  // returns the column shift of the slab data inside the buffer (16-byte superset loads)
+  // returns the column shift of the plane data inside the buffer (16-byte superset loads)
   auto issue = [&](int it, int buf) -> int {
     const int4 w = A.items[it];
     const SubD d = load_sub(A.subs + w.x);
     const int c = w.y, ex = d.ex, ey = d.ey;
     double* X = wbase + buf * PX_BUF;
-    if (INV) {  // work plane (32-byte aligned, stride ex): rows of ex, start shift by row parity
-      const double* base = A.src + d.ws_off + (int64_t)(c * d.ez + d.oz + w.z) * d.ps;
-      // row j starts at base + j*ex; copy 8-byte elements (rows are not 16B aligned when ex is odd)
-      for (int q = lane; q < ey * ex; q += 32) {
-        const int j = q / ex, i = q - j * ex;
-        cp_async8(X + j * PXS + i, base + q, A.factors);
-      }
-      return 0;
-    }
-    if (A.mode == FMP_SOLVE_FACES) {
+    if (INV || A.mode == FMP_SOLVE_FACES) {
       const int64_t P = (int64_t)ex * ey;
-      const double* base = A.src + d.in_off + c * P * d.ez + w.z * P;
-      for (int q = lane; q < ey * ex; q += 32) {
+      const double* base = INV ? A.src + d.ws_off + (int64_t)(c * d.ez + d.oz + w.z) * d.ps
+                               : A.src + d.in_off + c * P * d.ez + w.z * P;
+      for (int q = ptid; q < ey * ex; q += 64) {
         const int j = q / ex, i = q - j * ex;
         cp_async8(X + j * PXS + i, base + q, A.factors);
       }
@@ -566,7 +572,7 @@ __global__ void __launch_bounds__(PW_WARPS * 32, 1) k_plane_fast(FastPlaneArgs A
       const int shift = (int)(((uintptr_t)row0 >> 3) & 1);
       const int span = ex + shift, nch = (span + 1) >> 1;   // 16-byte chunks per row (last may be half)
       const double* a0 = row0 - shift;
-      for (int q = lane; q < ey * nch; q += 32) {
+      for (int q = ptid; q < ey * nch; q += 64) {
         const int j = q / nch, ch = q - j * nch;
         const double* sp = a0 + (int64_t)j * A.g.bx + 2 * ch;
         if (2 * ch + 1 < span)
@@ -576,7 +582,7 @@ __global__ void __launch_bounds__(PW_WARPS * 32, 1) k_plane_fast(FastPlaneArgs A
       }
       return shift;
     }
-    for (int q = lane; q < ey * ex; q += 32) {
+    for (int q = ptid; q < ey * ex; q += 64) {
       const int j = q / ex, i = q - j * ex;
       cp_async8(X + j * PXS + i, point_ptr(A.g, A.src, c, d.lz + w.z, d.ly + j, d.lx + i), A.factors);
     }
@@ -591,7 +597,7 @@ __global__ void __launch_bounds__(PW_WARPS * 32, 1) k_plane_fast(FastPlaneArgs A
     if (it + 1 < end) shift_next = issue(it + 1, buf ^ 1);
     cp_async_commit();
     cp_async_wait<1>();
-    __syncwarp();
+    pair_sync(pair);   // plane `buf` landed for both warps; T free (previous step 2 done)
     const int4 w = A.items[it];
     const SubD d = load_sub(A.subs + w.x);
     const int c = w.y, ex = d.ex, ey = d.ey;
@@ -603,7 +609,7 @@ __global__ void __launch_bounds__(PW_WARPS * 32, 1) k_plane_fast(FastPlaneArgs A
       const int k4 = pad4(ex) / 4;
       const double* fb = INV ? Fx + t * FSM + g : Fx + g * FSM + t;
 #pragma unroll 1
-      for (int m = 0; m < 5; ++m) {
+      for (int m = tlo; m < thi; ++m) {
         double acc[5][2];
 #pragma unroll
         for (int n = 0; n < 5; ++n) acc[n][0] = acc[n][1] = 0.0;
@@ -624,7 +630,7 @@ __global__ void __launch_bounds__(PW_WARPS * 32, 1) k_plane_fast(FastPlaneArgs A
         }
       }
     }
-    __syncwarp();
+    pair_sync(pair);
     // ---- step 2: O[b][a] = sum_j Fy[b][j] T[j][a]   (INV: O[j][i] = sum_b Fy[b][j] T[b][i])
     {
       const int k4 = pad4(ey) / 4;
@@ -632,7 +638,7 @@ __global__ void __launch_bounds__(PW_WARPS * 32, 1) k_plane_fast(FastPlaneArgs A
       const double* tb = T + t * FSM + g;
       const int64_t obase = INV ? 0 : d.ws_off + (int64_t)(c * d.ez + w.z) * d.ps;
 #pragma unroll 1
-      for (int n = 0; n < 5; ++n) {
+      for (int n = tlo; n < thi; ++n) {
         double acc[5][2];
 #pragma unroll
         for (int m = 0; m < 5; ++m) acc[m][0] = acc[m][1] = 0.0;
@@ -663,7 +669,6 @@ __global__ void __launch_bounds__(PW_WARPS * 32, 1) k_plane_fast(FastPlaneArgs A
         }
       }
     }
-    __syncwarp();
     shift_cur = shift_next;
     buf ^= 1;
   }
@@ -1035,7 +1040,7 @@ static void free_plan(fmp_precond* p) {
   delete p;
 }
 
-constexpr int kPlaneFastSmem = (RES_WORDS + PW_WARPS * PW_PER_WARP) * (int)sizeof(double);
+constexpr int kPlaneFastSmem = (RES_WORDS + PW_PAIRS * PW_PER_WARP) * (int)sizeof(double);
 constexpr int kColFastSmem = (RES_WORDS + CW_WARPS * 2 * CX_BUF) * (int)sizeof(double);
 
 static int plane_nt(const fmp_precond* p) { return std::max(p->max_ex, p->max_ey) <= 40 ? 5 : 9; }
@@ -1221,7 +1226,7 @@ static int plane_pass(fmp_precond* p, const fmp_block* blk, bool inv, int mode, 
     a.factors = p->d.factors;
     a.mode = mode;
     a.et = p->et;
-    const int grid = std::min(p->sms, (a.n_items + PW_WARPS - 1) / PW_WARPS);
+    const int grid = std::min(p->sms, (a.n_items + PW_PAIRS - 1) / PW_PAIRS);
     if (inv)
       k_plane_fast<true><<<grid, PW_WARPS * 32, kPlaneFastSmem, st>>>(a);
     else
