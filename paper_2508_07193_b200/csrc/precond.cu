@@ -555,14 +555,13 @@ __global__ void __launch_bounds__(PW_WARPS * 32, 1) k_plane_fast(FastPlaneArgs A
     const SubD d = load_sub(A.subs + w.x);
     const int c = w.y, ex = d.ex, ey = d.ey;
     double* X = wbase + buf * PX_BUF;
+    // no integer division in the copy loops: the XU pipe is the bottleneck otherwise
     if (INV || A.mode == FMP_SOLVE_FACES) {
       const int64_t P = (int64_t)ex * ey;
       const double* base = INV ? A.src + d.ws_off + (int64_t)(c * d.ez + d.oz + w.z) * d.ps
                                : A.src + d.in_off + c * P * d.ez + w.z * P;
-      for (int q = ptid; q < ey * ex; q += 64) {
-        const int j = q / ex, i = q - j * ex;
-        cp_async8(X + j * PXS + i, base + q, A.factors);
-      }
+      for (int j = half; j < ey; j += 2)
+        for (int i = lane; i < ex; i += 32) cp_async8(X + j * PXS + i, base + j * ex + i, A.factors);
       return 0;
     }
     const bool inside = d.lx >= 0 && d.ly >= 0 && d.lz >= 0 && d.lx + ex <= A.g.bx && d.ly + ey <= A.g.by &&
@@ -572,20 +571,21 @@ __global__ void __launch_bounds__(PW_WARPS * 32, 1) k_plane_fast(FastPlaneArgs A
       const int shift = (int)(((uintptr_t)row0 >> 3) & 1);
       const int span = ex + shift, nch = (span + 1) >> 1;   // 16-byte chunks per row (last may be half)
       const double* a0 = row0 - shift;
-      for (int q = ptid; q < ey * nch; q += 64) {
-        const int j = q / nch, ch = q - j * nch;
-        const double* sp = a0 + (int64_t)j * A.g.bx + 2 * ch;
-        if (2 * ch + 1 < span)
-          cp_async16(X + j * PXS + 2 * ch, sp);
-        else
-          cp_async8(X + j * PXS + 2 * ch, sp, A.factors);   // never read past the row
+      if (lane < nch) {
+        const int ch = lane;
+        for (int j = half; j < ey; j += 2) {
+          const double* sp = a0 + (int64_t)j * A.g.bx + 2 * ch;
+          if (2 * ch + 1 < span)
+            cp_async16(X + j * PXS + 2 * ch, sp);
+          else
+            cp_async8(X + j * PXS + 2 * ch, sp, A.factors);   // never read past the row
+        }
       }
       return shift;
     }
-    for (int q = ptid; q < ey * ex; q += 64) {
-      const int j = q / ex, i = q - j * ex;
-      cp_async8(X + j * PXS + i, point_ptr(A.g, A.src, c, d.lz + w.z, d.ly + j, d.lx + i), A.factors);
-    }
+    for (int j = half; j < ey; j += 2)
+      for (int i = lane; i < ex; i += 32)
+        cp_async8(X + j * PXS + i, point_ptr(A.g, A.src, c, d.lz + w.z, d.ly + j, d.lx + i), A.factors);
     return 0;
   };
 
@@ -710,16 +710,16 @@ __global__ void __launch_bounds__(CW_WARPS * 32, 1) k_column_fast(FastColArgs A)
     const double* src = A.src + d.ws_off + w.y;
     double* X = wbase + buf * CX_BUF;
     if (w.y + 8 <= d.ps) {   // 4 aligned 16-byte chunks per row (ps, ws_off, p0 all multiples of 4/8)
-      for (int q = lane; q < 3 * ez * 4; q += 32) {
-        const int r = q >> 2, ch = q & 3, cc = r / ez, k = r - cc * ez;
-        cp_async16(X + (cc * CXR + k) * CXS + 2 * ch, src + cc * V + (int64_t)k * d.ps + 2 * ch);
-      }
+      const int ch = lane & 3;
+      for (int cc = 0; cc < 3; ++cc)
+        for (int k = lane >> 2; k < ez; k += 8)
+          cp_async16(X + (cc * CXR + k) * CXS + 2 * ch, src + cc * V + (int64_t)k * d.ps + 2 * ch);
     } else {
-      for (int q = lane; q < 3 * ez * 8; q += 32) {
-        const int r = q >> 3, col = q & 7, cc = r / ez, k = r - cc * ez;
-        cp_async8(X + (cc * CXR + k) * CXS + col, w.y + col < P ? src + cc * V + (int64_t)k * d.ps + col : nullptr,
-                  A.factors);
-      }
+      const int col = lane & 7;
+      for (int cc = 0; cc < 3; ++cc)
+        for (int k = lane >> 3; k < ez; k += 4)
+          cp_async8(X + (cc * CXR + k) * CXS + col, w.y + col < P ? src + cc * V + (int64_t)k * d.ps + col : nullptr,
+                    A.factors);
     }
   };
 
@@ -749,7 +749,9 @@ __global__ void __launch_bounds__(CW_WARPS * 32, 1) k_column_fast(FastColArgs A)
       const double* Vy = res_factor(smem, A.et, 0, 1, ey);   // V^T_y
       const int col = lane & 7, p = p0 + col;
       if (p < P) {
-        const int b = p / ex, a = p - b * ex;
+        const int b0 = p0 / ex;
+        int b = b0, a = p - b0 * ex;
+        if (a >= ex) { a -= ex; ++b; }
         const double vy0 = Vy[b * FSM], vx0 = Vx[a * FSM], sx = Sx[a], sy = Sy[b];
         const double gx = cb[0 * pm2 + b * pm + a], gy = cb[2 * pm2 + b * pm + a];
         for (int cz = lane >> 3; cz < ez; cz += 4) {
@@ -790,13 +792,15 @@ __global__ void __launch_bounds__(CW_WARPS * 32, 1) k_column_fast(FastColArgs A)
       }
     }
     double* dst = A.dst + d.ws_off;
+    const int b0 = p0 / ex;   // one division per item; columns of the item span <= 2 rows
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int p = p0 + 2 * t + h;
       if (p >= P) continue;
       double sx = 0.0, sy = 0.0;
       if (!INV) {
-        const int b = p / ex, a = p - b * ex;
+        int b = b0, a = p - b0 * ex;
+        if (a >= ex) { a -= ex; ++b; }
         sx = Sx[a];
         sy = Sy[b];
       }
