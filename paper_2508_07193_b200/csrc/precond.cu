@@ -751,7 +751,7 @@ __global__ void __launch_bounds__(CW_WARPS * 32, 1) k_column_fast(FastColArgs A)
       if (p < P) {
         const int b0 = p0 / ex;
         int b = b0, a = p - b0 * ex;
-        if (a >= ex) { a -= ex; ++b; }
+        while (a >= ex) { a -= ex; ++b; }
         const double vy0 = Vy[b * FSM], vx0 = Vx[a * FSM], sx = Sx[a], sy = Sy[b];
         const double gx = cb[0 * pm2 + b * pm + a], gy = cb[2 * pm2 + b * pm + a];
         for (int cz = lane >> 3; cz < ez; cz += 4) {
@@ -792,7 +792,7 @@ __global__ void __launch_bounds__(CW_WARPS * 32, 1) k_column_fast(FastColArgs A)
       }
     }
     double* dst = A.dst + d.ws_off;
-    const int b0 = p0 / ex;   // one division per item; columns of the item span <= 2 rows
+    const int b0 = p0 / ex;   // one division per item; the 8 columns advance b a few times at most
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int p = p0 + 2 * t + h;
@@ -800,7 +800,7 @@ __global__ void __launch_bounds__(CW_WARPS * 32, 1) k_column_fast(FastColArgs A)
       double sx = 0.0, sy = 0.0;
       if (!INV) {
         int b = b0, a = p - b0 * ex;
-        if (a >= ex) { a -= ex; ++b; }
+        while (a >= ex) { a -= ex; ++b; }
         sx = Sx[a];
         sy = Sy[b];
       }
