@@ -560,8 +560,14 @@ __global__ void __launch_bounds__(PW_WARPS * 32, 1) k_plane_fast(FastPlaneArgs A
       const int64_t P = (int64_t)ex * ey;
       const double* base = INV ? A.src + d.ws_off + (int64_t)(c * d.ez + d.oz + w.z) * d.ps
                                : A.src + d.in_off + c * P * d.ez + w.z * P;
-      for (int j = half; j < ey; j += 2)
-        for (int i = lane; i < ex; i += 32) cp_async8(X + j * PXS + i, base + j * ex + i, A.factors);
+      // the plane is contiguous: walk it flat, tracking (j, i) incrementally
+      int j = 0, i = ptid;
+      while (i >= ex) { i -= ex; ++j; }
+      for (int q = ptid; q < ey * ex; q += 64) {
+        cp_async8(X + j * PXS + i, base + q, A.factors);
+        i += 64;
+        while (i >= ex) { i -= ex; ++j; }
+      }
       return 0;
     }
     const bool inside = d.lx >= 0 && d.ly >= 0 && d.lz >= 0 && d.lx + ex <= A.g.bx && d.ly + ey <= A.g.by &&
