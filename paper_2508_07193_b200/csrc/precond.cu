@@ -460,11 +460,12 @@ constexpr int FN = 40;               // padded extent (5 DMMA tiles)
 constexpr int FSM = 44;              // factor / T row stride (== 4 mod 8)
 constexpr int FMAT = FN * FSM;       // one padded factor matrix (doubles)
 constexpr int FX_MAXE = 2;           // distinct extents with resident factors
-constexpr int PXS = 36;              // plane slab row stride (== 4 mod 8)
-constexpr int PX_BUF = FN * PXS;     // one plane buffer
-constexpr int PW_WARPS = 8;          // warps per plane CTA: 4 pairs, one plane item per pair
-constexpr int PW_PAIRS = PW_WARPS / 2;
-constexpr int PW_PER_WARP = 2 * PX_BUF + FMAT;   // per pair: double-buffered plane + step-1 result
+constexpr int PXS = 36;              // plane buffer row stride (== 4 mod 8)
+constexpr int PX_ROWS = 36;          // plane buffer rows (DMMA row tile 4 reads rows 36..39 of the
+                                     // next buffer: finite data, discarded outputs)
+constexpr int PX_BUF = PX_ROWS * PXS;
+constexpr int PX_SLACK = 4 * PXS;    // after the last buffer
+constexpr int PW_WARPS = 8;          // warps per plane CTA, each independent
 constexpr int CXS = 12;              // column tile row stride (8 columns + 4)
 constexpr int CXR = 36;              // column tile rows per component (pad4 of the max extent)
 constexpr int CX_BUF = 3 * CXR * CXS;  // one column tile (3 components)
@@ -522,50 +523,38 @@ struct FastPlaneArgs {
 };
 
 // K1 (INV=false): plane k of S_i r -> Fy X Fx^T -> work;  K4 (INV=true): work plane -> Fy^T X Fx -> owned z
-// A pair of warps owns a plane item: warp 0 of the pair takes DMMA tiles 0-2, warp 1 tiles 3-4
-// of each 5-tile GEMM, synchronising only with each other (named barrier).  The two warps of a
-// pair sit on different SM sub-partitions and every sub-partition hosts one "3-tile" and one
-// "2-tile" warp, so the DMMA pipes stay balanced.
-__device__ __forceinline__ void pair_sync(int pair) {
-  asm volatile("bar.sync %0, 64;\n" ::"r"(pair + 1) : "memory");
-}
-
+// Every warp owns whole plane items and never waits on another warp.  The step-1 result T
+// overwrites the plane buffer in place (row m of T is written only after rows m of X were
+// consumed), so a warp needs just two 36x36 buffers and 8 warps (2 per SM sub-partition) fit.
 template <bool INV>
 __global__ void __launch_bounds__(PW_WARPS * 32, 1) k_plane_fast(FastPlaneArgs A) {
   extern __shared__ __align__(16) double smem[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
-  // pairs (0,5) (1,4) (2,7) (3,6): the members are on different SMSPs (warp % 4)
-  const int pair = warp < 4 ? warp : (warp == 4 ? 1 : warp == 5 ? 0 : warp == 6 ? 3 : 2);
-  const int half = warp < 4 ? 0 : 1;                      // 0: tiles 0..2, 1: tiles 3..4
-  const int tlo = half ? 3 : 0, thi = half ? 5 : 3;
-  const int ptid = half * 32 + lane;                       // thread index within the pair
   load_resident(smem, A.et, A.factors, tid, blockDim.x);
-  double* wbase = smem + RES_WORDS + pair * PW_PER_WARP;
-  double* T = wbase + 2 * PX_BUF;
-  for (int q = tid; q < PW_PAIRS * PW_PER_WARP; q += blockDim.x) smem[RES_WORDS + q] = 0.0;
+  double* wbase = smem + RES_WORDS + warp * 2 * PX_BUF;
+  for (int q = tid; q < PW_WARPS * 2 * PX_BUF + PX_SLACK; q += blockDim.x) smem[RES_WORDS + q] = 0.0;
   __syncthreads();
-  const int gp = blockIdx.x * PW_PAIRS + pair, np = gridDim.x * PW_PAIRS;
-  const int per = (A.n_items + np - 1) / np;
-  const int beg = gp * per, end = min(beg + per, A.n_items);
+  const int gw = blockIdx.x * PW_WARPS + warp, nw = gridDim.x * PW_WARPS;
+  const int per = (A.n_items + nw - 1) / nw;
+  const int beg = gw * per, end = min(beg + per, A.n_items);
   if (beg >= end) return;
 
-  // returns the column shift of the plane data inside the buffer (16-byte superset loads)
+  // returns the column shift of the plane data inside the buffer (16-byte superset loads);
+  // no integer division in the copy loops (the XU pipe would become the bottleneck)
   auto issue = [&](int it, int buf) -> int {
     const int4 w = A.items[it];
     const SubD d = load_sub(A.subs + w.x);
     const int c = w.y, ex = d.ex, ey = d.ey;
     double* X = wbase + buf * PX_BUF;
-    // no integer division in the copy loops: the XU pipe is the bottleneck otherwise
     if (INV || A.mode == FMP_SOLVE_FACES) {
       const int64_t P = (int64_t)ex * ey;
       const double* base = INV ? A.src + d.ws_off + (int64_t)(c * d.ez + d.oz + w.z) * d.ps
                                : A.src + d.in_off + c * P * d.ez + w.z * P;
-      // the plane is contiguous: walk it flat, tracking (j, i) incrementally
-      int j = 0, i = ptid;
+      int j = 0, i = lane;   // the plane is contiguous: walk it flat, tracking (j, i)
       while (i >= ex) { i -= ex; ++j; }
-      for (int q = ptid; q < ey * ex; q += 64) {
+      for (int q = lane; q < ey * ex; q += 32) {
         cp_async8(X + j * PXS + i, base + q, A.factors);
-        i += 64;
+        i += 32;
         while (i >= ex) { i -= ex; ++j; }
       }
       return 0;
@@ -577,9 +566,10 @@ __global__ void __launch_bounds__(PW_WARPS * 32, 1) k_plane_fast(FastPlaneArgs A
       const int shift = (int)(((uintptr_t)row0 >> 3) & 1);
       const int span = ex + shift, nch = (span + 1) >> 1;   // 16-byte chunks per row (last may be half)
       const double* a0 = row0 - shift;
-      if (lane < nch) {
-        const int ch = lane;
-        for (int j = half; j < ey; j += 2) {
+      // lanes 0..15 -> even rows, 16..31 -> odd rows; chunk = lane & 15 (+16)
+      const int ch0 = lane & 15, j0 = lane >> 4;
+      for (int j = j0; j < ey; j += 2) {
+        for (int ch = ch0; ch < nch; ch += 16) {
           const double* sp = a0 + (int64_t)j * A.g.bx + 2 * ch;
           if (2 * ch + 1 < span)
             cp_async16(X + j * PXS + 2 * ch, sp);
@@ -589,7 +579,7 @@ __global__ void __launch_bounds__(PW_WARPS * 32, 1) k_plane_fast(FastPlaneArgs A
       }
       return shift;
     }
-    for (int j = half; j < ey; j += 2)
+    for (int j = 0; j < ey; ++j)
       for (int i = lane; i < ex; i += 32)
         cp_async8(X + j * PXS + i, point_ptr(A.g, A.src, c, d.lz + w.z, d.ly + j, d.lx + i), A.factors);
     return 0;
@@ -603,19 +593,20 @@ __global__ void __launch_bounds__(PW_WARPS * 32, 1) k_plane_fast(FastPlaneArgs A
     if (it + 1 < end) shift_next = issue(it + 1, buf ^ 1);
     cp_async_commit();
     cp_async_wait<1>();
-    pair_sync(pair);   // plane `buf` landed for both warps; T free (previous step 2 done)
+    __syncwarp();
     const int4 w = A.items[it];
     const SubD d = load_sub(A.subs + w.x);
     const int c = w.y, ex = d.ex, ey = d.ey;
     const double* Fx = res_factor(smem, A.et, c, 0, ex);
     const double* Fy = res_factor(smem, A.et, c, 1, ey);
-    const double* X = wbase + buf * PX_BUF + shift_cur;
+    double* T = wbase + buf * PX_BUF;          // step-1 result, in place
+    const double* X = T + shift_cur;
     // ---- step 1: T[j][a] = sum_i X[j][i] Fx[a][i]   (INV: T[b][i] = sum_a X[b][a] Fx[a][i])
     {
       const int k4 = pad4(ex) / 4;
       const double* fb = INV ? Fx + t * FSM + g : Fx + g * FSM + t;
 #pragma unroll 1
-      for (int m = tlo; m < thi; ++m) {
+      for (int m = 0; m < 5; ++m) {
         double acc[5][2];
 #pragma unroll
         for (int n = 0; n < 5; ++n) acc[n][0] = acc[n][1] = 0.0;
@@ -628,28 +619,34 @@ __global__ void __launch_bounds__(PW_WARPS * 32, 1) k_plane_fast(FastPlaneArgs A
             dmma884(acc[n][0], acc[n][1], av, bv);
           }
         }
-        double* tr = T + (m * 8 + g) * FSM + 2 * t;
+        __syncwarp();   // every lane has read rows m*8.. of X before they are overwritten
+        const int r = m * 8 + g;
+        if (r < PX_ROWS) {
+          double* tr = T + r * PXS + 2 * t;
 #pragma unroll
-        for (int n = 0; n < 5; ++n) {
-          tr[n * 8] = acc[n][0];
-          tr[n * 8 + 1] = acc[n][1];
+          for (int n = 0; n < 5; ++n) {
+            if (n * 8 + 2 * t < PXS) {
+              tr[n * 8] = acc[n][0];
+              tr[n * 8 + 1] = acc[n][1];
+            }
+          }
         }
       }
     }
-    pair_sync(pair);
+    __syncwarp();
     // ---- step 2: O[b][a] = sum_j Fy[b][j] T[j][a]   (INV: O[j][i] = sum_b Fy[b][j] T[b][i])
     {
       const int k4 = pad4(ey) / 4;
       const double* fa = INV ? Fy + t * FSM + g : Fy + g * FSM + t;
-      const double* tb = T + t * FSM + g;
+      const double* tb = T + t * PXS + g;
       const int64_t obase = INV ? 0 : d.ws_off + (int64_t)(c * d.ez + w.z) * d.ps;
 #pragma unroll 1
-      for (int n = tlo; n < thi; ++n) {
+      for (int n = 0; n < 5; ++n) {
         double acc[5][2];
 #pragma unroll
         for (int m = 0; m < 5; ++m) acc[m][0] = acc[m][1] = 0.0;
         for (int kk = 0; kk < k4; ++kk) {
-          const double bv = tb[kk * 4 * FSM + n * 8];
+          const double bv = tb[kk * 4 * PXS + n * 8];
 #pragma unroll
           for (int m = 0; m < 5; ++m) {
             const double av = INV ? fa[kk * 4 * FSM + m * 8] : fa[m * 8 * FSM + kk * 4];
@@ -675,6 +672,7 @@ __global__ void __launch_bounds__(PW_WARPS * 32, 1) k_plane_fast(FastPlaneArgs A
         }
       }
     }
+    __syncwarp();
     shift_cur = shift_next;
     buf ^= 1;
   }
@@ -1050,7 +1048,7 @@ static void free_plan(fmp_precond* p) {
   delete p;
 }
 
-constexpr int kPlaneFastSmem = (RES_WORDS + PW_PAIRS * PW_PER_WARP) * (int)sizeof(double);
+constexpr int kPlaneFastSmem = (RES_WORDS + PW_WARPS * 2 * PX_BUF + PX_SLACK) * (int)sizeof(double);
 constexpr int kColFastSmem = (RES_WORDS + CW_WARPS * 2 * CX_BUF) * (int)sizeof(double);
 
 static int plane_nt(const fmp_precond* p) { return std::max(p->max_ex, p->max_ey) <= 40 ? 5 : 9; }
@@ -1236,7 +1234,7 @@ static int plane_pass(fmp_precond* p, const fmp_block* blk, bool inv, int mode, 
     a.factors = p->d.factors;
     a.mode = mode;
     a.et = p->et;
-    const int grid = std::min(p->sms, (a.n_items + PW_PAIRS - 1) / PW_PAIRS);
+    const int grid = std::min(p->sms, (a.n_items + PW_WARPS - 1) / PW_WARPS);
     if (inv)
       k_plane_fast<true><<<grid, PW_WARPS * 32, kPlaneFastSmem, st>>>(a);
     else
