@@ -464,7 +464,7 @@ constexpr int PXS = 36;              // plane buffer row stride (== 4 mod 8)
 constexpr int PX_ROWS = 36;          // plane buffer rows (DMMA row tile 4 reads rows 36..39 of the
                                      // next buffer: finite data, discarded outputs)
 constexpr int PX_BUF = PX_ROWS * PXS;
-constexpr int PX_SLACK = 4 * PXS;    // after the last buffer
+constexpr int PX_SLACK = 5 * PXS;    // after the last buffer (row tile 4 + the K-pad column overrun)
 constexpr int PW_WARPS = 8;          // warps per plane CTA, each independent
 constexpr int CXS = 12;              // column tile row stride (8 columns + 4)
 constexpr int CXR = 36;              // column tile rows per component (pad4 of the max extent)
