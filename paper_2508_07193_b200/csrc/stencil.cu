@@ -47,62 +47,95 @@ __device__ __forceinline__ void bracket(const Loader<GEN>& L, int k, int j, int 
   tz = 4.0 * ez - ez_im - ez_ip - ez_jm - ez_jp + ex_kp - ex - ex_im_kp + ex_im + ey_kp - ey - ey_jm_kp + ey_jm;
 }
 
-template <int MODE, bool GEN>
-__device__ __forceinline__ void spmv_tile(const Geo& g, double alpha, int bnd, const double* __restrict__ x,
-                                          double* __restrict__ y, const double* __restrict__ w, int i, int j,
-                                          int k0, double& acc0, double& acc1) {
-  if (i >= g.bx || j >= g.by) return;
-  const Loader<GEN> L{g, x};
-  const int kend = min(k0 + SZ, g.bz);
-  const int gi = g.gx0 + i, gj = g.gy0 + j;
-  const int64_t V = (int64_t)g.bx * g.by * g.bz;
-  for (int k = k0; k < kend; ++k) {
-    double tx, ty, tz, ex, ey, ez;
-    bracket<GEN>(L, k, j, i, tx, ty, tz, ex, ey, ez);
-    if (!bnd) {
-      const int gk = g.gz0 + k;
-      tx -= ((gj == 0) + (gk == 0)) * ex;
-      ty -= ((gi == 0) + (gk == 0)) * ey;
-      tz -= ((gi == 0) + (gj == 0)) * ez;
-    }
-    const double yx = ex + alpha * tx, yy = ey + alpha * ty, yz = ez + alpha * tz;
-    const int64_t o = fidx(g, 0, k, j, i);
-    if (MODE == 3) {
-      const double rx = w[o] - yx, ry = w[o + V] - yy, rz = w[o + 2 * V] - yz;
-      acc0 += rx * rx + ry * ry + rz * rz;
-    } else {
-      y[o] = yx;
-      y[o + V] = yy;
-      y[o + 2 * V] = yz;
-      if (MODE >= 1) acc0 += yx * w[o] + yy * w[o + V] + yz * w[o + 2 * V];
-      if (MODE == 2) acc1 += yx * yx + yy * yy + yz * yz;
-    }
+// ---------------------------------------------------------------- SpMV: 2.5-D blocked z-march
+// A CTA owns a 32 x 8 (x, y) column tile and marches a z-range.  Planes k-1, k, k+1 of all
+// three components (tile + 1-cell halo) sit in a 4-slot shared-memory ring; plane k+2 streams
+// in with cp.async while plane k is computed, so every x value is read from HBM about once
+// (halo rows/columns come from L2) and the 25 neighbour reads per point hit shared memory.
+constexpr int TX = 32, TY = 8, KZC = 64;               // tile and z-chunk
+constexpr int HX = TX + 2, HY = TY + 2, PLANE = HX * HY;  // haloed plane (per component)
+constexpr int NSLOT = 4;
+
+__device__ __forceinline__ void spmv_issue_plane(const Geo& g, const double* __restrict__ x, double* slot, int i0,
+                                                 int j0, int k) {
+  for (int q = threadIdx.x; q < 3 * PLANE; q += TX * TY) {
+    const int c = q / PLANE, rem = q - c * PLANE, r = rem / HX, col = rem - r * HX;
+    cp_async8(slot + q, point_ptr(g, x, c, k, j0 - 1 + r, i0 - 1 + col), x);
   }
 }
 
 template <int MODE>
-__global__ void __launch_bounds__(SX* SY) k_spmv(Geo g, double alpha, int bnd, const double* __restrict__ x,
+__global__ void __launch_bounds__(TX* TY) k_spmv(Geo g, double alpha, int bnd, const double* __restrict__ x,
                                                   double* __restrict__ y, const double* __restrict__ w,
                                                   double* __restrict__ partials, int tiles_x, int tiles_y,
-                                                  int tiles_z) {
-  __shared__ double red[SX * SY / 32];
+                                                  int nkc) {
+  __shared__ __align__(16) double ring[NSLOT][3 * PLANE];
+  __shared__ double red[TX * TY / 32];
+  const int tid = threadIdx.x, lx = tid % TX, ly = tid / TX;
   double acc0 = 0.0, acc1 = 0.0;
-  const int ntiles = tiles_x * tiles_y * tiles_z;
-  const int lx = threadIdx.x % SX, ly = threadIdx.x / SX;
-  for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    const int tx = t % tiles_x, rest = t / tiles_x, ty = rest % tiles_y, tz = rest / tiles_y;
-    const int i0 = tx * SX, j0 = ty * SY, k0 = tz * SZ;
-    const bool interior = i0 >= 1 && i0 + SX < g.bx && j0 >= 1 && j0 + SY < g.by && k0 >= 1 && k0 + SZ < g.bz;
-    if (interior)
-      spmv_tile<MODE, false>(g, alpha, bnd, x, y, w, i0 + lx, j0 + ly, k0, acc0, acc1);
-    else
-      spmv_tile<MODE, true>(g, alpha, bnd, x, y, w, i0 + lx, j0 + ly, k0, acc0, acc1);
+  const int ntiles = tiles_x * tiles_y * nkc;
+  const int64_t V = (int64_t)g.bx * g.by * g.bz;
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int tx = tile % tiles_x, rest = tile / tiles_x, ty = rest % tiles_y, kc = rest / tiles_y;
+    const int i0 = tx * TX, j0 = ty * TY, k0 = kc * KZC, k1 = min(k0 + KZC, g.bz);
+    const int i = i0 + lx, j = j0 + ly;
+    const bool active = i < g.bx && j < g.by;
+    const int gi = g.gx0 + i, gj = g.gy0 + j;
+    __syncthreads();   // ring reuse across tiles
+    for (int kk = k0 - 1; kk <= k0 + 1; ++kk) {
+      spmv_issue_plane(g, x, ring[(kk - k0 + 1 + NSLOT) % NSLOT], i0, j0, kk);
+      cp_async_commit();
+    }
+    for (int k = k0; k < k1; ++k) {
+      cp_async_wait<0>();
+      __syncthreads();   // planes k-1..k+1 visible; slot of k-2 free
+      if (k + 2 <= k1) spmv_issue_plane(g, x, ring[(k + 2 - k0 + 1) % NSLOT], i0, j0, k + 2);
+      cp_async_commit();
+      if (!active) continue;
+      const double* pm = ring[(k - 1 - k0 + 1) % NSLOT];
+      const double* p0 = ring[(k - k0 + 1) % NSLOT];
+      const double* pp = ring[(k + 1 - k0 + 1) % NSLOT];
+      const int o = (ly + 1) * HX + lx + 1;
+#define EX(P, dj, di) P[0 * PLANE + o + (dj) * HX + (di)]
+#define EY(P, dj, di) P[1 * PLANE + o + (dj) * HX + (di)]
+#define EZ(P, dj, di) P[2 * PLANE + o + (dj) * HX + (di)]
+      const double ex = EX(p0, 0, 0), ey = EY(p0, 0, 0), ez = EZ(p0, 0, 0);
+      // Appendix A: (C_b C_f + Lambda) x on the zero-ghost padded box
+      double tx = 4.0 * ex - EX(p0, -1, 0) - EX(p0, 1, 0) - EX(pm, 0, 0) - EX(pp, 0, 0) + EY(p0, 0, 1) - ey -
+                  EY(p0, -1, 1) + EY(p0, -1, 0) + EZ(p0, 0, 1) - ez - EZ(pm, 0, 1) + EZ(pm, 0, 0);
+      double ty = 4.0 * ey - EY(p0, 0, -1) - EY(p0, 0, 1) - EY(pm, 0, 0) - EY(pp, 0, 0) + EZ(p0, 1, 0) - ez -
+                  EZ(pm, 1, 0) + EZ(pm, 0, 0) + EX(p0, 1, 0) - ex - EX(p0, 1, -1) + EX(p0, 0, -1);
+      double tz = 4.0 * ez - EZ(p0, 0, -1) - EZ(p0, 0, 1) - EZ(p0, -1, 0) - EZ(p0, 1, 0) + EX(pp, 0, 0) - ex -
+                  EX(pp, 0, -1) + EX(p0, 0, -1) + EY(pp, 0, 0) - ey - EY(pp, -1, 0) + EY(p0, -1, 0);
+#undef EX
+#undef EY
+#undef EZ
+      if (!bnd) {
+        const int gk = g.gz0 + k;
+        tx -= ((gj == 0) + (gk == 0)) * ex;
+        ty -= ((gi == 0) + (gk == 0)) * ey;
+        tz -= ((gi == 0) + (gj == 0)) * ez;
+      }
+      const double yx = ex + alpha * tx, yy = ey + alpha * ty, yz = ez + alpha * tz;
+      const int64_t oi = fidx(g, 0, k, j, i);
+      if (MODE == 3) {
+        const double rx = w[oi] - yx, ry = w[oi + V] - yy, rz = w[oi + 2 * V] - yz;
+        acc0 += rx * rx + ry * ry + rz * rz;
+      } else {
+        y[oi] = yx;
+        y[oi + V] = yy;
+        y[oi + 2 * V] = yz;
+        if (MODE >= 1) acc0 += yx * w[oi] + yy * w[oi + V] + yz * w[oi + 2 * V];
+        if (MODE == 2) acc1 += yx * yx + yy * yy + yz * yz;
+      }
+    }
+    cp_async_wait<0>();
   }
   if (MODE >= 1) {
-    const double s0 = block_sum<SX * SY>(acc0, red);
+    const double s0 = block_sum<TX * TY>(acc0, red);
     if (threadIdx.x == 0) partials[blockIdx.x] = s0;
     if (MODE == 2) {
-      const double s1 = block_sum<SX * SY>(acc1, red);
+      const double s1 = block_sum<TX * TY>(acc1, red);
       if (threadIdx.x == 0) partials[gridDim.x + blockIdx.x] = s1;
     }
   }
@@ -191,15 +224,15 @@ extern "C" int fmp_stencil_apply(const fmp_block* blk, double alpha, int boundar
   FMP_REQUIRE(mode >= 0 && mode <= 3, "bad stencil mode %d", mode);
   FMP_REQUIRE(mode == 0 || (w && dots && scratch), "mode %d needs w, dots and scratch", mode);
   const Geo g = make_geo(blk);
-  const int tx = (g.bx + SX - 1) / SX, ty = (g.by + SY - 1) / SY, tz = (g.bz + SZ - 1) / SZ;
+  const int tx = (g.bx + TX - 1) / TX, ty = (g.by + TY - 1) / TY, tz = (g.bz + KZC - 1) / KZC;
   const int64_t nt = (int64_t)tx * ty * tz;
   const int grid = (int)(nt < kStencilGrid ? nt : kStencilGrid);
   cudaStream_t st = as_stream(stream);
   switch (mode) {
-    case 0: k_spmv<0><<<grid, SX * SY, 0, st>>>(g, alpha, boundary, x, y, w, scratch, tx, ty, tz); break;
-    case 1: k_spmv<1><<<grid, SX * SY, 0, st>>>(g, alpha, boundary, x, y, w, scratch, tx, ty, tz); break;
-    case 2: k_spmv<2><<<grid, SX * SY, 0, st>>>(g, alpha, boundary, x, y, w, scratch, tx, ty, tz); break;
-    case 3: k_spmv<3><<<grid, SX * SY, 0, st>>>(g, alpha, boundary, x, y, w, scratch, tx, ty, tz); break;
+    case 0: k_spmv<0><<<grid, TX * TY, 0, st>>>(g, alpha, boundary, x, y, w, scratch, tx, ty, tz); break;
+    case 1: k_spmv<1><<<grid, TX * TY, 0, st>>>(g, alpha, boundary, x, y, w, scratch, tx, ty, tz); break;
+    case 2: k_spmv<2><<<grid, TX * TY, 0, st>>>(g, alpha, boundary, x, y, w, scratch, tx, ty, tz); break;
+    case 3: k_spmv<3><<<grid, TX * TY, 0, st>>>(g, alpha, boundary, x, y, w, scratch, tx, ty, tz); break;
   }
   FMP_CHECK_LAUNCH();
   if (mode >= 1) return finish_reduce(scratch, grid, mode == 2 ? 2 : 1, dots, st);
