@@ -54,7 +54,7 @@ __device__ __forceinline__ void bracket(const Loader<GEN>& L, int k, int j, int 
 // (halo rows/columns come from L2) and the 25 neighbour reads per point hit shared memory.
 constexpr int TX = 32, TY = 8, KZC = 64;               // tile and z-chunk
 constexpr int HX = TX + 2, HY = TY + 2, PLANE = HX * HY;  // haloed plane (per component)
-constexpr int NSLOT = 4;
+constexpr int NSLOT = 5;   // planes k-1, k, k+1 in use, k+2 and k+3 in flight
 
 __device__ __forceinline__ void spmv_issue_plane(const Geo& g, const double* __restrict__ x, double* slot, int i0,
                                                  int j0, int k) {
@@ -82,14 +82,14 @@ __global__ void __launch_bounds__(TX* TY) k_spmv(Geo g, double alpha, int bnd, c
     const bool active = i < g.bx && j < g.by;
     const int gi = g.gx0 + i, gj = g.gy0 + j;
     __syncthreads();   // ring reuse across tiles
-    for (int kk = k0 - 1; kk <= k0 + 1; ++kk) {
-      spmv_issue_plane(g, x, ring[(kk - k0 + 1 + NSLOT) % NSLOT], i0, j0, kk);
+    for (int kk = k0 - 1; kk <= k0 + 2; ++kk) {   // one commit group per plane
+      if (kk <= k1) spmv_issue_plane(g, x, ring[(kk - k0 + 1) % NSLOT], i0, j0, kk);
       cp_async_commit();
     }
     for (int k = k0; k < k1; ++k) {
-      cp_async_wait<0>();
-      __syncthreads();   // planes k-1..k+1 visible; slot of k-2 free
-      if (k + 2 <= k1) spmv_issue_plane(g, x, ring[(k + 2 - k0 + 1) % NSLOT], i0, j0, k + 2);
+      cp_async_wait<1>();   // planes up to k+1 landed (k+2 may still be in flight)
+      __syncthreads();      // ... for everyone; slot of k-2 is free
+      if (k + 3 <= k1) spmv_issue_plane(g, x, ring[(k + 3 - k0 + 1) % NSLOT], i0, j0, k + 3);
       cp_async_commit();
       if (!active) continue;
       const double* pm = ring[(k - 1 - k0 + 1) % NSLOT];
