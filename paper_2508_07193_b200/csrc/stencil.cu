@@ -52,7 +52,7 @@ __device__ __forceinline__ void bracket(const Loader<GEN>& L, int k, int j, int 
 // three components (tile + 1-cell halo) sit in a 4-slot shared-memory ring; plane k+2 streams
 // in with cp.async while plane k is computed, so every x value is read from HBM about once
 // (halo rows/columns come from L2) and the 25 neighbour reads per point hit shared memory.
-constexpr int TX = 32, TY = 8, KZC = 64;               // tile and z-chunk
+constexpr int TX = 32, TY = 8;                         // column tile
 constexpr int HX = TX + 2, HY = TY + 2, PLANE = HX * HY;  // haloed plane (per component)
 constexpr int NSLOT = 5;   // planes k-1, k, k+1 in use, k+2 and k+3 in flight
 
@@ -64,24 +64,31 @@ __device__ __forceinline__ void spmv_issue_plane(const Geo& g, const double* __r
   }
 }
 
+// Work is split in "plane units" (one z-plane of one column tile): CTA b takes the contiguous
+// unit range [b*U/G, (b+1)*U/G) -- whole tiles or pieces of at most two -- so the grid is an
+// exact multiple of the SM count with no partial last wave.
 template <int MODE>
 __global__ void __launch_bounds__(TX* TY) k_spmv(Geo g, double alpha, int bnd, const double* __restrict__ x,
                                                   double* __restrict__ y, const double* __restrict__ w,
-                                                  double* __restrict__ partials, int tiles_x, int tiles_y,
-                                                  int nkc) {
+                                                  double* __restrict__ partials, int tiles_x, int tiles_y) {
   __shared__ __align__(16) double ring[NSLOT][3 * PLANE];
   __shared__ double red[TX * TY / 32];
   const int tid = threadIdx.x, lx = tid % TX, ly = tid / TX;
   double acc0 = 0.0, acc1 = 0.0;
-  const int ntiles = tiles_x * tiles_y * nkc;
   const int64_t V = (int64_t)g.bx * g.by * g.bz;
-  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int tx = tile % tiles_x, rest = tile / tiles_x, ty = rest % tiles_y, kc = rest / tiles_y;
-    const int i0 = tx * TX, j0 = ty * TY, k0 = kc * KZC, k1 = min(k0 + KZC, g.bz);
+  const int64_t units = (int64_t)tiles_x * tiles_y * g.bz;
+  const int64_t u0 = units * blockIdx.x / gridDim.x, u1 = units * (blockIdx.x + 1) / gridDim.x;
+  for (int64_t u = u0; u < u1;) {
+    const int tile = (int)(u / g.bz);
+    const int k0 = (int)(u - (int64_t)tile * g.bz);
+    const int k1 = (int)min<int64_t>(g.bz, k0 + (u1 - u));
+    u += k1 - k0;
+    const int tx = tile % tiles_x, ty = tile / tiles_x;
+    const int i0 = tx * TX, j0 = ty * TY;
     const int i = i0 + lx, j = j0 + ly;
     const bool active = i < g.bx && j < g.by;
     const int gi = g.gx0 + i, gj = g.gy0 + j;
-    __syncthreads();   // ring reuse across tiles
+    __syncthreads();   // ring reuse across segments
     for (int kk = k0 - 1; kk <= k0 + 2; ++kk) {   // one commit group per plane
       if (kk <= k1) spmv_issue_plane(g, x, ring[(kk - k0 + 1) % NSLOT], i0, j0, kk);
       cp_async_commit();
@@ -224,15 +231,17 @@ extern "C" int fmp_stencil_apply(const fmp_block* blk, double alpha, int boundar
   FMP_REQUIRE(mode >= 0 && mode <= 3, "bad stencil mode %d", mode);
   FMP_REQUIRE(mode == 0 || (w && dots && scratch), "mode %d needs w, dots and scratch", mode);
   const Geo g = make_geo(blk);
-  const int tx = (g.bx + TX - 1) / TX, ty = (g.by + TY - 1) / TY, tz = (g.bz + KZC - 1) / KZC;
-  const int64_t nt = (int64_t)tx * ty * tz;
-  const int grid = (int)(nt < kStencilGrid ? nt : kStencilGrid);
+  const int tx = (g.bx + TX - 1) / TX, ty = (g.by + TY - 1) / TY;
+  const int64_t units = (int64_t)tx * ty * g.bz;
+  // one full wave: SMs x resident CTAs (smem-limited to 5 of 41 KB), fewer for tiny blocks
+  const int64_t want = (int64_t)kNumSM * 5;
+  const int grid = (int)(units / 8 < want ? (units / 8 > 0 ? units / 8 : 1) : want);
   cudaStream_t st = as_stream(stream);
   switch (mode) {
-    case 0: k_spmv<0><<<grid, TX * TY, 0, st>>>(g, alpha, boundary, x, y, w, scratch, tx, ty, tz); break;
-    case 1: k_spmv<1><<<grid, TX * TY, 0, st>>>(g, alpha, boundary, x, y, w, scratch, tx, ty, tz); break;
-    case 2: k_spmv<2><<<grid, TX * TY, 0, st>>>(g, alpha, boundary, x, y, w, scratch, tx, ty, tz); break;
-    case 3: k_spmv<3><<<grid, TX * TY, 0, st>>>(g, alpha, boundary, x, y, w, scratch, tx, ty, tz); break;
+    case 0: k_spmv<0><<<grid, TX * TY, 0, st>>>(g, alpha, boundary, x, y, w, scratch, tx, ty); break;
+    case 1: k_spmv<1><<<grid, TX * TY, 0, st>>>(g, alpha, boundary, x, y, w, scratch, tx, ty); break;
+    case 2: k_spmv<2><<<grid, TX * TY, 0, st>>>(g, alpha, boundary, x, y, w, scratch, tx, ty); break;
+    case 3: k_spmv<3><<<grid, TX * TY, 0, st>>>(g, alpha, boundary, x, y, w, scratch, tx, ty); break;
   }
   FMP_CHECK_LAUNCH();
   if (mode >= 1) return finish_reduce(scratch, grid, mode == 2 ? 2 : 1, dots, st);
