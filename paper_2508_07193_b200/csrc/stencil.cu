@@ -81,7 +81,8 @@ __global__ void __launch_bounds__(TX* TY) k_spmv(Geo g, double alpha, int bnd, c
   for (int64_t u = u0; u < u1;) {
     const int tile = (int)(u / g.bz);
     const int k0 = (int)(u - (int64_t)tile * g.bz);
-    const int k1 = (int)min<int64_t>(g.bz, k0 + (u1 - u));
+    const int64_t left = u1 - u;
+    const int k1 = (int)(k0 + left < g.bz ? k0 + left : g.bz);
     u += k1 - k0;
     const int tx = tile % tiles_x, ty = tile / tiles_x;
     const int i0 = tx * TX, j0 = ty * TY;
