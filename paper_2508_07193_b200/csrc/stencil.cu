@@ -56,44 +56,11 @@ constexpr int TX = 32, TY = 8;                         // column tile
 constexpr int HX = TX + 2, HY = TY + 2, PLANE = HX * HY;  // haloed plane (per component)
 constexpr int NSLOT = 5;   // planes k-1, k, k+1 in use, k+2 and k+3 in flight
 
-// Per-thread copy plan for one segment: each thread owns <= 4 haloed-plane elements; their
-// (x, y) block offsets are fixed for the segment, only the plane term changes with k.
-constexpr int NE = (3 * PLANE + TX * TY - 1) / (TX * TY);
-struct CopyPlan {
-  int64_t off[NE];   // c*V + jj*bx + ii, or -1 when (ii, jj) is outside the block
-  short ii[NE], jj[NE];
-};
-
-__device__ __forceinline__ void spmv_plan(const Geo& g, int i0, int j0, CopyPlan& cp) {
-  const int64_t V = (int64_t)g.bx * g.by * g.bz;
-#pragma unroll
-  for (int e = 0; e < NE; ++e) {
-    const int q = threadIdx.x + e * TX * TY;
+__device__ __forceinline__ void spmv_issue_plane(const Geo& g, const double* __restrict__ x, double* slot, int i0,
+                                                 int j0, int k) {
+  for (int q = threadIdx.x; q < 3 * PLANE; q += TX * TY) {
     const int c = q / PLANE, rem = q - c * PLANE, r = rem / HX, col = rem - r * HX;
-    const int ii = i0 - 1 + col, jj = j0 - 1 + r;
-    cp.ii[e] = (short)ii;
-    cp.jj[e] = (short)jj;
-    const bool in = q < 3 * PLANE && (unsigned)ii < (unsigned)g.bx && (unsigned)jj < (unsigned)g.by;
-    cp.off[e] = in ? c * V + (int64_t)jj * g.bx + ii : -1;
-  }
-}
-
-__device__ __forceinline__ void spmv_issue_plane(const Geo& g, const double* __restrict__ x, double* slot,
-                                                 const CopyPlan& cp, int k) {
-  const int64_t pk = (int64_t)k * g.bx * g.by;
-  const bool kin = (unsigned)k < (unsigned)g.bz;
-#pragma unroll
-  for (int e = 0; e < NE; ++e) {
-    const int q = threadIdx.x + e * TX * TY;
-    if (q >= 3 * PLANE) break;
-    const double* src;
-    if (cp.off[e] >= 0 && kin) {
-      src = x + cp.off[e] + pk;
-    } else {  // outside the block in x, y or z: global zero ghost or a neighbour GPU's ghost shell
-      const int c = q / PLANE;
-      src = point_ptr(g, x, c, k, cp.jj[e], cp.ii[e]);
-    }
-    cp_async8(slot + q, src, x);
+    cp_async8(slot + q, point_ptr(g, x, c, k, j0 - 1 + r, i0 - 1 + col), x);
   }
 }
 
@@ -122,17 +89,15 @@ __global__ void __launch_bounds__(TX* TY) k_spmv(Geo g, double alpha, int bnd, c
     const int i = i0 + lx, j = j0 + ly;
     const bool active = i < g.bx && j < g.by;
     const int gi = g.gx0 + i, gj = g.gy0 + j;
-    CopyPlan cp;
-    spmv_plan(g, i0, j0, cp);
     __syncthreads();   // ring reuse across segments
     for (int kk = k0 - 1; kk <= k0 + 2; ++kk) {   // one commit group per plane
-      if (kk <= k1) spmv_issue_plane(g, x, ring[(kk - k0 + 1) % NSLOT], cp, kk);
+      if (kk <= k1) spmv_issue_plane(g, x, ring[(kk - k0 + 1) % NSLOT], i0, j0, kk);
       cp_async_commit();
     }
     for (int k = k0; k < k1; ++k) {
       cp_async_wait<1>();   // planes up to k+1 landed (k+2 may still be in flight)
       __syncthreads();      // ... for everyone; slot of k-2 is free
-      if (k + 3 <= k1) spmv_issue_plane(g, x, ring[(k + 3 - k0 + 1) % NSLOT], cp, k + 3);
+      if (k + 3 <= k1) spmv_issue_plane(g, x, ring[(k + 3 - k0 + 1) % NSLOT], i0, j0, k + 3);
       cp_async_commit();
       if (!active) continue;
       const double* pm = ring[(k - 1 - k0 + 1) % NSLOT];
