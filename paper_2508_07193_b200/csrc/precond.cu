@@ -874,51 +874,69 @@ __device__ __forceinline__ int ext_of(const SubD& d, int a) { return a == 0 ? d.
 
 // K5: Y[:, col] = e0 on the two faces per component, e0 = G^-1 y^ evaluated only there.
 // Projection along the face normal with weights F_n[t][0] (inverse factor row 0), then
-// a 2-D inverse transform over the in-plane axes.
-__global__ void __launch_bounds__(256) k_faces(FaceArgs A) {
-  extern __shared__ double smem[];
+// a 2-D inverse transform over the in-plane axes.  One CTA streams one component of one
+// subdomain (y^ read once, FC planes per chunk); all operands of the small transforms are
+// in shared memory, laid out so every warp access is contiguous or a broadcast.
+constexpr int FACE_THREADS = 256;
+constexpr int FACE_CHUNK = 4 * 1156;   // doubles of y^ staged per chunk (4 planes of 34^2)
+
+__global__ void __launch_bounds__(FACE_THREADS) k_faces(FaceArgs A) {
+  extern __shared__ __align__(16) double smem[];
   const SubD d = load_sub(A.subs + blockIdx.y);
-  const fmp_shape sh = A.shapes[d.shape];
-  const int c = blockIdx.x;
+  const fmp_shape& sh = A.shapes[d.shape];
+  const int c = blockIdx.x, tid = threadIdx.x;
   const int ex = d.ex, ey = d.ey, ez = d.ez, P = ex * ey;
   const int pm = A.pmax, pm2 = pm * pm;
-  double* sPlane = smem;          // [ey][ex]
-  double* sA = sPlane + pm2;      // primary projection   [u1][v1] (transformed indices)
-  double* sB = sA + pm2;          // secondary projection [u2][v2]
-  double* sT = sB + pm2;          // temp
+  const int ext[3] = {ex, ey, ez};
+  double* sF = smem;                 // 3 x [n][n] forward factors of component c (row-major)
+  double* sA = sF + 3 * pm2;         // primary projection   [u1][v1]
+  double* sB = sA + pm2;             // secondary projection [u2][v2]
+  double* sT = sB + pm2;             // temp
+  double* sC = sT + pm2;             // staged y^ planes
+  for (int a = 0; a < 3; ++a) {
+    const double* f = fwd_factor(A.factors, sh, c, a);
+    for (int q = tid; q < ext[a] * ext[a]; q += FACE_THREADS) sF[a * pm2 + q] = __ldg(f + q);
+  }
   const FaceGeo fg = face_geo(c);
-  const double* wn1 = fwd_factor(A.factors, sh, c, fg.n1);
-  const double* wn2 = fwd_factor(A.factors, sh, c, fg.n2);
-  const int nn1 = ext_of(d, fg.n1), nn2 = ext_of(d, fg.n2);
+  for (int q = tid; q < pm2; q += FACE_THREADS) sA[q] = 0.0;
+  const double* Wz = sF + 2 * pm2;   // weights F_n[t][0] = sF[n][t*n_n]
+  const double* Wy = sF + 1 * pm2;
+  const double* Wx = sF;
   const double* src = A.yhat + d.ws_off + (int64_t)c * d.cstride();
-  for (int q = threadIdx.x; q < pm2; q += blockDim.x) sA[q] = 0.0;
-  for (int cz = 0; cz < ez; ++cz) {
+  const int nz = max(1, min(ez, FACE_CHUNK / P));
+  for (int c0 = 0; c0 < ez; c0 += nz) {
+    const int n = min(nz, ez - c0);
     __syncthreads();
-    for (int q = threadIdx.x; q < P; q += blockDim.x) sPlane[q] = src[(int64_t)cz * d.ps + q];
+    for (int kk = 0; kk < n; ++kk)
+      for (int q = tid; q < P; q += FACE_THREADS) cp_async8(sC + kk * P + q, src + (int64_t)(c0 + kk) * d.ps + q, src);
+    cp_async_commit();
+    cp_async_wait<0>();
     __syncthreads();
-    // primary face
-    if (fg.n1 == 2) {  // z-normal: sA[b][a] += w[cz] * plane[b][a]
-      const double w = __ldg(wn1 + cz * nn1);
-      for (int q = threadIdx.x; q < P; q += blockDim.x) sA[(q / ex) * pm + q % ex] += w * sPlane[q];
-    } else {  // c = z: y-normal: sA[cz][a] = sum_b w[b] plane[b][a]
-      for (int a = threadIdx.x; a < ex; a += blockDim.x) {
-        double s = 0.0;
-        for (int b = 0; b < ey; ++b) s += __ldg(wn1 + b * nn1) * sPlane[b * ex + a];
-        sA[cz * pm + a] = s;
+    if (fg.n1 == 2) {   // components x, y: z-normal face, sA[b][a] += sum_cz w[cz] y^[cz][b][a]
+      for (int q = tid; q < P; q += FACE_THREADS) {
+        double acc = sA[q];
+        for (int kk = 0; kk < n; ++kk) acc += Wz[(c0 + kk) * ez] * sC[kk * P + q];
+        sA[q] = acc;
       }
     }
-    // secondary face
-    if (fg.n2 == 1) {  // c = x: y-normal: sB[cz][a] = sum_b w[b] plane[b][a]
-      for (int a = threadIdx.x; a < ex; a += blockDim.x) {
-        double s = 0.0;
-        for (int b = 0; b < ey; ++b) s += __ldg(wn2 + b * nn2) * sPlane[b * ex + a];
-        sB[cz * pm + a] = s;
+    // y-normal projection: [cz][a] = sum_b w[b] y^[cz][b][a]   (primary for z, secondary for x)
+    if (fg.n1 == 1 || fg.n2 == 1) {
+      double* dst = fg.n1 == 1 ? sA : sB;
+      for (int q = tid; q < n * ex; q += FACE_THREADS) {
+        const int kk = q / ex, a = q - kk * ex;
+        double acc = 0.0;
+        for (int b = 0; b < ey; ++b) acc += Wy[b * ey] * sC[kk * P + b * ex + a];
+        dst[(c0 + kk) * ex + a] = acc;
       }
-    } else {  // x-normal: sB[cz][b] = sum_a w[a] plane[b][a]
-      for (int b = threadIdx.x; b < ey; b += blockDim.x) {
-        double s = 0.0;
-        for (int a = 0; a < ex; ++a) s += __ldg(wn2 + a * nn2) * sPlane[b * ex + a];
-        sB[cz * pm + b] = s;
+    }
+    // x-normal projection: [cz][b] = sum_a w[a] y^[cz][b][a]   (secondary for y, z)
+    if (fg.n2 == 0) {
+      for (int q = tid; q < n * ey; q += FACE_THREADS) {
+        const int kk = q / ey, b = q - kk * ey;
+        double acc = 0.0;
+        const double* row = sC + kk * P + b * ex;
+        for (int a = 0; a < ex; ++a) acc += Wx[a * ex] * row[a];
+        sB[(c0 + kk) * ey + b] = acc;
       }
     }
   }
@@ -929,24 +947,24 @@ __global__ void __launch_bounds__(256) k_faces(FaceArgs A) {
   for (int q = 0; q < c; ++q) base += (int)sh.m_comp[q];
   for (int f = 0; f < 2; ++f) {
     const int ua = f == 0 ? fg.u1 : fg.u2, va = f == 0 ? fg.v1 : fg.v2;
-    const int nu = ext_of(d, ua), nv = ext_of(d, va);
-    const double* Fu = fwd_factor(A.factors, sh, c, ua);
-    const double* Fv = fwd_factor(A.factors, sh, c, va);
-    const double* Pj = f == 0 ? sA : sB;
-    for (int q = threadIdx.x; q < nu * nv; q += blockDim.x) {  // T[tu][v] = sum_tv Pj[tu][tv] Fv[tv][v]
+    const int nu = ext[ua], nv = ext[va];
+    const double* Fu = sF + ua * pm2;
+    const double* Fv = sF + va * pm2;
+    const double* Pj = f == 0 ? sA : sB;   // [tu][tv], row stride nv
+    for (int q = tid; q < nu * nv; q += FACE_THREADS) {   // T[tu][v] = sum_tv Pj[tu][tv] Fv[tv][v]
       const int tu = q / nv, v = q - tu * nv;
-      double s = 0.0;
-      for (int tv = 0; tv < nv; ++tv) s += Pj[tu * pm + tv] * __ldg(Fv + tv * nv + v);
-      sT[tu * pm + v] = s;
+      double acc = 0.0;
+      for (int tv = 0; tv < nv; ++tv) acc += Pj[tu * nv + tv] * Fv[tv * nv + v];
+      sT[q] = acc;
     }
     __syncthreads();
-    for (int q = threadIdx.x; q < nu * nv; q += blockDim.x) {  // E[u][v] = sum_tu Fu[tu][u] T[tu][v]
+    for (int q = tid; q < nu * nv; q += FACE_THREADS) {   // E[u][v] = sum_tu Fu[tu][u] T[tu][v]
       const int u = q / nv, v = q - u * nv;
       const int row = face_row(c, f, u, v, ex, ey);
       if (row < 0) continue;
-      double s = 0.0;
-      for (int tu = 0; tu < nu; ++tu) s += __ldg(Fu + tu * nu + u) * sT[tu * pm + v];
-      Y[base + row] = s;
+      double acc = 0.0;
+      for (int tu = 0; tu < nu; ++tu) acc += Fu[tu * nu + u] * sT[tu * nv + v];
+      Y[base + row] = acc;
     }
     __syncthreads();
   }
@@ -954,45 +972,57 @@ __global__ void __launch_bounds__(256) k_faces(FaceArgs A) {
 
 // K6: from Z (C^-1 Y) build, per component and face, the forward-transformed face plane
 // Proj[tu][tv] = sum_{u,v} Fu[tu][u] Fv[tv][v] Zface[u][v]  -> corr planes (see K3).
-__global__ void __launch_bounds__(256) k_corr(FaceArgs A) {
-  extern __shared__ double smem[];
+__global__ void __launch_bounds__(FACE_THREADS) k_corr(FaceArgs A) {
+  extern __shared__ __align__(16) double smem[];
   const SubD d = load_sub(A.subs + blockIdx.y);
-  const fmp_shape sh = A.shapes[d.shape];
-  const int c = blockIdx.x;
-  const int ex = d.ex, ey = d.ey;
+  const fmp_shape& sh = A.shapes[d.shape];
+  const int c = blockIdx.x, tid = threadIdx.x;
+  const int ex = d.ex, ey = d.ey, ez = d.ez;
+  const int ext[3] = {ex, ey, ez};
   const int pm = A.pmax, pm2 = pm * pm;
-  double* sZ = smem;       // [u][v]
-  double* sT = sZ + pm2;   // [u][tv]
+  double* sF = smem;          // 3 x [n][n] forward factors (row-major)
+  double* sFt = sF + 3 * pm2; // 3 x [n][n] their transposes
+  double* sZ = sFt + 3 * pm2; // [u][v]
+  double* sT = sZ + pm2;      // [u][tv]
+  for (int a = 0; a < 3; ++a) {
+    const double* f = fwd_factor(A.factors, sh, c, a);
+    const int n = ext[a];
+    for (int q = tid; q < n * n; q += FACE_THREADS) {
+      const double v = __ldg(f + q);
+      sF[a * pm2 + q] = v;
+      sFt[a * pm2 + (q % n) * n + q / n] = v;
+    }
+  }
   const FaceGeo fg = face_geo(c);
   const double* Z = A.zmat[d.shape] + (int64_t)d.column * sh.m;
   int base = 0;
   for (int q = 0; q < c; ++q) base += (int)sh.m_comp[q];
   for (int f = 0; f < 2; ++f) {
     const int ua = f == 0 ? fg.u1 : fg.u2, va = f == 0 ? fg.v1 : fg.v2;
-    const int nu = ext_of(d, ua), nv = ext_of(d, va);
-    const double* Fu = fwd_factor(A.factors, sh, c, ua);
-    const double* Fv = fwd_factor(A.factors, sh, c, va);
-    for (int q = threadIdx.x; q < nu * nv; q += blockDim.x) {
+    const int nu = ext[ua], nv = ext[va];
+    const double* Fu = sF + ua * pm2;
+    const double* Fvt = sFt + va * pm2;
+    __syncthreads();
+    for (int q = tid; q < nu * nv; q += FACE_THREADS) {
       const int u = q / nv, v = q - u * nv;
       const int row = face_row(c, f, u, v, ex, ey);
-      sZ[u * pm + v] = row < 0 ? 0.0 : Z[base + row];
+      sZ[q] = row < 0 ? 0.0 : Z[base + row];
     }
     __syncthreads();
-    for (int q = threadIdx.x; q < nu * nv; q += blockDim.x) {  // T[u][tv] = sum_v Z[u][v] Fv[tv][v]
+    for (int q = tid; q < nu * nv; q += FACE_THREADS) {   // T[u][tv] = sum_v Z[u][v] Fv[tv][v]
       const int u = q / nv, tv = q - u * nv;
-      double s = 0.0;
-      for (int v = 0; v < nv; ++v) s += sZ[u * pm + v] * __ldg(Fv + tv * nv + v);
-      sT[u * pm + tv] = s;
+      double acc = 0.0;
+      for (int v = 0; v < nv; ++v) acc += sZ[u * nv + v] * Fvt[v * nv + tv];
+      sT[q] = acc;
     }
     __syncthreads();
     double* out = A.corr + ((int64_t)blockIdx.y * 6 + c * 2 + f) * pm2;
-    for (int q = threadIdx.x; q < nu * nv; q += blockDim.x) {  // Proj[tu][tv] = sum_u Fu[tu][u] T[u][tv]
+    for (int q = tid; q < nu * nv; q += FACE_THREADS) {   // Proj[tu][tv] = sum_u Fu[tu][u] T[u][tv]
       const int tu = q / nv, tv = q - tu * nv;
-      double s = 0.0;
-      for (int u = 0; u < nu; ++u) s += __ldg(Fu + tu * nu + u) * sT[u * pm + tv];
-      out[tu * pm + tv] = s;
+      double acc = 0.0;
+      for (int u = 0; u < nu; ++u) acc += Fu[tu * nu + u] * sT[u * nv + tv];
+      out[tu * pm + tv] = acc;
     }
-    __syncthreads();
   }
 }
 
@@ -1276,7 +1306,8 @@ extern "C" int fmp_precond_apply(fmp_precond* p, const fmp_block* blk, int mode,
   const int pm = (int)p->d.pmax;
   FaceArgs fa{p->d.subs, p->d.shapes, p->d.factors, wb, p->d.corr, p->d_ymat, p->d_zmat, pm};
   if (mode != FMP_SOLVE_EXACT) {
-    k_faces<<<dim3(3, (unsigned)p->d.n_sub), 256, 4 * pm * pm * sizeof(double), st>>>(fa);
+    const size_t fs = (6 * (size_t)pm * pm + std::max<size_t>(FACE_CHUNK, (size_t)p->max_p)) * sizeof(double);
+    k_faces<<<dim3(3, (unsigned)p->d.n_sub), FACE_THREADS, fs, st>>>(fa);
     FMP_CHECK_LAUNCH();
   }
   if (mode == FMP_SOLVE_FACES) return 0;
@@ -1292,7 +1323,7 @@ extern "C" int fmp_precond_apply(fmp_precond* p, const fmp_block* blk, int mode,
                                       p->ymat[s], m, &zero, p->zmat[s], m);
       FMP_REQUIRE(bs == CUBLAS_STATUS_SUCCESS, "cublasDgemm failed (%d)", (int)bs);
     }
-    k_corr<<<dim3(3, (unsigned)p->d.n_sub), 256, 2 * pm * pm * sizeof(double), st>>>(fa);
+    k_corr<<<dim3(3, (unsigned)p->d.n_sub), FACE_THREADS, 8 * (size_t)pm * pm * sizeof(double), st>>>(fa);
     FMP_CHECK_LAUNCH();
   }
   if (int e = column_pass(p, true, wb, wa, mode == FMP_SOLVE_WOODBURY ? p->d.corr : nullptr, st)) return e;
