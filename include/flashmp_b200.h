@@ -129,7 +129,9 @@ typedef struct fmp_shape {       /* 20 x int64 */
   int64_t s_off[3];      /* offset of the singular values per axis */
   int64_t qw_off;        /* offset of the per-point block-inverse table: (q, w) pairs, point-major,
                             q = 1/(1+alpha|s|^2), w = (1-q)/|s|^2  so  B^-1 y = q y + w s (s.y) */
-  int64_t reserved[3];
+  int64_t ld;            /* row stride of C^-1 [m][ld], Y and Z [n_s][ld]: m rounded up to 4,
+                            padding zero-filled */
+  int64_t reserved[2];
 } fmp_shape;
 #define FMP_SUBDOMAIN_WORDS 16
 #define FMP_SHAPE_WORDS 20
@@ -143,12 +145,12 @@ typedef struct fmp_precond_desc {
   const fmp_shape* shapes_host;  /* host copy */
   const int64_t* shape_first;    /* host: first subdomain of each shape (n_shape+1 entries) */
   const double* factors;         /* device: concatenated U^T, V^T, S blocks */
-  const double* const* cinv;     /* host array of n_shape device pointers to m x m C^-1 */
+  const double* const* cinv;     /* host array of n_shape device pointers to C^-1, [m][ld] */
   double* work_a;                /* device workspace, >= sum 3*V_ext (+ padding) doubles */
   double* work_b;                /* device workspace, same size */
   double* corr;                  /* device: n_sub * 6 * pmax^2 doubles (correction planes) */
-  double* const* ymat;           /* host array of n_shape device pointers, m x n_s each */
-  double* const* zmat;           /* host array of n_shape device pointers, m x n_s each */
+  double* const* ymat;           /* host array of n_shape device pointers, [n_s][ld] each */
+  double* const* zmat;           /* host array of n_shape device pointers, [n_s][ld] each */
   int64_t pmax;                  /* max extent over all shapes */
 } fmp_precond_desc;
 

@@ -19,11 +19,28 @@
 // components of the extended box (x fastest), i.e. the reference's own order.
 #include <algorithm>
 #include <cstdlib>
+#include <string>
 #include <vector>
 #include <cublas_v2.h>
 #include "common.cuh"
 
 namespace fmp {
+
+// gemm.cu
+struct GemmShape {
+  const double* A;
+  const double* B;
+  double* C;
+  int m, n, ld;
+};
+struct GemmTile {
+  int shape, i0, n0, pad;
+};
+int gemm_setup();
+int gemm_config_of(int n);
+int gemm_tile_m(int cfg);
+int gemm_tile_n(int cfg);
+int gemm_launch(int cfg, const GemmShape* shapes, const GemmTile* tiles, int n_tiles, int sms, cudaStream_t st);
 
 __host__ __device__ constexpr int pad8(int n) { return (n + 7) & ~7; }
 __host__ __device__ constexpr int pad4(int n) { return (n + 3) & ~3; }
@@ -942,7 +959,7 @@ __global__ void __launch_bounds__(FACE_THREADS) k_faces(FaceArgs A) {
   }
   __syncthreads();
   // 2-D inverse transforms: E[u][v] = sum_tu Fu[tu][u] sum_tv Fv[tv][v] Proj[tu][tv]
-  double* Y = A.ymat[d.shape] + (int64_t)d.column * sh.m;
+  double* Y = A.ymat[d.shape] + (int64_t)d.column * sh.ld;
   int base = 0;
   for (int q = 0; q < c; ++q) base += (int)sh.m_comp[q];
   for (int f = 0; f < 2; ++f) {
@@ -994,7 +1011,7 @@ __global__ void __launch_bounds__(FACE_THREADS) k_corr(FaceArgs A) {
     }
   }
   const FaceGeo fg = face_geo(c);
-  const double* Z = A.zmat[d.shape] + (int64_t)d.column * sh.m;
+  const double* Z = A.zmat[d.shape] + (int64_t)d.column * sh.ld;
   int base = 0;
   for (int q = 0; q < c; ++q) base += (int)sh.m_comp[q];
   for (int f = 0; f < 2; ++f) {
@@ -1050,6 +1067,11 @@ struct fmp_precond {
   int4* d_finv = nullptr;
   int2* d_fcol = nullptr;
   int n_ffwd = 0, n_finv = 0, n_fcol = 0;
+  // Woodbury GEMM: own DMMA kernel (default) or cuBLAS (FMP_GEMM=cublas)
+  bool use_cublas = false;
+  GemmShape* d_gshapes = nullptr;
+  GemmTile* d_gtiles[3] = {nullptr, nullptr, nullptr};
+  int n_gtiles[3] = {0, 0, 0};
   cublasHandle_t blas = nullptr;
   int max_ex = 1, max_ey = 1, max_ez = 1, max_p = 1;
   int sms = kNumSM;
@@ -1075,6 +1097,8 @@ static void free_plan(fmp_precond* p) {
   cudaFree(p->d_ffwd);
   cudaFree(p->d_finv);
   cudaFree(p->d_fcol);
+  cudaFree(p->d_gshapes);
+  for (int c = 0; c < 3; ++c) cudaFree(p->d_gtiles[c]);
   delete p;
 }
 
@@ -1177,6 +1201,27 @@ extern "C" int fmp_precond_create(const fmp_precond_desc* desc, fmp_precond** ou
       upload(p->ymat, &p->d_ymat) || upload(p->zmat, &p->d_zmat)) {
     free_plan(p);
     return -1;
+  }
+  {  // grouped GEMM tables: one shape record per extended shape, tiles bucketed by configuration
+    const char* gm = getenv("FMP_GEMM");
+    p->use_cublas = gm && std::string(gm) == "cublas";
+    std::vector<GemmShape> gs;
+    std::vector<GemmTile> gt[3];
+    for (int64_t s2 = 0; s2 < desc->n_shape; ++s2) {
+      const auto& sh = p->shapes[s2];
+      const int n = (int)(p->first[s2 + 1] - p->first[s2]);
+      gs.push_back(GemmShape{p->cinv[s2], p->ymat[s2], p->zmat[s2], (int)sh.m, n, (int)sh.ld});
+      if (n == 0) continue;
+      const int cfg = gemm_config_of(n), mt = gemm_tile_m(cfg), nt = gemm_tile_n(cfg);
+      for (int i0 = 0; i0 < sh.m; i0 += mt)
+        for (int n0 = 0; n0 < n; n0 += nt) gt[cfg].push_back(GemmTile{(int)s2, i0, n0, 0});
+    }
+    if (upload(gs, &p->d_gshapes) || upload(gt[0], &p->d_gtiles[0]) || upload(gt[1], &p->d_gtiles[1]) ||
+        upload(gt[2], &p->d_gtiles[2]) || gemm_setup()) {
+      free_plan(p);
+      return -1;
+    }
+    for (int c = 0; c < 3; ++c) p->n_gtiles[c] = (int)gt[c].size();
   }
   if (cublasCreate(&p->blas) != CUBLAS_STATUS_SUCCESS) {
     free_plan(p);
@@ -1312,16 +1357,21 @@ extern "C" int fmp_precond_apply(fmp_precond* p, const fmp_block* blk, int mode,
   }
   if (mode == FMP_SOLVE_FACES) return 0;
   if (mode == FMP_SOLVE_WOODBURY) {
-    cublasSetStream(p->blas, st);
-    const double one = 1.0, zero = 0.0;
-    for (int64_t s = 0; s < p->d.n_shape; ++s) {
-      const int m = (int)p->shapes[s].m;
-      const int ncol = (int)(p->first[s + 1] - p->first[s]);
-      if (ncol == 0) continue;
-      // C^-1 is stored row-major (the reference's ndarray); OP_T makes cuBLAS use it as is.
-      cublasStatus_t bs = cublasDgemm(p->blas, CUBLAS_OP_T, CUBLAS_OP_N, m, ncol, m, &one, p->cinv[s], m,
-                                      p->ymat[s], m, &zero, p->zmat[s], m);
-      FMP_REQUIRE(bs == CUBLAS_STATUS_SUCCESS, "cublasDgemm failed (%d)", (int)bs);
+    if (p->use_cublas) {
+      cublasSetStream(p->blas, st);
+      const double one = 1.0, zero = 0.0;
+      for (int64_t s = 0; s < p->d.n_shape; ++s) {
+        const int m = (int)p->shapes[s].m, ld = (int)p->shapes[s].ld;
+        const int ncol = (int)(p->first[s + 1] - p->first[s]);
+        if (ncol == 0) continue;
+        // C^-1 is row-major [m][ld]; OP_T makes cuBLAS use it as is.
+        cublasStatus_t bs = cublasDgemm(p->blas, CUBLAS_OP_T, CUBLAS_OP_N, m, ncol, m, &one, p->cinv[s], ld,
+                                        p->ymat[s], ld, &zero, p->zmat[s], ld);
+        FMP_REQUIRE(bs == CUBLAS_STATUS_SUCCESS, "cublasDgemm failed (%d)", (int)bs);
+      }
+    } else {
+      for (int c = 0; c < 3; ++c)
+        if (int e = gemm_launch(c, p->d_gshapes, p->d_gtiles[c], p->n_gtiles[c], p->sms, st)) return e;
     }
     k_corr<<<dim3(3, (unsigned)p->d.n_sub), FACE_THREADS, 8 * (size_t)pm * pm * sizeof(double), st>>>(fa);
     FMP_CHECK_LAUNCH();

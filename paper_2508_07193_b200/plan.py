@@ -30,6 +30,21 @@ class SubSpec:
     in_off: int = 0
 
 
+def lead_dim(m: int) -> int:
+    """Row stride of C^-1 / Y / Z: m rounded up to 4 doubles (32-byte rows for the GEMM)."""
+    return (m + 3) // 4 * 4
+
+
+def pad_rows(t: torch.Tensor, ld: int) -> torch.Tensor:
+    """(m, m) -> (m, ld) with zero padding columns (shared when already padded)."""
+    m = t.shape[0]
+    if ld == m and t.is_contiguous():
+        return t
+    out = torch.zeros((m, ld), dtype=t.dtype, device=t.device)
+    out[:, :m] = t
+    return out
+
+
 def correction_counts(ext) -> tuple[int, int, int]:
     """Rows per component (ref:subdomain.py:235-238)."""
     nx, ny, nz = ext
@@ -96,7 +111,7 @@ class SolvePlan:
             self.m.append(sum(mc))
             offs = [self.factors.offsets[n] for n in e]
             sh_rec[q] = [*e, sum(mc), *mc, *(o[0] for o in offs), *(o[1] for o in offs), *(o[2] for o in offs),
-                         self.factors.qw[e], 0, 0, 0]
+                         self.factors.qw[e], lead_dim(sum(mc)), 0, 0]
         # ---- subdomain table, workspace layout
         sub_rec = np.zeros((len(self.subs), 16), dtype=np.int64)
         first = np.zeros(len(shapes) + 1, dtype=np.int64)
@@ -121,18 +136,22 @@ class SolvePlan:
         self.work_a = torch.zeros(ws, **f64)
         self.work_b = torch.zeros(ws, **f64)
         self.corr = torch.zeros(len(self.subs) * 6 * self.pmax * self.pmax, **f64)
-        # per-shape Y/Z matrices (column-major m x ncols == row-major (ncols, m))
-        self.ymat = [torch.zeros((max(1, n), m), **f64) for n, m in zip(self.ncols, self.m)]
-        self.zmat = [torch.zeros((max(1, n), m), **f64) for n, m in zip(self.ncols, self.m)]
+        # per-shape Y/Z matrices: row j = subdomain column j, row stride ld (zero padding)
+        self.ld = [lead_dim(m) for m in self.m]
+        self.ymat = [torch.zeros((max(1, n), ld), **f64) for n, ld in zip(self.ncols, self.ld)]
+        self.zmat = [torch.zeros((max(1, n), ld), **f64) for n, ld in zip(self.ncols, self.ld)]
         self.cinv = []
-        for e, m in zip(shapes, self.m):
+        for e, m, ld in zip(shapes, self.m, self.ld):
             t = (cinv or {}).get(e)
             if t is None:
                 if need_woodbury:
                     raise ValueError(f"missing C^-1 for shape {e}")
                 t = torch.zeros(1, **f64)
-            elif t.shape != (m, m) or t.dtype != torch.float64 or not t.is_contiguous():
-                raise ValueError(f"C^-1 for {e} must be a contiguous float64 ({m}, {m}) tensor")
+            else:
+                if t.dtype != torch.float64 or t.shape not in ((m, m), (m, ld)):
+                    raise ValueError(f"C^-1 for {e} must be a float64 ({m}, {m}) or ({m}, {ld}) tensor")
+                if t.shape != (m, ld) or not t.is_contiguous():
+                    t = pad_rows(t, ld)
             self.cinv.append(t)
         P = C.c_void_p
         self._cinv_arr = (P * len(shapes))(*[t.data_ptr() for t in self.cinv])

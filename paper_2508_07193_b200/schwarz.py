@@ -471,7 +471,7 @@ class RasPreconditioner:
                 if s.ext not in self.solvers:
                     data = solver_data_for(Box(*s.ext), self.alpha, dev)
                     self.solvers[s.ext] = data
-                    cinv[s.ext] = data.corr.inverse
+                    cinv[s.ext] = data.corr.padded
         self.plan = SolvePlan(specs, self.alpha, dev, cinv=cinv) if self.alpha != 0.0 else None
 
     def apply_into(self, r: torch.Tensor, z: torch.Tensor) -> torch.Tensor:

@@ -28,7 +28,7 @@ from . import _lib
 from .grid import Box, FieldVector
 from .instrument import NULL_TIMER, FlopCounter
 from .operators import OperatorParams
-from .plan import SolvePlan, SubSpec, block_struct, correction_counts
+from .plan import SolvePlan, SubSpec, block_struct, correction_counts, lead_dim, pad_rows
 from .transform import TransformSet
 
 CONDITION_LIMIT = 1e14          # ref:subdomain.py:48
@@ -46,7 +46,12 @@ class BoundaryCorrection:
     values: np.ndarray          # (m,) delta in {1, 2}
     m_per_component: tuple[int, int, int]
     weight_inv: np.ndarray      # 1 / (alpha delta)
-    inverse: torch.Tensor       # (m, m) C^-1 on the device, row-major
+    padded: torch.Tensor        # (m, ld) C^-1 on the device, rows zero-padded to ld (GEMM operand)
+
+    @property
+    def inverse(self) -> torch.Tensor:
+        """(m, m) view of C^-1 (ref:subdomain.py:74 `inverse`)."""
+        return self.padded[:, : self.m]
 
     @property
     def m(self) -> int:
@@ -156,7 +161,7 @@ def _assemble_correction(box: Box, alpha: float, device) -> BoundaryCorrection:
         X.zero_()
         X[ar[: hi - lo], rows_dev[lo:hi]] = 1.0
         plan.apply(blk, _lib.FMP_SOLVE_FACES, X, None)
-        CT[lo:hi] = plan.ymat[0][: hi - lo]
+        CT[lo:hi] = plan.ymat[0][: hi - lo, :m]
     weight_inv = 1.0 / (alpha * values)
     Cm = CT.t().contiguous()
     Cm.diagonal().add_(torch.from_numpy(weight_inv).to(device))
@@ -170,7 +175,7 @@ def _assemble_correction(box: Box, alpha: float, device) -> BoundaryCorrection:
         raise DegenerateConfigurationError(
             f"correction matrix condition ~{cond1:.2e} exceeds {CONDITION_LIMIT:.0e} "
             f"for box {box.extents}, alpha={alpha}")
-    return BoundaryCorrection(rows, values, per, weight_inv, inv.contiguous())
+    return BoundaryCorrection(rows, values, per, weight_inv, pad_rows(inv, lead_dim(m)))
 
 
 def precompute(params: OperatorParams, device=None) -> SubdomainSolverData:
@@ -185,7 +190,7 @@ def precompute(params: OperatorParams, device=None) -> SubdomainSolverData:
 
 def _single_plan(data: SubdomainSolverData, woodbury: bool) -> SolvePlan:
     e = data.box.extents
-    cinv = {e: data.corr.inverse} if (woodbury and data.corr is not None) else None
+    cinv = {e: data.corr.padded} if (woodbury and data.corr is not None) else None
     return SolvePlan([SubSpec(e, (0, 0, 0), (0, 0, 0), e)], data.params.alpha, data.device, cinv=cinv,
                      need_woodbury=woodbury)
 

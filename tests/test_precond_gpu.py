@@ -127,3 +127,17 @@ def test_fast_and_general_paths_agree(gext, grid, monkeypatch):
     if int(np.prod(gext)) <= 32 ** 3:
         want = O.ras_apply(gext, O.partition(gext, grid, 1), 0.25, r.cpu().numpy().ravel())
         assert rel(z_fast.cpu().numpy(), want) <= 1e-11
+
+
+def test_own_gemm_matches_cublas(monkeypatch):
+    """The DMMA Woodbury GEMM (default) and cuBLAS DGEMM (FMP_GEMM=cublas) agree."""
+    from paper_2508_07193_b200 import Box, RasPreconditioner, make_partition, make_transport
+    part = make_partition(Box(48, 32, 32), (3, 2, 2), 1)   # 3 shapes, n_s = 4 / 2 / ... columns
+    tr = make_transport("cuda")
+    r = torch.from_numpy(np.random.default_rng(8).uniform(-1, 1, part.global_box.dof)).cuda().view(
+        part.global_box.shape4)
+    monkeypatch.setenv("FMP_GEMM", "own")
+    z_own = RasPreconditioner(part, 0.25, tr).apply(r)
+    monkeypatch.setenv("FMP_GEMM", "cublas")
+    z_blas = RasPreconditioner(part, 0.25, tr).apply(r)
+    assert rel(z_own.cpu().numpy(), z_blas.cpu().numpy()) <= 1e-14
