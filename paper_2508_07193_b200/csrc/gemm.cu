@@ -39,7 +39,7 @@ __device__ __forceinline__ void cp16(double* dst, const double* src, bool valid)
 }
 
 template <int WM, int WN, int NWM, int NWN, int STAGES>
-__global__ void __launch_bounds__(32 * NWM * NWN, 1)
+__global__ void __launch_bounds__(32 * NWM * NWN)
     k_gemm(const GemmShape* __restrict__ shapes, const GemmTile* __restrict__ tiles, int n_tiles) {
   using L = GemmCfg<WM, WN, NWM, NWN, STAGES>;
   extern __shared__ __align__(16) double smem[];
@@ -116,17 +116,20 @@ __global__ void __launch_bounds__(32 * NWM * NWN, 1)
   }
 }
 
-// tile configurations: wide (n >= 48), narrow (16 < n < 48), skinny (n <= 16)
-using CfgWide = GemmCfg<4, 3, 3, 3, 4>;     //  96 x 72, 9 warps
-using CfgNarrow = GemmCfg<4, 3, 12, 1, 3>;  // 384 x 24, 12 warps
-using CfgSkinny = GemmCfg<4, 1, 12, 1, 3>;  // 384 x  8, 12 warps
+// tile configurations: wide (n >= 48): 96 x 72 CTAs, two per SM; narrow (16 < n < 48) and
+// skinny (n <= 16) are C^-1-streaming (memory-bound) products: one-warp 32-row CTAs so that
+// every SM streams several row panels at once.
+using CfgWide = GemmCfg<4, 3, 3, 3, 4>;    //  96 x 72, 9 warps
+using CfgNarrow = GemmCfg<4, 3, 1, 1, 4>;  //  32 x 24, 1 warp
+using CfgSkinny = GemmCfg<4, 1, 1, 1, 4>;  //  32 x  8, 1 warp
+constexpr int kCtasPerSm[3] = {2, 8, 8};
 
 int gemm_setup() {
   FMP_CHECK_CUDA(cudaFuncSetAttribute(k_gemm<4, 3, 3, 3, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)CfgWide::smem));
-  FMP_CHECK_CUDA(cudaFuncSetAttribute(k_gemm<4, 3, 12, 1, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  FMP_CHECK_CUDA(cudaFuncSetAttribute(k_gemm<4, 3, 1, 1, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)CfgNarrow::smem));
-  FMP_CHECK_CUDA(cudaFuncSetAttribute(k_gemm<4, 1, 12, 1, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  FMP_CHECK_CUDA(cudaFuncSetAttribute(k_gemm<4, 1, 1, 1, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)CfgSkinny::smem));
   return 0;
 }
@@ -138,13 +141,14 @@ int gemm_tile_n(int cfg) { return cfg == 0 ? CfgWide::NT : (cfg == 1 ? CfgNarrow
 // shapes/tiles are device arrays; tiles of one launch all use configuration `cfg`
 int gemm_launch(int cfg, const GemmShape* shapes, const GemmTile* tiles, int n_tiles, int sms, cudaStream_t st) {
   if (n_tiles <= 0) return 0;
-  const int grid = n_tiles < sms ? n_tiles : sms;
+  const int slots = kCtasPerSm[cfg] * sms;
+  const int grid = n_tiles < slots ? n_tiles : slots;
   if (cfg == 0)
     k_gemm<4, 3, 3, 3, 4><<<grid, 32 * CfgWide::WARPS, CfgWide::smem, st>>>(shapes, tiles, n_tiles);
   else if (cfg == 1)
-    k_gemm<4, 3, 12, 1, 3><<<grid, 32 * CfgNarrow::WARPS, CfgNarrow::smem, st>>>(shapes, tiles, n_tiles);
+    k_gemm<4, 3, 1, 1, 4><<<grid, 32 * CfgNarrow::WARPS, CfgNarrow::smem, st>>>(shapes, tiles, n_tiles);
   else
-    k_gemm<4, 1, 12, 1, 3><<<grid, 32 * CfgSkinny::WARPS, CfgSkinny::smem, st>>>(shapes, tiles, n_tiles);
+    k_gemm<4, 1, 1, 1, 4><<<grid, 32 * CfgSkinny::WARPS, CfgSkinny::smem, st>>>(shapes, tiles, n_tiles);
   FMP_CHECK_LAUNCH();
   return 0;
 }
