@@ -1068,7 +1068,12 @@ struct fmp_precond {
   int2* d_fcol = nullptr;
   int n_ffwd = 0, n_finv = 0, n_fcol = 0;
   // Woodbury GEMM: own DMMA kernel (default) or cuBLAS (FMP_GEMM=cublas)
-  bool use_cublas = false;
+  bool use_cublas = true;
+  static constexpr int kAux = 4;          // concurrent GEMM streams (small shapes are HBM-bound)
+  cudaStream_t aux[kAux] = {};
+  cublasHandle_t aux_blas[kAux] = {};
+  cudaEvent_t ev_fork = nullptr, ev_join[kAux] = {};
+  std::vector<int> gemm_order;            // shapes by decreasing GEMM size
   GemmShape* d_gshapes = nullptr;
   GemmTile* d_gtiles[3] = {nullptr, nullptr, nullptr};
   int n_gtiles[3] = {0, 0, 0};
@@ -1098,6 +1103,12 @@ static void free_plan(fmp_precond* p) {
   cudaFree(p->d_finv);
   cudaFree(p->d_fcol);
   cudaFree(p->d_gshapes);
+  for (int q = 0; q < fmp_precond::kAux; ++q) {
+    if (p->aux_blas[q]) cublasDestroy(p->aux_blas[q]);
+    if (p->aux[q]) cudaStreamDestroy(p->aux[q]);
+    if (p->ev_join[q]) cudaEventDestroy(p->ev_join[q]);
+  }
+  if (p->ev_fork) cudaEventDestroy(p->ev_fork);
   for (int c = 0; c < 3; ++c) cudaFree(p->d_gtiles[c]);
   delete p;
 }
@@ -1204,7 +1215,7 @@ extern "C" int fmp_precond_create(const fmp_precond_desc* desc, fmp_precond** ou
   }
   {  // grouped GEMM tables: one shape record per extended shape, tiles bucketed by configuration
     const char* gm = getenv("FMP_GEMM");
-    p->use_cublas = gm && std::string(gm) == "cublas";
+    p->use_cublas = !(gm && std::string(gm) == "own");
     std::vector<GemmShape> gs;
     std::vector<GemmTile> gt[3];
     for (int64_t s2 = 0; s2 < desc->n_shape; ++s2) {
@@ -1228,6 +1239,26 @@ extern "C" int fmp_precond_create(const fmp_precond_desc* desc, fmp_precond** ou
     FMP_REQUIRE(false, "cublasCreate failed");
   }
   cublasSetMathMode(p->blas, CUBLAS_DEFAULT_MATH);
+  for (int q = 0; q < fmp_precond::kAux; ++q) {
+    if (cudaStreamCreateWithFlags(&p->aux[q], cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&p->ev_join[q], cudaEventDisableTiming) != cudaSuccess ||
+        cublasCreate(&p->aux_blas[q]) != CUBLAS_STATUS_SUCCESS) {
+      free_plan(p);
+      FMP_REQUIRE(false, "auxiliary stream setup failed");
+    }
+    cublasSetStream(p->aux_blas[q], p->aux[q]);
+  }
+  if (cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming) != cudaSuccess) {
+    free_plan(p);
+    FMP_REQUIRE(false, "event creation failed");
+  }
+  for (int64_t s2 = 0; s2 < desc->n_shape; ++s2)
+    if (p->first[s2 + 1] > p->first[s2]) p->gemm_order.push_back((int)s2);
+  std::sort(p->gemm_order.begin(), p->gemm_order.end(), [&](int a, int b) {
+    const double fa = (double)p->shapes[a].m * p->shapes[a].m * (double)(p->first[a + 1] - p->first[a]);
+    const double fb = (double)p->shapes[b].m * p->shapes[b].m * (double)(p->first[b + 1] - p->first[b]);
+    return fa > fb;
+  });
   plane_attr<false, 5>(); plane_attr<true, 5>(); plane_attr<false, 9>(); plane_attr<true, 9>();
   column_attr<1>(); column_attr<2>(); column_attr<3>(); column_attr<4>(); column_attr<5>();
   column_attr<6>(); column_attr<7>(); column_attr<8>(); column_attr<9>();
@@ -1358,16 +1389,24 @@ extern "C" int fmp_precond_apply(fmp_precond* p, const fmp_block* blk, int mode,
   if (mode == FMP_SOLVE_FACES) return 0;
   if (mode == FMP_SOLVE_WOODBURY) {
     if (p->use_cublas) {
-      cublasSetStream(p->blas, st);
+      // one DGEMM per shape; shapes spread over auxiliary streams (forked from / joined into
+      // `st`) so the HBM-bound small-n products overlap the compute-bound large ones
+      FMP_CHECK_CUDA(cudaEventRecord(p->ev_fork, st));
+      const int naux = std::min<int>(fmp_precond::kAux, (int)p->gemm_order.size());
+      for (int q = 0; q < naux; ++q) FMP_CHECK_CUDA(cudaStreamWaitEvent(p->aux[q], p->ev_fork, 0));
       const double one = 1.0, zero = 0.0;
-      for (int64_t s = 0; s < p->d.n_shape; ++s) {
+      for (size_t o = 0; o < p->gemm_order.size(); ++o) {
+        const int s = p->gemm_order[o];
         const int m = (int)p->shapes[s].m, ld = (int)p->shapes[s].ld;
         const int ncol = (int)(p->first[s + 1] - p->first[s]);
-        if (ncol == 0) continue;
         // C^-1 is row-major [m][ld]; OP_T makes cuBLAS use it as is.
-        cublasStatus_t bs = cublasDgemm(p->blas, CUBLAS_OP_T, CUBLAS_OP_N, m, ncol, m, &one, p->cinv[s], ld,
-                                        p->ymat[s], ld, &zero, p->zmat[s], ld);
+        cublasStatus_t bs = cublasDgemm(p->aux_blas[o % naux], CUBLAS_OP_T, CUBLAS_OP_N, m, ncol, m, &one,
+                                        p->cinv[s], ld, p->ymat[s], ld, &zero, p->zmat[s], ld);
         FMP_REQUIRE(bs == CUBLAS_STATUS_SUCCESS, "cublasDgemm failed (%d)", (int)bs);
+      }
+      for (int q = 0; q < naux; ++q) {
+        FMP_CHECK_CUDA(cudaEventRecord(p->ev_join[q], p->aux[q]));
+        FMP_CHECK_CUDA(cudaStreamWaitEvent(st, p->ev_join[q], 0));
       }
     } else {
       for (int c = 0; c < 3; ++c)
