@@ -155,7 +155,11 @@ class DeviceTransport:
 
 
 class DistTransport:
-    """One process per GPU over torch.distributed (NCCL on GPUs, gloo for CPU tests)."""
+    """One process per GPU over torch.distributed.
+
+    NCCL moves device tensors directly (NVLink); with the gloo backend device tensors are
+    staged through host memory, which lets the multi-block path run (and be tested) with
+    several processes sharing one GPU, or on CPU tensors for the host-side logic."""
 
     name = "nccl"
     distributed = True
@@ -170,29 +174,47 @@ class DistTransport:
         self.group = group
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
+        self.name = dist.get_backend(group)
         if device is None:
-            if dist.get_backend(group) == "nccl":
+            if self.name == "nccl":
                 device = torch.device("cuda", int(os.environ.get("LOCAL_RANK", self.rank)) % torch.cuda.device_count())
-                torch.cuda.set_device(device)
             else:
                 device = torch.device("cpu")
         self.device = torch.device(device)
-        self.name = dist.get_backend(group)
+        if self.device.type == "cuda":
+            torch.cuda.set_device(self.device)
+        self.staged = self.name != "nccl" and self.device.type == "cuda"
 
     def run_ranks(self, fns) -> None:
         for fn in fns:
             fn()
 
     def allreduce_(self, t: torch.Tensor) -> torch.Tensor:
-        self.dist.all_reduce(t, group=self.group)
+        if self.staged:
+            h = t.cpu()
+            self.dist.all_reduce(h, group=self.group)
+            t.copy_(h)
+        else:
+            self.dist.all_reduce(t, group=self.group)
         return t
 
     def exchange(self, sends: list[tuple[int, torch.Tensor]], recvs: list[tuple[int, torch.Tensor]]) -> None:
+        if self.staged:
+            sends = [(p, t.cpu()) for p, t in sends]
+            hrecv = [(p, torch.empty(t.shape, dtype=t.dtype)) for p, t in recvs]
+        else:
+            hrecv = recvs
         ops = [self.dist.P2POp(self.dist.isend, t, peer, self.group) for peer, t in sends]
-        ops += [self.dist.P2POp(self.dist.irecv, t, peer, self.group) for peer, t in recvs]
+        ops += [self.dist.P2POp(self.dist.irecv, t, peer, self.group) for peer, t in hrecv]
         if ops:
             for w in self.dist.batch_isend_irecv(ops):
                 w.wait()
+        if self.staged:
+            for (_, dst), (_, h) in zip(recvs, hrecv):
+                dst.copy_(h)
+
+    def barrier(self) -> None:
+        self.dist.barrier(group=self.group)
 
     def close(self) -> None:
         pass
