@@ -164,10 +164,10 @@ class DistTransport:
     name = "nccl"
     distributed = True
 
-    def __init__(self, device=None, group=None):
+    def __init__(self, device=None, group=None, backend: str | None = None):
         import torch.distributed as dist
         if not dist.is_initialized():
-            backend = "nccl" if torch.cuda.is_available() else "gloo"
+            backend = backend or ("nccl" if torch.cuda.is_available() else "gloo")
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
             dist.init_process_group(backend=backend)
         self.dist = dist
@@ -225,7 +225,9 @@ def make_transport(name: str, nranks: int | None = None, device=None):
     device under torch.distributed).  Unknown names raise ValueError (ref:schwarz.py:174-179)."""
     if name in ("cuda", "serial", "threads"):
         return DeviceTransport(device)
-    if name in ("nccl", "gloo", "dist"):
+    if name in ("nccl", "gloo"):
+        return DistTransport(device, backend=name)
+    if name == "dist":
         return DistTransport(device)
     raise ValueError(f"unknown transport {name!r}")
 
