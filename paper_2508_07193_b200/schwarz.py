@@ -176,7 +176,7 @@ class DistTransport:
         self.rank = dist.get_rank(group)
         self.name = dist.get_backend(group)
         if device is None:
-            if self.name == "nccl":
+            if torch.cuda.is_available():
                 device = torch.device("cuda", int(os.environ.get("LOCAL_RANK", self.rank)) % torch.cuda.device_count())
             else:
                 device = torch.device("cpu")
