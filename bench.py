@@ -207,6 +207,22 @@ def run_ours(args):
     spmv_bytes = 48 * owned
     prec_tflops = flops_exec / t_prec / 1e12
 
+    # ---- per-phase breakdown of one extra step (reference categories, ref:instrument.py:17-25)
+    from paper_2508_07193_b200.instrument import PhaseTimer
+    timer = PhaseTimer()
+    solver.timer = timer
+    solver.op.timer = timer
+    solver.prec.timer = timer
+    torch.cuda.synchronize()
+    tb0 = time.perf_counter()
+    stepper.step()
+    torch.cuda.synchronize()
+    t_break = time.perf_counter() - tb0
+    breakdown = {k: round(v * 1e3, 3) for k, v in timer.seconds.items()}
+    breakdown["step_wall_ms"] = round(t_break * 1e3, 3)
+    from paper_2508_07193_b200.instrument import NULL_TIMER
+    solver.timer = solver.op.timer = solver.prec.timer = NULL_TIMER
+
     # ---- end-to-end through the public API: host fields in, host fields out, every step
     e2e = None
     if not args.no_e2e:
@@ -254,6 +270,7 @@ def run_ours(args):
                      "unit": "TFLOP/s", "frac": round(prec_tflops / peaks["fp64_tflops"], 3)
                      if peaks["fp64_tflops"] else None, "traffic": None,
                      "peak_source": peaks["fp64_source"], "flops_per_launch": flops_exec},
+        "breakdown_ms": breakdown,
         "gpu_launches": int(launches),
         "clocks": clocks.summary(),
         "e2e": e2e,
