@@ -482,7 +482,7 @@ constexpr int PX_ROWS = 36;          // plane buffer rows (DMMA row tile 4 reads
                                      // next buffer: finite data, discarded outputs)
 constexpr int PX_BUF = PX_ROWS * PXS;
 constexpr int PX_SLACK = 5 * PXS;    // after the last buffer (row tile 4 + the K-pad column overrun)
-constexpr int PW_WARPS = 8;          // warps per plane CTA, each independent
+constexpr int PW_WARPS = 12;         // warps per plane CTA, each independent (3 per SMSP)
 constexpr int CXS = 12;              // column tile row stride (8 columns + 4)
 constexpr int CXR = 36;              // column tile rows per component (pad4 of the max extent)
 constexpr int CX_BUF = 3 * CXR * CXS;  // one column tile (3 components)
@@ -541,28 +541,114 @@ struct FastPlaneArgs {
 
 // K1 (INV=false): plane k of S_i r -> Fy X Fx^T -> work;  K4 (INV=true): work plane -> Fy^T X Fx -> owned z
 // Every warp owns whole plane items and never waits on another warp.  The step-1 result T
-// overwrites the plane buffer in place (row m of T is written only after rows m of X were
-// consumed), so a warp needs just two 36x36 buffers and 8 warps (2 per SM sub-partition) fit.
+// overwrites the plane buffer in place (rows m of T are written only after rows m of X were
+// consumed), so a warp needs one 36x36 buffer and 12 warps (3 per SM sub-partition) fit; the
+// other warps of a sub-partition hide each warp's load latency.  Row/column tiles are taken
+// two at a time (10 independent DMMA chains, 0.7 fragment loads per DMMA).
+
+// step 1 for NM consecutive 8-row tiles starting at m0: T[rows][a] = sum_i X[rows][i] Fx[a][i]
+template <bool INV, int NM>
+__device__ __forceinline__ void plane_step1(const double* X, double* T, const double* Fx, int m0, int k4, int g,
+                                            int t) {
+  double acc[NM][5][2];
+#pragma unroll
+  for (int q = 0; q < NM; ++q)
+#pragma unroll
+    for (int n = 0; n < 5; ++n) acc[q][n][0] = acc[q][n][1] = 0.0;
+  const double* fb = INV ? Fx + t * FSM + g : Fx + g * FSM + t;
+  const double* xa = X + (m0 * 8 + g) * PXS + t;
+  for (int kk = 0; kk < k4; ++kk) {
+    double av[NM];
+#pragma unroll
+    for (int q = 0; q < NM; ++q) av[q] = xa[q * 8 * PXS + kk * 4];
+#pragma unroll
+    for (int n = 0; n < 5; ++n) {
+      const double bv = INV ? fb[kk * 4 * FSM + n * 8] : fb[n * 8 * FSM + kk * 4];
+#pragma unroll
+      for (int q = 0; q < NM; ++q) dmma884(acc[q][n][0], acc[q][n][1], av[q], bv);
+    }
+  }
+  __syncwarp();   // every lane has read these rows of X before they are overwritten
+#pragma unroll
+  for (int q = 0; q < NM; ++q) {
+    const int r = (m0 + q) * 8 + g;
+    if (r < PX_ROWS) {
+      double* tr = T + r * PXS + 2 * t;
+#pragma unroll
+      for (int n = 0; n < 5; ++n) {
+        if (n * 8 + 2 * t < PXS) {
+          tr[n * 8] = acc[q][n][0];
+          tr[n * 8 + 1] = acc[q][n][1];
+        }
+      }
+    }
+  }
+}
+
+// step 2 for NN consecutive 8-column tiles starting at n0: O[b][cols] = sum_j Fy[b][j] T[j][cols]
+template <bool INV, int NN>
+__device__ __forceinline__ void plane_step2(const double* T, const double* Fy, const FastPlaneArgs& A, const SubD& d,
+                                            int c, int kplane, int n0, int k4, int g, int t) {
+  double acc[NN][5][2];
+#pragma unroll
+  for (int q = 0; q < NN; ++q)
+#pragma unroll
+    for (int m = 0; m < 5; ++m) acc[q][m][0] = acc[q][m][1] = 0.0;
+  const double* fa = INV ? Fy + t * FSM + g : Fy + g * FSM + t;
+  const double* tb = T + t * PXS + n0 * 8 + g;
+  for (int kk = 0; kk < k4; ++kk) {
+    double bv[NN];
+#pragma unroll
+    for (int q = 0; q < NN; ++q) bv[q] = tb[kk * 4 * PXS + q * 8];
+#pragma unroll
+    for (int m = 0; m < 5; ++m) {
+      const double av = INV ? fa[kk * 4 * FSM + m * 8] : fa[m * 8 * FSM + kk * 4];
+#pragma unroll
+      for (int q = 0; q < NN; ++q) dmma884(acc[q][m][0], acc[q][m][1], av, bv[q]);
+    }
+  }
+  const int ex = d.ex, ey = d.ey;
+  const int64_t obase = INV ? 0 : d.ws_off + (int64_t)(c * d.ez + kplane) * d.ps;
+#pragma unroll
+  for (int m = 0; m < 5; ++m) {
+    const int row = m * 8 + g;
+    if (row >= ey) continue;
+#pragma unroll
+    for (int q = 0; q < NN; ++q)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int col = (n0 + q) * 8 + 2 * t + h;
+        if (col >= ex) continue;
+        if (!INV) {
+          A.dst[obase + row * ex + col] = acc[q][m][h];
+        } else {
+          const int jo = row - d.oy, io = col - d.ox;
+          if ((unsigned)jo < (unsigned)d.wy && (unsigned)io < (unsigned)d.wx)
+            A.dst[fidx(A.g, c, d.lz + d.oz + kplane, d.ly + row, d.lx + col)] = acc[q][m][h];
+        }
+      }
+  }
+}
+
 template <bool INV>
 __global__ void __launch_bounds__(PW_WARPS * 32, 1) k_plane_fast(FastPlaneArgs A) {
   extern __shared__ __align__(16) double smem[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
   load_resident(smem, A.et, A.factors, tid, blockDim.x);
-  double* wbase = smem + RES_WORDS + warp * 2 * PX_BUF;
-  for (int q = tid; q < PW_WARPS * 2 * PX_BUF + PX_SLACK; q += blockDim.x) smem[RES_WORDS + q] = 0.0;
+  double* T = smem + RES_WORDS + warp * PX_BUF;   // this warp's plane buffer (also the step-1 result)
+  for (int q = tid; q < PW_WARPS * PX_BUF + PX_SLACK; q += blockDim.x) smem[RES_WORDS + q] = 0.0;
   __syncthreads();
   const int gw = blockIdx.x * PW_WARPS + warp, nw = gridDim.x * PW_WARPS;
   const int per = (A.n_items + nw - 1) / nw;
   const int beg = gw * per, end = min(beg + per, A.n_items);
-  if (beg >= end) return;
 
   // returns the column shift of the plane data inside the buffer (16-byte superset loads);
   // no integer division in the copy loops (the XU pipe would become the bottleneck)
-  auto issue = [&](int it, int buf) -> int {
+  auto issue = [&](int it) -> int {
     const int4 w = A.items[it];
     const SubD d = load_sub(A.subs + w.x);
     const int c = w.y, ex = d.ex, ey = d.ey;
-    double* X = wbase + buf * PX_BUF;
+    double* X = T;
     if (INV || A.mode == FMP_SOLVE_FACES) {
       const int64_t P = (int64_t)ex * ey;
       const double* base = INV ? A.src + d.ws_off + (int64_t)(c * d.ez + d.oz + w.z) * d.ps
@@ -602,98 +688,29 @@ __global__ void __launch_bounds__(PW_WARPS * 32, 1) k_plane_fast(FastPlaneArgs A
     return 0;
   };
 
-  int buf = 0;
-  int shift_cur = issue(beg, 0);
-  cp_async_commit();
   for (int it = beg; it < end; ++it) {
-    int shift_next = 0;
-    if (it + 1 < end) shift_next = issue(it + 1, buf ^ 1);
+    const int shift = issue(it);
     cp_async_commit();
-    cp_async_wait<1>();
+    cp_async_wait<0>();
     __syncwarp();
     const int4 w = A.items[it];
     const SubD d = load_sub(A.subs + w.x);
-    const int c = w.y, ex = d.ex, ey = d.ey;
-    const double* Fx = res_factor(smem, A.et, c, 0, ex);
-    const double* Fy = res_factor(smem, A.et, c, 1, ey);
-    double* T = wbase + buf * PX_BUF;          // step-1 result, in place
-    const double* X = T + shift_cur;
+    const int c = w.y;
+    const double* Fx = res_factor(smem, A.et, c, 0, d.ex);
+    const double* Fy = res_factor(smem, A.et, c, 1, d.ey);
+    const double* X = T + shift;
+    const int k41 = pad4(d.ex) / 4, k42 = pad4(d.ey) / 4;
     // ---- step 1: T[j][a] = sum_i X[j][i] Fx[a][i]   (INV: T[b][i] = sum_a X[b][a] Fx[a][i])
-    {
-      const int k4 = pad4(ex) / 4;
-      const double* fb = INV ? Fx + t * FSM + g : Fx + g * FSM + t;
-#pragma unroll 1
-      for (int m = 0; m < 5; ++m) {
-        double acc[5][2];
-#pragma unroll
-        for (int n = 0; n < 5; ++n) acc[n][0] = acc[n][1] = 0.0;
-        const double* xa = X + (m * 8 + g) * PXS + t;
-        for (int kk = 0; kk < k4; ++kk) {
-          const double av = xa[kk * 4];
-#pragma unroll
-          for (int n = 0; n < 5; ++n) {
-            const double bv = INV ? fb[kk * 4 * FSM + n * 8] : fb[n * 8 * FSM + kk * 4];
-            dmma884(acc[n][0], acc[n][1], av, bv);
-          }
-        }
-        __syncwarp();   // every lane has read rows m*8.. of X before they are overwritten
-        const int r = m * 8 + g;
-        if (r < PX_ROWS) {
-          double* tr = T + r * PXS + 2 * t;
-#pragma unroll
-          for (int n = 0; n < 5; ++n) {
-            if (n * 8 + 2 * t < PXS) {
-              tr[n * 8] = acc[n][0];
-              tr[n * 8 + 1] = acc[n][1];
-            }
-          }
-        }
-      }
-    }
+    plane_step1<INV, 2>(X, T, Fx, 0, k41, g, t);
+    plane_step1<INV, 2>(X, T, Fx, 2, k41, g, t);
+    plane_step1<INV, 1>(X, T, Fx, 4, k41, g, t);
     __syncwarp();
     // ---- step 2: O[b][a] = sum_j Fy[b][j] T[j][a]   (INV: O[j][i] = sum_b Fy[b][j] T[b][i])
-    {
-      const int k4 = pad4(ey) / 4;
-      const double* fa = INV ? Fy + t * FSM + g : Fy + g * FSM + t;
-      const double* tb = T + t * PXS + g;
-      const int64_t obase = INV ? 0 : d.ws_off + (int64_t)(c * d.ez + w.z) * d.ps;
-#pragma unroll 1
-      for (int n = 0; n < 5; ++n) {
-        double acc[5][2];
-#pragma unroll
-        for (int m = 0; m < 5; ++m) acc[m][0] = acc[m][1] = 0.0;
-        for (int kk = 0; kk < k4; ++kk) {
-          const double bv = tb[kk * 4 * PXS + n * 8];
-#pragma unroll
-          for (int m = 0; m < 5; ++m) {
-            const double av = INV ? fa[kk * 4 * FSM + m * 8] : fa[m * 8 * FSM + kk * 4];
-            dmma884(acc[m][0], acc[m][1], av, bv);
-          }
-        }
-#pragma unroll
-        for (int m = 0; m < 5; ++m) {
-          const int row = m * 8 + g;
-          if (row >= ey) continue;
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int col = n * 8 + 2 * t + h;
-            if (col >= ex) continue;
-            if (!INV) {
-              A.dst[obase + row * ex + col] = acc[m][h];
-            } else {
-              const int jo = row - d.oy, io = col - d.ox;
-              if ((unsigned)jo < (unsigned)d.wy && (unsigned)io < (unsigned)d.wx)
-                A.dst[fidx(A.g, c, d.lz + d.oz + w.z, d.ly + row, d.lx + col)] = acc[m][h];
-            }
-          }
-        }
-      }
-    }
+    plane_step2<INV, 2>(T, Fy, A, d, c, w.z, 0, k42, g, t);
+    plane_step2<INV, 2>(T, Fy, A, d, c, w.z, 2, k42, g, t);
+    plane_step2<INV, 1>(T, Fy, A, d, c, w.z, 4, k42, g, t);
     __syncwarp();
-    shift_cur = shift_next;
-    buf ^= 1;
   }
-  cp_async_wait<0>();
 }
 
 struct FastColArgs {
@@ -1113,7 +1130,7 @@ static void free_plan(fmp_precond* p) {
   delete p;
 }
 
-constexpr int kPlaneFastSmem = (RES_WORDS + PW_WARPS * 2 * PX_BUF + PX_SLACK) * (int)sizeof(double);
+constexpr int kPlaneFastSmem = (RES_WORDS + PW_WARPS * PX_BUF + PX_SLACK) * (int)sizeof(double);
 constexpr int kColFastSmem = (RES_WORDS + CW_WARPS * 2 * CX_BUF) * (int)sizeof(double);
 
 static int plane_nt(const fmp_precond* p) { return std::max(p->max_ex, p->max_ey) <= 40 ? 5 : 9; }
