@@ -486,7 +486,7 @@ constexpr int PW_WARPS = 12;         // warps per plane CTA, each independent (3
 constexpr int CXS = 12;              // column tile row stride (8 columns + 4)
 constexpr int CXR = 36;              // column tile rows per component (pad4 of the max extent)
 constexpr int CX_BUF = 3 * CXR * CXS;  // one column tile (3 components)
-constexpr int CW_WARPS = 8;
+constexpr int CW_WARPS = 12;
 constexpr int FAST_MAX_EXT = CXR;    // the fast path serves plans whose extents are all <= 36
 
 struct ExtTable {
@@ -732,21 +732,21 @@ __global__ void __launch_bounds__(CW_WARPS * 32, 1) k_column_fast(FastColArgs A)
   extern __shared__ __align__(16) double smem[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
   load_resident(smem, A.et, A.factors, tid, blockDim.x);
-  double* wbase = smem + RES_WORDS + warp * 2 * CX_BUF;
-  for (int q = lane; q < 2 * CX_BUF; q += 32) wbase[q] = 0.0;
+  double* wbase = smem + RES_WORDS + warp * CX_BUF;   // single-buffered: 3 warps per SMSP hide the loads
+  for (int q = lane; q < CX_BUF; q += 32) wbase[q] = 0.0;
   __syncthreads();
   const int gw = blockIdx.x * CW_WARPS + warp, nw = gridDim.x * CW_WARPS;
   const int per = (A.n_items + nw - 1) / nw;
   const int beg = gw * per, end = min(beg + per, A.n_items);
   if (beg >= end) return;
 
-  auto issue = [&](int it, int buf) {
+  auto issue = [&](int it) {
     const int2 w = A.items[it];
     const SubD d = load_sub(A.subs + w.x);
     const int P = d.ex * d.ey, ez = d.ez;
     const int64_t V = d.cstride();
     const double* src = A.src + d.ws_off + w.y;
-    double* X = wbase + buf * CX_BUF;
+    double* X = wbase;
     if (w.y + 8 <= d.ps) {   // 4 aligned 16-byte chunks per row (ps, ws_off, p0 all multiples of 4/8)
       const int ch = lane & 3;
       for (int cc = 0; cc < 3; ++cc)
@@ -761,19 +761,16 @@ __global__ void __launch_bounds__(CW_WARPS * 32, 1) k_column_fast(FastColArgs A)
     }
   };
 
-  int buf = 0;
-  issue(beg, 0);
-  cp_async_commit();
   for (int it = beg; it < end; ++it) {
-    if (it + 1 < end) issue(it + 1, buf ^ 1);
+    issue(it);
     cp_async_commit();
-    cp_async_wait<1>();
+    cp_async_wait<0>();
     __syncwarp();
     const int2 w = A.items[it];
     const SubD d = load_sub(A.subs + w.x);
     const int ex = d.ex, ey = d.ey, ez = d.ez, P = ex * ey, p0 = w.y;
     const int64_t V = d.cstride();
-    double* X = wbase + buf * CX_BUF;
+    double* X = wbase;
     const double* Fv = res_factor(smem, A.et, 0, 2, ez);   // V^T_z (components x, y)
     const double* Fu = res_factor(smem, A.et, 2, 2, ez);   // U^T_z (component z)
     const double* Sx = res_sigma(smem, A.et, ex);
@@ -862,9 +859,7 @@ __global__ void __launch_bounds__(CW_WARPS * 32, 1) k_column_fast(FastColArgs A)
       }
     }
     __syncwarp();
-    buf ^= 1;
   }
-  cp_async_wait<0>();
 }
 
 // ---------------------------------------------------------------- K5 / K6: boundary faces
@@ -1131,7 +1126,7 @@ static void free_plan(fmp_precond* p) {
 }
 
 constexpr int kPlaneFastSmem = (RES_WORDS + PW_WARPS * PX_BUF + PX_SLACK) * (int)sizeof(double);
-constexpr int kColFastSmem = (RES_WORDS + CW_WARPS * 2 * CX_BUF) * (int)sizeof(double);
+constexpr int kColFastSmem = (RES_WORDS + CW_WARPS * CX_BUF) * (int)sizeof(double);
 
 static int plane_nt(const fmp_precond* p) { return std::max(p->max_ex, p->max_ey) <= 40 ? 5 : 9; }
 static int column_mt(const fmp_precond* p) { return pad8(p->max_ez) / 8; }
