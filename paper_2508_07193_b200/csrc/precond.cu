@@ -486,7 +486,8 @@ constexpr int PW_WARPS = 12;         // warps per plane CTA, each independent (3
 constexpr int CXS = 12;              // column tile row stride (8 columns + 4)
 constexpr int CXR = 36;              // column tile rows per component (pad4 of the max extent)
 constexpr int CX_BUF = 3 * CXR * CXS;  // one column tile (3 components)
-constexpr int CW_WARPS = 12;
+constexpr int CW_WARPS = 12;         // single-buffered inverse pass
+constexpr int CW_WARPS_DB = 8;       // double-buffered forward pass
 constexpr int FAST_MAX_EXT = CXR;    // the fast path serves plans whose extents are all <= 36
 
 struct ExtTable {
@@ -862,6 +863,147 @@ __global__ void __launch_bounds__(CW_WARPS * 32, 1) k_column_fast(FastColArgs A)
   }
 }
 
+// double-buffered variant (forward pass: no correction phase to overlap)
+template <bool INV>
+__global__ void __launch_bounds__(CW_WARPS_DB * 32, 1) k_column_fast_db(FastColArgs A) {
+  extern __shared__ __align__(16) double smem[];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
+  load_resident(smem, A.et, A.factors, tid, blockDim.x);
+  double* wbase = smem + RES_WORDS + warp * 2 * CX_BUF;
+  for (int q = lane; q < 2 * CX_BUF; q += 32) wbase[q] = 0.0;
+  __syncthreads();
+  const int gw = blockIdx.x * CW_WARPS_DB + warp, nw = gridDim.x * CW_WARPS_DB;
+  const int per = (A.n_items + nw - 1) / nw;
+  const int beg = gw * per, end = min(beg + per, A.n_items);
+  if (beg >= end) return;
+
+  auto issue = [&](int it, int buf) {
+    const int2 w = A.items[it];
+    const SubD d = load_sub(A.subs + w.x);
+    const int P = d.ex * d.ey, ez = d.ez;
+    const int64_t V = d.cstride();
+    const double* src = A.src + d.ws_off + w.y;
+    double* X = wbase + buf * CX_BUF;
+    if (w.y + 8 <= d.ps) {   // 4 aligned 16-byte chunks per row (ps, ws_off, p0 all multiples of 4/8)
+      const int ch = lane & 3;
+      for (int cc = 0; cc < 3; ++cc)
+        for (int k = lane >> 2; k < ez; k += 8)
+          cp_async16(X + (cc * CXR + k) * CXS + 2 * ch, src + cc * V + (int64_t)k * d.ps + 2 * ch);
+    } else {
+      const int col = lane & 7;
+      for (int cc = 0; cc < 3; ++cc)
+        for (int k = lane >> 3; k < ez; k += 4)
+          cp_async8(X + (cc * CXR + k) * CXS + col, w.y + col < P ? src + cc * V + (int64_t)k * d.ps + col : nullptr,
+                    A.factors);
+    }
+  };
+
+  int buf = 0;
+  issue(beg, 0);
+  cp_async_commit();
+  for (int it = beg; it < end; ++it) {
+    if (it + 1 < end) issue(it + 1, buf ^ 1);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncwarp();
+    const int2 w = A.items[it];
+    const SubD d = load_sub(A.subs + w.x);
+    const int ex = d.ex, ey = d.ey, ez = d.ez, P = ex * ey, p0 = w.y;
+    const int64_t V = d.cstride();
+    double* X = wbase + buf * CX_BUF;
+    const double* Fv = res_factor(smem, A.et, 0, 2, ez);   // V^T_z (components x, y)
+    const double* Fu = res_factor(smem, A.et, 2, 2, ez);   // U^T_z (component z)
+    const double* Sx = res_sigma(smem, A.et, ex);
+    const double* Sy = res_sigma(smem, A.et, ey);
+    const double* Sz = res_sigma(smem, A.et, ez);
+    if (INV && A.corr) {
+      // y^ -= B^-1 (G Q Z): two rank-structured face terms per component (K6)
+      const double* cb = A.corr + (int64_t)w.x * 6 * A.pmax * A.pmax;
+      const int pm = A.pmax, pm2 = pm * pm;
+      const double* Vx = res_factor(smem, A.et, 1, 0, ex);   // V^T_x
+      const double* Vy = res_factor(smem, A.et, 0, 1, ey);   // V^T_y
+      const int col = lane & 7, p = p0 + col;
+      if (p < P) {
+        const int b0 = p0 / ex;
+        int b = b0, a = p - b0 * ex;
+        while (a >= ex) { a -= ex; ++b; }
+        const double vy0 = Vy[b * FSM], vx0 = Vx[a * FSM], sx = Sx[a], sy = Sy[b];
+        const double gx = cb[0 * pm2 + b * pm + a], gy = cb[2 * pm2 + b * pm + a];
+        for (int cz = lane >> 3; cz < ez; cz += 4) {
+          const double vz0 = Fv[cz * FSM];
+          const double dx = vz0 * gx + vy0 * cb[1 * pm2 + cz * pm + a];
+          const double dy = vz0 * gy + vx0 * cb[3 * pm2 + cz * pm + b];
+          const double dz = vy0 * cb[4 * pm2 + cz * pm + a] + vx0 * cb[5 * pm2 + cz * pm + b];
+          const double sz = Sz[cz];
+          const double q = __drcp_rn(1.0 + A.alpha * (sx * sx + sy * sy + sz * sz));
+          const double pr = A.alpha * (sx * dx + sy * dy + sz * dz);
+          X[(0 * CXR + cz) * CXS + col] -= q * (dx + pr * sx);
+          X[(1 * CXR + cz) * CXS + col] -= q * (dy + pr * sy);
+          X[(2 * CXR + cz) * CXS + col] -= q * (dz + pr * sz);
+        }
+      }
+      __syncwarp();
+    }
+    const int k4 = pad4(ez) / 4;
+    double acc[3][5][2];
+#pragma unroll
+    for (int cc = 0; cc < 3; ++cc)
+#pragma unroll
+      for (int m = 0; m < 5; ++m) acc[cc][m][0] = acc[cc][m][1] = 0.0;
+    const double* xb = X + t * CXS + g;
+    const double* fv = INV ? Fv + t * FSM + g : Fv + g * FSM + t;
+    const double* fu = INV ? Fu + t * FSM + g : Fu + g * FSM + t;
+    for (int kk = 0; kk < k4; ++kk) {
+      const double b0 = xb[(0 * CXR + kk * 4) * CXS];
+      const double b1 = xb[(1 * CXR + kk * 4) * CXS];
+      const double b2 = xb[(2 * CXR + kk * 4) * CXS];
+#pragma unroll
+      for (int m = 0; m < 5; ++m) {
+        const double av = INV ? fv[kk * 4 * FSM + m * 8] : fv[m * 8 * FSM + kk * 4];
+        const double au = INV ? fu[kk * 4 * FSM + m * 8] : fu[m * 8 * FSM + kk * 4];
+        dmma884(acc[0][m][0], acc[0][m][1], av, b0);
+        dmma884(acc[1][m][0], acc[1][m][1], av, b1);
+        dmma884(acc[2][m][0], acc[2][m][1], au, b2);
+      }
+    }
+    double* dst = A.dst + d.ws_off;
+    const int b0 = p0 / ex;   // one division per item; the 8 columns advance b a few times at most
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int p = p0 + 2 * t + h;
+      if (p >= P) continue;
+      double sx = 0.0, sy = 0.0;
+      if (!INV) {
+        int b = b0, a = p - b0 * ex;
+        while (a >= ex) { a -= ex; ++b; }
+        sx = Sx[a];
+        sy = Sy[b];
+      }
+#pragma unroll
+      for (int m = 0; m < 5; ++m) {
+        const int r = m * 8 + g;
+        if (r >= ez) continue;
+        double y0 = acc[0][m][h], y1 = acc[1][m][h], y2 = acc[2][m][h];
+        if (!INV) {  // B^-1 y = q (y + alpha s (s . y)), q = 1/(1 + alpha |s|^2)  (ref:subdomain.py:145-153)
+          const double sz = Sz[r];
+          const double q = __drcp_rn(1.0 + A.alpha * (sx * sx + sy * sy + sz * sz));
+          const double pr = A.alpha * (sx * y0 + sy * y1 + sz * y2);
+          y0 = q * (y0 + pr * sx);
+          y1 = q * (y1 + pr * sy);
+          y2 = q * (y2 + pr * sz);
+        }
+        const int64_t o = (int64_t)r * d.ps + p;
+        dst[o] = y0;
+        dst[V + o] = y1;
+        dst[2 * V + o] = y2;
+      }
+    }
+    __syncwarp();
+    buf ^= 1;
+  }
+  cp_async_wait<0>();
+}
+
 // ---------------------------------------------------------------- K5 / K6: boundary faces
 // Component c has two boundary faces with nonzero delta (ref:operators.py:151-164):
 //   c = x: z-normal (k = 0, all j,i) and y-normal (j = 0, k >= 1)
@@ -1127,6 +1269,7 @@ static void free_plan(fmp_precond* p) {
 
 constexpr int kPlaneFastSmem = (RES_WORDS + PW_WARPS * PX_BUF + PX_SLACK) * (int)sizeof(double);
 constexpr int kColFastSmem = (RES_WORDS + CW_WARPS * CX_BUF) * (int)sizeof(double);
+constexpr int kColFastSmemDb = (RES_WORDS + CW_WARPS_DB * 2 * CX_BUF) * (int)sizeof(double);
 
 static int plane_nt(const fmp_precond* p) { return std::max(p->max_ex, p->max_ey) <= 40 ? 5 : 9; }
 static int column_mt(const fmp_precond* p) { return pad8(p->max_ez) / 8; }
@@ -1278,6 +1421,7 @@ extern "C" int fmp_precond_create(const fmp_precond_desc* desc, fmp_precond** ou
   cudaFuncSetAttribute(k_plane_fast<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kPlaneFastSmem);
   cudaFuncSetAttribute(k_column_fast<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kColFastSmem);
   cudaFuncSetAttribute(k_column_fast<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kColFastSmem);
+  cudaFuncSetAttribute(k_column_fast_db<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kColFastSmemDb);
   cudaFuncSetAttribute(k_faces, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   cudaFuncSetAttribute(k_corr, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   FMP_CHECK_CUDA(cudaGetLastError());
@@ -1304,11 +1448,13 @@ static int column_pass(fmp_precond* p, bool inv, const double* src, double* dst,
     a.pmax = (int)p->d.pmax;
     a.alpha = p->d.alpha;
     a.et = p->et;
-    const int grid = std::min(p->sms, (p->n_fcol + CW_WARPS - 1) / CW_WARPS);
-    if (inv)
+    if (inv) {
+      const int grid = std::min(p->sms, (p->n_fcol + CW_WARPS - 1) / CW_WARPS);
       k_column_fast<true><<<grid, CW_WARPS * 32, kColFastSmem, st>>>(a);
-    else
-      k_column_fast<false><<<grid, CW_WARPS * 32, kColFastSmem, st>>>(a);
+    } else {
+      const int grid = std::min(p->sms, (p->n_fcol + CW_WARPS_DB - 1) / CW_WARPS_DB);
+      k_column_fast_db<false><<<grid, CW_WARPS_DB * 32, kColFastSmemDb, st>>>(a);
+    }
     FMP_CHECK_LAUNCH();
     return 0;
   }
