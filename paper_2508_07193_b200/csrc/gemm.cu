@@ -22,7 +22,7 @@ struct GemmTile {
   int shape, i0, n0, pad;
 };
 
-constexpr int KC = 16;        // K chunk per stage
+constexpr int KC = 32;        // K chunk per stage
 constexpr int GS = KC + 4;    // smem row stride (== 4 mod 8: conflict-free fragment loads)
 
 template <int WM, int WN, int NWM, int NWN, int STAGES>
@@ -119,13 +119,13 @@ __global__ void __launch_bounds__(32 * NWM * NWN)
 // tile configurations: wide (n >= 48): 96 x 72 CTAs, two per SM; narrow (16 < n < 48) and
 // skinny (n <= 16) are C^-1-streaming (memory-bound) products: one-warp 32-row CTAs so that
 // every SM streams several row panels at once.
-using CfgWide = GemmCfg<4, 3, 3, 3, 4>;    //  96 x 72, 9 warps
+using CfgWide = GemmCfg<4, 3, 3, 3, 3>;    //  96 x 72, 9 warps
 using CfgNarrow = GemmCfg<4, 3, 1, 1, 4>;  //  32 x 24, 1 warp
 using CfgSkinny = GemmCfg<4, 1, 1, 1, 4>;  //  32 x  8, 1 warp
-constexpr int kCtasPerSm[3] = {2, 8, 8};
+constexpr int kCtasPerSm[3] = {1, 8, 8};
 
 int gemm_setup() {
-  FMP_CHECK_CUDA(cudaFuncSetAttribute(k_gemm<4, 3, 3, 3, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  FMP_CHECK_CUDA(cudaFuncSetAttribute(k_gemm<4, 3, 3, 3, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)CfgWide::smem));
   FMP_CHECK_CUDA(cudaFuncSetAttribute(k_gemm<4, 3, 1, 1, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)CfgNarrow::smem));
@@ -144,7 +144,7 @@ int gemm_launch(int cfg, const GemmShape* shapes, const GemmTile* tiles, int n_t
   const int slots = kCtasPerSm[cfg] * sms;
   const int grid = n_tiles < slots ? n_tiles : slots;
   if (cfg == 0)
-    k_gemm<4, 3, 3, 3, 4><<<grid, 32 * CfgWide::WARPS, CfgWide::smem, st>>>(shapes, tiles, n_tiles);
+    k_gemm<4, 3, 3, 3, 3><<<grid, 32 * CfgWide::WARPS, CfgWide::smem, st>>>(shapes, tiles, n_tiles);
   else if (cfg == 1)
     k_gemm<4, 3, 1, 1, 4><<<grid, 32 * CfgNarrow::WARPS, CfgNarrow::smem, st>>>(shapes, tiles, n_tiles);
   else

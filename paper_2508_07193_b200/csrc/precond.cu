@@ -1039,6 +1039,7 @@ struct FaceArgs {
   double* const* ymat;         // device array of per-shape Y pointers (K5 out)
   const double* const* zmat;   // device array of per-shape Z pointers (K6 in)
   int pmax;
+  int max_ps;                  // largest padded plane stride of the plan
 };
 
 __device__ __forceinline__ int ext_of(const SubD& d, int a) { return a == 0 ? d.ex : (a == 1 ? d.ey : d.ez); }
@@ -1074,19 +1075,34 @@ __global__ void __launch_bounds__(FACE_THREADS) k_faces(FaceArgs A) {
   const double* Wy = sF + 1 * pm2;
   const double* Wx = sF;
   const double* src = A.yhat + d.ws_off + (int64_t)c * d.cstride();
-  const int nz = max(1, min(ez, FACE_CHUNK / P));
-  for (int c0 = 0; c0 < ez; c0 += nz) {
-    const int n = min(nz, ez - c0);
-    __syncthreads();
+  // two staging buffers of FACE_CHUNK/2 doubles: chunk i+1 streams in (16-byte cp.async of the
+  // 32-byte aligned, padded workspace planes) while chunk i is reduced
+  const int stage = max(FACE_CHUNK / 2, A.max_ps);
+  const int nz = max(1, min(ez, stage / d.ps));
+  const int nchunks = (ez + nz - 1) / nz;
+  auto issue = [&](int ci) {
+    const int c0 = ci * nz, n = min(nz, ez - c0);
+    double* buf = sC + (ci & 1) * stage;
+    const int half = d.ps / 2;   // 16-byte chunks per padded plane
     for (int kk = 0; kk < n; ++kk)
-      for (int q = tid; q < P; q += FACE_THREADS) cp_async8(sC + kk * P + q, src + (int64_t)(c0 + kk) * d.ps + q, src);
+      for (int q = tid; q < half; q += FACE_THREADS)
+        cp_async16(buf + kk * d.ps + 2 * q, src + (int64_t)(c0 + kk) * d.ps + 2 * q);
+  };
+  issue(0);
+  cp_async_commit();
+  for (int ci = 0; ci < nchunks; ++ci) {
+    const int c0 = ci * nz, n = min(nz, ez - c0);
+    __syncthreads();   // buffer (ci+1)&1 is no longer read
+    if (ci + 1 < nchunks) issue(ci + 1);
     cp_async_commit();
-    cp_async_wait<0>();
+    cp_async_wait<1>();
     __syncthreads();
+    const double* chunk = sC + (ci & 1) * stage;
+    const int P2 = d.ps;   // staged plane stride
     if (fg.n1 == 2) {   // components x, y: z-normal face, sA[b][a] += sum_cz w[cz] y^[cz][b][a]
       for (int q = tid; q < P; q += FACE_THREADS) {
         double acc = sA[q];
-        for (int kk = 0; kk < n; ++kk) acc += Wz[(c0 + kk) * ez] * sC[kk * P + q];
+        for (int kk = 0; kk < n; ++kk) acc += Wz[(c0 + kk) * ez] * chunk[kk * P2 + q];
         sA[q] = acc;
       }
     }
@@ -1096,7 +1112,7 @@ __global__ void __launch_bounds__(FACE_THREADS) k_faces(FaceArgs A) {
       for (int q = tid; q < n * ex; q += FACE_THREADS) {
         const int kk = q / ex, a = q - kk * ex;
         double acc = 0.0;
-        for (int b = 0; b < ey; ++b) acc += Wy[b * ey] * sC[kk * P + b * ex + a];
+        for (int b = 0; b < ey; ++b) acc += Wy[b * ey] * chunk[kk * P2 + b * ex + a];
         dst[(c0 + kk) * ex + a] = acc;
       }
     }
@@ -1105,7 +1121,7 @@ __global__ void __launch_bounds__(FACE_THREADS) k_faces(FaceArgs A) {
       for (int q = tid; q < n * ey; q += FACE_THREADS) {
         const int kk = q / ey, b = q - kk * ey;
         double acc = 0.0;
-        const double* row = sC + kk * P + b * ex;
+        const double* row = chunk + kk * P2 + b * ex;
         for (int a = 0; a < ex; ++a) acc += Wx[a * ex] * row[a];
         sB[(c0 + kk) * ey + b] = acc;
       }
@@ -1538,9 +1554,10 @@ extern "C" int fmp_precond_apply(fmp_precond* p, const fmp_block* blk, int mode,
   if (int e = plane_pass(p, blk, false, mode, r, wa, st)) return e;
   if (int e = column_pass(p, false, wa, wb, nullptr, st)) return e;
   const int pm = (int)p->d.pmax;
-  FaceArgs fa{p->d.subs, p->d.shapes, p->d.factors, wb, p->d.corr, p->d_ymat, p->d_zmat, pm};
+  FaceArgs fa{p->d.subs, p->d.shapes, p->d.factors, wb, p->d.corr, p->d_ymat, p->d_zmat, pm, (p->max_p + 3) & ~3};
   if (mode != FMP_SOLVE_EXACT) {
-    const size_t fs = (6 * (size_t)pm * pm + std::max<size_t>(FACE_CHUNK, (size_t)p->max_p)) * sizeof(double);
+    const size_t stage = std::max<size_t>(FACE_CHUNK / 2, (size_t)((p->max_p + 3) & ~3));
+    const size_t fs = (6 * (size_t)pm * pm + 2 * stage) * sizeof(double);
     k_faces<<<dim3(3, (unsigned)p->d.n_sub), FACE_THREADS, fs, st>>>(fa);
     FMP_CHECK_LAUNCH();
   }
