@@ -42,6 +42,28 @@ int gemm_tile_m(int cfg);
 int gemm_tile_n(int cfg);
 int gemm_launch(int cfg, const GemmShape* shapes, const GemmTile* tiles, int n_tiles, int sms, cudaStream_t st);
 
+// ozaki.cu
+struct OzShape {
+  const int8_t* A;
+  const int* eA;
+  const int8_t* B;
+  const int* eB;
+  double* Z;
+  int m, n, ld, kchunks;
+};
+struct OzTile {
+  int shape, mt, nt, pad;
+};
+int ozaki_setup();
+int ozaki_slice_a(const double* cinv, int m, int ld, int kchunks, int8_t* dst, int* exps, cudaStream_t st);
+int ozaki_slice_b(const double* y, int n, int m, int ld, int kchunks, int8_t* dst, int* exps, cudaStream_t st);
+size_t ozaki_a_bytes(int m, int kchunks);
+size_t ozaki_b_bytes(int n, int kchunks);
+int ozaki_kchunks(int m);
+int ozaki_tile_m();
+int ozaki_tile_n();
+int ozaki_launch(const OzShape* shapes, const OzTile* tiles, int n_tiles, int sms, cudaStream_t st);
+
 __host__ __device__ constexpr int pad8(int n) { return (n + 7) & ~7; }
 __host__ __device__ constexpr int pad4(int n) { return (n + 3) & ~3; }
 // Row stride (doubles) for an operand with pad8(n) columns: == 4 (mod 8) so the
@@ -1239,6 +1261,13 @@ struct fmp_precond {
   int n_ffwd = 0, n_finv = 0, n_fcol = 0;
   // Woodbury GEMM: own DMMA kernel (default) or cuBLAS (FMP_GEMM=cublas)
   bool use_cublas = true;
+  // Ozaki INT8 tensor-core GEMM (FMP_GEMM=ozaki): int8 slices of C^-1 built once, Y sliced per apply
+  bool use_ozaki = false;
+  std::vector<int8_t*> oz_a, oz_b;
+  std::vector<int*> oz_ea, oz_eb;
+  OzShape* d_ozshapes = nullptr;
+  OzTile* d_oztiles = nullptr;
+  int n_oztiles = 0;
   static constexpr int kAux = 4;          // concurrent GEMM streams (small shapes are HBM-bound)
   cudaStream_t aux[kAux] = {};
   cublasHandle_t aux_blas[kAux] = {};
@@ -1279,6 +1308,12 @@ static void free_plan(fmp_precond* p) {
     if (p->ev_join[q]) cudaEventDestroy(p->ev_join[q]);
   }
   if (p->ev_fork) cudaEventDestroy(p->ev_fork);
+  for (auto* q : p->oz_a) cudaFree(q);
+  for (auto* q : p->oz_b) cudaFree(q);
+  for (auto* q : p->oz_ea) cudaFree(q);
+  for (auto* q : p->oz_eb) cudaFree(q);
+  cudaFree(p->d_ozshapes);
+  cudaFree(p->d_oztiles);
   for (int c = 0; c < 3; ++c) cudaFree(p->d_gtiles[c]);
   delete p;
 }
@@ -1386,7 +1421,9 @@ extern "C" int fmp_precond_create(const fmp_precond_desc* desc, fmp_precond** ou
   }
   {  // grouped GEMM tables: one shape record per extended shape, tiles bucketed by configuration
     const char* gm = getenv("FMP_GEMM");
-    p->use_cublas = !(gm && std::string(gm) == "own");
+    const std::string gmode = gm ? gm : "cublas";
+    p->use_cublas = gmode == "cublas";
+    p->use_ozaki = gmode == "ozaki";
     std::vector<GemmShape> gs;
     std::vector<GemmTile> gt[3];
     for (int64_t s2 = 0; s2 < desc->n_shape; ++s2) {
@@ -1404,6 +1441,34 @@ extern "C" int fmp_precond_create(const fmp_precond_desc* desc, fmp_precond** ou
       return -1;
     }
     for (int c = 0; c < 3; ++c) p->n_gtiles[c] = (int)gt[c].size();
+  }
+  if (p->use_ozaki && desc->alpha != 0.0) {   // slices of C^-1 (setup), buffers for the slices of Y
+    if (ozaki_setup()) { free_plan(p); return -1; }
+    std::vector<OzShape> os;
+    std::vector<OzTile> ot;
+    for (int64_t s2 = 0; s2 < desc->n_shape; ++s2) {
+      const auto& sh = p->shapes[s2];
+      const int m = (int)sh.m, n = (int)(p->first[s2 + 1] - p->first[s2]), kc = ozaki_kchunks(m);
+      int8_t *a = nullptr, *b = nullptr;
+      int *ea = nullptr, *eb = nullptr;
+      const size_t ab = ozaki_a_bytes(m, kc), bb = ozaki_b_bytes(std::max(n, 1), kc);
+      if (cudaMalloc(&a, ab) != cudaSuccess || cudaMalloc(&b, bb) != cudaSuccess ||
+          cudaMalloc(&ea, sizeof(int) * m) != cudaSuccess || cudaMalloc(&eb, sizeof(int) * std::max(n, 1)) != cudaSuccess) {
+        free_plan(p);
+        FMP_REQUIRE(false, "cudaMalloc of Ozaki slices failed");
+      }
+      p->oz_a.push_back(a);
+      p->oz_b.push_back(b);
+      p->oz_ea.push_back(ea);
+      p->oz_eb.push_back(eb);
+      if (ozaki_slice_a(p->cinv[s2], m, (int)sh.ld, kc, a, ea, 0)) { free_plan(p); return -1; }
+      os.push_back(OzShape{a, ea, b, eb, p->zmat[s2], m, n, (int)sh.ld, kc});
+      for (int mt = 0; mt * ozaki_tile_m() < m; ++mt)
+        for (int nt = 0; nt * ozaki_tile_n() < n; ++nt) ot.push_back(OzTile{(int)s2, mt, nt, 0});
+    }
+    if (upload(os, &p->d_ozshapes) || upload(ot, &p->d_oztiles)) { free_plan(p); return -1; }
+    p->n_oztiles = (int)ot.size();
+    FMP_CHECK_CUDA(cudaDeviceSynchronize());
   }
   if (cublasCreate(&p->blas) != CUBLAS_STATUS_SUCCESS) {
     free_plan(p);
@@ -1583,6 +1648,15 @@ extern "C" int fmp_precond_apply(fmp_precond* p, const fmp_block* blk, int mode,
         FMP_CHECK_CUDA(cudaEventRecord(p->ev_join[q], p->aux[q]));
         FMP_CHECK_CUDA(cudaStreamWaitEvent(st, p->ev_join[q], 0));
       }
+    } else if (p->use_ozaki) {
+      for (int64_t s2 = 0; s2 < p->d.n_shape; ++s2) {
+        const int m = (int)p->shapes[s2].m, n = (int)(p->first[s2 + 1] - p->first[s2]);
+        if (n == 0) continue;
+        if (int e = ozaki_slice_b(p->ymat[s2], n, m, (int)p->shapes[s2].ld, ozaki_kchunks(m), p->oz_b[s2],
+                                  p->oz_eb[s2], st))
+          return e;
+      }
+      if (int e = ozaki_launch(p->d_ozshapes, p->d_oztiles, p->n_oztiles, p->sms, st)) return e;
     } else {
       for (int c = 0; c < 3; ++c)
         if (int e = gemm_launch(c, p->d_gshapes, p->d_gtiles[c], p->n_gtiles[c], p->sms, st)) return e;

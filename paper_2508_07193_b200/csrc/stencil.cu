@@ -14,7 +14,6 @@
 
 namespace fmp {
 
-constexpr int SX = 32, SY = 4, SZ = 8;  // tile: 32 x 4 threads, each marching 8 planes in z
 
 template <bool GEN>
 struct Loader {
