@@ -1442,7 +1442,9 @@ extern "C" int fmp_precond_create(const fmp_precond_desc* desc, fmp_precond** ou
     }
     for (int c = 0; c < 3; ++c) p->n_gtiles[c] = (int)gt[c].size();
   }
-  if (p->use_ozaki && desc->alpha != 0.0) {   // slices of C^-1 (setup), buffers for the slices of Y
+  bool have_cinv = desc->alpha != 0.0;
+  for (const double* c : p->cinv) have_cinv = have_cinv && c != nullptr;
+  if (p->use_ozaki && have_cinv) {   // slices of C^-1 (setup), buffers for the slices of Y
     if (ozaki_setup()) { free_plan(p); return -1; }
     std::vector<OzShape> os;
     std::vector<OzTile> ot;
@@ -1649,6 +1651,7 @@ extern "C" int fmp_precond_apply(fmp_precond* p, const fmp_block* blk, int mode,
         FMP_CHECK_CUDA(cudaStreamWaitEvent(st, p->ev_join[q], 0));
       }
     } else if (p->use_ozaki) {
+      FMP_REQUIRE(p->d_ozshapes != nullptr, "Ozaki GEMM requested but the plan has no C^-1");
       for (int64_t s2 = 0; s2 < p->d.n_shape; ++s2) {
         const int m = (int)p->shapes[s2].m, n = (int)(p->first[s2 + 1] - p->first[s2]);
         if (n == 0) continue;

@@ -154,7 +154,9 @@ class SolvePlan:
                     t = pad_rows(t, ld)
             self.cinv.append(t)
         P = C.c_void_p
-        self._cinv_arr = (P * len(shapes))(*[t.data_ptr() for t in self.cinv])
+        # null C^-1 pointers tell the library this plan never applies the Woodbury correction
+        self._cinv_arr = (P * len(shapes))(*[(t.data_ptr() if t.numel() > 1 or need_woodbury else None)
+                                               for t in self.cinv])
         self._y_arr = (P * len(shapes))(*[t.data_ptr() for t in self.ymat])
         self._z_arr = (P * len(shapes))(*[t.data_ptr() for t in self.zmat])
         desc = _lib.FmpPrecondDesc()
