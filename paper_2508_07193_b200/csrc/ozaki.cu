@@ -6,10 +6,12 @@
 // flops per shape, the largest single block of the preconditioner -- is instead moved to the
 // INT8 tensor pipe:
 //   rows of A = C^-1 and of B = Y^T are scaled by powers of two (exponents eA_i, eB_n) into
-//   (-1, 1) and cut into S base-128 digits ("slices") a_p, b_q in [-127, 127];
-//   A B^T = 2^(eA_i + eB_n) * sum_L 2^(-7L) D_L,   D_L = sum_{p+q=L} a_p b_q^T   (L = 2 .. S+1),
-// each D_L an exact int32 sum (|a b| <= 127^2, K <= 2^15).  Truncating at L <= S+1 bounds the
-// error by ~2^(-7S) of the row/column scales (S = 6: 2^-42; tests/test_ozaki_gpu.py).
+//   (-1, 1), rounded to 8S-2 bits and cut into S balanced base-256 digits ("slices")
+//   a_p, b_q in [-128, 127]:   x = 2^(e+2) sum_p d_p 2^(-8p)  (error <= 2^(e-8S+1));
+//   A B^T = 2^(eA_i + eB_n + 4) * sum_L 2^(-8L) D_L,   D_L = sum_{p+q=L} a_p b_q^T  (L = 2 .. S+1),
+// each D_L an exact int32 sum (|a b| <= 2^14, K <= 16384 per level with <= S pairs).  S = 7 keeps
+// 54 bits per operand -- FP64-level agreement with DGEMM (tests/test_ozaki_gpu.py); dropping
+// the levels above S+1 costs ~2^-72.
 //
 // Layout: slices are stored pre-tiled in the UMMA canonical K-major SWIZZLE_NONE layout --
 // for each (128-row tile, 32-byte K chunk) the S slices are one contiguous block of
@@ -20,31 +22,21 @@
 // levels in FP64 and store Z.
 #include <cstdint>
 #include "common.cuh"
+#include "ozaki.cuh"
 
 namespace fmp {
 
-constexpr int OZ_S = 6;                 // slices per operand
+constexpr int OZ_S = 7;                 // slices per operand
 constexpr int OZ_M = 128;               // rows per tile (TMEM lanes)
-constexpr int OZ_N = 80;                // columns per tile: OZ_S * OZ_N <= 512 TMEM columns
+constexpr int OZ_WMAX = 64;             // column-tile width cap (multiple of 16): OZ_S * w <= 512 TMEM columns
+constexpr int OZ_MAX_K = 16384;         // int32 headroom: S pairs x 2^14 x K < 2^31
 constexpr int OZ_KC = 32;               // K bytes per MMA / stage
 constexpr int OZ_ABLK = OZ_M * OZ_KC;   // bytes of one A slice block
-constexpr int OZ_BBLK = OZ_N * OZ_KC;   // bytes of one B slice block
-constexpr int OZ_STAGE = OZ_S * (OZ_ABLK + OZ_BBLK);
-constexpr int OZ_STAGES = 4;
+constexpr int OZ_STAGE = OZ_S * (OZ_ABLK + OZ_WMAX * OZ_KC);
+constexpr int OZ_STAGES = 5;
 constexpr int OZ_THREADS = 192;         // warps 0-3 epilogue, 4 producer, 5 MMA
 constexpr int OZ_TMEM_COLS = 512;
-
-struct OzShape {
-  const int8_t* A;      // tiled slices of C^-1: [mtile][kchunk][S][OZ_ABLK]
-  const int* eA;        // [m] row exponents
-  const int8_t* B;      // tiled slices of Y: [ntile][kchunk][S][OZ_BBLK]
-  const int* eB;        // [n] column exponents
-  double* Z;            // [n][ld]
-  int m, n, ld, kchunks;
-};
-struct OzTile {
-  int shape, mt, nt, pad;
-};
+static_assert(OZ_S * OZ_WMAX <= OZ_TMEM_COLS, "levels x width exceed TMEM");
 
 __device__ __forceinline__ uint32_t s_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -89,6 +81,25 @@ __device__ __forceinline__ void umma_i8(uint32_t tmem, uint64_t da, uint64_t db,
       "l"(da), "l"(db), "r"(idesc), "r"(acc));
 }
 
+// One K chunk of a tile of width W: for each A slice p, MMAs of N <= 256 against the stacked B
+// slices 1..S+1-p (levels p+1..S+1).  W is a template constant so every descriptor and TMEM
+// offset folds to an immediate: the issue loop is ~4 instructions per MMA.
+template <int W>
+__device__ __forceinline__ void issue_chunk(uint64_t da0, uint64_t db0, uint32_t tmem, bool first) {
+  constexpr uint32_t IDESC0 = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(OZ_M >> 4) << 24);
+#pragma unroll
+  for (int p = 1; p <= OZ_S; ++p) {
+    const uint64_t da = da0 + (uint64_t)(((p - 1) * OZ_ABLK) >> 4);
+    const uint32_t acc = (first && p == 1) ? 0u : 1u;
+#pragma unroll
+    for (int r0 = 0; r0 < (OZ_S + 1 - p) * W; r0 += 256) {
+      const int nn = ((OZ_S + 1 - p) * W - r0) < 256 ? ((OZ_S + 1 - p) * W - r0) : 256;
+      umma_i8(tmem + (uint32_t)((p - 1) * W + r0), da, db0 + (uint64_t)((r0 * 16) >> 4),
+              IDESC0 | ((uint32_t)(nn >> 3) << 17), acc);
+    }
+  }
+}
+
 __global__ void __launch_bounds__(OZ_THREADS, 1)
     k_ozaki(const OzShape* __restrict__ shapes, const OzTile* __restrict__ tiles, int n_tiles) {
   extern __shared__ __align__(1024) uint8_t osm[];
@@ -122,25 +133,29 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
         const OzTile tl = tiles[ti];
         const OzShape sh = shapes[tl.shape];
         const int8_t* a = sh.A + (size_t)tl.mt * sh.kchunks * OZ_S * OZ_ABLK;
-        const int8_t* b = sh.B + (size_t)tl.nt * sh.kchunks * OZ_S * OZ_BBLK;
+        const uint32_t bblk = (uint32_t)sh.w * OZ_KC;
+        const int8_t* b = sh.B + (size_t)tl.nt * sh.kchunks * OZ_S * bblk;
         for (int kc = 0; kc < sh.kchunks; ++kc, ++it) {
           const int s = it % OZ_STAGES;
           const uint32_t ph = (it / OZ_STAGES) & 1;
           mbar_wait(&empty_bar[s], ph ^ 1);
           uint8_t* st = osm + s * OZ_STAGE;
-          mbar_expect_tx(&full_bar[s], OZ_STAGE);
+          mbar_expect_tx(&full_bar[s], OZ_S * (OZ_ABLK + bblk));
           bulk_g2s(st, a + (size_t)kc * OZ_S * OZ_ABLK, OZ_S * OZ_ABLK, &full_bar[s]);
-          bulk_g2s(st + OZ_S * OZ_ABLK, b + (size_t)kc * OZ_S * OZ_BBLK, OZ_S * OZ_BBLK, &full_bar[s]);
+          bulk_g2s(st + OZ_S * OZ_ABLK, b + (size_t)kc * OZ_S * bblk, OZ_S * bblk, &full_bar[s]);
         }
       }
     }
   } else if (warp == 5) {
-    // ---------------- MMA issuer: S(S+1)/2 MMAs per K chunk, level L -> TMEM columns [(L-2)*N, ...)
-    const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(OZ_N >> 3) << 17) |
-                           ((uint32_t)(OZ_M >> 4) << 24);
+    // ---------------- MMA issuer.  Level L = p + q accumulates in TMEM columns [(L-2) w, (L-1) w).
+    // The B slices of a stage are stacked along N ([K half][q][w rows]), so for a fixed A slice p
+    // ONE MMA of N = (S+1-p) w against B slices 1..S+1-p feeds levels p+1..S+1 at once (split at
+    // N = 256): S+3 MMAs per K chunk instead of S(S+1)/2, each A block read from smem once per p.
     int it = 0, tcount = 0;
     for (int ti = blockIdx.x; ti < n_tiles; ti += gridDim.x, ++tcount) {
       const OzShape sh = shapes[tiles[ti].shape];
+      const int w = sh.w;
+      const uint32_t lbo_b = (uint32_t)OZ_S * w * 16;
       if (tcount > 0) {   // the epilogue must have drained the accumulators of the previous tile
         mbar_wait(&tempty_bar, (tcount - 1) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;\n");
@@ -152,18 +167,14 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
         asm volatile("tcgen05.fence::after_thread_sync;\n");
         if (lane == 0) {
           const uint32_t sa = s_u32(osm + s * OZ_STAGE);
-          const uint32_t sb = sa + OZ_S * OZ_ABLK;
-#pragma unroll
-          for (int L = 2; L <= OZ_S + 1; ++L) {
-            const uint32_t dt = tmem + (uint32_t)((L - 2) * OZ_N);
-#pragma unroll
-            for (int p = 1; p < L; ++p) {
-              const int q = L - p;
-              if (q > OZ_S) continue;
-              const uint64_t da = umma_desc(sa + (p - 1) * OZ_ABLK, OZ_M * 16, 128);
-              const uint64_t db = umma_desc(sb + (q - 1) * OZ_BBLK, OZ_N * 16, 128);
-              umma_i8(dt, da, db, idesc, (kc > 0 || p > 1) ? 1u : 0u);
-            }
+          const uint64_t da0 = umma_desc(sa, OZ_M * 16, 128);
+          const uint64_t db0 = umma_desc(sa + OZ_S * OZ_ABLK, lbo_b, 128);
+          const bool first = kc == 0;
+          switch (w) {
+            case 16: issue_chunk<16>(da0, db0, tmem, first); break;
+            case 32: issue_chunk<32>(da0, db0, tmem, first); break;
+            case 48: issue_chunk<48>(da0, db0, tmem, first); break;
+            default: issue_chunk<64>(da0, db0, tmem, first); break;
           }
           umma_commit(&empty_bar[s]);                         // stage free once these MMAs retire
           if (kc == sh.kchunks - 1) umma_commit(&tfull_bar);  // accumulators complete
@@ -181,14 +192,14 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
       asm volatile("tcgen05.fence::after_thread_sync;\n");
       const int row = tl.mt * OZ_M + warp * 32 + lane;
       const int ea = row < sh.m ? sh.eA[row] : 0;
-      for (int c0 = 0; c0 < OZ_N; c0 += 16) {
+      for (int c0 = 0; c0 < sh.w; c0 += 16) {
         double acc[16];
 #pragma unroll
         for (int j = 0; j < 16; ++j) acc[j] = 0.0;
 #pragma unroll
         for (int L = OZ_S + 1; L >= 2; --L) {   // smallest terms first
           uint32_t v[16];
-          const uint32_t addr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)((L - 2) * OZ_N + c0);
+          const uint32_t addr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)((L - 2) * sh.w + c0);
           asm volatile(
               "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, "
               "[%16];\n"
@@ -197,15 +208,15 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
                 "=r"(v[15])
               : "r"(addr));
           asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-          const double w = ldexp(1.0, -7 * L);
+          const double wgt = ldexp(1.0, -8 * L);
 #pragma unroll
-          for (int j = 0; j < 16; ++j) acc[j] = fma((double)(int)v[j], w, acc[j]);
+          for (int j = 0; j < 16; ++j) acc[j] = fma((double)(int)v[j], wgt, acc[j]);
         }
         if (row < sh.m) {
 #pragma unroll
           for (int j = 0; j < 16; ++j) {
-            const int n = tl.nt * OZ_N + c0 + j;
-            if (n < sh.n) sh.Z[(size_t)n * sh.ld + row] = ldexp(acc[j], ea + sh.eB[n]);
+            const int n = tl.nt * sh.w + c0 + j;
+            if (n < sh.n) sh.Z[(size_t)n * sh.ld + row] = ldexp(acc[j], ea + sh.eB[n] + 4);
           }
         }
       }
@@ -219,59 +230,106 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
 }
 
 // ---------------------------------------------------------------- slicing
-// One warp per row r of src [rows][ld] (K = kvalid entries): exponent e = max |x| exponent,
-// digits of x * 2^-e in base 128, written into the tiled UMMA layout with tile height T.
-template <int T>
-__global__ void k_ozaki_slice(const double* __restrict__ src, int rows, int ld, int kvalid, int kchunks,
-                              int8_t* __restrict__ dst, int* __restrict__ exps) {
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  const int tiles_rows = (rows + T - 1) / T * T;
-  if (warp >= tiles_rows) return;
-  const int r = warp;
-  const bool valid = r < rows;
+// Batched over operands (OzSlice table).  Pass 1: one CTA per row -> exponent e with
+// max|x| < 2^e.  Pass 2: one thread per 16-byte K group of a row -> S digit bytes each, written
+// into the tiled UMMA layout of tile height T ([tile][kchunk][S][2 K halves][T/8][8 rows][16 B]).
+__device__ __forceinline__ int find_slice(const OzSlice* sl, int count, int64_t v, bool by_rows) {
+  int i = 0;
+  while (i + 1 < count && (by_rows ? sl[i + 1].row0 : sl[i + 1].q0) <= v) ++i;
+  return i;
+}
+
+__global__ void k_ozaki_exp(const OzSlice* __restrict__ sl, int count) {
+  __shared__ double red[8];
+  const OzSlice o = sl[find_slice(sl, count, blockIdx.x, true)];
+  const int r = (int)(blockIdx.x - o.row0);
+  const double* src = o.src + (size_t)r * o.ld;
   double mx = 0.0;
-  if (valid)
-    for (int k = lane; k < kvalid; k += 32) mx = fmax(mx, fabs(src[(size_t)r * ld + k]));
+  for (int k = threadIdx.x; k < o.kvalid; k += blockDim.x) mx = fmax(mx, fabs(src[k]));
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-  int e = 0;
-  if (mx > 0.0) frexp(mx, &e);   // mx = f 2^e, f in [0.5, 1): |x| 2^-e < 1
-  if (lane == 0 && valid) exps[r] = e;
-  const int rt = r / T, rr = r % T;
-  const size_t blk = (size_t)T * OZ_KC;
-  for (int k = lane; k < kchunks * OZ_KC; k += 32) {
-    double x = (valid && k < kvalid) ? ldexp(src[(size_t)r * ld + k], -e) : 0.0;
-    const int kc = k / OZ_KC, kb = k % OZ_KC, kh = kb / 16, kk = kb % 16;
-    int8_t* base = dst + ((size_t)rt * kchunks + kc) * OZ_S * blk + kh * (T * 16) + (rr / 8) * 128 + (rr % 8) * 16 + kk;
-#pragma unroll
-    for (int p = 0; p < OZ_S; ++p) {
-      x *= 128.0;
-      const double d = trunc(x);   // |d| <= 127, same sign as x; x - d exact
-      x -= d;
-      base[p * blk] = (int8_t)d;
-    }
+  for (int off = 16; off > 0; off >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) mx = fmax(mx, red[w]);
+    int e = 0;
+    if (mx > 0.0) frexp(mx, &e);
+    o.exps[r] = e;
   }
 }
 
-int ozaki_slice_a(const double* cinv, int m, int ld, int kchunks, int8_t* dst, int* exps, cudaStream_t st) {
-  const int rows = (m + OZ_M - 1) / OZ_M * OZ_M;
-  k_ozaki_slice<OZ_M><<<(rows * 32 + 255) / 256, 256, 0, st>>>(cinv, m, ld, m, kchunks, dst, exps);
+__global__ void k_ozaki_digits(const OzSlice* __restrict__ sl, int count) {
+  const int64_t gq = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int si = find_slice(sl, count, gq, false);
+  const OzSlice o = sl[si];
+  const int64_t q = gq - o.q0;
+  const int groups = o.kchunks * (OZ_KC / 16);
+  const int rows_p = (o.rows + o.T - 1) / o.T * o.T;
+  if (q >= (int64_t)rows_p * groups) return;
+  const int r = (int)(q / groups), gk = (int)(q - (int64_t)r * groups);
+  const bool valid = r < o.rows;
+  const int e = valid ? o.exps[r] : 0;
+  uint32_t w[OZ_S][4];
+#pragma unroll
+  for (int p = 0; p < OZ_S; ++p) w[p][0] = w[p][1] = w[p][2] = w[p][3] = 0u;
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    const int k = gk * 16 + j;
+    const double x = (valid && k < o.kvalid) ? o.src[(size_t)r * o.ld + k] : 0.0;
+    long long V = llrint(ldexp(x, 8 * OZ_S - 2 - e));   // |V| <= 2^(8S-2)
+#pragma unroll
+    for (int p = OZ_S - 1; p >= 0; --p) {                // balanced base-256 digits, least significant first
+      const int d = (int)(((V + 128) & 255) - 128);
+      V = (V - d) >> 8;
+      w[p][j >> 2] |= (uint32_t)(uint8_t)(int8_t)d << (8 * (j & 3));
+    }
+  }
+  // per-slice blocks [S][K half][T rows] (A) or slices stacked along N [K half][S][T rows] (B, stacked)
+  const int rt = r / o.T, rr = r % o.T, kc = gk / 2, kh = gk % 2;
+  const size_t slice_stride = o.stacked ? (size_t)o.T * 16 : (size_t)o.T * OZ_KC;
+  const size_t half_stride = o.stacked ? (size_t)OZ_S * o.T * 16 : (size_t)o.T * 16;
+  uint8_t* base = reinterpret_cast<uint8_t*>(o.dst) + ((size_t)rt * o.kchunks + kc) * OZ_S * (o.T * OZ_KC) +
+                  kh * half_stride + (rr / 8) * 128 + (rr % 8) * 16;
+#pragma unroll
+  for (int p = 0; p < OZ_S; ++p)
+    *reinterpret_cast<uint4*>(base + p * slice_stride) = make_uint4(w[p][0], w[p][1], w[p][2], w[p][3]);
+}
+
+void ozaki_plan_slices(OzSlice* s, int count, int64_t* rows, int64_t* threads) {
+  int64_t r = 0, q = 0;
+  for (int i = 0; i < count; ++i) {
+    s[i].row0 = r;
+    s[i].q0 = q;
+    r += s[i].rows;
+    q += (int64_t)((s[i].rows + s[i].T - 1) / s[i].T * s[i].T) * s[i].kchunks * (OZ_KC / 16);
+  }
+  *rows = r;
+  *threads = q;
+}
+
+int ozaki_slice(const OzSlice* d_slices, int count, int64_t rows, int64_t threads, cudaStream_t st) {
+  if (count <= 0 || rows <= 0) return 0;
+  k_ozaki_exp<<<(unsigned)rows, 256, 0, st>>>(d_slices, count);
+  FMP_CHECK_LAUNCH();
+  k_ozaki_digits<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(d_slices, count);
   FMP_CHECK_LAUNCH();
   return 0;
 }
 
-int ozaki_slice_b(const double* y, int n, int m, int ld, int kchunks, int8_t* dst, int* exps, cudaStream_t st) {
-  const int rows = (n + OZ_N - 1) / OZ_N * OZ_N;
-  k_ozaki_slice<OZ_N><<<(rows * 32 + 255) / 256, 256, 0, st>>>(y, n, ld, m, kchunks, dst, exps);
-  FMP_CHECK_LAUNCH();
-  return 0;
+int ozaki_width(int n) {
+  const int nt = (n + OZ_WMAX - 1) / OZ_WMAX;
+  const int w = nt > 0 ? (n + nt - 1) / nt : 1;
+  return (w + 15) / 16 * 16;
 }
-
 size_t ozaki_a_bytes(int m, int kchunks) { return (size_t)((m + OZ_M - 1) / OZ_M) * kchunks * OZ_S * OZ_ABLK; }
-size_t ozaki_b_bytes(int n, int kchunks) { return (size_t)((n + OZ_N - 1) / OZ_N) * kchunks * OZ_S * OZ_BBLK; }
-int ozaki_kchunks(int m) { return (m + OZ_KC - 1) / OZ_KC; }
+size_t ozaki_b_bytes(int n, int kchunks) {
+  const int w = ozaki_width(n);
+  return (size_t)((n + w - 1) / w) * kchunks * OZ_S * w * OZ_KC;
+}
+int ozaki_kchunks(int m) {
+  return m <= OZ_MAX_K ? (m + OZ_KC - 1) / OZ_KC : -1;
+}
 int ozaki_tile_m() { return OZ_M; }
-int ozaki_tile_n() { return OZ_N; }
 
 int ozaki_setup() {
   FMP_CHECK_CUDA(cudaFuncSetAttribute(k_ozaki, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -23,6 +23,7 @@
 #include <vector>
 #include <cublas_v2.h>
 #include "common.cuh"
+#include "ozaki.cuh"
 
 namespace fmp {
 
@@ -41,28 +42,6 @@ int gemm_config_of(int n);
 int gemm_tile_m(int cfg);
 int gemm_tile_n(int cfg);
 int gemm_launch(int cfg, const GemmShape* shapes, const GemmTile* tiles, int n_tiles, int sms, cudaStream_t st);
-
-// ozaki.cu
-struct OzShape {
-  const int8_t* A;
-  const int* eA;
-  const int8_t* B;
-  const int* eB;
-  double* Z;
-  int m, n, ld, kchunks;
-};
-struct OzTile {
-  int shape, mt, nt, pad;
-};
-int ozaki_setup();
-int ozaki_slice_a(const double* cinv, int m, int ld, int kchunks, int8_t* dst, int* exps, cudaStream_t st);
-int ozaki_slice_b(const double* y, int n, int m, int ld, int kchunks, int8_t* dst, int* exps, cudaStream_t st);
-size_t ozaki_a_bytes(int m, int kchunks);
-size_t ozaki_b_bytes(int n, int kchunks);
-int ozaki_kchunks(int m);
-int ozaki_tile_m();
-int ozaki_tile_n();
-int ozaki_launch(const OzShape* shapes, const OzTile* tiles, int n_tiles, int sms, cudaStream_t st);
 
 __host__ __device__ constexpr int pad8(int n) { return (n + 7) & ~7; }
 __host__ __device__ constexpr int pad4(int n) { return (n + 3) & ~3; }
@@ -1268,6 +1247,9 @@ struct fmp_precond {
   OzShape* d_ozshapes = nullptr;
   OzTile* d_oztiles = nullptr;
   int n_oztiles = 0;
+  OzSlice* d_ozslices = nullptr;          // per-apply slicing of Y, all shapes in two launches
+  int n_ozslices = 0;
+  int64_t oz_rows = 0, oz_threads = 0;
   static constexpr int kAux = 4;          // concurrent GEMM streams (small shapes are HBM-bound)
   cudaStream_t aux[kAux] = {};
   cublasHandle_t aux_blas[kAux] = {};
@@ -1314,6 +1296,7 @@ static void free_plan(fmp_precond* p) {
   for (auto* q : p->oz_eb) cudaFree(q);
   cudaFree(p->d_ozshapes);
   cudaFree(p->d_oztiles);
+  cudaFree(p->d_ozslices);
   for (int c = 0; c < 3; ++c) cudaFree(p->d_gtiles[c]);
   delete p;
 }
@@ -1448,9 +1431,12 @@ extern "C" int fmp_precond_create(const fmp_precond_desc* desc, fmp_precond** ou
     if (ozaki_setup()) { free_plan(p); return -1; }
     std::vector<OzShape> os;
     std::vector<OzTile> ot;
+    std::vector<OzSlice> sa, sb;
     for (int64_t s2 = 0; s2 < desc->n_shape; ++s2) {
       const auto& sh = p->shapes[s2];
       const int m = (int)sh.m, n = (int)(p->first[s2 + 1] - p->first[s2]), kc = ozaki_kchunks(m);
+      FMP_REQUIRE(kc > 0, "Ozaki GEMM: correction size m = %d exceeds the int32 accumulator range", m);
+      const int w = ozaki_width(std::max(n, 1));
       int8_t *a = nullptr, *b = nullptr;
       int *ea = nullptr, *eb = nullptr;
       const size_t ab = ozaki_a_bytes(m, kc), bb = ozaki_b_bytes(std::max(n, 1), kc);
@@ -1463,12 +1449,26 @@ extern "C" int fmp_precond_create(const fmp_precond_desc* desc, fmp_precond** ou
       p->oz_b.push_back(b);
       p->oz_ea.push_back(ea);
       p->oz_eb.push_back(eb);
-      if (ozaki_slice_a(p->cinv[s2], m, (int)sh.ld, kc, a, ea, 0)) { free_plan(p); return -1; }
-      os.push_back(OzShape{a, ea, b, eb, p->zmat[s2], m, n, (int)sh.ld, kc});
+      sa.push_back(OzSlice{p->cinv[s2], a, ea, m, (int)sh.ld, m, kc, ozaki_tile_m(), 0, 0, 0});
+      if (n > 0) sb.push_back(OzSlice{p->ymat[s2], b, eb, n, (int)sh.ld, m, kc, w, 1, 0, 0});
+      os.push_back(OzShape{a, ea, b, eb, p->zmat[s2], m, n, (int)sh.ld, kc, w, 0});
       for (int mt = 0; mt * ozaki_tile_m() < m; ++mt)
-        for (int nt = 0; nt * ozaki_tile_n() < n; ++nt) ot.push_back(OzTile{(int)s2, mt, nt, 0});
+        for (int nt = 0; nt * w < n; ++nt) ot.push_back(OzTile{(int)s2, mt, nt, 0});
     }
-    if (upload(os, &p->d_ozshapes) || upload(ot, &p->d_oztiles)) { free_plan(p); return -1; }
+    int64_t ra = 0, qa = 0;
+    ozaki_plan_slices(sa.data(), (int)sa.size(), &ra, &qa);
+    ozaki_plan_slices(sb.data(), (int)sb.size(), &p->oz_rows, &p->oz_threads);
+    OzSlice* d_sa = nullptr;
+    if (upload(sa, &d_sa) || upload(sb, &p->d_ozslices) || upload(os, &p->d_ozshapes) || upload(ot, &p->d_oztiles)) {
+      cudaFree(d_sa);
+      free_plan(p);
+      return -1;
+    }
+    p->n_ozslices = (int)sb.size();
+    const int rc = ozaki_slice(d_sa, (int)sa.size(), ra, qa, 0);
+    cudaDeviceSynchronize();
+    cudaFree(d_sa);
+    if (rc) { free_plan(p); return -1; }
     p->n_oztiles = (int)ot.size();
     FMP_CHECK_CUDA(cudaDeviceSynchronize());
   }
@@ -1652,13 +1652,7 @@ extern "C" int fmp_precond_apply(fmp_precond* p, const fmp_block* blk, int mode,
       }
     } else if (p->use_ozaki) {
       FMP_REQUIRE(p->d_ozshapes != nullptr, "Ozaki GEMM requested but the plan has no C^-1");
-      for (int64_t s2 = 0; s2 < p->d.n_shape; ++s2) {
-        const int m = (int)p->shapes[s2].m, n = (int)(p->first[s2 + 1] - p->first[s2]);
-        if (n == 0) continue;
-        if (int e = ozaki_slice_b(p->ymat[s2], n, m, (int)p->shapes[s2].ld, ozaki_kchunks(m), p->oz_b[s2],
-                                  p->oz_eb[s2], st))
-          return e;
-      }
+      if (int e = ozaki_slice(p->d_ozslices, p->n_ozslices, p->oz_rows, p->oz_threads, st)) return e;
       if (int e = ozaki_launch(p->d_ozshapes, p->d_oztiles, p->n_oztiles, p->sms, st)) return e;
     } else {
       for (int c = 0; c < 3; ++c)
