@@ -265,7 +265,7 @@ def run_ours(args):
                           "tflops_reference_count": round(flops_ref / t_prec / 1e12, 2)},
         "spmv": {"ms": round(t_spmv * 1e3, 4), "GB_per_s": round(spmv_bytes / t_spmv / 1e9, 1),
                  "frac_hbm": round(spmv_bytes / t_spmv / 1e9 / peaks["hbm_gbs"], 3)},
-        "roofline": {"kernel": "RAS precond apply (fused FlashMP sequence, FP64 DMMA + cuBLAS DGEMM)",
+        "roofline": {"kernel": "RAS precond apply (fused FlashMP sequence: FP64 DMMA transforms + Ozaki INT8 tcgen05 Woodbury GEMM)",
                      "bound": "tensor", "achieved": round(prec_tflops, 3), "peak": peaks["fp64_tflops"],
                      "unit": "TFLOP/s", "frac": round(prec_tflops / peaks["fp64_tflops"], 3)
                      if peaks["fp64_tflops"] else None, "traffic": None,

@@ -1404,7 +1404,7 @@ extern "C" int fmp_precond_create(const fmp_precond_desc* desc, fmp_precond** ou
   }
   {  // grouped GEMM tables: one shape record per extended shape, tiles bucketed by configuration
     const char* gm = getenv("FMP_GEMM");
-    const std::string gmode = gm ? gm : "cublas";
+    const std::string gmode = gm ? gm : "ozaki";   // cublas | own | ozaki
     p->use_cublas = gmode == "cublas";
     p->use_ozaki = gmode == "ozaki";
     std::vector<GemmShape> gs;
