@@ -3,6 +3,7 @@
 #include <atomic>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <cuda_runtime.h>
 #include "../../include/flashmp_b200.h"
 
@@ -30,6 +31,11 @@ extern std::atomic<int64_t> g_launches;
   do {                                                                              \
     if (!(cond)) { ::fmp::set_error(__VA_ARGS__); return -2; }                      \
   } while (0)
+
+inline bool getenv_flag(const char* name) {
+  const char* v = getenv(name);
+  return v && v[0] == '1';
+}
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 

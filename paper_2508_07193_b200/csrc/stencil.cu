@@ -11,6 +11,8 @@
 // Roofline: HBM-bound, 48 B per owned point (read x: 24 B, write y: 24 B);
 // mode 3 (true residual) reads x and b (48 B) and writes nothing.
 #include "common.cuh"
+#include "tma.cuh"
+#include <algorithm>
 
 namespace fmp {
 
@@ -148,6 +150,265 @@ __global__ void __launch_bounds__(TX* TY) k_spmv(Geo g, double alpha, int bnd, c
   }
 }
 
+// ---------------------------------------------------------------- SpMV, bulk-copy variant (sm_100a)
+// Same z-march, warp-specialised.  A producer warp streams each haloed plane of all three
+// components ([3][SY+2][SX+4] doubles, 16 KB) into a 4-slot shared-memory ring with one
+// cp.async.bulk per row (16-byte aligned, from x = i0-2); halo cells outside the block are
+// bulk-copied from a zero page (the zero-ghost physical boundary), so every row is exactly
+// 544 bytes and every plane exactly 16,320 -- one mbarrier transaction count per slot.
+// Tiles off the low faces take the whole plane as ONE TMA box load instead (tile-mode TMA
+// coordinates must be non-negative on this part -- tools/tma_test.cu -- so the low faces
+// cannot use it; cells beyond the high faces are zero-filled by the TMA unit).
+// Eight consumer warps wait on the slot's "full" barrier, compute, and release the slot on its
+// "empty" barrier; no CTA-wide barrier in the loop, so consumers and producer drift freely
+// within the ring.
+// GPU-block faces with neighbour ghosts are patched in shared memory after the plane lands.
+// Work: units (z-chunk of L planes) x (64 x 8 column tile), z-chunk-major, dealt round-robin
+// to a grid of exactly the resident CTAs, so CTAs that run concurrently hold neighbouring
+// tiles of the same z range and the halo rows/planes they share are L2 hits.
+constexpr int SX = 64, SY = 8;
+constexpr int SXR = SX + 4, SYH = SY + 2;          // smem row: logical i0-2 .. i0+SX+1
+constexpr int SPL = SXR * SYH, SPLANE = 3 * SPL;   // doubles per component plane / per plane
+constexpr int SSLOT = (SPLANE + 15) / 16 * 16;      // slot stride: TMA destinations are 128-byte aligned
+constexpr int SCONS = 8;                            // consumer warps
+constexpr int STHREADS = (SCONS + 1) * 32;
+constexpr uint32_t kPlaneBytes = SPLANE * 8;
+// [ring: NS x SSLOT doubles][2 x NS mbarriers][NS unit ids (int64)][SCONS reduction words]
+constexpr int spmv_bulk_smem(int ns) { return (ns * SSLOT + 3 * ns + SCONS) * (int)sizeof(double); }
+
+struct BulkSpmvArgs {
+  Geo g;
+  const double* x;
+  double* y;
+  const double* w;
+  double* partials;
+  const double* zeros;   // >= SXR doubles of 0.0 (16-byte aligned)
+  unsigned long long* counter;   // [fetch, done]: dynamic unit scheduler, zero between launches
+  double alpha;
+  int bnd, tiles_x, tiles_y, L, nzc, ghosts;
+};
+
+template <int MODE, int SNSLOT>
+__global__ void __launch_bounds__(STHREADS, SNSLOT <= 4 ? 3 : 2) k_spmv_bulk(const __grid_constant__ CUtensorMap tm, BulkSpmvArgs A) {
+  extern __shared__ __align__(128) double ring[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + SNSLOT * SSLOT);
+  uint64_t* empty = full + SNSLOT;
+  int64_t* slot_unit = reinterpret_cast<int64_t*>(empty + SNSLOT);   // unit of a unit's first load, -1 = done
+  double* red = reinterpret_cast<double*>(slot_unit + SNSLOT);
+  const Geo& g = A.g;
+  const int tid = threadIdx.x, warp = tid >> 5, lx = tid & 31;
+  const int ntiles = A.tiles_x * A.tiles_y;
+  const int64_t units = (int64_t)ntiles * A.nzc;
+  const int64_t V = (int64_t)g.bx * g.by * g.bz;
+  if (tid == 0) {
+    tma_prefetch_desc(&tm);
+    for (int s = 0; s < SNSLOT; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], SCONS);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  auto nplanes = [&](int64_t u) { return min(A.L, g.bz - (int)(u / ntiles) * A.L); };
+
+  if (warp == SCONS) {
+    // ---------------- producer: takes units from the global counter (z-chunk-major order, so
+    // the CTAs in flight hold neighbouring tiles of the same z range) and streams planes
+    // k0-1 .. k0+np of each; the unit id rides with the unit's first plane
+    int64_t q = 0;
+    for (;;) {
+      unsigned long long f = 0;
+      if (lx == 0) f = atomicAdd(A.counter, 1ull);
+      f = __shfl_sync(0xffffffffu, f, 0);
+      const int64_t u = (int64_t)f;
+      if (u >= units) {   // tell the consumers: a "unit" of -1 in the next slot
+        const int s = (int)(q % SNSLOT);
+        if (q >= SNSLOT) mbar_wait(&empty[s], (uint32_t)(((q / SNSLOT) - 1) & 1));
+        if (lx == 0) {
+          slot_unit[s] = -1;
+          mbar_arrive(&full[s]);
+          __threadfence();   // the last CTA out re-arms the scheduler for the next launch
+          if (atomicAdd(A.counter + 1, 1ull) == gridDim.x - 1) {
+            A.counter[0] = 0;
+            A.counter[1] = 0;
+          }
+        }
+        break;
+      }
+      const int tile = (int)(u % ntiles), zc = (int)(u / ntiles);
+      const int i0 = (tile % A.tiles_x) * SX, j0 = (tile / A.tiles_x) * SY, k0 = zc * A.L;
+      const int xs = max(i0 - 2, 0), xe = min(i0 + SX + 2, g.bx);   // in-block x range (even bounds)
+      const int c_lo = xs - (i0 - 2), c_hi = xe - (i0 - 2);          // its smem columns
+      const int np = nplanes(u);
+      for (int m = 0; m < np + 2; ++m, ++q) {
+        const int s = (int)(q % SNSLOT), k = k0 - 1 + m;
+        if (q >= SNSLOT) mbar_wait(&empty[s], (uint32_t)(((q / SNSLOT) - 1) & 1));
+        if (lx == 0) {
+          if (m == 0) slot_unit[s] = u;
+          mbar_expect_tx(&full[s], kPlaneBytes);
+        }
+        __syncwarp();
+        if (i0 >= 2 && j0 >= 1 && k >= 0) {   // one TMA box (beyond-the-end cells zero-filled)
+          if (lx == 0) tma_load_4d(ring + s * SSLOT, &tm, i0 - 2, j0 - 1, k, 0, &full[s]);
+        } else if (lx < 3 * SYH) {   // low faces: one bulk copy per (component, row) + zero page
+          const int c = lx / SYH, jj = lx - c * SYH, j = j0 - 1 + jj;
+          double* row = ring + s * SSLOT + c * SPL + jj * SXR;
+          if ((unsigned)j < (unsigned)g.by && (unsigned)k < (unsigned)g.bz) {
+            bulk_g2s(row + c_lo, A.x + fidx(g, c, k, j, xs), (uint32_t)(c_hi - c_lo) * 8, &full[s]);
+            if (c_lo > 0) bulk_g2s(row, A.zeros, (uint32_t)c_lo * 8, &full[s]);
+            if (c_hi < SXR) bulk_g2s(row + c_hi, A.zeros, (uint32_t)(SXR - c_hi) * 8, &full[s]);
+          } else {
+            bulk_g2s(row, A.zeros, SXR * 8, &full[s]);
+          }
+        }
+      }
+    }
+    return;
+  }
+
+  // ---------------- consumers: 8 warps, row ly = warp, points i0 + lane and i0 + lane + 32.
+  // Plane k-1 is never re-read from shared memory: the five values the stencil needs from it
+  // were read from plane k one step earlier and are carried in registers (20 shared loads per
+  // point instead of 25).  So only planes k and k+1 are held; plane k is released after the step.
+  const int ly = warp;
+  double acc0 = 0.0, acc1 = 0.0;
+  int64_t qbase = 0;   // load index of the current unit's first plane (k0 - 1)
+  for (;;) {
+    mbar_wait(&full[qbase % SNSLOT], (uint32_t)((qbase / SNSLOT) & 1));
+    const int64_t u = slot_unit[qbase % SNSLOT];
+    if (u < 0) break;
+    const int tile = (int)(u % ntiles), zc = (int)(u / ntiles);
+    const int i0 = (tile % A.tiles_x) * SX, j0 = (tile / A.tiles_x) * SY, k0 = zc * A.L;
+    const int np = nplanes(u);
+    // neighbour ghosts: halo cells outside the block in x / y (ii in [0, xa) u [xb, SX+2),
+    // jj in [0, ya) u [yb, SYH)) and whole planes outside it in z are overwritten by fetch()
+    const int xa = i0 == 0 ? 1 : 0, xb = min(SX + 2, g.bx - i0 + 1), nxs = xa + (SX + 2 - xb);
+    const int ya = j0 == 0 ? 1 : 0, yb = min(SYH, g.by - j0 + 1), nys = ya + (SYH - yb);
+    const bool edge = A.ghosts && (nxs > 0 || nys > 0 || k0 == 0 || k0 + np == g.bz);
+    double pe[2], pf[2], ph[2], pq[2], pr[2];   // plane k-1: ex, ey, ez, ez(i+1), ez(j+1)
+    for (int jz = 0; jz < np; ++jz) {
+      const int64_t q0 = qbase + jz;
+      for (int h = (jz == 0 ? 0 : 2); h < 3; ++h)
+        mbar_wait(&full[(q0 + h) % SNSLOT], (uint32_t)(((q0 + h) / SNSLOT) & 1));
+      if (edge) {
+        const int ct = tid, nct = SCONS * 32;
+        for (int h = (jz == 0 ? 0 : 2); h < 3; ++h) {
+          const int k = k0 + jz - 1 + h;
+          double* P = ring + ((q0 + h) % SNSLOT) * SSLOT;
+          if (k < 0 || k >= g.bz) {
+            for (int e = ct; e < 3 * SYH * (SX + 2); e += nct) {
+              const int c = e / (SYH * (SX + 2)), r = e - c * (SYH * (SX + 2)), jj = r / (SX + 2), ii = r - jj * (SX + 2);
+              P[c * SPL + jj * SXR + ii + 1] = fetch(g, A.x, c, k, j0 - 1 + jj, i0 - 1 + ii);
+            }
+            continue;
+          }
+          if (nxs > 0)
+            for (int e = ct; e < 3 * SYH * nxs; e += nct) {
+              const int c = e / (SYH * nxs), r = e - c * (SYH * nxs), jj = r / nxs, qq = r - jj * nxs;
+              const int ii = qq < xa ? qq : xb + (qq - xa);
+              P[c * SPL + jj * SXR + ii + 1] = fetch(g, A.x, c, k, j0 - 1 + jj, i0 - 1 + ii);
+            }
+          if (nys > 0)
+            for (int e = ct; e < 3 * nys * (SX + 2); e += nct) {
+              const int c = e / (nys * (SX + 2)), r = e - c * (nys * (SX + 2)), qq = r / (SX + 2), ii = r - qq * (SX + 2);
+              const int jj = qq < ya ? qq : yb + (qq - ya);
+              P[c * SPL + jj * SXR + ii + 1] = fetch(g, A.x, c, k, j0 - 1 + jj, i0 - 1 + ii);
+            }
+        }
+        fence_proxy_async();
+        asm volatile("bar.sync 1, %0;\n" ::"n"(SCONS * 32) : "memory");   // consumers only
+      }
+      const double* p0 = ring + ((q0 + 1) % SNSLOT) * SSLOT;
+      const double* pp = ring + ((q0 + 2) % SNSLOT) * SSLOT;
+      const int k = k0 + jz, j = j0 + ly;
+#define EX(P, dj, di) P[0 * SPL + o + (dj) * SXR + (di)]
+#define EY(P, dj, di) P[1 * SPL + o + (dj) * SXR + (di)]
+#define EZ(P, dj, di) P[2 * SPL + o + (dj) * SXR + (di)]
+#pragma unroll
+      for (int hx = 0; hx < 2; ++hx) {
+        const int i = i0 + lx + 32 * hx;
+        const int o = (ly + 1) * SXR + lx + 32 * hx + 2;
+        if (jz == 0) {   // unit start: prime the carried plane k0-1 values
+          const double* pm_ = ring + (q0 % SNSLOT) * SSLOT;
+          pe[hx] = EX(pm_, 0, 0);
+          pf[hx] = EY(pm_, 0, 0);
+          ph[hx] = EZ(pm_, 0, 0);
+          pq[hx] = EZ(pm_, 0, 1);
+          pr[hx] = EZ(pm_, 1, 0);
+        }
+        const double ex = EX(p0, 0, 0), ey = EY(p0, 0, 0), ez = EZ(p0, 0, 0);
+        const double ez_ip = EZ(p0, 0, 1), ez_jp = EZ(p0, 1, 0), ex_im = EX(p0, 0, -1), ey_jm = EY(p0, -1, 0);
+        const double nx = EX(pp, 0, 0), ny = EY(pp, 0, 0);
+        // Appendix A: (C_b C_f + Lambda) x on the zero-ghost padded box
+        double tx = 4.0 * ex - EX(p0, -1, 0) - EX(p0, 1, 0) - pe[hx] - nx + EY(p0, 0, 1) - ey - EY(p0, -1, 1) +
+                    ey_jm + ez_ip - ez - pq[hx] + ph[hx];
+        double ty = 4.0 * ey - EY(p0, 0, -1) - EY(p0, 0, 1) - pf[hx] - ny + ez_jp - ez - pr[hx] + ph[hx] +
+                    EX(p0, 1, 0) - ex - EX(p0, 1, -1) + ex_im;
+        double tz = 4.0 * ez - EZ(p0, 0, -1) - ez_ip - EZ(p0, -1, 0) - ez_jp + nx - ex - EX(pp, 0, -1) + ex_im + ny -
+                    ey - EY(pp, -1, 0) + ey_jm;
+        pe[hx] = ex;
+        pf[hx] = ey;
+        ph[hx] = ez;
+        pq[hx] = ez_ip;
+        pr[hx] = ez_jp;
+        if (i >= g.bx || j >= g.by) continue;
+        if (!A.bnd) {
+          const int gi = g.gx0 + i, gj = g.gy0 + j, gk = g.gz0 + k;
+          tx -= ((gj == 0) + (gk == 0)) * ex;
+          ty -= ((gi == 0) + (gk == 0)) * ey;
+          tz -= ((gi == 0) + (gj == 0)) * ez;
+        }
+        const double yx = ex + A.alpha * tx, yy = ey + A.alpha * ty, yz = ez + A.alpha * tz;
+        const int64_t oi = fidx(g, 0, k, j, i);
+        if (MODE == 3) {
+          const double rx = A.w[oi] - yx, ry = A.w[oi + V] - yy, rz = A.w[oi + 2 * V] - yz;
+          acc0 += rx * rx + ry * ry + rz * rz;
+        } else {
+          __stcs(A.y + oi, yx);   // streaming stores: keep L2 for the halo planes and rows
+          __stcs(A.y + oi + V, yy);
+          __stcs(A.y + oi + 2 * V, yz);
+          if (MODE >= 1) acc0 += yx * A.w[oi] + yy * A.w[oi + V] + yz * A.w[oi + 2 * V];
+          if (MODE == 2) acc1 += yx * yx + yy * yy + yz * yz;
+        }
+      }
+#undef EX
+#undef EY
+#undef EZ
+      __syncwarp();
+      if (lx == 0) {   // release plane k (and plane k-1 after the first step, k+1 after the last)
+        mbar_arrive(&empty[(q0 + 1) % SNSLOT]);
+        if (jz == 0) mbar_arrive(&empty[q0 % SNSLOT]);
+        if (jz == np - 1) mbar_arrive(&empty[(q0 + 2) % SNSLOT]);
+      }
+    }
+    qbase += np + 2;
+  }
+  if (MODE >= 1) {   // consumer-only reduction (named barrier 1)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      acc0 += __shfl_xor_sync(0xffffffffu, acc0, o);
+      acc1 += __shfl_xor_sync(0xffffffffu, acc1, o);
+    }
+    if (lx == 0) red[warp] = acc0;
+    asm volatile("bar.sync 1, %0;\n" ::"n"(SCONS * 32) : "memory");
+    if (tid == 0) {
+      double s0 = 0.0;
+      for (int w2 = 0; w2 < SCONS; ++w2) s0 += red[w2];
+      A.partials[blockIdx.x] = s0;
+    }
+    if (MODE == 2) {
+      asm volatile("bar.sync 1, %0;\n" ::"n"(SCONS * 32) : "memory");
+      if (lx == 0) red[warp] = acc1;
+      asm volatile("bar.sync 1, %0;\n" ::"n"(SCONS * 32) : "memory");
+      if (tid == 0) {
+        double s1 = 0.0;
+        for (int w2 = 0; w2 < SCONS; ++w2) s1 += red[w2];
+        A.partials[gridDim.x + blockIdx.x] = s1;
+      }
+    }
+  }
+}
+
 // ---------------------------------------------------------------- curls and CN stencils
 template <int KIND>  // 0 forward, 1 backward
 __device__ __forceinline__ void curl_at(const Geo& g, const double* __restrict__ f, int k, int j, int i, double& cx,
@@ -225,18 +486,102 @@ static int check_block(const fmp_block* b) {
   return 0;
 }
 
+// z-chunk length: minimise rounds x (planes + 2 halo planes) for the resident grid
+static void spmv_chunking(int64_t ntiles, int bz, int64_t resident, int* L_out, int* nzc_out) {
+  int bestL = bz;
+  double best = 1e300;
+  for (int L = 4; L <= 64; ++L) {
+    const int Lc = std::min(L, bz);
+    const int64_t nzc = (bz + Lc - 1) / Lc, units = ntiles * nzc;
+    const int64_t rounds = (units + resident - 1) / resident;
+    const double cost = (double)rounds * (Lc + 2);
+    if (cost < best - 1e-9) { best = cost; bestL = Lc; }
+    if (Lc == bz) break;
+  }
+  *L_out = bestL;
+  *nzc_out = (bz + bestL - 1) / bestL;
+}
+
+static bool bulk_ok(const fmp_block* b, const double* x) {
+  return b->bx % 2 == 0 && ((uintptr_t)x & 15) == 0 && b->bx <= ((int64_t)1 << 31) &&
+         b->by <= ((int64_t)1 << 31) && b->bz <= ((int64_t)1 << 31) && !getenv_flag("FMP_SPMV_LEGACY");
+}
+
 extern "C" int fmp_stencil_apply(const fmp_block* blk, double alpha, int boundary, int mode, const double* x,
                                  double* y, const double* w, double* dots, double* scratch, void* stream) {
   if (int e = check_block(blk)) return e;
   FMP_REQUIRE(mode >= 0 && mode <= 3, "bad stencil mode %d", mode);
   FMP_REQUIRE(mode == 0 || (w && dots && scratch), "mode %d needs w, dots and scratch", mode);
   const Geo g = make_geo(blk);
+  cudaStream_t st = as_stream(stream);
+  if (bulk_ok(blk, x)) {
+    static int resident4 = 0, resident6 = 0;
+    if (!resident4) {
+#define FMP_SPMV_ATTR(M, N)                                                                            \
+  FMP_CHECK_CUDA(cudaFuncSetAttribute(k_spmv_bulk<M, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                      spmv_bulk_smem(N)));
+      FMP_SPMV_ATTR(0, 4) FMP_SPMV_ATTR(1, 4) FMP_SPMV_ATTR(2, 4) FMP_SPMV_ATTR(3, 4)
+      FMP_SPMV_ATTR(0, 6) FMP_SPMV_ATTR(1, 6) FMP_SPMV_ATTR(2, 6) FMP_SPMV_ATTR(3, 6)
+#undef FMP_SPMV_ATTR
+      int r = 0;
+      FMP_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r, k_spmv_bulk<0, 4>, STHREADS, spmv_bulk_smem(4)));
+      resident4 = std::max(1, r);
+      FMP_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r, k_spmv_bulk<0, 6>, STHREADS, spmv_bulk_smem(6)));
+      resident6 = std::max(1, r);
+    }
+    const int ns = getenv_flag("FMP_SPMV_NS6") ? 6 : 4;
+    const int resident_per_sm = ns == 4 ? resident4 : resident6;
+    BulkSpmvArgs a{};
+    a.g = g;
+    a.x = x;
+    a.y = y;
+    a.w = w;
+    a.partials = scratch;
+    a.alpha = alpha;
+    a.bnd = boundary;
+    a.tiles_x = (g.bx + SX - 1) / SX;
+    a.tiles_y = (g.by + SY - 1) / SY;
+    a.ghosts = 0;
+    for (int q = 0; q < 6; ++q) a.ghosts |= g.ghost[q] != nullptr;
+    static double* zeros = nullptr;
+    if (!zeros) {
+      FMP_CHECK_CUDA(cudaMalloc(&zeros, 4096));
+      FMP_CHECK_CUDA(cudaMemset(zeros, 0, 4096));
+    }
+    a.zeros = zeros;
+    a.counter = reinterpret_cast<unsigned long long*>(zeros + 256);   // bytes 2048.. of the page
+    const int64_t ntiles = (int64_t)a.tiles_x * a.tiles_y;
+    const int64_t resident = (int64_t)kNumSM * resident_per_sm;
+    spmv_chunking(ntiles, g.bz, resident, &a.L, &a.nzc);
+    const int64_t units = ntiles * a.nzc;
+    const int grid = (int)std::min<int64_t>(units, std::min<int64_t>(resident, kScratchDoubles / 2));
+    CUtensorMap tm;
+    const uint64_t dims[4] = {(uint64_t)g.bx, (uint64_t)g.by, (uint64_t)g.bz, 3};
+    const uint64_t strides[3] = {(uint64_t)g.bx * 8, (uint64_t)g.bx * g.by * 8, (uint64_t)g.bx * g.by * g.bz * 8};
+    const uint32_t box[4] = {SXR, SYH, 1, 3};
+    if (int e = encode_tensor_map_f64(&tm, x, 4, dims, strides, box)) return e;
+#define FMP_SPMV_GO(N)                                                                                   \
+  switch (mode) {                                                                                        \
+    case 0: k_spmv_bulk<0, N><<<grid, STHREADS, spmv_bulk_smem(N), st>>>(tm, a); break;                  \
+    case 1: k_spmv_bulk<1, N><<<grid, STHREADS, spmv_bulk_smem(N), st>>>(tm, a); break;                  \
+    case 2: k_spmv_bulk<2, N><<<grid, STHREADS, spmv_bulk_smem(N), st>>>(tm, a); break;                  \
+    case 3: k_spmv_bulk<3, N><<<grid, STHREADS, spmv_bulk_smem(N), st>>>(tm, a); break;                  \
+  }
+    if (ns == 4) {
+      FMP_SPMV_GO(4)
+    } else {
+      FMP_SPMV_GO(6)
+    }
+#undef FMP_SPMV_GO
+    FMP_CHECK_LAUNCH();
+    if (mode >= 1) return finish_reduce(scratch, grid, mode == 2 ? 2 : 1, dots, st);
+    return 0;
+  }
   const int tx = (g.bx + TX - 1) / TX, ty = (g.by + TY - 1) / TY;
   const int64_t units = (int64_t)tx * ty * g.bz;
   // one full wave: SMs x resident CTAs (smem-limited to 5 of 41 KB), fewer for tiny blocks
   const int64_t want = (int64_t)kNumSM * 5;
   const int grid = (int)(units / 8 < want ? (units / 8 > 0 ? units / 8 : 1) : want);
-  cudaStream_t st = as_stream(stream);
   switch (mode) {
     case 0: k_spmv<0><<<grid, TX * TY, 0, st>>>(g, alpha, boundary, x, y, w, scratch, tx, ty); break;
     case 1: k_spmv<1><<<grid, TX * TY, 0, st>>>(g, alpha, boundary, x, y, w, scratch, tx, ty); break;
@@ -247,6 +592,7 @@ extern "C" int fmp_stencil_apply(const fmp_block* blk, double alpha, int boundar
   if (mode >= 1) return finish_reduce(scratch, grid, mode == 2 ? 2 : 1, dots, st);
   return 0;
 }
+
 
 extern "C" int fmp_curl(const fmp_block* blk, int kind, const double* x, double* out, void* stream) {
   if (int e = check_block(blk)) return e;
