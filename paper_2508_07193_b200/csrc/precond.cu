@@ -24,6 +24,7 @@
 #include <cublas_v2.h>
 #include "common.cuh"
 #include "ozaki.cuh"
+#include "tma.cuh"
 
 namespace fmp {
 
@@ -1045,86 +1046,198 @@ struct FaceArgs {
 
 __device__ __forceinline__ int ext_of(const SubD& d, int a) { return a == 0 ? d.ex : (a == 1 ? d.ey : d.ez); }
 
+// Small dense products of the face kernels on the FP64 tensor cores: C = op(A) op(B) for
+// zero-padded NT*8 x NT*8 matrices in shared memory (row stride NT*8+4, == 4 mod 8: the
+// fragment loads are bank-conflict free in either orientation); warps take 8x8 output tiles.
+template <int NT>
+struct FaceMat {
+  static constexpr int N = NT * 8, S = N + 4, WORDS = N * S;
+};
+template <int NT, bool TA, bool TB>
+__device__ __forceinline__ void face_mm(const double* A, const double* B, double* C, int warp, int nwarps,
+                                        int lane) {
+  constexpr int S = FaceMat<NT>::S;
+  const int g = lane >> 2, t = lane & 3;
+  for (int tile = warp; tile < NT * NT; tile += nwarps) {
+    const int m0 = (tile / NT) * 8, n0 = (tile % NT) * 8;
+    double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+    for (int k = 0; k < NT * 8; k += 4) {
+      const double a = TA ? A[(k + t) * S + m0 + g] : A[(m0 + g) * S + k + t];
+      const double b = TB ? B[(n0 + g) * S + k + t] : B[(k + t) * S + n0 + g];
+      dmma884(d0, d1, a, b);
+    }
+    C[(m0 + g) * S + n0 + 2 * t] = d0;
+    C[(m0 + g) * S + n0 + 2 * t + 1] = d1;
+  }
+}
+// zero-padded copy of the row-major n x n factor f into M (N x S)
+template <int NT>
+__device__ __forceinline__ void face_load_factor(double* M, const double* f, int n, int tid, int nth) {
+  constexpr int N = FaceMat<NT>::N, S = FaceMat<NT>::S;
+  for (int q = tid; q < N * S; q += nth) {
+    const int r = q / S, cc = q - r * S;
+    M[q] = (r < n && cc < n) ? __ldg(f + r * n + cc) : 0.0;
+  }
+}
+
 // K5: Y[:, col] = e0 on the two faces per component, e0 = G^-1 y^ evaluated only there.
 // Projection along the face normal with weights F_n[t][0] (inverse factor row 0), then
-// a 2-D inverse transform over the in-plane axes.  One CTA streams one component of one
-// subdomain (y^ read once, FC planes per chunk); all operands of the small transforms are
-// in shared memory, laid out so every warp access is contiguous or a broadcast.
-constexpr int FACE_THREADS = 256;
-constexpr int FACE_CHUNK = 4 * 1156;   // doubles of y^ staged per chunk (4 planes of 34^2)
+// a 2-D inverse transform over the in-plane axes (two DMMA products).  One CTA per
+// (component, subdomain).  A producer warp streams the component's y^ planes (contiguous,
+// 32-byte padded) into a shared-memory ring with one cp.async.bulk each (full/empty
+// mbarriers); consumer warp w owns the rows b = w, w+8, ... of every plane and lane l the
+// columns a = l, l+32, l+64, so no projection needs a CTA barrier per plane:
+//   z-normal [b][a] = sum_z w_z[z] y^[z][b][a]   accumulated in place in shared memory
+//                                                (every element owned by one thread);
+//   x-normal [z][b] = sum_a w_x[a] y^[z][b][a]   a warp-shuffle reduction per row;
+//   y-normal [z][a] = sum_b w_y[b] y^[z][b][a]   per-warp partials over the warp's rows,
+//                                                summed over warps in a fixed order once per
+//                                                chunk of FZ planes (consumer-only barrier).
+constexpr int FACE_WARPS = 8;                       // consumer warps
+constexpr int FACE_THREADS = (FACE_WARPS + 1) * 32; // + producer warp
+constexpr int FZ = 4;                               // planes per y-normal partial chunk
+template <int NT>
+struct FaceRing {
+  static constexpr int NS = NT <= 5 ? 4 : 2;                      // ring slots
+  static constexpr int SLOT = (FaceMat<NT>::N * FaceMat<NT>::N + 15) / 16 * 16;   // >= padded plane stride
+  // work region: max(Fu, Fv, temp) during the transforms vs ring + weights + partials
+  static constexpr int STREAM = NS * SLOT + 3 * FaceMat<NT>::N + FACE_WARPS * FZ * FaceMat<NT>::N;
+  static constexpr int WORK = STREAM > 3 * FaceMat<NT>::WORDS ? STREAM : 3 * FaceMat<NT>::WORDS;
+};
+template <int NT>
+constexpr int face_smem_words() { return 2 * FaceMat<NT>::WORDS + FaceRing<NT>::WORK; }
 
-__global__ void __launch_bounds__(FACE_THREADS) k_faces(FaceArgs A) {
-  extern __shared__ __align__(16) double smem[];
+// One staged y^ plane of the face projections (consumer warp `warp` of FACE_WARPS): all row
+// loads first, then the z-normal update, the y-normal partial and the x-normal row sums with
+// the FR shuffle reductions interleaved (independent chains, no early exit).
+template <int FR, int FA, int S>
+__device__ __forceinline__ void face_plane(const double* pl, int z, int ex, int ey, bool zn, bool xn, double wz,
+                                           const double* Wy, const double (&wx)[FA], double* sA, double* sB,
+                                           double (&yp)[FA], int warp, int lane) {
+  double val[FR][FA];
+#pragma unroll
+  for (int r = 0; r < FR; ++r)
+#pragma unroll
+    for (int h = 0; h < FA; ++h) {
+      const int b = warp + FACE_WARPS * r, a = lane + 32 * h;
+      val[r][h] = (b < ey && a < ex) ? pl[b * ex + a] : 0.0;
+    }
+  if (zn) {
+#pragma unroll
+    for (int r = 0; r < FR; ++r)
+#pragma unroll
+      for (int h = 0; h < FA; ++h) {
+        const int b = warp + FACE_WARPS * r, a = lane + 32 * h;
+        if (b < ey && a < ex) sA[b * S + a] += wz * val[r][h];
+      }
+  }
+#pragma unroll
+  for (int h = 0; h < FA; ++h) yp[h] = 0.0;
+#pragma unroll
+  for (int r = 0; r < FR; ++r) {
+    const int b = warp + FACE_WARPS * r;
+    const double wy = b < ey ? Wy[b] : 0.0;
+#pragma unroll
+    for (int h = 0; h < FA; ++h) yp[h] += wy * val[r][h];
+  }
+  if (xn) {
+    double xs[FR];
+#pragma unroll
+    for (int r = 0; r < FR; ++r) {
+      xs[r] = 0.0;
+#pragma unroll
+      for (int h = 0; h < FA; ++h) xs[r] += wx[h] * val[r][h];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+      for (int r = 0; r < FR; ++r) xs[r] += __shfl_xor_sync(0xffffffffu, xs[r], o);
+#pragma unroll
+    for (int r = 0; r < FR; ++r) {
+      const int b = warp + FACE_WARPS * r;
+      if (lane == r && b < ey) sB[z * S + b] = xs[r];
+    }
+  }
+}
+
+// FR rows per warp, FA columns per lane, NT 8-wide tiles per padded extent (register and
+// shared-memory footprints sized for the plan's extents)
+template <int FR, int FA, int NT>
+__global__ void __launch_bounds__(FACE_THREADS, NT <= 5 ? 2 : 1) k_faces(FaceArgs A) {
+  extern __shared__ __align__(128) double smem[];
+  __shared__ __align__(8) uint64_t full[FaceRing<NT>::NS], empty[FaceRing<NT>::NS];
+  constexpr int S = FaceMat<NT>::S, W = FaceMat<NT>::WORDS, N = FaceMat<NT>::N;
+  constexpr int NS = FaceRing<NT>::NS, SLOT = FaceRing<NT>::SLOT;
   const SubD d = load_sub(A.subs + blockIdx.y);
   const fmp_shape& sh = A.shapes[d.shape];
-  const int c = blockIdx.x, tid = threadIdx.x;
-  const int ex = d.ex, ey = d.ey, ez = d.ez, P = ex * ey;
-  const int pm = A.pmax, pm2 = pm * pm;
+  const int c = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int ex = d.ex, ey = d.ey, ez = d.ez;
   const int ext[3] = {ex, ey, ez};
-  double* sF = smem;                 // 3 x [n][n] forward factors of component c (row-major)
-  double* sA = sF + 3 * pm2;         // primary projection   [u1][v1]
-  double* sB = sA + pm2;             // secondary projection [u2][v2]
-  double* sT = sB + pm2;             // temp
-  double* sC = sT + pm2;             // staged y^ planes
-  for (int a = 0; a < 3; ++a) {
-    const double* f = fwd_factor(A.factors, sh, c, a);
-    for (int q = tid; q < ext[a] * ext[a]; q += FACE_THREADS) sF[a * pm2 + q] = __ldg(f + q);
-  }
-  const FaceGeo fg = face_geo(c);
-  for (int q = tid; q < pm2; q += FACE_THREADS) sA[q] = 0.0;
-  const double* Wz = sF + 2 * pm2;   // weights F_n[t][0] = sF[n][t*n_n]
-  const double* Wy = sF + 1 * pm2;
-  const double* Wx = sF;
+  double* sA = smem;                 // primary projection   [u1][v1]
+  double* sB = sA + W;               // secondary projection [u2][v2]
+  double* sX = sB + W;               // streaming: ring, weights, partials; transforms: Fu, Fv, temp
+  double* ring = sX;
+  double* sWt = ring + NS * SLOT;    // weights F_n[t][0] of axis n at sWt[n * N + t]
+  double* sP = sWt + 3 * N;          // y-normal partials [warp][FZ][N]
   const double* src = A.yhat + d.ws_off + (int64_t)c * d.cstride();
-  // two staging buffers of FACE_CHUNK/2 doubles: chunk i+1 streams in (16-byte cp.async of the
-  // 32-byte aligned, padded workspace planes) while chunk i is reduced
-  const int stage = max(FACE_CHUNK / 2, A.max_ps);
-  const int nz = max(1, min(ez, stage / d.ps));
-  const int nchunks = (ez + nz - 1) / nz;
-  auto issue = [&](int ci) {
-    const int c0 = ci * nz, n = min(nz, ez - c0);
-    double* buf = sC + (ci & 1) * stage;
-    const int half = d.ps / 2;   // 16-byte chunks per padded plane
-    for (int kk = 0; kk < n; ++kk)
-      for (int q = tid; q < half; q += FACE_THREADS)
-        cp_async16(buf + kk * d.ps + 2 * q, src + (int64_t)(c0 + kk) * d.ps + 2 * q);
-  };
-  issue(0);
-  cp_async_commit();
-  for (int ci = 0; ci < nchunks; ++ci) {
-    const int c0 = ci * nz, n = min(nz, ez - c0);
-    __syncthreads();   // buffer (ci+1)&1 is no longer read
-    if (ci + 1 < nchunks) issue(ci + 1);
-    cp_async_commit();
-    cp_async_wait<1>();
-    __syncthreads();
-    const double* chunk = sC + (ci & 1) * stage;
-    const int P2 = d.ps;   // staged plane stride
-    if (fg.n1 == 2) {   // components x, y: z-normal face, sA[b][a] += sum_cz w[cz] y^[cz][b][a]
-      for (int q = tid; q < P; q += FACE_THREADS) {
-        double acc = sA[q];
-        for (int kk = 0; kk < n; ++kk) acc += Wz[(c0 + kk) * ez] * chunk[kk * P2 + q];
-        sA[q] = acc;
-      }
+  if (tid == 0) {
+    for (int q = 0; q < NS; ++q) {
+      mbar_init(&full[q], 1);
+      mbar_init(&empty[q], FACE_WARPS);
     }
-    // y-normal projection: [cz][a] = sum_b w[b] y^[cz][b][a]   (primary for z, secondary for x)
-    if (fg.n1 == 1 || fg.n2 == 1) {
-      double* dst = fg.n1 == 1 ? sA : sB;
-      for (int q = tid; q < n * ex; q += FACE_THREADS) {
-        const int kk = q / ex, a = q - kk * ex;
-        double acc = 0.0;
-        for (int b = 0; b < ey; ++b) acc += Wy[b * ey] * chunk[kk * P2 + b * ex + a];
-        dst[(c0 + kk) * ex + a] = acc;
+    fence_mbar_init();
+  }
+  for (int q = tid; q < 3 * N; q += FACE_THREADS) {
+    const int n = q / N, t = q - n * N;
+    sWt[q] = t < ext[n] ? __ldg(fwd_factor(A.factors, sh, c, n) + t * ext[n]) : 0.0;
+  }
+  for (int q = tid; q < 2 * W; q += FACE_THREADS) sA[q] = 0.0;   // sA, sB: zero padding
+  const FaceGeo fg = face_geo(c);
+  const bool zn = fg.n1 == 2, yn = fg.n1 == 1 || fg.n2 == 1, xn = fg.n2 == 0;
+  double* sY = fg.n1 == 1 ? sA : sB;   // y-normal destination [z][a]
+  __syncthreads();
+  if (warp == FACE_WARPS) {
+    // ---------------- producer: one bulk copy per z-plane
+    if (lane == 0)
+      for (int z = 0; z < ez; ++z) {
+        const int slot = z % NS;
+        if (z >= NS) mbar_wait(&empty[slot], (uint32_t)(((z / NS) - 1) & 1));
+        mbar_expect_tx(&full[slot], (uint32_t)d.ps * 8);
+        bulk_g2s(ring + slot * SLOT, src + (int64_t)z * d.ps, (uint32_t)d.ps * 8, &full[slot]);
       }
-    }
-    // x-normal projection: [cz][b] = sum_a w[a] y^[cz][b][a]   (secondary for y, z)
-    if (fg.n2 == 0) {
-      for (int q = tid; q < n * ey; q += FACE_THREADS) {
-        const int kk = q / ey, b = q - kk * ey;
-        double acc = 0.0;
-        const double* row = chunk + kk * P2 + b * ex;
-        for (int a = 0; a < ex; ++a) acc += Wx[a * ex] * row[a];
-        sB[(c0 + kk) * ey + b] = acc;
+  } else {
+    // ---------------- consumers
+    const double* Wz = sWt + 2 * N;
+    const double* Wy = sWt + N;
+    double wx[FA];
+#pragma unroll
+    for (int h = 0; h < FA; ++h) wx[h] = lane + 32 * h < N ? sWt[lane + 32 * h] : 0.0;
+    for (int z0 = 0; z0 < ez; z0 += FZ) {
+      const int nzc = min(FZ, ez - z0);
+      for (int zz = 0; zz < nzc; ++zz) {
+        const int z = z0 + zz, slot = z % NS;
+        mbar_wait(&full[slot], (uint32_t)((z / NS) & 1));
+        const double* pl = ring + slot * SLOT;
+        double yp[FA];
+        face_plane<FR, FA, S>(pl, z, ex, ey, zn, xn, Wz[z], Wy, wx, sA, sB, yp, warp, lane);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[slot]);
+        if (yn) {
+#pragma unroll
+          for (int h = 0; h < FA; ++h)
+            if (lane + 32 * h < ex) sP[(warp * FZ + zz) * N + lane + 32 * h] = yp[h];
+        }
+      }
+      if (yn) {
+        asm volatile("bar.sync 1, %0;\n" ::"n"(FACE_WARPS * 32) : "memory");
+        for (int q = tid; q < nzc * ex; q += FACE_WARPS * 32) {
+          const int zz = q / ex, a = q - zz * ex;
+          double acc = 0.0;
+          for (int w = 0; w < FACE_WARPS; ++w) acc += sP[(w * FZ + zz) * N + a];
+          sY[(z0 + zz) * S + a] = acc;
+        }
+        asm volatile("bar.sync 1, %0;\n" ::"n"(FACE_WARPS * 32) : "memory");
       }
     }
   }
@@ -1135,52 +1248,43 @@ __global__ void __launch_bounds__(FACE_THREADS) k_faces(FaceArgs A) {
   for (int q = 0; q < c; ++q) base += (int)sh.m_comp[q];
   for (int f = 0; f < 2; ++f) {
     const int ua = f == 0 ? fg.u1 : fg.u2, va = f == 0 ? fg.v1 : fg.v2;
-    const int nu = ext[ua], nv = ext[va];
-    const double* Fu = sF + ua * pm2;
-    const double* Fv = sF + va * pm2;
-    const double* Pj = f == 0 ? sA : sB;   // [tu][tv], row stride nv
-    for (int q = tid; q < nu * nv; q += FACE_THREADS) {   // T[tu][v] = sum_tv Pj[tu][tv] Fv[tv][v]
-      const int tu = q / nv, v = q - tu * nv;
-      double acc = 0.0;
-      for (int tv = 0; tv < nv; ++tv) acc += Pj[tu * nv + tv] * Fv[tv * nv + v];
-      sT[q] = acc;
-    }
+    const int nu = ext[ua], nv_ = ext[va];
+    double *sFu = sX, *sFv = sX + W, *sT = sX + 2 * W;
+    face_load_factor<NT>(sFu, fwd_factor(A.factors, sh, c, ua), nu, tid, FACE_THREADS);
+    face_load_factor<NT>(sFv, fwd_factor(A.factors, sh, c, va), nv_, tid, FACE_THREADS);
     __syncthreads();
-    for (int q = tid; q < nu * nv; q += FACE_THREADS) {   // E[u][v] = sum_tu Fu[tu][u] T[tu][v]
-      const int u = q / nv, v = q - u * nv;
-      const int row = face_row(c, f, u, v, ex, ey);
-      if (row < 0) continue;
-      double acc = 0.0;
-      for (int tu = 0; tu < nu; ++tu) acc += Fu[tu * nu + u] * sT[tu * nv + v];
-      Y[base + row] = acc;
+    face_mm<NT, false, false>(f == 0 ? sA : sB, sFv, sT, warp, FACE_THREADS / 32, lane);   // T = Proj Fv
+    __syncthreads();
+    double* E = f == 0 ? sA : sB;                                                  // E = Fu^T T
+    face_mm<NT, true, false>(sFu, sT, E, warp, FACE_THREADS / 32, lane);
+    __syncthreads();
+    for (int q = tid; q < nu * nv_; q += FACE_THREADS) {
+      const int u = q / nv_, vv = q - u * nv_;
+      const int row = face_row(c, f, u, vv, ex, ey);
+      if (row >= 0) Y[base + row] = E[u * S + vv];
     }
     __syncthreads();
   }
 }
 
 // K6: from Z (C^-1 Y) build, per component and face, the forward-transformed face plane
-// Proj[tu][tv] = sum_{u,v} Fu[tu][u] Fv[tv][v] Zface[u][v]  -> corr planes (see K3).
+// Proj[tu][tv] = sum_{u,v} Fu[tu][u] Fv[tv][v] Zface[u][v]  -> corr planes (see K3);
+// the two products on DMMA.
+template <int NT>
 __global__ void __launch_bounds__(FACE_THREADS) k_corr(FaceArgs A) {
   extern __shared__ __align__(16) double smem[];
+  constexpr int S = FaceMat<NT>::S, W = FaceMat<NT>::WORDS;
   const SubD d = load_sub(A.subs + blockIdx.y);
   const fmp_shape& sh = A.shapes[d.shape];
-  const int c = blockIdx.x, tid = threadIdx.x;
+  const int c = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int ex = d.ex, ey = d.ey, ez = d.ez;
   const int ext[3] = {ex, ey, ez};
-  const int pm = A.pmax, pm2 = pm * pm;
-  double* sF = smem;          // 3 x [n][n] forward factors (row-major)
-  double* sFt = sF + 3 * pm2; // 3 x [n][n] their transposes
-  double* sZ = sFt + 3 * pm2; // [u][v]
-  double* sT = sZ + pm2;      // [u][tv]
-  for (int a = 0; a < 3; ++a) {
-    const double* f = fwd_factor(A.factors, sh, c, a);
-    const int n = ext[a];
-    for (int q = tid; q < n * n; q += FACE_THREADS) {
-      const double v = __ldg(f + q);
-      sF[a * pm2 + q] = v;
-      sFt[a * pm2 + (q % n) * n + q / n] = v;
-    }
-  }
+  const int pm = A.pmax;
+  double* sFu = smem;     // padded factors of the face's in-plane axes
+  double* sFv = sFu + W;
+  double* sZ = sFv + W;   // face values of Z, then the result
+  double* sT = sZ + W;
+  double* sO = sZ;
   const FaceGeo fg = face_geo(c);
   const double* Z = A.zmat[d.shape] + (int64_t)d.column * sh.ld;
   int base = 0;
@@ -1188,28 +1292,23 @@ __global__ void __launch_bounds__(FACE_THREADS) k_corr(FaceArgs A) {
   for (int f = 0; f < 2; ++f) {
     const int ua = f == 0 ? fg.u1 : fg.u2, va = f == 0 ? fg.v1 : fg.v2;
     const int nu = ext[ua], nv = ext[va];
-    const double* Fu = sF + ua * pm2;
-    const double* Fvt = sFt + va * pm2;
-    __syncthreads();
-    for (int q = tid; q < nu * nv; q += FACE_THREADS) {
-      const int u = q / nv, v = q - u * nv;
-      const int row = face_row(c, f, u, v, ex, ey);
+    __syncthreads();   // previous face's result has been written out
+    face_load_factor<NT>(sFu, fwd_factor(A.factors, sh, c, ua), nu, tid, FACE_THREADS);
+    face_load_factor<NT>(sFv, fwd_factor(A.factors, sh, c, va), nv, tid, FACE_THREADS);
+    for (int q = tid; q < W; q += FACE_THREADS) {
+      const int u = q / S, v = q - u * S;
+      const int row = (u < nu && v < nv) ? face_row(c, f, u, v, ex, ey) : -1;
       sZ[q] = row < 0 ? 0.0 : Z[base + row];
     }
     __syncthreads();
-    for (int q = tid; q < nu * nv; q += FACE_THREADS) {   // T[u][tv] = sum_v Z[u][v] Fv[tv][v]
-      const int u = q / nv, tv = q - u * nv;
-      double acc = 0.0;
-      for (int v = 0; v < nv; ++v) acc += sZ[u * nv + v] * Fvt[v * nv + tv];
-      sT[q] = acc;
-    }
+    face_mm<NT, false, true>(sZ, sFv, sT, warp, FACE_THREADS / 32, lane);    // T[u][tv] = sum_v Z[u][v] Fv[tv][v]
     __syncthreads();
-    double* out = A.corr + ((int64_t)blockIdx.y * 6 + c * 2 + f) * pm2;
-    for (int q = tid; q < nu * nv; q += FACE_THREADS) {   // Proj[tu][tv] = sum_u Fu[tu][u] T[u][tv]
+    face_mm<NT, false, false>(sFu, sT, sO, warp, FACE_THREADS / 32, lane);   // Proj = Fu T
+    __syncthreads();
+    double* out = A.corr + ((int64_t)blockIdx.y * 6 + c * 2 + f) * pm * pm;
+    for (int q = tid; q < nu * nv; q += FACE_THREADS) {
       const int tu = q / nv, tv = q - tu * nv;
-      double acc = 0.0;
-      for (int u = 0; u < nu; ++u) acc += Fu[tu * nu + u] * sT[u * nv + tv];
-      out[tu * pm + tv] = acc;
+      out[tu * pm + tv] = sO[tu * S + tv];
     }
   }
 }
@@ -1505,8 +1604,10 @@ extern "C" int fmp_precond_create(const fmp_precond_desc* desc, fmp_precond** ou
   cudaFuncSetAttribute(k_column_fast<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kColFastSmem);
   cudaFuncSetAttribute(k_column_fast<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kColFastSmem);
   cudaFuncSetAttribute(k_column_fast_db<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kColFastSmemDb);
-  cudaFuncSetAttribute(k_faces, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-  cudaFuncSetAttribute(k_corr, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(k_faces<5, 2, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize, face_smem_words<5>() * 8);
+  cudaFuncSetAttribute(k_faces<9, 3, 9>, cudaFuncAttributeMaxDynamicSharedMemorySize, face_smem_words<9>() * 8);
+  cudaFuncSetAttribute(k_corr<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * FaceMat<5>::WORDS * 8);
+  cudaFuncSetAttribute(k_corr<9>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * FaceMat<9>::WORDS * 8);
   FMP_CHECK_CUDA(cudaGetLastError());
   *out = p;
   return 0;
@@ -1623,9 +1724,11 @@ extern "C" int fmp_precond_apply(fmp_precond* p, const fmp_block* blk, int mode,
   const int pm = (int)p->d.pmax;
   FaceArgs fa{p->d.subs, p->d.shapes, p->d.factors, wb, p->d.corr, p->d_ymat, p->d_zmat, pm, (p->max_p + 3) & ~3};
   if (mode != FMP_SOLVE_EXACT) {
-    const size_t stage = std::max<size_t>(FACE_CHUNK / 2, (size_t)((p->max_p + 3) & ~3));
-    const size_t fs = (6 * (size_t)pm * pm + 2 * stage) * sizeof(double);
-    k_faces<<<dim3(3, (unsigned)p->d.n_sub), FACE_THREADS, fs, st>>>(fa);
+    const dim3 fg(3, (unsigned)p->d.n_sub);
+    if (pm <= 40)
+      k_faces<5, 2, 5><<<fg, FACE_THREADS, face_smem_words<5>() * sizeof(double), st>>>(fa);
+    else
+      k_faces<9, 3, 9><<<fg, FACE_THREADS, face_smem_words<9>() * sizeof(double), st>>>(fa);
     FMP_CHECK_LAUNCH();
   }
   if (mode == FMP_SOLVE_FACES) return 0;
@@ -1658,7 +1761,10 @@ extern "C" int fmp_precond_apply(fmp_precond* p, const fmp_block* blk, int mode,
       for (int c = 0; c < 3; ++c)
         if (int e = gemm_launch(c, p->d_gshapes, p->d_gtiles[c], p->n_gtiles[c], p->sms, st)) return e;
     }
-    k_corr<<<dim3(3, (unsigned)p->d.n_sub), FACE_THREADS, 8 * (size_t)pm * pm * sizeof(double), st>>>(fa);
+    if (pm <= 40)
+      k_corr<5><<<dim3(3, (unsigned)p->d.n_sub), FACE_THREADS, 4 * FaceMat<5>::WORDS * sizeof(double), st>>>(fa);
+    else
+      k_corr<9><<<dim3(3, (unsigned)p->d.n_sub), FACE_THREADS, 4 * FaceMat<9>::WORDS * sizeof(double), st>>>(fa);
     FMP_CHECK_LAUNCH();
   }
   if (int e = column_pass(p, true, wb, wa, mode == FMP_SOLVE_WOODBURY ? p->d.corr : nullptr, st)) return e;
