@@ -131,7 +131,12 @@ typedef struct fmp_shape {       /* 20 x int64 */
                             q = 1/(1+alpha|s|^2), w = (1-q)/|s|^2  so  B^-1 y = q y + w s (s.y) */
   int64_t ld;            /* row stride of C^-1 [m][ld], Y and Z [n_s][ld]: m rounded up to 4,
                             padding zero-filled */
-  int64_t reserved[2];
+  int64_t group;         /* shape whose C^-1, Y and Z this shape shares (itself if canonical).
+                            Shapes that are cyclic axis rotations of each other have C matrices
+                            equal up to a row/column permutation, so one C^-1 and one GEMM serve
+                            the whole group; members use disjoint Y/Z columns (fmp_subdomain.column) */
+  int64_t rowmap_off;    /* offset into desc->rowmap of this shape's map from its own correction
+                            rows to the group's rows (m int32 entries), or -1 for the identity */
 } fmp_shape;
 #define FMP_SUBDOMAIN_WORDS 16
 #define FMP_SHAPE_WORDS 20
@@ -145,13 +150,15 @@ typedef struct fmp_precond_desc {
   const fmp_shape* shapes_host;  /* host copy */
   const int64_t* shape_first;    /* host: first subdomain of each shape (n_shape+1 entries) */
   const double* factors;         /* device: concatenated U^T, V^T, S blocks */
-  const double* const* cinv;     /* host array of n_shape device pointers to C^-1, [m][ld] */
+  const double* const* cinv;     /* host array of n_shape device pointers to C^-1, [m][ld]
+                                    (members of a group pass the group's pointer) */
   double* work_a;                /* device workspace, >= sum 3*V_ext (+ padding) doubles */
   double* work_b;                /* device workspace, same size */
   double* corr;                  /* device: n_sub * 6 * pmax^2 doubles (correction planes) */
-  double* const* ymat;           /* host array of n_shape device pointers, [n_s][ld] each */
-  double* const* zmat;           /* host array of n_shape device pointers, [n_s][ld] each */
+  double* const* ymat;           /* host array of n_shape device pointers, [n_group_cols][ld] each */
+  double* const* zmat;           /* host array of n_shape device pointers, [n_group_cols][ld] each */
   int64_t pmax;                  /* max extent over all shapes */
+  const int32_t* rowmap;         /* device: concatenated row maps of non-canonical shapes (may be NULL) */
 } fmp_precond_desc;
 
 typedef struct fmp_precond fmp_precond;

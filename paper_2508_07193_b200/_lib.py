@@ -56,7 +56,7 @@ class FmpPrecondDesc(C.Structure):
                 ("subs_host", C.c_void_p), ("shapes_host", C.c_void_p),
                 ("shape_first", C.c_void_p), ("factors", C.c_void_p), ("cinv", C.c_void_p),
                 ("work_a", C.c_void_p), ("work_b", C.c_void_p), ("corr", C.c_void_p),
-                ("ymat", C.c_void_p), ("zmat", C.c_void_p), ("pmax", C.c_int64)]
+                ("ymat", C.c_void_p), ("zmat", C.c_void_p), ("pmax", C.c_int64), ("rowmap", C.c_void_p)]
 
 
 class FlashMPError(RuntimeError):

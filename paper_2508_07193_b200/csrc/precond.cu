@@ -1042,6 +1042,7 @@ struct FaceArgs {
   const double* const* zmat;   // device array of per-shape Z pointers (K6 in)
   int pmax;
   int max_ps;                  // largest padded plane stride of the plan
+  const int* rowmap;           // shape row -> group row maps (fmp_shape::rowmap_off), may be null
 };
 
 __device__ __forceinline__ int ext_of(const SubD& d, int a) { return a == 0 ? d.ex : (a == 1 ? d.ey : d.ez); }
@@ -1244,6 +1245,7 @@ __global__ void __launch_bounds__(FACE_THREADS, NT <= 5 ? 2 : 1) k_faces(FaceArg
   __syncthreads();
   // 2-D inverse transforms: E[u][v] = sum_tu Fu[tu][u] sum_tv Fv[tv][v] Proj[tu][tv]
   double* Y = A.ymat[d.shape] + (int64_t)d.column * sh.ld;
+  const int* rm = sh.rowmap_off >= 0 ? A.rowmap + sh.rowmap_off : nullptr;
   int base = 0;
   for (int q = 0; q < c; ++q) base += (int)sh.m_comp[q];
   for (int f = 0; f < 2; ++f) {
@@ -1261,7 +1263,7 @@ __global__ void __launch_bounds__(FACE_THREADS, NT <= 5 ? 2 : 1) k_faces(FaceArg
     for (int q = tid; q < nu * nv_; q += FACE_THREADS) {
       const int u = q / nv_, vv = q - u * nv_;
       const int row = face_row(c, f, u, vv, ex, ey);
-      if (row >= 0) Y[base + row] = E[u * S + vv];
+      if (row >= 0) Y[rm ? rm[base + row] : base + row] = E[u * S + vv];
     }
     __syncthreads();
   }
@@ -1287,6 +1289,7 @@ __global__ void __launch_bounds__(FACE_THREADS) k_corr(FaceArgs A) {
   double* sO = sZ;
   const FaceGeo fg = face_geo(c);
   const double* Z = A.zmat[d.shape] + (int64_t)d.column * sh.ld;
+  const int* rm = sh.rowmap_off >= 0 ? A.rowmap + sh.rowmap_off : nullptr;
   int base = 0;
   for (int q = 0; q < c; ++q) base += (int)sh.m_comp[q];
   for (int f = 0; f < 2; ++f) {
@@ -1298,7 +1301,7 @@ __global__ void __launch_bounds__(FACE_THREADS) k_corr(FaceArgs A) {
     for (int q = tid; q < W; q += FACE_THREADS) {
       const int u = q / S, v = q - u * S;
       const int row = (u < nu && v < nv) ? face_row(c, f, u, v, ex, ey) : -1;
-      sZ[q] = row < 0 ? 0.0 : Z[base + row];
+      sZ[q] = row < 0 ? 0.0 : Z[rm ? rm[base + row] : base + row];
     }
     __syncthreads();
     face_mm<NT, false, true>(sZ, sFv, sT, warp, FACE_THREADS / 32, lane);    // T[u][tv] = sum_v Z[u][v] Fv[tv][v]
@@ -1353,7 +1356,8 @@ struct fmp_precond {
   cudaStream_t aux[kAux] = {};
   cublasHandle_t aux_blas[kAux] = {};
   cudaEvent_t ev_fork = nullptr, ev_join[kAux] = {};
-  std::vector<int> gemm_order;            // shapes by decreasing GEMM size
+  std::vector<int> gemm_order;            // canonical shapes by decreasing GEMM size
+  std::vector<int> gcols;                 // Y/Z columns of each rotation group (0 for members)
   GemmShape* d_gshapes = nullptr;
   GemmTile* d_gtiles[3] = {nullptr, nullptr, nullptr};
   int n_gtiles[3] = {0, 0, 0};
@@ -1501,6 +1505,16 @@ extern "C" int fmp_precond_create(const fmp_precond_desc* desc, fmp_precond** ou
     free_plan(p);
     return -1;
   }
+  // rotation groups: one C^-1 / Y / Z / GEMM per group, n = all member columns
+  p->gcols.assign(desc->n_shape, 0);
+  for (int64_t s2 = 0; s2 < desc->n_shape; ++s2) {
+    const auto& sh = p->shapes[s2];
+    const int64_t g = sh.group;
+    FMP_REQUIRE(g >= 0 && g < desc->n_shape && p->shapes[g].group == g && p->shapes[g].m == sh.m &&
+                    p->shapes[g].ld == sh.ld && (g == s2 || (sh.rowmap_off >= 0 && desc->rowmap)),
+                "shape %lld: invalid rotation group %lld", (long long)s2, (long long)g);
+    p->gcols[g] += (int)(p->first[s2 + 1] - p->first[s2]);
+  }
   {  // grouped GEMM tables: one shape record per extended shape, tiles bucketed by configuration
     const char* gm = getenv("FMP_GEMM");
     const std::string gmode = gm ? gm : "ozaki";   // cublas | own | ozaki
@@ -1510,7 +1524,7 @@ extern "C" int fmp_precond_create(const fmp_precond_desc* desc, fmp_precond** ou
     std::vector<GemmTile> gt[3];
     for (int64_t s2 = 0; s2 < desc->n_shape; ++s2) {
       const auto& sh = p->shapes[s2];
-      const int n = (int)(p->first[s2 + 1] - p->first[s2]);
+      const int n = p->gcols[s2];
       gs.push_back(GemmShape{p->cinv[s2], p->ymat[s2], p->zmat[s2], (int)sh.m, n, (int)sh.ld});
       if (n == 0) continue;
       const int cfg = gemm_config_of(n), mt = gemm_tile_m(cfg), nt = gemm_tile_n(cfg);
@@ -1533,7 +1547,11 @@ extern "C" int fmp_precond_create(const fmp_precond_desc* desc, fmp_precond** ou
     std::vector<OzSlice> sa, sb;
     for (int64_t s2 = 0; s2 < desc->n_shape; ++s2) {
       const auto& sh = p->shapes[s2];
-      const int m = (int)sh.m, n = (int)(p->first[s2 + 1] - p->first[s2]), kc = ozaki_kchunks(m);
+      if (sh.group != s2) {   // member of a rotation group: the canonical shape's GEMM covers it
+        os.push_back(OzShape{});
+        continue;
+      }
+      const int m = (int)sh.m, n = p->gcols[s2], kc = ozaki_kchunks(m);
       FMP_REQUIRE(kc > 0, "Ozaki GEMM: correction size m = %d exceeds the int32 accumulator range", m);
       const int w = ozaki_width(std::max(n, 1));
       int8_t *a = nullptr, *b = nullptr;
@@ -1590,10 +1608,10 @@ extern "C" int fmp_precond_create(const fmp_precond_desc* desc, fmp_precond** ou
     FMP_REQUIRE(false, "event creation failed");
   }
   for (int64_t s2 = 0; s2 < desc->n_shape; ++s2)
-    if (p->first[s2 + 1] > p->first[s2]) p->gemm_order.push_back((int)s2);
+    if (p->gcols[s2] > 0) p->gemm_order.push_back((int)s2);
   std::sort(p->gemm_order.begin(), p->gemm_order.end(), [&](int a, int b) {
-    const double fa = (double)p->shapes[a].m * p->shapes[a].m * (double)(p->first[a + 1] - p->first[a]);
-    const double fb = (double)p->shapes[b].m * p->shapes[b].m * (double)(p->first[b + 1] - p->first[b]);
+    const double fa = (double)p->shapes[a].m * p->shapes[a].m * (double)p->gcols[a];
+    const double fb = (double)p->shapes[b].m * p->shapes[b].m * (double)p->gcols[b];
     return fa > fb;
   });
   plane_attr<false, 5>(); plane_attr<true, 5>(); plane_attr<false, 9>(); plane_attr<true, 9>();
@@ -1722,7 +1740,8 @@ extern "C" int fmp_precond_apply(fmp_precond* p, const fmp_block* blk, int mode,
   if (int e = plane_pass(p, blk, false, mode, r, wa, st)) return e;
   if (int e = column_pass(p, false, wa, wb, nullptr, st)) return e;
   const int pm = (int)p->d.pmax;
-  FaceArgs fa{p->d.subs, p->d.shapes, p->d.factors, wb, p->d.corr, p->d_ymat, p->d_zmat, pm, (p->max_p + 3) & ~3};
+  FaceArgs fa{p->d.subs, p->d.shapes, p->d.factors, wb, p->d.corr, p->d_ymat, p->d_zmat, pm, (p->max_p + 3) & ~3,
+              p->d.rowmap};
   if (mode != FMP_SOLVE_EXACT) {
     const dim3 fg(3, (unsigned)p->d.n_sub);
     if (pm <= 40)
@@ -1743,7 +1762,7 @@ extern "C" int fmp_precond_apply(fmp_precond* p, const fmp_block* blk, int mode,
       for (size_t o = 0; o < p->gemm_order.size(); ++o) {
         const int s = p->gemm_order[o];
         const int m = (int)p->shapes[s].m, ld = (int)p->shapes[s].ld;
-        const int ncol = (int)(p->first[s + 1] - p->first[s]);
+        const int ncol = p->gcols[s];
         // C^-1 is row-major [m][ld]; OP_T makes cuBLAS use it as is.
         cublasStatus_t bs = cublasDgemm(p->aux_blas[o % naux], CUBLAS_OP_T, CUBLAS_OP_N, m, ncol, m, &one,
                                         p->cinv[s], ld, p->ymat[s], ld, &zero, p->zmat[s], ld);

@@ -45,6 +45,69 @@ def pad_rows(t: torch.Tensor, ld: int) -> torch.Tensor:
     return out
 
 
+def rotate(ext):
+    """Cyclic axis rotation (x, y, z) -> (y, z, x) of a box: new x' = old y, y' = z, z' = x."""
+    return (ext[1], ext[2], ext[0])
+
+
+def rotation_groups(shapes) -> list[tuple[int, int]]:
+    """(index of the group's canonical shape, t) for every shape, with shape = rotate^t(canonical).
+
+    The double-curl operator is invariant under cyclic relabelling of the axes (component
+    x -> z', y -> x', z -> y', point (i, j, k) -> (j, k, i)), and so are the boundary deltas,
+    so the Woodbury matrices of rotated boxes are equal up to a permutation of their rows and
+    columns (checked in tests/test_host.py).  One C^-1 and one GEMM then serve a whole group."""
+    out = []
+    for q, e in enumerate(shapes):
+        hit = None
+        for g, (rep, t) in enumerate(out):
+            if rep != g:
+                continue
+            r = shapes[g]
+            for tt in (1, 2):
+                r = rotate(r)
+                if r == e and r != shapes[g]:
+                    hit = (g, tt)
+                    break
+            if hit:
+                break
+        out.append(hit if hit else (q, 0))
+    return out
+
+
+def correction_points(ext) -> np.ndarray:
+    """(m, 4) int array of (c, i, j, k) per correction row, in row order
+    (component-major, ascending linear index: ref:subdomain.py:183-194)."""
+    nx, ny, nz = ext
+    k, j, i = np.meshgrid(np.arange(nz), np.arange(ny), np.arange(nx), indexing="ij")
+    i0, j0, k0 = i == 0, j == 0, k == 0
+    pts = []
+    for c, w in enumerate(((j0 | k0), (i0 | k0), (i0 | j0))):
+        idx = np.flatnonzero(w.ravel())
+        pts.append(np.stack([np.full(idx.size, c), i.ravel()[idx], j.ravel()[idx], k.ravel()[idx]], axis=1))
+    return np.concatenate(pts).astype(np.int64)
+
+
+def rotation_rowmap(rep, t: int) -> np.ndarray:
+    """int32 map from the correction rows of rotate^t(rep) to the rows of rep."""
+    pts = correction_points(rep)
+    e = tuple(rep)
+    for _ in range(t):
+        c, i, j, k = pts.T
+        pts = np.stack([(c + 2) % 3, j, k, i], axis=1)
+        e = rotate(e)
+    nx, ny, nz = e
+    V = nx * ny * nz
+    key_rep = pts[:, 0] * V + pts[:, 3] * nx * ny + pts[:, 2] * nx + pts[:, 1]   # rows of rep, in e's indices
+    own = correction_points(e)
+    key_own = own[:, 0] * V + own[:, 3] * nx * ny + own[:, 2] * nx + own[:, 1]
+    pos = np.full(3 * V, -1, dtype=np.int64)
+    pos[key_own] = np.arange(key_own.size)
+    rowmap = np.empty(key_own.size, dtype=np.int32)
+    rowmap[pos[key_rep]] = np.arange(key_rep.size, dtype=np.int32)
+    return rowmap
+
+
 def correction_counts(ext) -> tuple[int, int, int]:
     """Rows per component (ref:subdomain.py:235-238)."""
     nx, ny, nz = ext
@@ -89,7 +152,7 @@ class SolvePlan:
     """Batched FlashMP subdomain solves over `subs` (see csrc/precond.cu)."""
 
     def __init__(self, subs: list[SubSpec], alpha: float, device, cinv: dict | None = None,
-                 need_woodbury: bool = True):
+                 need_woodbury: bool = True, share_rotations: bool = True):
         _lib.lib()
         self.device = torch.device(device)
         self.alpha = float(alpha)
@@ -103,6 +166,17 @@ class SolvePlan:
         self.shapes = shapes
         self.factors = FactorTable(shapes, self.alpha, self.device)
         self.pmax = max(max(e) for e in shapes)
+        # ---- rotation groups (one C^-1 / Y / Z / GEMM per group) and their row maps
+        self.groups = rotation_groups(shapes) if share_rotations else [(q, 0) for q in range(len(shapes))]
+        maps, rm_off, off = [], [], 0
+        for g, t in self.groups:
+            if t == 0:
+                rm_off.append(-1)
+            else:
+                maps.append(rotation_rowmap(shapes[g], t))
+                rm_off.append(off)
+                off += maps[-1].size
+        self.rowmap = torch.from_numpy(np.concatenate(maps)).to(self.device) if maps else None
         # ---- shape table
         sh_rec = np.zeros((len(shapes), 20), dtype=np.int64)
         self.m = []
@@ -111,16 +185,19 @@ class SolvePlan:
             self.m.append(sum(mc))
             offs = [self.factors.offsets[n] for n in e]
             sh_rec[q] = [*e, sum(mc), *mc, *(o[0] for o in offs), *(o[1] for o in offs), *(o[2] for o in offs),
-                         self.factors.qw[e], lead_dim(sum(mc)), 0, 0]
+                         self.factors.qw[e], lead_dim(sum(mc)), self.groups[q][0], rm_off[q]]
         # ---- subdomain table, workspace layout
         sub_rec = np.zeros((len(self.subs), 16), dtype=np.int64)
         first = np.zeros(len(shapes) + 1, dtype=np.int64)
         col_of_shape = [0] * len(shapes)
         ws = 0
+        col_of_group = [0] * len(shapes)
         for q, s in enumerate(self.subs):
             sid = shapes.index(s.ext)
-            sub_rec[q] = [*s.ext, *s.ext_lo, *s.own_off, *s.own, sid, col_of_shape[sid], ws, s.in_off]
+            gid = self.groups[sid][0]
+            sub_rec[q] = [*s.ext, *s.ext_lo, *s.own_off, *s.own, sid, col_of_group[gid], ws, s.in_off]
             col_of_shape[sid] += 1
+            col_of_group[gid] += 1
             ps = (s.ext[0] * s.ext[1] + 3) // 4 * 4      # plane stride of a workspace slot (csrc SubD::ps)
             ws += (3 * s.ext[2] * ps + 7) // 8 * 8
         for q in range(len(shapes)):
@@ -136,12 +213,24 @@ class SolvePlan:
         self.work_a = torch.zeros(ws, **f64)
         self.work_b = torch.zeros(ws, **f64)
         self.corr = torch.zeros(len(self.subs) * 6 * self.pmax * self.pmax, **f64)
-        # per-shape Y/Z matrices: row j = subdomain column j, row stride ld (zero padding)
+        # per-group Y/Z matrices: row j = group column j, row stride ld (zero padding); the
+        # members of a group alias the canonical shape's matrices
         self.ld = [lead_dim(m) for m in self.m]
-        self.ymat = [torch.zeros((max(1, n), ld), **f64) for n, ld in zip(self.ncols, self.ld)]
-        self.zmat = [torch.zeros((max(1, n), ld), **f64) for n, ld in zip(self.ncols, self.ld)]
+        self.gcols = col_of_group
+        self.ymat, self.zmat = [], []
+        for q, (g, _) in enumerate(self.groups):
+            if g == q:
+                self.ymat.append(torch.zeros((max(1, col_of_group[q]), self.ld[q]), **f64))
+                self.zmat.append(torch.zeros((max(1, col_of_group[q]), self.ld[q]), **f64))
+            else:
+                self.ymat.append(self.ymat[g])
+                self.zmat.append(self.zmat[g])
         self.cinv = []
-        for e, m, ld in zip(shapes, self.m, self.ld):
+        for q, (e, m, ld) in enumerate(zip(shapes, self.m, self.ld)):
+            g = self.groups[q][0]
+            if g != q:
+                self.cinv.append(self.cinv[g])
+                continue
             t = (cinv or {}).get(e)
             if t is None:
                 if need_woodbury:
@@ -171,6 +260,7 @@ class SolvePlan:
         desc.corr = self.corr.data_ptr()
         desc.ymat, desc.zmat = C.cast(self._y_arr, P), C.cast(self._z_arr, P)
         desc.pmax = self.pmax
+        desc.rowmap = self.rowmap.data_ptr() if self.rowmap is not None else None
         handle = C.c_void_p()
         _lib.check(_lib.lib().fmp_precond_create(C.byref(desc), C.byref(handle)), "fmp_precond_create")
         self._handle = handle

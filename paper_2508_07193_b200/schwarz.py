@@ -29,7 +29,7 @@ from . import _lib
 from .grid import Box, FieldVector
 from .instrument import NULL_TIMER
 from .operators import OperatorParams
-from .plan import SolvePlan, SubSpec, block_struct
+from .plan import SolvePlan, SubSpec, block_struct, rotation_groups
 from . import subdomain
 
 Range3 = tuple[tuple[int, int], tuple[int, int], tuple[int, int]]
@@ -491,11 +491,13 @@ class RasPreconditioner:
         specs = self.layout.sub_specs()
         cinv = {}
         if self.alpha != 0.0:
-            for s in specs:
-                if s.ext not in self.solvers:
-                    data = solver_data_for(Box(*s.ext), self.alpha, dev)
-                    self.solvers[s.ext] = data
-                    cinv[s.ext] = data.corr.padded
+            # C^-1 only for the canonical shape of each rotation group (plan.rotation_groups)
+            shapes = list(dict.fromkeys(s.ext for s in specs))
+            for (g, _), e in zip(rotation_groups(shapes), shapes):
+                if g == shapes.index(e):
+                    data = solver_data_for(Box(*e), self.alpha, dev)
+                    self.solvers[e] = data
+                    cinv[e] = data.corr.padded
         self.plan = SolvePlan(specs, self.alpha, dev, cinv=cinv) if self.alpha != 0.0 else None
 
     def apply_into(self, r: torch.Tensor, z: torch.Tensor) -> torch.Tensor:

@@ -136,3 +136,21 @@ def test_svd_factors_bit_identical_to_reference():
         s = svd_of_difference(n)
         assert np.array_equal(s.U, g[f"U_{n}"]) and np.array_equal(s.S, g[f"S_{n}"])
         assert np.array_equal(s.Vt, g[f"Vt_{n}"])
+
+
+@pytest.mark.parametrize("rep", [(3, 4, 5), (2, 2, 3), (4, 4, 3)])
+def test_rotation_groups_share_cinv(rep):
+    """Cyclic axis rotations of a box have the same C^-1 up to the plan's row map
+    (plan.rotation_rowmap): C^-1_member[i, j] == C^-1_rep[map[i], map[j]] (oracle, CPU)."""
+    from paper_2508_07193_b200.plan import correction_points, rotate, rotation_groups, rotation_rowmap
+    e1 = rotate(rep)
+    e2 = rotate(e1)
+    groups = rotation_groups([rep, (7, 7, 7), e1, e2])
+    assert groups == [(0, 0), (1, 0), (0, 1), (0, 2)]
+    assert correction_points(rep).shape == (O.correction_size(rep), 4)
+    base = O.precompute(rep, 0.25).Cinv
+    for t, e in ((1, e1), (2, e2)):
+        rm = rotation_rowmap(rep, t)
+        assert sorted(rm.tolist()) == list(range(rm.size))
+        got = O.precompute(e, 0.25).Cinv
+        assert np.abs(got - base[np.ix_(rm, rm)]).max() <= 1e-13 * np.abs(base).max()
