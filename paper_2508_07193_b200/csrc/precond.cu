@@ -552,13 +552,14 @@ struct FastPlaneArgs {
 // step 1 for NM consecutive 8-row tiles starting at m0: T[rows][a] = sum_i X[rows][i] Fx[a][i]
 template <bool INV, int NM>
 __device__ __forceinline__ void plane_step1(const double* X, double* T, const double* Fx, int m0, int k4, int g,
-                                            int t) {
+                                            int t, int nt = 5, int coff = 0) {
+  // INV: only the nt column tiles of the owned range [coff, coff + 8 nt) are produced
   double acc[NM][5][2];
 #pragma unroll
   for (int q = 0; q < NM; ++q)
 #pragma unroll
     for (int n = 0; n < 5; ++n) acc[q][n][0] = acc[q][n][1] = 0.0;
-  const double* fb = INV ? Fx + t * FSM + g : Fx + g * FSM + t;
+  const double* fb = INV ? Fx + t * FSM + g + coff : Fx + g * FSM + t;
   const double* xa = X + (m0 * 8 + g) * PXS + t;
   for (int kk = 0; kk < k4; ++kk) {
     double av[NM];
@@ -566,6 +567,7 @@ __device__ __forceinline__ void plane_step1(const double* X, double* T, const do
     for (int q = 0; q < NM; ++q) av[q] = xa[q * 8 * PXS + kk * 4];
 #pragma unroll
     for (int n = 0; n < 5; ++n) {
+      if (n >= nt) break;
       const double bv = INV ? fb[kk * 4 * FSM + n * 8] : fb[n * 8 * FSM + kk * 4];
 #pragma unroll
       for (int q = 0; q < NM; ++q) dmma884(acc[q][n][0], acc[q][n][1], av[q], bv);
@@ -579,7 +581,7 @@ __device__ __forceinline__ void plane_step1(const double* X, double* T, const do
       double* tr = T + r * PXS + 2 * t;
 #pragma unroll
       for (int n = 0; n < 5; ++n) {
-        if (n * 8 + 2 * t < PXS) {
+        if (n < nt && n * 8 + 2 * t < PXS) {
           tr[n * 8] = acc[q][n][0];
           tr[n * 8 + 1] = acc[q][n][1];
         }
@@ -589,15 +591,16 @@ __device__ __forceinline__ void plane_step1(const double* X, double* T, const do
 }
 
 // step 2 for NN consecutive 8-column tiles starting at n0: O[b][cols] = sum_j Fy[b][j] T[j][cols]
+// (INV: only the mt row tiles of the owned rows [d.oy, d.oy + 8 mt); columns are relative to d.ox)
 template <bool INV, int NN>
 __device__ __forceinline__ void plane_step2(const double* T, const double* Fy, const FastPlaneArgs& A, const SubD& d,
-                                            int c, int kplane, int n0, int k4, int g, int t) {
+                                            int c, int kplane, int n0, int k4, int g, int t, int mt = 5) {
   double acc[NN][5][2];
 #pragma unroll
   for (int q = 0; q < NN; ++q)
 #pragma unroll
     for (int m = 0; m < 5; ++m) acc[q][m][0] = acc[q][m][1] = 0.0;
-  const double* fa = INV ? Fy + t * FSM + g : Fy + g * FSM + t;
+  const double* fa = INV ? Fy + t * FSM + g + d.oy : Fy + g * FSM + t;
   const double* tb = T + t * PXS + n0 * 8 + g;
   for (int kk = 0; kk < k4; ++kk) {
     double bv[NN];
@@ -605,6 +608,7 @@ __device__ __forceinline__ void plane_step2(const double* T, const double* Fy, c
     for (int q = 0; q < NN; ++q) bv[q] = tb[kk * 4 * PXS + q * 8];
 #pragma unroll
     for (int m = 0; m < 5; ++m) {
+      if (m >= mt) break;
       const double av = INV ? fa[kk * 4 * FSM + m * 8] : fa[m * 8 * FSM + kk * 4];
 #pragma unroll
       for (int q = 0; q < NN; ++q) dmma884(acc[q][m][0], acc[q][m][1], av, bv[q]);
@@ -614,20 +618,19 @@ __device__ __forceinline__ void plane_step2(const double* T, const double* Fy, c
   const int64_t obase = INV ? 0 : d.ws_off + (int64_t)(c * d.ez + kplane) * d.ps;
 #pragma unroll
   for (int m = 0; m < 5; ++m) {
+    if (m >= mt) break;
     const int row = m * 8 + g;
-    if (row >= ey) continue;
+    if (!INV && row >= ey) continue;
+    if (INV && row >= d.wy) continue;
 #pragma unroll
     for (int q = 0; q < NN; ++q)
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int col = (n0 + q) * 8 + 2 * t + h;
-        if (col >= ex) continue;
         if (!INV) {
-          A.dst[obase + row * ex + col] = acc[q][m][h];
-        } else {
-          const int jo = row - d.oy, io = col - d.ox;
-          if ((unsigned)jo < (unsigned)d.wy && (unsigned)io < (unsigned)d.wx)
-            A.dst[fidx(A.g, c, d.lz + d.oz + kplane, d.ly + row, d.lx + col)] = acc[q][m][h];
+          if (col < ex) A.dst[obase + row * ex + col] = acc[q][m][h];
+        } else if (col < d.wx) {
+          A.dst[fidx(A.g, c, d.lz + d.oz + kplane, d.ly + d.oy + row, d.lx + d.ox + col)] = acc[q][m][h];
         }
       }
   }
@@ -656,6 +659,12 @@ __global__ void __launch_bounds__(PW_WARPS * 32, 1) k_plane_fast(FastPlaneArgs A
       const int64_t P = (int64_t)ex * ey;
       const double* base = INV ? A.src + d.ws_off + (int64_t)(c * d.ez + d.oz + w.z) * d.ps
                                : A.src + d.in_off + c * P * d.ez + w.z * P;
+      if ((ex & 1) == 0 && ((uintptr_t)base & 15) == 0) {   // 16-byte chunks of whole rows
+        const int nch = ex >> 1, ch0 = lane & 15, j0 = lane >> 4;
+        for (int j = j0; j < ey; j += 2)
+          for (int ch = ch0; ch < nch; ch += 16) cp_async16(X + j * PXS + 2 * ch, base + j * ex + 2 * ch);
+        return 0;
+      }
       int j = 0, i = lane;   // the plane is contiguous: walk it flat, tracking (j, i)
       while (i >= ex) { i -= ex; ++j; }
       for (int q = lane; q < ey * ex; q += 32) {
@@ -704,17 +713,20 @@ __global__ void __launch_bounds__(PW_WARPS * 32, 1) k_plane_fast(FastPlaneArgs A
     const double* X = T + shift;
     const int k41 = pad4(d.ex) / 4, k42 = pad4(d.ey) / 4;
     // ---- step 1: T[j][a] = sum_i X[j][i] Fx[a][i]   (INV: T[b][i] = sum_a X[b][a] Fx[a][i])
-    plane_step1<INV, 2>(X, T, Fx, 0, k41, g, t);
-    plane_step1<INV, 2>(X, T, Fx, 2, k41, g, t);
-    plane_step1<INV, 1>(X, T, Fx, 4, k41, g, t);
+    // INV (prolongation): only the owned columns / rows of the plane are formed
+    const int ntc = INV ? (d.wx + 7) / 8 : 5, ntr = INV ? (d.wy + 7) / 8 : 5;
+    plane_step1<INV, 2>(X, T, Fx, 0, k41, g, t, ntc, INV ? d.ox : 0);
+    plane_step1<INV, 2>(X, T, Fx, 2, k41, g, t, ntc, INV ? d.ox : 0);
+    plane_step1<INV, 1>(X, T, Fx, 4, k41, g, t, ntc, INV ? d.ox : 0);
     __syncwarp();
     // ---- step 2: O[b][a] = sum_j Fy[b][j] T[j][a]   (INV: O[j][i] = sum_b Fy[b][j] T[b][i])
-    plane_step2<INV, 2>(T, Fy, A, d, c, w.z, 0, k42, g, t);
-    plane_step2<INV, 2>(T, Fy, A, d, c, w.z, 2, k42, g, t);
-    plane_step2<INV, 1>(T, Fy, A, d, c, w.z, 4, k42, g, t);
+    plane_step2<INV, 2>(T, Fy, A, d, c, w.z, 0, k42, g, t, ntr);
+    if (ntc > 2) plane_step2<INV, 2>(T, Fy, A, d, c, w.z, 2, k42, g, t, ntr);
+    if (ntc > 4) plane_step2<INV, 1>(T, Fy, A, d, c, w.z, 4, k42, g, t, ntr);
     __syncwarp();
   }
 }
+
 
 struct FastColArgs {
   const fmp_subdomain* subs;
@@ -727,6 +739,7 @@ struct FastColArgs {
   int pmax;
   double alpha;
   ExtTable et;
+  int interleave;      // 1: warp gw takes items gw, gw + nw, ... (neighbouring warps read neighbouring columns)
 };
 
 // K2 (INV=false): y^ = B^-1 (Fz X) over 8 columns x all z, 3 components;  K3 (INV=true): Fz^T (y^ - corr)
@@ -740,7 +753,8 @@ __global__ void __launch_bounds__(CW_WARPS * 32, 1) k_column_fast(FastColArgs A)
   __syncthreads();
   const int gw = blockIdx.x * CW_WARPS + warp, nw = gridDim.x * CW_WARPS;
   const int per = (A.n_items + nw - 1) / nw;
-  const int beg = gw * per, end = min(beg + per, A.n_items);
+  const int beg = A.interleave ? gw : gw * per, end = A.interleave ? A.n_items : min(beg + per, A.n_items);
+  const int step = A.interleave ? nw : 1;
   if (beg >= end) return;
 
   auto issue = [&](int it) {
@@ -764,7 +778,7 @@ __global__ void __launch_bounds__(CW_WARPS * 32, 1) k_column_fast(FastColArgs A)
     }
   };
 
-  for (int it = beg; it < end; ++it) {
+  for (int it = beg; it < end; it += step) {
     issue(it);
     cp_async_commit();
     cp_async_wait<0>();
@@ -865,7 +879,12 @@ __global__ void __launch_bounds__(CW_WARPS * 32, 1) k_column_fast(FastColArgs A)
   }
 }
 
-// double-buffered variant (forward pass: no correction phase to overlap)
+// Double-buffered column pass for both directions (K2 forward + B^-1, K3 correction + inverse):
+// 8 independent warps per SM, each over a contiguous item range.  The item metadata is
+// software-pipelined (items[it+2] is fetched while item it computes; consecutive items of a
+// warp share their subdomain record, reloaded only when it changes), so the cp.async of the
+// next tile is issued with no dependent global round trip in front of it; the correction
+// planes of K3 are read with all loads of a lane hoisted ahead of the arithmetic.
 template <bool INV>
 __global__ void __launch_bounds__(CW_WARPS_DB * 32, 1) k_column_fast_db(FastColArgs A) {
   extern __shared__ __align__(16) double smem[];
@@ -879,9 +898,7 @@ __global__ void __launch_bounds__(CW_WARPS_DB * 32, 1) k_column_fast_db(FastColA
   const int beg = gw * per, end = min(beg + per, A.n_items);
   if (beg >= end) return;
 
-  auto issue = [&](int it, int buf) {
-    const int2 w = A.items[it];
-    const SubD d = load_sub(A.subs + w.x);
+  auto issue = [&](const int2 w, const SubD& d, int buf) {
     const int P = d.ex * d.ey, ez = d.ez;
     const int64_t V = d.cstride();
     const double* src = A.src + d.ws_off + w.y;
@@ -901,15 +918,23 @@ __global__ void __launch_bounds__(CW_WARPS_DB * 32, 1) k_column_fast_db(FastColA
   };
 
   int buf = 0;
-  issue(beg, 0);
+  int2 w_cur = A.items[beg];
+  SubD d_cur = load_sub(A.subs + w_cur.x);
+  int2 w_nxt = beg + 1 < end ? A.items[beg + 1] : w_cur;
+  issue(w_cur, d_cur, 0);
   cp_async_commit();
   for (int it = beg; it < end; ++it) {
-    if (it + 1 < end) issue(it + 1, buf ^ 1);
+    SubD d_nxt = d_cur;
+    if (it + 1 < end) {
+      if (w_nxt.x != w_cur.x) d_nxt = load_sub(A.subs + w_nxt.x);
+      issue(w_nxt, d_nxt, buf ^ 1);
+    }
+    const int2 w_nn = it + 2 < end ? A.items[it + 2] : w_nxt;   // consumed next iteration
     cp_async_commit();
     cp_async_wait<1>();
     __syncwarp();
-    const int2 w = A.items[it];
-    const SubD d = load_sub(A.subs + w.x);
+    const int2 w = w_cur;
+    const SubD& d = d_cur;
     const int ex = d.ex, ey = d.ey, ez = d.ez, P = ex * ey, p0 = w.y;
     const int64_t V = d.cstride();
     double* X = wbase + buf * CX_BUF;
@@ -931,11 +956,25 @@ __global__ void __launch_bounds__(CW_WARPS_DB * 32, 1) k_column_fast_db(FastColA
         while (a >= ex) { a -= ex; ++b; }
         const double vy0 = Vy[b * FSM], vx0 = Vx[a * FSM], sx = Sx[a], sy = Sy[b];
         const double gx = cb[0 * pm2 + b * pm + a], gy = cb[2 * pm2 + b * pm + a];
-        for (int cz = lane >> 3; cz < ez; cz += 4) {
+        constexpr int NZ = (CXR + 3) / 4;   // z rows per lane
+        double c1[NZ], c3[NZ], c4[NZ], c5[NZ];
+#pragma unroll
+        for (int u = 0; u < NZ; ++u) {   // every load of this lane in flight at once
+          const int cz = (lane >> 3) + 4 * u;
+          const bool ok = cz < ez;
+          c1[u] = ok ? cb[1 * pm2 + cz * pm + a] : 0.0;
+          c3[u] = ok ? cb[3 * pm2 + cz * pm + b] : 0.0;
+          c4[u] = ok ? cb[4 * pm2 + cz * pm + a] : 0.0;
+          c5[u] = ok ? cb[5 * pm2 + cz * pm + b] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < NZ; ++u) {
+          const int cz = (lane >> 3) + 4 * u;
+          if (cz >= ez) break;
           const double vz0 = Fv[cz * FSM];
-          const double dx = vz0 * gx + vy0 * cb[1 * pm2 + cz * pm + a];
-          const double dy = vz0 * gy + vx0 * cb[3 * pm2 + cz * pm + b];
-          const double dz = vy0 * cb[4 * pm2 + cz * pm + a] + vx0 * cb[5 * pm2 + cz * pm + b];
+          const double dx = vz0 * gx + vy0 * c1[u];
+          const double dy = vz0 * gy + vx0 * c3[u];
+          const double dz = vy0 * c4[u] + vx0 * c5[u];
           const double sz = Sz[cz];
           const double q = __drcp_rn(1.0 + A.alpha * (sx * sx + sy * sy + sz * sz));
           const double pr = A.alpha * (sx * dx + sy * dy + sz * dz);
@@ -952,15 +991,18 @@ __global__ void __launch_bounds__(CW_WARPS_DB * 32, 1) k_column_fast_db(FastColA
     for (int cc = 0; cc < 3; ++cc)
 #pragma unroll
       for (int m = 0; m < 5; ++m) acc[cc][m][0] = acc[cc][m][1] = 0.0;
+    // INV (prolongation): only the owned z rows [oz, oz + wz) are formed
+    const int mt = INV ? (d.wz + 7) / 8 : 5;
     const double* xb = X + t * CXS + g;
-    const double* fv = INV ? Fv + t * FSM + g : Fv + g * FSM + t;
-    const double* fu = INV ? Fu + t * FSM + g : Fu + g * FSM + t;
+    const double* fv = INV ? Fv + t * FSM + g + d.oz : Fv + g * FSM + t;
+    const double* fu = INV ? Fu + t * FSM + g + d.oz : Fu + g * FSM + t;
     for (int kk = 0; kk < k4; ++kk) {
       const double b0 = xb[(0 * CXR + kk * 4) * CXS];
       const double b1 = xb[(1 * CXR + kk * 4) * CXS];
       const double b2 = xb[(2 * CXR + kk * 4) * CXS];
 #pragma unroll
       for (int m = 0; m < 5; ++m) {
+        if (m >= mt) break;
         const double av = INV ? fv[kk * 4 * FSM + m * 8] : fv[m * 8 * FSM + kk * 4];
         const double au = INV ? fu[kk * 4 * FSM + m * 8] : fu[m * 8 * FSM + kk * 4];
         dmma884(acc[0][m][0], acc[0][m][1], av, b0);
@@ -983,7 +1025,9 @@ __global__ void __launch_bounds__(CW_WARPS_DB * 32, 1) k_column_fast_db(FastColA
       }
 #pragma unroll
       for (int m = 0; m < 5; ++m) {
-        const int r = m * 8 + g;
+        if (m >= mt) break;
+        if (INV && m * 8 + g >= d.wz) continue;
+        const int r = INV ? d.oz + m * 8 + g : m * 8 + g;
         if (r >= ez) continue;
         double y0 = acc[0][m][h], y1 = acc[1][m][h], y2 = acc[2][m][h];
         if (!INV) {  // B^-1 y = q (y + alpha s (s . y)), q = 1/(1 + alpha |s|^2)  (ref:subdomain.py:145-153)
@@ -1002,6 +1046,9 @@ __global__ void __launch_bounds__(CW_WARPS_DB * 32, 1) k_column_fast_db(FastColA
     }
     __syncwarp();
     buf ^= 1;
+    w_cur = w_nxt;
+    d_cur = d_nxt;
+    w_nxt = w_nn;
   }
   cp_async_wait<0>();
 }
@@ -1622,6 +1669,7 @@ extern "C" int fmp_precond_create(const fmp_precond_desc* desc, fmp_precond** ou
   cudaFuncSetAttribute(k_column_fast<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kColFastSmem);
   cudaFuncSetAttribute(k_column_fast<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kColFastSmem);
   cudaFuncSetAttribute(k_column_fast_db<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kColFastSmemDb);
+  cudaFuncSetAttribute(k_column_fast_db<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kColFastSmemDb);
   cudaFuncSetAttribute(k_faces<5, 2, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize, face_smem_words<5>() * 8);
   cudaFuncSetAttribute(k_faces<9, 3, 9>, cudaFuncAttributeMaxDynamicSharedMemorySize, face_smem_words<9>() * 8);
   cudaFuncSetAttribute(k_corr<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * FaceMat<5>::WORDS * 8);
@@ -1650,12 +1698,16 @@ static int column_pass(fmp_precond* p, bool inv, const double* src, double* dst,
     a.pmax = (int)p->d.pmax;
     a.alpha = p->d.alpha;
     a.et = p->et;
-    if (inv) {
+    a.interleave = 0;
+    if (inv && getenv_flag("FMP_COL_SINGLE")) {
       const int grid = std::min(p->sms, (p->n_fcol + CW_WARPS - 1) / CW_WARPS);
       k_column_fast<true><<<grid, CW_WARPS * 32, kColFastSmem, st>>>(a);
     } else {
       const int grid = std::min(p->sms, (p->n_fcol + CW_WARPS_DB - 1) / CW_WARPS_DB);
-      k_column_fast_db<false><<<grid, CW_WARPS_DB * 32, kColFastSmemDb, st>>>(a);
+      if (inv)
+        k_column_fast_db<true><<<grid, CW_WARPS_DB * 32, kColFastSmemDb, st>>>(a);
+      else
+        k_column_fast_db<false><<<grid, CW_WARPS_DB * 32, kColFastSmemDb, st>>>(a);
     }
     FMP_CHECK_LAUNCH();
     return 0;
