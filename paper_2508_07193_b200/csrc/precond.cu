@@ -1564,7 +1564,10 @@ extern "C" int fmp_precond_create(const fmp_precond_desc* desc, fmp_precond** ou
   }
   {  // grouped GEMM tables: one shape record per extended shape, tiles bucketed by configuration
     const char* gm = getenv("FMP_GEMM");
-    const std::string gmode = gm ? gm : "ozaki";   // cublas | own | ozaki
+    std::string gmode = gm ? gm : "ozaki";   // cublas | own | ozaki
+    if (gmode == "ozaki")   // the int32 level accumulators bound K = m (64^3-class subdomains exceed it)
+      for (const auto& sh : p->shapes)
+        if (ozaki_kchunks((int)sh.m) <= 0) gmode = "cublas";
     p->use_cublas = gmode == "cublas";
     p->use_ozaki = gmode == "ozaki";
     std::vector<GemmShape> gs;
