@@ -15,7 +15,7 @@ from .schwarz import (BlockLayout, CommunicationError, DistributedOperator, Exch
                       RasPreconditioner, exchange_halo, gather_field, make_partition, make_transport,
                       proc_grid_for, ras_apply, scatter_field, solver_data_for)
 from .krylov import SolveReport, SolverConfig, bicgstab, gmres, reduce_dot
-from .cn_driver import CnSolver, DeviceCnStepper, EmState, StepFailure, build_rhs, cn_step
+from .cn_driver import CnSolver, DeviceCnStepper, EmState, HostStepPipeline, StepFailure, build_rhs, cn_step
 from .instrument import BREAKDOWN_CATEGORIES, FlopCounter, NullTimer, PhaseTimer
 
 __version__ = "0.1.0"

@@ -117,6 +117,22 @@ def require_cuda(device=None) -> torch.device:
     return torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
 
 
+class HostScalars:
+    """A few FP64 reduction results that kernels write straight into pinned, device-mapped
+    (UVA) host memory.  Reading them costs one stream synchronisation and no copy, so the
+    Krylov scalars never queue behind bulk transfers on a copy engine."""
+
+    def __init__(self, n: int):
+        self.t = torch.zeros(n, dtype=torch.float64, pin_memory=True)
+
+    def ptr(self) -> int:
+        return self.t.data_ptr()
+
+    def read(self, n: int | None = None) -> list[float]:
+        torch.cuda.current_stream().synchronize()
+        return self.t[: n if n is not None else self.t.numel()].tolist()
+
+
 def ref(struct):
     """ctypes.byref for the C structs passed by pointer."""
     return C.byref(struct)

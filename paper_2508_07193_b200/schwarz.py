@@ -537,16 +537,24 @@ class DistributedOperator:
         self.exchanger = HaloExchanger(self.layout, 1)
         dev = self.layout.device
         self._dots = torch.zeros(2, dtype=torch.float64, device=dev)
+        # one GPU: the fused dot products land in pinned host memory (no device->host copy)
+        self._host = _lib.HostScalars(2) if transport.world == 1 else None
         self._scratch = torch.zeros(int(_lib.lib().fmp_reduce_scratch_doubles()), dtype=torch.float64, device=dev)
 
     def _run(self, mode: int, x: torch.Tensor, y, w):
         with self.timer.phase("p2p"):
             self.exchanger.exchange(x)
         blk = self.exchanger.block_struct()
+        dots = self._host.ptr() if self._host is not None else self._dots.data_ptr()
         with self.timer.phase("spmv"):
             _lib.call("fmp_stencil_apply", _lib.ref(blk), self.alpha, int(self.with_boundary), mode,
-                      x.data_ptr(), _lib.ptr(y), _lib.ptr(w), self._dots.data_ptr(), self._scratch.data_ptr(),
-                      _lib.stream())
+                      x.data_ptr(), _lib.ptr(y), _lib.ptr(w), dots, self._scratch.data_ptr(), _lib.stream())
+
+    def _reduced(self, n: int) -> list[float]:
+        with self.timer.phase("reduction"):
+            if self._host is not None:
+                return self._host.read(n)
+            return self.transport.allreduce_(self._dots[:n].clone()).tolist()
 
     def apply_into(self, x: torch.Tensor, y: torch.Tensor) -> torch.Tensor:
         self._run(0, x, y, None)
@@ -557,15 +565,12 @@ class DistributedOperator:
         y = self.apply_into(x, torch.empty_like(x))
         return self.layout.to_list(y) if was_list else y
 
-    def apply_dots(self, x: torch.Tensor, y: torch.Tensor, w: torch.Tensor, both: bool) -> torch.Tensor:
-        """y = A x; returns the device tensor [(y, w), (y, y)] (second entry only if both),
-        summed over GPUs."""
+    def apply_dots(self, x: torch.Tensor, y: torch.Tensor, w: torch.Tensor, both: bool) -> list[float]:
+        """y = A x; returns [(y, w)] or [(y, w), (y, y)] summed over GPUs."""
         self._run(2 if both else 1, x, y, w)
-        with self.timer.phase("reduction"):
-            return self.transport.allreduce_(self._dots.clone())
+        return self._reduced(2 if both else 1)
 
-    def residual_norm2(self, x: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
+    def residual_norm2(self, x: torch.Tensor, b: torch.Tensor) -> float:
         """||b - A x||^2 over all GPUs, without materialising A x."""
         self._run(3, x, None, b)
-        with self.timer.phase("reduction"):
-            return self.transport.allreduce_(self._dots[:1].clone())
+        return self._reduced(1)[0]

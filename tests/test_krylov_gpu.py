@@ -130,3 +130,21 @@ def test_cn_step_config1_matches_reference():
     idx = g[f"idx_{tag}"]
     assert np.linalg.norm(new.E.data[idx] - g[f"E1_{tag}"]) / np.linalg.norm(g[f"E1_{tag}"]) <= 1e-10
     assert np.linalg.norm(new.H.data[idx] - g[f"H1_{tag}"]) / np.linalg.norm(g[f"H1_{tag}"]) <= 1e-10
+
+
+def test_host_step_pipeline_matches_device_steps():
+    """HostStepPipeline (host fields, overlapped transfers) == DeviceCnStepper on the same fields."""
+    from paper_2508_07193_b200 import Box, CnSolver, DeviceCnStepper, HostStepPipeline, SolverConfig, make_transport
+    n = 32
+    solver = CnSolver(Box(n, n, n), (2, 2, 2), 1, 0.25, SolverConfig(), make_transport("cuda"))
+    g = torch.Generator(device="cuda").manual_seed(3)
+    E = torch.rand(3, n, n, n, dtype=torch.float64, device="cuda", generator=g)
+    H = torch.rand(3, n, n, n, dtype=torch.float64, device="cuda", generator=g)
+    st = DeviceCnStepper(solver, E.clone(), H.clone(), 1.0)
+    st.step()
+    Eh, Hh = E.cpu().pin_memory(), H.cpu().pin_memory()
+    Eo, Ho = torch.empty_like(Eh).pin_memory(), torch.empty_like(Hh).pin_memory()
+    reps = HostStepPipeline(solver, 1.0).run(Eh, Hh, Eo, Ho, steps=3)
+    torch.cuda.synchronize()
+    assert len(reps) == 3 and all(r.converged for r in reps)
+    assert torch.equal(Eo, st.E.cpu()) and torch.equal(Ho, st.H.cpu())

@@ -26,8 +26,8 @@ for mode in ("legacy", "tma"):
     t = sorted(ts)[len(ts) // 2]
     out[mode + "_ms"] = t
     out[mode + "_GBs"] = 48 * n ** 3 / t / 1e6
-    d = op.apply_dots(x, y, w, both=True).tolist()
-    r = float(op.residual_norm2(x, w).item())
+    d = op.apply_dots(x, y, w, both=True)
+    r = float(op.residual_norm2(x, w))
     out[mode + "_dots"] = d + [r]
     ys[mode] = y.clone()
 out["max_abs_diff"] = float((ys["tma"] - ys["legacy"]).abs().max())

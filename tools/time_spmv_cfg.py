@@ -26,7 +26,7 @@ for cfg, env in (("legacy", {"FMP_SPMV_LEGACY": "1"}), ("ns6", {"FMP_SPMV_NS6": 
         out[f"{cfg}_{name}_us"] = round(sorted(ts)[5] * 1e3, 1)
     op.apply_into(x, y)
     out[f"{cfg}_spmv_GBs"] = round(48 * n ** 3 / out[f"{cfg}_spmv_us"] / 1e3, 1)
-    ys[cfg] = (y.clone(), op.apply_dots(x, y, w, both=True).tolist(), float(op.residual_norm2(x, w)))
+    ys[cfg] = (y.clone(), op.apply_dots(x, y, w, both=True), float(op.residual_norm2(x, w)))
 for cfg in ("ns6", "ns4"):
     out[f"{cfg}_maxdiff"] = float((ys[cfg][0] - ys["legacy"][0]).abs().max())
     out[f"{cfg}_dots"] = ys[cfg][1] + [ys[cfg][2]]
