@@ -102,6 +102,67 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------------- ours
+INT8_PROBE_FILE = ROOT / "profiles" / "r01_umma_i8_rate.json"
+
+
+def int8_peak_tops() -> tuple[float, str]:
+    """Dense INT8 tcgen05 rate: the per-SM MAC/clk measured by tools/umma_rate.cu (M=128, N>=128)
+    x 2 x 148 SMs x max SM clock; the 4.5 POPS spec figure if the probe file is absent."""
+    if INT8_PROBE_FILE.exists():
+        mac = max(r["mac_per_clk"] for r in json.loads(INT8_PROBE_FILE.read_text())["results"])
+        return mac * 2 * 148 * 1.965e9 / 1e12, "profiles/r01_umma_i8_rate.json (measured tcgen05 kind::i8 rate)"
+    return 4500.0, "B200 dense INT8 spec"
+
+
+def stage_rooflines(prec, x, z, specs, peaks, reps):
+    """Per-kernel times of the preconditioner apply, from CUDA events recorded between its
+    kernels on the launching stream (fmp_precond_profile), averaged over `reps` applies, with
+    each kernel's algorithmic work and roofline ("Kernels")."""
+    from paper_2508_07193_b200.plan import correction_counts
+    plan = prec.plan
+    plan.profile(True)
+    acc = {}
+    for _ in range(reps):
+        prec.apply_into(x, z)
+        for k, v in plan.stage_ms().items():
+            acc[k] = acc.get(k, 0.0) + v / reps
+    plan.profile(False)
+    fl = {k: 0 for k in ("plane_fwd", "column_fwd", "column_inv", "plane_inv")}
+    faces_b = 0
+    for sp in specs:
+        nx, ny, nz = sp.ext
+        wx, wy, wz = sp.own
+        V = nx * ny * nz
+        fl["plane_fwd"] += 6 * V * (nx + ny)                       # x, y mode products, 3 components
+        fl["column_fwd"] += 6 * V * nz + 18 * V                    # z mode product + 3x3 block solve
+        fl["column_inv"] += 6 * nx * ny * nz * wz                  # z inverse on the owned rows
+        fl["plane_inv"] += 6 * wz * (ny * nx * wx + ny * wy * wx)  # x, y inverse on the owned tile
+        faces_b += 24 * V
+    gemm_f = 0
+    for g, (rep, _t) in enumerate(plan.groups):
+        if rep == g:
+            m = sum(correction_counts(plan.shapes[g]))
+            gemm_f += 2 * m * m * plan.gcols[g]
+    fp64, hbm = peaks["fp64_tflops"], peaks["hbm_gbs"]
+    out = {}
+    for k, ms in acc.items():
+        e = {"ms": round(ms, 4)}
+        if k in fl:
+            a = fl[k] / ms / 1e9
+            e.update(bound="tensor (FP64 DMMA)", achieved_tflops=round(a, 2), frac=round(a / fp64, 3))
+        elif k == "faces":
+            a = faces_b / ms / 1e6
+            e.update(bound="hbm", achieved_gbs=round(a, 1), frac=round(a / hbm, 3))
+        elif k == "gemm" and ms > 0:
+            a = gemm_f / ms / 1e9
+            pk, src = int8_peak_tops()
+            e.update(bound="tensor (INT8 tcgen05, Ozaki S=7: 28 int8 products per FP64 product)",
+                     fp64_equiv_tflops=round(a, 2), int8_tops=round(28 * a, 1),
+                     frac=round(28 * a / pk, 3), peak_int8_tops=round(pk, 1), peak_source=src)
+        out[k] = e
+    return out
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -207,6 +268,7 @@ def run_ours(args):
     peaks = measured_peaks()
     spmv_bytes = 48 * owned
     prec_tflops = flops_exec / t_prec / 1e12
+    stages = stage_rooflines(prec, x, z, specs, peaks, reps)
 
     # ---- per-phase breakdown of one extra step (reference categories, ref:instrument.py:17-25)
     from paper_2508_07193_b200.instrument import PhaseTimer
@@ -260,6 +322,7 @@ def run_ours(args):
                           "algorithmic_bytes": bytes_alg, "flops_reference_count": flops_ref,
                           "flops_executed": flops_exec, "tflops_executed": round(prec_tflops, 2),
                           "tflops_reference_count": round(flops_ref / t_prec / 1e12, 2)},
+        "precond_kernels": stages,
         "spmv": {"ms": round(t_spmv * 1e3, 4), "GB_per_s": round(spmv_bytes / t_spmv / 1e9, 1),
                  "frac_hbm": round(spmv_bytes / t_spmv / 1e9 / peaks["hbm_gbs"], 3)},
         "roofline": {"kernel": "RAS precond apply (fused FlashMP sequence: FP64 DMMA transforms + Ozaki INT8 tcgen05 Woodbury GEMM)",

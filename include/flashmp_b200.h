@@ -180,6 +180,17 @@ int fmp_precond_destroy(fmp_precond* p);
 int fmp_precond_apply(fmp_precond* p, const fmp_block* blk, int mode,
                       const double* r, double* z, void* stream);
 
+/* Stage timing (for benchmarks): enable=1 records CUDA events between the kernels of every
+ * later fmp_precond_apply on its stream; fmp_precond_stage_ms synchronises on the last apply's
+ * final event and writes up to n per-stage times in ms, in this order:
+ *   0 forward plane pass, 1 forward column pass + B^-1, 2 face projections (Y),
+ *   3 Y slicing (Ozaki; 0 otherwise), 4 Woodbury GEMM Z = C^-1 Y, 5 correction planes,
+ *   6 correction + inverse column pass, 7 inverse plane pass + prolongation.
+ * Returns the number of stages written. */
+#define FMP_PRECOND_STAGES 8
+int fmp_precond_profile(fmp_precond* p, int enable);
+int fmp_precond_stage_ms(fmp_precond* p, float* ms, int n);
+
 /* Restriction only: out[ws_off(i) ...] = S_i^gamma r for every subdomain i, in the
  * reference's extended-vector order (ref:schwarz.py:217-257).  out has the plan's
  * workspace size.  Exposes the index maps of the fused solve for bit-exact tests. */

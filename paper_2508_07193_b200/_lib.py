@@ -36,6 +36,8 @@ SIGNATURES = {
     "fmp_precond_destroy": (_i, [_p]),
     "fmp_precond_apply": (_i, [_p, _p, _i, _p, _p, _p]),
     "fmp_precond_restrict": (_i, [_p, _p, _p, _p, _p]),
+    "fmp_precond_profile": (_i, [_p, _i]),
+    "fmp_precond_stage_ms": (_i, [_p, C.POINTER(C.c_float), _i]),
 }
 
 FMP_SOLVE_WOODBURY, FMP_SOLVE_EXACT, FMP_SOLVE_FACES = 0, 1, 2

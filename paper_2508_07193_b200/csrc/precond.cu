@@ -1411,6 +1411,8 @@ struct fmp_precond {
   cublasHandle_t blas = nullptr;
   int max_ex = 1, max_ey = 1, max_ez = 1, max_p = 1;
   int sms = kNumSM;
+  bool profile = false;                   // stage events (fmp_precond_profile)
+  cudaEvent_t stage_ev[FMP_PRECOND_STAGES + 1] = {};
 };
 
 template <class T>
@@ -1423,6 +1425,8 @@ static int upload(const std::vector<T>& v, T** out) {
 }
 
 static void free_plan(fmp_precond* p) {
+  for (auto& e : p->stage_ev)
+    if (e) cudaEventDestroy(e);
   if (!p) return;
   if (p->blas) cublasDestroy(p->blas);
   cudaFree(p->d_ymat);
@@ -1792,8 +1796,14 @@ extern "C" int fmp_precond_apply(fmp_precond* p, const fmp_block* blk, int mode,
   cudaStream_t st = as_stream(stream);
   double* wa = p->d.work_a;
   double* wb = p->d.work_b;
+  auto mark = [&](int i) {
+    if (p->profile) cudaEventRecord(p->stage_ev[i], st);
+  };
+  mark(0);
   if (int e = plane_pass(p, blk, false, mode, r, wa, st)) return e;
+  mark(1);
   if (int e = column_pass(p, false, wa, wb, nullptr, st)) return e;
+  mark(2);
   const int pm = (int)p->d.pmax;
   FaceArgs fa{p->d.subs, p->d.shapes, p->d.factors, wb, p->d.corr, p->d_ymat, p->d_zmat, pm, (p->max_p + 3) & ~3,
               p->d.rowmap};
@@ -1805,8 +1815,10 @@ extern "C" int fmp_precond_apply(fmp_precond* p, const fmp_block* blk, int mode,
       k_faces<9, 3, 9><<<fg, FACE_THREADS, face_smem_words<9>() * sizeof(double), st>>>(fa);
     FMP_CHECK_LAUNCH();
   }
+  mark(3);
   if (mode == FMP_SOLVE_FACES) return 0;
   if (mode == FMP_SOLVE_WOODBURY) {
+    if (!p->use_ozaki) mark(4);
     if (p->use_cublas) {
       // one DGEMM per shape; shapes spread over auxiliary streams (forked from / joined into
       // `st`) so the HBM-bound small-n products overlap the compute-bound large ones
@@ -1830,19 +1842,42 @@ extern "C" int fmp_precond_apply(fmp_precond* p, const fmp_block* blk, int mode,
     } else if (p->use_ozaki) {
       FMP_REQUIRE(p->d_ozshapes != nullptr, "Ozaki GEMM requested but the plan has no C^-1");
       if (int e = ozaki_slice(p->d_ozslices, p->n_ozslices, p->oz_rows, p->oz_threads, st)) return e;
+      mark(4);
       if (int e = ozaki_launch(p->d_ozshapes, p->d_oztiles, p->n_oztiles, p->sms, st)) return e;
     } else {
       for (int c = 0; c < 3; ++c)
         if (int e = gemm_launch(c, p->d_gshapes, p->d_gtiles[c], p->n_gtiles[c], p->sms, st)) return e;
     }
+    mark(5);
     if (pm <= 40)
       k_corr<5><<<dim3(3, (unsigned)p->d.n_sub), FACE_THREADS, 4 * FaceMat<5>::WORDS * sizeof(double), st>>>(fa);
     else
       k_corr<9><<<dim3(3, (unsigned)p->d.n_sub), FACE_THREADS, 4 * FaceMat<9>::WORDS * sizeof(double), st>>>(fa);
     FMP_CHECK_LAUNCH();
   }
+  mark(6);
   if (int e = column_pass(p, true, wb, wa, mode == FMP_SOLVE_WOODBURY ? p->d.corr : nullptr, st)) return e;
-  return plane_pass(p, blk, true, mode, wa, z, st);
+  mark(7);
+  if (int e = plane_pass(p, blk, true, mode, wa, z, st)) return e;
+  mark(8);
+  return 0;
+}
+
+extern "C" int fmp_precond_profile(fmp_precond* p, int enable) {
+  FMP_REQUIRE(p, "null plan");
+  if (enable)
+    for (auto& e : p->stage_ev)
+      if (!e) FMP_CHECK_CUDA(cudaEventCreate(&e));
+  p->profile = enable != 0;
+  return 0;
+}
+
+extern "C" int fmp_precond_stage_ms(fmp_precond* p, float* ms, int n) {
+  FMP_REQUIRE(p && ms && p->profile, "stage timing not enabled on this plan");
+  FMP_CHECK_CUDA(cudaEventSynchronize(p->stage_ev[FMP_PRECOND_STAGES]));
+  const int k = std::min(n, FMP_PRECOND_STAGES);
+  for (int i = 0; i < k; ++i) FMP_CHECK_CUDA(cudaEventElapsedTime(&ms[i], p->stage_ev[i], p->stage_ev[i + 1]));
+  return k;
 }
 
 extern "C" int fmp_precond_restrict(fmp_precond* p, const fmp_block* blk, const double* r, double* out,

@@ -270,6 +270,19 @@ class SolvePlan:
                                                 _lib.ptr(z) if z is not None else None, _lib.stream()),
                    "fmp_precond_apply")
 
+    STAGES = ("plane_fwd", "column_fwd", "faces", "slice_y", "gemm", "corr", "column_inv", "plane_inv")
+
+    def profile(self, enable: bool = True) -> None:
+        """Record CUDA events between the kernels of later applies (fmp_precond_profile)."""
+        _lib.check(_lib.lib().fmp_precond_profile(self._handle, int(enable)), "fmp_precond_profile")
+
+    def stage_ms(self) -> dict:
+        """Per-stage times (ms) of the last Woodbury apply (synchronises on it)."""
+        buf = (C.c_float * len(self.STAGES))()
+        n = _lib.lib().fmp_precond_stage_ms(self._handle, buf, len(self.STAGES))
+        _lib.check(0 if n >= 0 else n, "fmp_precond_stage_ms")
+        return {k: float(buf[i]) for i, k in enumerate(self.STAGES[:n])}
+
     def restrict(self, blk: _lib.FmpBlock, r: torch.Tensor) -> torch.Tensor:
         """Every subdomain's extended vector, concatenated in plan order at ws offsets."""
         out = torch.empty_like(self.work_a)
