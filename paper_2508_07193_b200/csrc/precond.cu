@@ -550,10 +550,11 @@ struct FastPlaneArgs {
 // two at a time (10 independent DMMA chains, 0.7 fragment loads per DMMA).
 
 // step 1 for NM consecutive 8-row tiles starting at m0: T[rows][a] = sum_i X[rows][i] Fx[a][i]
-template <bool INV, int NM>
+template <bool INV, int NM, int nt = 5>
 __device__ __forceinline__ void plane_step1(const double* X, double* T, const double* Fx, int m0, int k4, int g,
-                                            int t, int nt = 5, int coff = 0) {
+                                            int t, int coff = 0) {
   // INV: only the nt column tiles of the owned range [coff, coff + 8 nt) are produced
+  // (nt is a template constant: a runtime tile count breaks the DMMA issue schedule)
   double acc[NM][5][2];
 #pragma unroll
   for (int q = 0; q < NM; ++q)
@@ -592,9 +593,9 @@ __device__ __forceinline__ void plane_step1(const double* X, double* T, const do
 
 // step 2 for NN consecutive 8-column tiles starting at n0: O[b][cols] = sum_j Fy[b][j] T[j][cols]
 // (INV: only the mt row tiles of the owned rows [d.oy, d.oy + 8 mt); columns are relative to d.ox)
-template <bool INV, int NN>
+template <bool INV, int NN, int mt = 5>
 __device__ __forceinline__ void plane_step2(const double* T, const double* Fy, const FastPlaneArgs& A, const SubD& d,
-                                            int c, int kplane, int n0, int k4, int g, int t, int mt = 5) {
+                                            int c, int kplane, int n0, int k4, int g, int t) {
   double acc[NN][5][2];
 #pragma unroll
   for (int q = 0; q < NN; ++q)
@@ -713,16 +714,25 @@ __global__ void __launch_bounds__(PW_WARPS * 32, 1) k_plane_fast(FastPlaneArgs A
     const double* X = T + shift;
     const int k41 = pad4(d.ex) / 4, k42 = pad4(d.ey) / 4;
     // ---- step 1: T[j][a] = sum_i X[j][i] Fx[a][i]   (INV: T[b][i] = sum_a X[b][a] Fx[a][i])
-    // INV (prolongation): only the owned columns / rows of the plane are formed
-    const int ntc = INV ? (d.wx + 7) / 8 : 5, ntr = INV ? (d.wy + 7) / 8 : 5;
-    plane_step1<INV, 2>(X, T, Fx, 0, k41, g, t, ntc, INV ? d.ox : 0);
-    plane_step1<INV, 2>(X, T, Fx, 2, k41, g, t, ntc, INV ? d.ox : 0);
-    plane_step1<INV, 1>(X, T, Fx, 4, k41, g, t, ntc, INV ? d.ox : 0);
-    __syncwarp();
-    // ---- step 2: O[b][a] = sum_j Fy[b][j] T[j][a]   (INV: O[j][i] = sum_b Fy[b][j] T[b][i])
-    plane_step2<INV, 2>(T, Fy, A, d, c, w.z, 0, k42, g, t, ntr);
-    if (ntc > 2) plane_step2<INV, 2>(T, Fy, A, d, c, w.z, 2, k42, g, t, ntr);
-    if (ntc > 4) plane_step2<INV, 1>(T, Fy, A, d, c, w.z, 4, k42, g, t, ntr);
+    // INV (prolongation): only the owned columns / rows of the plane are formed (4 tiles
+    // when the owned tile is <= 32 wide, the common case)
+    if (INV && d.wx <= 32 && d.wy <= 32) {
+      plane_step1<INV, 2, 4>(X, T, Fx, 0, k41, g, t, d.ox);
+      plane_step1<INV, 2, 4>(X, T, Fx, 2, k41, g, t, d.ox);
+      plane_step1<INV, 1, 4>(X, T, Fx, 4, k41, g, t, d.ox);
+      __syncwarp();
+      plane_step2<INV, 2, 4>(T, Fy, A, d, c, w.z, 0, k42, g, t);
+      plane_step2<INV, 2, 4>(T, Fy, A, d, c, w.z, 2, k42, g, t);
+    } else {
+      plane_step1<INV, 2>(X, T, Fx, 0, k41, g, t, INV ? d.ox : 0);
+      plane_step1<INV, 2>(X, T, Fx, 2, k41, g, t, INV ? d.ox : 0);
+      plane_step1<INV, 1>(X, T, Fx, 4, k41, g, t, INV ? d.ox : 0);
+      __syncwarp();
+      // ---- step 2: O[b][a] = sum_j Fy[b][j] T[j][a]   (INV: O[j][i] = sum_b Fy[b][j] T[b][i])
+      plane_step2<INV, 2>(T, Fy, A, d, c, w.z, 0, k42, g, t);
+      plane_step2<INV, 2>(T, Fy, A, d, c, w.z, 2, k42, g, t);
+      plane_step2<INV, 1>(T, Fy, A, d, c, w.z, 4, k42, g, t);
+    }
     __syncwarp();
   }
 }
@@ -879,6 +889,25 @@ __global__ void __launch_bounds__(CW_WARPS * 32, 1) k_column_fast(FastColArgs A)
   }
 }
 
+// z mode product of one 8-column item: acc[c][m] += F(rows m) * X(column tile), MT row tiles
+template <bool INV, int MT>
+__device__ __forceinline__ void col_mma(double (&acc)[3][5][2], const double* xb, const double* fv, const double* fu,
+                                        int k4) {
+  for (int kk = 0; kk < k4; ++kk) {
+    const double b0 = xb[(0 * CXR + kk * 4) * CXS];
+    const double b1 = xb[(1 * CXR + kk * 4) * CXS];
+    const double b2 = xb[(2 * CXR + kk * 4) * CXS];
+#pragma unroll
+    for (int m = 0; m < MT; ++m) {
+      const double av = INV ? fv[kk * 4 * FSM + m * 8] : fv[m * 8 * FSM + kk * 4];
+      const double au = INV ? fu[kk * 4 * FSM + m * 8] : fu[m * 8 * FSM + kk * 4];
+      dmma884(acc[0][m][0], acc[0][m][1], av, b0);
+      dmma884(acc[1][m][0], acc[1][m][1], av, b1);
+      dmma884(acc[2][m][0], acc[2][m][1], au, b2);
+    }
+  }
+}
+
 // Double-buffered column pass for both directions (K2 forward + B^-1, K3 correction + inverse):
 // 8 independent warps per SM, each over a contiguous item range.  The item metadata is
 // software-pipelined (items[it+2] is fetched while item it computes; consecutive items of a
@@ -991,25 +1020,16 @@ __global__ void __launch_bounds__(CW_WARPS_DB * 32, 1) k_column_fast_db(FastColA
     for (int cc = 0; cc < 3; ++cc)
 #pragma unroll
       for (int m = 0; m < 5; ++m) acc[cc][m][0] = acc[cc][m][1] = 0.0;
-    // INV (prolongation): only the owned z rows [oz, oz + wz) are formed
-    const int mt = INV ? (d.wz + 7) / 8 : 5;
+    // INV (prolongation): only the owned z rows [oz, oz + wz) are formed (4 row tiles when
+    // wz <= 32; the tile count is a template constant of col_mma)
+    const int mt = INV && d.wz <= 32 ? 4 : 5;
     const double* xb = X + t * CXS + g;
     const double* fv = INV ? Fv + t * FSM + g + d.oz : Fv + g * FSM + t;
     const double* fu = INV ? Fu + t * FSM + g + d.oz : Fu + g * FSM + t;
-    for (int kk = 0; kk < k4; ++kk) {
-      const double b0 = xb[(0 * CXR + kk * 4) * CXS];
-      const double b1 = xb[(1 * CXR + kk * 4) * CXS];
-      const double b2 = xb[(2 * CXR + kk * 4) * CXS];
-#pragma unroll
-      for (int m = 0; m < 5; ++m) {
-        if (m >= mt) break;
-        const double av = INV ? fv[kk * 4 * FSM + m * 8] : fv[m * 8 * FSM + kk * 4];
-        const double au = INV ? fu[kk * 4 * FSM + m * 8] : fu[m * 8 * FSM + kk * 4];
-        dmma884(acc[0][m][0], acc[0][m][1], av, b0);
-        dmma884(acc[1][m][0], acc[1][m][1], av, b1);
-        dmma884(acc[2][m][0], acc[2][m][1], au, b2);
-      }
-    }
+    if (mt == 4)
+      col_mma<INV, 4>(acc, xb, fv, fu, k4);
+    else
+      col_mma<INV, 5>(acc, xb, fv, fu, k4);
     double* dst = A.dst + d.ws_off;
     const int b0 = p0 / ex;   // one division per item; the 8 columns advance b a few times at most
 #pragma unroll
