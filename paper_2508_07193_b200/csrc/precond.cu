@@ -1167,14 +1167,17 @@ constexpr int FACE_THREADS = (FACE_WARPS + 1) * 32; // + producer warp
 constexpr int FZ = 4;                               // planes per y-normal partial chunk
 template <int NT>
 struct FaceRing {
-  static constexpr int NS = NT <= 5 ? 4 : 2;                      // ring slots
-  static constexpr int SLOT = (FaceMat<NT>::N * FaceMat<NT>::N + 15) / 16 * 16;   // >= padded plane stride
-  // work region: max(Fu, Fv, temp) during the transforms vs ring + weights + partials
-  static constexpr int STREAM = NS * SLOT + 3 * FaceMat<NT>::N + FACE_WARPS * FZ * FaceMat<NT>::N;
-  static constexpr int WORK = STREAM > 3 * FaceMat<NT>::WORDS ? STREAM : 3 * FaceMat<NT>::WORDS;
+  static constexpr int NS = NT <= 5 ? 3 : 2;   // ring slots (3: three CTAs per SM at 34^3 planes)
 };
+// ring slot (doubles): the plan's largest padded plane, rounded to 128 bytes
+__host__ __device__ inline int face_slot(int max_ps) { return (max_ps + 15) / 16 * 16; }
+// work region: max(Fu, Fv, temp) during the transforms vs ring + weights + partials
 template <int NT>
-constexpr int face_smem_words() { return 2 * FaceMat<NT>::WORDS + FaceRing<NT>::WORK; }
+inline size_t face_smem_bytes(int slot) {
+  const size_t stream = (size_t)FaceRing<NT>::NS * slot + 3 * FaceMat<NT>::N + FACE_WARPS * FZ * FaceMat<NT>::N;
+  const size_t work = std::max<size_t>(stream, 3 * (size_t)FaceMat<NT>::WORDS);
+  return (2 * (size_t)FaceMat<NT>::WORDS + work) * sizeof(double);
+}
 
 // One staged y^ plane of the face projections (consumer warp `warp` of FACE_WARPS): all row
 // loads first, then the z-normal update, the y-normal partial and the x-normal row sums with
@@ -1232,11 +1235,12 @@ __device__ __forceinline__ void face_plane(const double* pl, int z, int ex, int 
 // FR rows per warp, FA columns per lane, NT 8-wide tiles per padded extent (register and
 // shared-memory footprints sized for the plan's extents)
 template <int FR, int FA, int NT>
-__global__ void __launch_bounds__(FACE_THREADS, NT <= 5 ? 2 : 1) k_faces(FaceArgs A) {
+__global__ void __launch_bounds__(FACE_THREADS, NT <= 5 ? 3 : 1) k_faces(FaceArgs A) {
   extern __shared__ __align__(128) double smem[];
   __shared__ __align__(8) uint64_t full[FaceRing<NT>::NS], empty[FaceRing<NT>::NS];
   constexpr int S = FaceMat<NT>::S, W = FaceMat<NT>::WORDS, N = FaceMat<NT>::N;
-  constexpr int NS = FaceRing<NT>::NS, SLOT = FaceRing<NT>::SLOT;
+  constexpr int NS = FaceRing<NT>::NS;
+  const int SLOT = face_slot(A.max_ps);
   const SubD d = load_sub(A.subs + blockIdx.y);
   const fmp_shape& sh = A.shapes[d.shape];
   const int c = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -1697,8 +1701,11 @@ extern "C" int fmp_precond_create(const fmp_precond_desc* desc, fmp_precond** ou
   cudaFuncSetAttribute(k_column_fast<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kColFastSmem);
   cudaFuncSetAttribute(k_column_fast_db<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kColFastSmemDb);
   cudaFuncSetAttribute(k_column_fast_db<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kColFastSmemDb);
-  cudaFuncSetAttribute(k_faces<5, 2, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize, face_smem_words<5>() * 8);
-  cudaFuncSetAttribute(k_faces<9, 3, 9>, cudaFuncAttributeMaxDynamicSharedMemorySize, face_smem_words<9>() * 8);
+  {
+    const int slot = face_slot((p->max_p + 3) & ~3);
+    cudaFuncSetAttribute(k_faces<5, 2, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)face_smem_bytes<5>(slot));
+    cudaFuncSetAttribute(k_faces<9, 3, 9>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)face_smem_bytes<9>(slot));
+  }
   cudaFuncSetAttribute(k_corr<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * FaceMat<5>::WORDS * 8);
   cudaFuncSetAttribute(k_corr<9>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * FaceMat<9>::WORDS * 8);
   FMP_CHECK_CUDA(cudaGetLastError());
@@ -1829,10 +1836,11 @@ extern "C" int fmp_precond_apply(fmp_precond* p, const fmp_block* blk, int mode,
               p->d.rowmap};
   if (mode != FMP_SOLVE_EXACT) {
     const dim3 fg(3, (unsigned)p->d.n_sub);
+    const int slot = face_slot(fa.max_ps);
     if (pm <= 40)
-      k_faces<5, 2, 5><<<fg, FACE_THREADS, face_smem_words<5>() * sizeof(double), st>>>(fa);
+      k_faces<5, 2, 5><<<fg, FACE_THREADS, face_smem_bytes<5>(slot), st>>>(fa);
     else
-      k_faces<9, 3, 9><<<fg, FACE_THREADS, face_smem_words<9>() * sizeof(double), st>>>(fa);
+      k_faces<9, 3, 9><<<fg, FACE_THREADS, face_smem_bytes<9>(slot), st>>>(fa);
     FMP_CHECK_LAUNCH();
   }
   mark(3);
