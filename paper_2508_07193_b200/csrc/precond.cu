@@ -540,6 +540,7 @@ struct FastPlaneArgs {
   const double* factors;
   int mode;
   ExtTable et;
+  int tma_rows;        // > 0: forward planes inside the block arrive as one TMA box of PXS x tma_rows
 };
 
 // K1 (INV=false): plane k of S_i r -> Fy X Fx^T -> work;  K4 (INV=true): work plane -> Fy^T X Fx -> owned z
@@ -638,12 +639,21 @@ __device__ __forceinline__ void plane_step2(const double* T, const double* Fy, c
 }
 
 template <bool INV>
-__global__ void __launch_bounds__(PW_WARPS * 32, 1) k_plane_fast(FastPlaneArgs A) {
-  extern __shared__ __align__(16) double smem[];
+__global__ void __launch_bounds__(PW_WARPS * 32, 1) k_plane_fast(const __grid_constant__ CUtensorMap tm,
+                                                                  FastPlaneArgs A) {
+  extern __shared__ __align__(128) double smem[];
+  __shared__ __align__(8) uint64_t pbar[PW_WARPS];   // per-warp TMA completion (forward planes)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
   load_resident(smem, A.et, A.factors, tid, blockDim.x);
   double* T = smem + RES_WORDS + warp * PX_BUF;   // this warp's plane buffer (also the step-1 result)
   for (int q = tid; q < PW_WARPS * PX_BUF + PX_SLACK; q += blockDim.x) smem[RES_WORDS + q] = 0.0;
+  if (!INV && A.tma_rows > 0 && lane == 0) {
+    mbar_init(&pbar[warp], 1);
+    fence_mbar_init();
+  }
+  uint32_t tphase = 0;
+  // TMA destinations must be 128-byte aligned (RES_WORDS and PX_BUF keep the warp buffers so)
+  const bool tma_ok = !INV && A.tma_rows > 0 && (s_u32(T) & 127) == 0;
   __syncthreads();
   const int gw = blockIdx.x * PW_WARPS + warp, nw = gridDim.x * PW_WARPS;
   const int per = (A.n_items + nw - 1) / nw;
@@ -651,9 +661,7 @@ __global__ void __launch_bounds__(PW_WARPS * 32, 1) k_plane_fast(FastPlaneArgs A
 
   // returns the column shift of the plane data inside the buffer (16-byte superset loads);
   // no integer division in the copy loops (the XU pipe would become the bottleneck)
-  auto issue = [&](int it) -> int {
-    const int4 w = A.items[it];
-    const SubD d = load_sub(A.subs + w.x);
+  auto issue = [&](const int4 w, const SubD& d) -> int {
     const int c = w.y, ex = d.ex, ey = d.ey;
     double* X = T;
     if (INV || A.mode == FMP_SOLVE_FACES) {
@@ -677,6 +685,9 @@ __global__ void __launch_bounds__(PW_WARPS * 32, 1) k_plane_fast(FastPlaneArgs A
     }
     const bool inside = d.lx >= 0 && d.ly >= 0 && d.lz >= 0 && d.lx + ex <= A.g.bx && d.ly + ey <= A.g.by &&
                         d.lz + d.ez <= A.g.bz;
+    // the caller issues one TMA box (below); the box starts at an even x (16-byte aligned
+    // inner coordinate, tools/tma_test.cu), so odd-x planes land shifted by one column
+    if (!INV && inside && tma_ok) return -1 - (d.lx & 1);
     if (inside && (A.g.bx & 1) == 0) {
       const double* row0 = A.src + fidx(A.g, c, d.lz + w.z, d.ly, d.lx);
       const int shift = (int)(((uintptr_t)row0 >> 3) & 1);
@@ -701,13 +712,35 @@ __global__ void __launch_bounds__(PW_WARPS * 32, 1) k_plane_fast(FastPlaneArgs A
     return 0;
   };
 
+  // item metadata is software-pipelined: items[it+1] (and its subdomain record, when it
+  // changes) is fetched while item it computes, so no dependent global round trip sits in
+  // front of the next plane's copies
+  if (beg >= end) return;
+  int4 w_cur = A.items[beg];
+  SubD d_cur = load_sub(A.subs + w_cur.x);
   for (int it = beg; it < end; ++it) {
-    const int shift = issue(it);
+    int shift = issue(w_cur, d_cur);
+    if (shift < 0) {   // one TMA box: rows of PXS doubles land at stride PXS (issued here, in the
+                       // kernel body: the tensor map must stay a __grid_constant__ parameter)
+      fence_proxy_async();   // earlier generic accesses of the buffer before the async write
+      __syncwarp();
+      if (lane == 0) {
+        mbar_expect_tx(&pbar[warp], (uint32_t)(PXS * A.tma_rows * 8));
+        tma_load_4d(T, &tm, d_cur.lx & ~1, d_cur.ly, d_cur.lz + w_cur.z, w_cur.y, &pbar[warp]);
+      }
+    }
     cp_async_commit();
-    cp_async_wait<0>();
+    const int4 w_nxt = it + 1 < end ? A.items[it + 1] : w_cur;
+    if (shift < 0) {
+      mbar_wait(&pbar[warp], tphase);
+      tphase ^= 1u;
+      shift = -1 - shift;
+    } else {
+      cp_async_wait<0>();
+    }
     __syncwarp();
-    const int4 w = A.items[it];
-    const SubD d = load_sub(A.subs + w.x);
+    const int4 w = w_cur;
+    const SubD& d = d_cur;
     const int c = w.y;
     const double* Fx = res_factor(smem, A.et, c, 0, d.ex);
     const double* Fy = res_factor(smem, A.et, c, 1, d.ey);
@@ -734,6 +767,8 @@ __global__ void __launch_bounds__(PW_WARPS * 32, 1) k_plane_fast(FastPlaneArgs A
       plane_step2<INV, 1>(T, Fy, A, d, c, w.z, 4, k42, g, t);
     }
     __syncwarp();
+    if (w_nxt.x != w_cur.x) d_cur = load_sub(A.subs + w_nxt.x);
+    w_cur = w_nxt;
   }
 }
 
@@ -1786,11 +1821,23 @@ static int plane_pass(fmp_precond* p, const fmp_block* blk, bool inv, int mode, 
     a.factors = p->d.factors;
     a.mode = mode;
     a.et = p->et;
+    CUtensorMap tm{};
+    a.tma_rows = 0;
+    if (!inv && mode != FMP_SOLVE_FACES && (blk->bx & 1) == 0 && ((uintptr_t)src & 15) == 0 &&
+        !getenv_flag("FMP_PLANE_NO_TMA")) {
+      // the block field as a 4-D tensor (x, y, z, component); box = one haloed subdomain plane
+      const uint64_t dims[4] = {(uint64_t)blk->bx, (uint64_t)blk->by, (uint64_t)blk->bz, 3};
+      const uint64_t strides[3] = {(uint64_t)blk->bx * 8, (uint64_t)(blk->bx * blk->by) * 8,
+                                   (uint64_t)(blk->bx * blk->by * blk->bz) * 8};
+      const uint32_t box[4] = {PXS, (uint32_t)p->max_ey, 1, 1};
+      if (int e = encode_tensor_map_f64(&tm, src, 4, dims, strides, box)) return e;
+      a.tma_rows = p->max_ey;
+    }
     const int grid = std::min(p->sms, (a.n_items + PW_WARPS - 1) / PW_WARPS);
     if (inv)
-      k_plane_fast<true><<<grid, PW_WARPS * 32, kPlaneFastSmem, st>>>(a);
+      k_plane_fast<true><<<grid, PW_WARPS * 32, kPlaneFastSmem, st>>>(tm, a);
     else
-      k_plane_fast<false><<<grid, PW_WARPS * 32, kPlaneFastSmem, st>>>(a);
+      k_plane_fast<false><<<grid, PW_WARPS * 32, kPlaneFastSmem, st>>>(tm, a);
     FMP_CHECK_LAUNCH();
     return 0;
   }

@@ -156,15 +156,16 @@ __global__ void __launch_bounds__(TX* TY) k_spmv(Geo g, double alpha, int bnd, c
 // cp.async.bulk per row (16-byte aligned, from x = i0-2); halo cells outside the block are
 // bulk-copied from a zero page (the zero-ghost physical boundary), so every row is exactly
 // 544 bytes and every plane exactly 16,320 -- one mbarrier transaction count per slot.
-// Tiles off the low faces take the whole plane as ONE TMA box load instead (tile-mode TMA
-// coordinates must be non-negative on this part -- tools/tma_test.cu -- so the low faces
-// cannot use it; cells beyond the high faces are zero-filled by the TMA unit).
+// Tiles off the low faces take the whole plane as ONE TMA box load instead (cells beyond the
+// high faces are zero-filled by the TMA unit; the low faces keep the row copies because the
+// halo starts at x = -1 and a tile-mode box must start at a 16-byte aligned inner coordinate,
+// tools/tma_test.cu).
 // Eight consumer warps wait on the slot's "full" barrier, compute, and release the slot on its
 // "empty" barrier; no CTA-wide barrier in the loop, so consumers and producer drift freely
 // within the ring.
 // GPU-block faces with neighbour ghosts are patched in shared memory after the plane lands.
-// Work: units (z-chunk of L planes) x (64 x 8 column tile), z-chunk-major, dealt round-robin
-// to a grid of exactly the resident CTAs, so CTAs that run concurrently hold neighbouring
+// Work: units (z-chunk of L planes) x (64 x 8 column tile), z-chunk-major, handed out by an
+// atomic counter to a grid of exactly the resident CTAs, so CTAs that run concurrently hold neighbouring
 // tiles of the same z range and the halo rows/planes they share are L2 hits.
 constexpr int SX = 64, SY = 8;
 constexpr int SXR = SX + 4, SYH = SY + 2;          // smem row: logical i0-2 .. i0+SX+1
@@ -173,8 +174,8 @@ constexpr int SSLOT = (SPLANE + 15) / 16 * 16;      // slot stride: TMA destinat
 constexpr int SCONS = 8;                            // consumer warps
 constexpr int STHREADS = (SCONS + 1) * 32;
 constexpr uint32_t kPlaneBytes = SPLANE * 8;
-// [ring: NS x SSLOT doubles][2 x NS mbarriers][NS unit ids (int64)][SCONS reduction words]
-constexpr int spmv_bulk_smem(int ns) { return (ns * SSLOT + 3 * ns + SCONS) * (int)sizeof(double); }
+// [ring: NS x SSLOT doubles][2 x NS mbarriers][NS unit ids (int64)][2 x SCONS reduction words]
+constexpr int spmv_bulk_smem(int ns) { return (ns * SSLOT + 3 * ns + 2 * SCONS) * (int)sizeof(double); }
 
 struct BulkSpmvArgs {
   Geo g;
@@ -270,10 +271,13 @@ __global__ void __launch_bounds__(STHREADS, SNSLOT <= 4 ? 3 : 2) k_spmv_bulk(con
   // Plane k-1 is never re-read from shared memory: the five values the stencil needs from it
   // were read from plane k one step earlier and are carried in registers (20 shared loads per
   // point instead of 25).  So only planes k and k+1 are held; plane k is released after the step.
+  // Fused dot products: one partial per UNIT (not per CTA), summed over the 8 consumer warps in a
+  // fixed order, so the result does not depend on which CTA the scheduler gave a unit to and the
+  // final fixed-order reduction over units is deterministic.
   const int ly = warp;
-  double acc0 = 0.0, acc1 = 0.0;
   int64_t qbase = 0;   // load index of the current unit's first plane (k0 - 1)
   for (;;) {
+    double acc0 = 0.0, acc1 = 0.0;
     mbar_wait(&full[qbase % SNSLOT], (uint32_t)((qbase / SNSLOT) & 1));
     const int64_t u = slot_unit[qbase % SNSLOT];
     if (u < 0) break;
@@ -382,29 +386,27 @@ __global__ void __launch_bounds__(STHREADS, SNSLOT <= 4 ? 3 : 2) k_spmv_bulk(con
       }
     }
     qbase += np + 2;
-  }
-  if (MODE >= 1) {   // consumer-only reduction (named barrier 1)
+    if (MODE >= 1) {   // this unit's partial(s): consumer-only reduction (named barrier 1)
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      acc0 += __shfl_xor_sync(0xffffffffu, acc0, o);
-      acc1 += __shfl_xor_sync(0xffffffffu, acc1, o);
-    }
-    if (lx == 0) red[warp] = acc0;
-    asm volatile("bar.sync 1, %0;\n" ::"n"(SCONS * 32) : "memory");
-    if (tid == 0) {
-      double s0 = 0.0;
-      for (int w2 = 0; w2 < SCONS; ++w2) s0 += red[w2];
-      A.partials[blockIdx.x] = s0;
-    }
-    if (MODE == 2) {
-      asm volatile("bar.sync 1, %0;\n" ::"n"(SCONS * 32) : "memory");
-      if (lx == 0) red[warp] = acc1;
+      for (int o = 16; o > 0; o >>= 1) {
+        acc0 += __shfl_xor_sync(0xffffffffu, acc0, o);
+        acc1 += __shfl_xor_sync(0xffffffffu, acc1, o);
+      }
+      if (lx == 0) {
+        red[warp] = acc0;
+        red[SCONS + warp] = acc1;
+      }
       asm volatile("bar.sync 1, %0;\n" ::"n"(SCONS * 32) : "memory");
       if (tid == 0) {
-        double s1 = 0.0;
-        for (int w2 = 0; w2 < SCONS; ++w2) s1 += red[w2];
-        A.partials[gridDim.x + blockIdx.x] = s1;
+        double s0 = 0.0, s1 = 0.0;
+        for (int w2 = 0; w2 < SCONS; ++w2) {
+          s0 += red[w2];
+          s1 += red[SCONS + w2];
+        }
+        A.partials[u] = s0;
+        if (MODE == 2) A.partials[units + u] = s1;
       }
+      asm volatile("bar.sync 1, %0;\n" ::"n"(SCONS * 32) : "memory");
     }
   }
 }
@@ -553,8 +555,14 @@ extern "C" int fmp_stencil_apply(const fmp_block* blk, double alpha, int boundar
     const int64_t ntiles = (int64_t)a.tiles_x * a.tiles_y;
     const int64_t resident = (int64_t)kNumSM * resident_per_sm;
     spmv_chunking(ntiles, g.bz, resident, &a.L, &a.nzc);
+    if (mode >= 1)   // one partial per unit (two in mode 2) must fit the scratch: longer chunks
+      while (ntiles * a.nzc > kScratchDoubles / 2 && a.L < g.bz) {
+        a.L = std::min(g.bz, 2 * a.L);
+        a.nzc = (g.bz + a.L - 1) / a.L;
+      }
     const int64_t units = ntiles * a.nzc;
-    const int grid = (int)std::min<int64_t>(units, std::min<int64_t>(resident, kScratchDoubles / 2));
+    FMP_REQUIRE(mode == 0 || units <= kScratchDoubles / 2, "block too large for the SpMV reduction scratch");
+    const int grid = (int)std::min<int64_t>(units, resident);
     CUtensorMap tm;
     const uint64_t dims[4] = {(uint64_t)g.bx, (uint64_t)g.by, (uint64_t)g.bz, 3};
     const uint64_t strides[3] = {(uint64_t)g.bx * 8, (uint64_t)g.bx * g.by * 8, (uint64_t)g.bx * g.by * g.bz * 8};
@@ -574,7 +582,7 @@ extern "C" int fmp_stencil_apply(const fmp_block* blk, double alpha, int boundar
     }
 #undef FMP_SPMV_GO
     FMP_CHECK_LAUNCH();
-    if (mode >= 1) return finish_reduce(scratch, grid, mode == 2 ? 2 : 1, dots, st);
+    if (mode >= 1) return finish_reduce(scratch, (int)units, mode == 2 ? 2 : 1, dots, st);
     return 0;
   }
   const int tx = (g.bx + TX - 1) / TX, ty = (g.by + TY - 1) / TY;

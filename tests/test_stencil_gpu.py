@@ -139,3 +139,18 @@ def test_cn_stencils_match_reference():
         H = FieldVector(box, rng.uniform(-1, 1, box.dof))
         R = build_rhs(EmState(E, H, 0, 1.0))
         assert rel(R.data, g[f"rhs_{tag}"]) <= 1e-14
+
+
+def test_fused_dots_are_deterministic():
+    """The SpMV's fused dot products do not depend on the dynamic unit scheduling: repeated
+    launches give bitwise-identical sums (per-unit partials, fixed-order final reduction)."""
+    from paper_2508_07193_b200 import Box, DistributedOperator, make_partition, make_transport
+    n = 128
+    op = DistributedOperator(make_partition(Box(n, n, n), (4, 4, 4), 1), 0.25, make_transport("cuda"))
+    g = torch.Generator(device="cuda").manual_seed(5)
+    x = torch.rand(3, n, n, n, dtype=torch.float64, device="cuda", generator=g)
+    w = torch.rand_like(x)
+    y = torch.empty_like(x)
+    first = (op.apply_dots(x, y, w, both=True), op.residual_norm2(x, w))
+    for _ in range(8):
+        assert (op.apply_dots(x, y, w, both=True), op.residual_norm2(x, w)) == first

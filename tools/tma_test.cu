@@ -24,7 +24,8 @@ __global__ void k(const __grid_constant__ CUtensorMap tm, double* out, int rank,
   __syncthreads();
   if (threadIdx.x == 0) {
     mbar_expect_tx(bar, bytes);
-    if (rank == 4) tma_load_4d(sm, &tm, cx, c0, 0, 0, bar);
+    if (rank % 100 == 44) tma_load_4d(sm, &tm, cx, c0, (rank / 100) % 10, rank / 1000, bar);
+    else if (rank == 4) tma_load_4d(sm, &tm, cx, c0, 0, 0, bar);
     else tma2d(sm, &tm, cx, c0, bar);
   }
   mbar_wait(bar, 0);
@@ -53,6 +54,19 @@ int main(int argc, char** argv) {
   const uint32_t box[4] = {(uint32_t)bxw, 10, 1, 3};
   const uint64_t dims2[2] = {bx, (uint64_t)by * bz * 3};
   int e;
+  if (variant >= 10) {   // box probes: argv = variant bw bh bc cx cy cz cc
+    const int bw = atoi(argv[2]), bh = atoi(argv[3]), bc = atoi(argv[4]);
+    const int cx = atoi(argv[5]), cy = atoi(argv[6]), cz = atoi(argv[7]), cc = atoi(argv[8]);
+    const uint64_t d10[4] = {bx, by, bz, 3};
+    const uint32_t b10[4] = {(uint32_t)bw, (uint32_t)bh, 1, (uint32_t)bc};
+    e = encode_tensor_map_f64(&tm, x, 4, d10, strides, b10);
+    printf("box {%d,%d,1,%d} at (%d,%d,%d,%d) encode %d\n", bw, bh, bc, cx, cy, cz, cc, e);
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 8192 * 8 + 128);
+    k<<<1, 128, 8192 * 8 + 128>>>(tm, out, 44 + 100 * cz + 1000 * cc, bw * bh * bc * 8, cx, cy, bw * bh * bc);
+    cudaError_t err = cudaDeviceSynchronize();
+    printf("  -> %s\n", cudaGetErrorString(err));
+    return err ? 1 : 0;
+  }
   if (variant >= 5) {   // same bytes as 32-bit or 64-bit integer elements
     const int dt = variant == 5 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : variant == 6 ? CU_TENSOR_MAP_DATA_TYPE_INT64
                                                                                  : CU_TENSOR_MAP_DATA_TYPE_UINT32;
