@@ -150,23 +150,17 @@ __global__ void __launch_bounds__(TX* TY) k_spmv(Geo g, double alpha, int bnd, c
   }
 }
 
-// ---------------------------------------------------------------- SpMV, bulk-copy variant (sm_100a)
-// Same z-march, warp-specialised.  A producer warp streams each haloed plane of all three
-// components ([3][SY+2][SX+4] doubles, 16 KB) into a 4-slot shared-memory ring with one
-// cp.async.bulk per row (16-byte aligned, from x = i0-2); halo cells outside the block are
-// bulk-copied from a zero page (the zero-ghost physical boundary), so every row is exactly
-// 544 bytes and every plane exactly 16,320 -- one mbarrier transaction count per slot.
-// Tiles off the low faces take the whole plane as ONE TMA box load instead (cells beyond the
-// high faces are zero-filled by the TMA unit; the low faces keep the row copies because the
-// halo starts at x = -1 and a tile-mode box must start at a 16-byte aligned inner coordinate,
-// tools/tma_test.cu).
-// Eight consumer warps wait on the slot's "full" barrier, compute, and release the slot on its
-// "empty" barrier; no CTA-wide barrier in the loop, so consumers and producer drift freely
-// within the ring.
+// ---------------------------------------------------------------- SpMV, TMA z-march (sm_100a)
+// Warp-specialised.  A producer warp streams each haloed plane of all three components
+// ([3][SY+2][SX+4] doubles, 16 KB) into a 4-slot shared-memory ring with ONE TMA box load per
+// plane; cells outside the block (the zero-ghost physical boundary) are the TMA unit's
+// out-of-bounds zero fill, so there is no boundary code.  Eight consumer warps wait on the
+// slot's "full" mbarrier, compute, and release the slot on its "empty" mbarrier; no CTA-wide
+// barrier in the loop, so consumers and producer drift freely within the ring.
 // GPU-block faces with neighbour ghosts are patched in shared memory after the plane lands.
 // Work: units (z-chunk of L planes) x (64 x 8 column tile), z-chunk-major, handed out by an
-// atomic counter to a grid of exactly the resident CTAs, so CTAs that run concurrently hold neighbouring
-// tiles of the same z range and the halo rows/planes they share are L2 hits.
+// atomic counter to a grid of exactly the resident CTAs, so CTAs that run concurrently hold
+// neighbouring tiles of the same z range and the halo rows/planes they share are L2 hits.
 constexpr int SX = 64, SY = 8;
 constexpr int SXR = SX + 4, SYH = SY + 2;          // smem row: logical i0-2 .. i0+SX+1
 constexpr int SPL = SXR * SYH, SPLANE = 3 * SPL;   // doubles per component plane / per plane
@@ -183,7 +177,6 @@ struct BulkSpmvArgs {
   double* y;
   const double* w;
   double* partials;
-  const double* zeros;   // >= SXR doubles of 0.0 (16-byte aligned)
   unsigned long long* counter;   // [fetch, done]: dynamic unit scheduler, zero between launches
   double alpha;
   int bnd, tiles_x, tiles_y, L, nzc, ghosts;
@@ -238,8 +231,6 @@ __global__ void __launch_bounds__(STHREADS, SNSLOT <= 4 ? 3 : 2) k_spmv_bulk(con
       }
       const int tile = (int)(u % ntiles), zc = (int)(u / ntiles);
       const int i0 = (tile % A.tiles_x) * SX, j0 = (tile / A.tiles_x) * SY, k0 = zc * A.L;
-      const int xs = max(i0 - 2, 0), xe = min(i0 + SX + 2, g.bx);   // in-block x range (even bounds)
-      const int c_lo = xs - (i0 - 2), c_hi = xe - (i0 - 2);          // its smem columns
       const int np = nplanes(u);
       for (int m = 0; m < np + 2; ++m, ++q) {
         const int s = (int)(q % SNSLOT), k = k0 - 1 + m;
@@ -249,19 +240,11 @@ __global__ void __launch_bounds__(STHREADS, SNSLOT <= 4 ? 3 : 2) k_spmv_bulk(con
           mbar_expect_tx(&full[s], kPlaneBytes);
         }
         __syncwarp();
-        if (i0 >= 2 && j0 >= 1 && k >= 0) {   // one TMA box (beyond-the-end cells zero-filled)
-          if (lx == 0) tma_load_4d(ring + s * SSLOT, &tm, i0 - 2, j0 - 1, k, 0, &full[s]);
-        } else if (lx < 3 * SYH) {   // low faces: one bulk copy per (component, row) + zero page
-          const int c = lx / SYH, jj = lx - c * SYH, j = j0 - 1 + jj;
-          double* row = ring + s * SSLOT + c * SPL + jj * SXR;
-          if ((unsigned)j < (unsigned)g.by && (unsigned)k < (unsigned)g.bz) {
-            bulk_g2s(row + c_lo, A.x + fidx(g, c, k, j, xs), (uint32_t)(c_hi - c_lo) * 8, &full[s]);
-            if (c_lo > 0) bulk_g2s(row, A.zeros, (uint32_t)c_lo * 8, &full[s]);
-            if (c_hi < SXR) bulk_g2s(row + c_hi, A.zeros, (uint32_t)(SXR - c_hi) * 8, &full[s]);
-          } else {
-            bulk_g2s(row, A.zeros, SXR * 8, &full[s]);
-          }
-        }
+        // one TMA box per plane; cells outside the block (negative or beyond-the-end
+        // coordinates) are zero-filled by the TMA unit = the zero-ghost boundary.  The box
+        // starts at x = i0 - 2: tile-mode boxes need a 16-byte aligned inner coordinate
+        // (negative ones are fine), tools/tma_test.cu
+        if (lx == 0) tma_load_4d(ring + s * SSLOT, &tm, i0 - 2, j0 - 1, k, 0, &full[s]);
       }
     }
     return;
@@ -545,13 +528,12 @@ extern "C" int fmp_stencil_apply(const fmp_block* blk, double alpha, int boundar
     a.tiles_y = (g.by + SY - 1) / SY;
     a.ghosts = 0;
     for (int q = 0; q < 6; ++q) a.ghosts |= g.ghost[q] != nullptr;
-    static double* zeros = nullptr;
-    if (!zeros) {
-      FMP_CHECK_CUDA(cudaMalloc(&zeros, 4096));
-      FMP_CHECK_CUDA(cudaMemset(zeros, 0, 4096));
+    static unsigned long long* counter = nullptr;   // [fetch, done] of the unit scheduler, zero at rest
+    if (!counter) {
+      FMP_CHECK_CUDA(cudaMalloc(&counter, 2 * sizeof(unsigned long long)));
+      FMP_CHECK_CUDA(cudaMemset(counter, 0, 2 * sizeof(unsigned long long)));
     }
-    a.zeros = zeros;
-    a.counter = reinterpret_cast<unsigned long long*>(zeros + 256);   // bytes 2048.. of the page
+    a.counter = counter;
     const int64_t ntiles = (int64_t)a.tiles_x * a.tiles_y;
     const int64_t resident = (int64_t)kNumSM * resident_per_sm;
     spmv_chunking(ntiles, g.bz, resident, &a.L, &a.nzc);
