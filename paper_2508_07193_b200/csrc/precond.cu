@@ -485,11 +485,12 @@ constexpr int PX_ROWS = 36;          // plane buffer rows (DMMA row tile 4 reads
 constexpr int PX_BUF = PX_ROWS * PXS;
 constexpr int PX_SLACK = 5 * PXS;    // after the last buffer (row tile 4 + the K-pad column overrun)
 constexpr int PW_WARPS = 12;         // warps per plane CTA, each independent (3 per SMSP)
-constexpr int CXS = 12;              // column tile row stride (8 columns + 4)
+constexpr int CXS = 8;               // column tile row stride (8 columns; fragment loads are contiguous)
 constexpr int CXR = 36;              // column tile rows per component (pad4 of the max extent)
 constexpr int CX_BUF = 3 * CXR * CXS;  // one column tile (3 components)
 constexpr int CW_WARPS = 12;         // single-buffered inverse pass
-constexpr int CW_WARPS_DB = 8;       // double-buffered forward pass
+constexpr int CW_WARPS_FWD = 8;      // double-buffered forward column pass
+constexpr int CW_WARPS_INV = 12;     // double-buffered inverse column pass (3 warps per SM sub-partition)
 constexpr int FAST_MAX_EXT = CXR;    // the fast path serves plans whose extents are all <= 36
 
 struct ExtTable {
@@ -949,15 +950,15 @@ __device__ __forceinline__ void col_mma(double (&acc)[3][5][2], const double* xb
 // warp share their subdomain record, reloaded only when it changes), so the cp.async of the
 // next tile is issued with no dependent global round trip in front of it; the correction
 // planes of K3 are read with all loads of a lane hoisted ahead of the arithmetic.
-template <bool INV>
-__global__ void __launch_bounds__(CW_WARPS_DB * 32, 1) k_column_fast_db(FastColArgs A) {
+template <bool INV, int NW = INV ? CW_WARPS_INV : CW_WARPS_FWD>
+__global__ void __launch_bounds__(NW * 32, 1) k_column_fast_db(FastColArgs A) {
   extern __shared__ __align__(16) double smem[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
   load_resident(smem, A.et, A.factors, tid, blockDim.x);
   double* wbase = smem + RES_WORDS + warp * 2 * CX_BUF;
   for (int q = lane; q < 2 * CX_BUF; q += 32) wbase[q] = 0.0;
   __syncthreads();
-  const int gw = blockIdx.x * CW_WARPS_DB + warp, nw = gridDim.x * CW_WARPS_DB;
+  const int gw = blockIdx.x * NW + warp, nw = gridDim.x * NW;
   const int per = (A.n_items + nw - 1) / nw;
   const int beg = gw * per, end = min(beg + per, A.n_items);
   if (beg >= end) return;
@@ -1516,7 +1517,7 @@ static void free_plan(fmp_precond* p) {
 
 constexpr int kPlaneFastSmem = (RES_WORDS + PW_WARPS * PX_BUF + PX_SLACK) * (int)sizeof(double);
 constexpr int kColFastSmem = (RES_WORDS + CW_WARPS * CX_BUF) * (int)sizeof(double);
-constexpr int kColFastSmemDb = (RES_WORDS + CW_WARPS_DB * 2 * CX_BUF) * (int)sizeof(double);
+constexpr int col_db_smem(int nw) { return (RES_WORDS + nw * 2 * CX_BUF) * (int)sizeof(double); }
 
 static int plane_nt(const fmp_precond* p) { return std::max(p->max_ex, p->max_ey) <= 40 ? 5 : 9; }
 static int column_mt(const fmp_precond* p) { return pad8(p->max_ez) / 8; }
@@ -1734,8 +1735,8 @@ extern "C" int fmp_precond_create(const fmp_precond_desc* desc, fmp_precond** ou
   cudaFuncSetAttribute(k_plane_fast<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kPlaneFastSmem);
   cudaFuncSetAttribute(k_column_fast<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kColFastSmem);
   cudaFuncSetAttribute(k_column_fast<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kColFastSmem);
-  cudaFuncSetAttribute(k_column_fast_db<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kColFastSmemDb);
-  cudaFuncSetAttribute(k_column_fast_db<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kColFastSmemDb);
+  cudaFuncSetAttribute(k_column_fast_db<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, col_db_smem(CW_WARPS_FWD));
+  cudaFuncSetAttribute(k_column_fast_db<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, col_db_smem(CW_WARPS_INV));
   {
     const int slot = face_slot((p->max_p + 3) & ~3);
     cudaFuncSetAttribute(k_faces<5, 2, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)face_smem_bytes<5>(slot));
@@ -1772,11 +1773,12 @@ static int column_pass(fmp_precond* p, bool inv, const double* src, double* dst,
       const int grid = std::min(p->sms, (p->n_fcol + CW_WARPS - 1) / CW_WARPS);
       k_column_fast<true><<<grid, CW_WARPS * 32, kColFastSmem, st>>>(a);
     } else {
-      const int grid = std::min(p->sms, (p->n_fcol + CW_WARPS_DB - 1) / CW_WARPS_DB);
+      const int nwarp = inv ? CW_WARPS_INV : CW_WARPS_FWD;
+      const int grid = std::min(p->sms, (p->n_fcol + nwarp - 1) / nwarp);
       if (inv)
-        k_column_fast_db<true><<<grid, CW_WARPS_DB * 32, kColFastSmemDb, st>>>(a);
+        k_column_fast_db<true><<<grid, nwarp * 32, col_db_smem(nwarp), st>>>(a);
       else
-        k_column_fast_db<false><<<grid, CW_WARPS_DB * 32, kColFastSmemDb, st>>>(a);
+        k_column_fast_db<false><<<grid, nwarp * 32, col_db_smem(nwarp), st>>>(a);
     }
     FMP_CHECK_LAUNCH();
     return 0;
