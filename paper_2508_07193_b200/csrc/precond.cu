@@ -484,7 +484,7 @@ constexpr int PX_ROWS = 36;          // plane buffer rows (DMMA row tile 4 reads
                                      // next buffer: finite data, discarded outputs)
 constexpr int PX_BUF = PX_ROWS * PXS;
 constexpr int PX_SLACK = 5 * PXS;    // after the last buffer (row tile 4 + the K-pad column overrun)
-constexpr int PW_WARPS = 12;         // warps per plane CTA, each independent (3 per SMSP)
+constexpr int PW_WARPS = 16;         // warps per plane CTA, each independent (4 per SMSP)
 constexpr int CXS = 8;               // column tile row stride (8 columns; fragment loads are contiguous)
 constexpr int CXR = 36;              // column tile rows per component (pad4 of the max extent)
 constexpr int CX_BUF = 3 * CXR * CXS;  // one column tile (3 components)
