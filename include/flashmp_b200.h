@@ -95,6 +95,15 @@ int fmp_vec_scale(int64_t n, double a, const double* x, double* out, void* strea
 /* out[0] = (x, y)                     ref: krylov.py:108-112 (_Dist.dot) */
 int fmp_vec_dot(int64_t n, const double* x, const double* y, double* out,
                 double* scratch, void* stream);
+/* y += a*x, then dots[0] = (z, y_new); z may equal y (the norm)   ref: krylov.py:301-309
+ * (one modified Gram-Schmidt step fused with the next step's inner product) */
+int fmp_vec_axpy_dot(int64_t n, double a, const double* x, double* y, const double* z,
+                     double* dots, double* scratch, void* stream);
+/* out = x + c_0 v_0 + c_1 v_1 + ... evaluated left to right with every product and sum rounded,
+ * i.e. the reference's copy + axpy_into loop (ref: krylov.py:348-350) in one pass.
+ * v and coef are HOST arrays of k device pointers / coefficients. */
+int fmp_vec_combine(int64_t n, const double* x, int k, const double* const* v, const double* coef,
+                    double* out, void* stream);
 /* BiCGSTAB p-update, in place: p = r + beta*(p + (-omega)*v)   ref: krylov.py:181-182 */
 int fmp_bicg_p(int64_t n, const double* r, double* p, const double* v,
                double beta, double omega, void* stream);

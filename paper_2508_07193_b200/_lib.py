@@ -30,6 +30,8 @@ SIGNATURES = {
     "fmp_vec_axpy": (_i, [_i64, _d, _p, _p, _p]),
     "fmp_vec_scale": (_i, [_i64, _d, _p, _p, _p]),
     "fmp_vec_dot": (_i, [_i64, _p, _p, _p, _p, _p]),
+    "fmp_vec_axpy_dot": (_i, [_i64, _d, _p, _p, _p, _p, _p, _p]),
+    "fmp_vec_combine": (_i, [_i64, _p, _i, _p, _p, _p, _p]),
     "fmp_bicg_p": (_i, [_i64, _p, _p, _p, _d, _d, _p]),
     "fmp_bicg_xr": (_i, [_i64, _p, _p, _p, _p, _p, _p, _p, _d, _d, _p, _p, _p]),
     "fmp_precond_create": (_i, [_p, C.POINTER(_p)]),

@@ -6,6 +6,7 @@
 // Roofline: HBM-bound; bytes per double = 8 x (vectors read + written).
 #include <cstdarg>
 #include <cstring>
+#include <algorithm>
 #include "common.cuh"
 
 namespace fmp {
@@ -101,6 +102,38 @@ __global__ void __launch_bounds__(kVecThreads) k_bicg_xr(int64_t n, double* __re
   if (threadIdx.x == 0) partials[blockIdx.x] = acc;
 }
 
+// y += a*x, then partial of (z, y_new)   (one MGS step of ref:krylov.py:301-309 fused with the
+// next step's inner product; z = y gives the norm that ends the sweep)
+__global__ void __launch_bounds__(kVecThreads) k_axpy_dot(int64_t n, double a, const double* __restrict__ x,
+                                                          double* y, const double* z,
+                                                          double* __restrict__ partials) {
+  __shared__ double red[kVecThreads / 32];
+  double acc = 0.0;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x) {
+    const double yv = add_rn(y[q], mul_rn(a, x[q]));
+    y[q] = yv;
+    acc = fma(z == y ? yv : z[q], yv, acc);
+  }
+  acc = block_sum<kVecThreads>(acc, red);
+  if (threadIdx.x == 0) partials[blockIdx.x] = acc;
+}
+
+// out = x; out += c_0 v_0; out += c_1 v_1; ...  in that order, each product and sum rounded
+// (the reference's copy + axpy_into loop, ref:krylov.py:348-350), one pass over memory
+constexpr int kCombineMax = 32;
+struct CombineArgs {
+  const double* v[kCombineMax];
+  double c[kCombineMax];
+  int k;
+};
+__global__ void k_combine(int64_t n, const double* __restrict__ x, const CombineArgs A, double* __restrict__ out) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x) {
+    double t = x[q];
+    for (int i = 0; i < A.k; ++i) t = add_rn(t, mul_rn(A.c[i], A.v[i][q]));
+    out[q] = t;
+  }
+}
+
 static inline int vec_grid(int64_t n) {
   const int64_t need = (n + kVecThreads - 1) / kVecThreads;
   return (int)(need < kVecGrid ? (need > 0 ? need : 1) : kVecGrid);
@@ -151,6 +184,36 @@ extern "C" int fmp_vec_dot(int64_t n, const double* x, const double* y, double* 
   k_dot<<<grid, kVecThreads, 0, st>>>(n, x, y, scratch);
   FMP_CHECK_LAUNCH();
   return finish_reduce(scratch, grid, 1, out, st);
+}
+
+extern "C" int fmp_vec_axpy_dot(int64_t n, double a, const double* x, double* y, const double* z, double* dots,
+                                double* scratch, void* stream) {
+  const int grid = vec_grid(n);
+  cudaStream_t st = as_stream(stream);
+  k_axpy_dot<<<grid, kVecThreads, 0, st>>>(n, a, x, y, z, scratch);
+  FMP_CHECK_LAUNCH();
+  return finish_reduce(scratch, grid, 1, dots, st);
+}
+
+extern "C" int fmp_vec_combine(int64_t n, const double* x, int k, const double* const* v, const double* coef,
+                               double* out, void* stream) {
+  FMP_REQUIRE(k >= 0 && (k == 0 || (v && coef)), "bad combine arguments");
+  if (n <= 0) return 0;
+  cudaStream_t st = as_stream(stream);
+  const double* src = x;
+  for (int i0 = 0; i0 < k || i0 == 0; i0 += kCombineMax) {   // chunks of kCombineMax terms, in order
+    CombineArgs a{};
+    a.k = std::min(kCombineMax, k - i0);
+    for (int i = 0; i < a.k; ++i) {
+      a.v[i] = v[i0 + i];
+      a.c[i] = coef[i0 + i];
+    }
+    k_combine<<<vec_grid(n), kVecThreads, 0, st>>>(n, src, a, out);
+    FMP_CHECK_LAUNCH();
+    src = out;
+    if (k == 0) break;
+  }
+  return 0;
 }
 
 extern "C" int fmp_bicg_p(int64_t n, const double* r, double* p, const double* v, double beta, double omega,
