@@ -103,6 +103,17 @@ class ClockSampler:
 
 # ----------------------------------------------------------------------------------- ours
 INT8_PROBE_FILE = ROOT / "profiles" / "r01_umma_i8_rate.json"
+NCU_TRAFFIC_FILE = ROOT / "profiles" / "r01_v18_ncu_traffic.json"
+# bench stage -> ncu kernel name(s) whose DRAM bytes (one ncu --set full capture) it covers
+STAGE_KERNELS = {"plane_fwd": ["k_plane_fast<0>"], "column_fwd": ["k_column_fast_db<0, 8>"],
+                 "faces": ["k_faces<5, 2, 5>"], "slice_y": ["k_ozaki_exp", "k_ozaki_digits"], "gemm": ["k_ozaki"],
+                 "corr": ["k_corr<5>"], "column_inv": ["k_column_fast_db<1, 12>"], "plane_inv": ["k_plane_fast<1>"]}
+
+
+def ncu_traffic() -> dict:
+    """DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum) from the committed
+    ncu --set full capture of the cfg4 apply (tools/ncu_full.sh + tools/ncu_traffic.py)."""
+    return json.loads(NCU_TRAFFIC_FILE.read_text()) if NCU_TRAFFIC_FILE.exists() else {}
 
 
 def int8_peak_tops() -> tuple[float, str]:
@@ -144,9 +155,13 @@ def stage_rooflines(prec, x, z, specs, peaks, reps):
             m = sum(correction_counts(plan.shapes[g]))
             gemm_f += 2 * m * m * plan.gcols[g]
     fp64, hbm = peaks["fp64_tflops"], peaks["hbm_gbs"]
+    traffic = ncu_traffic()
     out = {}
     for k, ms in acc.items():
         e = {"ms": round(ms, 4)}
+        tb = [traffic[n]["traffic_bytes"] for n in STAGE_KERNELS.get(k, []) if n in traffic]
+        if tb:
+            e["traffic_bytes"] = sum(tb)
         if k in fl:
             a = fl[k] / ms / 1e9
             e.update(bound="tensor (FP64 DMMA)", achieved_tflops=round(a, 2), frac=round(a / fp64, 3))
@@ -324,11 +339,17 @@ def run_ours(args):
                           "tflops_reference_count": round(flops_ref / t_prec / 1e12, 2)},
         "precond_kernels": stages,
         "spmv": {"ms": round(t_spmv * 1e3, 4), "GB_per_s": round(spmv_bytes / t_spmv / 1e9, 1),
+                 "algorithmic_bytes": spmv_bytes,
+                 "traffic_bytes": ncu_traffic().get("k_spmv_bulk<0, 4>", {}).get("traffic_bytes"),
                  "frac_hbm": round(spmv_bytes / t_spmv / 1e9 / peaks["hbm_gbs"], 3)},
         "roofline": {"kernel": "RAS precond apply (fused FlashMP sequence: FP64 DMMA transforms + Ozaki INT8 tcgen05 Woodbury GEMM)",
                      "bound": "tensor", "achieved": round(prec_tflops, 3), "peak": peaks["fp64_tflops"],
                      "unit": "TFLOP/s", "frac": round(prec_tflops / peaks["fp64_tflops"], 3)
-                     if peaks["fp64_tflops"] else None, "traffic": None,
+                     if peaks["fp64_tflops"] else None,
+                     "traffic": (sum(v.get("traffic_bytes", 0) for v in stages.values()) or None),
+                     "traffic_note": "DRAM bytes per apply, sum over its kernels from one ncu --set full capture "
+                                     "(profiles/r01_v18_ncu_traffic.json); algorithmic bytes "
+                                     f"{bytes_alg} (precond_apply.algorithmic_bytes)",
                      "peak_source": peaks["fp64_source"], "flops_per_launch": flops_exec},
         "breakdown_ms": breakdown,
         "gpu_launches": int(launches),
