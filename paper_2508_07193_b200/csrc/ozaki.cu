@@ -204,45 +204,12 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
 }
 
 // ---------------------------------------------------------------- slicing
-// Batched over operands (OzSlice table).  Pass 1: one CTA per row -> exponent e with
-// max|x| < 2^e.  Pass 2: one thread per 16-byte K group of a row -> S digit bytes each, written
-// into the tiled UMMA layout of tile height T ([tile][kchunk][S][2 K halves][T/8][8 rows][16 B]).
-__device__ __forceinline__ int find_slice(const OzSlice* sl, int count, int64_t v, bool by_rows) {
-  int i = 0;
-  while (i + 1 < count && (by_rows ? sl[i + 1].row0 : sl[i + 1].q0) <= v) ++i;
-  return i;
-}
+// Batched over operands (OzSlice table): one CTA per padded row computes the row exponent e
+// (max|x| < 2^e) and writes the row's S digit bytes per 16-byte K group into the tiled UMMA layout.
 
-__global__ void k_ozaki_exp(const OzSlice* __restrict__ sl, int count) {
-  __shared__ double red[8];
-  const OzSlice o = sl[find_slice(sl, count, blockIdx.x, true)];
-  const int r = (int)(blockIdx.x - o.row0);
-  const double* src = o.src + (size_t)r * o.ld;
-  double mx = 0.0;
-  for (int k = threadIdx.x; k < o.kvalid; k += blockDim.x) mx = fmax(mx, fabs(src[k]));
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, off));
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) mx = fmax(mx, red[w]);
-    int e = 0;
-    if (mx > 0.0) frexp(mx, &e);
-    o.exps[r] = e;
-  }
-}
-
-__global__ void k_ozaki_digits(const OzSlice* __restrict__ sl, int count) {
-  const int64_t gq = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int si = find_slice(sl, count, gq, false);
-  const OzSlice o = sl[si];
-  const int64_t q = gq - o.q0;
-  const int groups = o.kchunks * (OZ_KC / 16);
-  const int rows_p = (o.rows + o.T - 1) / o.T * o.T;
-  if (q >= (int64_t)rows_p * groups) return;
-  const int r = (int)(q / groups), gk = (int)(q - (int64_t)r * groups);
-  const bool valid = r < o.rows;
-  const int e = valid ? o.exps[r] : 0;
+// S balanced base-256 digits of one 16-byte K group of row r, written into the tiled UMMA layout
+// of tile height T ([tile][kchunk][S][2 K halves][T/8][8 rows][16 B]; B slices stacked along N)
+__device__ __forceinline__ void ozaki_write_digits(const OzSlice& o, int r, int gk, int e, bool valid) {
   uint32_t w[OZ_S][4];
 #pragma unroll
   for (int p = 0; p < OZ_S; ++p) w[p][0] = w[p][1] = w[p][2] = w[p][3] = 0u;
@@ -258,7 +225,6 @@ __global__ void k_ozaki_digits(const OzSlice* __restrict__ sl, int count) {
       w[p][j >> 2] |= (uint32_t)(uint8_t)(int8_t)d << (8 * (j & 3));
     }
   }
-  // per-slice blocks [S][K half][T rows] (A) or slices stacked along N [K half][S][T rows] (B, stacked)
   const int rt = r / o.T, rr = r % o.T, kc = gk / 2, kh = gk % 2;
   const size_t slice_stride = o.stacked ? (size_t)o.T * 16 : (size_t)o.T * OZ_KC;
   const size_t half_stride = o.stacked ? (size_t)OZ_S * o.T * 16 : (size_t)o.T * 16;
@@ -269,23 +235,55 @@ __global__ void k_ozaki_digits(const OzSlice* __restrict__ sl, int count) {
     *reinterpret_cast<uint4*>(base + p * slice_stride) = make_uint4(w[p][0], w[p][1], w[p][2], w[p][3]);
 }
 
+// One CTA per (padded) row: the row's exponent (max |x|), then its digits -- one launch, the row
+// re-read from L1/L2.  Padding rows of the last tile get zero digits.
+__global__ void __launch_bounds__(256) k_ozaki_slice_rows(const OzSlice* __restrict__ sl, int count) {
+  __shared__ double red[8];
+  __shared__ int e_sh;
+  int si = 0;
+  while (si + 1 < count && sl[si + 1].prow0 <= (int64_t)blockIdx.x) ++si;
+  const OzSlice o = sl[si];
+  const int r = (int)(blockIdx.x - o.prow0);
+  const bool valid = r < o.rows;
+  double mx = 0.0;
+  if (valid) {
+    const double* src = o.src + (size_t)r * o.ld;
+    for (int k = threadIdx.x; k < o.kvalid; k += blockDim.x) mx = fmax(mx, fabs(src[k]));
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) mx = fmax(mx, red[w]);
+    int e = 0;
+    if (mx > 0.0) frexp(mx, &e);
+    if (valid) o.exps[r] = e;
+    e_sh = e;
+  }
+  __syncthreads();
+  const int e = e_sh, groups = o.kchunks * (OZ_KC / 16);
+  for (int gk = threadIdx.x; gk < groups; gk += blockDim.x) ozaki_write_digits(o, r, gk, e, valid);
+}
+
 void ozaki_plan_slices(OzSlice* s, int count, int64_t* rows, int64_t* threads) {
-  int64_t r = 0, q = 0;
+  int64_t r = 0, q = 0, pr = 0;
   for (int i = 0; i < count; ++i) {
     s[i].row0 = r;
     s[i].q0 = q;
+    s[i].prow0 = pr;
+    const int64_t padded = (s[i].rows + s[i].T - 1) / s[i].T * s[i].T;
     r += s[i].rows;
-    q += (int64_t)((s[i].rows + s[i].T - 1) / s[i].T * s[i].T) * s[i].kchunks * (OZ_KC / 16);
+    q += padded * s[i].kchunks * (OZ_KC / 16);
+    pr += padded;
   }
   *rows = r;
-  *threads = q;
+  *threads = pr;   // the slicing grid: one CTA per padded row
 }
 
-int ozaki_slice(const OzSlice* d_slices, int count, int64_t rows, int64_t threads, cudaStream_t st) {
+int ozaki_slice(const OzSlice* d_slices, int count, int64_t rows, int64_t padded_rows, cudaStream_t st) {
   if (count <= 0 || rows <= 0) return 0;
-  k_ozaki_exp<<<(unsigned)rows, 256, 0, st>>>(d_slices, count);
-  FMP_CHECK_LAUNCH();
-  k_ozaki_digits<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(d_slices, count);
+  k_ozaki_slice_rows<<<(unsigned)padded_rows, 256, 0, st>>>(d_slices, count);
   FMP_CHECK_LAUNCH();
   return 0;
 }

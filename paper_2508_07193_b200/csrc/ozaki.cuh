@@ -23,6 +23,7 @@ struct OzSlice {
   int* exps;
   int rows, ld, kvalid, kchunks, T, stacked;   // stacked = 1: slices stacked along N (B operand)
   int64_t row0, q0;   // prefix offsets of this operand in the batched exponent / digit grids
+  int64_t prow0;      // prefix of padded rows (tile multiples) in the batched slicing grid
 };
 
 int ozaki_setup();
@@ -31,9 +32,9 @@ int ozaki_tile_m();
 int ozaki_width(int n);                       // column-tile width for n columns
 size_t ozaki_a_bytes(int m, int kchunks);
 size_t ozaki_b_bytes(int n, int kchunks);
-// Fill row0/q0 of a batch; returns the totals through rows/threads.
-void ozaki_plan_slices(OzSlice* s, int count, int64_t* rows, int64_t* threads);
-int ozaki_slice(const OzSlice* d_slices, int count, int64_t rows, int64_t threads, cudaStream_t st);
+// Fill row0/q0/prow0 of a batch; returns the total rows and padded rows (the slicing grid).
+void ozaki_plan_slices(OzSlice* s, int count, int64_t* rows, int64_t* padded_rows);
+int ozaki_slice(const OzSlice* d_slices, int count, int64_t rows, int64_t padded_rows, cudaStream_t st);
 int ozaki_launch(const OzShape* shapes, const OzTile* tiles, int n_tiles, int sms, cudaStream_t st);
 
 }  // namespace fmp
