@@ -395,28 +395,37 @@ __global__ void __launch_bounds__(STHREADS, SNSLOT <= 4 ? 3 : 2) k_spmv_bulk(con
 }
 
 // ---------------------------------------------------------------- curls and CN stencils
-template <int KIND>  // 0 forward, 1 backward
-__device__ __forceinline__ void curl_at(const Geo& g, const double* __restrict__ f, int k, int j, int i, double& cx,
-                                        double& cy, double& cz) {
+// A point whose stencil stays inside the block reads with plain loads (Loader<false>); only the
+// block's surface layer goes through fetch() (global zero boundary, neighbour ghosts).
+template <int KIND, bool GEN>  // 0 forward, 1 backward
+__device__ __forceinline__ void curl_at(const Loader<GEN>& L, int k, int j, int i, double& cx, double& cy,
+                                        double& cz) {
+  const double ex = L(0, k, j, i), ey = L(1, k, j, i), ez = L(2, k, j, i);
   if (KIND == 0) {  // D^f u(i) = u(i+1) - u(i), zero beyond the high face (ref:operators.py:94-96)
-    const double ex = fetch(g, f, 0, k, j, i), ey = fetch(g, f, 1, k, j, i), ez = fetch(g, f, 2, k, j, i);
-    cx = (fetch(g, f, 2, k, j + 1, i) - ez) - (fetch(g, f, 1, k + 1, j, i) - ey);
-    cy = (fetch(g, f, 0, k + 1, j, i) - ex) - (fetch(g, f, 2, k, j, i + 1) - ez);
-    cz = (fetch(g, f, 1, k, j, i + 1) - ey) - (fetch(g, f, 0, k, j + 1, i) - ex);
+    cx = (L(2, k, j + 1, i) - ez) - (L(1, k + 1, j, i) - ey);
+    cy = (L(0, k + 1, j, i) - ex) - (L(2, k, j, i + 1) - ez);
+    cz = (L(1, k, j, i + 1) - ey) - (L(0, k, j + 1, i) - ex);
   } else {  // D^b u(i) = u(i) - u(i-1), zero before the low face (ref:operators.py:97-99)
-    const double ex = fetch(g, f, 0, k, j, i), ey = fetch(g, f, 1, k, j, i), ez = fetch(g, f, 2, k, j, i);
-    cx = (ez - fetch(g, f, 2, k, j - 1, i)) - (ey - fetch(g, f, 1, k - 1, j, i));
-    cy = (ex - fetch(g, f, 0, k - 1, j, i)) - (ez - fetch(g, f, 2, k, j, i - 1));
-    cz = (ey - fetch(g, f, 1, k, j, i - 1)) - (ex - fetch(g, f, 0, k, j - 1, i));
+    cx = (ez - L(2, k, j - 1, i)) - (ey - L(1, k - 1, j, i));
+    cy = (ex - L(0, k - 1, j, i)) - (ez - L(2, k, j, i - 1));
+    cz = (ey - L(1, k, j, i - 1)) - (ex - L(0, k, j - 1, i));
   }
 }
+__device__ __forceinline__ bool inner(const Geo& g, int k, int j, int i) {
+  return i >= 1 && j >= 1 && k >= 1 && i + 1 < g.bx && j + 1 < g.by && k + 1 < g.bz;
+}
+// 2-D thread blocks (32 x 8): the j-neighbours a thread reads were just read by its block
+constexpr int CBX = 32, CBY = 8;
 
 template <int KIND>
-__global__ void k_curl(Geo g, const double* __restrict__ f, double* __restrict__ out) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x, j = blockIdx.y, k = blockIdx.z;
-  if (i >= g.bx) return;
+__global__ void __launch_bounds__(CBX* CBY) k_curl(Geo g, const double* __restrict__ f, double* __restrict__ out) {
+  const int i = blockIdx.x * CBX + threadIdx.x, j = blockIdx.y * CBY + threadIdx.y, k = blockIdx.z;
+  if (i >= g.bx || j >= g.by) return;
   double cx, cy, cz;
-  curl_at<KIND>(g, f, k, j, i, cx, cy, cz);
+  if (inner(g, k, j, i))
+    curl_at<KIND>(Loader<false>{g, f}, k, j, i, cx, cy, cz);
+  else
+    curl_at<KIND>(Loader<true>{g, f}, k, j, i, cx, cy, cz);
   const int64_t o = fidx(g, 0, k, j, i), V = (int64_t)g.bx * g.by * g.bz;
   out[o] = cx;
   out[o + V] = cy;
@@ -424,16 +433,19 @@ __global__ void k_curl(Geo g, const double* __restrict__ f, double* __restrict__
 }
 
 // R = E + dt*curl_b(H) - alpha*(C_b C_f E), alpha = dt^2/4  (ref:cn_driver.py:54-59)
-__global__ void k_cn_rhs(Geo gE, Geo gH, double dt, const double* __restrict__ E, const double* __restrict__ H,
-                         double* __restrict__ R) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x, j = blockIdx.y, k = blockIdx.z;
-  if (i >= gE.bx) return;
+__global__ void __launch_bounds__(CBX* CBY) k_cn_rhs(Geo gE, Geo gH, double dt, const double* __restrict__ E,
+                                                    const double* __restrict__ H, double* __restrict__ R) {
+  const int i = blockIdx.x * CBX + threadIdx.x, j = blockIdx.y * CBY + threadIdx.y, k = blockIdx.z;
+  if (i >= gE.bx || j >= gE.by) return;
   const double alpha = dt * dt / 4.0;
-  double hx, hy, hz;
-  curl_at<1>(gH, H, k, j, i, hx, hy, hz);
-  const Loader<true> L{gE, E};
-  double tx, ty, tz, ex, ey, ez;
-  bracket<true>(L, k, j, i, tx, ty, tz, ex, ey, ez);
+  double hx, hy, hz, tx, ty, tz, ex, ey, ez;
+  if (inner(gE, k, j, i)) {
+    curl_at<1>(Loader<false>{gH, H}, k, j, i, hx, hy, hz);
+    bracket<false>(Loader<false>{gE, E}, k, j, i, tx, ty, tz, ex, ey, ez);
+  } else {
+    curl_at<1>(Loader<true>{gH, H}, k, j, i, hx, hy, hz);
+    bracket<true>(Loader<true>{gE, E}, k, j, i, tx, ty, tz, ex, ey, ez);
+  }
   const int gi = gE.gx0 + i, gj = gE.gy0 + j, gk = gE.gz0 + k;
   tx -= ((gj == 0) + (gk == 0)) * ex;  // C_b C_f without Lambda
   ty -= ((gi == 0) + (gk == 0)) * ey;
@@ -445,13 +457,19 @@ __global__ void k_cn_rhs(Geo gE, Geo gH, double dt, const double* __restrict__ E
 }
 
 // H_new = H - (0.5 dt) (curl_f(E_new) + curl_f(E_old))  (ref:cn_driver.py:90-91)
-__global__ void k_cn_h(Geo gN, Geo gO, double hdt, const double* __restrict__ H, const double* __restrict__ En,
-                       const double* __restrict__ Eo, double* __restrict__ Hn) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x, j = blockIdx.y, k = blockIdx.z;
-  if (i >= gN.bx) return;
+__global__ void __launch_bounds__(CBX* CBY) k_cn_h(Geo gN, Geo gO, double hdt, const double* __restrict__ H,
+                                                  const double* __restrict__ En, const double* __restrict__ Eo,
+                                                  double* __restrict__ Hn) {
+  const int i = blockIdx.x * CBX + threadIdx.x, j = blockIdx.y * CBY + threadIdx.y, k = blockIdx.z;
+  if (i >= gN.bx || j >= gN.by) return;
   double ax, ay, az, bx, by, bz;
-  curl_at<0>(gN, En, k, j, i, ax, ay, az);
-  curl_at<0>(gO, Eo, k, j, i, bx, by, bz);
+  if (inner(gN, k, j, i)) {
+    curl_at<0>(Loader<false>{gN, En}, k, j, i, ax, ay, az);
+    curl_at<0>(Loader<false>{gO, Eo}, k, j, i, bx, by, bz);
+  } else {
+    curl_at<0>(Loader<true>{gN, En}, k, j, i, ax, ay, az);
+    curl_at<0>(Loader<true>{gO, Eo}, k, j, i, bx, by, bz);
+  }
   const int64_t o = fidx(gN, 0, k, j, i), V = (int64_t)gN.bx * gN.by * gN.bz;
   Hn[o] = H[o] - hdt * (ax + bx);
   Hn[o + V] = H[o + V] - hdt * (ay + by);
@@ -587,11 +605,11 @@ extern "C" int fmp_stencil_apply(const fmp_block* blk, double alpha, int boundar
 extern "C" int fmp_curl(const fmp_block* blk, int kind, const double* x, double* out, void* stream) {
   if (int e = check_block(blk)) return e;
   const Geo g = make_geo(blk);
-  dim3 grid((g.bx + 127) / 128, g.by, g.bz);
+  const dim3 grid((g.bx + CBX - 1) / CBX, (g.by + CBY - 1) / CBY, g.bz), block(CBX, CBY);
   if (kind == 0)
-    k_curl<0><<<grid, 128, 0, as_stream(stream)>>>(g, x, out);
+    k_curl<0><<<grid, block, 0, as_stream(stream)>>>(g, x, out);
   else
-    k_curl<1><<<grid, 128, 0, as_stream(stream)>>>(g, x, out);
+    k_curl<1><<<grid, block, 0, as_stream(stream)>>>(g, x, out);
   FMP_CHECK_LAUNCH();
   return 0;
 }
@@ -600,8 +618,8 @@ extern "C" int fmp_cn_rhs(const fmp_block* blkE, const fmp_block* blkH, double d
                           double* R, void* stream) {
   if (int e = check_block(blkE)) return e;
   const Geo gE = make_geo(blkE), gH = make_geo(blkH);
-  dim3 grid((gE.bx + 127) / 128, gE.by, gE.bz);
-  k_cn_rhs<<<grid, 128, 0, as_stream(stream)>>>(gE, gH, dt, E, H, R);
+  const dim3 grid((gE.bx + CBX - 1) / CBX, (gE.by + CBY - 1) / CBY, gE.bz), block(CBX, CBY);
+  k_cn_rhs<<<grid, block, 0, as_stream(stream)>>>(gE, gH, dt, E, H, R);
   FMP_CHECK_LAUNCH();
   return 0;
 }
@@ -610,8 +628,8 @@ extern "C" int fmp_cn_h_update(const fmp_block* blkNew, const fmp_block* blkOld,
                                const double* E_new, const double* E_old, double* H_new, void* stream) {
   if (int e = check_block(blkNew)) return e;
   const Geo gN = make_geo(blkNew), gO = make_geo(blkOld);
-  dim3 grid((gN.bx + 127) / 128, gN.by, gN.bz);
-  k_cn_h<<<grid, 128, 0, as_stream(stream)>>>(gN, gO, 0.5 * dt, H, E_new, E_old, H_new);
+  const dim3 grid((gN.bx + CBX - 1) / CBX, (gN.by + CBY - 1) / CBY, gN.bz), block(CBX, CBY);
+  k_cn_h<<<grid, block, 0, as_stream(stream)>>>(gN, gO, 0.5 * dt, H, E_new, E_old, H_new);
   FMP_CHECK_LAUNCH();
   return 0;
 }
