@@ -13,6 +13,7 @@
 #include "common.cuh"
 #include "tma.cuh"
 #include <algorithm>
+#include <atomic>
 
 namespace fmp {
 
@@ -546,12 +547,22 @@ extern "C" int fmp_stencil_apply(const fmp_block* blk, double alpha, int boundar
     a.tiles_y = (g.by + SY - 1) / SY;
     a.ghosts = 0;
     for (int q = 0; q < 6; ++q) a.ghosts |= g.ghost[q] != nullptr;
-    static unsigned long long* counter = nullptr;   // [fetch, done] of the unit scheduler, zero at rest
-    if (!counter) {
-      FMP_CHECK_CUDA(cudaMalloc(&counter, 2 * sizeof(unsigned long long)));
-      FMP_CHECK_CUDA(cudaMemset(counter, 0, 2 * sizeof(unsigned long long)));
+    // [fetch, done] counter pairs of the unit scheduler, zero at rest (each launch re-arms its
+    // own pair).  A ring of pairs, so launches in flight on different streams or devices of this
+    // process never share one (per device: the ring is allocated on the current device).
+    constexpr int kCounterRing = 64;
+    static unsigned long long* counters[64] = {};
+    static std::atomic<unsigned> next_pair{0};
+    int dev = 0;
+    FMP_CHECK_CUDA(cudaGetDevice(&dev));
+    FMP_REQUIRE(dev < 64, "device index %d out of range", dev);
+    if (!counters[dev]) {
+      unsigned long long* c = nullptr;
+      FMP_CHECK_CUDA(cudaMalloc(&c, 2 * kCounterRing * sizeof(unsigned long long)));
+      FMP_CHECK_CUDA(cudaMemset(c, 0, 2 * kCounterRing * sizeof(unsigned long long)));
+      counters[dev] = c;
     }
-    a.counter = counter;
+    a.counter = counters[dev] + 2 * (next_pair.fetch_add(1, std::memory_order_relaxed) % kCounterRing);
     const int64_t ntiles = (int64_t)a.tiles_x * a.tiles_y;
     const int64_t resident = (int64_t)kNumSM * resident_per_sm;
     spmv_chunking(ntiles, g.bz, resident, &a.L, &a.nzc);
