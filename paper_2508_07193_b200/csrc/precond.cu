@@ -1220,8 +1220,8 @@ inline size_t face_smem_bytes(int slot) {
 // the FR shuffle reductions interleaved (independent chains, no early exit).
 template <int FR, int FA, int S>
 __device__ __forceinline__ void face_plane(const double* pl, int z, int ex, int ey, bool zn, bool xn, double wz,
-                                           const double* Wy, const double (&wx)[FA], double* sA, double* sB,
-                                           double (&yp)[FA], int warp, int lane) {
+                                           const double* Wy, const double (&wx)[FA], double (&za)[FR][FA],
+                                           double* sB, double (&yp)[FA], int warp, int lane) {
   double val[FR][FA];
 #pragma unroll
   for (int r = 0; r < FR; ++r)
@@ -1230,14 +1230,11 @@ __device__ __forceinline__ void face_plane(const double* pl, int z, int ex, int 
       const int b = warp + FACE_WARPS * r, a = lane + 32 * h;
       val[r][h] = (b < ey && a < ex) ? pl[b * ex + a] : 0.0;
     }
-  if (zn) {
+  if (zn) {   // z-normal: this thread's (b, a) accumulators live in registers
 #pragma unroll
     for (int r = 0; r < FR; ++r)
 #pragma unroll
-      for (int h = 0; h < FA; ++h) {
-        const int b = warp + FACE_WARPS * r, a = lane + 32 * h;
-        if (b < ey && a < ex) sA[b * S + a] += wz * val[r][h];
-      }
+      for (int h = 0; h < FA; ++h) za[r][h] += wz * val[r][h];
   }
 #pragma unroll
   for (int h = 0; h < FA; ++h) yp[h] = 0.0;
@@ -1318,9 +1315,13 @@ __global__ void __launch_bounds__(FACE_THREADS, NT <= 5 ? 3 : 1) k_faces(FaceArg
     // ---------------- consumers
     const double* Wz = sWt + 2 * N;
     const double* Wy = sWt + N;
-    double wx[FA];
+    double wx[FA], za[FR][FA];
 #pragma unroll
     for (int h = 0; h < FA; ++h) wx[h] = lane + 32 * h < N ? sWt[lane + 32 * h] : 0.0;
+#pragma unroll
+    for (int r = 0; r < FR; ++r)
+#pragma unroll
+      for (int h = 0; h < FA; ++h) za[r][h] = 0.0;
     for (int z0 = 0; z0 < ez; z0 += FZ) {
       const int nzc = min(FZ, ez - z0);
       for (int zz = 0; zz < nzc; ++zz) {
@@ -1328,7 +1329,7 @@ __global__ void __launch_bounds__(FACE_THREADS, NT <= 5 ? 3 : 1) k_faces(FaceArg
         mbar_wait(&full[slot], (uint32_t)((z / NS) & 1));
         const double* pl = ring + slot * SLOT;
         double yp[FA];
-        face_plane<FR, FA, S>(pl, z, ex, ey, zn, xn, Wz[z], Wy, wx, sA, sB, yp, warp, lane);
+        face_plane<FR, FA, S>(pl, z, ex, ey, zn, xn, Wz[z], Wy, wx, za, sB, yp, warp, lane);
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[slot]);
         if (yn) {
@@ -1347,6 +1348,15 @@ __global__ void __launch_bounds__(FACE_THREADS, NT <= 5 ? 3 : 1) k_faces(FaceArg
         }
         asm volatile("bar.sync 1, %0;\n" ::"n"(FACE_WARPS * 32) : "memory");
       }
+    }
+    if (zn) {   // z-normal projection [b][a] from the register accumulators
+#pragma unroll
+      for (int r = 0; r < FR; ++r)
+#pragma unroll
+        for (int h = 0; h < FA; ++h) {
+          const int b = warp + FACE_WARPS * r, a = lane + 32 * h;
+          if (b < ey && a < ex) sA[b * S + a] = za[r][h];
+        }
     }
   }
   __syncthreads();
