@@ -141,3 +141,27 @@ def test_own_gemm_matches_cublas(monkeypatch):
     monkeypatch.setenv("FMP_GEMM", "cublas")
     z_blas = RasPreconditioner(part, 0.25, tr).apply(r)
     assert rel(z_own.cpu().numpy(), z_blas.cpu().numpy()) <= 1e-14
+
+
+def test_stage_timing_api():
+    """fmp_precond_profile / fmp_precond_stage_ms: eight non-negative stage times whose sum
+    matches the whole apply measured with events on the same stream (within launch gaps)."""
+    from paper_2508_07193_b200 import Box, RasPreconditioner, make_partition, make_transport
+    part = make_partition(Box(64, 64, 64), (2, 2, 2), 1)
+    prec = RasPreconditioner(part, 0.25, make_transport("cuda"))
+    r = torch.rand(3, 64, 64, 64, dtype=torch.float64, device="cuda")
+    z = torch.empty_like(r)
+    prec.apply_into(r, z)
+    want = z.clone()
+    prec.plan.profile(True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    prec.apply_into(r, z)
+    e1.record()
+    st = prec.plan.stage_ms()
+    prec.plan.profile(False)
+    torch.cuda.synchronize()
+    assert list(st) == list(prec.plan.STAGES)
+    assert all(v >= 0.0 for v in st.values())
+    assert sum(st.values()) <= e0.elapsed_time(e1) * 1.05 + 0.05
+    assert torch.equal(z, want)   # timing does not change the result
