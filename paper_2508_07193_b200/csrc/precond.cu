@@ -1253,14 +1253,41 @@ __device__ __forceinline__ void face_plane(const double* pl, int z, int ex, int 
 #pragma unroll
       for (int h = 0; h < FA; ++h) xs[r] += wx[h] * val[r][h];
     }
+    if (FR <= 8) {
+      // transpose-reduce of up to 8 row sums over the 32 lanes: each exchange halves the values a
+      // lane carries (4 + 2 + 1 + 1 + 1 shuffles instead of 5 per row)
+      double v[8];
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1)
+      for (int r = 0; r < 8; ++r) v[r] = r < FR ? xs[r] : 0.0;
+      const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
 #pragma unroll
-      for (int r = 0; r < FR; ++r) xs[r] += __shfl_xor_sync(0xffffffffu, xs[r], o);
+      for (int i = 0; i < 4; ++i) {
+        const double send = b4 ? v[i] : v[i + 4], keep = b4 ? v[i + 4] : v[i];
+        v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+      }
 #pragma unroll
-    for (int r = 0; r < FR; ++r) {
-      const int b = warp + FACE_WARPS * r;
-      if (lane == r && b < ey) sB[z * S + b] = xs[r];
+      for (int i = 0; i < 2; ++i) {
+        const double send = b3 ? v[i] : v[i + 2], keep = b3 ? v[i + 2] : v[i];
+        v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+      }
+      {
+        const double send = b2 ? v[0] : v[1], keep = b2 ? v[1] : v[0];
+        v[0] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+      }
+      v[0] += __shfl_xor_sync(0xffffffffu, v[0], 2);
+      v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
+      const int r = (b4 ? 4 : 0) + (b3 ? 2 : 0) + (b2 ? 1 : 0), b = warp + FACE_WARPS * r;
+      if ((lane & 3) == 0 && r < FR && b < ey) sB[z * S + b] = v[0];
+    } else {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int r = 0; r < FR; ++r) xs[r] += __shfl_xor_sync(0xffffffffu, xs[r], o);
+#pragma unroll
+      for (int r = 0; r < FR; ++r) {
+        const int b = warp + FACE_WARPS * r;
+        if (lane == r && b < ey) sB[z * S + b] = xs[r];
+      }
     }
   }
 }
