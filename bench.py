@@ -318,9 +318,23 @@ def run_ours(args):
         a1.record()
         torch.cuda.synchronize()
         t_e2e = max_over_ranks(a0.elapsed_time(a1) * 1e-3)
+        # this box's host link (one pinned field each way), to read the e2e number against
+        c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        dbuf = torch.empty_like(stepper.E)
+        c0.record()
+        dbuf.copy_(Eh, non_blocking=True)
+        c1.record()
+        torch.cuda.synchronize()
+        h2d_gbs = Eh.numel() * 8 / c0.elapsed_time(c1) / 1e6
+        c0.record()
+        Eo.copy_(dbuf, non_blocking=True)
+        c1.record()
+        torch.cuda.synchronize()
+        d2h_gbs = Eh.numel() * 8 / c0.elapsed_time(c1) / 1e6
         e2e = {"value": round(dof * ke / t_e2e / 1e6, 3), "unit": "MDoF/s",
                "h2d_bytes_per_step": 2 * Eh.numel() * 8, "d2h_bytes_per_step": 2 * Eo.numel() * 8,
-               "steps": ke, "ms_per_step": round(t_e2e / ke * 1e3, 3)}
+               "steps": ke, "ms_per_step": round(t_e2e / ke * 1e3, 3),
+               "host_link_gbs": {"h2d": round(h2d_gbs, 1), "d2h": round(d2h_gbs, 1)}}
 
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": "MDoF/s", "n_gpus": world, "steps": args.steps,
