@@ -20,7 +20,9 @@
 // (shape, row tile, column tile); warp 4 streams operands, warp 5 issues the S(S+1)/2 MMAs
 // per K chunk into S TMEM accumulators (one per level), warps 0-3 drain TMEM, combine the
 // levels in FP64 and store Z.
+#include <algorithm>
 #include <cstdint>
+#include <vector>
 #include "common.cuh"
 #include "ozaki.cuh"
 #include "tma.cuh"
@@ -75,7 +77,7 @@ __device__ __forceinline__ void issue_chunk(uint64_t da0, uint64_t db0, uint32_t
 }
 
 __global__ void __launch_bounds__(OZ_THREADS, 1)
-    k_ozaki(const OzShape* __restrict__ shapes, const OzTile* __restrict__ tiles, int n_tiles) {
+    k_ozaki(const OzShape* __restrict__ shapes, const OzTile* __restrict__ tiles, const int* __restrict__ offs) {
   extern __shared__ __align__(1024) uint8_t osm[];
   __shared__ __align__(8) uint64_t full_bar[OZ_STAGES], empty_bar[OZ_STAGES], tfull_bar, tempty_bar;
   __shared__ uint32_t tmem_base;
@@ -103,7 +105,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
     // ---------------- producer: two bulk copies per stage
     if (lane == 0) {
       int it = 0;
-      for (int ti = blockIdx.x; ti < n_tiles; ti += gridDim.x) {
+      for (int ti = offs[blockIdx.x]; ti < offs[blockIdx.x + 1]; ++ti) {
         const OzTile tl = tiles[ti];
         const OzShape sh = shapes[tl.shape];
         const int8_t* a = sh.A + (size_t)tl.mt * sh.kchunks * OZ_S * OZ_ABLK;
@@ -126,7 +128,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
     // ONE MMA of N = (S+1-p) w against B slices 1..S+1-p feeds levels p+1..S+1 at once (split at
     // N = 256): S+3 MMAs per K chunk instead of S(S+1)/2, each A block read from smem once per p.
     int it = 0, tcount = 0;
-    for (int ti = blockIdx.x; ti < n_tiles; ti += gridDim.x, ++tcount) {
+    for (int ti = offs[blockIdx.x]; ti < offs[blockIdx.x + 1]; ++ti, ++tcount) {
       const OzShape sh = shapes[tiles[ti].shape];
       const int w = sh.w;
       const uint32_t lbo_b = (uint32_t)OZ_S * w * 16;
@@ -159,7 +161,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
   } else {
     // ---------------- epilogue warps 0-3: lane quadrant = warp, one row per thread
     int tcount = 0;
-    for (int ti = blockIdx.x; ti < n_tiles; ti += gridDim.x, ++tcount) {
+    for (int ti = offs[blockIdx.x]; ti < offs[blockIdx.x + 1]; ++ti, ++tcount) {
       const OzTile tl = tiles[ti];
       const OzShape sh = shapes[tl.shape];
       mbar_wait(&tfull_bar, tcount & 1);
@@ -309,12 +311,49 @@ int ozaki_setup() {
   return 0;
 }
 
-int ozaki_launch(const OzShape* shapes, const OzTile* tiles, int n_tiles, int sms, cudaStream_t st) {
-  if (n_tiles <= 0) return 0;
-  const int grid = n_tiles < sms ? n_tiles : sms;
-  k_ozaki<<<grid, OZ_THREADS, OZ_STAGES * OZ_STAGE, st>>>(shapes, tiles, n_tiles);
+int ozaki_launch(const OzShape* shapes, const OzTile* tiles, const int* offs, int grid, cudaStream_t st) {
+  if (grid <= 0) return 0;
+  k_ozaki<<<grid, OZ_THREADS, OZ_STAGES * OZ_STAGE, st>>>(shapes, tiles, offs);
   FMP_CHECK_LAUNCH();
   return 0;
+}
+
+// Tensor-pipe cycles of one K chunk of a column tile of width w: per A slice p, one MMA per
+// <= 256 columns of the stacked B slices, each >= ~46 cycles (tools/umma_rate.cu)
+static double chunk_cycles(int w) {
+  double c = 0.0;
+  for (int p = 1; p <= OZ_S; ++p)
+    for (int n = (OZ_S + 1 - p) * w; n > 0; n -= 256) c += std::max(46.0, std::min(n, 256) / 2.0);
+  return c;
+}
+
+void ozaki_schedule(const std::vector<OzShape>& shapes, std::vector<OzTile>& tiles, int grid, std::vector<int>& offs) {
+  // longest-processing-time-first assignment of tiles to the persistent CTAs; equal-cost tiles
+  // keep their (shape, row tile, column tile) order, so CTAs working at the same time still
+  // share C^-1 row tiles in L2.  Each CTA then walks its list in the original order.
+  std::vector<double> cost(tiles.size());
+  for (size_t i = 0; i < tiles.size(); ++i) {
+    const OzShape& sh = shapes[tiles[i].shape];
+    cost[i] = sh.kchunks * chunk_cycles(sh.w);
+  }
+  std::vector<int> order(tiles.size());
+  for (size_t i = 0; i < order.size(); ++i) order[i] = (int)i;
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return cost[a] > cost[b]; });
+  std::vector<double> load(grid, 0.0);
+  std::vector<std::vector<int>> lists(grid);
+  for (int i : order) {
+    const int c = (int)(std::min_element(load.begin(), load.end()) - load.begin());
+    load[c] += cost[i];
+    lists[c].push_back(i);
+  }
+  std::vector<OzTile> out;
+  offs.assign(1, 0);
+  for (auto& l : lists) {
+    std::sort(l.begin(), l.end());
+    for (int i : l) out.push_back(tiles[i]);
+    offs.push_back((int)out.size());
+  }
+  tiles.swap(out);
 }
 
 }  // namespace fmp

@@ -1,6 +1,7 @@
 // Host interface of the Ozaki INT8 tensor-core Woodbury GEMM (ozaki.cu), used by precond.cu.
 #pragma once
 #include <cstdint>
+#include <vector>
 #include <cuda_runtime.h>
 
 namespace fmp {
@@ -35,6 +36,8 @@ size_t ozaki_b_bytes(int n, int kchunks);
 // Fill row0/q0/prow0 of a batch; returns the total rows and padded rows (the slicing grid).
 void ozaki_plan_slices(OzSlice* s, int count, int64_t* rows, int64_t* padded_rows);
 int ozaki_slice(const OzSlice* d_slices, int count, int64_t rows, int64_t padded_rows, cudaStream_t st);
-int ozaki_launch(const OzShape* shapes, const OzTile* tiles, int n_tiles, int sms, cudaStream_t st);
+// tiles reordered into per-CTA lists (CTA b runs tiles [offs[b], offs[b+1])), balanced by cost
+void ozaki_schedule(const std::vector<OzShape>& shapes, std::vector<OzTile>& tiles, int grid, std::vector<int>& offs);
+int ozaki_launch(const OzShape* shapes, const OzTile* tiles, const int* offs, int grid, cudaStream_t st);
 
 }  // namespace fmp

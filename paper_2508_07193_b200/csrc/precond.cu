@@ -1492,6 +1492,8 @@ struct fmp_precond {
   std::vector<int*> oz_ea, oz_eb;
   OzShape* d_ozshapes = nullptr;
   OzTile* d_oztiles = nullptr;
+  int* d_ozoffs = nullptr;                // per-CTA tile list offsets (ozaki_schedule)
+  int oz_grid = 0;
   int n_oztiles = 0;
   OzSlice* d_ozslices = nullptr;          // per-apply slicing of Y, all shapes in two launches
   int n_ozslices = 0;
@@ -1547,6 +1549,7 @@ static void free_plan(fmp_precond* p) {
   for (auto* q : p->oz_eb) cudaFree(q);
   cudaFree(p->d_ozshapes);
   cudaFree(p->d_oztiles);
+  cudaFree(p->d_ozoffs);
   cudaFree(p->d_ozslices);
   for (int c = 0; c < 3; ++c) cudaFree(p->d_gtiles[c]);
   delete p;
@@ -1727,7 +1730,11 @@ extern "C" int fmp_precond_create(const fmp_precond_desc* desc, fmp_precond** ou
     ozaki_plan_slices(sa.data(), (int)sa.size(), &ra, &qa);
     ozaki_plan_slices(sb.data(), (int)sb.size(), &p->oz_rows, &p->oz_threads);
     OzSlice* d_sa = nullptr;
-    if (upload(sa, &d_sa) || upload(sb, &p->d_ozslices) || upload(os, &p->d_ozshapes) || upload(ot, &p->d_oztiles)) {
+    p->oz_grid = std::min<int>((int)ot.size(), p->sms);
+    std::vector<int> offs;
+    ozaki_schedule(os, ot, p->oz_grid, offs);
+    if (upload(sa, &d_sa) || upload(sb, &p->d_ozslices) || upload(os, &p->d_ozshapes) || upload(ot, &p->d_oztiles) ||
+        upload(offs, &p->d_ozoffs)) {
       cudaFree(d_sa);
       free_plan(p);
       return -1;
@@ -1957,7 +1964,7 @@ extern "C" int fmp_precond_apply(fmp_precond* p, const fmp_block* blk, int mode,
       FMP_REQUIRE(p->d_ozshapes != nullptr, "Ozaki GEMM requested but the plan has no C^-1");
       if (int e = ozaki_slice(p->d_ozslices, p->n_ozslices, p->oz_rows, p->oz_threads, st)) return e;
       mark(4);
-      if (int e = ozaki_launch(p->d_ozshapes, p->d_oztiles, p->n_oztiles, p->sms, st)) return e;
+      if (int e = ozaki_launch(p->d_ozshapes, p->d_oztiles, p->d_ozoffs, p->oz_grid, st)) return e;
     } else {
       for (int c = 0; c < 3; ++c)
         if (int e = gemm_launch(c, p->d_gshapes, p->d_gtiles[c], p->n_gtiles[c], p->sms, st)) return e;
