@@ -165,3 +165,18 @@ def test_stage_timing_api():
     assert all(v >= 0.0 for v in st.values())
     assert sum(st.values()) <= e0.elapsed_time(e1) * 1.05 + 0.05
     assert torch.equal(z, want)   # timing does not change the result
+
+
+@pytest.mark.parametrize("n", [49, 66])
+def test_single_subdomain_preconditioner_is_the_exact_inverse(n):
+    """With one subdomain covering the box, RAS is the exact solve: M^-1 (A x) == x.  Covers the
+    large-extent paths: general (CTA) transform kernels, the 9-tile face kernels (extent > 40), the
+    Ozaki GEMM at m = 14,259 (n = 49) and the cuBLAS fallback past its K bound (n = 66, m = 25,938)."""
+    from paper_2508_07193_b200 import Box, DistributedOperator, RasPreconditioner, make_partition, make_transport
+    part = make_partition(Box(n, n, n), (1, 1, 1), 1)
+    tr = make_transport("cuda")
+    op = DistributedOperator(part, 0.25, tr)
+    prec = RasPreconditioner(part, 0.25, tr)
+    x = torch.from_numpy(np.random.default_rng(11).uniform(-1, 1, 3 * n ** 3)).cuda().view(3, n, n, n)
+    z = prec.apply(op.apply(x))
+    assert rel(z.cpu().numpy(), x.cpu().numpy()) <= 1e-11
