@@ -1783,9 +1783,11 @@ extern "C" int fmp_precond_create(const fmp_precond_desc* desc, fmp_precond** ou
   cudaFuncSetAttribute(k_column_fast_db<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, col_db_smem(CW_WARPS_INV));
   {
     const int slot = face_slot((p->max_p + 3) & ~3);
+    cudaFuncSetAttribute(k_faces<3, 1, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)face_smem_bytes<3>(slot));
     cudaFuncSetAttribute(k_faces<5, 2, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)face_smem_bytes<5>(slot));
     cudaFuncSetAttribute(k_faces<9, 3, 9>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)face_smem_bytes<9>(slot));
   }
+  cudaFuncSetAttribute(k_corr<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * FaceMat<3>::WORDS * 8);
   cudaFuncSetAttribute(k_corr<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * FaceMat<5>::WORDS * 8);
   cudaFuncSetAttribute(k_corr<9>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * FaceMat<9>::WORDS * 8);
   FMP_CHECK_CUDA(cudaGetLastError());
@@ -1930,7 +1932,9 @@ extern "C" int fmp_precond_apply(fmp_precond* p, const fmp_block* blk, int mode,
   if (mode != FMP_SOLVE_EXACT) {
     const dim3 fg(3, (unsigned)p->d.n_sub);
     const int slot = face_slot(fa.max_ps);
-    if (pm <= 40)
+    if (pm <= 24)   // 16^3-class subdomains: 3 DMMA tiles per padded extent
+      k_faces<3, 1, 3><<<fg, FACE_THREADS, face_smem_bytes<3>(slot), st>>>(fa);
+    else if (pm <= 40)
       k_faces<5, 2, 5><<<fg, FACE_THREADS, face_smem_bytes<5>(slot), st>>>(fa);
     else
       k_faces<9, 3, 9><<<fg, FACE_THREADS, face_smem_bytes<9>(slot), st>>>(fa);
@@ -1970,7 +1974,9 @@ extern "C" int fmp_precond_apply(fmp_precond* p, const fmp_block* blk, int mode,
         if (int e = gemm_launch(c, p->d_gshapes, p->d_gtiles[c], p->n_gtiles[c], p->sms, st)) return e;
     }
     mark(5);
-    if (pm <= 40)
+    if (pm <= 24)
+      k_corr<3><<<dim3(3, (unsigned)p->d.n_sub), FACE_THREADS, 4 * FaceMat<3>::WORDS * sizeof(double), st>>>(fa);
+    else if (pm <= 40)
       k_corr<5><<<dim3(3, (unsigned)p->d.n_sub), FACE_THREADS, 4 * FaceMat<5>::WORDS * sizeof(double), st>>>(fa);
     else
       k_corr<9><<<dim3(3, (unsigned)p->d.n_sub), FACE_THREADS, 4 * FaceMat<9>::WORDS * sizeof(double), st>>>(fa);
