@@ -639,7 +639,7 @@ __device__ __forceinline__ void plane_step2(const double* T, const double* Fy, c
   }
 }
 
-template <bool INV>
+template <bool INV, int NT = 5>   // NT: 8-row DMMA tiles per padded extent (3: extents <= 24, 5: <= 40)
 __global__ void __launch_bounds__(PW_WARPS * 32, 1) k_plane_fast(const __grid_constant__ CUtensorMap tm,
                                                                   FastPlaneArgs A) {
   extern __shared__ __align__(128) double smem[];
@@ -750,7 +750,20 @@ __global__ void __launch_bounds__(PW_WARPS * 32, 1) k_plane_fast(const __grid_co
     // ---- step 1: T[j][a] = sum_i X[j][i] Fx[a][i]   (INV: T[b][i] = sum_a X[b][a] Fx[a][i])
     // INV (prolongation): only the owned columns / rows of the plane are formed (4 tiles
     // when the owned tile is <= 32 wide, the common case)
-    if (INV && d.wx <= 32 && d.wy <= 32) {
+    if (NT == 3) {   // extents <= 24 (16^3-class subdomains): 3 tiles, 2 for an owned tile <= 16
+      if (INV && d.wx <= 16 && d.wy <= 16) {
+        plane_step1<INV, 2, 2>(X, T, Fx, 0, k41, g, t, d.ox);
+        plane_step1<INV, 1, 2>(X, T, Fx, 2, k41, g, t, d.ox);
+        __syncwarp();
+        plane_step2<INV, 2, 2>(T, Fy, A, d, c, w.z, 0, k42, g, t);
+      } else {
+        plane_step1<INV, 2, 3>(X, T, Fx, 0, k41, g, t, INV ? d.ox : 0);
+        plane_step1<INV, 1, 3>(X, T, Fx, 2, k41, g, t, INV ? d.ox : 0);
+        __syncwarp();
+        plane_step2<INV, 2, 3>(T, Fy, A, d, c, w.z, 0, k42, g, t);
+        plane_step2<INV, 1, 3>(T, Fy, A, d, c, w.z, 2, k42, g, t);
+      }
+    } else if (INV && d.wx <= 32 && d.wy <= 32) {
       plane_step1<INV, 2, 4>(X, T, Fx, 0, k41, g, t, d.ox);
       plane_step1<INV, 2, 4>(X, T, Fx, 2, k41, g, t, d.ox);
       plane_step1<INV, 1, 4>(X, T, Fx, 4, k41, g, t, d.ox);
@@ -950,7 +963,7 @@ __device__ __forceinline__ void col_mma(double (&acc)[3][5][2], const double* xb
 // warp share their subdomain record, reloaded only when it changes), so the cp.async of the
 // next tile is issued with no dependent global round trip in front of it; the correction
 // planes of K3 are read with all loads of a lane hoisted ahead of the arithmetic.
-template <bool INV, int NW = INV ? CW_WARPS_INV : CW_WARPS_FWD>
+template <bool INV, int NW = INV ? CW_WARPS_INV : CW_WARPS_FWD, int NT = 5>   // NT: z tiles (3 or 5)
 __global__ void __launch_bounds__(NW * 32, 1) k_column_fast_db(FastColArgs A) {
   extern __shared__ __align__(16) double smem[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
@@ -1058,11 +1071,16 @@ __global__ void __launch_bounds__(NW * 32, 1) k_column_fast_db(FastColArgs A) {
       for (int m = 0; m < 5; ++m) acc[cc][m][0] = acc[cc][m][1] = 0.0;
     // INV (prolongation): only the owned z rows [oz, oz + wz) are formed (4 row tiles when
     // wz <= 32; the tile count is a template constant of col_mma)
-    const int mt = INV && d.wz <= 32 ? 4 : 5;
+    const int mt = NT == 3 ? (INV && d.wz <= 16 ? 2 : 3) : (INV && d.wz <= 32 ? 4 : 5);
     const double* xb = X + t * CXS + g;
     const double* fv = INV ? Fv + t * FSM + g + d.oz : Fv + g * FSM + t;
     const double* fu = INV ? Fu + t * FSM + g + d.oz : Fu + g * FSM + t;
-    if (mt == 4)
+    if (NT == 3) {
+      if (mt == 2)
+        col_mma<INV, 2>(acc, xb, fv, fu, k4);
+      else
+        col_mma<INV, 3>(acc, xb, fv, fu, k4);
+    } else if (mt == 4)
       col_mma<INV, 4>(acc, xb, fv, fu, k4);
     else
       col_mma<INV, 5>(acc, xb, fv, fu, k4);
@@ -1777,10 +1795,16 @@ extern "C" int fmp_precond_create(const fmp_precond_desc* desc, fmp_precond** ou
   column_attr<6>(); column_attr<7>(); column_attr<8>(); column_attr<9>();
   cudaFuncSetAttribute(k_plane_fast<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kPlaneFastSmem);
   cudaFuncSetAttribute(k_plane_fast<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kPlaneFastSmem);
+  cudaFuncSetAttribute(k_plane_fast<false, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, kPlaneFastSmem);
+  cudaFuncSetAttribute(k_plane_fast<true, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, kPlaneFastSmem);
   cudaFuncSetAttribute(k_column_fast<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kColFastSmem);
   cudaFuncSetAttribute(k_column_fast<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kColFastSmem);
   cudaFuncSetAttribute(k_column_fast_db<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, col_db_smem(CW_WARPS_FWD));
   cudaFuncSetAttribute(k_column_fast_db<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, col_db_smem(CW_WARPS_INV));
+  cudaFuncSetAttribute(k_column_fast_db<false, CW_WARPS_FWD, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       col_db_smem(CW_WARPS_FWD));
+  cudaFuncSetAttribute(k_column_fast_db<true, CW_WARPS_INV, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       col_db_smem(CW_WARPS_INV));
   {
     const int slot = face_slot((p->max_p + 3) & ~3);
     cudaFuncSetAttribute(k_faces<3, 1, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)face_smem_bytes<3>(slot));
@@ -1821,8 +1845,13 @@ static int column_pass(fmp_precond* p, bool inv, const double* src, double* dst,
     } else {
       const int nwarp = inv ? CW_WARPS_INV : CW_WARPS_FWD;
       const int grid = std::min(p->sms, (p->n_fcol + nwarp - 1) / nwarp);
-      if (inv)
+      const bool small = std::max(p->max_ex, std::max(p->max_ey, p->max_ez)) <= 24;
+      if (inv && small)
+        k_column_fast_db<true, CW_WARPS_INV, 3><<<grid, nwarp * 32, col_db_smem(nwarp), st>>>(a);
+      else if (inv)
         k_column_fast_db<true><<<grid, nwarp * 32, col_db_smem(nwarp), st>>>(a);
+      else if (small)
+        k_column_fast_db<false, CW_WARPS_FWD, 3><<<grid, nwarp * 32, col_db_smem(nwarp), st>>>(a);
       else
         k_column_fast_db<false><<<grid, nwarp * 32, col_db_smem(nwarp), st>>>(a);
     }
@@ -1882,8 +1911,13 @@ static int plane_pass(fmp_precond* p, const fmp_block* blk, bool inv, int mode, 
       a.tma_rows = p->max_ey;
     }
     const int grid = std::min(p->sms, (a.n_items + PW_WARPS - 1) / PW_WARPS);
-    if (inv)
+    const bool small = std::max(p->max_ex, std::max(p->max_ey, p->max_ez)) <= 24;
+    if (inv && small)
+      k_plane_fast<true, 3><<<grid, PW_WARPS * 32, kPlaneFastSmem, st>>>(tm, a);
+    else if (inv)
       k_plane_fast<true><<<grid, PW_WARPS * 32, kPlaneFastSmem, st>>>(tm, a);
+    else if (small)
+      k_plane_fast<false, 3><<<grid, PW_WARPS * 32, kPlaneFastSmem, st>>>(tm, a);
     else
       k_plane_fast<false><<<grid, PW_WARPS * 32, kPlaneFastSmem, st>>>(tm, a);
     FMP_CHECK_LAUNCH();
