@@ -194,6 +194,39 @@ def gen_cn(big: bool):
     np.savez_compressed(OUT / ("cn_big.npz" if big else "cn.npz"), **out)
 
 
+def gen_reports():
+    """Reference CSV outputs (cli.py writers) for the harness-schema parity tests: the writers on
+    a fixed synthetic report, the cost table, and two small real runs (solve + CN)."""
+    import shutil
+    import tempfile
+    from flashmp import cli as rcli
+    d = OUT / "reports"
+    if d.exists():
+        shutil.rmtree(d)
+    d.mkdir()
+    rep = rkr.SolveReport(method="bicgstab", iterations=3, converged=True, final_relres=5.846e-13,
+                          trace=[(0, 1.0, 0.0), (1, 3.277e-05, 0.0125), (2, 2.933e-09, 0.025),
+                                 (3, 5.846e-13, 0.0375)],
+                          breakdown={"fast_solve": 1.25, "spmv": 0.5, "axpy_dot": 0.125}, seconds=1.875)
+    rcli.write_trace_csv(d / "trace.csv", rep)
+    rcli.write_trace_csv(d / "trace_zero.csv", rep, zero_times=True)
+    rcli.write_breakdown_csv(d / "breakdown.csv", rep)
+    cfg = rcli.ExperimentConfig(sub=(32, 32, 32), grid=(2, 2, 2), transport="cuda")
+    rcli.write_summary_csv(d / "summary.csv", [rcli.RunSummary(cfg, rep, 2.5, 0.75),
+                                               rcli.RunSummary(cfg, rep, 2.5, None)])
+    for n in (16, 32):
+        c = rcli.ExperimentConfig(sub=(n, n, n), out=str(d), mode="costs")
+        rcli.run_costs(c)
+        (d / "costs.csv").rename(d / f"costs_{n}.csv")
+    with tempfile.TemporaryDirectory() as tmp:
+        c = rcli.ExperimentConfig(sub=(4, 4, 4), grid=(2, 1, 1), out=tmp, zero_times=True)
+        rcli.run_solve(c)
+        shutil.copy(Path(tmp) / "trace.csv", d / "run_trace.csv")
+        c = rcli.ExperimentConfig(mode="cn", sub=(4, 4, 4), grid=(2, 1, 1), steps=2, out=tmp)
+        rcli.run_cn(c)
+        shutil.copy(Path(tmp) / "cn_steps.csv", d / "run_cn_steps.csv")
+
+
 if __name__ == "__main__":
     big = "--big" in sys.argv
     if not big:
@@ -203,3 +236,5 @@ if __name__ == "__main__":
         gen_schwarz()
     gen_krylov(big)
     gen_cn(big)
+    if not big:
+        gen_reports()
