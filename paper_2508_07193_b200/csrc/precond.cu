@@ -489,7 +489,7 @@ constexpr int CXS = 8;               // column tile row stride (8 columns; fragm
 constexpr int CXR = 36;              // column tile rows per component (pad4 of the max extent)
 constexpr int CX_BUF = 3 * CXR * CXS;  // one column tile (3 components)
 constexpr int CW_WARPS = 12;         // single-buffered inverse pass
-constexpr int CW_WARPS_FWD = 8;      // double-buffered forward column pass
+constexpr int CW_WARPS_FWD = 12;     // double-buffered forward column pass (3 warps per SM sub-partition)
 constexpr int CW_WARPS_INV = 12;     // double-buffered inverse column pass (3 warps per SM sub-partition)
 constexpr int FAST_MAX_EXT = CXR;    // the fast path serves plans whose extents are all <= 36
 
@@ -787,6 +787,18 @@ __global__ void __launch_bounds__(PW_WARPS * 32, 1) k_plane_fast(const __grid_co
 }
 
 
+// 1 / x for x in [1, 1 + 12 alpha] (the block-solve denominators): hardware seed + two Newton
+// steps, branch-free (__drcp_rn's special-case branch serialised the column epilogues); within
+// one ulp of the correctly rounded reciprocal.
+__device__ __forceinline__ double rcp_pos(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+
 struct FastColArgs {
   const fmp_subdomain* subs;
   const int2* items;   // (sub, p0), 8 columns each
@@ -799,6 +811,7 @@ struct FastColArgs {
   double alpha;
   ExtTable et;
   int interleave;      // 1: warp gw takes items gw, gw + nw, ... (neighbouring warps read neighbouring columns)
+  const CUtensorMap* maps;   // k_column_fast_db: per-subdomain [3][ez][ps] maps of src (box 8 x CXR x 3), or null
 };
 
 // K2 (INV=false): y^ = B^-1 (Fz X) over 8 columns x all z, 3 components;  K3 (INV=true): Fz^T (y^ - corr)
@@ -963,20 +976,41 @@ __device__ __forceinline__ void col_mma(double (&acc)[3][5][2], const double* xb
 // warp share their subdomain record, reloaded only when it changes), so the cp.async of the
 // next tile is issued with no dependent global round trip in front of it; the correction
 // planes of K3 are read with all loads of a lane hoisted ahead of the arithmetic.
-template <bool INV, int NW = INV ? CW_WARPS_INV : CW_WARPS_FWD, int NT = 5>   // NT: z tiles (3 or 5)
+// NB = 1 (TMA only): one tile buffer per warp; the next tile is requested as soon as the DMMA
+// loop has consumed the current one, so its latency hides behind the epilogue.
+template <bool INV, int NW = INV ? CW_WARPS_INV : CW_WARPS_FWD, int NT = 5, int NB = 2>   // NT: z tiles (3 or 5)
 __global__ void __launch_bounds__(NW * 32, 1) k_column_fast_db(FastColArgs A) {
   extern __shared__ __align__(16) double smem[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
   load_resident(smem, A.et, A.factors, tid, blockDim.x);
-  double* wbase = smem + RES_WORDS + warp * 2 * CX_BUF;
-  for (int q = lane; q < 2 * CX_BUF; q += 32) wbase[q] = 0.0;
+  double* wbase = smem + RES_WORDS + warp * NB * CX_BUF;
+  for (int q = lane; q < NB * CX_BUF; q += 32) wbase[q] = 0.0;
   __syncthreads();
   const int gw = blockIdx.x * NW + warp, nw = gridDim.x * NW;
   const int per = (A.n_items + nw - 1) / nw;
-  const int beg = gw * per, end = min(beg + per, A.n_items);
+  // interleaved: warp gw takes items gw, gw + nw, ... so the warps in flight read and write
+  // neighbouring 8-column tiles (whole DRAM pages) instead of nw scattered 64-byte rows
+  const int stp = A.interleave ? nw : 1;
+  const int beg = A.interleave ? gw : gw * per, end = A.interleave ? A.n_items : min(beg + per, A.n_items);
   if (beg >= end) return;
 
+  __shared__ __align__(8) uint64_t cbar[NW][2];   // TMA tile arrival, per warp and buffer
+  const bool tma = A.maps != nullptr;
+  if (lane == 0) {
+    mbar_init(&cbar[warp][0], 1);
+    mbar_init(&cbar[warp][1], 1);
+    fence_mbar_init();
+  }
+  uint32_t phase = 0;   // bit b: parity of buffer b's next completion
   auto issue = [&](const int2 w, const SubD& d, int buf) {
+    if (tma) {   // one box: 8 columns x CXR z rows x 3 components, zero-filled past ez / the plane
+      if (lane == 0) {
+        fence_proxy_async();   // this buffer's generic reads/writes precede the async-proxy fill
+        mbar_expect_tx(&cbar[warp][buf], CX_BUF * (int)sizeof(double));
+        tma_load_3d(wbase + buf * CX_BUF, A.maps + w.x, w.y, 0, 0, &cbar[warp][buf]);
+      }
+      return;
+    }
     const int P = d.ex * d.ey, ez = d.ez;
     const int64_t V = d.cstride();
     const double* src = A.src + d.ws_off + w.y;
@@ -998,18 +1032,27 @@ __global__ void __launch_bounds__(NW * 32, 1) k_column_fast_db(FastColArgs A) {
   int buf = 0;
   int2 w_cur = A.items[beg];
   SubD d_cur = load_sub(A.subs + w_cur.x);
-  int2 w_nxt = beg + 1 < end ? A.items[beg + 1] : w_cur;
+  int2 w_nxt = beg + stp < end ? A.items[beg + stp] : w_cur;
+  __syncwarp();
   issue(w_cur, d_cur, 0);
-  cp_async_commit();
-  for (int it = beg; it < end; ++it) {
+  if (!tma) cp_async_commit();
+  for (int it = beg; it < end; it += stp) {
     SubD d_nxt = d_cur;
-    if (it + 1 < end) {
+    if (it + stp < end) {
       if (w_nxt.x != w_cur.x) d_nxt = load_sub(A.subs + w_nxt.x);
-      issue(w_nxt, d_nxt, buf ^ 1);
+      if (NB == 2) issue(w_nxt, d_nxt, buf ^ 1);
     }
-    const int2 w_nn = it + 2 < end ? A.items[it + 2] : w_nxt;   // consumed next iteration
-    cp_async_commit();
-    cp_async_wait<1>();
+    const int2 w_nn = it + 2 * stp < end ? A.items[it + 2 * stp] : w_nxt;   // consumed next iteration
+    if (tma) {
+      mbar_wait(&cbar[warp][buf], (phase >> buf) & 1);
+      phase ^= 1u << buf;
+    } else {
+      cp_async_commit();
+      if (NB == 2)
+        cp_async_wait<1>();
+      else
+        cp_async_wait<0>();
+    }
     __syncwarp();
     const int2 w = w_cur;
     const SubD& d = d_cur;
@@ -1054,7 +1097,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_column_fast_db(FastColArgs A) {
           const double dy = vz0 * gy + vx0 * c3[u];
           const double dz = vy0 * c4[u] + vx0 * c5[u];
           const double sz = Sz[cz];
-          const double q = __drcp_rn(1.0 + A.alpha * (sx * sx + sy * sy + sz * sz));
+          const double q = rcp_pos(1.0 + A.alpha * (sx * sx + sy * sy + sz * sz));
           const double pr = A.alpha * (sx * dx + sy * dy + sz * dz);
           X[(0 * CXR + cz) * CXS + col] -= q * (dx + pr * sx);
           X[(1 * CXR + cz) * CXS + col] -= q * (dy + pr * sy);
@@ -1084,6 +1127,10 @@ __global__ void __launch_bounds__(NW * 32, 1) k_column_fast_db(FastColArgs A) {
       col_mma<INV, 4>(acc, xb, fv, fu, k4);
     else
       col_mma<INV, 5>(acc, xb, fv, fu, k4);
+    if (NB == 1 && it + stp < end) {   // the tile is consumed: fetch the next one under the epilogue
+      __syncwarp();
+      issue(w_nxt, d_nxt, 0);
+    }
     double* dst = A.dst + d.ws_off;
     const int b0 = p0 / ex;   // one division per item; the 8 columns advance b a few times at most
 #pragma unroll
@@ -1106,7 +1153,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_column_fast_db(FastColArgs A) {
         double y0 = acc[0][m][h], y1 = acc[1][m][h], y2 = acc[2][m][h];
         if (!INV) {  // B^-1 y = q (y + alpha s (s . y)), q = 1/(1 + alpha |s|^2)  (ref:subdomain.py:145-153)
           const double sz = Sz[r];
-          const double q = __drcp_rn(1.0 + A.alpha * (sx * sx + sy * sy + sz * sz));
+          const double q = rcp_pos(1.0 + A.alpha * (sx * sx + sy * sy + sz * sz));
           const double pr = A.alpha * (sx * y0 + sy * y1 + sz * y2);
           y0 = q * (y0 + pr * sx);
           y1 = q * (y1 + pr * sy);
@@ -1119,7 +1166,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_column_fast_db(FastColArgs A) {
       }
     }
     __syncwarp();
-    buf ^= 1;
+    buf ^= NB - 1;
     w_cur = w_nxt;
     d_cur = d_nxt;
     w_nxt = w_nn;
@@ -1502,6 +1549,7 @@ struct fmp_precond {
   int4* d_finv = nullptr;
   int2* d_fcol = nullptr;
   int n_ffwd = 0, n_finv = 0, n_fcol = 0;
+  CUtensorMap* d_colmaps = nullptr;       // column tiles by TMA: [work_a maps | work_b maps], one per subdomain
   // Woodbury GEMM: own DMMA kernel (default) or cuBLAS (FMP_GEMM=cublas)
   bool use_cublas = true;
   // Ozaki INT8 tensor-core GEMM (FMP_GEMM=ozaki): int8 slices of C^-1 built once, Y sliced per apply
@@ -1554,6 +1602,7 @@ static void free_plan(fmp_precond* p) {
   cudaFree(p->d_ffwd);
   cudaFree(p->d_finv);
   cudaFree(p->d_fcol);
+  cudaFree(p->d_colmaps);
   cudaFree(p->d_gshapes);
   for (int q = 0; q < fmp_precond::kAux; ++q) {
     if (p->aux_blas[q]) cublasDestroy(p->aux_blas[q]);
@@ -1575,7 +1624,7 @@ static void free_plan(fmp_precond* p) {
 
 constexpr int kPlaneFastSmem = (RES_WORDS + PW_WARPS * PX_BUF + PX_SLACK) * (int)sizeof(double);
 constexpr int kColFastSmem = (RES_WORDS + CW_WARPS * CX_BUF) * (int)sizeof(double);
-constexpr int col_db_smem(int nw) { return (RES_WORDS + nw * 2 * CX_BUF) * (int)sizeof(double); }
+constexpr int col_db_smem(int nw, int nb = 2) { return (RES_WORDS + nw * nb * CX_BUF) * (int)sizeof(double); }
 
 static int plane_nt(const fmp_precond* p) { return std::max(p->max_ex, p->max_ey) <= 40 ? 5 : 9; }
 static int column_mt(const fmp_precond* p) { return pad8(p->max_ez) / 8; }
@@ -1660,6 +1709,33 @@ extern "C" int fmp_precond_create(const fmp_precond_desc* desc, fmp_precond** ou
       if (upload(ff, &p->d_ffwd) || upload(fi, &p->d_finv) || upload(fc, &p->d_fcol)) {
         free_plan(p);
         return -1;
+      }
+      // one 3-D tensor map per subdomain slot and workspace: (column p, z, component), so a
+      // column tile (8 columns x CXR z x 3 components) is a single TMA box; z rows past ez and
+      // columns past the plane come back zero-filled
+      bool col_tma = !getenv_flag("FMP_COL_NO_TMA") && ((uintptr_t)desc->work_a & 15) == 0 &&
+                     ((uintptr_t)desc->work_b & 15) == 0;
+      for (int64_t q = 0; q < desc->n_sub; ++q) col_tma = col_tma && (p->subs[q].ws_off & 1) == 0;
+      if (col_tma) {
+        std::vector<CUtensorMap> maps(2 * desc->n_sub);
+        for (int w = 0; w < 2; ++w) {
+          const double* base = w == 0 ? desc->work_a : desc->work_b;
+          for (int64_t q = 0; q < desc->n_sub; ++q) {
+            const auto& sd = p->subs[q];
+            const uint64_t ps = (uint64_t)((sd.ext[0] * sd.ext[1] + 3) & ~3LL), ez = (uint64_t)sd.ext[2];
+            const uint64_t dims[3] = {ps, ez, 3};
+            const uint64_t strides[2] = {ps * 8, ps * ez * 8};
+            const uint32_t box[3] = {8, CXR, 3};
+            if (encode_tensor_map_f64(&maps[w * desc->n_sub + q], base + sd.ws_off, 3, dims, strides, box)) {
+              free_plan(p);
+              return -1;
+            }
+          }
+        }
+        if (upload(maps, &p->d_colmaps)) {
+          free_plan(p);
+          return -1;
+        }
       }
     }
   }
@@ -1805,6 +1881,7 @@ extern "C" int fmp_precond_create(const fmp_precond_desc* desc, fmp_precond** ou
                        col_db_smem(CW_WARPS_FWD));
   cudaFuncSetAttribute(k_column_fast_db<true, CW_WARPS_INV, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        col_db_smem(CW_WARPS_INV));
+
   {
     const int slot = face_slot((p->max_p + 3) & ~3);
     cudaFuncSetAttribute(k_faces<3, 1, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)face_smem_bytes<3>(slot));
@@ -1838,22 +1915,22 @@ static int column_pass(fmp_precond* p, bool inv, const double* src, double* dst,
     a.pmax = (int)p->d.pmax;
     a.alpha = p->d.alpha;
     a.et = p->et;
-    a.interleave = 0;
+    a.interleave = getenv_flag("FMP_COL_CONTIG") ? 0 : 1;
+    a.maps = p->d_colmaps ? p->d_colmaps + (src == p->d.work_a ? 0 : p->d.n_sub) : nullptr;
+    if (a.maps && src != p->d.work_a && src != p->d.work_b) a.maps = nullptr;
     if (inv && getenv_flag("FMP_COL_SINGLE")) {
       const int grid = std::min(p->sms, (p->n_fcol + CW_WARPS - 1) / CW_WARPS);
       k_column_fast<true><<<grid, CW_WARPS * 32, kColFastSmem, st>>>(a);
     } else {
+      const bool small = std::max(p->max_ex, std::max(p->max_ey, p->max_ez)) <= 24;
       const int nwarp = inv ? CW_WARPS_INV : CW_WARPS_FWD;
       const int grid = std::min(p->sms, (p->n_fcol + nwarp - 1) / nwarp);
-      const bool small = std::max(p->max_ex, std::max(p->max_ey, p->max_ez)) <= 24;
-      if (inv && small)
-        k_column_fast_db<true, CW_WARPS_INV, 3><<<grid, nwarp * 32, col_db_smem(nwarp), st>>>(a);
-      else if (inv)
-        k_column_fast_db<true><<<grid, nwarp * 32, col_db_smem(nwarp), st>>>(a);
-      else if (small)
-        k_column_fast_db<false, CW_WARPS_FWD, 3><<<grid, nwarp * 32, col_db_smem(nwarp), st>>>(a);
-      else
-        k_column_fast_db<false><<<grid, nwarp * 32, col_db_smem(nwarp), st>>>(a);
+#define FMP_COLF(I, S) k_column_fast_db<I, I ? CW_WARPS_INV : CW_WARPS_FWD, S><<<grid, nwarp * 32, col_db_smem(nwarp), st>>>(a);
+      if (inv && small) { FMP_COLF(true, 3) }
+      else if (inv) { FMP_COLF(true, 5) }
+      else if (small) { FMP_COLF(false, 3) }
+      else { FMP_COLF(false, 5) }
+#undef FMP_COLF
     }
     FMP_CHECK_LAUNCH();
     return 0;
