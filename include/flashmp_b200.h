@@ -200,6 +200,11 @@ int fmp_precond_apply(fmp_precond* p, const fmp_block* blk, int mode,
 int fmp_precond_profile(fmp_precond* p, int enable);
 int fmp_precond_stage_ms(fmp_precond* p, float* ms, int n);
 
+/* Diagnostics: with FMP_OZ_PROF=1 in the environment, the last Ozaki GEMM launch's per-CTA
+ * MMA-issuer cycles {total, waiting for operand stages, waiting for the epilogue, tiles} for the
+ * first n CTAs (tools/oz_prof.py).  Returns -1 when profiling is off. */
+int fmp_debug_ozaki_prof(long long* out, int n);
+
 /* Restriction only: out[ws_off(i) ...] = S_i^gamma r for every subdomain i, in the
  * reference's extended-vector order (ref:schwarz.py:217-257).  out has the plan's
  * workspace size.  Exposes the index maps of the fused solve for bit-exact tests. */

@@ -40,6 +40,7 @@ SIGNATURES = {
     "fmp_precond_restrict": (_i, [_p, _p, _p, _p, _p]),
     "fmp_precond_profile": (_i, [_p, _i]),
     "fmp_precond_stage_ms": (_i, [_p, C.POINTER(C.c_float), _i]),
+    "fmp_debug_ozaki_prof": (_i, [_p, _i]),
 }
 
 FMP_SOLVE_WOODBURY, FMP_SOLVE_EXACT, FMP_SOLVE_FACES = 0, 1, 2

@@ -77,7 +77,8 @@ __device__ __forceinline__ void issue_chunk(uint64_t da0, uint64_t db0, uint32_t
 }
 
 __global__ void __launch_bounds__(OZ_THREADS, 1)
-    k_ozaki(const OzShape* __restrict__ shapes, const OzTile* __restrict__ tiles, const int* __restrict__ offs) {
+    k_ozaki(const OzShape* __restrict__ shapes, const OzTile* __restrict__ tiles, const int* __restrict__ offs,
+            long long* __restrict__ prof) {
   extern __shared__ __align__(1024) uint8_t osm[];
   __shared__ __align__(8) uint64_t full_bar[OZ_STAGES], empty_bar[OZ_STAGES], tfull_bar, tempty_bar;
   __shared__ uint32_t tmem_base;
@@ -128,18 +129,23 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
     // ONE MMA of N = (S+1-p) w against B slices 1..S+1-p feeds levels p+1..S+1 at once (split at
     // N = 256): S+3 MMAs per K chunk instead of S(S+1)/2, each A block read from smem once per p.
     int it = 0, tcount = 0;
+    long long t0 = clock64(), w_full = 0, w_empty = 0, t1;
     for (int ti = offs[blockIdx.x]; ti < offs[blockIdx.x + 1]; ++ti, ++tcount) {
       const OzShape sh = shapes[tiles[ti].shape];
       const int w = sh.w;
       const uint32_t lbo_b = (uint32_t)OZ_S * w * 16;
       if (tcount > 0) {   // the epilogue must have drained the accumulators of the previous tile
+        if (prof) t1 = clock64();
         mbar_wait(&tempty_bar, (tcount - 1) & 1);
+        if (prof) w_empty += clock64() - t1;
         asm volatile("tcgen05.fence::after_thread_sync;\n");
       }
       for (int kc = 0; kc < sh.kchunks; ++kc, ++it) {
         const int s = it % OZ_STAGES;
         const uint32_t ph = (it / OZ_STAGES) & 1;
+        if (prof) t1 = clock64();
         mbar_wait(&full_bar[s], ph);
+        if (prof) w_full += clock64() - t1;
         asm volatile("tcgen05.fence::after_thread_sync;\n");
         if (lane == 0) {
           const uint32_t sa = s_u32(osm + s * OZ_STAGE);
@@ -157,6 +163,12 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
         }
         __syncwarp();
       }
+    }
+    if (prof && lane == 0) {   // FMP_OZ_PROF: MMA-warp cycles waiting for operands / for the epilogue
+      prof[blockIdx.x * 4 + 0] = clock64() - t0;
+      prof[blockIdx.x * 4 + 1] = w_full;
+      prof[blockIdx.x * 4 + 2] = w_empty;
+      prof[blockIdx.x * 4 + 3] = tcount;
     }
   } else {
     // ---------------- epilogue warps 0-3: lane quadrant = warp, one row per thread
@@ -311,9 +323,12 @@ int ozaki_setup() {
   return 0;
 }
 
+static long long* g_oz_prof = nullptr;   // FMP_OZ_PROF=1: per-CTA MMA-warp wait cycles (tools)
+
 int ozaki_launch(const OzShape* shapes, const OzTile* tiles, const int* offs, int grid, cudaStream_t st) {
   if (grid <= 0) return 0;
-  k_ozaki<<<grid, OZ_THREADS, OZ_STAGES * OZ_STAGE, st>>>(shapes, tiles, offs);
+  if (!g_oz_prof && getenv_flag("FMP_OZ_PROF")) FMP_CHECK_CUDA(cudaMalloc(&g_oz_prof, 4096 * 4 * sizeof(long long)));
+  k_ozaki<<<grid, OZ_THREADS, OZ_STAGES * OZ_STAGE, st>>>(shapes, tiles, offs, g_oz_prof);
   FMP_CHECK_LAUNCH();
   return 0;
 }
@@ -357,3 +372,11 @@ void ozaki_schedule(const std::vector<OzShape>& shapes, std::vector<OzTile>& til
 }
 
 }  // namespace fmp
+
+// Diagnostics (tools/oz_prof.py): the last Ozaki launch's per-CTA MMA-warp cycles
+// [total, waiting for operand stages, waiting for the epilogue, tiles], FMP_OZ_PROF=1 only.
+extern "C" int fmp_debug_ozaki_prof(long long* out, int n) {
+  if (!fmp::g_oz_prof) return -1;
+  FMP_CHECK_CUDA(cudaMemcpy(out, fmp::g_oz_prof, (size_t)n * 4 * sizeof(long long), cudaMemcpyDeviceToHost));
+  return 0;
+}
