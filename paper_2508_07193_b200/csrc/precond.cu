@@ -1284,17 +1284,16 @@ inline size_t face_smem_bytes(int slot) {
 // loads first, then the z-normal update, the y-normal partial and the x-normal row sums with
 // the FR shuffle reductions interleaved (independent chains, no early exit).
 template <int FR, int FA, int S>
-__device__ __forceinline__ void face_plane(const double* pl, int z, int ex, int ey, bool zn, bool xn, double wz,
-                                           const double* Wy, const double (&wx)[FA], double (&za)[FR][FA],
-                                           double* sB, double (&yp)[FA], int warp, int lane) {
+__device__ __forceinline__ void face_plane(const double* pl, int z, int rowstep, uint32_t vmask, bool zn, bool xn,
+                                           double wz, const double* Wy, const double (&wx)[FA],
+                                           double (&za)[FR][FA], double* sB, double (&yp)[FA], int ey, int warp,
+                                           int lane) {
+  // pl points at this thread's first point (row warp, column lane); vmask bit r*FA+h: (b, a) inside
   double val[FR][FA];
 #pragma unroll
   for (int r = 0; r < FR; ++r)
 #pragma unroll
-    for (int h = 0; h < FA; ++h) {
-      const int b = warp + FACE_WARPS * r, a = lane + 32 * h;
-      val[r][h] = (b < ey && a < ex) ? pl[b * ex + a] : 0.0;
-    }
+    for (int h = 0; h < FA; ++h) val[r][h] = (vmask >> (r * FA + h)) & 1u ? pl[r * rowstep + 32 * h] : 0.0;
   if (zn) {   // z-normal: this thread's (b, a) accumulators live in registers
 #pragma unroll
     for (int r = 0; r < FR; ++r)
@@ -1305,8 +1304,7 @@ __device__ __forceinline__ void face_plane(const double* pl, int z, int ex, int 
   for (int h = 0; h < FA; ++h) yp[h] = 0.0;
 #pragma unroll
   for (int r = 0; r < FR; ++r) {
-    const int b = warp + FACE_WARPS * r;
-    const double wy = b < ey ? Wy[b] : 0.0;
+    const double wy = Wy[warp + FACE_WARPS * r];   // zero-padded past ey
 #pragma unroll
     for (int h = 0; h < FA; ++h) yp[h] += wy * val[r][h];
   }
@@ -1407,23 +1405,37 @@ __global__ void __launch_bounds__(FACE_THREADS, NT <= 5 ? 3 : 1) k_faces(FaceArg
     // ---------------- consumers
     const double* Wz = sWt + 2 * N;
     const double* Wy = sWt + N;
+    // plane-invariant per-thread state, computed once: which of this thread's points lie in the
+    // plane (bit mask), its first point's offset and the row step of its point rows
     double wx[FA], za[FR][FA];
+    uint32_t vmask = 0;
 #pragma unroll
     for (int h = 0; h < FA; ++h) wx[h] = lane + 32 * h < N ? sWt[lane + 32 * h] : 0.0;
 #pragma unroll
     for (int r = 0; r < FR; ++r)
 #pragma unroll
-      for (int h = 0; h < FA; ++h) za[r][h] = 0.0;
+      for (int h = 0; h < FA; ++h) {
+        const int b = warp + FACE_WARPS * r, a = lane + 32 * h;
+        if (b < ey && a < ex) vmask |= 1u << (r * FA + h);
+        za[r][h] = 0.0;
+      }
+    const int first = warp * ex + lane, rowstep = FACE_WARPS * ex;
+    int slot = 0;
+    uint32_t ph = 0;
     for (int z0 = 0; z0 < ez; z0 += FZ) {
       const int nzc = min(FZ, ez - z0);
       for (int zz = 0; zz < nzc; ++zz) {
-        const int z = z0 + zz, slot = z % NS;
-        mbar_wait(&full[slot], (uint32_t)((z / NS) & 1));
-        const double* pl = ring + slot * SLOT;
+        const int z = z0 + zz;
+        mbar_wait(&full[slot], ph);
+        const double* pl = ring + slot * SLOT + first;
         double yp[FA];
-        face_plane<FR, FA, S>(pl, z, ex, ey, zn, xn, Wz[z], Wy, wx, za, sB, yp, warp, lane);
+        face_plane<FR, FA, S>(pl, z, rowstep, vmask, zn, xn, Wz[z], Wy, wx, za, sB, yp, ey, warp, lane);
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[slot]);
+        if (++slot == NS) {
+          slot = 0;
+          ph ^= 1u;
+        }
         if (yn) {
 #pragma unroll
           for (int h = 0; h < FA; ++h)
