@@ -648,7 +648,7 @@ __global__ void __launch_bounds__(PW_WARPS * 32, 1) k_plane_fast(const __grid_co
   load_resident(smem, A.et, A.factors, tid, blockDim.x);
   double* T = smem + RES_WORDS + warp * PX_BUF;   // this warp's plane buffer (also the step-1 result)
   for (int q = tid; q < PW_WARPS * PX_BUF + PX_SLACK; q += blockDim.x) smem[RES_WORDS + q] = 0.0;
-  if (!INV && A.tma_rows > 0 && lane == 0) {
+  if ((INV || A.tma_rows > 0) && lane == 0) {   // forward TMA boxes / inverse bulk rows
     mbar_init(&pbar[warp], 1);
     fence_mbar_init();
   }
@@ -669,6 +669,16 @@ __global__ void __launch_bounds__(PW_WARPS * 32, 1) k_plane_fast(const __grid_co
       const int64_t P = (int64_t)ex * ey;
       const double* base = INV ? A.src + d.ws_off + (int64_t)(c * d.ez + d.oz + w.z) * d.ps
                                : A.src + d.in_off + c * P * d.ez + w.z * P;
+      if (INV && (ex & 1) == 0 && ((uintptr_t)base & 15) == 0) {
+        // one bulk copy per row (rows of an even extent are 16-byte aligned), completion on the
+        // warp's mbarrier; the generic reads of the previous plane precede the async writes
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) mbar_expect_tx(&pbar[warp], (uint32_t)(ex * ey * 8));
+        __syncwarp();
+        for (int j = lane; j < ey; j += 32) bulk_g2s(X + j * PXS, base + j * ex, (uint32_t)(ex * 8), &pbar[warp]);
+        return -16;
+      }
       if ((ex & 1) == 0 && ((uintptr_t)base & 15) == 0) {   // 16-byte chunks of whole rows
         const int nch = ex >> 1, ch0 = lane & 15, j0 = lane >> 4;
         for (int j = j0; j < ey; j += 2)
@@ -721,7 +731,7 @@ __global__ void __launch_bounds__(PW_WARPS * 32, 1) k_plane_fast(const __grid_co
   SubD d_cur = load_sub(A.subs + w_cur.x);
   for (int it = beg; it < end; ++it) {
     int shift = issue(w_cur, d_cur);
-    if (shift < 0) {   // one TMA box: rows of PXS doubles land at stride PXS (issued here, in the
+    if (shift < 0 && shift != -16) {   // one TMA box: rows of PXS doubles land at stride PXS (issued here, in the
                        // kernel body: the tensor map must stay a __grid_constant__ parameter)
       fence_proxy_async();   // earlier generic accesses of the buffer before the async write
       __syncwarp();
@@ -732,10 +742,10 @@ __global__ void __launch_bounds__(PW_WARPS * 32, 1) k_plane_fast(const __grid_co
     }
     cp_async_commit();
     const int4 w_nxt = it + 1 < end ? A.items[it + 1] : w_cur;
-    if (shift < 0) {
+    if (shift < 0) {   // TMA box or bulk rows
       mbar_wait(&pbar[warp], tphase);
       tphase ^= 1u;
-      shift = -1 - shift;
+      shift = shift == -16 ? 0 : -1 - shift;
     } else {
       cp_async_wait<0>();
     }
