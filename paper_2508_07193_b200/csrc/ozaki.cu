@@ -32,8 +32,10 @@ namespace fmp {
 constexpr int OZ_S = 7;                 // slices per operand
 constexpr int OZ_M = 128;               // rows per tile (TMEM lanes)
 constexpr int OZ_WMAX = 64;             // column-tile width cap (multiple of 16): OZ_S * w <= 512 TMEM columns
-constexpr int OZ_MAX_K = 16384;         // int32 headroom: S pairs x 2^14 x K < 2^31
+constexpr int OZ_MAX_K = 16384;         // int32 headroom: S pairs x 2^14 x K < 2^31 (per K part)
 constexpr int OZ_KC = 32;               // K bytes per MMA / stage
+constexpr int OZ_PART = OZ_MAX_K / OZ_KC;   // K chunks per part: larger K is split into parts whose
+                                             // FP64 results the epilogue adds (same CTA, in order)
 constexpr int OZ_ABLK = OZ_M * OZ_KC;   // bytes of one A slice block
 constexpr int OZ_STAGE = OZ_S * (OZ_ABLK + OZ_WMAX * OZ_KC);
 constexpr int OZ_STAGES = 5;
@@ -112,7 +114,8 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
         const int8_t* a = sh.A + (size_t)tl.mt * sh.kchunks * OZ_S * OZ_ABLK;
         const uint32_t bblk = (uint32_t)sh.w * OZ_KC;
         const int8_t* b = sh.B + (size_t)tl.nt * sh.kchunks * OZ_S * bblk;
-        for (int kc = 0; kc < sh.kchunks; ++kc, ++it) {
+        const int k0 = tl.kpart * OZ_PART, k1 = min(sh.kchunks, k0 + OZ_PART);
+        for (int kc = k0; kc < k1; ++kc, ++it) {
           const int s = it % OZ_STAGES;
           const uint32_t ph = (it / OZ_STAGES) & 1;
           mbar_wait(&empty_bar[s], ph ^ 1);
@@ -131,8 +134,10 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
     int it = 0, tcount = 0;
     long long t0 = clock64(), w_full = 0, w_empty = 0, t1;
     for (int ti = offs[blockIdx.x]; ti < offs[blockIdx.x + 1]; ++ti, ++tcount) {
-      const OzShape sh = shapes[tiles[ti].shape];
+      const OzTile tl = tiles[ti];
+      const OzShape sh = shapes[tl.shape];
       const int w = sh.w;
+      const int k0 = tl.kpart * OZ_PART, k1 = min(sh.kchunks, k0 + OZ_PART);
       const uint32_t lbo_b = (uint32_t)OZ_S * w * 16;
       if (tcount > 0) {   // the epilogue must have drained the accumulators of the previous tile
         if (prof) t1 = clock64();
@@ -140,7 +145,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
         if (prof) w_empty += clock64() - t1;
         asm volatile("tcgen05.fence::after_thread_sync;\n");
       }
-      for (int kc = 0; kc < sh.kchunks; ++kc, ++it) {
+      for (int kc = k0; kc < k1; ++kc, ++it) {
         const int s = it % OZ_STAGES;
         const uint32_t ph = (it / OZ_STAGES) & 1;
         if (prof) t1 = clock64();
@@ -151,7 +156,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
           const uint32_t sa = s_u32(osm + s * OZ_STAGE);
           const uint64_t da0 = umma_desc(sa, OZ_M * 16, 128);
           const uint64_t db0 = umma_desc(sa + OZ_S * OZ_ABLK, lbo_b, 128);
-          const bool first = kc == 0;
+          const bool first = kc == k0;
           switch (w) {
             case 16: issue_chunk<16>(da0, db0, tmem, first); break;
             case 32: issue_chunk<32>(da0, db0, tmem, first); break;
@@ -159,7 +164,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
             default: issue_chunk<64>(da0, db0, tmem, first); break;
           }
           umma_commit(&empty_bar[s]);                         // stage free once these MMAs retire
-          if (kc == sh.kchunks - 1) umma_commit(&tfull_bar);  // accumulators complete
+          if (kc == k1 - 1) umma_commit(&tfull_bar);  // accumulators complete
         }
         __syncwarp();
       }
@@ -204,7 +209,11 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
 #pragma unroll
           for (int j = 0; j < 16; ++j) {
             const int n = tl.nt * sh.w + c0 + j;
-            if (n < sh.n) sh.Z[(size_t)n * sh.ld + row] = ldexp(acc[j], ea + sh.eB[n] + 4);
+            if (n < sh.n) {
+              double* z = sh.Z + (size_t)n * sh.ld + row;
+              const double v = ldexp(acc[j], ea + sh.eB[n] + 4);
+              *z = tl.kpart == 0 ? v : *z + v;   // later K parts: this CTA wrote the earlier ones
+            }
           }
         }
       }
@@ -312,9 +321,8 @@ size_t ozaki_b_bytes(int n, int kchunks) {
   const int w = ozaki_width(n);
   return (size_t)((n + w - 1) / w) * kchunks * OZ_S * w * OZ_KC;
 }
-int ozaki_kchunks(int m) {
-  return m <= OZ_MAX_K ? (m + OZ_KC - 1) / OZ_KC : -1;
-}
+int ozaki_kchunks(int m) { return (m + OZ_KC - 1) / OZ_KC; }
+int ozaki_kparts(int kchunks) { return (kchunks + OZ_PART - 1) / OZ_PART; }
 int ozaki_tile_m() { return OZ_M; }
 
 int ozaki_setup() {
@@ -349,18 +357,31 @@ void ozaki_schedule(const std::vector<OzShape>& shapes, std::vector<OzTile>& til
   std::vector<double> cost(tiles.size());
   for (size_t i = 0; i < tiles.size(); ++i) {
     const OzShape& sh = shapes[tiles[i].shape];
-    cost[i] = sh.kchunks * chunk_cycles(sh.w);
+    const int k0 = tiles[i].kpart * OZ_PART;
+    cost[i] = std::min(OZ_PART, sh.kchunks - k0) * chunk_cycles(sh.w);
   }
-  std::vector<int> order(tiles.size());
+  // the K parts of one (shape, row tile, column tile) are one unit: same CTA, original order
+  std::vector<int> unit_of(tiles.size());
+  std::vector<double> ucost;
+  for (size_t i = 0; i < tiles.size(); ++i) {
+    const bool same = i > 0 && tiles[i].shape == tiles[i - 1].shape && tiles[i].mt == tiles[i - 1].mt &&
+                      tiles[i].nt == tiles[i - 1].nt;
+    if (!same) ucost.push_back(0.0);
+    unit_of[i] = (int)ucost.size() - 1;
+    ucost.back() += cost[i];
+  }
+  std::vector<int> order(ucost.size());
   for (size_t i = 0; i < order.size(); ++i) order[i] = (int)i;
-  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return cost[a] > cost[b]; });
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return ucost[a] > ucost[b]; });
   std::vector<double> load(grid, 0.0);
-  std::vector<std::vector<int>> lists(grid);
-  for (int i : order) {
+  std::vector<int> cta_of_unit(ucost.size());
+  for (int u : order) {
     const int c = (int)(std::min_element(load.begin(), load.end()) - load.begin());
-    load[c] += cost[i];
-    lists[c].push_back(i);
+    load[c] += ucost[u];
+    cta_of_unit[u] = c;
   }
+  std::vector<std::vector<int>> lists(grid);
+  for (size_t i = 0; i < tiles.size(); ++i) lists[cta_of_unit[unit_of[i]]].push_back((int)i);
   std::vector<OzTile> out;
   offs.assign(1, 0);
   for (auto& l : lists) {

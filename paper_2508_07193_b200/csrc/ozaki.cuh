@@ -15,7 +15,7 @@ struct OzShape {
   int m, n, ld, kchunks, w, pad;   // w: column-tile width (multiple of 16, S*w <= 512)
 };
 struct OzTile {
-  int shape, mt, nt, pad;
+  int shape, mt, nt, kpart;   // kpart: K part (chunks [kpart * 512, ...)) for K > 16384
 };
 // One operand to slice: rows x kvalid doubles (row stride ld) -> tiles of height T.
 struct OzSlice {
@@ -29,6 +29,7 @@ struct OzSlice {
 
 int ozaki_setup();
 int ozaki_kchunks(int m);
+int ozaki_kparts(int kchunks);                 // K parts of <= 16384 bytes (int32 level headroom)
 int ozaki_tile_m();
 int ozaki_width(int n);                       // column-tile width for n columns
 size_t ozaki_a_bytes(int m, int kchunks);

@@ -1785,9 +1785,6 @@ extern "C" int fmp_precond_create(const fmp_precond_desc* desc, fmp_precond** ou
   {  // grouped GEMM tables: one shape record per extended shape, tiles bucketed by configuration
     const char* gm = getenv("FMP_GEMM");
     std::string gmode = gm ? gm : "ozaki";   // cublas | own | ozaki
-    if (gmode == "ozaki")   // the int32 level accumulators bound K = m (64^3-class subdomains exceed it)
-      for (const auto& sh : p->shapes)
-        if (ozaki_kchunks((int)sh.m) <= 0) gmode = "cublas";
     p->use_cublas = gmode == "cublas";
     p->use_ozaki = gmode == "ozaki";
     std::vector<GemmShape> gs;
@@ -1822,7 +1819,6 @@ extern "C" int fmp_precond_create(const fmp_precond_desc* desc, fmp_precond** ou
         continue;
       }
       const int m = (int)sh.m, n = p->gcols[s2], kc = ozaki_kchunks(m);
-      FMP_REQUIRE(kc > 0, "Ozaki GEMM: correction size m = %d exceeds the int32 accumulator range", m);
       const int w = ozaki_width(std::max(n, 1));
       int8_t *a = nullptr, *b = nullptr;
       int *ea = nullptr, *eb = nullptr;
@@ -1840,7 +1836,8 @@ extern "C" int fmp_precond_create(const fmp_precond_desc* desc, fmp_precond** ou
       if (n > 0) sb.push_back(OzSlice{p->ymat[s2], b, eb, n, (int)sh.ld, m, kc, w, 1, 0, 0});
       os.push_back(OzShape{a, ea, b, eb, p->zmat[s2], m, n, (int)sh.ld, kc, w, 0});
       for (int mt = 0; mt * ozaki_tile_m() < m; ++mt)
-        for (int nt = 0; nt * w < n; ++nt) ot.push_back(OzTile{(int)s2, mt, nt, 0});
+        for (int nt = 0; nt * w < n; ++nt)
+          for (int kp = 0; kp < ozaki_kparts(kc); ++kp) ot.push_back(OzTile{(int)s2, mt, nt, kp});
     }
     int64_t ra = 0, qa = 0;
     ozaki_plan_slices(sa.data(), (int)sa.size(), &ra, &qa);

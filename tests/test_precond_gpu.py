@@ -171,7 +171,8 @@ def test_stage_timing_api():
 def test_single_subdomain_preconditioner_is_the_exact_inverse(n):
     """With one subdomain covering the box, RAS is the exact solve: M^-1 (A x) == x.  Covers the
     large-extent paths: general (CTA) transform kernels, the 9-tile face kernels (extent > 40), the
-    Ozaki GEMM at m = 14,259 (n = 49) and the cuBLAS fallback past its K bound (n = 66, m = 25,938)."""
+    Ozaki GEMM at m = 14,259 (n = 49) and its K-split form past the int32 level bound (n = 66,
+    m = 25,938: two K parts added in FP64)."""
     from paper_2508_07193_b200 import Box, DistributedOperator, RasPreconditioner, make_partition, make_transport
     part = make_partition(Box(n, n, n), (1, 1, 1), 1)
     tr = make_transport("cuda")

@@ -37,6 +37,6 @@ for sd in subs:
         print(json.dumps({"grid": n, "subdomain": sd, "method": method, "iters": rep.iterations,
                           "final_relres": rep.final_relres, "step_ms": round(ms, 3),
                           "mdofs": round(3 * n ** 3 / ms / 1e3, 1), "setup_s": round(setup, 2),
-                          "gemm": "cublas" if sd >= 64 else "ozaki"}), flush=True)
+                          "gemm": "ozaki (2 K parts)" if sd >= 64 else "ozaki"}), flush=True)
         del st, solver
         torch.cuda.empty_cache()
