@@ -542,6 +542,7 @@ struct FastPlaneArgs {
   int mode;
   ExtTable et;
   int tma_rows;        // > 0: forward planes inside the block arrive as one TMA box of PXS x tma_rows
+  int interleave;      // 1: warp gw takes items gw, gw + nw, ... (round-robin plane order)
 };
 
 // K1 (INV=false): plane k of S_i r -> Fy X Fx^T -> work;  K4 (INV=true): work plane -> Fy^T X Fx -> owned z
@@ -658,7 +659,8 @@ __global__ void __launch_bounds__(PW_WARPS * 32, 1) k_plane_fast(const __grid_co
   __syncthreads();
   const int gw = blockIdx.x * PW_WARPS + warp, nw = gridDim.x * PW_WARPS;
   const int per = (A.n_items + nw - 1) / nw;
-  const int beg = gw * per, end = min(beg + per, A.n_items);
+  const int stp = A.interleave ? nw : 1;
+  const int beg = A.interleave ? gw : gw * per, end = A.interleave ? A.n_items : min(beg + per, A.n_items);
 
   // returns the column shift of the plane data inside the buffer (16-byte superset loads);
   // no integer division in the copy loops (the XU pipe would become the bottleneck)
@@ -729,7 +731,7 @@ __global__ void __launch_bounds__(PW_WARPS * 32, 1) k_plane_fast(const __grid_co
   if (beg >= end) return;
   int4 w_cur = A.items[beg];
   SubD d_cur = load_sub(A.subs + w_cur.x);
-  for (int it = beg; it < end; ++it) {
+  for (int it = beg; it < end; it += stp) {
     int shift = issue(w_cur, d_cur);
     if (shift < 0 && shift != -16) {   // one TMA box: rows of PXS doubles land at stride PXS (issued here, in the
                        // kernel body: the tensor map must stay a __grid_constant__ parameter)
@@ -741,7 +743,7 @@ __global__ void __launch_bounds__(PW_WARPS * 32, 1) k_plane_fast(const __grid_co
       }
     }
     cp_async_commit();
-    const int4 w_nxt = it + 1 < end ? A.items[it + 1] : w_cur;
+    const int4 w_nxt = it + stp < end ? A.items[it + stp] : w_cur;
     if (shift < 0) {   // TMA box or bulk rows
       mbar_wait(&pbar[warp], tphase);
       tphase ^= 1u;
@@ -1994,6 +1996,7 @@ static int plane_pass(fmp_precond* p, const fmp_block* blk, bool inv, int mode, 
     a.factors = p->d.factors;
     a.mode = mode;
     a.et = p->et;
+    a.interleave = getenv_flag("FMP_PLANE_CONTIG") ? 0 : 1;   // round-robin planes (DRAM page locality)
     CUtensorMap tm{};
     a.tma_rows = 0;
     if (!inv && mode != FMP_SOLVE_FACES && (blk->bx & 1) == 0 && ((uintptr_t)src & 15) == 0 &&

@@ -186,7 +186,8 @@ def test_single_subdomain_preconditioner_is_the_exact_inverse(n):
 @pytest.mark.parametrize("gext,grid", [((64, 64, 64), (2, 2, 2)), ((48, 48, 48), (3, 3, 3))])
 def test_column_tile_paths_bitwise(gext, grid, monkeypatch):
     """The column passes' TMA tiles (per-subdomain tensor maps, zero fill past ez), the cp.async
-    tile loads (FMP_COL_NO_TMA) and the contiguous per-warp tile order (FMP_COL_CONTIG) run the
+    tile loads (FMP_COL_NO_TMA) and the contiguous per-warp tile / plane orders (FMP_COL_CONTIG,
+    FMP_PLANE_CONTIG) run the
     same arithmetic: bit-identical preconditioner outputs, including ragged last 8-column tiles."""
     from paper_2508_07193_b200 import Box, RasPreconditioner, make_partition, make_transport
     part = make_partition(Box(*gext), grid, 1)
@@ -198,5 +199,6 @@ def test_column_tile_paths_bitwise(gext, grid, monkeypatch):
     z1 = RasPreconditioner(part, 0.25, tr).apply(r)
     monkeypatch.delenv("FMP_COL_NO_TMA")
     monkeypatch.setenv("FMP_COL_CONTIG", "1")
+    monkeypatch.setenv("FMP_PLANE_CONTIG", "1")
     z2 = RasPreconditioner(part, 0.25, tr).apply(r)
     assert torch.equal(z0, z1) and torch.equal(z0, z2)
