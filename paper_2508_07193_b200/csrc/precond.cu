@@ -1143,38 +1143,55 @@ __global__ void __launch_bounds__(NW * 32, 1) k_column_fast_db(FastColArgs A) {
       __syncwarp();
       issue(w_nxt, d_nxt, 0);
     }
+    // epilogue: this lane's column pair p = p0 + 2t, p + 1 (adjacent doubles, one 16-byte store
+    // per row and component when both lie in the plane)
     double* dst = A.dst + d.ws_off;
-    const int b0 = p0 / ex;   // one division per item; the 8 columns advance b a few times at most
+    const int pA = p0 + 2 * t;
+    const bool v0 = pA < P, v1 = pA + 1 < P;
+    double sx[2] = {0.0, 0.0}, sy[2] = {0.0, 0.0};
+    if (!INV) {
+      const int b0 = p0 / ex;   // one division per item; the 8 columns advance b a few times at most
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int p = p0 + 2 * t + h;
-      if (p >= P) continue;
-      double sx = 0.0, sy = 0.0;
-      if (!INV) {
-        int b = b0, a = p - b0 * ex;
+      for (int h = 0; h < 2; ++h) {
+        if (pA + h >= P) continue;
+        int b = b0, a = pA + h - b0 * ex;
         while (a >= ex) { a -= ex; ++b; }
-        sx = Sx[a];
-        sy = Sy[b];
+        sx[h] = Sx[a];
+        sy[h] = Sy[b];
       }
+    }
+    if (v0) {
 #pragma unroll
       for (int m = 0; m < 5; ++m) {
         if (m >= mt) break;
         if (INV && m * 8 + g >= d.wz) continue;
         const int r = INV ? d.oz + m * 8 + g : m * 8 + g;
         if (r >= ez) continue;
-        double y0 = acc[0][m][h], y1 = acc[1][m][h], y2 = acc[2][m][h];
-        if (!INV) {  // B^-1 y = q (y + alpha s (s . y)), q = 1/(1 + alpha |s|^2)  (ref:subdomain.py:145-153)
-          const double sz = Sz[r];
-          const double q = rcp_pos(1.0 + A.alpha * (sx * sx + sy * sy + sz * sz));
-          const double pr = A.alpha * (sx * y0 + sy * y1 + sz * y2);
-          y0 = q * (y0 + pr * sx);
-          y1 = q * (y1 + pr * sy);
-          y2 = q * (y2 + pr * sz);
+        double y[3][2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          double y0 = acc[0][m][h], y1 = acc[1][m][h], y2 = acc[2][m][h];
+          if (!INV) {  // B^-1 y = q (y + alpha s (s . y)), q = 1/(1 + alpha |s|^2)  (ref:subdomain.py:145-153)
+            const double sz = Sz[r];
+            const double q = rcp_pos(1.0 + A.alpha * (sx[h] * sx[h] + sy[h] * sy[h] + sz * sz));
+            const double pr = A.alpha * (sx[h] * y0 + sy[h] * y1 + sz * y2);
+            y0 = q * (y0 + pr * sx[h]);
+            y1 = q * (y1 + pr * sy[h]);
+            y2 = q * (y2 + pr * sz);
+          }
+          y[0][h] = y0;
+          y[1][h] = y1;
+          y[2][h] = y2;
         }
-        const int64_t o = (int64_t)r * d.ps + p;
-        dst[o] = y0;
-        dst[V + o] = y1;
-        dst[2 * V + o] = y2;
+        const int64_t o = (int64_t)r * d.ps + pA;
+        if (v1) {
+#pragma unroll
+          for (int cc = 0; cc < 3; ++cc)
+            *reinterpret_cast<double2*>(dst + cc * V + o) = make_double2(y[cc][0], y[cc][1]);
+        } else {
+#pragma unroll
+          for (int cc = 0; cc < 3; ++cc) dst[cc * V + o] = y[cc][0];
+        }
       }
     }
     __syncwarp();
