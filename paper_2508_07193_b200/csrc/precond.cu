@@ -627,16 +627,28 @@ __device__ __forceinline__ void plane_step2(const double* T, const double* Fy, c
     if (!INV && row >= ey) continue;
     if (INV && row >= d.wy) continue;
 #pragma unroll
-    for (int q = 0; q < NN; ++q)
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int col = (n0 + q) * 8 + 2 * t + h;
-        if (!INV) {
-          if (col < ex) A.dst[obase + row * ex + col] = acc[q][m][h];
-        } else if (col < d.wx) {
-          A.dst[fidx(A.g, c, d.lz + d.oz + kplane, d.ly + d.oy + row, d.lx + d.ox + col)] = acc[q][m][h];
+    for (int q = 0; q < NN; ++q) {
+      // the lane's adjacent column pair: one 16-byte store when both columns are in range and the
+      // pair is 16-byte aligned (even plane rows forward; the owned tile starts at an even x)
+      const int col = (n0 + q) * 8 + 2 * t;
+      if (!INV) {
+        double* o = A.dst + obase + row * ex + col;
+        if ((ex & 1) == 0 && col + 1 < ex) {
+          *reinterpret_cast<double2*>(o) = make_double2(acc[q][m][0], acc[q][m][1]);
+        } else {
+          if (col < ex) o[0] = acc[q][m][0];
+          if (col + 1 < ex) o[1] = acc[q][m][1];
+        }
+      } else if (col < d.wx) {
+        double* o = A.dst + fidx(A.g, c, d.lz + d.oz + kplane, d.ly + d.oy + row, d.lx + d.ox + col);
+        if (col + 1 < d.wx && (((uintptr_t)o) & 15) == 0) {
+          *reinterpret_cast<double2*>(o) = make_double2(acc[q][m][0], acc[q][m][1]);
+        } else {
+          o[0] = acc[q][m][0];
+          if (col + 1 < d.wx) o[1] = acc[q][m][1];
         }
       }
+    }
   }
 }
 
