@@ -433,34 +433,50 @@ __global__ void __launch_bounds__(CW * 32, 2) k_column(ColArgs A) {
         dmma884(acc[2][m][0], acc[2][m][1], au, b2);
       }
     }
+    // epilogue per row tile over the lane's column pair (16-byte stores when both are in the plane)
     double* dst = A.dst + d.ws_off;
+    const int pA = p0 + warp * 8 + 2 * t;
+    const bool v0 = pA < P, v1 = pA + 1 < P;
+    double sx[2] = {0.0, 0.0}, sy[2] = {0.0, 0.0};
+    if (!INV) {
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int p = p0 + warp * 8 + 2 * t + h;
-      if (p >= P) continue;
-      double sx = 0.0, sy = 0.0;
-      if (!INV) {
-        const int b = p / ex, a = p - b * ex;
-        sx = __ldg(Sx + a);
-        sy = __ldg(Sy + b);
+      for (int h = 0; h < 2; ++h) {
+        if (pA + h >= P) continue;
+        const int b = (pA + h) / ex, a = pA + h - b * ex;
+        sx[h] = __ldg(Sx + a);
+        sy[h] = __ldg(Sy + b);
       }
+    }
+    if (v0) {
 #pragma unroll
       for (int m = 0; m < MT; ++m) {
         const int r = m * 8 + g;
         if (r >= ez) continue;
-        double y0 = acc[0][m][h], y1 = acc[1][m][h], y2 = acc[2][m][h];
-        if (!INV) {  // B^-1 y = q y + w s (s . y)   (ref:subdomain.py:145-153, table form)
-          const double sz = __ldg(Sz + r);
-          const double q = __ldg(QW + 2 * ((int64_t)r * P + p)), wq = __ldg(QW + 2 * ((int64_t)r * P + p) + 1);
-          const double pr = wq * (sx * y0 + sy * y1 + sz * y2);
-          y0 = q * y0 + pr * sx;
-          y1 = q * y1 + pr * sy;
-          y2 = q * y2 + pr * sz;
+        double y[3][2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          double y0 = acc[0][m][h], y1 = acc[1][m][h], y2 = acc[2][m][h];
+          if (!INV && (h == 0 || v1)) {  // B^-1 y = q y + w s (s . y)   (ref:subdomain.py:145-153, table form)
+            const double sz = __ldg(Sz + r);
+            const double2 qw = __ldg(reinterpret_cast<const double2*>(QW) + ((int64_t)r * P + pA + h));
+            const double pr = qw.y * (sx[h] * y0 + sy[h] * y1 + sz * y2);
+            y0 = qw.x * y0 + pr * sx[h];
+            y1 = qw.x * y1 + pr * sy[h];
+            y2 = qw.x * y2 + pr * sz;
+          }
+          y[0][h] = y0;
+          y[1][h] = y1;
+          y[2][h] = y2;
         }
-        const int64_t o = (int64_t)r * d.ps + p;
-        dst[o] = y0;
-        dst[V + o] = y1;
-        dst[2 * V + o] = y2;
+        const int64_t o = (int64_t)r * d.ps + pA;
+        if (v1) {
+#pragma unroll
+          for (int cc = 0; cc < 3; ++cc)
+            *reinterpret_cast<double2*>(dst + cc * V + o) = make_double2(y[cc][0], y[cc][1]);
+        } else {
+#pragma unroll
+          for (int cc = 0; cc < 3; ++cc) dst[cc * V + o] = y[cc][0];
+        }
       }
     }
     buf ^= 1;
