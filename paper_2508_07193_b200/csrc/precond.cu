@@ -852,6 +852,7 @@ struct FastColArgs {
   ExtTable et;
   int interleave;      // 1: warp gw takes items gw, gw + nw, ... (neighbouring warps read neighbouring columns)
   const CUtensorMap* maps;   // k_column_fast_db: per-subdomain [3][ez][ps] maps of src (box 8 x CXR x 3), or null
+  int no_rem;                // 1: the fifth row tile on DMMA too (FMP_COL_NO_REM, A/B)
 };
 
 // K2 (INV=false): y^ = B^-1 (Fz X) over 8 columns x all z, 3 components;  K3 (INV=true): Fz^T (y^ - corr)
@@ -1154,7 +1155,10 @@ __global__ void __launch_bounds__(NW * 32, 1) k_column_fast_db(FastColArgs A) {
       for (int m = 0; m < 5; ++m) acc[cc][m][0] = acc[cc][m][1] = 0.0;
     // INV (prolongation): only the owned z rows [oz, oz + wz) are formed (4 row tiles when
     // wz <= 32; the tile count is a template constant of col_mma)
-    const int mt = NT == 3 ? (INV && d.wz <= 16 ? 2 : 3) : (INV && d.wz <= 32 ? 4 : 5);
+    // forward, 33/34-point columns: rows 32.. of the fifth 8-row tile would be 75-88% padding,
+    // so the DMMA covers rows 0-31 and the one or two remainder rows are DFMA dot products below
+    const bool rem = !INV && NT == 5 && ez > 32 && ez <= 34 && !A.no_rem;
+    const int mt = NT == 3 ? (INV && d.wz <= 16 ? 2 : 3) : ((INV && d.wz <= 32) || rem ? 4 : 5);
     const double* xb = X + t * CXS + g;
     const double* fv = INV ? Fv + t * FSM + g + d.oz : Fv + g * FSM + t;
     const double* fu = INV ? Fu + t * FSM + g + d.oz : Fu + g * FSM + t;
@@ -1171,9 +1175,39 @@ __global__ void __launch_bounds__(NW * 32, 1) k_column_fast_db(FastColArgs A) {
       __syncwarp();
       issue(w_nxt, d_nxt, 0);
     }
+    double* dst = A.dst + d.ws_off;
+    if (!INV && rem) {
+      // remainder rows r = 32 + (lane >> 4): lanes split K in halves ((lane >> 3) & 1) and add by
+      // shuffle; column lane & 7; then the 3x3 block solve of the point and its three stores
+      const int rr = 32 + (lane >> 4), half = (lane >> 3) & 1, col = lane & 7;
+      const int kb = half * 17, ke = min(ez, kb + 17);
+      double o3[3] = {0.0, 0.0, 0.0};
+      const double* fvr = Fv + min(rr, ez - 1) * FSM;
+      const double* fur = Fu + min(rr, ez - 1) * FSM;
+      for (int k = kb; k < ke; ++k) {
+        const double fv0 = fvr[k], fu0 = fur[k];
+        o3[0] = fma(fv0, X[(0 * CXR + k) * CXS + col], o3[0]);
+        o3[1] = fma(fv0, X[(1 * CXR + k) * CXS + col], o3[1]);
+        o3[2] = fma(fu0, X[(2 * CXR + k) * CXS + col], o3[2]);
+      }
+#pragma unroll
+      for (int cc = 0; cc < 3; ++cc) o3[cc] += __shfl_xor_sync(0xffffffffu, o3[cc], 8);
+      const int p = p0 + col;
+      if (half == 0 && rr < ez && p < P) {
+        const int b0 = p0 / ex;
+        int b = b0, a = p - b0 * ex;
+        while (a >= ex) { a -= ex; ++b; }
+        const double sxv = Sx[a], syv = Sy[b], sz = Sz[rr];
+        const double q = rcp_pos(1.0 + A.alpha * (sxv * sxv + syv * syv + sz * sz));
+        const double pr = A.alpha * (sxv * o3[0] + syv * o3[1] + sz * o3[2]);
+        const int64_t o = (int64_t)rr * d.ps + p;
+        dst[o] = q * (o3[0] + pr * sxv);
+        dst[V + o] = q * (o3[1] + pr * syv);
+        dst[2 * V + o] = q * (o3[2] + pr * sz);
+      }
+    }
     // epilogue: this lane's column pair p = p0 + 2t, p + 1 (adjacent doubles, one 16-byte store
     // per row and component when both lie in the plane)
-    double* dst = A.dst + d.ws_off;
     const int pA = p0 + 2 * t;
     const bool v0 = pA < P, v1 = pA + 1 < P;
     double sx[2] = {0.0, 0.0}, sy[2] = {0.0, 0.0};
@@ -1982,6 +2016,7 @@ static int column_pass(fmp_precond* p, bool inv, const double* src, double* dst,
     a.alpha = p->d.alpha;
     a.et = p->et;
     a.interleave = getenv_flag("FMP_COL_CONTIG") ? 0 : 1;
+    a.no_rem = getenv_flag("FMP_COL_NO_REM") ? 1 : 0;
     a.maps = p->d_colmaps ? p->d_colmaps + (src == p->d.work_a ? 0 : p->d.n_sub) : nullptr;
     if (a.maps && src != p->d.work_a && src != p->d.work_b) a.maps = nullptr;
     if (inv && getenv_flag("FMP_COL_SINGLE")) {
