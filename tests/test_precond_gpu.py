@@ -110,7 +110,8 @@ def test_ras_device_tensor_path_and_no_aliasing():
     assert not prec.apply(torch.zeros_like(r)).any()
 
 
-@pytest.mark.parametrize("gext,grid", [((32, 32, 32), (2, 2, 2)), ((48, 32, 32), (3, 2, 2)), ((16, 16, 16), (1, 1, 1))])
+@pytest.mark.parametrize("gext,grid", [((32, 32, 32), (2, 2, 2)), ((48, 32, 32), (3, 2, 2)), ((16, 16, 16), (1, 1, 1)),
+                                       ((64, 64, 64), (2, 2, 2))])
 def test_fast_and_general_paths_agree(gext, grid, monkeypatch):
     """The warp-independent fast kernels (<= 2 distinct extents <= 36) and the general
     CTA-synchronous kernels compute the same preconditioner."""
@@ -202,3 +203,17 @@ def test_column_tile_paths_bitwise(gext, grid, monkeypatch):
     monkeypatch.setenv("FMP_PLANE_CONTIG", "1")
     z2 = RasPreconditioner(part, 0.25, tr).apply(r)
     assert torch.equal(z0, z1) and torch.equal(z0, z2)
+
+
+def test_column_remainder_rows_match_dmma_tile(monkeypatch):
+    """Forward column pass on 33/34-point columns: the DFMA remainder rows (default) and the
+    fifth DMMA row tile (FMP_COL_NO_REM) agree to rounding."""
+    from paper_2508_07193_b200 import Box, RasPreconditioner, make_partition, make_transport
+    part = make_partition(Box(96, 64, 64), (3, 2, 2), 1)   # extents 33 and 34
+    tr = make_transport("cuda")
+    r = torch.from_numpy(np.random.default_rng(13).uniform(-1, 1, part.global_box.dof)).cuda().view(
+        part.global_box.shape4)
+    z0 = RasPreconditioner(part, 0.25, tr).apply(r)
+    monkeypatch.setenv("FMP_COL_NO_REM", "1")
+    z1 = RasPreconditioner(part, 0.25, tr).apply(r)
+    assert rel(z0.cpu().numpy(), z1.cpu().numpy()) <= 1e-14
