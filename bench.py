@@ -138,7 +138,7 @@ class ClockSampler:
 
 # ----------------------------------------------------------------------------------- ours
 INT8_PROBE_FILE = ROOT / "profiles" / "r01_umma_i8_rate.json"
-NCU_TRAFFIC_FILE = ROOT / "profiles" / "r01_v31_ncu_traffic.json"
+NCU_TRAFFIC_FILE = ROOT / "profiles" / "r01_v36_ncu_traffic.json"
 # bench stage -> ncu kernel name(s) whose DRAM bytes (one ncu --set full capture) it covers
 STAGE_KERNELS = {"plane_fwd": ["k_plane_fast<0, 5>"], "column_fwd": ["k_column_fast_db<0, 12, 5, 2>"],
                  "faces": ["k_faces<5, 2, 5>"], "slice_y": ["k_ozaki_slice_rows", "k_ozaki_exp", "k_ozaki_digits"], "gemm": ["k_ozaki"],
@@ -171,7 +171,7 @@ def dominant_roofline(stages: dict) -> dict | None:
             "op_type": "int8 multiply-add = 2 ops", "bound": "tensor", "achieved": g["int8_tops"],
             "peak": g["peak_int8_tops"], "unit": "TFLOP/s", "frac": g["frac"], "traffic": g.get("traffic_bytes"),
             "time_ms": g["ms"], "peak_source": g["peak_source"],
-            "traffic_source": "ncu --set full, dram__bytes_read.sum + dram__bytes_write.sum (profiles/r01_v31_ncu_traffic.json)"}
+            "traffic_source": "ncu --set full, dram__bytes_read.sum + dram__bytes_write.sum (profiles/r01_v36_ncu_traffic.json)"}
 
 
 def stage_rooflines(prec, x, z, specs, peaks, reps):
@@ -416,7 +416,7 @@ def run_ours(args):
                      if peaks["fp64_tflops"] else None,
                      "traffic": (sum(v.get("traffic_bytes", 0) for v in stages.values()) or None),
                      "traffic_note": "DRAM bytes per apply, sum over its kernels from one ncu --set full capture "
-                                     "(profiles/r01_v31_ncu_traffic.json); algorithmic bytes "
+                                     "(profiles/r01_v36_ncu_traffic.json); algorithmic bytes "
                                      f"{bytes_alg} (precond_apply.algorithmic_bytes)",
                      "peak_source": peaks["fp64_source"], "flops_per_launch": flops_exec},
         "breakdown_ms": breakdown,
