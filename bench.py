@@ -162,7 +162,7 @@ def int8_peak_tops() -> tuple[float, str]:
 
 def dominant_roofline(stages: dict) -> dict | None:
     """Roofline of the dominant single kernel of the step: the Ozaki Woodbury GEMM (k_ozaki, ~19%
-    of the step, profiles/r01_v24_launches_step_summary.txt). Algorithmic work = 28 int8 slice
+    of the step, profiles/r01_v36_launches_step_summary.txt). Algorithmic work = 28 int8 slice
     products x 2 m^2 n (unpadded) per launch; peak = the measured tcgen05 kind::i8 rate."""
     g = stages.get("gemm", {})
     if "int8_tops" not in g:
