@@ -60,10 +60,15 @@ int64_t fmp_launch_count(void);
  * y = x + alpha*(C_b C_f x + Lambda x) with boundary=1, the corrected operator
  *   ref: pkg/src/flashmp/operators.py:167-175 (apply_operator) and the CSR blocks of
  *   DistributedOperator.apply, ref: pkg/src/flashmp/schwarz.py:377-388;
- * boundary=0 drops Lambda (ref: operators.py:172-173, with_boundary=False).
+ * boundary is a bit set: FMP_STENCIL_LAMBDA (1) includes Lambda; without it Lambda is dropped
+ *   (ref: operators.py:172-173, with_boundary=False); FMP_STENCIL_NO_IDENTITY (2) drops the
+ *   identity, y = alpha*(C_b C_f [+ Lambda]) x, so boundary=2 with alpha=1 is the double curl
+ *   M x itself (ref: operators.py:128-131, apply_double_curl).
  * mode: 0 = y only; 1 = y and dots[0] = (y, w); 2 = y, dots[0] = (y, w), dots[1] = (y, y);
  *       3 = no y: dots[0] = ||w - A x||^2   (the true-residual check, ref: krylov.py:139-143).
  * dots is a device pointer to >= 2 doubles; scratch has fmp_reduce_scratch_doubles(). */
+#define FMP_STENCIL_LAMBDA 1
+#define FMP_STENCIL_NO_IDENTITY 2
 int fmp_stencil_apply(const fmp_block* blk, double alpha, int boundary, int mode,
                       const double* x, double* y, const double* w,
                       double* dots, double* scratch, void* stream);

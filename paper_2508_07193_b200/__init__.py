@@ -17,6 +17,7 @@ from .schwarz import (BlockLayout, CommunicationError, DistributedOperator, Exch
 from .krylov import SolveReport, SolverConfig, bicgstab, gmres, reduce_dot
 from .cn_driver import CnSolver, DeviceCnStepper, EmState, HostStepPipeline, StepFailure, build_rhs, cn_step
 from .instrument import BREAKDOWN_CATEGORIES, FlopCounter, NullTimer, PhaseTimer
+from ._lib import FlashMPError
 from . import reports
 
 __version__ = "0.1.0"

@@ -1653,10 +1653,11 @@ struct fmp_precond {
   int2* d_fcol = nullptr;
   int n_ffwd = 0, n_finv = 0, n_fcol = 0;
   CUtensorMap* d_colmaps = nullptr;       // column tiles by TMA: [work_a maps | work_b maps], one per subdomain
-  // Woodbury GEMM: own DMMA kernel (default) or cuBLAS (FMP_GEMM=cublas)
-  bool use_cublas = true;
-  // Ozaki INT8 tensor-core GEMM (FMP_GEMM=ozaki): int8 slices of C^-1 built once, Y sliced per apply
-  bool use_ozaki = false;
+  // Woodbury GEMM (set at plan creation from FMP_GEMM): Ozaki INT8 tensor-core GEMM (default,
+  // "ozaki": int8 slices of C^-1 built once, Y sliced per apply), the own DMMA kernel ("own") or
+  // cuBLAS DGEMM ("cublas")
+  bool use_cublas = false;
+  bool use_ozaki = true;
   std::vector<int8_t*> oz_a, oz_b;
   std::vector<int*> oz_ea, oz_eb;
   OzShape* d_ozshapes = nullptr;

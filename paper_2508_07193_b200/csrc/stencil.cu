@@ -120,13 +120,15 @@ __global__ void __launch_bounds__(TX* TY) k_spmv(Geo g, double alpha, int bnd, c
 #undef EX
 #undef EY
 #undef EZ
-      if (!bnd) {
+      if (!(bnd & FMP_STENCIL_LAMBDA)) {
         const int gk = g.gz0 + k;
         tx -= ((gj == 0) + (gk == 0)) * ex;
         ty -= ((gi == 0) + (gk == 0)) * ey;
         tz -= ((gi == 0) + (gj == 0)) * ez;
       }
-      const double yx = ex + alpha * tx, yy = ey + alpha * ty, yz = ez + alpha * tz;
+      const bool id = !(bnd & FMP_STENCIL_NO_IDENTITY);
+      const double yx = id ? ex + alpha * tx : alpha * tx, yy = id ? ey + alpha * ty : alpha * ty,
+                   yz = id ? ez + alpha * tz : alpha * tz;
       const int64_t oi = fidx(g, 0, k, j, i);
       if (MODE == 3) {
         const double rx = w[oi] - yx, ry = w[oi + V] - yy, rz = w[oi + 2 * V] - yz;
@@ -340,13 +342,15 @@ __global__ void __launch_bounds__(STHREADS, SNSLOT <= 4 ? 3 : 2) k_spmv_bulk(con
         pq[hx] = ez_ip;
         pr[hx] = ez_jp;
         if (i >= g.bx || j >= g.by) continue;
-        if (!A.bnd) {
+        if (!(A.bnd & FMP_STENCIL_LAMBDA)) {
           const int gi = g.gx0 + i, gj = g.gy0 + j, gk = g.gz0 + k;
           tx -= ((gj == 0) + (gk == 0)) * ex;
           ty -= ((gi == 0) + (gk == 0)) * ey;
           tz -= ((gi == 0) + (gj == 0)) * ez;
         }
-        const double yx = ex + A.alpha * tx, yy = ey + A.alpha * ty, yz = ez + A.alpha * tz;
+        const bool id = !(A.bnd & FMP_STENCIL_NO_IDENTITY);
+        const double yx = id ? ex + A.alpha * tx : A.alpha * tx, yy = id ? ey + A.alpha * ty : A.alpha * ty,
+                     yz = id ? ez + A.alpha * tz : A.alpha * tz;
         const int64_t oi = fidx(g, 0, k, j, i);
         if (MODE == 3) {
           const double rx = A.w[oi] - yx, ry = A.w[oi + V] - yy, rz = A.w[oi + 2 * V] - yz;
@@ -515,11 +519,18 @@ extern "C" int fmp_stencil_apply(const fmp_block* blk, double alpha, int boundar
                                  double* y, const double* w, double* dots, double* scratch, void* stream) {
   if (int e = check_block(blk)) return e;
   FMP_REQUIRE(mode >= 0 && mode <= 3, "bad stencil mode %d", mode);
+  FMP_REQUIRE(boundary >= 0 && boundary <= 3, "bad stencil boundary flags %d", boundary);
   FMP_REQUIRE(mode == 0 || (w && dots && scratch), "mode %d needs w, dots and scratch", mode);
   const Geo g = make_geo(blk);
   cudaStream_t st = as_stream(stream);
   if (bulk_ok(blk, x)) {
-    static int resident4 = 0, resident6 = 0;
+    // the smem attribute and the occupancy are per device: set them once on each device used
+    static int resident4s[64] = {}, resident6s[64] = {};
+    int cur = 0;
+    FMP_CHECK_CUDA(cudaGetDevice(&cur));
+    FMP_REQUIRE(cur < 64, "device index %d out of range", cur);
+    int& resident4 = resident4s[cur];
+    int& resident6 = resident6s[cur];
     if (!resident4) {
 #define FMP_SPMV_ATTR(M, N)                                                                            \
   FMP_CHECK_CUDA(cudaFuncSetAttribute(k_spmv_bulk<M, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, \

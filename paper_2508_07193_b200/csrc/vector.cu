@@ -126,7 +126,9 @@ struct CombineArgs {
   double c[kCombineMax];
   int k;
 };
-__global__ void k_combine(int64_t n, const double* __restrict__ x, const CombineArgs A, double* __restrict__ out) {
+// x and out alias for every chunk after the first (fmp_vec_combine, k > kCombineMax): no
+// __restrict__ on them; each element is read before it is written by the same thread.
+__global__ void k_combine(int64_t n, const double* x, const CombineArgs A, double* out) {
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x) {
     double t = x[q];
     for (int i = 0; i < A.k; ++i) t = add_rn(t, mul_rn(A.c[i], A.v[i][q]));

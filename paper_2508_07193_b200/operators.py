@@ -41,6 +41,8 @@ def _to_device(E, box: Box) -> torch.Tensor:
         if tuple(E.shape) != box.shape4 and E.numel() != box.dof:
             raise ValueError(f"tensor of {tuple(E.shape)} does not match box {box.extents}")
         _lib.require_cuda()
+        if not E.is_cuda or E.dtype != torch.float64:
+            raise _lib.FlashMPError("device fields must be float64 CUDA tensors (host data: pass a FieldVector)")
         return E.reshape(box.shape4).contiguous()
     raise TypeError(f"unsupported field type {type(E)!r}")
 
@@ -49,13 +51,19 @@ def _like_input(E, box: Box, out: torch.Tensor):
     return FieldVector(box, out.cpu().numpy().ravel()) if isinstance(E, FieldVector) else out
 
 
-def stencil_apply(x: torch.Tensor, alpha: float, with_boundary: bool = True, blk=None) -> torch.Tensor:
-    """y = A x on a device block (single-GPU block covers the global box)."""
+FMP_STENCIL_LAMBDA, FMP_STENCIL_NO_IDENTITY = 1, 2   # fmp_stencil_apply boundary flags
+
+
+def stencil_apply(x: torch.Tensor, alpha: float, with_boundary: bool = True, blk=None,
+                  identity: bool = True) -> torch.Tensor:
+    """y = A x on a device block (single-GPU block covers the global box); identity=False
+    gives y = alpha (C_b C_f [+ Lambda]) x."""
     if blk is None:
         blk = block_struct(x.shape[3], x.shape[2], x.shape[1])
     y = torch.empty_like(x)
-    _lib.call("fmp_stencil_apply", _lib.ref(blk), float(alpha), int(with_boundary), 0,
-              x.data_ptr(), y.data_ptr(), None, None, None, _lib.stream())
+    flags = (FMP_STENCIL_LAMBDA if with_boundary else 0) | (0 if identity else FMP_STENCIL_NO_IDENTITY)
+    _lib.call("fmp_stencil_apply", _lib.ref(blk), float(alpha), flags, 0,
+              _lib.ptr(x), _lib.ptr(y), None, None, None, _lib.stream())
     return y
 
 
@@ -73,15 +81,15 @@ def apply_curl(kind: str, E):
     x = _to_device(E, box)
     out = torch.empty_like(x)
     blk = block_struct(*box.extents)
-    _lib.call("fmp_curl", _lib.ref(blk), 0 if kind == "forward" else 1, x.data_ptr(), out.data_ptr(),
+    _lib.call("fmp_curl", _lib.ref(blk), 0 if kind == "forward" else 1, _lib.ptr(x), _lib.ptr(out),
               _lib.stream())
     return _like_input(E, box, out)
 
 
 def apply_double_curl(E):
-    """C_b C_f E (ref:operators.py:128-131) = (A0 E - E) / alpha evaluated with alpha = 1."""
+    """C_b C_f E (ref:operators.py:128-131): the stencil without the identity and Lambda, alpha = 1,
+    so M E is formed directly (no cancellation against E)."""
     box = E.box if isinstance(E, FieldVector) else Box(E.shape[-1], E.shape[-2], E.shape[-3])
     x = _to_device(E, box)
-    out = stencil_apply(x, 1.0, with_boundary=False)
-    out.sub_(x)
+    out = stencil_apply(x, 1.0, with_boundary=False, identity=False)
     return _like_input(E, box, out)

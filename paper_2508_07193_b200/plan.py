@@ -10,6 +10,7 @@ by the plan; the C library only sees their addresses.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -154,6 +155,7 @@ class SolvePlan:
     def __init__(self, subs: list[SubSpec], alpha: float, device, cinv: dict | None = None,
                  need_woodbury: bool = True, share_rotations: bool = True):
         _lib.lib()
+        self._gemm = os.environ.get("FMP_GEMM", "ozaki")   # read by fmp_precond_create below
         self.device = torch.device(device)
         self.alpha = float(alpha)
         shapes: list[tuple[int, int, int]] = []
@@ -269,6 +271,10 @@ class SolvePlan:
         _lib.check(_lib.lib().fmp_precond_apply(self._handle, C.byref(blk), mode, _lib.ptr(r),
                                                 _lib.ptr(z) if z is not None else None, _lib.stream()),
                    "fmp_precond_apply")
+
+    def gemm_kind(self) -> str:
+        """Woodbury GEMM this plan was created with: 'ozaki' (default), 'own' or 'cublas'."""
+        return self._gemm
 
     STAGES = ("plane_fwd", "column_fwd", "faces", "slice_y", "gemm", "corr", "column_inv", "plane_inv")
 

@@ -480,7 +480,7 @@ class RasPreconditioner:
     owned tiles straight into the output block."""
 
     def __init__(self, partition: Partition, alpha: float, transport, timer=NULL_TIMER,
-                 record_trace: bool = False):
+                 record_trace: bool = False, share_rotations: bool = True):
         self.partition = partition
         self.alpha = float(alpha)
         self.timer = timer
@@ -492,13 +492,15 @@ class RasPreconditioner:
         cinv = {}
         if self.alpha != 0.0:
             # C^-1 only for the canonical shape of each rotation group (plan.rotation_groups)
+            # (every shape's own C^-1 with share_rotations=False: the unshared reference layout)
             shapes = list(dict.fromkeys(s.ext for s in specs))
             for (g, _), e in zip(rotation_groups(shapes), shapes):
-                if g == shapes.index(e):
+                if g == shapes.index(e) or not share_rotations:
                     data = solver_data_for(Box(*e), self.alpha, dev)
                     self.solvers[e] = data
                     cinv[e] = data.corr.padded
-        self.plan = SolvePlan(specs, self.alpha, dev, cinv=cinv) if self.alpha != 0.0 else None
+        self.plan = SolvePlan(specs, self.alpha, dev, cinv=cinv, share_rotations=share_rotations) \
+            if self.alpha != 0.0 else None
 
     def apply_into(self, r: torch.Tensor, z: torch.Tensor) -> torch.Tensor:
         with self.timer.phase("asm_comm"):
@@ -545,10 +547,10 @@ class DistributedOperator:
         with self.timer.phase("p2p"):
             self.exchanger.exchange(x)
         blk = self.exchanger.block_struct()
-        dots = self._host.ptr() if self._host is not None else self._dots.data_ptr()
+        dots = self._host.ptr() if self._host is not None else _lib.ptr(self._dots)
         with self.timer.phase("spmv"):
             _lib.call("fmp_stencil_apply", _lib.ref(blk), self.alpha, int(self.with_boundary), mode,
-                      x.data_ptr(), _lib.ptr(y), _lib.ptr(w), dots, self._scratch.data_ptr(), _lib.stream())
+                      _lib.ptr(x), _lib.ptr(y), _lib.ptr(w), dots, _lib.ptr(self._scratch), _lib.stream())
 
     def _reduced(self, n: int) -> list[float]:
         with self.timer.phase("reduction"):

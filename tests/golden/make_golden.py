@@ -7,7 +7,11 @@ Run in the build container (where /root/reference exists):
 The reference is imported read-only from /root/reference/pkg/src; nothing is
 copied.  Outputs are small .npz files next to this script.  `--big` also runs
 BASELINE configs 1 and 2 (32^3 single subdomain CN step; 64^3 2x2x2 of 32^3),
-which take a few minutes because of the reference's CPU precompute.
+which take a few minutes because of the reference's CPU precompute.  `--huge`
+runs the benchmarked configuration itself (256^3, 8x8x8 subdomains of 32^3:
+RAS apply, BiCGSTAB solve and one CN step), a 96^3 3x3x3 partition whose
+extended boxes include every rotated (34,33,33)-type shape, and the 16^3-subdomain
+config-5 case (64^3, 4x4x4), about 25 minutes on 8 cores; outputs are sampled.
 
 The GPU box has no /root/reference: tests there only read these fixtures.
 """
@@ -227,7 +231,78 @@ def gen_reports():
         shutil.copy(Path(tmp) / "cn_steps.csv", d / "run_cn_steps.csv")
 
 
+def gen_huge():
+    """Reference runs at the benchmarked sizes (ref cli.py:98-136 solve mode, cli.py:139-182 CN).
+
+    Everything is sampled (SAMPLE indices from default_rng(0)) plus the 2-norm and the
+    per-(component, z-plane) sums of each field, so the fixture stays small while the GPU test
+    still sees every subdomain's contribution."""
+    out = {}
+
+    def put(tag, vec, box):
+        idx = np.random.default_rng(0).choice(vec.size, SAMPLE, replace=False)
+        out[f"idx_{tag}"] = idx
+        out[f"s_{tag}"] = vec[idx]
+        out[f"norm_{tag}"] = np.array([np.linalg.norm(vec)])
+        out[f"zsum_{tag}"] = vec.reshape(3, box.nz, box.ny * box.nx).sum(axis=2)
+
+    alpha = 0.25
+    cases = [((96, 96, 96), (3, 3, 3), "bicgstab", True),
+             ((64, 64, 64), (4, 4, 4), "bicgstab", False),
+             ((64, 64, 64), (4, 4, 4), "gmres", False),
+             ((256, 256, 256), (8, 8, 8), "bicgstab", True)]
+    for gext, grid, method, full in cases:
+        gbox = rgrid.Box(*gext)
+        tag = "_".join(map(str, gext)) + "_g" + "".join(map(str, grid)) + f"_{method}"
+        part = rsw.make_partition(gbox, grid, 1)
+        tr = rsw.SerialTransport()
+        t0 = time.perf_counter()
+        op = rsw.DistributedOperator(part, alpha, tr)
+        prec = rsw.RasPreconditioner(part, alpha, tr)
+        if full:
+            r = rng_field(gbox, 3)
+            ras = rsw.gather_field(part, prec.apply(rsw.scatter_field(part, r)))
+            put(f"ras_{tag}", ras, gbox)
+            del ras, r
+        print(f"{tag}: setup+ras {time.perf_counter() - t0:.1f}s", flush=True)
+        x0 = np.random.default_rng(42).uniform(-1.0, 1.0, gbox.dof)   # ref:cli.py:98-102
+        b = op.apply(rsw.scatter_field(part, x0))
+        del x0
+        cfg = rkr.SolverConfig(method=method)
+        runner = rkr.bicgstab if method == "bicgstab" else rkr.gmres
+        t0 = time.perf_counter()
+        x, rep = runner(op, prec, b, cfg)
+        sec = time.perf_counter() - t0
+        out[f"relres_{tag}"] = np.array([t[1] for t in rep.trace])
+        out[f"meta_{tag}"] = np.array([rep.iterations, int(rep.converged)])
+        out[f"seconds_{tag}"] = np.array([sec])
+        put(f"x_{tag}", rsw.gather_field(part, x), gbox)
+        print(f"{tag}: it={rep.iterations} conv={rep.converged} {sec:.1f}s "
+              f"trace={[f'{t[1]:.3e}' for t in rep.trace]}", flush=True)
+        del x, b
+        if full and gext[0] == 256:
+            rng = np.random.default_rng(42)                       # ref:cli.py:143-149
+            E = rgrid.FieldVector(gbox, rng.uniform(-1.0, 1.0, gbox.dof))
+            H = rgrid.FieldVector(gbox, rng.uniform(-1.0, 1.0, gbox.dof))
+            state = rcn.EmState(E, H, 0, 2.0 * np.sqrt(alpha))
+            solver = rcn.CnSolver(gbox, grid, 1, alpha, rkr.SolverConfig(), tr)
+            t0 = time.perf_counter()
+            new, rep = rcn.cn_step(state, solver)
+            sec = time.perf_counter() - t0
+            ctag = f"cn_{tag}"
+            out[f"relres_{ctag}"] = np.array([t[1] for t in rep.trace])
+            out[f"meta_{ctag}"] = np.array([rep.iterations, int(rep.converged)])
+            out[f"seconds_{ctag}"] = np.array([sec])
+            put(f"E1_{ctag}", new.E.data, gbox)
+            put(f"H1_{ctag}", new.H.data, gbox)
+            print(f"{ctag}: it={rep.iterations} {sec:.1f}s", flush=True)
+        np.savez_compressed(OUT / "huge.npz", **out)
+
+
 if __name__ == "__main__":
+    if "--huge" in sys.argv:
+        gen_huge()
+        sys.exit(0)
     big = "--big" in sys.argv
     if not big:
         gen_svd()

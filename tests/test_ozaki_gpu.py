@@ -50,3 +50,41 @@ def test_ozaki_solver_parity_small(case, monkeypatch):
     g = np.load(GOLDEN / "krylov.npz")
     x, rep = K.run(*case)
     K.check(rep, x, g, K.tag_of(*case))
+
+
+@pytest.mark.parametrize("gext,grid", [((256, 256, 256), (8, 8, 8)), ((66, 66, 66), (1, 1, 1))])
+def test_ozaki_elementwise_vs_dgemm(gext, grid):
+    """Per-element accuracy of the Ozaki Z = C^-1 Y on the REAL Y of an apply: the cfg4 block
+    (4 rotation groups, m = 6834 for the 34^3 group, 216 columns) and one 66^3 subdomain
+    (m = 25,938: the K-split form, two int32 parts added in FP64), against cuBLAS DGEMM on the
+    same operands.  Row/column power-of-two scaling keeps each entry to 2^-53 of its row's
+    (column's) maximum, so the bound is per element:
+        |dZ_ij| <= 2^-52 (max_k|C_ik| ||Y_j||_1 + max_k|Y_kj| ||C_i||_1) + m 2^-53 (|C||Y|)_ij
+    (the last term is DGEMM's own rounding), and normwise ||dZ||_F <= 1e-14 ||Z||_F."""
+    from paper_2508_07193_b200 import Box, RasPreconditioner, make_partition, make_transport
+    part = make_partition(Box(*gext), grid, 1)
+    prec = RasPreconditioner(part, 0.25, make_transport("cuda"))
+    assert prec.plan.gemm_kind() == "ozaki"
+    gbox = part.global_box
+    r = torch.from_numpy(np.random.default_rng(16).uniform(-1, 1, gbox.dof)).cuda().view(gbox.shape4)
+    prec.apply(r)
+    torch.cuda.synchronize()
+    plan = prec.plan
+    worst = 0.0
+    for q, (gi, _) in enumerate(plan.groups):
+        if gi != q:
+            continue
+        m, ncol = plan.m[q], plan.gcols[q]
+        Y, Z, Ci = plan.ymat[q][:ncol, :m], plan.zmat[q][:ncol, :m], plan.cinv[q][:, :m]
+        Zref = Y @ Ci.T                                # cuBLAS DGEMM, FP64
+        dZ = (Z - Zref).abs()
+        Ca, Ya = Ci.abs(), Y.abs()
+        bound = 2.0 ** -52 * (Ya.sum(1)[:, None] * Ca.amax(1)[None, :] + Ya.amax(1)[:, None] * Ca.sum(1)[None, :])
+        bound += m * 2.0 ** -53 * (Ya @ Ca.T)
+        ratio = float((dZ / bound).max())
+        nrm = float(torch.linalg.norm(Z - Zref) / torch.linalg.norm(Zref))
+        print(f"group {plan.shapes[q]} m={m} cols={ncol}: max |dZ|/bound {ratio:.3f}, normwise {nrm:.2e}")
+        assert ratio <= 1.0
+        assert nrm <= 1e-14
+        worst = max(worst, ratio)
+    assert worst > 0.0   # the comparison actually ran on nonzero differences or bounds

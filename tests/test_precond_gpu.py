@@ -131,7 +131,8 @@ def test_fast_and_general_paths_agree(gext, grid, monkeypatch):
 
 
 def test_own_gemm_matches_cublas(monkeypatch):
-    """The DMMA Woodbury GEMM (default) and cuBLAS DGEMM (FMP_GEMM=cublas) agree."""
+    """The own DMMA Woodbury GEMM (FMP_GEMM=own) and cuBLAS DGEMM (FMP_GEMM=cublas) agree (the
+    default Ozaki GEMM is checked against both in test_ozaki_gpu.py)."""
     from paper_2508_07193_b200 import Box, RasPreconditioner, make_partition, make_transport
     part = make_partition(Box(48, 32, 32), (3, 2, 2), 1)   # 3 shapes, n_s = 4 / 2 / ... columns
     tr = make_transport("cuda")
