@@ -11,7 +11,8 @@ _proc_grid_for(N).  value = 3 * global grid points / step seconds / 1e6 (MDoF/s,
 reference's definition ref:cli.py:41,84-85) over all N GPUs.
 
 Rank 0 prints ONE JSON line.  --impl reference times the CPU reference algorithm (the
-numpy oracle port, oracle/flashmp_oracle.py) on the host cores instead.
+numpy oracle port, oracle/flashmp_oracle.py) on the host cores instead: real CN steps on a
+bounded sample grid (CPU_SAMPLE, same subdomains and tolerances).
 """
 
 from __future__ import annotations
@@ -425,7 +426,7 @@ def run_ours(args):
         "e2e": e2e,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(gext, sub, overlap, iters, budget_s=args.cpu_budget)
+        line["cpu_baseline"] = cpu_baseline(args.config, steps=args.cpu_steps)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -434,77 +435,70 @@ def run_ours(args):
 
 
 # ----------------------------------------------------------------------------------- CPU reference
-def cpu_sample(gext, sub, overlap, iters_per_step, budget_s=20.0):
-    """Time the CPU reference algorithm (oracle port, numpy/OpenBLAS, all host threads) on a
-    bounded sample of one CN step at the full workload and compose the per-step time:
-        step = rhs + H update + iters * (2 * sum_subdomains solve + 3 * SpMV + vector ops)
-    Sample: one global SpMV, one global RHS, one Woodbury solve per distinct extended shape
-    (timing-only C^-1: a random symmetric matrix of the true size m; the reference's own
-    precompute takes 38-55 s per shape and is excluded from its solve time anyway), and the
-    BiCGSTAB vector updates on full-size vectors."""
-    sys.path.insert(0, str(ROOT / "oracle"))
-    import flashmp_oracle as O
-    t_start = time.perf_counter()
-    rng = np.random.default_rng(0)
-    shape = (3, gext[2], gext[1], gext[0])
-    E = rng.uniform(-1, 1, shape)
-    H = rng.uniform(-1, 1, shape)
-    t0 = time.perf_counter()
-    R = O.build_rhs(E, H, 1.0)
-    t_rhs = time.perf_counter() - t0
-    t0 = time.perf_counter()
-    O.apply_A(0.25, E, True)
-    t_spmv = time.perf_counter() - t0
-    t0 = time.perf_counter()
-    _ = H - 0.5 * (O.curl("forward", E) + O.curl("forward", R))
-    t_h = time.perf_counter() - t0
-    # vector ops of one BiCGSTAB iteration: 6 axpy-type + 4 dots + true-residual lincomb/norm
-    a, b = E.ravel(), H.ravel()
-    t_vec_unit = math.inf
-    for _ in range(2):
+# The reference is pure Python (numpy/scipy), so "the reference's own CPU implementation" is the
+# numpy restatement oracle/flashmp_oracle.py (the reference cannot travel to the GPU box).  It is
+# timed on REAL CN steps (RHS -> BiCGSTAB to 1e-12 with the real Woodbury C^-1 -> H update,
+# ref:cn_driver.py:82-94, cli.py:139-182) on a bounded sample of the workload: the same 32^3
+# subdomains, alpha, overlap and tolerance on a smaller grid (CPU_SAMPLE), so a step takes a few
+# seconds on the host cores.  Precompute (C^-1 per extended shape) is setup, outside the timed
+# region, as in the reference's own cn_steps.csv seconds (ref:cli.py:164-171).
+CPU_SAMPLE = {"cfg4": ((128, 128, 128), (32, 32, 32)), "cfg2": ((64, 64, 64), (32, 32, 32)),
+              "cfg1": ((32, 32, 32), (32, 32, 32))}
+
+
+class CpuCnSample:
+    """Real CN steps of the CPU reference algorithm (oracle port) on the sample grid."""
+
+    def __init__(self, config: str, seed: int = 42):
+        sys.path.insert(0, str(ROOT / "oracle"))
+        import flashmp_oracle as O
+        self.O = O
+        self.gext, sub = CPU_SAMPLE[config]
+        self.grid = tuple(n // s for n, s in zip(self.gext, sub))
+        self.alpha = 0.25
+        self.dt = 2.0 * math.sqrt(self.alpha)      # ref:cli.py:145
+        self.ranks = O.partition(self.gext, self.grid, 1)
         t0 = time.perf_counter()
-        c = 1.0 * a + 0.5 * b
-        d = float(a @ b)
-        t_vec_unit = min(t_vec_unit, time.perf_counter() - t0)
-    t_vec = 7 * t_vec_unit
-    del c, d
-    ranks = O.partition(tuple(gext), tuple(n // s for n, s in zip(gext, sub)), overlap)
-    census: dict = {}
-    for r in ranks:
-        census[r.ext] = census.get(r.ext, 0) + 1
-    t_solve_total = 0.0
-    for ext, count in census.items():
-        V = int(np.prod(ext))
-        m = O.correction_size(ext)
-        binv = O.point_block_inverses(ext, 0.25)
-        Cinv = rng.standard_normal((m, m))
-        data = O.SubdomainData(ext, 0.25, binv, *O.correction_rows(ext), Cinv)
-        r = rng.uniform(-1, 1, 3 * V)
-        best = math.inf
-        for _ in range(2):
-            t0 = time.perf_counter()
-            O.solve(data, r)
-            best = min(best, time.perf_counter() - t0)
-        t_solve_total += best * count
-        if time.perf_counter() - t_start > budget_s * 3:
-            break
-    iters = statistics.mean(iters_per_step) if iters_per_step else 4
-    per_iter = 2 * t_solve_total + 3 * t_spmv + t_vec
-    step = t_rhs + t_h + iters * per_iter
-    return step, {"rhs_s": t_rhs, "spmv_s": t_spmv, "h_update_s": t_h, "vector_ops_s": t_vec,
-                  "ras_apply_s": t_solve_total, "iters": iters, "wall_s": time.perf_counter() - t_start,
-                  "shapes": len(census)}
+        for r in self.ranks:                       # C^-1 per distinct extended shape (setup)
+            O.solver_data(r.ext, self.alpha, closed_form=True)
+        self.setup_s = time.perf_counter() - t0
+        rng = np.random.default_rng(seed)          # ref:cli.py:143-149
+        shape = (3, self.gext[2], self.gext[1], self.gext[0])
+        self.E = rng.uniform(-1.0, 1.0, shape)
+        self.H = rng.uniform(-1.0, 1.0, shape)
+        self.dof = 3 * int(np.prod(self.gext))
+        self.iters: list[int] = []
+
+    def step(self) -> float:
+        O, g, a = self.O, self.gext, self.alpha
+        op = lambda u: O.op_apply(g, a, u)
+        prec = lambda u: O.ras_apply(g, self.ranks, a, u)
+
+        def solve(rhs):
+            return O.bicgstab(op, prec, rhs.ravel(), tol=1e-12, max_iter=1000)
+
+        t0 = time.perf_counter()
+        self.E, self.H, rep = O.cn_step(self.E, self.H, self.dt, solve)
+        sec = time.perf_counter() - t0
+        self.iters.append(rep.iterations)
+        return sec
+
+    def describe(self, steps: int) -> str:
+        return (f"oracle/flashmp_oracle.py (numpy restatement of the reference; OpenBLAS threads = host cores): "
+                f"{steps} real CN steps (RHS, BiCGSTAB to 1e-12 with real C^-1, H update; time-marching) on a "
+                f"{'x'.join(map(str, self.gext))} grid of {len(self.ranks)} subdomains of 32^3 (overlap 1, "
+                f"alpha 0.25), measured iterations per step {self.iters}; C^-1 precompute {self.setup_s:.1f} s "
+                f"untimed (setup)")
 
 
-def cpu_baseline(gext, sub, overlap, iters, budget_s=20.0):
-    step, parts = cpu_sample(gext, sub, overlap, iters, budget_s)
-    dof = 3 * int(np.prod(gext))
-    return {"value": round(dof / step / 1e6, 4), "unit": "MDoF/s", "cores": os.cpu_count(), "kind": "port",
-            "sample": "oracle/flashmp_oracle.py (numpy restatement of the reference) on this host: one RHS, one "
-                      "SpMV, one Woodbury solve per extended shape x census, vector ops; composed per step with "
-                      f"the GPU-measured iteration count ({parts['iters']}); parts(s)="
-                      + json.dumps({k: round(v, 3) if isinstance(v, float) else v for k, v in parts.items()}),
-            "step_s": round(step, 3)}
+def cpu_baseline(config: str, steps: int = 2):
+    """Rank-0, N=1 CPU baseline beside our own line: `steps` real CN steps of the sample."""
+    smp = CpuCnSample(config)
+    smp.step()                                    # warm-up (first-touch, BLAS thread pool)
+    times = [smp.step() for _ in range(steps)]
+    sec = statistics.mean(times)
+    return {"value": round(smp.dof / sec / 1e6, 4), "unit": "MDoF/s", "cores": os.cpu_count(), "kind": "port",
+            "sample": smp.describe(steps), "step_s": round(sec, 3), "setup_s": round(smp.setup_s, 1)}
 
 
 def run_reference(args):
@@ -512,31 +506,28 @@ def run_reference(args):
     if rank != 0:
         return
     world = int(os.environ.get("WORLD_SIZE", "1"))
-    from paper_2508_07193_b200.schwarz import proc_grid_for
+    smp = CpuCnSample(args.config)
+    for _ in range(args.warmup):
+        smp.step()
+    smp.iters.clear()
+    t0 = time.perf_counter()
+    times = [smp.step() for _ in range(args.steps)]
+    t_total = time.perf_counter() - t0
+    step = t_total / args.steps
+    value = smp.dof / step / 1e6
     block, sub, overlap = CONFIGS[args.config]
-    ggrid = proc_grid_for(args.gpus)
-    gext = tuple(b * g for b, g in zip(block, ggrid))
-    iters = [4]   # reference CPU iteration count at 256^3 / 512 subdomains (measured)
-    for _ in range(args.warmup if args.warmup <= 1 else 1):
-        pass
-    times = []
-    for _ in range(args.steps):
-        step, parts = cpu_sample(gext, sub, overlap, iters, args.cpu_budget)
-        times.append(step)
-    step = statistics.mean(times)
-    dof = 3 * int(np.prod(gext))
-    value = dof / step / 1e6
     line = {"impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "MDoF/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(step * 1e3, 1),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic U[-1,1) (numpy PCG64 seed 0)",
-            "config": {"workload": f"{args.config}: CN-FDTD step, BiCGSTAB+FlashMP RAS (CPU reference algorithm)",
-                       "global_grid": list(gext), "subdomain": list(sub), "world_launch": world},
+            "data": "synthetic: E,H ~ U[-1,1) (numpy PCG64 seed 42, ref:cli.py:143-149)",
+            "config": {"workload": f"{args.config}: CN-FDTD step, BiCGSTAB+FlashMP RAS, tol 1e-12, alpha 0.25, "
+                                   f"overlap {overlap} (CPU reference algorithm on a bounded sample grid)",
+                       "sample_grid": list(smp.gext), "subdomain": list(sub), "subdomain_grid": list(smp.grid),
+                       "world_launch": world},
+            "iters_per_step": smp.iters, "step_times_s": [round(t, 3) for t in times],
+            "setup_s": round(smp.setup_s, 1),
             "cpu_baseline": {"value": round(value, 4), "unit": "MDoF/s", "cores": os.cpu_count(), "kind": "port",
-                             "sample": "per step: oracle RHS + SpMV + one Woodbury solve per extended shape "
-                                       "(census-weighted) + vector ops, composed with 4 iterations/step; "
-                                       + json.dumps({k: round(v, 3) if isinstance(v, float) else v
-                                                     for k, v in parts.items()})},
+                             "sample": smp.describe(args.steps)},
             "e2e": {"value": round(value, 4), "unit": "MDoF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -550,7 +541,7 @@ def main():
     ap.add_argument("--config", default="cfg4", choices=sorted(CONFIGS))
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-budget", type=float, default=20.0)
+    ap.add_argument("--cpu-steps", type=int, default=2, help="timed CN steps of the CPU baseline sample")
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
                     help="torch.distributed backend for N > 1 (gloo stages through host memory; testing only)")
     args = ap.parse_args()

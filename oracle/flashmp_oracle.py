@@ -224,6 +224,73 @@ def precompute(dims, alpha: float) -> SubdomainData:
     return data
 
 
+def precompute_faces(dims, alpha: float) -> SubdomainData:
+    """The same Woodbury data as `precompute` (ref:subdomain.py:196-215), with C assembled in
+    closed form instead of m exact solves on unit vectors -- setup acceleration for the timed
+    CPU baseline, checked equal to `precompute` in tests/test_oracle.py.
+
+    A unit vector at correction point p = (c, k, j, i) transforms to a rank-one tensor
+    Fz_c[:, k] x Fy_c[:, j] x Fx_c[:, i] in component c; B^-1 couples it into component c'; the
+    inverse transform and the row selection read it back at q = (c', k', j', i').  Correction
+    points lie on the low faces (fixed coordinate 0), so every (component, face) pair of rows
+    and columns is one einsum whose fixed axes contract against one factor row/column:
+        C0[q, p] = sum_{kk,jj,ii} Iz_c'[k', kk] Iy_c'[j', jj] Ix_c'[i', ii] binv[kk,jj,ii,c',c]
+                                  Fz_c[kk, k] Fy_c[jj, j] Fx_c[ii, i]."""
+    dims = tuple(dims)
+    nx, ny, nz = dims
+    binv = point_block_inverses(dims, alpha)
+    data = SubdomainData(dims, alpha, binv)
+    if alpha == 0.0:
+        return data
+    rows, values = correction_rows(dims)
+    m, V = rows.size, nx * ny * nz
+    pos = np.full(3 * V, -1, dtype=np.int64)
+    pos[rows] = np.arange(m)
+    fwd, inv = factors(dims, inverse=False), factors(dims, inverse=True)
+    faces = {0: ("y", "z"), 1: ("x", "z"), 2: ("x", "y")}   # low faces carrying each component's deltas
+    ext = {"x": nx, "y": ny, "z": nz}
+
+    def side(c, fixed, mats, row):
+        """einsum operands / subscripts / point positions of one (component, face) side."""
+        T = dict(zip("xyz", mats[c]))
+        letters = {"z": "KJI"[0], "y": "KJI"[1], "x": "KJI"[2]} if row else {"z": "k", "y": "j", "x": "i"}
+        inner = {"z": "a", "y": "b", "x": "d"}
+        ops, subs, free = [], [], []
+        for ax in "zyx":
+            if ax == fixed:
+                ops.append(T[ax][0, :] if row else T[ax][:, 0])
+                subs.append(inner[ax])
+            else:
+                ops.append(T[ax])
+                subs.append(letters[ax] + inner[ax] if row else inner[ax] + letters[ax])
+                free.append(ax)
+        grids = np.meshgrid(*[np.arange(ext[a]) for a in free], indexing="ij")
+        coord = {a: g.ravel() for a, g in zip(free, grids)}
+        coord[fixed] = np.zeros_like(grids[0].ravel())
+        lin = c * V + coord["z"] * nx * ny + coord["y"] * nx + coord["x"]
+        return ops, subs, "".join(letters[a] for a in free), pos[lin]
+
+    C = np.empty((m, m))
+    for cq in range(3):
+        for fq in faces[cq]:
+            rops, rsubs, rout, rpos = side(cq, fq, inv, True)
+            for cp in range(3):
+                for fp in faces[cp]:
+                    cops, csubs, cout, cpos = side(cp, fp, fwd, False)
+                    spec = ",".join(rsubs + ["abd"] + csubs) + "->" + rout + cout
+                    blk = np.einsum(spec, *rops, binv[:, :, :, cq, cp], *cops, optimize="greedy")
+                    C[np.ix_(rpos, cpos)] = blk.reshape(rpos.size, cpos.size)
+    C[np.diag_indices(m)] += 1.0 / (alpha * values)
+    try:
+        Cinv = np.linalg.inv(C)
+    except np.linalg.LinAlgError as exc:
+        raise DegenerateConfigurationError(str(exc)) from exc
+    if np.abs(C).sum(0).max() * np.abs(Cinv).sum(0).max() > CONDITION_LIMIT:
+        raise DegenerateConfigurationError(f"correction matrix ill-conditioned for {dims}")
+    data.rows, data.values, data.Cinv = rows, values, Cinv
+    return data
+
+
 def solve(data: SubdomainData, r: np.ndarray) -> np.ndarray:
     """Woodbury solve of I + alpha (M + Lambda) (ref:subdomain.py:265-287)."""
     if data.alpha == 0.0:
@@ -309,11 +376,12 @@ def gather(gdims, ranks, parts) -> np.ndarray:
 _CACHE: dict = {}
 
 
-def solver_data(dims, alpha) -> SubdomainData:
-    """Per-(extents, alpha) cache (ref:schwarz.py:295-305)."""
+def solver_data(dims, alpha, closed_form: bool = False) -> SubdomainData:
+    """Per-(extents, alpha) cache (ref:schwarz.py:295-305); closed_form=True builds a missing
+    entry with precompute_faces (same data, faster setup)."""
     key = (tuple(dims), float(alpha))
     if key not in _CACHE:
-        _CACHE[key] = precompute(dims, alpha)
+        _CACHE[key] = (precompute_faces if closed_form else precompute)(dims, alpha)
     return _CACHE[key]
 
 

@@ -91,6 +91,21 @@ def test_subdomain_solves_match_reference(ext, alpha):
         assert np.abs(data.Cinv - g[f"Cinv_{tag}"]).max() <= 1e-12
 
 
+@pytest.mark.parametrize("ext", [(1, 1, 1), (2, 2, 2), (3, 3, 3), (4, 5, 6), (6, 2, 4), (1, 3, 4), (5, 1, 2),
+                                 (9, 8, 7)])
+@pytest.mark.parametrize("alpha", [0.05, 0.25])
+def test_precompute_faces_equals_precompute(ext, alpha):
+    """The closed-form C assembly (bench CPU baseline setup) equals the reference's m exact solves:
+    same rows/values, C^-1 to rounding, and the reference golden C^-1 where one exists."""
+    a, b = O.precompute(ext, alpha), O.precompute_faces(ext, alpha)
+    assert np.array_equal(a.rows, b.rows) and np.array_equal(a.values, b.values)
+    assert np.abs(a.Cinv - b.Cinv).max() <= 1e-14 * max(1.0, np.abs(a.Cinv).max())
+    tag = "_".join(map(str, ext)) + f"_a{alpha}"
+    g = load("subdomain.npz")
+    if f"Cinv_{tag}" in g:
+        assert np.abs(b.Cinv - g[f"Cinv_{tag}"]).max() <= 1e-12
+
+
 SCHWARZ = [((8, 8, 8), (2, 1, 1), 0), ((8, 8, 8), (2, 1, 1), 1), ((8, 8, 4), (2, 2, 1), 1),
            ((12, 8, 8), (3, 2, 2), 2), ((8, 4, 6), (2, 2, 3), 1)]
 
