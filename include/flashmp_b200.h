@@ -73,6 +73,17 @@ int fmp_stencil_apply(const fmp_block* blk, double alpha, int boundary, int mode
                       const double* x, double* y, const double* w,
                       double* dots, double* scratch, void* stream);
 
+/* Split form for overlapping a ghost exchange (multi-GPU): FMP_PART_INTERIOR computes
+ * every point whose stencil reads no neighbour ghost cell (call it while the ghosts are in flight),
+ * FMP_PART_BOUNDARY the rest plus the fused reductions (call it after they landed).  Both parts
+ * together write exactly what fmp_stencil_apply (FMP_PART_ALL) writes, with the same dots. */
+#define FMP_PART_ALL 0
+#define FMP_PART_INTERIOR 1
+#define FMP_PART_BOUNDARY 2
+int fmp_stencil_apply_part(const fmp_block* blk, double alpha, int boundary, int mode, int part,
+                           const double* x, double* y, const double* w,
+                           double* dots, double* scratch, void* stream);
+
 /* out = curl_f(x) (kind 0) or curl_b(x) (kind 1)      ref: operators.py:119-125 */
 int fmp_curl(const fmp_block* blk, int kind, const double* x, double* out, void* stream);
 
@@ -193,6 +204,33 @@ int fmp_precond_destroy(fmp_precond* p);
  *   the shape's Y matrices (z unused). */
 int fmp_precond_apply(fmp_precond* p, const fmp_block* blk, int mode,
                       const double* r, double* z, void* stream);
+
+/* Split form for overlapping a ghost exchange: FMP_PART_INTERIOR runs the work that reads no
+ * neighbour ghost (the forward restriction + x/y transform of the subdomains whose extended boxes
+ * stay inside the block), FMP_PART_BOUNDARY everything else.  Call INTERIOR while the ghosts are
+ * in flight and BOUNDARY after they landed (same stream); together they equal fmp_precond_apply. */
+int fmp_precond_apply_part(fmp_precond* p, const fmp_block* blk, int mode, int part,
+                           const double* r, double* z, void* stream);
+
+/* ---------------------------------------------------------------- halo exchange (K10)
+ * The ghost shell of fmp_block is filled in three phases -- 0: z faces, 1: y faces extended over
+ * the z ghosts, 2: x faces extended over both (edges and corners without diagonal messages);
+ * side 0 = the low face, 1 = the high face.  ref: the Exchanger messages of schwarz.py:217-257.
+ * fmp_halo_slab_doubles: doubles in one slab of the phase (a message is that + 1 tag double).
+ * fmp_halo_pack: out[0..n) = the slab this block sends to its neighbour on `side` (read through
+ *   the ghosts of the earlier phases already set in blk), out[n] = tag.
+ * fmp_halo_unpack: copy a received message (n + 1 doubles) into blk->ghost[slot of phase, side]
+ *   unless `in` already IS that slot, and compare its tag with `tag`: a mismatch (lost or stale
+ *   message) ORs bit (1 << slot) into *status (device-visible, e.g. pinned host memory; may be
+ *   NULL).  Ghost slots must hold n + 1 doubles. */
+#define FMP_HALO_Z 0
+#define FMP_HALO_Y 1
+#define FMP_HALO_X 2
+int64_t fmp_halo_slab_doubles(const fmp_block* blk, int phase);
+int fmp_halo_pack(const fmp_block* blk, int phase, int side, const double* x, double* out,
+                  double tag, void* stream);
+int fmp_halo_unpack(const fmp_block* blk, int phase, int side, const double* in, double tag,
+                    int* status, void* stream);
 
 /* Stage timing (for benchmarks): enable=1 records CUDA events between the kernels of every
  * later fmp_precond_apply on its stream; fmp_precond_stage_ms synchronises on the last apply's

@@ -41,7 +41,15 @@ SIGNATURES = {
     "fmp_precond_profile": (_i, [_p, _i]),
     "fmp_precond_stage_ms": (_i, [_p, C.POINTER(C.c_float), _i]),
     "fmp_debug_ozaki_prof": (_i, [_p, _i]),
+    "fmp_stencil_apply_part": (_i, [_p, _d, _i, _i, _i, _p, _p, _p, _p, _p, _p]),
+    "fmp_precond_apply_part": (_i, [_p, _p, _i, _i, _p, _p, _p]),
+    "fmp_halo_slab_doubles": (_i64, [_p, _i]),
+    "fmp_halo_pack": (_i, [_p, _i, _i, _p, _p, _d, _p]),
+    "fmp_halo_unpack": (_i, [_p, _i, _i, _p, _d, _p, _p]),
 }
+
+FMP_PART_ALL, FMP_PART_INTERIOR, FMP_PART_BOUNDARY = 0, 1, 2
+FMP_HALO_Z, FMP_HALO_Y, FMP_HALO_X = 0, 1, 2
 
 FMP_SOLVE_WOODBURY, FMP_SOLVE_EXACT, FMP_SOLVE_FACES = 0, 1, 2
 

@@ -1652,6 +1652,7 @@ struct fmp_precond {
   int4* d_finv = nullptr;
   int2* d_fcol = nullptr;
   int n_ffwd = 0, n_finv = 0, n_fcol = 0;
+  int n_ffwd_int = 0;                     // forward plane items of subdomains that read no ghost (listed first)
   CUtensorMap* d_colmaps = nullptr;       // column tiles by TMA: [work_a maps | work_b maps], one per subdomain
   // Woodbury GEMM (set at plan creation from FMP_GEMM): Ozaki INT8 tensor-core GEMM (default,
   // "ozaki": int8 slices of C^-1 built once, Y sliced per apply), the own DMMA kernel ("own") or
@@ -1796,17 +1797,27 @@ extern "C" int fmp_precond_create(const fmp_precond_desc* desc, fmp_precond** ou
               p->et.sg[e] = sh.s_off[a];
             }
       }
-      std::vector<int4> ff, fi;
+      std::vector<int4> ff, ffb, fi;
       std::vector<int2> fc;
+      // block extents = the union of the owned tiles; a subdomain whose extended box leaves the
+      // block reads neighbour ghosts (its forward plane items go last, fmp_precond_apply_part)
+      int64_t blk_ext[3] = {0, 0, 0};
+      for (int64_t q = 0; q < desc->n_sub; ++q)
+        for (int a = 0; a < 3; ++a)
+          blk_ext[a] = std::max(blk_ext[a], p->subs[q].ext_lo[a] + p->subs[q].own_off[a] + p->subs[q].own[a]);
       for (int64_t q = 0; q < desc->n_sub; ++q) {
         const auto& sd = p->subs[q];
         const int ez = (int)sd.ext[2], wz = (int)sd.own[2], P = (int)(sd.ext[0] * sd.ext[1]);
+        bool ghost = false;
+        for (int a = 0; a < 3; ++a) ghost = ghost || sd.ext_lo[a] < 0 || sd.ext_lo[a] + sd.ext[a] > blk_ext[a];
         for (int c = 0; c < 3; ++c) {
-          for (int k = 0; k < ez; ++k) ff.push_back(make_int4((int)q, c, k, 1));
+          for (int k = 0; k < ez; ++k) (ghost ? ffb : ff).push_back(make_int4((int)q, c, k, 1));
           for (int k = 0; k < wz; ++k) fi.push_back(make_int4((int)q, c, k, 1));
         }
         for (int p0 = 0; p0 < P; p0 += 8) fc.push_back(make_int2((int)q, p0));
       }
+      p->n_ffwd_int = (int)ff.size();
+      ff.insert(ff.end(), ffb.begin(), ffb.end());
       p->n_ffwd = (int)ff.size();
       p->n_finv = (int)fi.size();
       p->n_fcol = (int)fc.size();
@@ -2065,12 +2076,18 @@ static int column_pass(fmp_precond* p, bool inv, const double* src, double* dst,
 }
 
 static int plane_pass(fmp_precond* p, const fmp_block* blk, bool inv, int mode, const double* src, double* dst,
-                      cudaStream_t st) {
+                      cudaStream_t st, int part = FMP_PART_ALL) {
   if (p->fast) {
     FastPlaneArgs a{};
     a.subs = p->d.subs;
     a.items = inv ? p->d_finv : p->d_ffwd;
     a.n_items = inv ? p->n_finv : p->n_ffwd;
+    if (!inv && part == FMP_PART_INTERIOR) a.n_items = p->n_ffwd_int;
+    if (!inv && part == FMP_PART_BOUNDARY) {
+      a.items += p->n_ffwd_int;
+      a.n_items -= p->n_ffwd_int;
+    }
+    if (a.n_items == 0) return 0;
     a.g = make_geo(blk);
     a.src = src;
     a.dst = dst;
@@ -2125,8 +2142,22 @@ static int plane_pass(fmp_precond* p, const fmp_block* blk, bool inv, int mode, 
   return 0;
 }
 
+static int precond_apply(fmp_precond* p, const fmp_block* blk, int mode, int part, const double* r, double* z,
+                         void* stream);
+
 extern "C" int fmp_precond_apply(fmp_precond* p, const fmp_block* blk, int mode, const double* r, double* z,
                                  void* stream) {
+  return precond_apply(p, blk, mode, FMP_PART_ALL, r, z, stream);
+}
+
+extern "C" int fmp_precond_apply_part(fmp_precond* p, const fmp_block* blk, int mode, int part, const double* r,
+                                      double* z, void* stream) {
+  FMP_REQUIRE(part >= FMP_PART_ALL && part <= FMP_PART_BOUNDARY, "bad part %d", part);
+  return precond_apply(p, blk, mode, part, r, z, stream);
+}
+
+static int precond_apply(fmp_precond* p, const fmp_block* blk, int mode, int part, const double* r, double* z,
+                         void* stream) {
   FMP_REQUIRE(p && blk, "null argument");
   FMP_REQUIRE(mode >= FMP_SOLVE_WOODBURY && mode <= FMP_SOLVE_FACES, "bad solve mode %d", mode);
   cudaStream_t st = as_stream(stream);
@@ -2135,8 +2166,14 @@ extern "C" int fmp_precond_apply(fmp_precond* p, const fmp_block* blk, int mode,
   auto mark = [&](int i) {
     if (p->profile) cudaEventRecord(p->stage_ev[i], st);
   };
-  mark(0);
-  if (int e = plane_pass(p, blk, false, mode, r, wa, st)) return e;
+  // Only the forward plane pass reads the input field (and its ghosts); every later kernel reads
+  // the workspaces.  The interior part is that pass over the subdomains that read no ghost; the
+  // boundary part is the pass over the others and everything after it.  (The general kernels and
+  // FACES mode run whole in the boundary part.)
+  const bool split = p->fast && mode != FMP_SOLVE_FACES;
+  if (part == FMP_PART_INTERIOR) return split ? plane_pass(p, blk, false, mode, r, wa, st, FMP_PART_INTERIOR) : 0;
+  if (part != FMP_PART_BOUNDARY) mark(0);
+  if (int e = plane_pass(p, blk, false, mode, r, wa, st, split ? part : FMP_PART_ALL)) return e;
   mark(1);
   if (int e = column_pass(p, false, wa, wb, nullptr, st)) return e;
   mark(2);

@@ -14,6 +14,9 @@
 #include "tma.cuh"
 #include <algorithm>
 #include <atomic>
+#include <map>
+#include <mutex>
+#include <vector>
 
 namespace fmp {
 
@@ -181,6 +184,8 @@ struct BulkSpmvArgs {
   const double* w;
   double* partials;
   unsigned long long* counter;   // [fetch, done]: dynamic unit scheduler, zero between launches
+  const int* ulist;              // units of this launch (nullptr: all units 0 .. units-1)
+  int64_t nlaunch;               // units handed out by this launch
   double alpha;
   int bnd, tiles_x, tiles_y, L, nzc, ghosts;
 };
@@ -217,8 +222,7 @@ __global__ void __launch_bounds__(STHREADS, SNSLOT <= 4 ? 3 : 2) k_spmv_bulk(con
       unsigned long long f = 0;
       if (lx == 0) f = atomicAdd(A.counter, 1ull);
       f = __shfl_sync(0xffffffffu, f, 0);
-      const int64_t u = (int64_t)f;
-      if (u >= units) {   // tell the consumers: a "unit" of -1 in the next slot
+      if ((int64_t)f >= A.nlaunch) {   // tell the consumers: a "unit" of -1 in the next slot
         const int s = (int)(q % SNSLOT);
         if (q >= SNSLOT) mbar_wait(&empty[s], (uint32_t)(((q / SNSLOT) - 1) & 1));
         if (lx == 0) {
@@ -232,6 +236,7 @@ __global__ void __launch_bounds__(STHREADS, SNSLOT <= 4 ? 3 : 2) k_spmv_bulk(con
         }
         break;
       }
+      const int64_t u = A.ulist ? (int64_t)A.ulist[f] : (int64_t)f;
       const int tile = (int)(u % ntiles), zc = (int)(u / ntiles);
       const int i0 = (tile % A.tiles_x) * SX, j0 = (tile / A.tiles_x) * SY, k0 = zc * A.L;
       const int np = nplanes(u);
@@ -515,8 +520,63 @@ static bool bulk_ok(const fmp_block* b, const double* x) {
          b->by <= ((int64_t)1 << 31) && b->bz <= ((int64_t)1 << 31) && !getenv_flag("FMP_SPMV_LEGACY");
 }
 
+// Units of one part of the SpMV (z-chunk x column tile, in scheduler order): FMP_PART_INTERIOR =
+// units that read no neighbour ghost cell, FMP_PART_BOUNDARY = the others.  A unit covers
+// i in [i0-1, i0+SX], j in [j0-1, j0+SY], k in [k0-1, k0+np]; it reads a ghost slab when that range
+// leaves the block on a side whose ghost pointer is set.  Lists are built once per geometry and
+// kept on the device (one small allocation per distinct (device, block, chunking, ghost mask)).
+static int unit_list(const Geo& g, int tiles_x, int tiles_y, int L, int nzc, int part, const int** out,
+                     int64_t* count) {
+  static std::mutex mu;
+  static std::map<std::vector<int64_t>, std::pair<int*, int64_t>> cache;
+  int dev = 0;
+  FMP_CHECK_CUDA(cudaGetDevice(&dev));
+  int mask = 0;
+  for (int q = 0; q < 6; ++q) mask |= (g.ghost[q] != nullptr) << q;
+  const std::vector<int64_t> key{dev, g.bx, g.by, g.bz, L, nzc, mask, part};
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = cache.find(key);
+  if (it == cache.end()) {
+    std::vector<int> units;
+    const int64_t ntiles = (int64_t)tiles_x * tiles_y;
+    for (int64_t u = 0; u < ntiles * nzc; ++u) {
+      const int tile = (int)(u % ntiles), zc = (int)(u / ntiles);
+      const int i0 = (tile % tiles_x) * SX, j0 = (tile / tiles_x) * SY, k0 = zc * L;
+      const int np = std::min(L, g.bz - k0);
+      const bool ghost = (i0 == 0 && (mask & 1)) || (i0 + SX >= g.bx && (mask & 2)) || (j0 == 0 && (mask & 4)) ||
+                         (j0 + SY >= g.by && (mask & 8)) || (k0 == 0 && (mask & 16)) ||
+                         (k0 + np >= g.bz && (mask & 32));
+      if (ghost == (part == FMP_PART_BOUNDARY)) units.push_back((int)u);
+    }
+    int* d = nullptr;
+    if (!units.empty()) {
+      FMP_CHECK_CUDA(cudaMalloc(&d, units.size() * sizeof(int)));
+      FMP_CHECK_CUDA(cudaMemcpy(d, units.data(), units.size() * sizeof(int), cudaMemcpyHostToDevice));
+    }
+    it = cache.emplace(key, std::make_pair(d, (int64_t)units.size())).first;
+  }
+  *out = it->second.first;
+  *count = it->second.second;
+  return 0;
+}
+
+static int stencil_apply(const fmp_block* blk, double alpha, int boundary, int mode, int part, const double* x,
+                         double* y, const double* w, double* dots, double* scratch, void* stream);
+
 extern "C" int fmp_stencil_apply(const fmp_block* blk, double alpha, int boundary, int mode, const double* x,
                                  double* y, const double* w, double* dots, double* scratch, void* stream) {
+  return stencil_apply(blk, alpha, boundary, mode, FMP_PART_ALL, x, y, w, dots, scratch, stream);
+}
+
+extern "C" int fmp_stencil_apply_part(const fmp_block* blk, double alpha, int boundary, int mode, int part,
+                                      const double* x, double* y, const double* w, double* dots, double* scratch,
+                                      void* stream) {
+  FMP_REQUIRE(part >= FMP_PART_ALL && part <= FMP_PART_BOUNDARY, "bad part %d", part);
+  return stencil_apply(blk, alpha, boundary, mode, part, x, y, w, dots, scratch, stream);
+}
+
+static int stencil_apply(const fmp_block* blk, double alpha, int boundary, int mode, int part, const double* x,
+                         double* y, const double* w, double* dots, double* scratch, void* stream) {
   if (int e = check_block(blk)) return e;
   FMP_REQUIRE(mode >= 0 && mode <= 3, "bad stencil mode %d", mode);
   FMP_REQUIRE(boundary >= 0 && boundary <= 3, "bad stencil boundary flags %d", boundary);
@@ -584,7 +644,13 @@ extern "C" int fmp_stencil_apply(const fmp_block* blk, double alpha, int boundar
       }
     const int64_t units = ntiles * a.nzc;
     FMP_REQUIRE(mode == 0 || units <= kScratchDoubles / 2, "block too large for the SpMV reduction scratch");
-    const int grid = (int)std::min<int64_t>(units, resident);
+    a.ulist = nullptr;
+    a.nlaunch = units;
+    if (part != FMP_PART_ALL) {
+      if (int e = unit_list(g, a.tiles_x, a.tiles_y, a.L, a.nzc, part, &a.ulist, &a.nlaunch)) return e;
+    }
+    const int grid = (int)std::min<int64_t>(a.nlaunch, resident);
+    if (grid > 0) {
     CUtensorMap tm;
     const uint64_t dims[4] = {(uint64_t)g.bx, (uint64_t)g.by, (uint64_t)g.bz, 3};
     const uint64_t strides[3] = {(uint64_t)g.bx * 8, (uint64_t)g.bx * g.by * 8, (uint64_t)g.bx * g.by * g.bz * 8};
@@ -604,9 +670,13 @@ extern "C" int fmp_stencil_apply(const fmp_block* blk, double alpha, int boundar
     }
 #undef FMP_SPMV_GO
     FMP_CHECK_LAUNCH();
-    if (mode >= 1) return finish_reduce(scratch, (int)units, mode == 2 ? 2 : 1, dots, st);
+    }
+    // the interior part leaves its per-unit partials in scratch; the boundary part adds its own
+    // and reduces all of them in the fixed unit order
+    if (mode >= 1 && part != FMP_PART_INTERIOR) return finish_reduce(scratch, (int)units, mode == 2 ? 2 : 1, dots, st);
     return 0;
   }
+  if (part == FMP_PART_INTERIOR) return 0;   // the thread-per-point fallback runs whole in the boundary part
   const int tx = (g.bx + TX - 1) / TX, ty = (g.by + TY - 1) / TY;
   const int64_t units = (int64_t)tx * ty * g.bz;
   // one full wave: SMs x resident CTAs (smem-limited to 5 of 41 KB), fewer for tiny blocks

@@ -267,10 +267,16 @@ class SolvePlan:
         _lib.check(_lib.lib().fmp_precond_create(C.byref(desc), C.byref(handle)), "fmp_precond_create")
         self._handle = handle
 
-    def apply(self, blk: _lib.FmpBlock, mode: int, r: torch.Tensor, z: torch.Tensor | None) -> None:
-        _lib.check(_lib.lib().fmp_precond_apply(self._handle, C.byref(blk), mode, _lib.ptr(r),
-                                                _lib.ptr(z) if z is not None else None, _lib.stream()),
-                   "fmp_precond_apply")
+    def apply(self, blk: _lib.FmpBlock, mode: int, r: torch.Tensor, z: torch.Tensor | None,
+              part: int = _lib.FMP_PART_ALL) -> None:
+        """fmp_precond_apply; part = FMP_PART_INTERIOR / _BOUNDARY splits it around a ghost exchange."""
+        zp = _lib.ptr(z) if z is not None else None
+        if part == _lib.FMP_PART_ALL:
+            rc = _lib.lib().fmp_precond_apply(self._handle, C.byref(blk), mode, _lib.ptr(r), zp, _lib.stream())
+        else:
+            rc = _lib.lib().fmp_precond_apply_part(self._handle, C.byref(blk), mode, part, _lib.ptr(r), zp,
+                                                   _lib.stream())
+        _lib.check(rc, "fmp_precond_apply")
 
     def gemm_kind(self) -> str:
         """Woodbury GEMM this plan was created with: 'ozaki' (default), 'own' or 'cublas'."""

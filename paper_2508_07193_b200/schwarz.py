@@ -190,28 +190,23 @@ class DistTransport:
             fn()
 
     def allreduce_(self, t: torch.Tensor) -> torch.Tensor:
-        if self.staged:
+        if self.staged:   # gloo with device tensors: through a host copy (testing backend)
             h = t.cpu()
             self.dist.all_reduce(h, group=self.group)
             t.copy_(h)
-        else:
+        else:             # NCCL: in place, on the current stream
             self.dist.all_reduce(t, group=self.group)
         return t
 
     def exchange(self, sends: list[tuple[int, torch.Tensor]], recvs: list[tuple[int, torch.Tensor]]) -> None:
-        if self.staged:
-            sends = [(p, t.cpu()) for p, t in sends]
-            hrecv = [(p, torch.empty(t.shape, dtype=t.dtype)) for p, t in recvs]
-        else:
-            hrecv = recvs
+        """Grouped point-to-point messages.  NCCL: device tensors, issued on the current stream and
+        waited for on it (no host block).  gloo: host tensors (HaloExchanger stages device slabs
+        through pinned buffers), blocking."""
         ops = [self.dist.P2POp(self.dist.isend, t, peer, self.group) for peer, t in sends]
-        ops += [self.dist.P2POp(self.dist.irecv, t, peer, self.group) for peer, t in hrecv]
+        ops += [self.dist.P2POp(self.dist.irecv, t, peer, self.group) for peer, t in recvs]
         if ops:
             for w in self.dist.batch_isend_irecv(ops):
                 w.wait()
-        if self.staged:
-            for (_, dst), (_, h) in zip(recvs, hrecv):
-                dst.copy_(h)
 
     def barrier(self) -> None:
         self.dist.barrier(group=self.group)
@@ -302,74 +297,234 @@ class BlockLayout:
 class HaloExchanger:
     """Fills the ghost shell (width P) of a block field from the neighbour GPUs.
 
-    Three phases: z faces, then y faces extended over the z ghosts, then x faces
-    extended over both, so edges and corners arrive without diagonal messages.  The
-    slab layout is the one fmp_block documents (include/flashmp_b200.h).
+    Three phases: z faces, then y faces extended over the z ghosts, then x faces extended over
+    both, so edges and corners arrive without diagonal messages (slab layout: fmp_block in
+    include/flashmp_b200.h).  Replaces the reference's per-subdomain mailbox messages
+    (ref:schwarz.py:217-257) with one slab per GPU face and phase.
+
+    * Allocation-free: send slabs and ghost slots (each with a trailing tag double) are allocated
+      once here; NCCL receives straight into the ghost slots.
+    * Device packing: fmp_halo_pack builds every slab in one kernel (reading the ghosts of the
+      earlier phases); fmp_halo_unpack checks the slab's tag (epoch * 3 + phase), so a lost or
+      stale message sets a bit in a host-mapped status word and `check()` raises
+      CommunicationError (ref:schwarz.py:237-257).
+    * Overlap: `start(x)` issues the exchange on a side stream (NCCL) or a worker thread (gloo
+      staging through pinned host buffers) and returns; the caller launches the interior work
+      (FMP_PART_INTERIOR) and then `finish()` orders its stream after the ghosts.
+    * CPU tensors (gloo, host-logic tests) take the same three phases with torch slicing.
+
+    `trace` keeps the reference's message rows (epoch, src, dst, bytes) for the SUBDOMAIN
+    messages this block's subdomains send (ref:schwarz.py:186-188, 234-235; inside a GPU they are
+    in-place reads, across GPUs they travel inside the slabs); `gpu_trace` the slabs actually sent.
     """
+
+    PHASE_SLOTS = ((4, 5), (2, 3), (0, 1))   # ghost slots (lo, hi) of phases z, y, x
 
     def __init__(self, layout: BlockLayout, width: int, record_trace: bool = False):
         self.layout = layout
         self.P = P = int(width)
         self.epoch = 0
         self.trace: list[tuple[int, int, int, int]] = []
+        self.gpu_trace: list[tuple[int, int, int, int]] = []
         self.record_trace = record_trace
+        self.drop_phase = None   # test hook: (phase, side) whose message is neither sent nor received
         bx, by, bz = layout.block
         dev = layout.device
-        mk = lambda shape: torch.zeros(shape, dtype=torch.float64, device=dev)
         nb = [layout.neighbor(a, s) for a in (0, 1, 2) for s in (-1, 1)]
         self.nb = nb   # xlo, xhi, ylo, yhi, zlo, zhi
         shapes = [(3, bz + 2 * P, by + 2 * P, P)] * 2 + [(3, bz + 2 * P, P, bx)] * 2 + [(3, P, by, bx)] * 2
-        self.ghosts = [mk(s) if (n is not None and P > 0) else None for s, n in zip(shapes, nb)]
         self.active = any(n is not None for n in nb) and P > 0
+        self.cuda = dev.type == "cuda"
+        f64 = dict(dtype=torch.float64, device=dev)
+        # ghost slot q = a flat buffer of numel + 1 doubles (the tag last); ghosts[q] is its view
+        self._gbuf = [torch.zeros(int(np.prod(sh)) + 1, **f64) if (n is not None and P > 0) else None
+                      for sh, n in zip(shapes, nb)]
+        self.ghosts = [b[:-1].view(sh) if b is not None else None for b, sh in zip(self._gbuf, shapes)]
+        # send slab of (phase, side): the same size as the receiving ghost slot on the other side
+        self._send = {}
+        for ph, slots in enumerate(self.PHASE_SLOTS):
+            for side, q in enumerate(slots):
+                if nb[q] is not None and P > 0:
+                    self._send[(ph, side)] = torch.zeros(int(np.prod(shapes[q])) + 1, **f64)
+        self._msgs = self._subdomain_messages() if record_trace else []
+        tr = layout.transport
+        self.staged = bool(getattr(tr, "staged", False)) and self.cuda
+        self._thread = None
+        self._error = None
+        if self.cuda and self.active:
+            self.stream = torch.cuda.Stream(device=dev)
+            self.done = torch.cuda.Event()
+            self._status = torch.zeros(1, dtype=torch.int32, pin_memory=True)
+            if self.staged:   # pinned host staging for gloo: sends and receives, allocated once
+                self._hsend = {k: torch.empty(v.numel(), dtype=torch.float64, pin_memory=True)
+                               for k, v in self._send.items()}
+                self._hrecv = {q: torch.empty(b.numel(), dtype=torch.float64, pin_memory=True)
+                               for q, b in enumerate(self._gbuf) if b is not None}
+
+    # ---- geometry / trace
+    def _subdomain_messages(self):
+        """The reference Exchanger's messages sent by this block's subdomains, in its pack order:
+        rank i sends intersect(owned_i, ext_j) to each neighbour j (ref:schwarz.py:203-213)."""
+        part = self.layout.partition
+        mine = {r.rank for r in self.layout.local_ranks}
+        rows = []
+        for info in part.ranks:
+            if info.rank not in mine:
+                continue
+            for _, j in info.neighbors:
+                reg = _intersect(info.owned_range(), part.ranks[j].ext_range())
+                if reg is not None:
+                    rows.append((info.rank, j, 3 * 8 * int(np.prod([hi - lo for lo, hi in reg]))))
+        return rows
 
     def block_struct(self) -> _lib.FmpBlock:
         return self.layout.block_struct(self.ghosts if self.active else None, self.P if self.active else 0)
 
-    def _swap(self, pairs):
-        """pairs: list of (peer, send_tensor, recv_tensor)."""
-        tr = self.layout.transport
-        sends = [(p, s.contiguous()) for p, s, _ in pairs]
-        recvs = [(p, r) for p, _, r in pairs]
-        if self.record_trace:
-            for p, s in sends:
-                self.trace.append((self.epoch, self.layout.rank, p, s.numel() * 8))
-        tmp = [(p, torch.empty_like(r)) for p, r in recvs]
-        tr.exchange(sends, tmp)
-        for (p, r), (_, t) in zip(recvs, tmp):
-            r.copy_(t)
+    def _tag(self, phase: int) -> float:
+        return float(self.epoch * 3 + phase)
 
+    # ---- exchange
     def exchange(self, x: torch.Tensor) -> None:
+        """Synchronous form: start + finish (the ghosts are ready on the current stream)."""
+        self.start(x)
+        self.finish()
+
+    def start(self, x: torch.Tensor) -> None:
+        if self.record_trace:
+            self.trace.extend((self.epoch + 1, s, d, b) for s, d, b in self._msgs)
         if not self.active:
+            self.epoch += 1
             return
         self.epoch += 1
+        if not self.cuda:
+            self._run_cpu(x)
+            return
+        self.stream.wait_stream(torch.cuda.current_stream())   # x is ready on the caller's stream
+        if self.staged:
+            import threading
+            dev = self.layout.device
+
+            def work():
+                try:
+                    torch.cuda.set_device(dev)
+                    self._run_device(x)
+                except BaseException as e:   # re-raised by finish()
+                    self._error = e
+            self._thread = threading.Thread(target=work, daemon=True)
+            self._thread.start()
+        else:
+            self._run_device(x)
+
+    def finish(self) -> None:
+        if not (self.active and self.cuda):
+            return
+        if self._thread is not None:
+            self._thread.join()
+            self._thread = None
+            if self._error is not None:
+                e, self._error = self._error, None
+                raise e
+        torch.cuda.current_stream().wait_event(self.done)
+
+    def check(self) -> None:
+        """Raise CommunicationError if any unpack saw a wrong tag (lost / stale message).  The
+        status word is written by the device; read it after a synchronisation point."""
+        if self.active and self.cuda:
+            bits = int(self._status[0])
+            if bits:
+                names = ["x-lo", "x-hi", "y-lo", "y-hi", "z-lo", "z-hi"]
+                self._status.zero_()
+                raise CommunicationError(f"rank {self.layout.rank}: missing or stale halo message "
+                                         f"({', '.join(n for q, n in enumerate(names) if bits >> q & 1)}) "
+                                         f"by epoch {self.epoch}")
+
+    def _pairs(self, phase):
+        """[(side, peer, ghost slot)] of the phase, minus a test-dropped message."""
+        out = []
+        for side, q in enumerate(self.PHASE_SLOTS[phase]):
+            peer = self.nb[q]
+            if peer is None:
+                continue
+            out.append((side, peer, q))
+        return out
+
+    def _dropped(self, phase, side, sending):
+        """Test hook: drop_phase = (phase, side) skips this rank's send toward `side` and, on the
+        neighbour, the matching receive (its opposite side)."""
+        if self.drop_phase is None:
+            return False
+        dp, ds = self.drop_phase
+        return dp == phase and (ds == side if sending else ds == 1 - side)
+
+    def _run_device(self, x):
+        tr = self.layout.transport
+        lib = _lib.lib()
+        with torch.cuda.stream(self.stream):
+            st = self.stream.cuda_stream
+            blk = self.block_struct()
+            for ph in range(3):
+                pairs = self._pairs(ph)
+                tag = self._tag(ph)
+                for side, peer, q in pairs:
+                    _lib.check(lib.fmp_halo_pack(_lib.ref(blk), ph, side, _lib.ptr(x),
+                                                 _lib.ptr(self._send[(ph, side)]), tag, st), "fmp_halo_pack")
+                sends = [(peer, self._send[(ph, side)], side) for side, peer, q in pairs
+                         if not self._dropped(ph, side, True)]
+                recvs = [(peer, self._gbuf[q], q) for side, peer, q in pairs if not self._dropped(ph, side, False)]
+                if self.record_trace:
+                    self.gpu_trace.extend((self.epoch, self.layout.rank, p, (b.numel() - 1) * 8) for p, b, _ in sends)
+                if self.staged:
+                    for p, b, side in sends:
+                        self._hsend[(ph, side)].copy_(b, non_blocking=True)
+                    self.stream.synchronize()
+                    tr.exchange([(p, self._hsend[(ph, side)]) for p, b, side in sends],
+                                [(p, self._hrecv[q]) for p, b, q in recvs])
+                    for p, b, q in recvs:
+                        b.copy_(self._hrecv[q], non_blocking=True)
+                else:
+                    tr.exchange([(p, b) for p, b, _ in sends], [(p, b) for p, b, _ in recvs])
+                for side, peer, q in pairs:
+                    _lib.check(lib.fmp_halo_unpack(_lib.ref(blk), ph, side, _lib.ptr(self._gbuf[q]), tag,
+                                                   self._status.data_ptr(), st), "fmp_halo_unpack")
+            self.done.record(self.stream)
+
+    def _run_cpu(self, x):
+        """Host tensors (gloo): the same three phases built with torch slicing."""
         P = self.P
         bx, by, bz = self.layout.block
         xlo, xhi, ylo, yhi, zlo, zhi = self.ghosts
-        nxl, nxh, nyl, nyh, nzl, nzh = self.nb
-        # phase z
-        pairs = []
-        if nzl is not None:
-            pairs.append((nzl, x[:, :P], zlo))
-        if nzh is not None:
-            pairs.append((nzh, x[:, bz - P:], zhi))
-        self._swap(pairs)
+        tr = self.layout.transport
+
+        def swap(ph, slabs):
+            pairs = self._pairs(ph)
+            sends = []
+            for side, peer, q in pairs:
+                buf = self._send[(ph, side)]
+                buf[:-1].view(slabs[side].shape).copy_(slabs[side])
+                buf[-1] = self._tag(ph)
+                if not self._dropped(ph, side, True):
+                    sends.append((peer, buf))
+            recvs = [(peer, self._gbuf[q]) for side, peer, q in pairs if not self._dropped(ph, side, False)]
+            if self.record_trace:
+                self.gpu_trace.extend((self.epoch, self.layout.rank, p, (b.numel() - 1) * 8) for p, b in sends)
+            tr.exchange(sends, recvs)
+            for side, peer, q in pairs:
+                if float(self._gbuf[q][-1]) != self._tag(ph):
+                    raise CommunicationError(f"rank {self.layout.rank}: missing or stale halo message from "
+                                             f"{peer} in epoch {self.epoch}")
+
+        swap(0, {0: x[:, :P], 1: x[:, bz - P:]})
 
         def zext(rows: slice):  # (3, bz+2P, |rows|, bx): block rows with the z ghosts around them
-            parts = [zlo[:, :, rows] if zlo is not None else x.new_zeros((3, P, rows.stop - rows.start, bx)),
-                     x[:, :, rows],
-                     zhi[:, :, rows] if zhi is not None else x.new_zeros((3, P, rows.stop - rows.start, bx))]
+            w = rows.stop - rows.start
+            parts = [zlo[:, :, rows] if zlo is not None else x.new_zeros((3, P, w, bx)), x[:, :, rows],
+                     zhi[:, :, rows] if zhi is not None else x.new_zeros((3, P, w, bx))]
             return torch.cat(parts, dim=1)
 
-        pairs = []
-        if nyl is not None:
-            pairs.append((nyl, zext(slice(0, P)), ylo))
-        if nyh is not None:
-            pairs.append((nyh, zext(slice(by - P, by)), yhi))
-        self._swap(pairs)
+        swap(1, {0: zext(slice(0, P)), 1: zext(slice(by - P, by))})
 
         def padded_cols(c0: int, c1: int):  # (3, bz+2P, by+2P, c1-c0)
-            w = c1 - c0
-            out = x.new_zeros((3, bz + 2 * P, by + 2 * P, w))
+            out = x.new_zeros((3, bz + 2 * P, by + 2 * P, c1 - c0))
             out[:, P:P + bz, P:P + by] = x[..., c0:c1]
             if ylo is not None:
                 out[:, :, :P] = ylo[..., c0:c1]
@@ -381,14 +536,10 @@ class HaloExchanger:
                 out[:, P + bz:, P:P + by] = zhi[..., c0:c1]
             return out
 
-        pairs = []
-        if nxl is not None:
-            pairs.append((nxl, padded_cols(0, P), xlo))
-        if nxh is not None:
-            pairs.append((nxh, padded_cols(bx - P, bx), xhi))
-        self._swap(pairs)
+        swap(2, {0: padded_cols(0, P), 1: padded_cols(bx - P, bx)})
 
     def write_trace_csv(self, path) -> None:
+        """The reference's comm trace schema (ref:schwarz.py:259-266)."""
         import csv
         with open(path, "w", newline="") as f:
             w = csv.writer(f)
@@ -503,13 +654,26 @@ class RasPreconditioner:
             if self.alpha != 0.0 else None
 
     def apply_into(self, r: torch.Tensor, z: torch.Tensor) -> torch.Tensor:
-        with self.timer.phase("asm_comm"):
-            self.exchanger.exchange(r)
+        ex = self.exchanger
+        ex.check()   # a lost / stale message of an earlier apply (status is final after any sync)
+        if self.plan is None:
+            ex.exchange(r)
+            z.copy_(r)
+            return z
+        if not ex.active:
+            with self.timer.phase("fast_solve"):
+                self.plan.apply(ex.block_struct(), _lib.FMP_SOLVE_WOODBURY, r, z)
+            return z
+        # multi-GPU: the ghost exchange runs beside the interior subdomains' restriction and
+        # x/y transforms; "asm_comm" times only the exposed wait for the ghosts
+        ex.start(r)
+        blk = ex.block_struct()
         with self.timer.phase("fast_solve"):
-            if self.plan is None:
-                z.copy_(r)
-            else:
-                self.plan.apply(self.exchanger.block_struct(), _lib.FMP_SOLVE_WOODBURY, r, z)
+            self.plan.apply(blk, _lib.FMP_SOLVE_WOODBURY, r, z, part=_lib.FMP_PART_INTERIOR)
+        with self.timer.phase("asm_comm"):
+            ex.finish()
+        with self.timer.phase("fast_solve"):
+            self.plan.apply(blk, _lib.FMP_SOLVE_WOODBURY, r, z, part=_lib.FMP_PART_BOUNDARY)
         return z
 
     def apply(self, r_dist):
@@ -544,19 +708,33 @@ class DistributedOperator:
         self._scratch = torch.zeros(int(_lib.lib().fmp_reduce_scratch_doubles()), dtype=torch.float64, device=dev)
 
     def _run(self, mode: int, x: torch.Tensor, y, w):
-        with self.timer.phase("p2p"):
-            self.exchanger.exchange(x)
-        blk = self.exchanger.block_struct()
+        ex = self.exchanger
         dots = self._host.ptr() if self._host is not None else _lib.ptr(self._dots)
+        args = (self.alpha, int(self.with_boundary), mode)
+        ptrs = (_lib.ptr(x), _lib.ptr(y), _lib.ptr(w), dots, _lib.ptr(self._scratch), _lib.stream())
+        if not ex.active:
+            with self.timer.phase("spmv"):
+                _lib.call("fmp_stencil_apply", _lib.ref(ex.block_struct()), *args, *ptrs)
+            return
+        # multi-GPU: interior units while the width-1 ghosts are in flight, then the faces;
+        # "p2p" times only the exposed wait
+        ex.start(x)
+        blk = ex.block_struct()
         with self.timer.phase("spmv"):
-            _lib.call("fmp_stencil_apply", _lib.ref(blk), self.alpha, int(self.with_boundary), mode,
-                      _lib.ptr(x), _lib.ptr(y), _lib.ptr(w), dots, _lib.ptr(self._scratch), _lib.stream())
+            _lib.call("fmp_stencil_apply_part", _lib.ref(blk), *args, _lib.FMP_PART_INTERIOR, *ptrs)
+        with self.timer.phase("p2p"):
+            ex.finish()
+        with self.timer.phase("spmv"):
+            _lib.call("fmp_stencil_apply_part", _lib.ref(blk), *args, _lib.FMP_PART_BOUNDARY, *ptrs)
 
     def _reduced(self, n: int) -> list[float]:
         with self.timer.phase("reduction"):
             if self._host is not None:
-                return self._host.read(n)
-            return self.transport.allreduce_(self._dots[:n].clone()).tolist()
+                out = self._host.read(n)
+            else:
+                out = self.transport.allreduce_(self._dots[:n]).tolist()
+        self.exchanger.check()   # synchronised here: a lost / stale ghost message raises now
+        return out
 
     def apply_into(self, x: torch.Tensor, y: torch.Tensor) -> torch.Tensor:
         self._run(0, x, y, None)

@@ -94,3 +94,84 @@ def solve_worker(rank, world, port, gext, sgrid, out):
     import torch.distributed as dist
     dist.barrier()
     dist.destroy_process_group()
+
+
+def trace_worker(rank, world, port, gext, sgrid, ov, out):
+    """The subdomain message rows this rank's block records over two exchanges."""
+    import torch
+    init(rank, world, port)
+    from paper_2508_07193_b200 import Box, make_partition
+    from paper_2508_07193_b200.schwarz import BlockLayout, DistTransport, HaloExchanger
+    tr = DistTransport(device="cpu")
+    part = make_partition(Box(*gext), sgrid, ov)
+    lay = BlockLayout(part, tr)
+    hx = HaloExchanger(lay, max(1, ov), record_trace=True)
+    x = torch.zeros(lay.shape4, dtype=torch.float64)
+    hx.exchange(x)
+    hx.exchange(x)
+    out.put((rank, list(hx.trace)))
+    import torch.distributed as dist
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def drop_worker(rank, world, port, gext, sgrid, device, out):
+    """Rank 0 drops its z-phase message toward the high side (and rank 1 its matching receive) in
+    the second exchange: rank 1's ghost keeps the first epoch's tag, which must raise
+    CommunicationError (host path: at once; device path: at check())."""
+    import torch
+    init(rank, world, port)
+    from paper_2508_07193_b200 import Box, CommunicationError, make_partition
+    from paper_2508_07193_b200.schwarz import BlockLayout, DistTransport, HaloExchanger
+    tr = DistTransport(device=device)
+    part = make_partition(Box(*gext), sgrid, 1)
+    lay = BlockLayout(part, tr)
+    hx = HaloExchanger(lay, 1)
+    x = torch.ones(lay.shape4, dtype=torch.float64, device=device)
+    hx.exchange(x)
+    if device != "cpu":
+        torch.cuda.synchronize()
+        hx.check()
+    ok_first = True
+    hx.drop_phase = (2, 1)   # x phase (the GPU grid is (2,1,1)): rank 0 -> its high side
+    raised = False
+    try:
+        hx.exchange(x)
+        if device != "cpu":
+            torch.cuda.synchronize()
+            hx.check()
+    except CommunicationError:
+        raised = True
+    out.put((rank, ok_first, raised))
+    import torch.distributed as dist
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def alloc_worker(rank, world, port, gext, sgrid, out):
+    """Device allocator growth over repeated exchanges and split SpMV / RAS applies (gloo staging,
+    all ranks on cuda:0): the exchange path allocates nothing after the first call."""
+    import torch
+    init(rank, world, port)
+    from paper_2508_07193_b200 import Box, DistributedOperator, RasPreconditioner, make_partition
+    from paper_2508_07193_b200.schwarz import DistTransport
+    tr = DistTransport(device="cuda:0")
+    part = make_partition(Box(*gext), sgrid, 1)
+    op = DistributedOperator(part, 0.25, tr)
+    prec = RasPreconditioner(part, 0.25, tr)
+    x = torch.rand(op.layout.shape4, dtype=torch.float64, device="cuda:0")
+    y, z = torch.empty_like(x), torch.empty_like(x)
+    op.apply_into(x, y)
+    prec.apply_into(x, z)
+    torch.cuda.synchronize()
+    before = torch.cuda.memory_allocated()
+    for _ in range(5):
+        op.exchanger.exchange(x)
+        op.apply_into(x, y)
+        prec.apply_into(x, z)
+    torch.cuda.synchronize()
+    after = torch.cuda.memory_allocated()
+    out.put((rank, before, after))
+    import torch.distributed as dist
+    dist.barrier()
+    dist.destroy_process_group()

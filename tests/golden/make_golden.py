@@ -113,6 +113,19 @@ def gen_schwarz():
         out[f"extidx_{tag}"] = np.concatenate(exts).astype(np.int64)
         out[f"geom_{tag}"] = np.array([[*i.owned_lo, *i.owned.extents, *i.ext_lo, *i.ext.extents]
                                        for i in part.ranks], dtype=np.int64)
+        # the reference's comm trace: one (epoch, src, dst, bytes) row per message (two exchanges)
+        ex = rsw.Exchanger(part, tr, record_trace=True)
+        ex.exchange(rsw.scatter_field(part, lin))
+        ex.exchange(rsw.scatter_field(part, lin))
+        out[f"trace_{tag}"] = np.array(ex.trace, dtype=np.int64).reshape(-1, 4)
+    for gext, grid, ov in [((8, 8, 8), (2, 2, 2), 1), ((16, 8, 16), (4, 2, 4), 1)]:   # multi-GPU trace cases
+        part = rsw.make_partition(rgrid.Box(*gext), grid, ov)
+        tag = "_".join(map(str, gext)) + "_g" + "".join(map(str, grid)) + f"_o{ov}"
+        ex = rsw.Exchanger(part, rsw.SerialTransport(), record_trace=True)
+        lin = np.arange(rgrid.Box(*gext).dof, dtype=np.float64)
+        ex.exchange(rsw.scatter_field(part, lin))
+        ex.exchange(rsw.scatter_field(part, lin))
+        out[f"trace_{tag}"] = np.array(ex.trace, dtype=np.int64).reshape(-1, 4)
     np.savez_compressed(OUT / "schwarz.npz", **out)
 
 
@@ -300,6 +313,9 @@ def gen_huge():
 
 
 if __name__ == "__main__":
+    if "--schwarz" in sys.argv:
+        gen_schwarz()
+        sys.exit(0)
     if "--huge" in sys.argv:
         gen_huge()
         sys.exit(0)

@@ -154,3 +154,22 @@ def test_rotation_groups_share_cinv(rep):
         assert sorted(rm.tolist()) == list(range(rm.size))
         got = O.precompute(e, 0.25).Cinv
         assert np.abs(got - base[np.ix_(rm, rm)]).max() <= 1e-13 * np.abs(base).max()
+
+
+@pytest.mark.parametrize("tag", ["8_8_8_g211_o0", "8_8_8_g211_o1", "8_8_4_g221_o1", "12_8_8_g322_o2", "8_4_6_g223_o1",
+                                 "8_8_8_g222_o1"])
+def test_subdomain_trace_matches_reference(tag):
+    """One block: the exchanger's message rows equal the reference Exchanger's trace row for row
+    (same order: ranks ascending, neighbours in (dz, dy, dx) order; ref:schwarz.py:203-235)."""
+    import torch
+    from paper_2508_07193_b200 import Box, make_partition
+    from paper_2508_07193_b200.schwarz import BlockLayout, DeviceTransport, HaloExchanger
+    g = np.load(GOLDEN / "schwarz.npz")
+    gs, grid, ov = tag.split("_g")[0], tag.split("_g")[1].split("_o")[0], int(tag.split("_o")[1])
+    part = make_partition(Box(*map(int, gs.split("_"))), tuple(int(c) for c in grid), ov)
+    lay = BlockLayout(part, DeviceTransport("cpu"))
+    hx = HaloExchanger(lay, max(1, ov), record_trace=True)
+    x = torch.zeros(lay.shape4, dtype=torch.float64)
+    hx.exchange(x)
+    hx.exchange(x)
+    assert np.array_equal(np.array(hx.trace, dtype=np.int64).reshape(-1, 4), g[f"trace_{tag}"])

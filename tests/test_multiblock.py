@@ -66,3 +66,36 @@ def test_multiblock_matches_single_block(world, gext, sgrid):
         assert iters == rep.iterations
         assert np.abs(np.array(trace) - np.array([t[1] for t in rep.trace])).max() <= 1e-12
         assert np.abs(xx - X[sl]).max() <= 1e-11 * np.abs(X).max()
+
+
+@pytest.mark.parametrize("world,gext,sgrid,ov", [(2, (8, 8, 8), (2, 1, 1), 1), (2, (8, 8, 8), (2, 2, 2), 1),
+                                                 (4, (16, 8, 16), (4, 2, 4), 1)])
+def test_subdomain_trace_matches_reference_multiblock(world, gext, sgrid, ov):
+    """Across GPU blocks, the union of every block's subdomain message rows equals the reference
+    Exchanger's trace (ref:schwarz.py:186-188, 234-235; golden from the reference itself)."""
+    from conftest import GOLDEN
+    g = np.load(GOLDEN / "schwarz.npz")
+    tag = "_".join(map(str, gext)) + "_g" + "".join(map(str, sgrid)) + f"_o{ov}"
+    res = run(H.trace_worker, world, gext, sgrid, ov)
+    rows = sorted(tuple(r) for _, t in res for r in t)
+    want = sorted(tuple(int(v) for v in r) for r in g[f"trace_{tag}"])
+    assert rows == want
+
+
+def test_lost_halo_message_raises_host_path():
+    res = run(H.drop_worker, 2, (8, 8, 8), (2, 1, 1), "cpu")
+    # rank 1 misses rank 0's x-phase slab (rank 0 still receives rank 1's)
+    assert [r[2] for r in res] == [False, True]
+
+
+@pytest.mark.gpu
+def test_lost_halo_message_raises_device_path():
+    res = run(H.drop_worker, 2, (16, 8, 8), (2, 1, 1), "cuda:0")
+    assert [r[2] for r in res] == [False, True]
+
+
+@pytest.mark.gpu
+def test_exchange_is_allocation_free():
+    res = run(H.alloc_worker, 2, (32, 16, 16), (4, 2, 2))
+    for rank, before, after in res:
+        assert after == before, (rank, before, after)
