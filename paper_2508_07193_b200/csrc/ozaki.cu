@@ -31,17 +31,21 @@ namespace fmp {
 
 constexpr int OZ_S = 7;                 // slices per operand
 constexpr int OZ_M = 128;               // rows per tile (TMEM lanes)
-constexpr int OZ_WMAX = 64;             // column-tile width cap (multiple of 16): OZ_S * w <= 512 TMEM columns
-constexpr int OZ_MAX_K = 16384;         // int32 headroom: S pairs x 2^14 x K < 2^31 (per K part)
+constexpr int OZ_WMAX = 72;             // column-tile width cap (multiple of 8): 7 levels x 72 = 504 TMEM columns
+constexpr int OZ_RMAX = 512;            // stacked B rows: pad16(S w) <= 512
+constexpr int OZ_MAX_K = 16384;         // int32 headroom: S pairs x 2^14 x K < 2^31 (per K segment)
 constexpr int OZ_KC = 32;               // K bytes per MMA / stage
-constexpr int OZ_PART = OZ_MAX_K / OZ_KC;   // K chunks per part: larger K is split into parts whose
-                                             // FP64 results the epilogue adds (same CTA, in order)
+constexpr int OZ_PART = OZ_MAX_K / OZ_KC;   // max K chunks of one segment
 constexpr int OZ_ABLK = OZ_M * OZ_KC;   // bytes of one A slice block
-constexpr int OZ_STAGE = OZ_S * (OZ_ABLK + OZ_WMAX * OZ_KC);
+constexpr int OZ_STAGE = OZ_S * OZ_ABLK + OZ_RMAX * OZ_KC;
 constexpr int OZ_STAGES = 5;
 constexpr int OZ_THREADS = 192;         // warps 0-3 epilogue, 4 producer, 5 MMA
 constexpr int OZ_TMEM_COLS = 512;
-static_assert(OZ_S * OZ_WMAX <= OZ_TMEM_COLS, "levels x width exceed TMEM");
+constexpr int OZ_SLOT = OZ_WMAX * OZ_M; // doubles of one partial slot ([column][row])
+static_assert(OZ_S * OZ_WMAX + 8 <= OZ_TMEM_COLS, "levels x width exceed TMEM");
+static_assert(OZ_STAGES * OZ_STAGE <= 227 * 1024, "stages exceed shared memory");
+
+__host__ __device__ constexpr int oz_pad16(int x) { return (x + 15) / 16 * 16; }
 
 __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
   return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
@@ -59,9 +63,11 @@ __device__ __forceinline__ void umma_i8(uint32_t tmem, uint64_t da, uint64_t db,
       "l"(da), "l"(db), "r"(idesc), "r"(acc));
 }
 
-// One K chunk of a tile of width W: for each A slice p, MMAs of N <= 256 against the stacked B
-// slices 1..S+1-p (levels p+1..S+1).  W is a template constant so every descriptor and TMEM
-// offset folds to an immediate: the issue loop is ~4 instructions per MMA.
+// One K chunk of a tile of width W: for each A slice p, MMAs (N <= 256, multiples of 16) against
+// the stacked B slices 1..S+1-p (levels p+1..S+1), N = pad16((S+1-p) W).  Level L = p + q sits in
+// TMEM columns [(L-2) W, (L-1) W); the pad16 tail of an MMA reads the next stacked slice (or the
+// zero rows past the last one) and lands in columns >= 7 W, which no level uses.  W is a template
+// constant so every descriptor and TMEM offset folds to an immediate.
 template <int W>
 __device__ __forceinline__ void issue_chunk(uint64_t da0, uint64_t db0, uint32_t tmem, bool first) {
   constexpr uint32_t IDESC0 = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(OZ_M >> 4) << 24);
@@ -69,21 +75,29 @@ __device__ __forceinline__ void issue_chunk(uint64_t da0, uint64_t db0, uint32_t
   for (int p = 1; p <= OZ_S; ++p) {
     const uint64_t da = da0 + (uint64_t)(((p - 1) * OZ_ABLK) >> 4);
     const uint32_t acc = (first && p == 1) ? 0u : 1u;
+    const int N = oz_pad16((OZ_S + 1 - p) * W);
 #pragma unroll
-    for (int r0 = 0; r0 < (OZ_S + 1 - p) * W; r0 += 256) {
-      const int nn = ((OZ_S + 1 - p) * W - r0) < 256 ? ((OZ_S + 1 - p) * W - r0) : 256;
+    for (int r0 = 0; r0 < N; r0 += 256) {
+      const int nn = (N - r0) < 256 ? (N - r0) : 256;
       umma_i8(tmem + (uint32_t)((p - 1) * W + r0), da, db0 + (uint64_t)((r0 * 16) >> 4),
               IDESC0 | ((uint32_t)(nn >> 3) << 17), acc);
     }
   }
 }
 
+__device__ __forceinline__ void tmem_ld8(uint32_t addr, uint32_t (&v)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+               : "r"(addr));
+}
+
 __global__ void __launch_bounds__(OZ_THREADS, 1)
-    k_ozaki(const OzShape* __restrict__ shapes, const OzTile* __restrict__ tiles, const int* __restrict__ offs,
-            long long* __restrict__ prof) {
+    k_ozaki(const OzShape* __restrict__ shapes, const OzItem* __restrict__ items, const int* __restrict__ offs,
+            double* __restrict__ zpart, int* __restrict__ counters, long long* __restrict__ prof) {
   extern __shared__ __align__(1024) uint8_t osm[];
   __shared__ __align__(8) uint64_t full_bar[OZ_STAGES], empty_bar[OZ_STAGES], tfull_bar, tempty_bar;
   __shared__ uint32_t tmem_base;
+  __shared__ int last_flag;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(s_u32(&tmem_base)),
@@ -109,43 +123,38 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
     if (lane == 0) {
       int it = 0;
       for (int ti = offs[blockIdx.x]; ti < offs[blockIdx.x + 1]; ++ti) {
-        const OzTile tl = tiles[ti];
+        const OzItem tl = items[ti];
         const OzShape sh = shapes[tl.shape];
         const int8_t* a = sh.A + (size_t)tl.mt * sh.kchunks * OZ_S * OZ_ABLK;
-        const uint32_t bblk = (uint32_t)sh.w * OZ_KC;
-        const int8_t* b = sh.B + (size_t)tl.nt * sh.kchunks * OZ_S * bblk;
-        const int k0 = tl.kpart * OZ_PART, k1 = min(sh.kchunks, k0 + OZ_PART);
-        for (int kc = k0; kc < k1; ++kc, ++it) {
+        const uint32_t bblk = (uint32_t)sh.R * OZ_KC;
+        const int8_t* b = sh.B + (size_t)tl.nt * sh.kchunks * bblk;
+        for (int kc = tl.k0; kc < tl.k1; ++kc, ++it) {
           const int s = it % OZ_STAGES;
           const uint32_t ph = (it / OZ_STAGES) & 1;
           mbar_wait(&empty_bar[s], ph ^ 1);
           uint8_t* st = osm + s * OZ_STAGE;
-          mbar_expect_tx(&full_bar[s], OZ_S * (OZ_ABLK + bblk));
+          mbar_expect_tx(&full_bar[s], OZ_S * OZ_ABLK + bblk);
           bulk_g2s(st, a + (size_t)kc * OZ_S * OZ_ABLK, OZ_S * OZ_ABLK, &full_bar[s]);
-          bulk_g2s(st + OZ_S * OZ_ABLK, b + (size_t)kc * OZ_S * bblk, OZ_S * bblk, &full_bar[s]);
+          bulk_g2s(st + OZ_S * OZ_ABLK, b + (size_t)kc * bblk, bblk, &full_bar[s]);
         }
       }
     }
   } else if (warp == 5) {
-    // ---------------- MMA issuer.  Level L = p + q accumulates in TMEM columns [(L-2) w, (L-1) w).
-    // The B slices of a stage are stacked along N ([K half][q][w rows]), so for a fixed A slice p
-    // ONE MMA of N = (S+1-p) w against B slices 1..S+1-p feeds levels p+1..S+1 at once (split at
-    // N = 256): S+3 MMAs per K chunk instead of S(S+1)/2, each A block read from smem once per p.
+    // ---------------- MMA issuer
     int it = 0, tcount = 0;
     long long t0 = clock64(), w_full = 0, w_empty = 0, t1;
     for (int ti = offs[blockIdx.x]; ti < offs[blockIdx.x + 1]; ++ti, ++tcount) {
-      const OzTile tl = tiles[ti];
+      const OzItem tl = items[ti];
       const OzShape sh = shapes[tl.shape];
       const int w = sh.w;
-      const int k0 = tl.kpart * OZ_PART, k1 = min(sh.kchunks, k0 + OZ_PART);
-      const uint32_t lbo_b = (uint32_t)OZ_S * w * 16;
-      if (tcount > 0) {   // the epilogue must have drained the accumulators of the previous tile
+      const uint32_t lbo_b = (uint32_t)sh.R * 16;
+      if (tcount > 0) {   // the epilogue must have drained the accumulators of the previous item
         if (prof) t1 = clock64();
         mbar_wait(&tempty_bar, (tcount - 1) & 1);
         if (prof) w_empty += clock64() - t1;
         asm volatile("tcgen05.fence::after_thread_sync;\n");
       }
-      for (int kc = k0; kc < k1; ++kc, ++it) {
+      for (int kc = tl.k0; kc < tl.k1; ++kc, ++it) {
         const int s = it % OZ_STAGES;
         const uint32_t ph = (it / OZ_STAGES) & 1;
         if (prof) t1 = clock64();
@@ -156,15 +165,20 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
           const uint32_t sa = s_u32(osm + s * OZ_STAGE);
           const uint64_t da0 = umma_desc(sa, OZ_M * 16, 128);
           const uint64_t db0 = umma_desc(sa + OZ_S * OZ_ABLK, lbo_b, 128);
-          const bool first = kc == k0;
+          const bool first = kc == tl.k0;
           switch (w) {
+            case 8: issue_chunk<8>(da0, db0, tmem, first); break;
             case 16: issue_chunk<16>(da0, db0, tmem, first); break;
+            case 24: issue_chunk<24>(da0, db0, tmem, first); break;
             case 32: issue_chunk<32>(da0, db0, tmem, first); break;
+            case 40: issue_chunk<40>(da0, db0, tmem, first); break;
             case 48: issue_chunk<48>(da0, db0, tmem, first); break;
-            default: issue_chunk<64>(da0, db0, tmem, first); break;
+            case 56: issue_chunk<56>(da0, db0, tmem, first); break;
+            case 64: issue_chunk<64>(da0, db0, tmem, first); break;
+            default: issue_chunk<72>(da0, db0, tmem, first); break;
           }
-          umma_commit(&empty_bar[s]);                         // stage free once these MMAs retire
-          if (kc == k1 - 1) umma_commit(&tfull_bar);  // accumulators complete
+          umma_commit(&empty_bar[s]);                 // stage free once these MMAs retire
+          if (kc == tl.k1 - 1) umma_commit(&tfull_bar);  // accumulators complete
         }
         __syncwarp();
       }
@@ -179,46 +193,62 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
     // ---------------- epilogue warps 0-3: lane quadrant = warp, one row per thread
     int tcount = 0;
     for (int ti = offs[blockIdx.x]; ti < offs[blockIdx.x + 1]; ++ti, ++tcount) {
-      const OzTile tl = tiles[ti];
+      const OzItem tl = items[ti];
       const OzShape sh = shapes[tl.shape];
+      const int w = sh.w;
       mbar_wait(&tfull_bar, tcount & 1);
       asm volatile("tcgen05.fence::after_thread_sync;\n");
-      const int row = tl.mt * OZ_M + warp * 32 + lane;
+      const int rr = warp * 32 + lane, row = tl.mt * OZ_M + rr;
       const int ea = row < sh.m ? sh.eA[row] : 0;
-      for (int c0 = 0; c0 < sh.w; c0 += 16) {
-        double acc[16];
+      double* part = tl.nseg > 1 ? zpart + (size_t)(tl.slot0 + tl.seg) * OZ_SLOT : nullptr;
+      for (int c0 = 0; c0 < w; c0 += 8) {
+        uint32_t v[OZ_S][8];
+        const uint32_t base = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0;
 #pragma unroll
-        for (int j = 0; j < 16; ++j) acc[j] = 0.0;
+        for (int L = 2; L <= OZ_S + 1; ++L) tmem_ld8(base + (uint32_t)((L - 2) * w), v[L - 2]);
+        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+        double acc[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[j] = 0.0;
 #pragma unroll
         for (int L = OZ_S + 1; L >= 2; --L) {   // smallest terms first
-          uint32_t v[16];
-          const uint32_t addr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)((L - 2) * sh.w + c0);
-          asm volatile(
-              "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, "
-              "[%16];\n"
-              : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-                "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
-                "=r"(v[15])
-              : "r"(addr));
-          asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
           const double wgt = ldexp(1.0, -8 * L);
 #pragma unroll
-          for (int j = 0; j < 16; ++j) acc[j] = fma((double)(int)v[j], wgt, acc[j]);
+          for (int j = 0; j < 8; ++j) acc[j] = fma((double)(int)v[L - 2][j], wgt, acc[j]);
         }
-        if (row < sh.m) {
 #pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            const int n = tl.nt * sh.w + c0 + j;
-            if (n < sh.n) {
-              double* z = sh.Z + (size_t)n * sh.ld + row;
-              const double v = ldexp(acc[j], ea + sh.eB[n] + 4);
-              *z = tl.kpart == 0 ? v : *z + v;   // later K parts: this CTA wrote the earlier ones
-            }
+        for (int j = 0; j < 8; ++j) {
+          const int n = tl.nt * w + c0 + j;
+          const double val = (row < sh.m && n < sh.n) ? ldexp(acc[j], ea + sh.eB[n] + 4) : 0.0;
+          if (part) {
+            part[(c0 + j) * OZ_M + rr] = val;   // [column][row]: coalesced over the warp's rows
+          } else if (row < sh.m && n < sh.n) {
+            sh.Z[(size_t)n * sh.ld + row] = val;
           }
         }
       }
       asm volatile("tcgen05.fence::before_thread_sync;\n");
-      mbar_arrive(&tempty_bar);
+      mbar_arrive(&tempty_bar);   // the MMA warp may overwrite the accumulators now
+      if (tl.nseg > 1) {
+        // split tile: publish this segment, and the last segment to arrive sums all of them in
+        // segment order (deterministic, independent of which CTA finishes last)
+        __threadfence();
+        asm volatile("bar.sync 1, 128;\n" ::: "memory");
+        if (rr == 0) last_flag = atomicAdd(&counters[tl.slot0], 1) == tl.nseg - 1;
+        asm volatile("bar.sync 1, 128;\n" ::: "memory");
+        if (last_flag) {
+          __threadfence();
+          if (row < sh.m)
+            for (int c = 0; c < w; ++c) {
+              const int n = tl.nt * w + c;
+              if (n >= sh.n) break;
+              double sum = 0.0;
+              for (int sg = 0; sg < tl.nseg; ++sg) sum += __ldcg(zpart + (size_t)(tl.slot0 + sg) * OZ_SLOT + c * OZ_M + rr);
+              sh.Z[(size_t)n * sh.ld + row] = sum;
+            }
+          if (rr == 0) counters[tl.slot0] = 0;   // re-armed for the next launch
+        }
+      }
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n");
@@ -231,7 +261,9 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
 // (max|x| < 2^e) and writes the row's S digit bytes per 16-byte K group into the tiled UMMA layout.
 
 // S balanced base-256 digits of one 16-byte K group of row r, written into the tiled UMMA layout
-// of tile height T ([tile][kchunk][S][2 K halves][T/8][8 rows][16 B]; B slices stacked along N)
+// of tile height T.  A operand: [tile][kchunk][S][2 K halves][T/8][8 rows][16 B].  B operand
+// (stacked): [tile][kchunk][2 K halves][R rows][16 B] with slice p in rows [p T, (p+1) T) and
+// zero rows [S T, R) (T a multiple of 8, so every slice starts on an 8-row core matrix).
 __device__ __forceinline__ void ozaki_write_digits(const OzSlice& o, int r, int gk, int e, bool valid) {
   uint32_t w[OZ_S][4];
 #pragma unroll
@@ -249,10 +281,11 @@ __device__ __forceinline__ void ozaki_write_digits(const OzSlice& o, int r, int 
     }
   }
   const int rt = r / o.T, rr = r % o.T, kc = gk / 2, kh = gk % 2;
+  const size_t blk = o.stacked ? (size_t)o.R * OZ_KC : (size_t)OZ_S * o.T * OZ_KC;
   const size_t slice_stride = o.stacked ? (size_t)o.T * 16 : (size_t)o.T * OZ_KC;
-  const size_t half_stride = o.stacked ? (size_t)OZ_S * o.T * 16 : (size_t)o.T * 16;
-  uint8_t* base = reinterpret_cast<uint8_t*>(o.dst) + ((size_t)rt * o.kchunks + kc) * OZ_S * (o.T * OZ_KC) +
-                  kh * half_stride + (rr / 8) * 128 + (rr % 8) * 16;
+  const size_t half_stride = o.stacked ? (size_t)o.R * 16 : (size_t)o.T * 16;
+  uint8_t* base = reinterpret_cast<uint8_t*>(o.dst) + ((size_t)rt * o.kchunks + kc) * blk + kh * half_stride +
+                  (rr / 8) * 128 + (rr % 8) * 16;
 #pragma unroll
   for (int p = 0; p < OZ_S; ++p)
     *reinterpret_cast<uint4*>(base + p * slice_stride) = make_uint4(w[p][0], w[p][1], w[p][2], w[p][3]);
@@ -311,18 +344,20 @@ int ozaki_slice(const OzSlice* d_slices, int count, int64_t rows, int64_t padded
   return 0;
 }
 
+// Column tiles of at most OZ_WMAX columns, as even as possible, width a multiple of 8 (TMEM
+// column offsets and 8-row core matrices of the stacked B): 216 -> 3 x 72, 72 -> 72, 8 -> 8.
 int ozaki_width(int n) {
   const int nt = (n + OZ_WMAX - 1) / OZ_WMAX;
   const int w = nt > 0 ? (n + nt - 1) / nt : 1;
-  return (w + 15) / 16 * 16;
+  return std::min(OZ_WMAX, (w + 7) / 8 * 8);
 }
+int ozaki_stack_rows(int w) { return oz_pad16(OZ_S * w); }
 size_t ozaki_a_bytes(int m, int kchunks) { return (size_t)((m + OZ_M - 1) / OZ_M) * kchunks * OZ_S * OZ_ABLK; }
 size_t ozaki_b_bytes(int n, int kchunks) {
   const int w = ozaki_width(n);
-  return (size_t)((n + w - 1) / w) * kchunks * OZ_S * w * OZ_KC;
+  return (size_t)((n + w - 1) / w) * kchunks * ozaki_stack_rows(w) * OZ_KC;
 }
 int ozaki_kchunks(int m) { return (m + OZ_KC - 1) / OZ_KC; }
-int ozaki_kparts(int kchunks) { return (kchunks + OZ_PART - 1) / OZ_PART; }
 int ozaki_tile_m() { return OZ_M; }
 
 int ozaki_setup() {
@@ -333,63 +368,138 @@ int ozaki_setup() {
 
 static long long* g_oz_prof = nullptr;   // FMP_OZ_PROF=1: per-CTA MMA-warp wait cycles (tools)
 
-int ozaki_launch(const OzShape* shapes, const OzTile* tiles, const int* offs, int grid, cudaStream_t st) {
-  if (grid <= 0) return 0;
+int ozaki_launch(const OzPlan& p, cudaStream_t st) {
+  if (p.grid <= 0) return 0;
   if (!g_oz_prof && getenv_flag("FMP_OZ_PROF")) FMP_CHECK_CUDA(cudaMalloc(&g_oz_prof, 4096 * 4 * sizeof(long long)));
-  k_ozaki<<<grid, OZ_THREADS, OZ_STAGES * OZ_STAGE, st>>>(shapes, tiles, offs, g_oz_prof);
+  k_ozaki<<<p.grid, OZ_THREADS, OZ_STAGES * OZ_STAGE, st>>>(p.shapes, p.items, p.offs, p.zpart, p.counters,
+                                                            g_oz_prof);
   FMP_CHECK_LAUNCH();
   return 0;
 }
 
-// Tensor-pipe cycles of one K chunk of a column tile of width w: per A slice p, one MMA per
-// <= 256 columns of the stacked B slices, each >= ~46 cycles (tools/umma_rate.cu)
+// Cost model of one K chunk (cycles): the tensor pipe (per MMA N/2 cycles, >= ~46 for small N,
+// tools/umma_rate.cu) or shared-memory bandwidth (128 B/clk: stage writes, A re-reads per MMA,
+// stacked-B reads), whichever is larger.
 static double chunk_cycles(int w) {
-  double c = 0.0;
+  double tensor = 0.0, bytes = OZ_S * OZ_ABLK + ozaki_stack_rows(w) * OZ_KC;
   for (int p = 1; p <= OZ_S; ++p)
-    for (int n = (OZ_S + 1 - p) * w; n > 0; n -= 256) c += std::max(46.0, std::min(n, 256) / 2.0);
-  return c;
+    for (int n = oz_pad16((OZ_S + 1 - p) * w); n > 0; n -= 256) {
+      const int nn = std::min(n, 256);
+      tensor += std::max(46.0, nn / 2.0);
+      bytes += OZ_ABLK + nn * OZ_KC;
+    }
+  return std::max(tensor, bytes / 128.0);
 }
 
-void ozaki_schedule(const std::vector<OzShape>& shapes, std::vector<OzTile>& tiles, int grid, std::vector<int>& offs) {
-  // longest-processing-time-first assignment of tiles to the persistent CTAs; equal-cost tiles
-  // keep their (shape, row tile, column tile) order, so CTAs working at the same time still
-  // share C^-1 row tiles in L2.  Each CTA then walks its list in the original order.
-  std::vector<double> cost(tiles.size());
-  for (size_t i = 0; i < tiles.size(); ++i) {
-    const OzShape& sh = shapes[tiles[i].shape];
-    const int k0 = tiles[i].kpart * OZ_PART;
-    cost[i] = std::min(OZ_PART, sh.kchunks - k0) * chunk_cycles(sh.w);
-  }
-  // the K parts of one (shape, row tile, column tile) are one unit: same CTA, original order
-  std::vector<int> unit_of(tiles.size());
-  std::vector<double> ucost;
-  for (size_t i = 0; i < tiles.size(); ++i) {
-    const bool same = i > 0 && tiles[i].shape == tiles[i - 1].shape && tiles[i].mt == tiles[i - 1].mt &&
-                      tiles[i].nt == tiles[i - 1].nt;
-    if (!same) ucost.push_back(0.0);
-    unit_of[i] = (int)ucost.size() - 1;
-    ucost.back() += cost[i];
-  }
-  std::vector<int> order(ucost.size());
+// Longest-processing-time assignment that keeps equal-cost items in their list order, so the CTAs
+// running at the same time hold consecutive items (same row tile and K segment, neighbouring
+// column tiles: their C^-1 slices are read from DRAM once and shared in L2).  Returns the makespan.
+static double lpt(const std::vector<double>& cost, int grid, std::vector<int>* cta_of) {
+  std::vector<int> order(cost.size());
   for (size_t i = 0; i < order.size(); ++i) order[i] = (int)i;
-  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return ucost[a] > ucost[b]; });
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return cost[a] > cost[b]; });
   std::vector<double> load(grid, 0.0);
-  std::vector<int> cta_of_unit(ucost.size());
+  if (cta_of) cta_of->assign(cost.size(), 0);
   for (int u : order) {
     const int c = (int)(std::min_element(load.begin(), load.end()) - load.begin());
-    load[c] += ucost[u];
-    cta_of_unit[u] = c;
+    load[c] += cost[u];
+    if (cta_of) (*cta_of)[u] = c;
   }
+  return *std::max_element(load.begin(), load.end());
+}
+
+int ozaki_build(const std::vector<OzShape>& shapes, int sms, OzPlan* out) {
+  *out = OzPlan{};
+  // tiles (shape, row tile, column tile) and their K-chunk counts and per-chunk cost
+  struct T { int shape, mt, nt, kc; double cc; };
+  std::vector<T> tiles;
+  double total = 0.0;
+  for (size_t s = 0; s < shapes.size(); ++s) {
+    const OzShape& sh = shapes[s];
+    if (sh.n <= 0 || !sh.A) continue;
+    const double cc = chunk_cycles(sh.w);
+    for (int mt = 0; mt * OZ_M < sh.m; ++mt)
+      for (int nt = 0; nt * sh.w < sh.n; ++nt) {
+        tiles.push_back(T{(int)s, mt, nt, sh.kchunks, cc});
+        total += cc * sh.kchunks;
+      }
+  }
+  if (tiles.empty()) return 0;
+  const int grid = std::min<int>(sms, (int)tiles.size() * 8);
+  // K segments per tile: q target rounds of equal items; each item also pays an epilogue (TMEM
+  // drain, partial store/fix-up, ~4000 cycles).  Pick the q with the smallest modelled makespan.
+  const double epi = 4000.0;
+  std::vector<OzItem> best_items;
+  double best = 1e300;
+  for (int q = 1; q <= 12; ++q) {
+    const double unit = total / ((double)grid * q);
+    std::vector<OzItem> items;
+    std::vector<double> cost;
+    int slots = 0;
+    // order: shape, row tile, K segment, column tile (concurrent items share C^-1 row tiles)
+    size_t t0 = 0;
+    while (t0 < tiles.size()) {
+      size_t t1 = t0;
+      while (t1 < tiles.size() && tiles[t1].shape == tiles[t0].shape && tiles[t1].mt == tiles[t0].mt) ++t1;
+      const T& tt = tiles[t0];
+      const int kc = tt.kc;
+      int nseg = std::max(1, (int)std::lround(tt.cc * kc / unit));
+      nseg = std::max(nseg, (kc + OZ_PART - 1) / OZ_PART);
+      nseg = std::min(nseg, kc);
+      for (int sg = 0; sg < nseg; ++sg) {
+        const int k0 = (int)((int64_t)kc * sg / nseg), k1 = (int)((int64_t)kc * (sg + 1) / nseg);
+        for (size_t t = t0; t < t1; ++t) {
+          const int slot0 = nseg > 1 ? slots + (int)(t - t0) * nseg : 0;
+          items.push_back(OzItem{tiles[t].shape, tiles[t].mt, tiles[t].nt, k0, k1, sg, nseg, slot0});
+          cost.push_back(tiles[t].cc * (k1 - k0) + epi);
+        }
+      }
+      if (nseg > 1) slots += (int)(t1 - t0) * nseg;
+      t0 = t1;
+    }
+    const double mk = lpt(cost, grid, nullptr);
+    if (mk < best * 0.995) {
+      best = mk;
+      best_items.swap(items);
+      out->n_slots = slots;
+    }
+  }
+  std::vector<double> cost;
+  for (const auto& it : best_items) cost.push_back(shapes[it.shape].A ? chunk_cycles(shapes[it.shape].w) * (it.k1 - it.k0) + epi : 0.0);
+  std::vector<int> cta_of;
+  lpt(cost, grid, &cta_of);
   std::vector<std::vector<int>> lists(grid);
-  for (size_t i = 0; i < tiles.size(); ++i) lists[cta_of_unit[unit_of[i]]].push_back((int)i);
-  std::vector<OzTile> out;
-  offs.assign(1, 0);
+  for (size_t i = 0; i < best_items.size(); ++i) lists[cta_of[i]].push_back((int)i);
+  std::vector<OzItem> items;
+  std::vector<int> offs(1, 0);
   for (auto& l : lists) {
     std::sort(l.begin(), l.end());
-    for (int i : l) out.push_back(tiles[i]);
-    offs.push_back((int)out.size());
+    for (int i : l) items.push_back(best_items[i]);
+    offs.push_back((int)items.size());
   }
-  tiles.swap(out);
+  out->grid = grid;
+  out->n_items = (int)items.size();
+  FMP_CHECK_CUDA(cudaMalloc(&out->shapes, sizeof(OzShape) * shapes.size()));
+  FMP_CHECK_CUDA(cudaMemcpy(out->shapes, shapes.data(), sizeof(OzShape) * shapes.size(), cudaMemcpyHostToDevice));
+  FMP_CHECK_CUDA(cudaMalloc(&out->items, sizeof(OzItem) * items.size()));
+  FMP_CHECK_CUDA(cudaMemcpy(out->items, items.data(), sizeof(OzItem) * items.size(), cudaMemcpyHostToDevice));
+  FMP_CHECK_CUDA(cudaMalloc(&out->offs, sizeof(int) * offs.size()));
+  FMP_CHECK_CUDA(cudaMemcpy(out->offs, offs.data(), sizeof(int) * offs.size(), cudaMemcpyHostToDevice));
+  if (out->n_slots > 0) {
+    FMP_CHECK_CUDA(cudaMalloc(&out->zpart, sizeof(double) * OZ_SLOT * (size_t)out->n_slots));
+    FMP_CHECK_CUDA(cudaMalloc(&out->counters, sizeof(int) * out->n_slots));
+    FMP_CHECK_CUDA(cudaMemset(out->counters, 0, sizeof(int) * out->n_slots));
+  }
+  return 0;
+}
+
+void ozaki_free(OzPlan* p) {
+  cudaFree(p->shapes);
+  cudaFree(p->items);
+  cudaFree(p->offs);
+  cudaFree(p->zpart);
+  cudaFree(p->counters);
+  *p = OzPlan{};
 }
 
 }  // namespace fmp

@@ -9,13 +9,26 @@ namespace fmp {
 struct OzShape {
   const int8_t* A;   // tiled slices of C^-1: [mtile][kchunk][S][128 x 32 B]
   const int* eA;     // [m] row exponents of C^-1
-  const int8_t* B;   // tiled slices of Y: [ntile][kchunk][S][w x 32 B]
+  const int8_t* B;   // tiled slices of Y: [ntile][kchunk][2 K halves][R stacked rows x 16 B]
   const int* eB;     // [n] row exponents of Y^T
   double* Z;         // [n][ld]
-  int m, n, ld, kchunks, w, pad;   // w: column-tile width (multiple of 16, S*w <= 512)
+  int m, n, ld, kchunks, w, R;   // w: column-tile width (multiple of 8, <= 72); R = pad16(S w) stacked B rows
 };
-struct OzTile {
-  int shape, mt, nt, kpart;   // kpart: K part (chunks [kpart * 512, ...)) for K > 16384
+// One work item: K chunks [k0, k1) of column tile nt of row tile mt.  A tile whose K range is
+// split into nseg > 1 segments (load balance, or K > 16384 int32 headroom) writes per-segment FP64
+// partials to partial slots slot0 + seg; the last segment to finish sums them in segment order
+// (deterministic) into Z.  nseg == 1: the item writes Z directly.
+struct OzItem {
+  int shape, mt, nt, k0, k1, seg, nseg, slot0;
+};
+// Device tables of one batched Ozaki GEMM (all rotation groups of a plan).
+struct OzPlan {
+  OzShape* shapes = nullptr;
+  OzItem* items = nullptr;
+  int* offs = nullptr;        // CTA b runs items [offs[b], offs[b+1])
+  double* zpart = nullptr;    // [slots][OZ_WMAX][128] partial results of split tiles
+  int* counters = nullptr;    // [slots] arrivals per split tile (slot0), zero at rest
+  int grid = 0, n_items = 0, n_slots = 0;
 };
 // One operand to slice: rows x kvalid doubles (row stride ld) -> tiles of height T.
 struct OzSlice {
@@ -23,22 +36,25 @@ struct OzSlice {
   int8_t* dst;
   int* exps;
   int rows, ld, kvalid, kchunks, T, stacked;   // stacked = 1: slices stacked along N (B operand)
+  int R;              // stacked: rows per K half of a (tile, kchunk) block (>= S * T, zero padding)
   int64_t row0, q0;   // prefix offsets of this operand in the batched exponent / digit grids
   int64_t prow0;      // prefix of padded rows (tile multiples) in the batched slicing grid
 };
 
 int ozaki_setup();
 int ozaki_kchunks(int m);
-int ozaki_kparts(int kchunks);                 // K parts of <= 16384 bytes (int32 level headroom)
 int ozaki_tile_m();
 int ozaki_width(int n);                       // column-tile width for n columns
+int ozaki_stack_rows(int w);                  // R: stacked B rows of a column tile of width w
 size_t ozaki_a_bytes(int m, int kchunks);
 size_t ozaki_b_bytes(int n, int kchunks);
 // Fill row0/q0/prow0 of a batch; returns the total rows and padded rows (the slicing grid).
 void ozaki_plan_slices(OzSlice* s, int count, int64_t* rows, int64_t* padded_rows);
 int ozaki_slice(const OzSlice* d_slices, int count, int64_t rows, int64_t padded_rows, cudaStream_t st);
-// tiles reordered into per-CTA lists (CTA b runs tiles [offs[b], offs[b+1])), balanced by cost
-void ozaki_schedule(const std::vector<OzShape>& shapes, std::vector<OzTile>& tiles, int grid, std::vector<int>& offs);
-int ozaki_launch(const OzShape* shapes, const OzTile* tiles, const int* offs, int grid, cudaStream_t st);
+// Work items (column tiles x K segments) for the shapes (entries with n == 0 are skipped), balanced
+// over `sms` persistent CTAs, uploaded with the partial-slot workspace.  Returns 0 or -1.
+int ozaki_build(const std::vector<OzShape>& shapes, int sms, OzPlan* out);
+void ozaki_free(OzPlan* p);
+int ozaki_launch(const OzPlan& p, cudaStream_t st);
 
 }  // namespace fmp

@@ -1661,11 +1661,7 @@ struct fmp_precond {
   bool use_ozaki = true;
   std::vector<int8_t*> oz_a, oz_b;
   std::vector<int*> oz_ea, oz_eb;
-  OzShape* d_ozshapes = nullptr;
-  OzTile* d_oztiles = nullptr;
-  int* d_ozoffs = nullptr;                // per-CTA tile list offsets (ozaki_schedule)
-  int oz_grid = 0;
-  int n_oztiles = 0;
+  OzPlan oz;                              // work items, schedule and split-K workspace
   OzSlice* d_ozslices = nullptr;          // per-apply slicing of Y, all shapes in two launches
   int n_ozslices = 0;
   int64_t oz_rows = 0, oz_threads = 0;
@@ -1719,9 +1715,7 @@ static void free_plan(fmp_precond* p) {
   for (auto* q : p->oz_b) cudaFree(q);
   for (auto* q : p->oz_ea) cudaFree(q);
   for (auto* q : p->oz_eb) cudaFree(q);
-  cudaFree(p->d_ozshapes);
-  cudaFree(p->d_oztiles);
-  cudaFree(p->d_ozoffs);
+  ozaki_free(&p->oz);
   cudaFree(p->d_ozslices);
   for (int c = 0; c < 3; ++c) cudaFree(p->d_gtiles[c]);
   delete p;
@@ -1903,7 +1897,6 @@ extern "C" int fmp_precond_create(const fmp_precond_desc* desc, fmp_precond** ou
   if (p->use_ozaki && have_cinv) {   // slices of C^-1 (setup), buffers for the slices of Y
     if (ozaki_setup()) { free_plan(p); return -1; }
     std::vector<OzShape> os;
-    std::vector<OzTile> ot;
     std::vector<OzSlice> sa, sb;
     for (int64_t s2 = 0; s2 < desc->n_shape; ++s2) {
       const auto& sh = p->shapes[s2];
@@ -1917,7 +1910,8 @@ extern "C" int fmp_precond_create(const fmp_precond_desc* desc, fmp_precond** ou
       int *ea = nullptr, *eb = nullptr;
       const size_t ab = ozaki_a_bytes(m, kc), bb = ozaki_b_bytes(std::max(n, 1), kc);
       if (cudaMalloc(&a, ab) != cudaSuccess || cudaMalloc(&b, bb) != cudaSuccess ||
-          cudaMalloc(&ea, sizeof(int) * m) != cudaSuccess || cudaMalloc(&eb, sizeof(int) * std::max(n, 1)) != cudaSuccess) {
+          cudaMalloc(&ea, sizeof(int) * m) != cudaSuccess || cudaMalloc(&eb, sizeof(int) * std::max(n, 1)) != cudaSuccess ||
+          cudaMemset(b, 0, bb) != cudaSuccess) {   // the stacked rows past S w stay zero
         free_plan(p);
         FMP_REQUIRE(false, "cudaMalloc of Ozaki slices failed");
       }
@@ -1925,22 +1919,15 @@ extern "C" int fmp_precond_create(const fmp_precond_desc* desc, fmp_precond** ou
       p->oz_b.push_back(b);
       p->oz_ea.push_back(ea);
       p->oz_eb.push_back(eb);
-      sa.push_back(OzSlice{p->cinv[s2], a, ea, m, (int)sh.ld, m, kc, ozaki_tile_m(), 0, 0, 0});
-      if (n > 0) sb.push_back(OzSlice{p->ymat[s2], b, eb, n, (int)sh.ld, m, kc, w, 1, 0, 0});
-      os.push_back(OzShape{a, ea, b, eb, p->zmat[s2], m, n, (int)sh.ld, kc, w, 0});
-      for (int mt = 0; mt * ozaki_tile_m() < m; ++mt)
-        for (int nt = 0; nt * w < n; ++nt)
-          for (int kp = 0; kp < ozaki_kparts(kc); ++kp) ot.push_back(OzTile{(int)s2, mt, nt, kp});
+      sa.push_back(OzSlice{p->cinv[s2], a, ea, m, (int)sh.ld, m, kc, ozaki_tile_m(), 0, 0, 0, 0, 0});
+      if (n > 0) sb.push_back(OzSlice{p->ymat[s2], b, eb, n, (int)sh.ld, m, kc, w, 1, ozaki_stack_rows(w), 0, 0, 0});
+      os.push_back(OzShape{a, ea, b, eb, p->zmat[s2], m, n, (int)sh.ld, kc, w, ozaki_stack_rows(w)});
     }
     int64_t ra = 0, qa = 0;
     ozaki_plan_slices(sa.data(), (int)sa.size(), &ra, &qa);
     ozaki_plan_slices(sb.data(), (int)sb.size(), &p->oz_rows, &p->oz_threads);
     OzSlice* d_sa = nullptr;
-    p->oz_grid = std::min<int>((int)ot.size(), p->sms);
-    std::vector<int> offs;
-    ozaki_schedule(os, ot, p->oz_grid, offs);
-    if (upload(sa, &d_sa) || upload(sb, &p->d_ozslices) || upload(os, &p->d_ozshapes) || upload(ot, &p->d_oztiles) ||
-        upload(offs, &p->d_ozoffs)) {
+    if (upload(sa, &d_sa) || upload(sb, &p->d_ozslices) || ozaki_build(os, p->sms, &p->oz)) {
       cudaFree(d_sa);
       free_plan(p);
       return -1;
@@ -1950,7 +1937,6 @@ extern "C" int fmp_precond_create(const fmp_precond_desc* desc, fmp_precond** ou
     cudaDeviceSynchronize();
     cudaFree(d_sa);
     if (rc) { free_plan(p); return -1; }
-    p->n_oztiles = (int)ot.size();
     FMP_CHECK_CUDA(cudaDeviceSynchronize());
   }
   if (cublasCreate(&p->blas) != CUBLAS_STATUS_SUCCESS) {
@@ -2171,8 +2157,8 @@ static int precond_apply(fmp_precond* p, const fmp_block* blk, int mode, int par
   // boundary part is the pass over the others and everything after it.  (The general kernels and
   // FACES mode run whole in the boundary part.)
   const bool split = p->fast && mode != FMP_SOLVE_FACES;
+  if (part != FMP_PART_BOUNDARY) mark(0);   // split: stage 0 spans interior pass, ghost wait, boundary pass
   if (part == FMP_PART_INTERIOR) return split ? plane_pass(p, blk, false, mode, r, wa, st, FMP_PART_INTERIOR) : 0;
-  if (part != FMP_PART_BOUNDARY) mark(0);
   if (int e = plane_pass(p, blk, false, mode, r, wa, st, split ? part : FMP_PART_ALL)) return e;
   mark(1);
   if (int e = column_pass(p, false, wa, wb, nullptr, st)) return e;
@@ -2216,10 +2202,10 @@ static int precond_apply(fmp_precond* p, const fmp_block* blk, int mode, int par
         FMP_CHECK_CUDA(cudaStreamWaitEvent(st, p->ev_join[q], 0));
       }
     } else if (p->use_ozaki) {
-      FMP_REQUIRE(p->d_ozshapes != nullptr, "Ozaki GEMM requested but the plan has no C^-1");
+      FMP_REQUIRE(p->oz.shapes != nullptr, "Ozaki GEMM requested but the plan has no C^-1");
       if (int e = ozaki_slice(p->d_ozslices, p->n_ozslices, p->oz_rows, p->oz_threads, st)) return e;
       mark(4);
-      if (int e = ozaki_launch(p->d_ozshapes, p->d_oztiles, p->d_ozoffs, p->oz_grid, st)) return e;
+      if (int e = ozaki_launch(p->oz, st)) return e;
     } else {
       for (int c = 0; c < 3; ++c)
         if (int e = gemm_launch(c, p->d_gshapes, p->d_gtiles[c], p->n_gtiles[c], p->sms, st)) return e;
