@@ -52,14 +52,21 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint
          ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | ((uint64_t)1 << 46);   // version 1, SWIZZLE_NONE
 }
 
+// The MMA warp runs its loop with all 32 lanes converged; each tcgen05 instruction is issued by
+// the lane elect.sync picks inside the same asm block.  (Issuing under `if (lane == 0)` made
+// ptxas wrap every MMA in an ELECT / BRA.U.ANY loop with an R2UR per operand: ~50 extra cycles
+// per MMA, tools/umma_chunk.cu.)  elect.sync picks the same lane every time, so the commits
+// track the MMAs of the thread that issued them.
 __device__ __forceinline__ void umma_commit(uint64_t* b) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(s_u32(b))
-               : "memory");
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}\n" ::"r"(s_u32(b))
+      : "memory");
 }
 __device__ __forceinline__ void umma_i8(uint32_t tmem, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
   asm volatile(
-      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem),
+      "{\n\t.reg .pred p, e;\n\tsetp.ne.b32 p, %4, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem),
       "l"(da), "l"(db), "r"(idesc), "r"(acc));
 }
 
@@ -76,9 +83,14 @@ __device__ __forceinline__ void issue_chunk(uint64_t da0, uint64_t db0, uint32_t
     const uint64_t da = da0 + (uint64_t)(((p - 1) * OZ_ABLK) >> 4);
     const uint32_t acc = (first && p == 1) ? 0u : 1u;
     const int N = oz_pad16((OZ_S + 1 - p) * W);
+    // N > 256 is split into near-equal parts (multiples of 16): an MMA costs max(N/2, ~50) cycles,
+    // so 288 -> 144 + 144 beats 256 + 32 (tools/umma_chunk.cu)
+    constexpr int kMax = 256;
+    const int parts = (N + kMax - 1) / kMax;
+    const int step = oz_pad16((N + parts - 1) / parts);
 #pragma unroll
-    for (int r0 = 0; r0 < N; r0 += 256) {
-      const int nn = (N - r0) < 256 ? (N - r0) : 256;
+    for (int r0 = 0; r0 < N; r0 += step) {
+      const int nn = (N - r0) < step ? (N - r0) : step;
       umma_i8(tmem + (uint32_t)((p - 1) * W + r0), da, db0 + (uint64_t)((r0 * 16) >> 4),
               IDESC0 | ((uint32_t)(nn >> 3) << 17), acc);
     }
@@ -93,11 +105,12 @@ __device__ __forceinline__ void tmem_ld8(uint32_t addr, uint32_t (&v)[8]) {
 
 __global__ void __launch_bounds__(OZ_THREADS, 1)
     k_ozaki(const OzShape* __restrict__ shapes, const OzItem* __restrict__ items, const int* __restrict__ offs,
-            double* __restrict__ zpart, int* __restrict__ counters, long long* __restrict__ prof) {
+            double* __restrict__ zpart, int* __restrict__ counters, long long* __restrict__ prof, int dbg) {
   extern __shared__ __align__(1024) uint8_t osm[];
   __shared__ __align__(8) uint64_t full_bar[OZ_STAGES], empty_bar[OZ_STAGES], tfull_bar, tempty_bar;
   __shared__ uint32_t tmem_base;
   __shared__ int last_flag;
+  __shared__ int eb_sh[OZ_WMAX];   // column exponents (+4) of the epilogue's current item
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(s_u32(&tmem_base)),
@@ -132,6 +145,10 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
           const int s = it % OZ_STAGES;
           const uint32_t ph = (it / OZ_STAGES) & 1;
           mbar_wait(&empty_bar[s], ph ^ 1);
+          if (dbg & 1) {   // FMP_OZ_DBG=1 (timing diagnostics only, wrong results): no operand loads
+            mbar_arrive(&full_bar[s]);
+            continue;
+          }
           uint8_t* st = osm + s * OZ_STAGE;
           mbar_expect_tx(&full_bar[s], OZ_S * OZ_ABLK + bblk);
           bulk_g2s(st, a + (size_t)kc * OZ_S * OZ_ABLK, OZ_S * OZ_ABLK, &full_bar[s]);
@@ -161,12 +178,12 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
         mbar_wait(&full_bar[s], ph);
         if (prof) w_full += clock64() - t1;
         asm volatile("tcgen05.fence::after_thread_sync;\n");
-        if (lane == 0) {
+        {
           const uint32_t sa = s_u32(osm + s * OZ_STAGE);
           const uint64_t da0 = umma_desc(sa, OZ_M * 16, 128);
           const uint64_t db0 = umma_desc(sa + OZ_S * OZ_ABLK, lbo_b, 128);
           const bool first = kc == tl.k0;
-          switch (w) {
+          if (!(dbg & 2)) switch (w) {   // FMP_OZ_DBG=2: no MMAs
             case 8: issue_chunk<8>(da0, db0, tmem, first); break;
             case 16: issue_chunk<16>(da0, db0, tmem, first); break;
             case 24: issue_chunk<24>(da0, db0, tmem, first); break;
@@ -196,11 +213,21 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
       const OzItem tl = items[ti];
       const OzShape sh = shapes[tl.shape];
       const int w = sh.w;
+      const int rr = warp * 32 + lane, row = tl.mt * OZ_M + rr;
+      // operand exponents of this item, fetched while the MMAs still run: the row's into a
+      // register, the tile's column exponents into shared memory (one global load per column
+      // instead of one dependent L2 round trip per 8 columns inside the drain loop)
+      const int ea = row < sh.m ? sh.eA[row] : 0;
+      asm volatile("bar.sync 1, 128;\n" ::: "memory");   // previous item's readers of eb_sh are done
+      if (rr < w) {
+        const int n = tl.nt * w + rr;
+        eb_sh[rr] = n < sh.n ? sh.eB[n] + 4 : 0;
+      }
+      asm volatile("bar.sync 1, 128;\n" ::: "memory");
+      double* part = tl.nseg > 1 ? zpart + (size_t)(tl.slot0 + tl.seg) * OZ_SLOT : nullptr;
+      const int nvalid = min(w, sh.n - tl.nt * w);
       mbar_wait(&tfull_bar, tcount & 1);
       asm volatile("tcgen05.fence::after_thread_sync;\n");
-      const int rr = warp * 32 + lane, row = tl.mt * OZ_M + rr;
-      const int ea = row < sh.m ? sh.eA[row] : 0;
-      double* part = tl.nseg > 1 ? zpart + (size_t)(tl.slot0 + tl.seg) * OZ_SLOT : nullptr;
       for (int c0 = 0; c0 < w; c0 += 8) {
         uint32_t v[OZ_S][8];
         const uint32_t base = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0;
@@ -218,12 +245,13 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
         }
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-          const int n = tl.nt * w + c0 + j;
-          const double val = (row < sh.m && n < sh.n) ? ldexp(acc[j], ea + sh.eB[n] + 4) : 0.0;
+          const int c = c0 + j;
+          const bool ok = row < sh.m && c < nvalid;
+          const double val = ok ? ldexp(acc[j], ea + eb_sh[c]) : 0.0;
           if (part) {
-            part[(c0 + j) * OZ_M + rr] = val;   // [column][row]: coalesced over the warp's rows
-          } else if (row < sh.m && n < sh.n) {
-            sh.Z[(size_t)n * sh.ld + row] = val;
+            part[c * OZ_M + rr] = val;   // [column][row]: coalesced over the warp's rows
+          } else if (ok) {
+            sh.Z[(size_t)(tl.nt * w + c) * sh.ld + row] = val;
           }
         }
       }
@@ -238,14 +266,32 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
         asm volatile("bar.sync 1, 128;\n" ::: "memory");
         if (last_flag) {
           __threadfence();
-          if (row < sh.m)
-            for (int c = 0; c < w; ++c) {
-              const int n = tl.nt * w + c;
-              if (n >= sh.n) break;
-              double sum = 0.0;
-              for (int sg = 0; sg < tl.nseg; ++sg) sum += __ldcg(zpart + (size_t)(tl.slot0 + sg) * OZ_SLOT + c * OZ_M + rr);
-              sh.Z[(size_t)n * sh.ld + row] = sum;
+          if (row < sh.m) {
+            const double* src = zpart + (size_t)tl.slot0 * OZ_SLOT + rr;
+            for (int c0 = 0; c0 < nvalid; c0 += 8) {   // 8 columns x 2 segments of loads in flight
+              double s[8];
+#pragma unroll
+              for (int j = 0; j < 8; ++j) s[j] = 0.0;
+              int sg = 0;
+              for (; sg + 1 < tl.nseg; sg += 2) {
+                double v0[8], v1[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                  v0[j] = __ldcg(src + (size_t)sg * OZ_SLOT + (c0 + j) * OZ_M);
+                  v1[j] = __ldcg(src + (size_t)(sg + 1) * OZ_SLOT + (c0 + j) * OZ_M);
+                }
+#pragma unroll
+                for (int j = 0; j < 8; ++j) s[j] = (s[j] + v0[j]) + v1[j];
+              }
+              if (sg < tl.nseg) {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) s[j] += __ldcg(src + (size_t)sg * OZ_SLOT + (c0 + j) * OZ_M);
+              }
+#pragma unroll
+              for (int j = 0; j < 8; ++j)
+                if (c0 + j < nvalid) sh.Z[(size_t)(tl.nt * w + c0 + j) * sh.ld + row] = s[j];
             }
+          }
           if (rr == 0) counters[tl.slot0] = 0;   // re-armed for the next launch
         }
       }
@@ -371,114 +417,135 @@ static long long* g_oz_prof = nullptr;   // FMP_OZ_PROF=1: per-CTA MMA-warp wait
 int ozaki_launch(const OzPlan& p, cudaStream_t st) {
   if (p.grid <= 0) return 0;
   if (!g_oz_prof && getenv_flag("FMP_OZ_PROF")) FMP_CHECK_CUDA(cudaMalloc(&g_oz_prof, 4096 * 4 * sizeof(long long)));
+  static const int dbg = getenv("FMP_OZ_DBG") ? atoi(getenv("FMP_OZ_DBG")) : 0;
   k_ozaki<<<p.grid, OZ_THREADS, OZ_STAGES * OZ_STAGE, st>>>(p.shapes, p.items, p.offs, p.zpart, p.counters,
-                                                            g_oz_prof);
+                                                            g_oz_prof, dbg);
   FMP_CHECK_LAUNCH();
   return 0;
 }
 
-// Cost model of one K chunk (cycles): the tensor pipe (per MMA N/2 cycles, >= ~46 for small N,
-// tools/umma_rate.cu) or shared-memory bandwidth (128 B/clk: stage writes, A re-reads per MMA,
-// stacked-B reads), whichever is larger.
+// Cost model of one K chunk (cycles): each MMA of the chunk costs max(N/2, 50) on the tensor pipe
+// (tools/umma_chunk.cu: N/2 for N >= 128, a ~50-cycle floor below), with the same N splits as
+// issue_chunk.  Only the ratios matter (w = 72 vs w = 8 tiles); the absolute rate is ~14% slower.
 static double chunk_cycles(int w) {
-  double tensor = 0.0, bytes = OZ_S * OZ_ABLK + ozaki_stack_rows(w) * OZ_KC;
-  for (int p = 1; p <= OZ_S; ++p)
-    for (int n = oz_pad16((OZ_S + 1 - p) * w); n > 0; n -= 256) {
-      const int nn = std::min(n, 256);
-      tensor += std::max(46.0, nn / 2.0);
-      bytes += OZ_ABLK + nn * OZ_KC;
-    }
-  return std::max(tensor, bytes / 128.0);
-}
-
-// Longest-processing-time assignment that keeps equal-cost items in their list order, so the CTAs
-// running at the same time hold consecutive items (same row tile and K segment, neighbouring
-// column tiles: their C^-1 slices are read from DRAM once and shared in L2).  Returns the makespan.
-static double lpt(const std::vector<double>& cost, int grid, std::vector<int>* cta_of) {
-  std::vector<int> order(cost.size());
-  for (size_t i = 0; i < order.size(); ++i) order[i] = (int)i;
-  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return cost[a] > cost[b]; });
-  std::vector<double> load(grid, 0.0);
-  if (cta_of) cta_of->assign(cost.size(), 0);
-  for (int u : order) {
-    const int c = (int)(std::min_element(load.begin(), load.end()) - load.begin());
-    load[c] += cost[u];
-    if (cta_of) (*cta_of)[u] = c;
+  double tensor = 0.0;
+  for (int p = 1; p <= OZ_S; ++p) {
+    const int N = oz_pad16((OZ_S + 1 - p) * w);
+    const int parts = (N + 255) / 256, step = oz_pad16((N + parts - 1) / parts);
+    for (int r0 = 0; r0 < N; r0 += step) tensor += std::max(50.0, std::min(step, N - r0) / 2.0);
   }
-  return *std::max_element(load.begin(), load.end());
+  return tensor;
 }
 
+// Work plan of one batched GEMM over the persistent CTAs (data-parallel waves + a stream-K
+// remainder, after Osama et al.'s hybrid):
+//  * a "tile" is (shape, 128-row tile mt, column tile nt); tiles whose K exceeds the int32 level
+//    headroom (OZ_PART chunks) are cut into K parts first;
+//  * "shared" parts belong to shapes with several column tiles.  They go round-robin in
+//    (shape, mt, K part, nt) order, in F = floor(shared / grid) waves, so the CTAs of one wave that
+//    hold the column tiles of one row tile stream the same C^-1 slice chunks at the same time (one
+//    DRAM read, L2 hits for the siblings);
+//  * the remaining shared parts and the "solo" parts (shapes with one column tile, e.g. 72 or 8
+//    columns: C^-1 read from DRAM for few columns, HBM-heavy) are laid end to end by K chunk and
+//    cut into `grid` ranges of equal modelled cost, one piece per CTA.  Each team of 3 CTAs runs
+//    its piece at a different position among its waves (before wave (b/3) mod (F+1)), so the
+//    HBM-heavy pieces are spread over the launch instead of all landing at its end;
+//  * a tile cut into several segments is completed by the last segment to finish (partials summed
+//    in segment order: deterministic).
 int ozaki_build(const std::vector<OzShape>& shapes, int sms, OzPlan* out) {
   *out = OzPlan{};
-  // tiles (shape, row tile, column tile) and their K-chunk counts and per-chunk cost
-  struct T { int shape, mt, nt, kc; double cc; };
-  std::vector<T> tiles;
-  double total = 0.0;
+  struct Part { int shape, mt, nt, k0, k1, tile; double cc; };
+  std::vector<Part> shared, solo;
+  const char* sv = getenv("FMP_OZ_SOLO");   // modelled floor (cycles per chunk) of a solo chunk
+  const double solo_min = sv ? atof(sv) : 800.0;
+  int n_tiles = 0;
   for (size_t s = 0; s < shapes.size(); ++s) {
     const OzShape& sh = shapes[s];
     if (sh.n <= 0 || !sh.A) continue;
-    const double cc = chunk_cycles(sh.w);
-    for (int mt = 0; mt * OZ_M < sh.m; ++mt)
-      for (int nt = 0; nt * sh.w < sh.n; ++nt) {
-        tiles.push_back(T{(int)s, mt, nt, sh.kchunks, cc});
-        total += cc * sh.kchunks;
+    const int nts = (sh.n + sh.w - 1) / sh.w;
+    const double cc = nts > 1 ? chunk_cycles(sh.w) : std::max(solo_min, chunk_cycles(sh.w));
+    const int kparts = (sh.kchunks + OZ_PART - 1) / OZ_PART;
+    for (int mt = 0; mt * OZ_M < sh.m; ++mt) {
+      for (int kp = 0; kp < kparts; ++kp) {
+        const int k0 = (int)((int64_t)sh.kchunks * kp / kparts), k1 = (int)((int64_t)sh.kchunks * (kp + 1) / kparts);
+        for (int nt = 0; nt < nts; ++nt)
+          (nts > 1 ? shared : solo).push_back(Part{(int)s, mt, nt, k0, k1, n_tiles + nt, cc});
       }
+      n_tiles += nts;
+    }
   }
-  if (tiles.empty()) return 0;
-  const int grid = std::min<int>(sms, (int)tiles.size() * 8);
-  // K segments per tile: q target rounds of equal items; each item also pays an epilogue (TMEM
-  // drain, partial store/fix-up, ~4000 cycles).  Pick the q with the smallest modelled makespan.
-  const double epi = 4000.0;
-  std::vector<OzItem> best_items;
-  double best = 1e300;
-  for (int q = 1; q <= 12; ++q) {
-    const double unit = total / ((double)grid * q);
-    std::vector<OzItem> items;
-    std::vector<double> cost;
-    int slots = 0;
-    // order: shape, row tile, K segment, column tile (concurrent items share C^-1 row tiles)
-    size_t t0 = 0;
-    while (t0 < tiles.size()) {
-      size_t t1 = t0;
-      while (t1 < tiles.size() && tiles[t1].shape == tiles[t0].shape && tiles[t1].mt == tiles[t0].mt) ++t1;
-      const T& tt = tiles[t0];
-      const int kc = tt.kc;
-      int nseg = std::max(1, (int)std::lround(tt.cc * kc / unit));
-      nseg = std::max(nseg, (kc + OZ_PART - 1) / OZ_PART);
-      nseg = std::min(nseg, kc);
-      for (int sg = 0; sg < nseg; ++sg) {
-        const int k0 = (int)((int64_t)kc * sg / nseg), k1 = (int)((int64_t)kc * (sg + 1) / nseg);
-        for (size_t t = t0; t < t1; ++t) {
-          const int slot0 = nseg > 1 ? slots + (int)(t - t0) * nseg : 0;
-          items.push_back(OzItem{tiles[t].shape, tiles[t].mt, tiles[t].nt, k0, k1, sg, nseg, slot0});
-          cost.push_back(tiles[t].cc * (k1 - k0) + epi);
+  if (shared.empty() && solo.empty()) return 0;
+  const int grid = std::min<int>(sms, (int)(shared.size() + solo.size()));
+  const char* fv = getenv("FMP_OZ_WAVES");   // diagnostics: cap the number of data-parallel waves
+  int waves = (int)(shared.size() / grid);
+  if (fv) waves = std::min(waves, atoi(fv));
+  std::vector<Part> rest(shared.begin() + (size_t)waves * grid, shared.end());
+  rest.insert(rest.end(), solo.begin(), solo.end());
+  double total = 0.0;
+  for (const Part& r : rest) total += r.cc * (r.k1 - r.k0);
+  // cut the remainder into `grid` contiguous pieces of equal cost (at K-chunk granularity)
+  std::vector<std::vector<Part>> piece(grid);
+  {
+    int b = 0;
+    double used = 0.0;   // cost assigned to CTAs < b plus the current CTA's share so far
+    for (const Part& r : rest) {
+      int k = r.k0;
+      while (k < r.k1) {
+        const double target = total * (b + 1) / grid;
+        int take = r.k1 - k;
+        if (b < grid - 1 && used + take * r.cc > target) {
+          take = (int)std::floor((target - used) / r.cc + 0.5);
+          take = std::max(0, std::min(take, r.k1 - k));
         }
+        if (take > 0) {
+          Part seg = r;
+          seg.k0 = k;
+          seg.k1 = k + take;
+          piece[b].push_back(seg);
+          used += take * r.cc;
+          k += take;
+        }
+        if (k < r.k1 || used >= target - 0.5 * r.cc) b = std::min(b + 1, grid - 1);
       }
-      if (nseg > 1) slots += (int)(t1 - t0) * nseg;
-      t0 = t1;
-    }
-    const double mk = lpt(cost, grid, nullptr);
-    if (mk < best * 0.995) {
-      best = mk;
-      best_items.swap(items);
-      out->n_slots = slots;
     }
   }
-  std::vector<double> cost;
-  for (const auto& it : best_items) cost.push_back(shapes[it.shape].A ? chunk_cycles(shapes[it.shape].w) * (it.k1 - it.k0) + epi : 0.0);
-  std::vector<int> cta_of;
-  lpt(cost, grid, &cta_of);
-  std::vector<std::vector<int>> lists(grid);
-  for (size_t i = 0; i < best_items.size(); ++i) lists[cta_of[i]].push_back((int)i);
+  std::vector<std::vector<Part>> lists(grid);
+  for (int b = 0; b < grid; ++b) {
+    const int pos = (b / 3) % (waves + 1);
+    for (int j = 0; j <= waves; ++j) {
+      if (j == pos) lists[b].insert(lists[b].end(), piece[b].begin(), piece[b].end());
+      if (j < waves) lists[b].push_back(shared[(size_t)j * grid + b]);
+    }
+  }
+  // segments per tile (in K order), partial slots for the split tiles
+  std::vector<std::vector<std::pair<int, int>>> segs(n_tiles);   // (k0, owner index) per tile
   std::vector<OzItem> items;
   std::vector<int> offs(1, 0);
   for (auto& l : lists) {
-    std::sort(l.begin(), l.end());
-    for (int i : l) items.push_back(best_items[i]);
+    for (const Part& q : l) {
+      items.push_back(OzItem{q.shape, q.mt, q.nt, q.k0, q.k1, 0, 1, 0});
+      segs[q.tile].emplace_back(q.k0, (int)items.size() - 1);
+    }
     offs.push_back((int)items.size());
   }
+  int slots = 0;
+  for (auto& sg : segs) {
+    if (sg.size() <= 1) continue;
+    std::sort(sg.begin(), sg.end());
+    for (size_t j = 0; j < sg.size(); ++j) {
+      OzItem& it = items[sg[j].second];
+      it.seg = (int)j;
+      it.nseg = (int)sg.size();
+      it.slot0 = slots;
+    }
+    slots += (int)sg.size();
+  }
+  out->n_slots = slots;
   out->grid = grid;
   out->n_items = (int)items.size();
+  if (getenv_flag("FMP_OZ_VERBOSE"))
+    fprintf(stderr, "ozaki schedule: %d items on %d CTAs (%d waves of %zu shared parts; %zu solo parts; %zu remainder parts), %d split slots\n",
+            out->n_items, grid, waves, shared.size(), solo.size(), rest.size(), out->n_slots);
   FMP_CHECK_CUDA(cudaMalloc(&out->shapes, sizeof(OzShape) * shapes.size()));
   FMP_CHECK_CUDA(cudaMemcpy(out->shapes, shapes.data(), sizeof(OzShape) * shapes.size(), cudaMemcpyHostToDevice));
   FMP_CHECK_CUDA(cudaMalloc(&out->items, sizeof(OzItem) * items.size()));
