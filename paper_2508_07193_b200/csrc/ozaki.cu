@@ -47,6 +47,12 @@ static_assert(OZ_STAGES * OZ_STAGE <= 227 * 1024, "stages exceed shared memory")
 
 __host__ __device__ constexpr int oz_pad16(int x) { return (x + 15) / 16 * 16; }
 
+__device__ __forceinline__ uint64_t globaltimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
 __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
   return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
          ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | ((uint64_t)1 << 46);   // version 1, SWIZZLE_NONE
@@ -107,6 +113,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
     k_ozaki(const OzShape* __restrict__ shapes, const OzItem* __restrict__ items, const int* __restrict__ offs,
             double* __restrict__ zpart, int* __restrict__ counters, long long* __restrict__ prof, int dbg) {
   extern __shared__ __align__(1024) uint8_t osm[];
+  if (prof && threadIdx.x == 0) prof[blockIdx.x * 8 + 4] = (long long)globaltimer();
   __shared__ __align__(8) uint64_t full_bar[OZ_STAGES], empty_bar[OZ_STAGES], tfull_bar, tempty_bar;
   __shared__ uint32_t tmem_base;
   __shared__ int last_flag;
@@ -201,10 +208,10 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
       }
     }
     if (prof && lane == 0) {   // FMP_OZ_PROF: MMA-warp cycles waiting for operands / for the epilogue
-      prof[blockIdx.x * 4 + 0] = clock64() - t0;
-      prof[blockIdx.x * 4 + 1] = w_full;
-      prof[blockIdx.x * 4 + 2] = w_empty;
-      prof[blockIdx.x * 4 + 3] = tcount;
+      prof[blockIdx.x * 8 + 0] = clock64() - t0;
+      prof[blockIdx.x * 8 + 1] = w_full;
+      prof[blockIdx.x * 8 + 2] = w_empty;
+      prof[blockIdx.x * 8 + 3] = tcount;
     }
   } else {
     // ---------------- epilogue warps 0-3: lane quadrant = warp, one row per thread
@@ -234,20 +241,27 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
 #pragma unroll
         for (int L = 2; L <= OZ_S + 1; ++L) tmem_ld8(base + (uint32_t)((L - 2) * w), v[L - 2]);
         asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+        // levels combined in int64 first: hi = D2 2^16 + D3 2^8 + D4 (< 2^48, exact as a double),
+        // lo = D5 2^24 + D6 2^16 + D7 2^8 + D8 (< 2^56); sum_L D_L 2^-8L = 2^-32 (hi + 2^-32 lo)
+        // with one rounding (fma) -- two int64 conversions instead of seven int32 ones
+        static_assert(OZ_S == 7, "level combination written for S = 7");
         double acc[8];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) acc[j] = 0.0;
-#pragma unroll
-        for (int L = OZ_S + 1; L >= 2; --L) {   // smallest terms first
-          const double wgt = ldexp(1.0, -8 * L);
-#pragma unroll
-          for (int j = 0; j < 8; ++j) acc[j] = fma((double)(int)v[L - 2][j], wgt, acc[j]);
+        for (int j = 0; j < 8; ++j) {
+          const long long hi = ((long long)(int)v[0][j] << 16) + ((long long)(int)v[1][j] << 8) + (long long)(int)v[2][j];
+          const long long lo = ((long long)(int)v[3][j] << 24) + ((long long)(int)v[4][j] << 16) +
+                               ((long long)(int)v[5][j] << 8) + (long long)(int)v[6][j];
+          acc[j] = fma((double)lo, 0x1p-32, (double)hi);
         }
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
           const int c = c0 + j;
           const bool ok = row < sh.m && c < nvalid;
-          const double val = ok ? ldexp(acc[j], ea + eb_sh[c]) : 0.0;
+          const int e = ea + eb_sh[c] - 32;
+          // 2^e as a double (exact scaling) in the normal range, ldexp outside it
+          const double val = !ok ? 0.0
+                             : (e >= -1022 && e <= 1023) ? acc[j] * __longlong_as_double((long long)(e + 1023) << 52)
+                                                         : ldexp(acc[j], e);
           if (part) {
             part[c * OZ_M + rr] = val;   // [column][row]: coalesced over the warp's rows
           } else if (ok) {
@@ -268,27 +282,20 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
           __threadfence();
           if (row < sh.m) {
             const double* src = zpart + (size_t)tl.slot0 * OZ_SLOT + rr;
-            for (int c0 = 0; c0 < nvalid; c0 += 8) {   // 8 columns x 2 segments of loads in flight
-              double s[8];
+            constexpr int FC = 24;   // columns per round: FC loads of one segment in flight
+            for (int c0 = 0; c0 < nvalid; c0 += FC) {
+              double s[FC];
 #pragma unroll
-              for (int j = 0; j < 8; ++j) s[j] = 0.0;
-              int sg = 0;
-              for (; sg + 1 < tl.nseg; sg += 2) {
-                double v0[8], v1[8];
+              for (int j = 0; j < FC; ++j) s[j] = 0.0;
+              for (int sg = 0; sg < tl.nseg; ++sg) {
+                double v[FC];
 #pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                  v0[j] = __ldcg(src + (size_t)sg * OZ_SLOT + (c0 + j) * OZ_M);
-                  v1[j] = __ldcg(src + (size_t)(sg + 1) * OZ_SLOT + (c0 + j) * OZ_M);
-                }
+                for (int j = 0; j < FC; ++j) v[j] = c0 + j < w ? __ldcg(src + (size_t)sg * OZ_SLOT + (c0 + j) * OZ_M) : 0.0;
 #pragma unroll
-                for (int j = 0; j < 8; ++j) s[j] = (s[j] + v0[j]) + v1[j];
-              }
-              if (sg < tl.nseg) {
-#pragma unroll
-                for (int j = 0; j < 8; ++j) s[j] += __ldcg(src + (size_t)sg * OZ_SLOT + (c0 + j) * OZ_M);
+                for (int j = 0; j < FC; ++j) s[j] += v[j];
               }
 #pragma unroll
-              for (int j = 0; j < 8; ++j)
+              for (int j = 0; j < FC; ++j)
                 if (c0 + j < nvalid) sh.Z[(size_t)(tl.nt * w + c0 + j) * sh.ld + row] = s[j];
             }
           }
@@ -299,6 +306,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n");
   __syncthreads();
+  if (prof && tid == 0) prof[blockIdx.x * 8 + 5] = (long long)globaltimer();
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(OZ_TMEM_COLS));
 }
 
@@ -416,7 +424,7 @@ static long long* g_oz_prof = nullptr;   // FMP_OZ_PROF=1: per-CTA MMA-warp wait
 
 int ozaki_launch(const OzPlan& p, cudaStream_t st) {
   if (p.grid <= 0) return 0;
-  if (!g_oz_prof && getenv_flag("FMP_OZ_PROF")) FMP_CHECK_CUDA(cudaMalloc(&g_oz_prof, 4096 * 4 * sizeof(long long)));
+  if (!g_oz_prof && getenv_flag("FMP_OZ_PROF")) FMP_CHECK_CUDA(cudaMalloc(&g_oz_prof, 4096 * 8 * sizeof(long long)));
   static const int dbg = getenv("FMP_OZ_DBG") ? atoi(getenv("FMP_OZ_DBG")) : 0;
   k_ozaki<<<p.grid, OZ_THREADS, OZ_STAGES * OZ_STAGE, st>>>(p.shapes, p.items, p.offs, p.zpart, p.counters,
                                                             g_oz_prof, dbg);
@@ -572,9 +580,10 @@ void ozaki_free(OzPlan* p) {
 }  // namespace fmp
 
 // Diagnostics (tools/oz_prof.py): the last Ozaki launch's per-CTA MMA-warp cycles
-// [total, waiting for operand stages, waiting for the epilogue, tiles], FMP_OZ_PROF=1 only.
+// [total, waiting for operand stages, waiting for the epilogue, tiles, CTA start ns, CTA end ns,
+// -, -] (8 per CTA), FMP_OZ_PROF=1 only.
 extern "C" int fmp_debug_ozaki_prof(long long* out, int n) {
   if (!fmp::g_oz_prof) return -1;
-  FMP_CHECK_CUDA(cudaMemcpy(out, fmp::g_oz_prof, (size_t)n * 4 * sizeof(long long), cudaMemcpyDeviceToHost));
+  FMP_CHECK_CUDA(cudaMemcpy(out, fmp::g_oz_prof, (size_t)n * 8 * sizeof(long long), cudaMemcpyDeviceToHost));
   return 0;
 }

@@ -14,11 +14,14 @@ for _ in range(3):
     prec.apply_into(x, z)
 torch.cuda.synchronize()
 lib = ctypes.CDLL(str(_lib.LIB_PATH))
-buf = np.zeros((148, 4), dtype=np.int64)
+buf = np.zeros((148, 8), dtype=np.int64)
 assert lib.fmp_debug_ozaki_prof(buf.ctypes.data_as(ctypes.c_void_p), 148) == 0
-tot, full, empty, tiles = buf.T
+tot, full, empty, tiles, ts, te = buf.T[:6]
+t0 = ts.min()
 busy = tot - full - empty
 print(json.dumps({"ctas": 148, "total_max_us": round(tot.max() / 1965, 1), "total_mean_us": round(tot.mean() / 1965, 1),
                   "wait_full_mean_us": round(full.mean() / 1965, 1), "wait_epilogue_mean_us": round(empty.mean() / 1965, 1),
                   "issue_mean_us": round(busy.mean() / 1965, 1), "tiles_mean": float(tiles.mean()),
-                  "wait_full_max_us": round(full.max() / 1965, 1)}))
+                  "wait_full_max_us": round(full.max() / 1965, 1),
+                  "cta_start_spread_us": round((ts.max() - t0) / 1e3, 1), "cta_end_min_us": round((te.min() - t0) / 1e3, 1),
+                  "cta_end_max_us": round((te.max() - t0) / 1e3, 1), "cta_span_mean_us": round((te - ts).mean() / 1e3, 1)}))
