@@ -243,6 +243,15 @@ int fmp_halo_unpack(const fmp_block* blk, int phase, int side, const double* in,
 int fmp_precond_profile(fmp_precond* p, int enable);
 int fmp_precond_stage_ms(fmp_precond* p, float* ms, int n);
 
+/* Kernel family the plan runs its transform passes with (diagnostics and tests; no reference
+ * counterpart): FMP_PATH_GENERAL (CTA-synchronous kernels, any extent <= 72), FMP_PATH_FAST
+ * (warp-independent, <= 2 distinct extents <= 36), FMP_PATH_LARGE (warp-independent, extents
+ * 41..72).  FMP_FORCE_GENERAL=1 in the environment at plan creation selects the general path. */
+#define FMP_PATH_GENERAL 0
+#define FMP_PATH_FAST 1
+#define FMP_PATH_LARGE 2
+int fmp_precond_path(const fmp_precond* p);
+
 /* Diagnostics: with FMP_OZ_PROF=1 in the environment, the last Ozaki GEMM launch's per-CTA
  * MMA-issuer cycles {total, waiting for operand stages, waiting for the epilogue, tiles} for the
  * first n CTAs (tools/oz_prof.py).  Returns -1 when profiling is off. */

@@ -1265,6 +1265,275 @@ __global__ void __launch_bounds__(NW * 32, 1) k_column_fast_db(FastColArgs A) {
   cp_async_wait<0>();
 }
 
+// ================================================================ large path (extents 41..72)
+// Warp-independent column and plane passes for 64^3-class subdomains (extents up to 72 = 9 DMMA
+// tiles), replacing the CTA-synchronous general kernels there.  Factors of every extent do not
+// fit in shared memory next to 64^3-class tiles, so the host groups the work: a column-pass
+// launch serves one z extent (its V^T_z / U^T_z resident), a plane-pass CTA one
+// (component, ex, ey) combination (its F_x / F_y resident).
+constexpr int LN = 72;                     // padded extent (9 DMMA tiles)
+constexpr int LSM = 76;                    // factor / plane row stride (== 4 mod 8)
+constexpr int LMAT = LN * LSM;             // one padded factor matrix (doubles)
+constexpr int LCXR = 72;                   // column tile rows per component
+constexpr int LCX_BUF = 3 * LCXR * CXS;    // one column tile: 3 components x 72 z x 8 columns
+constexpr int LCW = 8;                     // warps per large column CTA (single-buffered tiles)
+constexpr int kColLargeSmem = (2 * LMAT + LCW * LCX_BUF) * (int)sizeof(double);
+
+struct LargeColArgs {
+  const fmp_subdomain* subs;
+  const fmp_shape* shapes;
+  const int2* items;   // (sub, p0): 8 columns of a subdomain whose z extent is `ez`
+  int n_items;
+  const double* src;
+  double* dst;
+  const double* factors;
+  int64_t ut, vt;      // U^T_z / V^T_z of extent ez (offsets into factors)
+  int ez;
+  const double* corr;  // K3 only (Woodbury), may be null
+  int pmax;
+  double alpha;
+  const CUtensorMap* maps;   // per-subdomain (p, z, component) maps with box 8 x 72 x 3, or null
+};
+
+// z mode product of one 8-column item with the resident factors (stride LSM): MT row tiles
+template <bool INV, int MT>
+__device__ __forceinline__ void col_mma_large(double (&acc)[3][MT][2], const double* xb, const double* fv,
+                                              const double* fu, int k4) {
+  for (int kk = 0; kk < k4; ++kk) {
+    const double b0 = xb[(0 * LCXR + kk * 4) * CXS];
+    const double b1 = xb[(1 * LCXR + kk * 4) * CXS];
+    const double b2 = xb[(2 * LCXR + kk * 4) * CXS];
+#pragma unroll
+    for (int m = 0; m < MT; ++m) {
+      const double av = INV ? fv[kk * 4 * LSM + m * 8] : fv[m * 8 * LSM + kk * 4];
+      const double au = INV ? fu[kk * 4 * LSM + m * 8] : fu[m * 8 * LSM + kk * 4];
+      dmma884(acc[0][m][0], acc[0][m][1], av, b0);
+      dmma884(acc[1][m][0], acc[1][m][1], av, b1);
+      dmma884(acc[2][m][0], acc[2][m][1], au, b2);
+    }
+  }
+}
+
+// K2 (INV=false): y^ = B^-1 (Fz X), rows 0..8MT-1 on DMMA and the remainder rows 8MT..ez-1 (at
+// most 4) as DFMA dot products;  K3 (INV=true): Fz^T (y^ - corr) over the owned rows (MT tiles).
+// One warp per 8-column item; the next item's tile is requested as soon as the current one is
+// consumed, so its TMA latency hides behind this warp's epilogue and the other warps' DMMA.
+template <bool INV, int MT>
+__global__ void __launch_bounds__(LCW * 32, 1) k_column_large(LargeColArgs A) {
+  extern __shared__ __align__(128) double smem[];
+  __shared__ __align__(8) uint64_t cbar[LCW];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
+  double* Fv = smem;              // V^T_z (components x, y), zero padded to LN x LSM
+  double* Fu = smem + LMAT;       // U^T_z (component z)
+  double* X = smem + 2 * LMAT + warp * LCX_BUF;
+  const int ez = A.ez;
+  for (int q = tid; q < LMAT; q += blockDim.x) {
+    const int r = q / LSM, c = q - r * LSM;
+    const bool ok = r < ez && c < ez;
+    Fv[q] = ok ? __ldg(A.factors + A.vt + r * ez + c) : 0.0;
+    Fu[q] = ok ? __ldg(A.factors + A.ut + r * ez + c) : 0.0;
+  }
+  for (int q = lane; q < LCX_BUF; q += 32) X[q] = 0.0;
+  if (lane == 0) {
+    mbar_init(&cbar[warp], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const int gw = blockIdx.x * LCW + warp, nw = gridDim.x * LCW;
+  if (gw >= A.n_items) return;
+  const bool tma = A.maps != nullptr;
+  uint32_t phase = 0;
+  auto issue = [&](const int2 w, const SubD& d) {
+    if (tma) {   // one box: 8 columns x 72 z rows x 3 components, zero-filled past ez / the plane
+      if (lane == 0) {
+        fence_proxy_async();
+        mbar_expect_tx(&cbar[warp], LCX_BUF * (int)sizeof(double));
+        tma_load_3d(X, A.maps + w.x, w.y, 0, 0, &cbar[warp]);
+      }
+      return;
+    }
+    const int P = d.ex * d.ey;
+    const int64_t V = d.cstride();
+    const double* src = A.src + d.ws_off + w.y;
+    const int col = lane & 7;
+    for (int cc = 0; cc < 3; ++cc)
+      for (int k = lane >> 3; k < LCXR; k += 4)
+        cp_async8(X + (cc * LCXR + k) * CXS + col,
+                  (k < d.ez && w.y + col < P) ? src + cc * V + (int64_t)k * d.ps + col : nullptr, A.factors);
+    cp_async_commit();
+  };
+  int2 w = A.items[gw];
+  SubD d = load_sub(A.subs + w.x);
+  issue(w, d);
+  const int k4 = pad4(ez) / 4;
+  for (int it = gw; it < A.n_items; it += nw) {
+    const bool more = it + nw < A.n_items;
+    const int2 wn = more ? A.items[it + nw] : w;
+    const SubD dn = (more && wn.x != w.x) ? load_sub(A.subs + wn.x) : d;
+    const fmp_shape& sh = A.shapes[d.shape];
+    const double* Sx = A.factors + sh.s_off[0];
+    const double* Sy = A.factors + sh.s_off[1];
+    const double* Sz = A.factors + sh.s_off[2];
+    const int ex = d.ex, ey = d.ey, P = ex * ey, p0 = w.y;
+    const int64_t V = d.cstride();
+    if (tma) {
+      mbar_wait(&cbar[warp], phase);
+      phase ^= 1u;
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncwarp();
+    if (INV && A.corr) {
+      // y^ -= B^-1 (G Q Z): two rank-structured face terms per component (K6), in two halves of
+      // the lane's z rows with every load of a half in flight at once
+      const double* cb = A.corr + (int64_t)w.x * 6 * A.pmax * A.pmax;
+      const int pm = A.pmax, pm2 = pm * pm;
+      const int col = lane & 7, p = p0 + col;
+      if (p < P) {
+        const int b0 = p0 / ex;
+        int b = b0, a = p - b0 * ex;
+        while (a >= ex) { a -= ex; ++b; }
+        const double vy0 = __ldg(A.factors + sh.vt_off[1] + b * ey), vx0 = __ldg(A.factors + sh.vt_off[0] + a * ex);
+        const double sx = __ldg(Sx + a), sy = __ldg(Sy + b);
+        const double gx = cb[0 * pm2 + b * pm + a], gy = cb[2 * pm2 + b * pm + a];
+        constexpr int NZ = LCXR / 8;   // z rows per lane and half
+#pragma unroll
+        for (int hf = 0; hf < 2; ++hf) {
+          double c1[NZ], c3[NZ], c4[NZ], c5[NZ];
+#pragma unroll
+          for (int u = 0; u < NZ; ++u) {
+            const int cz = (lane >> 3) + 4 * (hf * NZ + u);
+            const bool ok = cz < ez;
+            c1[u] = ok ? cb[1 * pm2 + cz * pm + a] : 0.0;
+            c3[u] = ok ? cb[3 * pm2 + cz * pm + b] : 0.0;
+            c4[u] = ok ? cb[4 * pm2 + cz * pm + a] : 0.0;
+            c5[u] = ok ? cb[5 * pm2 + cz * pm + b] : 0.0;
+          }
+#pragma unroll
+          for (int u = 0; u < NZ; ++u) {
+            const int cz = (lane >> 3) + 4 * (hf * NZ + u);
+            if (cz >= ez) break;
+            const double vz0 = Fv[cz * LSM];
+            const double dx = vz0 * gx + vy0 * c1[u];
+            const double dy = vz0 * gy + vx0 * c3[u];
+            const double dz = vy0 * c4[u] + vx0 * c5[u];
+            const double sz = __ldg(Sz + cz);
+            const double q = rcp_pos(1.0 + A.alpha * (sx * sx + sy * sy + sz * sz));
+            const double pr = A.alpha * (sx * dx + sy * dy + sz * dz);
+            X[(0 * LCXR + cz) * CXS + col] -= q * (dx + pr * sx);
+            X[(1 * LCXR + cz) * CXS + col] -= q * (dy + pr * sy);
+            X[(2 * LCXR + cz) * CXS + col] -= q * (dz + pr * sz);
+          }
+        }
+      }
+      __syncwarp();
+    }
+    double acc[3][MT][2];
+#pragma unroll
+    for (int cc = 0; cc < 3; ++cc)
+#pragma unroll
+      for (int m = 0; m < MT; ++m) acc[cc][m][0] = acc[cc][m][1] = 0.0;
+    const double* xb = X + t * CXS + g;
+    const double* fv = INV ? Fv + t * LSM + g + d.oz : Fv + g * LSM + t;
+    const double* fu = INV ? Fu + t * LSM + g + d.oz : Fu + g * LSM + t;
+    col_mma_large<INV, MT>(acc, xb, fv, fu, k4);
+    // forward remainder rows 8MT..ez-1 (at most 4): lane -> (column lane & 7, row / K part lane >> 3)
+    const int rem = INV ? 0 : ez - 8 * MT;
+    double o3[3] = {0.0, 0.0, 0.0};
+    int rr = 0;
+    if (rem > 0) {
+      const int ks = rem == 1 ? 4 : (rem == 2 ? 2 : 1);   // K parts per row
+      const int sub = lane >> 3, col = lane & 7, part = sub % ks;
+      rr = 8 * MT + sub / ks;
+      const int kb = ez * part / ks, ke = ez * (part + 1) / ks;
+      const double* fvr = Fv + min(rr, ez - 1) * LSM;
+      const double* fur = Fu + min(rr, ez - 1) * LSM;
+      for (int k = kb; k < ke; ++k) {
+        const double fv0 = fvr[k], fu0 = fur[k];
+        o3[0] = fma(fv0, X[(0 * LCXR + k) * CXS + col], o3[0]);
+        o3[1] = fma(fv0, X[(1 * LCXR + k) * CXS + col], o3[1]);
+        o3[2] = fma(fu0, X[(2 * LCXR + k) * CXS + col], o3[2]);
+      }
+      if (ks >= 2)
+#pragma unroll
+        for (int cc = 0; cc < 3; ++cc) o3[cc] += __shfl_xor_sync(0xffffffffu, o3[cc], 8);
+      if (ks == 4)
+#pragma unroll
+        for (int cc = 0; cc < 3; ++cc) o3[cc] += __shfl_xor_sync(0xffffffffu, o3[cc], 16);
+    }
+    __syncwarp();   // the tile is consumed: fetch the next one under the epilogue
+    if (more) issue(wn, dn);
+    double* dst = A.dst + d.ws_off;
+    if (rem > 0) {
+      const int ks = rem == 1 ? 4 : (rem == 2 ? 2 : 1);
+      const int sub = lane >> 3, col = lane & 7, p = p0 + col;
+      if (sub % ks == 0 && rr < ez && p < P) {
+        const int b0 = p0 / ex;
+        int b = b0, a = p - b0 * ex;
+        while (a >= ex) { a -= ex; ++b; }
+        const double sxv = __ldg(Sx + a), syv = __ldg(Sy + b), sz = __ldg(Sz + rr);
+        const double q = rcp_pos(1.0 + A.alpha * (sxv * sxv + syv * syv + sz * sz));
+        const double pr = A.alpha * (sxv * o3[0] + syv * o3[1] + sz * o3[2]);
+        const int64_t o = (int64_t)rr * d.ps + p;
+        dst[o] = q * (o3[0] + pr * sxv);
+        dst[V + o] = q * (o3[1] + pr * syv);
+        dst[2 * V + o] = q * (o3[2] + pr * sz);
+      }
+    }
+    // epilogue: this lane's column pair p = p0 + 2t, p + 1 (one 16-byte store per row and component)
+    const int pA = p0 + 2 * t;
+    const bool v0 = pA < P, v1 = pA + 1 < P;
+    double sx[2] = {0.0, 0.0}, sy[2] = {0.0, 0.0};
+    if (!INV) {
+      const int b0 = p0 / ex;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        if (pA + h >= P) continue;
+        int b = b0, a = pA + h - b0 * ex;
+        while (a >= ex) { a -= ex; ++b; }
+        sx[h] = __ldg(Sx + a);
+        sy[h] = __ldg(Sy + b);
+      }
+    }
+    if (v0) {
+#pragma unroll
+      for (int m = 0; m < MT; ++m) {
+        if (INV && m * 8 + g >= d.wz) continue;
+        const int r = INV ? d.oz + m * 8 + g : m * 8 + g;
+        if (r >= ez) continue;
+        double y[3][2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          double y0 = acc[0][m][h], y1 = acc[1][m][h], y2 = acc[2][m][h];
+          if (!INV) {  // B^-1 y = q (y + alpha s (s . y)), q = 1/(1 + alpha |s|^2)  (ref:subdomain.py:145-153)
+            const double sz = __ldg(Sz + r);
+            const double q = rcp_pos(1.0 + A.alpha * (sx[h] * sx[h] + sy[h] * sy[h] + sz * sz));
+            const double pr = A.alpha * (sx[h] * y0 + sy[h] * y1 + sz * y2);
+            y0 = q * (y0 + pr * sx[h]);
+            y1 = q * (y1 + pr * sy[h]);
+            y2 = q * (y2 + pr * sz);
+          }
+          y[0][h] = y0;
+          y[1][h] = y1;
+          y[2][h] = y2;
+        }
+        const int64_t o = (int64_t)r * d.ps + pA;
+        if (v1) {
+#pragma unroll
+          for (int cc = 0; cc < 3; ++cc)
+            *reinterpret_cast<double2*>(dst + cc * V + o) = make_double2(y[cc][0], y[cc][1]);
+        } else {
+#pragma unroll
+          for (int cc = 0; cc < 3; ++cc) dst[cc * V + o] = y[cc][0];
+        }
+      }
+    }
+    w = wn;
+    d = dn;
+  }
+  cp_async_wait<0>();
+}
+
 // ---------------------------------------------------------------- K5 / K6: boundary faces
 // Component c has two boundary faces with nonzero delta (ref:operators.py:151-164):
 //   c = x: z-normal (k = 0, all j,i) and y-normal (j = 0, k >= 1)
@@ -1654,6 +1923,13 @@ struct fmp_precond {
   int n_ffwd = 0, n_finv = 0, n_fcol = 0;
   int n_ffwd_int = 0;                     // forward plane items of subdomains that read no ghost (listed first)
   CUtensorMap* d_colmaps = nullptr;       // column tiles by TMA: [work_a maps | work_b maps], one per subdomain
+  // large path (extents 41..72): column items grouped by z extent (one launch per group, its z
+  // factors resident), column tile maps with 72-row boxes
+  struct LColGroup { int ez, off, n, mt_fwd, mt_inv; int64_t ut, vt; };
+  bool large = false;
+  std::vector<LColGroup> lcol;
+  int2* d_lcol = nullptr;
+  CUtensorMap* d_lcolmaps = nullptr;
   // Woodbury GEMM (set at plan creation from FMP_GEMM): Ozaki INT8 tensor-core GEMM (default,
   // "ozaki": int8 slices of C^-1 built once, Y sliced per apply), the own DMMA kernel ("own") or
   // cuBLAS DGEMM ("cublas")
@@ -1704,6 +1980,8 @@ static void free_plan(fmp_precond* p) {
   cudaFree(p->d_finv);
   cudaFree(p->d_fcol);
   cudaFree(p->d_colmaps);
+  cudaFree(p->d_lcol);
+  cudaFree(p->d_lcolmaps);
   cudaFree(p->d_gshapes);
   for (int q = 0; q < fmp_precond::kAux; ++q) {
     if (p->aux_blas[q]) cublasDestroy(p->aux_blas[q]);
@@ -1842,6 +2120,66 @@ extern "C" int fmp_precond_create(const fmp_precond_desc* desc, fmp_precond** ou
           }
         }
         if (upload(maps, &p->d_colmaps)) {
+          free_plan(p);
+          return -1;
+        }
+      }
+    }
+  }
+  // large-path eligibility (not fast, every extent <= LN): column items per z extent
+  {
+    const char* force = getenv("FMP_FORCE_GENERAL");
+    p->large = !p->fast && mx <= LN && !(force && force[0] == '1') && !getenv_flag("FMP_NO_LARGE");
+    if (p->large) {
+      std::vector<int> ezs;
+      for (const auto& sd : p->subs)
+        if (std::find(ezs.begin(), ezs.end(), (int)sd.ext[2]) == ezs.end()) ezs.push_back((int)sd.ext[2]);
+      std::sort(ezs.begin(), ezs.end());
+      std::vector<int2> items;
+      for (int ez : ezs) {
+        fmp_precond::LColGroup gr{ez, (int)items.size(), 0, 0, 0, -1, -1};
+        int wzmax = 1;
+        for (int64_t q = 0; q < desc->n_sub; ++q) {
+          const auto& sd = p->subs[q];
+          if ((int)sd.ext[2] != ez) continue;
+          wzmax = std::max(wzmax, (int)sd.own[2]);
+          for (int p0 = 0; p0 < (int)(sd.ext[0] * sd.ext[1]); p0 += 8) items.push_back(make_int2((int)q, p0));
+        }
+        for (const auto& sh : p->shapes)
+          if ((int)sh.ext[2] == ez) {
+            gr.ut = sh.ut_off[2];
+            gr.vt = sh.vt_off[2];
+          }
+        gr.n = (int)items.size() - gr.off;
+        gr.mt_fwd = ez % 8 <= 4 ? ez / 8 : ez / 8 + 1;   // remainder rows (<= 4) on DFMA
+        gr.mt_inv = pad8(wzmax) / 8;
+        if (gr.mt_fwd < 5 || gr.mt_fwd > 9 || gr.mt_inv < 5 || gr.mt_inv > 9) p->large = false;
+        p->lcol.push_back(gr);
+      }
+      if (p->large && upload(items, &p->d_lcol)) {
+        free_plan(p);
+        return -1;
+      }
+      bool col_tma = p->large && !getenv_flag("FMP_COL_NO_TMA") && ((uintptr_t)desc->work_a & 15) == 0 &&
+                     ((uintptr_t)desc->work_b & 15) == 0;
+      for (int64_t q = 0; q < desc->n_sub; ++q) col_tma = col_tma && (p->subs[q].ws_off & 1) == 0;
+      if (col_tma) {
+        std::vector<CUtensorMap> maps(2 * desc->n_sub);
+        for (int w = 0; w < 2; ++w) {
+          const double* base = w == 0 ? desc->work_a : desc->work_b;
+          for (int64_t q = 0; q < desc->n_sub; ++q) {
+            const auto& sd = p->subs[q];
+            const uint64_t ps = (uint64_t)((sd.ext[0] * sd.ext[1] + 3) & ~3LL), ez = (uint64_t)sd.ext[2];
+            const uint64_t dims[3] = {ps, ez, 3};
+            const uint64_t strides[2] = {ps * 8, ps * ez * 8};
+            const uint32_t box[3] = {8, LCXR, 3};
+            if (encode_tensor_map_f64(&maps[w * desc->n_sub + q], base + sd.ws_off, 3, dims, strides, box)) {
+              free_plan(p);
+              return -1;
+            }
+          }
+        }
+        if (upload(maps, &p->d_lcolmaps)) {
           free_plan(p);
           return -1;
         }
@@ -1989,9 +2327,21 @@ extern "C" int fmp_precond_create(const fmp_precond_desc* desc, fmp_precond** ou
   cudaFuncSetAttribute(k_corr<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * FaceMat<3>::WORDS * 8);
   cudaFuncSetAttribute(k_corr<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * FaceMat<5>::WORDS * 8);
   cudaFuncSetAttribute(k_corr<9>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * FaceMat<9>::WORDS * 8);
+  if (p->large) {
+#define FMP_LCA(MT)                                                                                              \
+  cudaFuncSetAttribute(k_column_large<false, MT>, cudaFuncAttributeMaxDynamicSharedMemorySize, kColLargeSmem); \
+  cudaFuncSetAttribute(k_column_large<true, MT>, cudaFuncAttributeMaxDynamicSharedMemorySize, kColLargeSmem);
+    FMP_LCA(5) FMP_LCA(6) FMP_LCA(7) FMP_LCA(8) FMP_LCA(9)
+#undef FMP_LCA
+  }
   FMP_CHECK_CUDA(cudaGetLastError());
   *out = p;
   return 0;
+}
+
+extern "C" int fmp_precond_path(const fmp_precond* p) {
+  FMP_REQUIRE(p, "null plan");
+  return p->fast ? FMP_PATH_FAST : (p->large ? FMP_PATH_LARGE : FMP_PATH_GENERAL);
 }
 
 extern "C" int fmp_precond_destroy(fmp_precond* p) {
@@ -2032,6 +2382,42 @@ static int column_pass(fmp_precond* p, bool inv, const double* src, double* dst,
 #undef FMP_COLF
     }
     FMP_CHECK_LAUNCH();
+    return 0;
+  }
+  if (p->large) {
+    for (const auto& gr : p->lcol) {
+      LargeColArgs a{};
+      a.subs = p->d.subs;
+      a.shapes = p->d.shapes;
+      a.items = p->d_lcol + gr.off;
+      a.n_items = gr.n;
+      a.src = src;
+      a.dst = dst;
+      a.factors = p->d.factors;
+      a.ut = gr.ut;
+      a.vt = gr.vt;
+      a.ez = gr.ez;
+      a.corr = corr;
+      a.pmax = (int)p->d.pmax;
+      a.alpha = p->d.alpha;
+      a.maps = p->d_lcolmaps ? p->d_lcolmaps + (src == p->d.work_a ? 0 : p->d.n_sub) : nullptr;
+      if (a.maps && src != p->d.work_a && src != p->d.work_b) a.maps = nullptr;
+      const int grid = std::min(p->sms, (gr.n + LCW - 1) / LCW);
+      const int mt = inv ? gr.mt_inv : gr.mt_fwd;
+#define FMP_LCL(MT)                                                                     \
+  case MT:                                                                              \
+    if (inv)                                                                            \
+      k_column_large<true, MT><<<grid, LCW * 32, kColLargeSmem, st>>>(a);               \
+    else                                                                                \
+      k_column_large<false, MT><<<grid, LCW * 32, kColLargeSmem, st>>>(a);              \
+    break;
+      switch (mt) {
+        FMP_LCL(5) FMP_LCL(6) FMP_LCL(7) FMP_LCL(8) FMP_LCL(9)
+        default: FMP_REQUIRE(false, "unsupported large column tile count %d", mt);
+      }
+#undef FMP_LCL
+      FMP_CHECK_LAUNCH();
+    }
     return 0;
   }
   ColArgs a{};

@@ -278,6 +278,10 @@ class SolvePlan:
                                                    _lib.stream())
         _lib.check(rc, "fmp_precond_apply")
 
+    def path(self) -> str:
+        """Transform kernel family of this plan: 'fast', 'large' or 'general' (fmp_precond_path)."""
+        return {0: "general", 1: "fast", 2: "large"}[_lib.lib().fmp_precond_path(self._handle)]
+
     def gemm_kind(self) -> str:
         """Woodbury GEMM this plan was created with: 'ozaki' (default), 'own' or 'cublas'."""
         return self._gemm
