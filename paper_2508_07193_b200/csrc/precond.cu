@@ -20,6 +20,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <string>
+#include <type_traits>
 #include <vector>
 #include <cublas_v2.h>
 #include "common.cuh"
@@ -1534,6 +1535,224 @@ __global__ void __launch_bounds__(LCW * 32, 1) k_column_large(LargeColArgs A) {
   cp_async_wait<0>();
 }
 
+// Plane passes for extents up to 72: a CTA holds the F_x / F_y of one (component, ex, ey)
+// combination and LPG groups of 4 warps; each group transforms one plane at a time in its own
+// buffer (the step-1 result overwrites the plane in place, rows split over the group's warps),
+// with named barriers inside the group only, so the groups overlap each other's loads.
+constexpr int LPG = 3;                     // warp groups per CTA
+constexpr int kPlaneLargeSmem = (2 * LMAT + LPG * LMAT) * (int)sizeof(double);
+
+struct LargePlaneCta {   // one CTA's work: items [beg, end) of one (component, ex, ey) combination
+  int beg, end, c, ex, ey, pad;
+  int64_t fx, fy;        // forward factors along x and y (offsets into the factor buffer)
+};
+
+struct LargePlaneArgs {
+  const fmp_subdomain* subs;
+  const LargePlaneCta* ctas;
+  const int2* items;     // (sub, plane): forward planes k < ez, inverse planes k < wz (owned)
+  Geo g;
+  const double* src;
+  double* dst;
+  const double* factors;
+  int mode;
+  int tma_rows;          // > 0: forward planes inside the block arrive as one TMA box of LSM x tma_rows
+};
+
+__device__ __forceinline__ void group_sync(int gi) {
+  asm volatile("bar.sync %0, 128;\n" ::"r"(gi + 1) : "memory");
+}
+
+// acc[r][n] += X(row tile rows[r]) * B(col tile n), NR row tiles x NN column tiles of 8, K = 4 k4
+//   A(m, k) = Xa[(8 rows[r] + g) * sa + 4 kk + t]          (row-major operand, lda = sa)
+//   B(k, n) = INV-style or forward-style addressing through (bk, bn) strides
+template <int NR, int NN>
+__device__ __forceinline__ void lmma(double (&acc)[NR][NN][2], const double* a0, int sa, const double* b0, int bsk,
+                                     int bsn, int k4, const int (&rows)[NR]) {
+  for (int kk = 0; kk < k4; ++kk) {
+    double av[NR];
+#pragma unroll
+    for (int r = 0; r < NR; ++r) av[r] = a0[rows[r] * 8 * sa + kk * 4];
+#pragma unroll
+    for (int n = 0; n < NN; ++n) {
+      const double bv = b0[kk * 4 * bsk + n * 8 * bsn];
+#pragma unroll
+      for (int r = 0; r < NR; ++r) dmma884(acc[r][n][0], acc[r][n][1], av[r], bv);
+    }
+  }
+}
+
+// Steps 1 and 2 of one plane of k_plane_large (group barrier between them).  FULL: 9 output
+// tiles per axis (forward, and inverse when the owned tile is wider than 64); else 8.
+template <bool INV, bool FULL>
+__device__ __forceinline__ void plane_large_steps(double* X, const double* Fx, const double* Fy, const SubD& d,
+                                                  const LargePlaneArgs& A, int2 w, int c, int ex, int ey, int k41,
+                                                  int k42, int shift, int role, int gi, int g, int t) {
+    // ---- step 1: T[r][a] = sum_i X[r][i] Fx[a][i]  (INV: T[b][i'] = sum_a X[b][a] Fx[a][ox + i'])
+    // row tiles of this warp: role, role + 4 (+ 8 for role 0); 9 column tiles (INV: 8, owned)
+    {
+      const double* xa = X + g * LSM + t + shift;
+      const double* fb = INV ? Fx + t * LSM + g + d.ox : Fx + g * LSM + t;
+      const int bsk = INV ? LSM : 1, bsn = INV ? 1 : LSM;
+      constexpr int NN = FULL ? 9 : 8;   // INV: only the owned columns (8 tiles when wx <= 64)
+      if (role == 0) {
+        double acc[3][NN][2] = {};
+        const int rows[3] = {0, 4, 8};
+        lmma<3, NN>(acc, xa, LSM, fb, bsk, bsn, k41, rows);
+        __syncwarp();   // this warp's X rows are consumed: overwrite them with T
+#pragma unroll
+        for (int r = 0; r < 3; ++r) {
+          double* tr = X + (rows[r] * 8 + g) * LSM + 2 * t;
+#pragma unroll
+          for (int n = 0; n < NN; ++n) *reinterpret_cast<double2*>(tr + n * 8) = make_double2(acc[r][n][0], acc[r][n][1]);
+        }
+      } else {
+        double acc[2][NN][2] = {};
+        const int rows[2] = {role, role + 4};
+        lmma<2, NN>(acc, xa, LSM, fb, bsk, bsn, k41, rows);
+        __syncwarp();
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+          double* tr = X + (rows[r] * 8 + g) * LSM + 2 * t;
+#pragma unroll
+          for (int n = 0; n < NN; ++n) *reinterpret_cast<double2*>(tr + n * 8) = make_double2(acc[r][n][0], acc[r][n][1]);
+        }
+      }
+    }
+    // the shifted forward plane: T starts at column 0 (written above); rows keep their index
+    group_sync(gi);
+    // ---- step 2: O[b][a] = sum_j Fy[b][j] T[j][a]  (INV: O[j'][i'] = sum_b Fy[b][oy + j'] T[b][i'])
+    // column tiles of this warp: role, role + 4 (+ 8 for role 0); 9 row tiles (INV: 8, owned)
+    {
+      const double* fa = INV ? Fy + t * LSM + g + d.oy : Fy + g * LSM + t;   // A(m, k) = Fy-based
+      const int ask = INV ? LSM : 1, asm_ = INV ? 1 : LSM;
+      const int64_t obase = INV ? 0 : d.ws_off + (int64_t)(c * d.ez + w.y) * d.ps;
+      auto run = [&](auto ncols) {
+        constexpr int NC = decltype(ncols)::value;
+        int cols[NC];
+        cols[0] = role;
+        cols[1] = role + 4;
+        if (NC == 3) cols[NC - 1] = 8;
+        double acc[9][NC][2] = {};
+        const double* tb = X + t * LSM + g;
+        for (int kk = 0; kk < k42; ++kk) {
+          double bv[NC];
+#pragma unroll
+          for (int q = 0; q < NC; ++q) bv[q] = tb[kk * 4 * LSM + cols[q] * 8];
+#pragma unroll
+          for (int m = 0; m < 9; ++m) {
+            if (!FULL && m == 8) break;
+            const double av = fa[kk * 4 * ask + m * 8 * asm_];
+#pragma unroll
+            for (int q = 0; q < NC; ++q) dmma884(acc[m][q][0], acc[m][q][1], av, bv[q]);
+          }
+        }
+#pragma unroll
+        for (int m = 0; m < 9; ++m) {
+          if (!FULL && m == 8) break;
+          const int row = m * 8 + g;
+          if (!INV && row >= ey) continue;
+          if (INV && row >= d.wy) continue;
+#pragma unroll
+          for (int q = 0; q < NC; ++q) {
+            const int col = cols[q] * 8 + 2 * t;
+            if (!INV) {
+              double* o = A.dst + obase + row * ex + col;
+              if ((ex & 1) == 0 && col + 1 < ex) {
+                *reinterpret_cast<double2*>(o) = make_double2(acc[m][q][0], acc[m][q][1]);
+              } else {
+                if (col < ex) o[0] = acc[m][q][0];
+                if (col + 1 < ex) o[1] = acc[m][q][1];
+              }
+            } else if (col < d.wx) {
+              double* o = A.dst + fidx(A.g, c, d.lz + d.oz + w.y, d.ly + d.oy + row, d.lx + d.ox + col);
+              if (col + 1 < d.wx && (((uintptr_t)o) & 15) == 0) {
+                *reinterpret_cast<double2*>(o) = make_double2(acc[m][q][0], acc[m][q][1]);
+              } else {
+                o[0] = acc[m][q][0];
+                if (col + 1 < d.wx) o[1] = acc[m][q][1];
+              }
+            }
+          }
+        }
+      };
+      if (role == 0 && FULL)
+        run(std::integral_constant<int, 3>{});
+      else
+        run(std::integral_constant<int, 2>{});
+    }
+}
+
+template <bool INV>
+__global__ void __launch_bounds__(LPG * 128, 1) k_plane_large(const __grid_constant__ CUtensorMap tm, LargePlaneArgs A) {
+  extern __shared__ __align__(128) double smem[];
+  __shared__ __align__(8) uint64_t pbar[LPG];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
+  const int gi = warp >> 2, wq = warp & 3;
+  // rotated row-tile role inside the group: the heavy role (3 tiles) lands on a different SM
+  // sub-partition in each group
+  const int role = (wq + gi) & 3;
+  const LargePlaneCta cw = A.ctas[blockIdx.x];
+  double* Fx = smem;
+  double* Fy = smem + LMAT;
+  double* X = smem + (2 + gi) * LMAT;
+  const int ex = cw.ex, ey = cw.ey;
+  for (int q = tid; q < LMAT; q += blockDim.x) {
+    const int r = q / LSM, c = q - r * LSM;
+    Fx[q] = (r < ex && c < ex) ? __ldg(A.factors + cw.fx + r * ex + c) : 0.0;
+    Fy[q] = (r < ey && c < ey) ? __ldg(A.factors + cw.fy + r * ey + c) : 0.0;
+  }
+  for (int q = tid; q < LPG * LMAT; q += blockDim.x) smem[2 * LMAT + q] = 0.0;
+  if (tid == 0) {
+    for (int q = 0; q < LPG; ++q) mbar_init(&pbar[q], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const int c = cw.c;
+  uint32_t tphase = 0;
+  const int k41 = pad4(ex) / 4, k42 = pad4(ey) / 4;
+  for (int it = cw.beg + gi; it < cw.end; it += LPG) {
+    const int2 w = A.items[it];
+    const SubD d = load_sub(A.subs + w.x);
+    // ---- load the plane (rows at stride LSM): TMA box (forward, inside the block) or cp.async
+    int shift = 0;
+    const bool inside = d.lx >= 0 && d.ly >= 0 && d.lz >= 0 && d.lx + ex <= A.g.bx && d.ly + ey <= A.g.by &&
+                        d.lz + d.ez <= A.g.bz;
+    if (!INV && A.mode != FMP_SOLVE_FACES && inside && A.tma_rows > 0) {
+      shift = d.lx & 1;   // the box starts at an even x (16-byte aligned inner coordinate)
+      if (wq == 0 && lane == 0) {
+        fence_proxy_async();
+        mbar_expect_tx(&pbar[gi], (uint32_t)(LSM * A.tma_rows * 8));
+        tma_load_4d(X, &tm, d.lx & ~1, d.ly, d.lz + w.y, c, &pbar[gi]);
+      }
+      mbar_wait(&pbar[gi], tphase);
+      tphase ^= 1u;
+    } else {
+      const int64_t P = (int64_t)ex * ey;
+      for (int j = wq; j < ey; j += 4) {
+        for (int i = lane; i < ex; i += 32) {
+          const double* sp;
+          if (INV)
+            sp = A.src + d.ws_off + (int64_t)(c * d.ez + d.oz + w.y) * d.ps + j * ex + i;
+          else if (A.mode == FMP_SOLVE_FACES)
+            sp = A.src + d.in_off + c * P * d.ez + w.y * P + j * ex + i;
+          else
+            sp = point_ptr(A.g, A.src, c, d.lz + w.y, d.ly + j, d.lx + i);
+          cp_async8(X + j * LSM + i, sp, A.factors);
+        }
+      }
+      cp_async_commit();
+      cp_async_wait<0>();
+    }
+    group_sync(gi);
+    if (!INV || d.wx > 64 || d.wy > 64)
+      plane_large_steps<INV, true>(X, Fx, Fy, d, A, w, c, ex, ey, k41, k42, shift, role, gi, g, t);
+    else
+      plane_large_steps<INV, false>(X, Fx, Fy, d, A, w, c, ex, ey, k41, k42, shift, role, gi, g, t);
+    group_sync(gi);   // the buffer is free for the group's next plane
+  }
+}
+
 // ---------------------------------------------------------------- K5 / K6: boundary faces
 // Component c has two boundary faces with nonzero delta (ref:operators.py:151-164):
 //   c = x: z-normal (k = 0, all j,i) and y-normal (j = 0, k >= 1)
@@ -1930,6 +2149,10 @@ struct fmp_precond {
   std::vector<LColGroup> lcol;
   int2* d_lcol = nullptr;
   CUtensorMap* d_lcolmaps = nullptr;
+  // large plane passes: per-CTA (combination, item range) tables, forward and inverse
+  LargePlaneCta* d_lpc[2] = {nullptr, nullptr};
+  int2* d_lpi[2] = {nullptr, nullptr};
+  int n_lpc[2] = {0, 0};
   // Woodbury GEMM (set at plan creation from FMP_GEMM): Ozaki INT8 tensor-core GEMM (default,
   // "ozaki": int8 slices of C^-1 built once, Y sliced per apply), the own DMMA kernel ("own") or
   // cuBLAS DGEMM ("cublas")
@@ -1982,6 +2205,10 @@ static void free_plan(fmp_precond* p) {
   cudaFree(p->d_colmaps);
   cudaFree(p->d_lcol);
   cudaFree(p->d_lcolmaps);
+  for (int q = 0; q < 2; ++q) {
+    cudaFree(p->d_lpc[q]);
+    cudaFree(p->d_lpi[q]);
+  }
   cudaFree(p->d_gshapes);
   for (int q = 0; q < fmp_precond::kAux; ++q) {
     if (p->aux_blas[q]) cublasDestroy(p->aux_blas[q]);
@@ -2160,6 +2387,49 @@ extern "C" int fmp_precond_create(const fmp_precond_desc* desc, fmp_precond** ou
         free_plan(p);
         return -1;
       }
+      // plane items grouped by (component, ex, ey); CTAs assigned to combinations in proportion
+      // to their planes, each CTA a contiguous range of one combination's items
+      int sms_now = kNumSM;
+      {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms_now, cudaDevAttrMultiProcessorCount, dev);
+      }
+      for (int dir = 0; dir < 2 && p->large; ++dir) {
+        struct Combo { int c, ex, ey; int64_t fx, fy; std::vector<int2> items; };
+        std::vector<Combo> combos;
+        for (int64_t q = 0; q < desc->n_sub; ++q) {
+          const auto& sd = p->subs[q];
+          const auto& sh = p->shapes[sd.shape];
+          const int ex = (int)sd.ext[0], ey = (int)sd.ext[1], np = dir == 0 ? (int)sd.ext[2] : (int)sd.own[2];
+          for (int c = 0; c < 3; ++c) {
+            size_t k = 0;
+            while (k < combos.size() && !(combos[k].c == c && combos[k].ex == ex && combos[k].ey == ey)) ++k;
+            if (k == combos.size())
+              combos.push_back(Combo{c, ex, ey, c == 0 ? sh.ut_off[0] : sh.vt_off[0], c == 1 ? sh.ut_off[1] : sh.vt_off[1], {}});
+            for (int z = 0; z < np; ++z) combos[k].items.push_back(make_int2((int)q, z));
+          }
+        }
+        int64_t total = 0;
+        for (const auto& cb : combos) total += (int64_t)cb.items.size();
+        const int budget = std::max<int>(sms_now, (int)combos.size());
+        std::vector<LargePlaneCta> ctas;
+        std::vector<int2> items;
+        for (const auto& cb : combos) {
+          const int n = (int)cb.items.size();
+          const int nc = std::max(1, std::min(n, (int)((int64_t)budget * n / std::max<int64_t>(total, 1))));
+          const int base = (int)items.size();
+          items.insert(items.end(), cb.items.begin(), cb.items.end());
+          for (int b = 0; b < nc; ++b)
+            ctas.push_back(LargePlaneCta{base + (int)((int64_t)n * b / nc), base + (int)((int64_t)n * (b + 1) / nc), cb.c,
+                                         cb.ex, cb.ey, 0, cb.fx, cb.fy});
+        }
+        p->n_lpc[dir] = (int)ctas.size();
+        if (upload(ctas, &p->d_lpc[dir]) || upload(items, &p->d_lpi[dir])) {
+          free_plan(p);
+          return -1;
+        }
+      }
       bool col_tma = p->large && !getenv_flag("FMP_COL_NO_TMA") && ((uintptr_t)desc->work_a & 15) == 0 &&
                      ((uintptr_t)desc->work_b & 15) == 0;
       for (int64_t q = 0; q < desc->n_sub; ++q) col_tma = col_tma && (p->subs[q].ws_off & 1) == 0;
@@ -2333,6 +2603,8 @@ extern "C" int fmp_precond_create(const fmp_precond_desc* desc, fmp_precond** ou
   cudaFuncSetAttribute(k_column_large<true, MT>, cudaFuncAttributeMaxDynamicSharedMemorySize, kColLargeSmem);
     FMP_LCA(5) FMP_LCA(6) FMP_LCA(7) FMP_LCA(8) FMP_LCA(9)
 #undef FMP_LCA
+    cudaFuncSetAttribute(k_plane_large<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kPlaneLargeSmem);
+    cudaFuncSetAttribute(k_plane_large<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kPlaneLargeSmem);
   }
   FMP_CHECK_CUDA(cudaGetLastError());
   *out = p;
@@ -2489,6 +2761,35 @@ static int plane_pass(fmp_precond* p, const fmp_block* blk, bool inv, int mode, 
       k_plane_fast<false, 3><<<grid, PW_WARPS * 32, kPlaneFastSmem, st>>>(tm, a);
     else
       k_plane_fast<false><<<grid, PW_WARPS * 32, kPlaneFastSmem, st>>>(tm, a);
+    FMP_CHECK_LAUNCH();
+    return 0;
+  }
+  if (p->large && !getenv_flag("FMP_NO_LARGE_PLANE")) {
+    const int dir = inv ? 1 : 0;
+    LargePlaneArgs a{};
+    a.subs = p->d.subs;
+    a.ctas = p->d_lpc[dir];
+    a.items = p->d_lpi[dir];
+    a.g = make_geo(blk);
+    a.src = src;
+    a.dst = dst;
+    a.factors = p->d.factors;
+    a.mode = mode;
+    CUtensorMap tm{};
+    a.tma_rows = 0;
+    if (!inv && mode != FMP_SOLVE_FACES && (blk->bx & 1) == 0 && ((uintptr_t)src & 15) == 0 &&
+        !getenv_flag("FMP_PLANE_NO_TMA")) {
+      const uint64_t dims[4] = {(uint64_t)blk->bx, (uint64_t)blk->by, (uint64_t)blk->bz, 3};
+      const uint64_t strides[3] = {(uint64_t)blk->bx * 8, (uint64_t)(blk->bx * blk->by) * 8,
+                                   (uint64_t)(blk->bx * blk->by * blk->bz) * 8};
+      const uint32_t box[4] = {LSM, (uint32_t)p->max_ey, 1, 1};
+      if (int e = encode_tensor_map_f64(&tm, src, 4, dims, strides, box)) return e;
+      a.tma_rows = p->max_ey;
+    }
+    if (inv)
+      k_plane_large<true><<<p->n_lpc[dir], LPG * 128, kPlaneLargeSmem, st>>>(tm, a);
+    else
+      k_plane_large<false><<<p->n_lpc[dir], LPG * 128, kPlaneLargeSmem, st>>>(tm, a);
     FMP_CHECK_LAUNCH();
     return 0;
   }
