@@ -10,8 +10,8 @@ The reference assembles C with m exact solves on identity columns and a CPU
 `np.linalg.inv` (38-55 s per 32^3-class box).  Here the m columns go through the
 same batched GPU kernels as the preconditioner (mode FACES: forward transform,
 block solve, and the inverse transform evaluated on the two boundary faces only),
-and the inverse is a device LU (`torch.linalg.inv`), with the reference's
-1-norm condition guard.
+and the inverse is a device Cholesky inverse (C is SPD; LU fallback), with the
+reference's 1-norm condition guard.
 
 `exact_solve` / `solve` run a one-subdomain plan; the RAS preconditioner
 (schwarz.py) batches every subdomain of a GPU block into one plan.
@@ -165,11 +165,20 @@ def _assemble_correction(box: Box, alpha: float, device) -> BoundaryCorrection:
     weight_inv = 1.0 / (alpha * values)
     Cm = CT.t().contiguous()
     Cm.diagonal().add_(torch.from_numpy(weight_inv).to(device))
-    try:
-        inv = torch.linalg.inv(Cm)
-    except RuntimeError as exc:   # torch raises on exactly singular input
-        raise DegenerateConfigurationError(
-            f"correction matrix singular for box {box.extents}, alpha={alpha}") from exc
+    # C = Q^T (I + alpha M)^-1 Q + diag(1 / (alpha delta)) is symmetric positive definite (the
+    # double-curl operator is SPD), so the inverse goes through a Cholesky factorisation of its
+    # lower triangle (an exactly symmetric C^-1, as SURVEY 8f #1 plans); LU only if the
+    # factorisation reports a non-positive pivot.
+    L, info = torch.linalg.cholesky_ex(Cm)
+    if int(info) == 0:
+        inv = torch.cholesky_inverse(L)
+    else:
+        try:
+            inv = torch.linalg.inv(Cm)
+        except RuntimeError as exc:   # torch raises on exactly singular input
+            raise DegenerateConfigurationError(
+                f"correction matrix singular for box {box.extents}, alpha={alpha}") from exc
+    del L
     cond1 = float(Cm.abs().sum(0).max() * inv.abs().sum(0).max())
     if not np.isfinite(cond1) or cond1 > CONDITION_LIMIT:
         raise DegenerateConfigurationError(
