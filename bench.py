@@ -40,6 +40,10 @@ CONFIGS = {
     "cfg4": ((256, 256, 256), (32, 32, 32), 1),
     "cfg2": ((64, 64, 64), (32, 32, 32), 1),
     "cfg1": ((32, 32, 32), (32, 32, 32), 1),
+    # BASELINE config 5 (subdomain-size sweep at 512^3 on 8 GPUs): the per-GPU 256^3 block with
+    # 16^3 / 64^3 subdomains (32^3 is cfg4); --method gmres for its GMRES leg
+    "cfg5_sd16": ((256, 256, 256), (16, 16, 16), 1),
+    "cfg5_sd64": ((256, 256, 256), (64, 64, 64), 1),
 }
 
 
@@ -139,7 +143,7 @@ class ClockSampler:
 
 # ----------------------------------------------------------------------------------- ours
 INT8_PROBE_FILE = ROOT / "profiles" / "r01_umma_i8_rate.json"
-NCU_TRAFFIC_FILE = ROOT / "profiles" / "r01_v36_ncu_traffic.json"
+NCU_TRAFFIC_FILE = ROOT / "profiles" / "r02_v01_ncu_traffic.json"
 # bench stage -> ncu kernel name(s) whose DRAM bytes (one ncu --set full capture) it covers
 STAGE_KERNELS = {"plane_fwd": ["k_plane_fast<0, 5>"], "column_fwd": ["k_column_fast_db<0, 12, 5, 2>"],
                  "faces": ["k_faces<5, 2, 5>"], "slice_y": ["k_ozaki_slice_rows", "k_ozaki_exp", "k_ozaki_digits"], "gemm": ["k_ozaki"],
@@ -162,8 +166,8 @@ def int8_peak_tops() -> tuple[float, str]:
 
 
 def dominant_roofline(stages: dict) -> dict | None:
-    """Roofline of the dominant single kernel of the step: the Ozaki Woodbury GEMM (k_ozaki, ~19%
-    of the step, profiles/r01_v36_launches_step_summary.txt). Algorithmic work = 28 int8 slice
+    """Roofline of the dominant single kernel of the step: the Ozaki Woodbury GEMM (k_ozaki, ~17%
+    of the step, profiles/r02_v01_launches_step_summary.txt). Algorithmic work = 28 int8 slice
     products x 2 m^2 n (unpadded) per launch; peak = the measured tcgen05 kind::i8 rate."""
     g = stages.get("gemm", {})
     if "int8_tops" not in g:
@@ -172,7 +176,7 @@ def dominant_roofline(stages: dict) -> dict | None:
             "op_type": "int8 multiply-add = 2 ops", "bound": "tensor", "achieved": g["int8_tops"],
             "peak": g["peak_int8_tops"], "unit": "TFLOP/s", "frac": g["frac"], "traffic": g.get("traffic_bytes"),
             "time_ms": g["ms"], "peak_source": g["peak_source"],
-            "traffic_source": "ncu --set full, dram__bytes_read.sum + dram__bytes_write.sum (profiles/r01_v36_ncu_traffic.json)"}
+            "traffic_source": f"ncu --set full, dram__bytes_read.sum + dram__bytes_write.sum ({NCU_TRAFFIC_FILE.relative_to(ROOT)})"}
 
 
 def stage_rooflines(prec, x, z, specs, peaks, reps):
@@ -250,7 +254,7 @@ def run_ours(args):
     sgrid = tuple(n // s for n, s in zip(gext, sub))
     alpha = 0.25
     dt = 2.0 * math.sqrt(alpha)     # ref:cli.py:145
-    cfg = SolverConfig(method="bicgstab", tol=1e-12, max_iter=1000)
+    cfg = SolverConfig(method=args.method, tol=1e-12, max_iter=1000)
     t_setup = time.perf_counter()
     solver = CnSolver(Box(*gext), sgrid, overlap, alpha, cfg, tr)
     torch.cuda.synchronize()
@@ -392,7 +396,7 @@ def run_ours(args):
         "metric": METRIC, "value": round(value, 3), "unit": "MDoF/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms_per_step, 3), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic: E,H ~ U[-1,1) (torch Philox, seed 42+rank)",
-        "config": {"workload": f"{args.config}: CN-FDTD step, BiCGSTAB+FlashMP RAS, tol 1e-12, alpha 0.25, "
+        "config": {"workload": f"{args.config}: CN-FDTD step, {'GMRES(30)' if getattr(args, 'method', 'bicgstab') == 'gmres' else 'BiCGSTAB'}+FlashMP RAS, tol 1e-12, alpha 0.25, "
                                f"overlap {overlap}", "global_grid": list(gext), "per_gpu_block": list(block),
                    "subdomain": list(sub), "subdomain_grid": list(sgrid), "gpu_grid": list(ggrid),
                    "parallelism": f"domain decomposition x{world}",
@@ -417,7 +421,7 @@ def run_ours(args):
                      if peaks["fp64_tflops"] else None,
                      "traffic": (sum(v.get("traffic_bytes", 0) for v in stages.values()) or None),
                      "traffic_note": "DRAM bytes per apply, sum over its kernels from one ncu --set full capture "
-                                     "(profiles/r01_v36_ncu_traffic.json); algorithmic bytes "
+                                     f"({NCU_TRAFFIC_FILE.relative_to(ROOT)}); algorithmic bytes "
                                      f"{bytes_alg} (precond_apply.algorithmic_bytes)",
                      "peak_source": peaks["fp64_source"], "flops_per_launch": flops_exec},
         "breakdown_ms": breakdown,
@@ -426,7 +430,7 @@ def run_ours(args):
         "e2e": e2e,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(args.config, steps=args.cpu_steps)
+        line["cpu_baseline"] = cpu_baseline(args.config, steps=args.cpu_steps, method=args.method)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -443,17 +447,19 @@ def run_ours(args):
 # seconds on the host cores.  Precompute (C^-1 per extended shape) is setup, outside the timed
 # region, as in the reference's own cn_steps.csv seconds (ref:cli.py:164-171).
 CPU_SAMPLE = {"cfg4": ((128, 128, 128), (32, 32, 32)), "cfg2": ((64, 64, 64), (32, 32, 32)),
-              "cfg1": ((32, 32, 32), (32, 32, 32))}
+              "cfg1": ((32, 32, 32), (32, 32, 32)), "cfg5_sd16": ((64, 64, 64), (16, 16, 16)),
+              "cfg5_sd64": ((64, 64, 64), (64, 64, 64))}
 
 
 class CpuCnSample:
     """Real CN steps of the CPU reference algorithm (oracle port) on the sample grid."""
 
-    def __init__(self, config: str, seed: int = 42):
+    def __init__(self, config: str, seed: int = 42, method: str = "bicgstab"):
         sys.path.insert(0, str(ROOT / "oracle"))
         import flashmp_oracle as O
         self.O = O
         self.gext, sub = CPU_SAMPLE[config]
+        self.sub, self.method = sub, method
         self.grid = tuple(n // s for n, s in zip(self.gext, sub))
         self.alpha = 0.25
         self.dt = 2.0 * math.sqrt(self.alpha)      # ref:cli.py:145
@@ -475,6 +481,8 @@ class CpuCnSample:
         prec = lambda u: O.ras_apply(g, self.ranks, a, u)
 
         def solve(rhs):
+            if self.method == "gmres":
+                return O.gmres(op, prec, rhs.ravel(), restart=30, tol=1e-12, max_iter=1000)
             return O.bicgstab(op, prec, rhs.ravel(), tol=1e-12, max_iter=1000)
 
         t0 = time.perf_counter()
@@ -485,15 +493,16 @@ class CpuCnSample:
 
     def describe(self, steps: int) -> str:
         return (f"oracle/flashmp_oracle.py (numpy restatement of the reference; OpenBLAS threads = host cores): "
-                f"{steps} real CN steps (RHS, BiCGSTAB to 1e-12 with real C^-1, H update; time-marching) on a "
-                f"{'x'.join(map(str, self.gext))} grid of {len(self.ranks)} subdomains of 32^3 (overlap 1, "
+                f"{steps} real CN steps (RHS, {'GMRES(30)' if self.method == 'gmres' else 'BiCGSTAB'} to 1e-12 with "
+                f"real C^-1, H update; time-marching) on a {'x'.join(map(str, self.gext))} grid of "
+                f"{len(self.ranks)} subdomains of {self.sub[0]}^3 (overlap 1, "
                 f"alpha 0.25), measured iterations per step {self.iters}; C^-1 precompute {self.setup_s:.1f} s "
                 f"untimed (setup)")
 
 
-def cpu_baseline(config: str, steps: int = 2):
+def cpu_baseline(config: str, steps: int = 2, method: str = "bicgstab"):
     """Rank-0, N=1 CPU baseline beside our own line: `steps` real CN steps of the sample."""
-    smp = CpuCnSample(config)
+    smp = CpuCnSample(config, method=method)
     smp.step()                                    # warm-up (first-touch, BLAS thread pool)
     times = [smp.step() for _ in range(steps)]
     sec = statistics.mean(times)
@@ -506,7 +515,7 @@ def run_reference(args):
     if rank != 0:
         return
     world = int(os.environ.get("WORLD_SIZE", "1"))
-    smp = CpuCnSample(args.config)
+    smp = CpuCnSample(args.config, method=args.method)
     for _ in range(args.warmup):
         smp.step()
     smp.iters.clear()
@@ -520,7 +529,7 @@ def run_reference(args):
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(step * 1e3, 1),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic: E,H ~ U[-1,1) (numpy PCG64 seed 42, ref:cli.py:143-149)",
-            "config": {"workload": f"{args.config}: CN-FDTD step, BiCGSTAB+FlashMP RAS, tol 1e-12, alpha 0.25, "
+            "config": {"workload": f"{args.config}: CN-FDTD step, {'GMRES(30)' if getattr(args, 'method', 'bicgstab') == 'gmres' else 'BiCGSTAB'}+FlashMP RAS, tol 1e-12, alpha 0.25, "
                                    f"overlap {overlap} (CPU reference algorithm on a bounded sample grid)",
                        "sample_grid": list(smp.gext), "subdomain": list(sub), "subdomain_grid": list(smp.grid),
                        "world_launch": world},
@@ -539,6 +548,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="cfg4", choices=sorted(CONFIGS))
+    ap.add_argument("--method", default="bicgstab", choices=["bicgstab", "gmres"],
+                    help="Krylov method (BASELINE configs 1-4: BiCGSTAB; config 5 also GMRES(30))")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-steps", type=int, default=2, help="timed CN steps of the CPU baseline sample")
