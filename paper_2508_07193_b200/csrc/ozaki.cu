@@ -17,8 +17,9 @@
 // for each (128-row tile, 32-byte K chunk) the S slices are one contiguous block of
 // S x [2 K-halves][16 row groups][8 rows][16 B] -- so a pipeline stage is two bulk copies
 // (cp.async.bulk, mbarrier complete_tx), no tensor maps.  One CTA per SM, persistent over
-// (shape, row tile, column tile); warp 4 streams operands, warp 5 issues the S(S+1)/2 MMAs
-// per K chunk into S TMEM accumulators (one per level), warps 0-3 drain TMEM, combine the
+// (shape, row tile, column tile); warp 8 streams operands, warp 9 issues the S(S+1)/2 MMAs
+// per K chunk into S TMEM accumulators (one per level), warps 0-7 drain TMEM (two per lane
+// quadrant, alternate 8-column groups), combine the
 // levels in FP64 and store Z.
 #include <algorithm>
 #include <cstdint>
@@ -39,7 +40,8 @@ constexpr int OZ_PART = OZ_MAX_K / OZ_KC;   // max K chunks of one segment
 constexpr int OZ_ABLK = OZ_M * OZ_KC;   // bytes of one A slice block
 constexpr int OZ_STAGE = OZ_S * OZ_ABLK + OZ_RMAX * OZ_KC;
 constexpr int OZ_STAGES = 5;
-constexpr int OZ_THREADS = 192;         // warps 0-3 epilogue, 4 producer, 5 MMA
+constexpr int OZ_EPI = 8;               // epilogue warps: two per TMEM lane quadrant, each half the column groups
+constexpr int OZ_THREADS = (OZ_EPI + 2) * 32;   // warps 0-7 epilogue, 8 producer, 9 MMA
 constexpr int OZ_TMEM_COLS = 512;
 constexpr int OZ_SLOT = OZ_WMAX * OZ_M; // doubles of one partial slot ([column][row])
 static_assert(OZ_S * OZ_WMAX + 8 <= OZ_TMEM_COLS, "levels x width exceed TMEM");
@@ -81,11 +83,12 @@ __device__ __forceinline__ void umma_i8(uint32_t tmem, uint64_t da, uint64_t db,
 // TMEM columns [(L-2) W, (L-1) W); the pad16 tail of an MMA reads the next stacked slice (or the
 // zero rows past the last one) and lands in columns >= 7 W, which no level uses.  W is a template
 // constant so every descriptor and TMEM offset folds to an immediate.
-template <int W>
-__device__ __forceinline__ void issue_chunk(uint64_t da0, uint64_t db0, uint32_t tmem, bool first) {
+template <int W, bool REV>
+__device__ __forceinline__ void issue_chunk_order(uint64_t da0, uint64_t db0, uint32_t tmem, bool first) {
   constexpr uint32_t IDESC0 = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(OZ_M >> 4) << 24);
 #pragma unroll
-  for (int p = 1; p <= OZ_S; ++p) {
+  for (int pi = 1; pi <= OZ_S; ++pi) {
+    const int p = REV ? OZ_S + 1 - pi : pi;
     const uint64_t da = da0 + (uint64_t)(((p - 1) * OZ_ABLK) >> 4);
     const uint32_t acc = (first && p == 1) ? 0u : 1u;
     const int N = oz_pad16((OZ_S + 1 - p) * W);
@@ -102,6 +105,16 @@ __device__ __forceinline__ void issue_chunk(uint64_t da0, uint64_t db0, uint32_t
     }
   }
 }
+// The first chunk of a tile runs p = 1 first (its acc = 0 MMA spans every level's columns); the
+// others run p = S .. 1, so the chunk ends on its widest MMAs and the tensor pipe still holds
+// ~256 cycles of work while the issuing warp commits, waits for the next stage and sets up.
+template <int W>
+__device__ __forceinline__ void issue_chunk(uint64_t da0, uint64_t db0, uint32_t tmem, bool first, bool rev) {
+  if (first || !rev)
+    issue_chunk_order<W, false>(da0, db0, tmem, first);
+  else
+    issue_chunk_order<W, true>(da0, db0, tmem, false);
+}
 
 __device__ __forceinline__ void tmem_ld8(uint32_t addr, uint32_t (&v)[8]) {
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
@@ -112,6 +125,7 @@ __device__ __forceinline__ void tmem_ld8(uint32_t addr, uint32_t (&v)[8]) {
 __global__ void __launch_bounds__(OZ_THREADS, 1)
     k_ozaki(const OzShape* __restrict__ shapes, const OzItem* __restrict__ items, const int* __restrict__ offs,
             double* __restrict__ zpart, int* __restrict__ counters, long long* __restrict__ prof, int dbg) {
+  const bool rev = !(dbg & 16);   // FMP_OZ_DBG bit 4 (A/B): forward MMA order in every chunk
   extern __shared__ __align__(1024) uint8_t osm[];
   if (prof && threadIdx.x == 0) prof[blockIdx.x * 8 + 4] = (long long)globaltimer();
   __shared__ __align__(8) uint64_t full_bar[OZ_STAGES], empty_bar[OZ_STAGES], tfull_bar, tempty_bar;
@@ -130,7 +144,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
       mbar_init(&empty_bar[s], 1);
     }
     mbar_init(&tfull_bar, 1);
-    mbar_init(&tempty_bar, 128);
+    mbar_init(&tempty_bar, OZ_EPI * 32);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n");
@@ -138,7 +152,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
   asm volatile("tcgen05.fence::after_thread_sync;\n");
   const uint32_t tmem = tmem_base;
 
-  if (warp == 4) {
+  if (warp == OZ_EPI) {
     // ---------------- producer: two bulk copies per stage
     if (lane == 0) {
       int it = 0;
@@ -163,10 +177,10 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
         }
       }
     }
-  } else if (warp == 5) {
+  } else if (warp == OZ_EPI + 1) {
     // ---------------- MMA issuer
     int it = 0, tcount = 0;
-    long long t0 = clock64(), w_full = 0, w_empty = 0, t1;
+    long long t0 = clock64(), w_full = 0, w_empty = 0, w_first = 0, t1;
     for (int ti = offs[blockIdx.x]; ti < offs[blockIdx.x + 1]; ++ti, ++tcount) {
       const OzItem tl = items[ti];
       const OzShape sh = shapes[tl.shape];
@@ -183,7 +197,11 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
         const uint32_t ph = (it / OZ_STAGES) & 1;
         if (prof) t1 = clock64();
         mbar_wait(&full_bar[s], ph);
-        if (prof) w_full += clock64() - t1;
+        if (prof) {
+          const long long dt = clock64() - t1;
+          w_full += dt;
+          if (kc == tl.k0) w_first += dt;
+        }
         asm volatile("tcgen05.fence::after_thread_sync;\n");
         {
           const uint32_t sa = s_u32(osm + s * OZ_STAGE);
@@ -191,15 +209,15 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
           const uint64_t db0 = umma_desc(sa + OZ_S * OZ_ABLK, lbo_b, 128);
           const bool first = kc == tl.k0;
           if (!(dbg & 2)) switch (w) {   // FMP_OZ_DBG=2: no MMAs
-            case 8: issue_chunk<8>(da0, db0, tmem, first); break;
-            case 16: issue_chunk<16>(da0, db0, tmem, first); break;
-            case 24: issue_chunk<24>(da0, db0, tmem, first); break;
-            case 32: issue_chunk<32>(da0, db0, tmem, first); break;
-            case 40: issue_chunk<40>(da0, db0, tmem, first); break;
-            case 48: issue_chunk<48>(da0, db0, tmem, first); break;
-            case 56: issue_chunk<56>(da0, db0, tmem, first); break;
-            case 64: issue_chunk<64>(da0, db0, tmem, first); break;
-            default: issue_chunk<72>(da0, db0, tmem, first); break;
+            case 8: issue_chunk<8>(da0, db0, tmem, first, rev); break;
+            case 16: issue_chunk<16>(da0, db0, tmem, first, rev); break;
+            case 24: issue_chunk<24>(da0, db0, tmem, first, rev); break;
+            case 32: issue_chunk<32>(da0, db0, tmem, first, rev); break;
+            case 40: issue_chunk<40>(da0, db0, tmem, first, rev); break;
+            case 48: issue_chunk<48>(da0, db0, tmem, first, rev); break;
+            case 56: issue_chunk<56>(da0, db0, tmem, first, rev); break;
+            case 64: issue_chunk<64>(da0, db0, tmem, first, rev); break;
+            default: issue_chunk<72>(da0, db0, tmem, first, rev); break;
           }
           umma_commit(&empty_bar[s]);                 // stage free once these MMAs retire
           if (kc == tl.k1 - 1) umma_commit(&tfull_bar);  // accumulators complete
@@ -212,32 +230,34 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
       prof[blockIdx.x * 8 + 1] = w_full;
       prof[blockIdx.x * 8 + 2] = w_empty;
       prof[blockIdx.x * 8 + 3] = tcount;
+      prof[blockIdx.x * 8 + 6] = w_first;
     }
   } else {
-    // ---------------- epilogue warps 0-3: lane quadrant = warp, one row per thread
+    // ---------------- epilogue warps 0-7: lane quadrant = warp & 3, one row per thread
     int tcount = 0;
     for (int ti = offs[blockIdx.x]; ti < offs[blockIdx.x + 1]; ++ti, ++tcount) {
       const OzItem tl = items[ti];
       const OzShape sh = shapes[tl.shape];
       const int w = sh.w;
-      const int rr = warp * 32 + lane, row = tl.mt * OZ_M + rr;
+      const int quad = warp & 3, half = warp >> 2;   // TMEM lanes 32 quad .. +31; column groups half, half + 2, ...
+      const int rr = quad * 32 + lane, row = tl.mt * OZ_M + rr;
       // operand exponents of this item, fetched while the MMAs still run: the row's into a
       // register, the tile's column exponents into shared memory (one global load per column
       // instead of one dependent L2 round trip per 8 columns inside the drain loop)
       const int ea = row < sh.m ? sh.eA[row] : 0;
-      asm volatile("bar.sync 1, 128;\n" ::: "memory");   // previous item's readers of eb_sh are done
-      if (rr < w) {
+      asm volatile("bar.sync 1, 256;\n" ::: "memory");   // previous item's readers of eb_sh are done
+      if (half == 0 && rr < w) {
         const int n = tl.nt * w + rr;
         eb_sh[rr] = n < sh.n ? sh.eB[n] + 4 : 0;
       }
-      asm volatile("bar.sync 1, 128;\n" ::: "memory");
+      asm volatile("bar.sync 1, 256;\n" ::: "memory");
       double* part = tl.nseg > 1 ? zpart + (size_t)(tl.slot0 + tl.seg) * OZ_SLOT : nullptr;
       const int nvalid = min(w, sh.n - tl.nt * w);
       mbar_wait(&tfull_bar, tcount & 1);
       asm volatile("tcgen05.fence::after_thread_sync;\n");
-      for (int c0 = 0; c0 < w; c0 += 8) {
+      for (int c0 = half * 8; c0 < w; c0 += 16) {
         uint32_t v[OZ_S][8];
-        const uint32_t base = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0;
+        const uint32_t base = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)c0;
 #pragma unroll
         for (int L = 2; L <= OZ_S + 1; ++L) tmem_ld8(base + (uint32_t)((L - 2) * w), v[L - 2]);
         asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
@@ -275,15 +295,15 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
         // split tile: publish this segment, and the last segment to arrive sums all of them in
         // segment order (deterministic, independent of which CTA finishes last)
         __threadfence();
-        asm volatile("bar.sync 1, 128;\n" ::: "memory");
-        if (rr == 0) last_flag = atomicAdd(&counters[tl.slot0], 1) == tl.nseg - 1;
-        asm volatile("bar.sync 1, 128;\n" ::: "memory");
+        asm volatile("bar.sync 1, 256;\n" ::: "memory");
+        if (tid == 0) last_flag = atomicAdd(&counters[tl.slot0], 1) == tl.nseg - 1;
+        asm volatile("bar.sync 1, 256;\n" ::: "memory");
         if (last_flag) {
           __threadfence();
           if (row < sh.m) {
             const double* src = zpart + (size_t)tl.slot0 * OZ_SLOT + rr;
             constexpr int FC = 24;   // columns per round: FC loads of one segment in flight
-            for (int c0 = 0; c0 < nvalid; c0 += FC) {
+            for (int c0 = half * FC; c0 < nvalid; c0 += 2 * FC) {
               double s[FC];
 #pragma unroll
               for (int j = 0; j < FC; ++j) s[j] = 0.0;
@@ -299,7 +319,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
                 if (c0 + j < nvalid) sh.Z[(size_t)(tl.nt * w + c0 + j) * sh.ld + row] = s[j];
             }
           }
-          if (rr == 0) counters[tl.slot0] = 0;   // re-armed for the next launch
+          if (tid == 0) counters[tl.slot0] = 0;   // re-armed for the next launch
         }
       }
     }
@@ -432,15 +452,18 @@ int ozaki_launch(const OzPlan& p, cudaStream_t st) {
   return 0;
 }
 
-// Cost model of one K chunk (cycles): each MMA of the chunk costs max(N/2, 50) on the tensor pipe
-// (tools/umma_chunk.cu: N/2 for N >= 128, a ~50-cycle floor below), with the same N splits as
-// issue_chunk.  Only the ratios matter (w = 72 vs w = 8 tiles); the absolute rate is ~14% slower.
+// Cost model of one K chunk (cycles), fitted to the per-CTA MMA-warp cycles of a cfg4 apply
+// (tools/oz_prof.py with FMP_OZ_DUMP=1: ~1154 per 72-column chunk, ~602 per 8-column chunk, ~16.6K
+// per item): each MMA costs max(N/2, 80) on the tensor pipe (N/2 for N >= 160, tools/umma_seq.cu),
+// with the same N splits as issue_chunk, plus ~60 cycles of per-chunk issue overhead (stage
+// wait, commit); every work item adds OZ_ITEM_CYCLES (accumulator drain, pipeline restart).
+constexpr double OZ_ITEM_CYCLES = 16000.0;
 static double chunk_cycles(int w) {
-  double tensor = 0.0;
+  double tensor = 60.0;
   for (int p = 1; p <= OZ_S; ++p) {
     const int N = oz_pad16((OZ_S + 1 - p) * w);
     const int parts = (N + 255) / 256, step = oz_pad16((N + parts - 1) / parts);
-    for (int r0 = 0; r0 < N; r0 += step) tensor += std::max(50.0, std::min(step, N - r0) / 2.0);
+    for (int r0 = 0; r0 < N; r0 += step) tensor += std::max(80.0, std::min(step, N - r0) / 2.0);
   }
   return tensor;
 }
@@ -465,7 +488,7 @@ int ozaki_build(const std::vector<OzShape>& shapes, int sms, OzPlan* out) {
   struct Part { int shape, mt, nt, k0, k1, tile; double cc; };
   std::vector<Part> shared, solo;
   const char* sv = getenv("FMP_OZ_SOLO");   // modelled floor (cycles per chunk) of a solo chunk
-  const double solo_min = sv ? atof(sv) : 800.0;
+  const double solo_min = sv ? atof(sv) : 0.0;
   int n_tiles = 0;
   for (size_t s = 0; s < shapes.size(); ++s) {
     const OzShape& sh = shapes[s];
@@ -484,45 +507,93 @@ int ozaki_build(const std::vector<OzShape>& shapes, int sms, OzPlan* out) {
   }
   if (shared.empty() && solo.empty()) return 0;
   const int grid = std::min<int>(sms, (int)(shared.size() + solo.size()));
+  // sibling teams: when every shared shape has the same number k of column tiles, the waves use
+  // gw = grid - grid % k CTAs, so CTAs k t .. k t + k - 1 hold the k column tiles of one row tile
+  // in EVERY wave and share one remainder position (they stream the same C^-1 chunks together);
+  // the grid % k CTAs left out of the waves take a larger remainder piece instead
+  int team = 0;
+  for (const Part& r : shared) {
+    const int nts = (shapes[r.shape].n + shapes[r.shape].w - 1) / shapes[r.shape].w;
+    team = team == 0 ? nts : (team == nts ? team : -1);
+  }
+  const int gw = team > 1 && grid >= team ? grid - grid % team : grid;
+  const int tsz = team > 1 ? team : 3;
   const char* fv = getenv("FMP_OZ_WAVES");   // diagnostics: cap the number of data-parallel waves
-  int waves = (int)(shared.size() / grid);
+  int waves = (int)(shared.size() / gw);
   if (fv) waves = std::min(waves, atoi(fv));
-  std::vector<Part> rest(shared.begin() + (size_t)waves * grid, shared.end());
+  std::vector<Part> rest(shared.begin() + (size_t)waves * gw, shared.end());
   rest.insert(rest.end(), solo.begin(), solo.end());
-  double total = 0.0;
-  for (const Part& r : rest) total += r.cc * (r.k1 - r.k0);
-  // cut the remainder into `grid` contiguous pieces of equal cost (at K-chunk granularity)
-  std::vector<std::vector<Part>> piece(grid);
-  {
+  double total = 0.0, rest_total = 0.0;
+  for (const Part& r : rest) rest_total += r.cc * (r.k1 - r.k0) + OZ_ITEM_CYCLES;
+  rest_total += OZ_ITEM_CYCLES * grid;   // about one extra item per piece boundary
+  std::vector<double> wave_cost(grid, 0.0);
+  for (int j = 0; j < waves; ++j)
+    for (int b = 0; b < gw; ++b) {
+      const Part& q = shared[(size_t)j * gw + b];
+      wave_cost[b] += q.cc * (q.k1 - q.k0) + OZ_ITEM_CYCLES;
+    }
+  for (int b = 0; b < grid; ++b) total += wave_cost[b];
+  total += rest_total;
+  // piece b gets (total / grid - wave_cost[b]); cumulative targets for the cut below
+  // Cut the remainder into `grid` contiguous pieces (K-chunk granularity) so that every CTA's
+  // modelled load -- its wave items plus its piece, each item charged OZ_ITEM_CYCLES -- comes out
+  // at the same level T: greedy fill for a given T, T found by bisection so that the remainder
+  // is exactly used up.
+  auto cut = [&](double T, std::vector<std::vector<Part>>* out) -> double {   // returns the last CTA's load
+    if (out) out->assign(grid, {});
     int b = 0;
-    double used = 0.0;   // cost assigned to CTAs < b plus the current CTA's share so far
+    double load = wave_cost[0];
     for (const Part& r : rest) {
       int k = r.k0;
       while (k < r.k1) {
-        const double target = total * (b + 1) / grid;
         int take = r.k1 - k;
-        if (b < grid - 1 && used + take * r.cc > target) {
-          take = (int)std::floor((target - used) / r.cc + 0.5);
+        if (b < grid - 1 && load + OZ_ITEM_CYCLES + take * r.cc > T) {
+          take = (int)std::floor((T - load - OZ_ITEM_CYCLES) / r.cc + 0.5);
           take = std::max(0, std::min(take, r.k1 - k));
         }
         if (take > 0) {
-          Part seg = r;
-          seg.k0 = k;
-          seg.k1 = k + take;
-          piece[b].push_back(seg);
-          used += take * r.cc;
+          if (out) {
+            Part seg = r;
+            seg.k0 = k;
+            seg.k1 = k + take;
+            (*out)[b].push_back(seg);
+          }
+          load += take * r.cc + OZ_ITEM_CYCLES;
           k += take;
         }
-        if (k < r.k1 || used >= target - 0.5 * r.cc) b = std::min(b + 1, grid - 1);
+        if (k < r.k1 && b < grid - 1) load = wave_cost[++b];
       }
     }
+    return b == grid - 1 ? load : 0.0;
+  };
+  double lo = 0.0, hi = total / grid * 2.0 + OZ_ITEM_CYCLES * 8;
+  for (int itn = 0; itn < 60; ++itn) {
+    const double mid = 0.5 * (lo + hi);
+    if (cut(mid, nullptr) > mid) lo = mid; else hi = mid;
   }
+  std::vector<std::vector<Part>> piece;
+  cut(hi, &piece);
   std::vector<std::vector<Part>> lists(grid);
   for (int b = 0; b < grid; ++b) {
-    const int pos = (b / 3) % (waves + 1);
+    const int pos = (b / tsz) % (waves + 1);
     for (int j = 0; j <= waves; ++j) {
       if (j == pos) lists[b].insert(lists[b].end(), piece[b].begin(), piece[b].end());
-      if (j < waves) lists[b].push_back(shared[(size_t)j * grid + b]);
+      if (j < waves && b < gw) lists[b].push_back(shared[(size_t)j * gw + b]);
+    }
+  }
+  if (getenv_flag("FMP_OZ_DUMP")) {   // per CTA: items, modelled cost, chunks by kind (tools/oz_prof.py)
+    for (int b = 0; b < grid; ++b) {
+      double cost = 0.0;
+      long sh_ch = 0, solo_wide = 0, solo_narrow = 0, segs = 0;
+      for (const Part& q : lists[b]) {
+        const int nts = (shapes[q.shape].n + shapes[q.shape].w - 1) / shapes[q.shape].w;
+        cost += q.cc * (q.k1 - q.k0);
+        segs += (q.k1 - q.k0) < shapes[q.shape].kchunks;
+        if (nts > 1) sh_ch += q.k1 - q.k0;
+        else if (shapes[q.shape].w >= 32) solo_wide += q.k1 - q.k0;
+        else solo_narrow += q.k1 - q.k0;
+      }
+      fprintf(stderr, "ozdump %d %zu %.0f %ld %ld %ld %ld\n", b, lists[b].size(), cost, sh_ch, solo_wide, solo_narrow, segs);
     }
   }
   // segments per tile (in K order), partial slots for the split tiles
@@ -552,8 +623,8 @@ int ozaki_build(const std::vector<OzShape>& shapes, int sms, OzPlan* out) {
   out->grid = grid;
   out->n_items = (int)items.size();
   if (getenv_flag("FMP_OZ_VERBOSE"))
-    fprintf(stderr, "ozaki schedule: %d items on %d CTAs (%d waves of %zu shared parts; %zu solo parts; %zu remainder parts), %d split slots\n",
-            out->n_items, grid, waves, shared.size(), solo.size(), rest.size(), out->n_slots);
+    fprintf(stderr, "ozaki schedule: %d items on %d CTAs (%d waves of %d CTAs over %zu shared parts, teams of %d; %zu solo parts; %zu remainder parts), %d split slots\n",
+            out->n_items, grid, waves, gw, shared.size(), tsz, solo.size(), rest.size(), out->n_slots);
   FMP_CHECK_CUDA(cudaMalloc(&out->shapes, sizeof(OzShape) * shapes.size()));
   FMP_CHECK_CUDA(cudaMemcpy(out->shapes, shapes.data(), sizeof(OzShape) * shapes.size(), cudaMemcpyHostToDevice));
   FMP_CHECK_CUDA(cudaMalloc(&out->items, sizeof(OzItem) * items.size()));

@@ -16,11 +16,13 @@ torch.cuda.synchronize()
 lib = ctypes.CDLL(str(_lib.LIB_PATH))
 buf = np.zeros((148, 8), dtype=np.int64)
 assert lib.fmp_debug_ozaki_prof(buf.ctypes.data_as(ctypes.c_void_p), 148) == 0
-tot, full, empty, tiles, ts, te = buf.T[:6]
+tot, full, empty, tiles, ts, te, first = buf.T[:7]
 t0 = ts.min()
 busy = tot - full - empty
+if os.environ.get("FMP_OZ_DUMP"):
+    print(json.dumps({"per_cta": [[int(tot[i]), int(full[i]), int(empty[i]), int(ts[i] - t0), int(te[i] - t0)] for i in range(148)]}))
 print(json.dumps({"ctas": 148, "total_max_us": round(tot.max() / 1965, 1), "total_mean_us": round(tot.mean() / 1965, 1),
-                  "wait_full_mean_us": round(full.mean() / 1965, 1), "wait_epilogue_mean_us": round(empty.mean() / 1965, 1),
+                  "wait_full_mean_us": round(full.mean() / 1965, 1), "wait_full_first_chunk_mean_us": round(first.mean() / 1965, 1), "wait_epilogue_mean_us": round(empty.mean() / 1965, 1),
                   "issue_mean_us": round(busy.mean() / 1965, 1), "tiles_mean": float(tiles.mean()),
                   "wait_full_max_us": round(full.max() / 1965, 1),
                   "cta_start_spread_us": round((ts.max() - t0) / 1e3, 1), "cta_end_min_us": round((te.min() - t0) / 1e3, 1),
