@@ -363,7 +363,9 @@ def run_ours(args):
         Eo, Ho = torch.empty_like(Eh).pin_memory(), torch.empty_like(Hh).pin_memory()
         pipe = HostStepPipeline(solver, dt)   # public API: host fields in/out, overlapped transfers
         pipe.run(Eh, Hh, Eo, Ho, steps=1)     # warm-up
-        ke = max(args.steps, 8)   # enough steps that the pipeline fill (first H2D) and drain (last D2H) amortise
+        # enough steps that the pipeline fill (the first step's H2D, ~15 ms) and drain (the last
+        # step's D2H) amortise: the steady state is one device step plus ~0.7 ms of copy interference
+        ke = max(args.steps, 16)
         torch.cuda.synchronize()
         barrier()
         a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

@@ -1962,15 +1962,19 @@ __global__ void __launch_bounds__(FACE_THREADS, NT <= 5 ? 3 : 1) k_faces(FaceArg
     }
     fence_mbar_init();
   }
-  for (int q = tid; q < 3 * N; q += FACE_THREADS) {
-    const int n = q / N, t = q - n * N;
-    sWt[q] = t < ext[n] ? __ldg(fwd_factor(A.factors, sh, c, n) + t * ext[n]) : 0.0;
-  }
-  for (int q = tid; q < 2 * W; q += FACE_THREADS) sA[q] = 0.0;   // sA, sB: zero padding
   const FaceGeo fg = face_geo(c);
   const bool zn = fg.n1 == 2, yn = fg.n1 == 1 || fg.n2 == 1, xn = fg.n2 == 0;
   double* sY = fg.n1 == 1 ? sA : sB;   // y-normal destination [z][a]
-  __syncthreads();
+  __syncthreads();   // barriers initialised: the producer streams while the consumers set up
+  if (warp != FACE_WARPS) {
+    constexpr int CT = FACE_WARPS * 32;
+    for (int q = tid; q < 3 * N; q += CT) {
+      const int n = q / N, t = q - n * N;
+      sWt[q] = t < ext[n] ? __ldg(fwd_factor(A.factors, sh, c, n) + t * ext[n]) : 0.0;
+    }
+    for (int q = tid; q < 2 * W; q += CT) sA[q] = 0.0;   // sA, sB: zero padding
+    asm volatile("bar.sync 1, %0;\n" ::"n"(CT) : "memory");
+  }
   if (warp == FACE_WARPS) {
     // ---------------- producer: one bulk copy per z-plane
     if (lane == 0)
