@@ -143,7 +143,7 @@ class ClockSampler:
 
 # ----------------------------------------------------------------------------------- ours
 INT8_PROBE_FILE = ROOT / "profiles" / "r01_umma_i8_rate.json"
-NCU_TRAFFIC_FILE = ROOT / "profiles" / "r02_v02_ncu_traffic.json"
+NCU_TRAFFIC_FILE = ROOT / "profiles" / "r02_v03_ncu_traffic.json"
 # bench stage -> ncu kernel name(s) whose DRAM bytes (one ncu --set full capture) it covers
 STAGE_KERNELS = {"plane_fwd": ["k_plane_fast<0, 5>"], "column_fwd": ["k_column_fast_db<0, 12, 5, 2>"],
                  "faces": ["k_faces<5, 2, 5>"], "slice_y": ["k_ozaki_slice_rows", "k_ozaki_exp", "k_ozaki_digits"], "gemm": ["k_ozaki"],
@@ -165,18 +165,31 @@ def int8_peak_tops() -> tuple[float, str]:
     return 4500.0, "B200 dense INT8 spec"
 
 
-def dominant_roofline(stages: dict) -> dict | None:
-    """Roofline of the dominant single kernel of the step: the Ozaki Woodbury GEMM (k_ozaki, ~17%
-    of the step, profiles/r02_v01_launches_step_summary.txt). Algorithmic work = 28 int8 slice
-    products x 2 m^2 n (unpadded) per launch; peak = the measured tcgen05 kind::i8 rate."""
-    g = stages.get("gemm", {})
-    if "int8_tops" not in g:
+def dominant_roofline(stages: dict, peaks: dict) -> dict | None:
+    """Roofline of the dominant single kernel of the step: the longest kernel of the
+    preconditioner apply (the apply is ~2/3 of the step and every one of its kernels runs 8 times
+    per step; since the Ozaki GEMM skips its all-zero C^-1 slice blocks that is the forward plane
+    pass k_plane_fast<0>, profiles/r02_v03_launches_step_summary.txt).  Algorithmic work per launch
+    as in stage_rooflines; peak = the measured DMMA / HBM / INT8 rate (MEASURED_PEAKS.json and the
+    committed probes)."""
+    cand = {k: v for k, v in stages.items() if "frac" in v}
+    if not cand:
         return None
-    return {"kernel": "k_ozaki (Z = C^-1 Y, Ozaki S=7 slices on tcgen05.mma kind::i8, TMEM accumulators)",
-            "op_type": "int8 multiply-add = 2 ops", "bound": "tensor", "achieved": g["int8_tops"],
-            "peak": g["peak_int8_tops"], "unit": "TFLOP/s", "frac": g["frac"], "traffic": g.get("traffic_bytes"),
-            "time_ms": g["ms"], "peak_source": g["peak_source"],
-            "traffic_source": f"ncu --set full, dram__bytes_read.sum + dram__bytes_write.sum ({NCU_TRAFFIC_FILE.relative_to(ROOT)})"}
+    k = max(cand, key=lambda q: cand[q]["ms"])
+    g = cand[k]
+    src = f"ncu --set full, dram__bytes_read.sum + dram__bytes_write.sum ({NCU_TRAFFIC_FILE.relative_to(ROOT)})"
+    out = {"kernel": f"{STAGE_KERNELS.get(k, [k])[0]} ({k})", "time_ms": g["ms"], "traffic": g.get("traffic_bytes"),
+           "traffic_source": src}
+    if "achieved_tflops" in g:
+        out.update(op_type="FP64 multiply-add = 2 flops", bound="tensor", achieved=g["achieved_tflops"],
+                   peak=peaks["fp64_tflops"], unit="TFLOP/s", frac=g["frac"], peak_source=peaks["fp64_source"])
+    elif "achieved_gbs" in g:
+        out.update(bound="hbm", achieved=g["achieved_gbs"], peak=peaks["hbm_gbs"], unit="GB/s", frac=g["frac"],
+                   peak_source=peaks["hbm_source"])
+    else:
+        out.update(op_type="int8 multiply-add = 2 ops", bound="tensor", achieved=g["int8_tops"],
+                   peak=g["peak_int8_tops"], unit="TFLOP/s", frac=g["frac"], peak_source=g["peak_source"])
+    return out
 
 
 def stage_rooflines(prec, x, z, specs, peaks, reps):
@@ -223,11 +236,16 @@ def stage_rooflines(prec, x, z, specs, peaks, reps):
             a = faces_b / ms / 1e6
             e.update(bound="hbm", achieved_gbs=round(a, 1), frac=round(a / hbm, 3))
         elif k == "gemm" and ms > 0:
+            # executed work: the MMAs of the non-zero C^-1 slice blocks (fmp_precond_ozaki_stats);
+            # the dense-equivalent rate (every slice product) is reported beside it
             a = gemm_f / ms / 1e9
+            kept = plan.ozaki_stats() if plan.gemm_kind() == "ozaki" else {"kept_slices": 1.0, "kept_mma": 1.0}
             pk, src = int8_peak_tops()
-            e.update(bound="tensor (INT8 tcgen05, Ozaki S=7: 28 int8 products per FP64 product)",
-                     fp64_equiv_tflops=round(a, 2), int8_tops=round(28 * a, 1),
-                     frac=round(28 * a / pk, 3), peak_int8_tops=round(pk, 1), peak_source=src)
+            ex = 28 * a * kept["kept_mma"]
+            e.update(bound="tensor (INT8 tcgen05, Ozaki S=7: 28 int8 products per FP64 product, all-zero slice blocks skipped)",
+                     fp64_equiv_tflops=round(a, 2), int8_tops=round(ex, 1), dense_equiv_int8_tops=round(28 * a, 1),
+                     kept_slices=round(kept["kept_slices"], 4), kept_mma=round(kept["kept_mma"], 4),
+                     frac=round(ex / pk, 3), peak_int8_tops=round(pk, 1), peak_source=src)
         out[k] = e
     return out
 
@@ -414,7 +432,7 @@ def run_ours(args):
                  "algorithmic_bytes": spmv_bytes,
                  "traffic_bytes": ncu_traffic().get("k_spmv_bulk<0, 4>", {}).get("traffic_bytes"),
                  "frac_hbm": round(spmv_bytes / t_spmv / 1e9 / peaks["hbm_gbs"], 3)},
-        "roofline": dominant_roofline(stages),
+        "roofline": dominant_roofline(stages, peaks),
         "roofline_apply": {"kernel": "RAS precond apply (fused FlashMP sequence: FP64 DMMA transforms + Ozaki INT8 tcgen05 Woodbury GEMM)",
                      "note": "composite: executed FP64-equivalent flops of all 8 kernels over the FP64 DMMA peak; "
                              "the Woodbury GEMM's share runs on the INT8 pipe, so this can exceed an FP64-only bound",

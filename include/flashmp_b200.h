@@ -252,6 +252,14 @@ int fmp_precond_stage_ms(fmp_precond* p, float* ms, int n);
 #define FMP_PATH_LARGE 2
 int fmp_precond_path(const fmp_precond* p);
 
+/* Zero-slice skipping of the plan's Ozaki GEMM: out[0] = fraction of the C^-1 INT8 slice blocks
+ * streamed, out[1] = fraction of the dense MMA work (28 slice products per chunk) issued.  The
+ * all-zero slice blocks (leading digits of entries far from the diagonal, whole zero K chunks)
+ * are skipped, which changes no bit of the result (diagnostics and tests; no reference
+ * counterpart).  1.0 for the cuBLAS / own GEMMs or with FMP_OZ_DENSE=1.  Returns the number of
+ * values written (<= n). */
+int fmp_precond_ozaki_stats(const fmp_precond* p, double* out, int n);
+
 /* Diagnostics: with FMP_OZ_PROF=1 in the environment, the last Ozaki GEMM launch's per-CTA
  * MMA-issuer cycles {total, waiting for operand stages, waiting for the epilogue, tiles} for the
  * first n CTAs (tools/oz_prof.py).  Returns -1 when profiling is off. */

@@ -41,6 +41,7 @@ SIGNATURES = {
     "fmp_precond_profile": (_i, [_p, _i]),
     "fmp_precond_stage_ms": (_i, [_p, C.POINTER(C.c_float), _i]),
     "fmp_precond_path": (_i, [_p]),
+    "fmp_precond_ozaki_stats": (_i, [_p, _p, _i]),
     "fmp_debug_ozaki_prof": (_i, [_p, _i]),
     "fmp_stencil_apply_part": (_i, [_p, _d, _i, _i, _i, _p, _p, _p, _p, _p, _p]),
     "fmp_precond_apply_part": (_i, [_p, _p, _i, _i, _p, _p, _p]),

@@ -84,11 +84,12 @@ __device__ __forceinline__ void umma_i8(uint32_t tmem, uint64_t da, uint64_t db,
 // zero rows past the last one) and lands in columns >= 7 W, which no level uses.  W is a template
 // constant so every descriptor and TMEM offset folds to an immediate.
 template <int W, bool REV>
-__device__ __forceinline__ void issue_chunk_order(uint64_t da0, uint64_t db0, uint32_t tmem, bool first) {
+__device__ __forceinline__ void issue_chunk_order(uint64_t da0, uint64_t db0, uint32_t tmem, bool first, int p0) {
   constexpr uint32_t IDESC0 = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(OZ_M >> 4) << 24);
 #pragma unroll
   for (int pi = 1; pi <= OZ_S; ++pi) {
     const int p = REV ? OZ_S + 1 - pi : pi;
+    if (p <= p0) continue;   // leading all-zero slices of this chunk: their products are zero
     const uint64_t da = da0 + (uint64_t)(((p - 1) * OZ_ABLK) >> 4);
     const uint32_t acc = (first && p == 1) ? 0u : 1u;
     const int N = oz_pad16((OZ_S + 1 - p) * W);
@@ -109,11 +110,11 @@ __device__ __forceinline__ void issue_chunk_order(uint64_t da0, uint64_t db0, ui
 // others run p = S .. 1, so the chunk ends on its widest MMAs and the tensor pipe still holds
 // ~256 cycles of work while the issuing warp commits, waits for the next stage and sets up.
 template <int W>
-__device__ __forceinline__ void issue_chunk(uint64_t da0, uint64_t db0, uint32_t tmem, bool first, bool rev) {
+__device__ __forceinline__ void issue_chunk(uint64_t da0, uint64_t db0, uint32_t tmem, bool first, bool rev, int p0) {
   if (first || !rev)
-    issue_chunk_order<W, false>(da0, db0, tmem, first);
+    issue_chunk_order<W, false>(da0, db0, tmem, first, first ? 0 : p0);
   else
-    issue_chunk_order<W, true>(da0, db0, tmem, false);
+    issue_chunk_order<W, true>(da0, db0, tmem, false, p0);
 }
 
 __device__ __forceinline__ void tmem_ld8(uint32_t addr, uint32_t (&v)[8]) {
@@ -132,6 +133,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
   __shared__ uint32_t tmem_base;
   __shared__ int last_flag;
   __shared__ int eb_sh[OZ_WMAX];   // column exponents (+4) of the epilogue's current item
+  __shared__ int stage_p0[OZ_STAGES];   // leading zero slices of the chunk in each stage (producer -> MMA warp)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(s_u32(&tmem_base)),
@@ -162,17 +164,26 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
         const int8_t* a = sh.A + (size_t)tl.mt * sh.kchunks * OZ_S * OZ_ABLK;
         const uint32_t bblk = (uint32_t)sh.R * OZ_KC;
         const int8_t* b = sh.B + (size_t)tl.nt * sh.kchunks * bblk;
-        for (int kc = tl.k0; kc < tl.k1; ++kc, ++it) {
+        const int base = sh.koff[tl.mt];
+        int kc_n = sh.klist[base + tl.k0], p0_n = sh.kp0[base + tl.k0];   // entry j, fetched one ahead
+        for (int j = tl.k0; j < tl.k1; ++j, ++it) {
+          const int kc = kc_n, p0 = j == tl.k0 ? 0 : p0_n;   // an item's first chunk zeroes every level: all slices
+          if (j + 1 < tl.k1) {
+            kc_n = sh.klist[base + j + 1];
+            p0_n = sh.kp0[base + j + 1];
+          }
           const int s = it % OZ_STAGES;
           const uint32_t ph = (it / OZ_STAGES) & 1;
           mbar_wait(&empty_bar[s], ph ^ 1);
+          stage_p0[s] = p0;   // published to the MMA warp by the full barrier's arrive
           if (dbg & 1) {   // FMP_OZ_DBG=1 (timing diagnostics only, wrong results): no operand loads
             mbar_arrive(&full_bar[s]);
             continue;
           }
           uint8_t* st = osm + s * OZ_STAGE;
-          mbar_expect_tx(&full_bar[s], OZ_S * OZ_ABLK + bblk);
-          bulk_g2s(st, a + (size_t)kc * OZ_S * OZ_ABLK, OZ_S * OZ_ABLK, &full_bar[s]);
+          const uint32_t abytes = (uint32_t)(OZ_S - p0) * OZ_ABLK;   // slices p0 .. S-1 land at their usual offsets
+          mbar_expect_tx(&full_bar[s], abytes + bblk);
+          bulk_g2s(st + p0 * OZ_ABLK, a + ((size_t)kc * OZ_S + p0) * OZ_ABLK, abytes, &full_bar[s]);
           bulk_g2s(st + OZ_S * OZ_ABLK, b + (size_t)kc * bblk, bblk, &full_bar[s]);
         }
       }
@@ -192,7 +203,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
         if (prof) w_empty += clock64() - t1;
         asm volatile("tcgen05.fence::after_thread_sync;\n");
       }
-      for (int kc = tl.k0; kc < tl.k1; ++kc, ++it) {
+      for (int j = tl.k0; j < tl.k1; ++j, ++it) {
         const int s = it % OZ_STAGES;
         const uint32_t ph = (it / OZ_STAGES) & 1;
         if (prof) t1 = clock64();
@@ -200,27 +211,28 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
         if (prof) {
           const long long dt = clock64() - t1;
           w_full += dt;
-          if (kc == tl.k0) w_first += dt;
+          if (j == tl.k0) w_first += dt;
         }
         asm volatile("tcgen05.fence::after_thread_sync;\n");
         {
+          const int p0 = *reinterpret_cast<volatile int*>(&stage_p0[s]);
           const uint32_t sa = s_u32(osm + s * OZ_STAGE);
           const uint64_t da0 = umma_desc(sa, OZ_M * 16, 128);
           const uint64_t db0 = umma_desc(sa + OZ_S * OZ_ABLK, lbo_b, 128);
-          const bool first = kc == tl.k0;
+          const bool first = j == tl.k0;
           if (!(dbg & 2)) switch (w) {   // FMP_OZ_DBG=2: no MMAs
-            case 8: issue_chunk<8>(da0, db0, tmem, first, rev); break;
-            case 16: issue_chunk<16>(da0, db0, tmem, first, rev); break;
-            case 24: issue_chunk<24>(da0, db0, tmem, first, rev); break;
-            case 32: issue_chunk<32>(da0, db0, tmem, first, rev); break;
-            case 40: issue_chunk<40>(da0, db0, tmem, first, rev); break;
-            case 48: issue_chunk<48>(da0, db0, tmem, first, rev); break;
-            case 56: issue_chunk<56>(da0, db0, tmem, first, rev); break;
-            case 64: issue_chunk<64>(da0, db0, tmem, first, rev); break;
-            default: issue_chunk<72>(da0, db0, tmem, first, rev); break;
+            case 8: issue_chunk<8>(da0, db0, tmem, first, rev, p0); break;
+            case 16: issue_chunk<16>(da0, db0, tmem, first, rev, p0); break;
+            case 24: issue_chunk<24>(da0, db0, tmem, first, rev, p0); break;
+            case 32: issue_chunk<32>(da0, db0, tmem, first, rev, p0); break;
+            case 40: issue_chunk<40>(da0, db0, tmem, first, rev, p0); break;
+            case 48: issue_chunk<48>(da0, db0, tmem, first, rev, p0); break;
+            case 56: issue_chunk<56>(da0, db0, tmem, first, rev, p0); break;
+            case 64: issue_chunk<64>(da0, db0, tmem, first, rev, p0); break;
+            default: issue_chunk<72>(da0, db0, tmem, first, rev, p0); break;
           }
           umma_commit(&empty_bar[s]);                 // stage free once these MMAs retire
-          if (kc == tl.k1 - 1) umma_commit(&tfull_bar);  // accumulators complete
+          if (j == tl.k1 - 1) umma_commit(&tfull_bar);   // accumulators complete
         }
         __syncwarp();
       }
@@ -452,15 +464,114 @@ int ozaki_launch(const OzPlan& p, cudaStream_t st) {
   return 0;
 }
 
+// ---------------------------------------------------------------- zero-slice skipping
+// C^-1 decays fast away from the diagonal (the capacitance couples nearby face points; at
+// 34^3-class boxes the median 128 x 128 block of the row-scaled C^-1 is ~1e-11 of its rows'
+// maxima), so most 128 x 32 B slice blocks of the leading (most significant) slices -- and
+// whole chunks -- are all zero digits.  Their products are exactly zero: skipping them changes
+// no bit of the result.  One warp per (row tile, K chunk) finds the leading all-zero slice
+// count (S when the whole chunk is zero).
+__global__ void k_ozaki_p0(const int8_t* __restrict__ A, int nchunks, uint8_t* __restrict__ p0) {
+  const int c = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (c >= nchunks) return;
+  const uint4* blk = reinterpret_cast<const uint4*>(A + (size_t)c * OZ_S * OZ_ABLK);
+  int lead = OZ_S;
+  for (int p = 0; p < OZ_S; ++p) {
+    uint32_t any = 0;
+    for (int q = lane; q < OZ_ABLK / 16; q += 32) {
+      const uint4 v = __ldg(blk + p * (OZ_ABLK / 16) + q);
+      any |= v.x | v.y | v.z | v.w;
+    }
+    if (__any_sync(0xffffffffu, any != 0)) {
+      lead = p;
+      break;
+    }
+  }
+  if (lane == 0) p0[c] = (uint8_t)lead;
+}
+
+int ozaki_chunk_lists(std::vector<OzShape>& shapes, std::vector<OzLists>* lists, OzPlan* plan) {
+  const bool dense = getenv_flag("FMP_OZ_DENSE");
+  lists->assign(shapes.size(), OzLists{});
+  std::vector<uint16_t> kl;
+  std::vector<uint8_t> kp;
+  std::vector<int> ko;
+  std::vector<size_t> kl0(shapes.size(), 0), ko0(shapes.size(), 0);
+  size_t kept = 0, total = 0;
+  double mma_kept = 0.0, mma_total = 0.0;   // in units of one slice product of one chunk
+  for (size_t s = 0; s < shapes.size(); ++s) {
+    const OzShape& sh = shapes[s];
+    if (!sh.A) continue;
+    const int mtiles = (sh.m + OZ_M - 1) / OZ_M, nch = mtiles * sh.kchunks;
+    FMP_REQUIRE(sh.kchunks <= 65535, "Ozaki: %d K chunks exceed the 16-bit chunk list", sh.kchunks);
+    std::vector<uint8_t> h(nch, 0);
+    if (!dense) {
+      uint8_t* d = nullptr;
+      FMP_CHECK_CUDA(cudaMalloc(&d, nch));
+      k_ozaki_p0<<<(nch + 7) / 8, 256>>>(sh.A, nch, d);
+      FMP_CHECK_LAUNCH();
+      const cudaError_t e = cudaMemcpy(h.data(), d, nch, cudaMemcpyDeviceToHost);
+      cudaFree(d);
+      FMP_CHECK_CUDA(e);
+    }
+    OzLists& L = (*lists)[s];
+    L.koff.push_back(0);
+    for (int mt = 0; mt < mtiles; ++mt) {
+      const size_t before = L.klist.size();
+      for (int kc = 0; kc < sh.kchunks; ++kc) {
+        const uint8_t lead = h[(size_t)mt * sh.kchunks + kc];
+        if (lead < OZ_S) {
+          L.klist.push_back((uint16_t)kc);
+          L.kp0.push_back(lead);
+          kept += OZ_S - lead;
+          for (int p = lead + 1; p <= OZ_S; ++p) mma_kept += OZ_S + 1 - p;
+        }
+      }
+      mma_total += (double)sh.kchunks * OZ_S * (OZ_S + 1) / 2;
+      if (L.klist.size() == before) {   // an all-zero row tile still runs one chunk (it writes Z = 0)
+        L.klist.push_back(0);
+        L.kp0.push_back(0);
+        kept += OZ_S;
+      }
+      L.koff.push_back((int)L.klist.size());
+      total += (size_t)OZ_S * sh.kchunks;
+    }
+    kl0[s] = kl.size();
+    ko0[s] = ko.size();
+    kl.insert(kl.end(), L.klist.begin(), L.klist.end());
+    kp.insert(kp.end(), L.kp0.begin(), L.kp0.end());
+    ko.insert(ko.end(), L.koff.begin(), L.koff.end());
+  }
+  plan->kept_slices = total ? (double)kept / (double)total : 1.0;
+  plan->kept_mma = mma_total > 0.0 ? mma_kept / mma_total : 1.0;
+  if (kl.empty()) return 0;
+  FMP_CHECK_CUDA(cudaMalloc(&plan->klist, kl.size() * sizeof(uint16_t)));
+  FMP_CHECK_CUDA(cudaMalloc(&plan->kp0, kp.size()));
+  FMP_CHECK_CUDA(cudaMalloc(&plan->koff, ko.size() * sizeof(int)));
+  FMP_CHECK_CUDA(cudaMemcpy(plan->klist, kl.data(), kl.size() * sizeof(uint16_t), cudaMemcpyHostToDevice));
+  FMP_CHECK_CUDA(cudaMemcpy(plan->kp0, kp.data(), kp.size(), cudaMemcpyHostToDevice));
+  FMP_CHECK_CUDA(cudaMemcpy(plan->koff, ko.data(), ko.size() * sizeof(int), cudaMemcpyHostToDevice));
+  for (size_t s = 0; s < shapes.size(); ++s) {
+    if (!shapes[s].A) continue;
+    shapes[s].klist = plan->klist + kl0[s];
+    shapes[s].kp0 = plan->kp0 + kl0[s];
+    shapes[s].koff = plan->koff + ko0[s];
+  }
+  if (getenv_flag("FMP_OZ_VERBOSE"))
+    fprintf(stderr, "ozaki chunk lists: %.3f of the C^-1 slice blocks, %.3f of the MMA work kept%s\n", plan->kept_slices,
+            plan->kept_mma, dense ? " (dense)" : "");
+  return 0;
+}
+
 // Cost model of one K chunk (cycles), fitted to the per-CTA MMA-warp cycles of a cfg4 apply
 // (tools/oz_prof.py with FMP_OZ_DUMP=1: ~1154 per 72-column chunk, ~602 per 8-column chunk, ~16.6K
 // per item): each MMA costs max(N/2, 80) on the tensor pipe (N/2 for N >= 160, tools/umma_seq.cu),
 // with the same N splits as issue_chunk, plus ~60 cycles of per-chunk issue overhead (stage
 // wait, commit); every work item adds OZ_ITEM_CYCLES (accumulator drain, pipeline restart).
 constexpr double OZ_ITEM_CYCLES = 16000.0;
-static double chunk_cycles(int w) {
+static double chunk_cycles(int w, int p0 = 0) {
   double tensor = 60.0;
-  for (int p = 1; p <= OZ_S; ++p) {
+  for (int p = p0 + 1; p <= OZ_S; ++p) {
     const int N = oz_pad16((OZ_S + 1 - p) * w);
     const int parts = (N + 255) / 256, step = oz_pad16((N + parts - 1) / parts);
     for (int r0 = 0; r0 < N; r0 += step) tensor += std::max(80.0, std::min(step, N - r0) / 2.0);
@@ -483,34 +594,47 @@ static double chunk_cycles(int w) {
 //    HBM-heavy pieces are spread over the launch instead of all landing at its end;
 //  * a tile cut into several segments is completed by the last segment to finish (partials summed
 //    in segment order: deterministic).
-int ozaki_build(const std::vector<OzShape>& shapes, int sms, OzPlan* out) {
-  *out = OzPlan{};
-  struct Part { int shape, mt, nt, k0, k1, tile; double cc; };
+int ozaki_build(const std::vector<OzShape>& shapes, const std::vector<OzLists>& klists, int sms, OzPlan* out) {
+  // a part = list entries [k0, k1) of row tile mt, column tile nt
+  struct Part { int shape, mt, nt, k0, k1, tile; };
   std::vector<Part> shared, solo;
-  const char* sv = getenv("FMP_OZ_SOLO");   // modelled floor (cycles per chunk) of a solo chunk
-  const double solo_min = sv ? atof(sv) : 0.0;
+  // per shape: modelled cycles of a chunk with p0 leading zero slices, and prefix sums of the
+  // entry costs over the shape's concatenated lists
+  std::vector<std::vector<double>> cyc(shapes.size()), pref(shapes.size());
   int n_tiles = 0;
   for (size_t s = 0; s < shapes.size(); ++s) {
     const OzShape& sh = shapes[s];
     if (sh.n <= 0 || !sh.A) continue;
+    const OzLists& L = klists[s];
+    for (int q = 0; q <= OZ_S; ++q) cyc[s].push_back(chunk_cycles(sh.w, std::min(q, OZ_S)));
+    pref[s].assign(L.klist.size() + 1, 0.0);
+    for (size_t e = 0; e < L.klist.size(); ++e) pref[s][e + 1] = pref[s][e] + cyc[s][L.kp0[e]];
     const int nts = (sh.n + sh.w - 1) / sh.w;
-    const double cc = nts > 1 ? chunk_cycles(sh.w) : std::max(solo_min, chunk_cycles(sh.w));
-    const int kparts = (sh.kchunks + OZ_PART - 1) / OZ_PART;
     for (int mt = 0; mt * OZ_M < sh.m; ++mt) {
+      const int ne = L.koff[mt + 1] - L.koff[mt];
+      const int kparts = (ne + OZ_PART - 1) / OZ_PART;   // <= 16384 K terms per accumulation
       for (int kp = 0; kp < kparts; ++kp) {
-        const int k0 = (int)((int64_t)sh.kchunks * kp / kparts), k1 = (int)((int64_t)sh.kchunks * (kp + 1) / kparts);
+        const int k0 = (int)((int64_t)ne * kp / kparts), k1 = (int)((int64_t)ne * (kp + 1) / kparts);
         for (int nt = 0; nt < nts; ++nt)
-          (nts > 1 ? shared : solo).push_back(Part{(int)s, mt, nt, k0, k1, n_tiles + nt, cc});
+          (nts > 1 ? shared : solo).push_back(Part{(int)s, mt, nt, k0, k1, n_tiles + nt});
       }
       n_tiles += nts;
     }
   }
   if (shared.empty() && solo.empty()) return 0;
+  // modelled cycles of entries [k0, k1) of part r run as one item (its first chunk runs every slice)
+  auto cost = [&](const Part& r, int k0, int k1) -> double {
+    if (k1 <= k0) return 0.0;
+    const std::vector<double>& P = pref[r.shape];
+    const int base = klists[r.shape].koff[r.mt];
+    return P[base + k1] - P[base + k0] + cyc[r.shape][0] - cyc[r.shape][klists[r.shape].kp0[base + k0]];
+  };
   const int grid = std::min<int>(sms, (int)(shared.size() + solo.size()));
   // sibling teams: when every shared shape has the same number k of column tiles, the waves use
   // gw = grid - grid % k CTAs, so CTAs k t .. k t + k - 1 hold the k column tiles of one row tile
-  // in EVERY wave and share one remainder position (they stream the same C^-1 chunks together);
-  // the grid % k CTAs left out of the waves take a larger remainder piece instead
+  // in EVERY wave and share one remainder position (they stream the same C^-1 chunks together;
+  // siblings have the same chunk list, so the same cost); the grid % k CTAs left out of the waves
+  // take a larger remainder piece instead
   int team = 0;
   for (const Part& r : shared) {
     const int nts = (shapes[r.shape].n + shapes[r.shape].w - 1) / shapes[r.shape].w;
@@ -523,43 +647,48 @@ int ozaki_build(const std::vector<OzShape>& shapes, int sms, OzPlan* out) {
   if (fv) waves = std::min(waves, atoi(fv));
   std::vector<Part> rest(shared.begin() + (size_t)waves * gw, shared.end());
   rest.insert(rest.end(), solo.begin(), solo.end());
-  double total = 0.0, rest_total = 0.0;
-  for (const Part& r : rest) rest_total += r.cc * (r.k1 - r.k0) + OZ_ITEM_CYCLES;
-  rest_total += OZ_ITEM_CYCLES * grid;   // about one extra item per piece boundary
+  double total = 0.0;
+  for (const Part& r : rest) total += cost(r, r.k0, r.k1) + OZ_ITEM_CYCLES;
   std::vector<double> wave_cost(grid, 0.0);
   for (int j = 0; j < waves; ++j)
     for (int b = 0; b < gw; ++b) {
       const Part& q = shared[(size_t)j * gw + b];
-      wave_cost[b] += q.cc * (q.k1 - q.k0) + OZ_ITEM_CYCLES;
+      wave_cost[b] += cost(q, q.k0, q.k1) + OZ_ITEM_CYCLES;
     }
   for (int b = 0; b < grid; ++b) total += wave_cost[b];
-  total += rest_total;
-  // piece b gets (total / grid - wave_cost[b]); cumulative targets for the cut below
-  // Cut the remainder into `grid` contiguous pieces (K-chunk granularity) so that every CTA's
+  // Cut the remainder into `grid` contiguous pieces (list-entry granularity) so that every CTA's
   // modelled load -- its wave items plus its piece, each item charged OZ_ITEM_CYCLES -- comes out
   // at the same level T: greedy fill for a given T, T found by bisection so that the remainder
   // is exactly used up.
-  auto cut = [&](double T, std::vector<std::vector<Part>>* out) -> double {   // returns the last CTA's load
-    if (out) out->assign(grid, {});
+  auto cut = [&](double T, std::vector<std::vector<Part>>* outp) -> double {   // the last CTA's load
+    if (outp) outp->assign(grid, {});
     int b = 0;
     double load = wave_cost[0];
     for (const Part& r : rest) {
       int k = r.k0;
       while (k < r.k1) {
-        int take = r.k1 - k;
-        if (b < grid - 1 && load + OZ_ITEM_CYCLES + take * r.cc > T) {
-          take = (int)std::floor((T - load - OZ_ITEM_CYCLES) / r.cc + 0.5);
-          take = std::max(0, std::min(take, r.k1 - k));
+        int e = k;
+        if (b == grid - 1) {
+          e = r.k1;
+        } else {
+          while (e < r.k1) {
+            const double cn = cost(r, k, e + 1), cp = cost(r, k, e);
+            if (load + OZ_ITEM_CYCLES + cn > T) {
+              if (T - (load + OZ_ITEM_CYCLES + cp) >= 0.5 * (cn - cp)) ++e;   // more than half of it fits
+              break;
+            }
+            ++e;
+          }
         }
-        if (take > 0) {
-          if (out) {
+        if (e > k) {
+          if (outp) {
             Part seg = r;
             seg.k0 = k;
-            seg.k1 = k + take;
-            (*out)[b].push_back(seg);
+            seg.k1 = e;
+            (*outp)[b].push_back(seg);
           }
-          load += take * r.cc + OZ_ITEM_CYCLES;
-          k += take;
+          load += cost(r, k, e) + OZ_ITEM_CYCLES;
+          k = e;
         }
         if (k < r.k1 && b < grid - 1) load = wave_cost[++b];
       }
@@ -574,6 +703,13 @@ int ozaki_build(const std::vector<OzShape>& shapes, int sms, OzPlan* out) {
   std::vector<std::vector<Part>> piece;
   cut(hi, &piece);
   std::vector<std::vector<Part>> lists(grid);
+  if (getenv_flag("FMP_OZ_NOSPLIT")) {   // tests: whole tiles round-robin, no K segments (schedule-independent sums)
+    std::vector<Part> all(shared);
+    all.insert(all.end(), solo.begin(), solo.end());
+    for (auto& pc : piece) pc.clear();
+    for (size_t i = 0; i < all.size(); ++i) piece[i % grid].push_back(all[i]);
+    waves = 0;
+  }
   for (int b = 0; b < grid; ++b) {
     const int pos = (b / tsz) % (waves + 1);
     for (int j = 0; j <= waves; ++j) {
@@ -581,19 +717,20 @@ int ozaki_build(const std::vector<OzShape>& shapes, int sms, OzPlan* out) {
       if (j < waves && b < gw) lists[b].push_back(shared[(size_t)j * gw + b]);
     }
   }
-  if (getenv_flag("FMP_OZ_DUMP")) {   // per CTA: items, modelled cost, chunks by kind (tools/oz_prof.py)
+  if (getenv_flag("FMP_OZ_DUMP")) {   // per CTA: items, modelled cost, list entries by kind (tools/oz_prof.py)
     for (int b = 0; b < grid; ++b) {
-      double cost = 0.0;
+      double c = 0.0;
       long sh_ch = 0, solo_wide = 0, solo_narrow = 0, segs = 0;
       for (const Part& q : lists[b]) {
         const int nts = (shapes[q.shape].n + shapes[q.shape].w - 1) / shapes[q.shape].w;
-        cost += q.cc * (q.k1 - q.k0);
-        segs += (q.k1 - q.k0) < shapes[q.shape].kchunks;
+        c += cost(q, q.k0, q.k1);
+        const int ne = klists[q.shape].koff[q.mt + 1] - klists[q.shape].koff[q.mt];
+        segs += (q.k1 - q.k0) < ne;
         if (nts > 1) sh_ch += q.k1 - q.k0;
         else if (shapes[q.shape].w >= 32) solo_wide += q.k1 - q.k0;
         else solo_narrow += q.k1 - q.k0;
       }
-      fprintf(stderr, "ozdump %d %zu %.0f %ld %ld %ld %ld\n", b, lists[b].size(), cost, sh_ch, solo_wide, solo_narrow, segs);
+      fprintf(stderr, "ozdump %d %zu %.0f %ld %ld %ld %ld\n", b, lists[b].size(), c, sh_ch, solo_wide, solo_narrow, segs);
     }
   }
   // segments per tile (in K order), partial slots for the split tiles
@@ -640,6 +777,9 @@ int ozaki_build(const std::vector<OzShape>& shapes, int sms, OzPlan* out) {
 }
 
 void ozaki_free(OzPlan* p) {
+  cudaFree(p->klist);
+  cudaFree(p->kp0);
+  cudaFree(p->koff);
   cudaFree(p->shapes);
   cudaFree(p->items);
   cudaFree(p->offs);

@@ -13,11 +13,24 @@ struct OzShape {
   const int* eB;     // [n] row exponents of Y^T
   double* Z;         // [n][ld]
   int m, n, ld, kchunks, w, R;   // w: column-tile width (multiple of 8, <= 72); R = pad16(S w) stacked B rows
+  // Zero-slice skipping: the K chunks of row tile mt whose C^-1 slices are not all zero are
+  // klist[koff[mt] .. koff[mt+1]) (ascending), kp0 the number of leading all-zero slices of each
+  // (those slices and their MMAs are skipped: their digits contribute exactly zero).
+  const uint16_t* klist;
+  const uint8_t* kp0;
+  const int* koff;
 };
-// One work item: K chunks [k0, k1) of column tile nt of row tile mt.  A tile whose K range is
-// split into nseg > 1 segments (load balance, or K > 16384 int32 headroom) writes per-segment FP64
-// partials to partial slots slot0 + seg; the last segment to finish sums them in segment order
-// (deterministic) into Z.  nseg == 1: the item writes Z directly.
+// Host copy of one shape's chunk lists (ozaki_chunk_lists -> ozaki_build).
+struct OzLists {
+  std::vector<uint16_t> klist;
+  std::vector<uint8_t> kp0;
+  std::vector<int> koff;
+};
+// One work item: list entries [k0, k1) of row tile mt (K chunks klist[koff[mt] + j]), column
+// tile nt.  A tile whose list is split into nseg > 1 segments (load balance, or more than 16384
+// K terms: int32 headroom) writes per-segment FP64 partials to partial slots slot0 + seg; the last
+// segment to finish sums them in segment order (deterministic) into Z.  nseg == 1: the item
+// writes Z directly.
 struct OzItem {
   int shape, mt, nt, k0, k1, seg, nseg, slot0;
 };
@@ -28,7 +41,12 @@ struct OzPlan {
   int* offs = nullptr;        // CTA b runs items [offs[b], offs[b+1])
   double* zpart = nullptr;    // [slots][OZ_WMAX][128] partial results of split tiles
   int* counters = nullptr;    // [slots] arrivals per split tile (slot0), zero at rest
+  uint16_t* klist = nullptr;  // chunk lists of all shapes (OzShape::klist / kp0 / koff point in)
+  uint8_t* kp0 = nullptr;
+  int* koff = nullptr;
   int grid = 0, n_items = 0, n_slots = 0;
+  double kept_slices = 1.0;   // fraction of C^-1 slice blocks streamed (diagnostics)
+  double kept_mma = 1.0;      // fraction of the dense MMA work (28 slice products) issued
 };
 // One operand to slice: rows x kvalid doubles (row stride ld) -> tiles of height T.
 struct OzSlice {
@@ -51,9 +69,14 @@ size_t ozaki_b_bytes(int n, int kchunks);
 // Fill row0/q0/prow0 of a batch; returns the total rows and padded rows (the slicing grid).
 void ozaki_plan_slices(OzSlice* s, int count, int64_t* rows, int64_t* padded_rows);
 int ozaki_slice(const OzSlice* d_slices, int count, int64_t rows, int64_t padded_rows, cudaStream_t st);
-// Work items (column tiles x K segments) for the shapes (entries with n == 0 are skipped), balanced
-// over `sms` persistent CTAs, uploaded with the partial-slot workspace.  Returns 0 or -1.
-int ozaki_build(const std::vector<OzShape>& shapes, int sms, OzPlan* out);
+// After the C^-1 slices exist: per row tile, the K chunks with a non-zero slice and their
+// leading all-zero slice counts (FMP_OZ_DENSE=1: every chunk, no skipping); uploads the lists
+// into `plan` and points the shapes at them.  Returns 0 or -1.
+int ozaki_chunk_lists(std::vector<OzShape>& shapes, std::vector<OzLists>* lists, OzPlan* plan);
+// Work items (column tiles x list segments) for the shapes (entries with n == 0 are skipped),
+// balanced over `sms` persistent CTAs, uploaded with the partial-slot workspace.  `plan` already
+// holds the chunk lists (ozaki_chunk_lists).  Returns 0 or -1.
+int ozaki_build(const std::vector<OzShape>& shapes, const std::vector<OzLists>& lists, int sms, OzPlan* plan);
 void ozaki_free(OzPlan* p);
 int ozaki_launch(const OzPlan& p, cudaStream_t st);
 

@@ -2539,7 +2539,7 @@ extern "C" int fmp_precond_create(const fmp_precond_desc* desc, fmp_precond** ou
     ozaki_plan_slices(sa.data(), (int)sa.size(), &ra, &qa);
     ozaki_plan_slices(sb.data(), (int)sb.size(), &p->oz_rows, &p->oz_threads);
     OzSlice* d_sa = nullptr;
-    if (upload(sa, &d_sa) || upload(sb, &p->d_ozslices) || ozaki_build(os, p->sms, &p->oz)) {
+    if (upload(sa, &d_sa) || upload(sb, &p->d_ozslices)) {
       cudaFree(d_sa);
       free_plan(p);
       return -1;
@@ -2550,6 +2550,12 @@ extern "C" int fmp_precond_create(const fmp_precond_desc* desc, fmp_precond** ou
     cudaFree(d_sa);
     if (rc) { free_plan(p); return -1; }
     FMP_CHECK_CUDA(cudaDeviceSynchronize());
+    // chunk lists of the non-zero C^-1 slice blocks (zero-slice skipping), then the schedule
+    std::vector<OzLists> lists;
+    if (ozaki_chunk_lists(os, &lists, &p->oz) || ozaki_build(os, lists, p->sms, &p->oz)) {
+      free_plan(p);
+      return -1;
+    }
   }
   if (cublasCreate(&p->blas) != CUBLAS_STATUS_SUCCESS) {
     free_plan(p);
@@ -2618,6 +2624,13 @@ extern "C" int fmp_precond_create(const fmp_precond_desc* desc, fmp_precond** ou
 extern "C" int fmp_precond_path(const fmp_precond* p) {
   FMP_REQUIRE(p, "null plan");
   return p->fast ? FMP_PATH_FAST : (p->large ? FMP_PATH_LARGE : FMP_PATH_GENERAL);
+}
+
+extern "C" int fmp_precond_ozaki_stats(const fmp_precond* p, double* out, int n) {
+  FMP_REQUIRE(p && out, "null argument");
+  const double v[2] = {p->use_ozaki ? p->oz.kept_slices : 1.0, p->use_ozaki ? p->oz.kept_mma : 1.0};
+  for (int i = 0; i < n && i < 2; ++i) out[i] = v[i];
+  return n < 2 ? n : 2;
 }
 
 extern "C" int fmp_precond_destroy(fmp_precond* p) {

@@ -282,6 +282,17 @@ class SolvePlan:
         """Transform kernel family of this plan: 'fast', 'large' or 'general' (fmp_precond_path)."""
         return {0: "general", 1: "fast", 2: "large"}[_lib.lib().fmp_precond_path(self._handle)]
 
+    def ozaki_stats(self) -> dict:
+        """Zero-slice skipping of the Ozaki GEMM (fmp_precond_ozaki_stats): fractions of the C^-1
+        slice blocks streamed and of the dense MMA work issued."""
+        buf = (C.c_double * 2)()
+        n = _lib.lib().fmp_precond_ozaki_stats(self._handle, buf, 2)
+        _lib.check(0 if n >= 0 else n, "fmp_precond_ozaki_stats")
+        return {"kept_slices": float(buf[0]), "kept_mma": float(buf[1])}
+
+    def ozaki_kept_slices(self) -> float:
+        return self.ozaki_stats()["kept_slices"]
+
     def gemm_kind(self) -> str:
         """Woodbury GEMM this plan was created with: 'ozaki' (default), 'own' or 'cublas'."""
         return self._gemm
