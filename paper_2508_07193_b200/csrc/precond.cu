@@ -1863,16 +1863,19 @@ inline size_t face_smem_bytes(int slot) {
 // loads first, then the z-normal update, the y-normal partial and the x-normal row sums with
 // the FR shuffle reductions interleaved (independent chains, no early exit).
 template <int FR, int FA, int S>
-__device__ __forceinline__ void face_plane(const double* pl, int z, int rowstep, uint32_t vmask, bool zn, bool xn,
+__device__ __forceinline__ void face_plane(const double* pl, int z, int rowstep, bool zn, bool xn,
                                            double wz, const double* Wy, const double (&wx)[FA],
                                            double (&za)[FR][FA], double* sB, double (&yp)[FA], int ey, int warp,
                                            int lane) {
-  // pl points at this thread's first point (row warp, column lane); vmask bit r*FA+h: (b, a) inside
+  // pl points at this thread's first point (row warp, column lane).  Points outside the plane
+  // (b >= ey or a >= ex) are loaded unpredicated: they read other rows, the zeroed slot tail, the
+  // next slot or the zeroed weights / partials -- always finite -- and meet zero weights (x, y
+  // normals) or are never written out (z normal), so no per-point predicate is needed
   double val[FR][FA];
 #pragma unroll
   for (int r = 0; r < FR; ++r)
 #pragma unroll
-    for (int h = 0; h < FA; ++h) val[r][h] = (vmask >> (r * FA + h)) & 1u ? pl[r * rowstep + 32 * h] : 0.0;
+    for (int h = 0; h < FA; ++h) val[r][h] = pl[r * rowstep + 32 * h];
   if (zn) {   // z-normal: this thread's (b, a) accumulators live in registers
 #pragma unroll
     for (int r = 0; r < FR; ++r)
@@ -1962,6 +1965,10 @@ __global__ void __launch_bounds__(FACE_THREADS, NT <= 5 ? 3 : 1) k_faces(FaceArg
     }
     fence_mbar_init();
   }
+  // ring, weights and partials zeroed before the first bulk copy: the consumers' unpredicated
+  // loads of points outside a plane may reach past its slot (face_plane)
+  for (int q = tid; q < NS * SLOT + 3 * N + FACE_WARPS * FZ * N; q += FACE_THREADS) ring[q] = 0.0;
+  fence_proxy_async();   // these generic writes precede the async-proxy fills of the ring
   const FaceGeo fg = face_geo(c);
   const bool zn = fg.n1 == 2, yn = fg.n1 == 1 || fg.n2 == 1, xn = fg.n2 == 0;
   double* sY = fg.n1 == 1 ? sA : sB;   // y-normal destination [z][a]
@@ -1989,7 +1996,7 @@ __global__ void __launch_bounds__(FACE_THREADS, NT <= 5 ? 3 : 1) k_faces(FaceArg
     const double* Wz = sWt + 2 * N;
     const double* Wy = sWt + N;
     // plane-invariant per-thread state, computed once: which of this thread's points lie in the
-    // plane (bit mask), its first point's offset and the row step of its point rows
+    // plane (bit mask, for the z-normal write-out), its first point's offset and the row step
     double wx[FA], za[FR][FA];
     uint32_t vmask = 0;
 #pragma unroll
@@ -2012,7 +2019,7 @@ __global__ void __launch_bounds__(FACE_THREADS, NT <= 5 ? 3 : 1) k_faces(FaceArg
         mbar_wait(&full[slot], ph);
         const double* pl = ring + slot * SLOT + first;
         double yp[FA];
-        face_plane<FR, FA, S>(pl, z, rowstep, vmask, zn, xn, Wz[z], Wy, wx, za, sB, yp, ey, warp, lane);
+        face_plane<FR, FA, S>(pl, z, rowstep, zn, xn, Wz[z], Wy, wx, za, sB, yp, ey, warp, lane);
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[slot]);
         if (++slot == NS) {
