@@ -730,7 +730,14 @@ int ozaki_build(const std::vector<OzShape>& shapes, const std::vector<OzLists>& 
         else if (shapes[q.shape].w >= 32) solo_wide += q.k1 - q.k0;
         else solo_narrow += q.k1 - q.k0;
       }
-      fprintf(stderr, "ozdump %d %zu %.0f %ld %ld %ld %ld\n", b, lists[b].size(), c, sh_ch, solo_wide, solo_narrow, segs);
+      double mma = 0.0;   // modelled tensor cycles without the per-chunk constant
+      long nch = 0;
+      for (const Part& q : lists[b]) {
+        nch += q.k1 - q.k0;
+        mma += cost(q, q.k0, q.k1) - 60.0 * (q.k1 - q.k0);
+      }
+      fprintf(stderr, "ozdump %d %zu %.0f %ld %ld %ld %ld %ld %.0f\n", b, lists[b].size(), c, sh_ch, solo_wide, solo_narrow,
+              segs, nch, mma);
     }
   }
   // segments per tile (in K order), partial slots for the split tiles

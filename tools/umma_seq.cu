@@ -27,7 +27,8 @@ struct Op { int a, brow, d, n; };
 __constant__ Op c_ops[64];
 
 constexpr int SCR = 44 * 1024;   // scratch region written by the concurrent bulk-copy warp
-__constant__ int c_flags;   // 1: commit per chunk, 2: fence::after_thread_sync per chunk, 4: rotate D by 64 cols per chunk (sets of 7)
+__constant__ int c_flags;
+__constant__ int c_setoff;   // flag 64: chunk c accumulates at D + (c & 1) * c_setoff   // 1: commit per chunk, 2: fence::after_thread_sync per chunk, 4: rotate D by 64 cols per chunk (sets of 7)
 __global__ void k(int nops, int chunks, int lboB_rows, long long* out, const uint8_t* gsrc, int copy_mode) {
   extern __shared__ __align__(1024) uint8_t sm[];
   __shared__ uint32_t tb;
@@ -57,7 +58,7 @@ __global__ void k(int nops, int chunks, int lboB_rows, long long* out, const uin
       const uint32_t st = su(sm + (c % NST) * STAGE);
       const int fl = c_flags;
       if (fl & 2) asm volatile("tcgen05.fence::after_thread_sync;\n");
-      const uint32_t dset = (fl & 4) ? (uint32_t)((c % 7) * 64) : 0u;
+      const uint32_t dset = (fl & 4) ? (uint32_t)((c % 7) * 64) : (fl & 64) ? (uint32_t)((c & 1) * c_setoff) : 0u;
       for (int i = 0; i < nops; ++i) {
         const Op o = c_ops[i];
         mma(tmem + o.d + dset, desc(st + o.a * 4096, lboA, sboA), desc(st + 28672 + o.brow * 16, lboB, sboB),
@@ -132,6 +133,18 @@ static void run(const char* name, const std::vector<Op>& ops, int lbo_rows = 512
 
 // the kernel's per-chunk sequence for width W: A slice p against stacked B rows [0, N_p), N_p =
 // pad16((8-p) W), split into near-equal parts of <= 256
+static std::vector<Op> sparse_seq(int W, int p0) {   // the kernel's REV order, slices p0+1..7 only
+  std::vector<Op> v;
+  for (int p = 7; p > p0; --p) {
+    const int N = ((8 - p) * W + 15) / 16 * 16;
+    const int parts = (N + 255) / 256, step = ((N + parts - 1) / parts + 15) / 16 * 16;
+    for (int r0 = 0; r0 < N; r0 += step) {
+      const int nn = N - r0 < step ? N - r0 : step;
+      v.push_back(Op{p - 1, r0, (p - 1) * W + r0, nn});
+    }
+  }
+  return v;
+}
 static std::vector<Op> real_seq(int W, bool fixed_b, bool alt_d, bool same_a) {
   std::vector<Op> v;
   int flip = 0;
@@ -181,6 +194,41 @@ int main() {
     cudaMemcpyToSymbol(c_flags, &f, sizeof(int));
     run("real_w8_rot7sets_commit", real_seq(8, false, false, false));
     f = 0;
+    cudaMemcpyToSymbol(c_flags, &f, sizeof(int));
+  }
+  for (int p0 : {0, 2, 3, 4, 5}) {
+    for (int f : {0, 1}) {
+      cudaMemcpyToSymbol(c_flags, &f, sizeof(int));
+      char nm[64];
+      snprintf(nm, 64, "sparse_w72_p0_%d_commit%d", p0, f);
+      run(nm, sparse_seq(72, p0));
+    }
+  }
+  {
+    int f = 0;
+    cudaMemcpyToSymbol(c_flags, &f, sizeof(int));
+    for (int n : {32, 64, 128}) {
+      std::vector<Op> v;
+      char nm[64];
+      v.clear(); for (int i = 0; i < 8; ++i) v.push_back(Op{i % 7, 0, 0, n}); snprintf(nm, 64, "n%d_x8_sameD", n); run(nm, v);
+      v.clear(); for (int i = 0; i < 8; ++i) v.push_back(Op{i % 7, 0, i * 64, n}); snprintf(nm, 64, "n%d_x8_distinctD", n); run(nm, v);
+      v.clear(); for (int i = 0; i < 8; ++i) v.push_back(Op{i % 7, i * 32, i * 64, n}); snprintf(nm, 64, "n%d_x8_distinctD_distinctB", n); run(nm, v);
+    }
+  }
+  for (int W : {32, 24}) {
+    int off = 7 * W + 16;
+    cudaMemcpyToSymbol(c_setoff, &off, sizeof(int));
+    for (int p0 : {0, 2, 3, 4, 5}) {
+      for (int f : {1, 65}) {
+        cudaMemcpyToSymbol(c_flags, &f, sizeof(int));
+        char nm[64];
+        snprintf(nm, 64, "sparse_w%d_p0_%d_%s", W, p0, f & 64 ? "altsets" : "oneset");
+        run(nm, sparse_seq(W, p0));
+      }
+    }
+  }
+  {
+    int f = 0;
     cudaMemcpyToSymbol(c_flags, &f, sizeof(int));
   }
   printf("{\"probe\": \"umma_seq\", \"results\": [\n");
