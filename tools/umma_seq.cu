@@ -207,7 +207,7 @@ int main() {
   {
     int f = 0;
     cudaMemcpyToSymbol(c_flags, &f, sizeof(int));
-    for (int n : {32, 64, 128}) {
+    for (int n : {32, 64}) {   // 8 distinct D ranges of 64 columns fit the 512 allocated
       std::vector<Op> v;
       char nm[64];
       v.clear(); for (int i = 0; i < 8; ++i) v.push_back(Op{i % 7, 0, 0, n}); snprintf(nm, 64, "n%d_x8_sameD", n); run(nm, v);
