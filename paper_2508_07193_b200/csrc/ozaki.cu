@@ -563,20 +563,16 @@ int ozaki_chunk_lists(std::vector<OzShape>& shapes, std::vector<OzLists>* lists,
   return 0;
 }
 
-// Cost model of one K chunk (cycles), fitted to the per-CTA MMA-warp cycles of a cfg4 apply
-// (tools/oz_prof.py with FMP_OZ_DUMP=1: ~1154 per 72-column chunk, ~602 per 8-column chunk, ~16.6K
-// per item): each MMA costs max(N/2, 80) on the tensor pipe (N/2 for N >= 160, tools/umma_seq.cu),
-// with the same N splits as issue_chunk, plus ~60 cycles of per-chunk issue overhead (stage
-// wait, commit); every work item adds OZ_ITEM_CYCLES (accumulator drain, pipeline restart).
-constexpr double OZ_ITEM_CYCLES = 16000.0;
+// Cost model of one K chunk (cycles), fitted to the per-CTA MMA-warp cycles of cfg4 and 64^3
+// applies with zero-slice skipping (tools/oz_prof.py with FMP_OZ_DUMP=1) and to the MMA-sequence
+// probe (tools/umma_seq.cu): ~560 cycles per chunk (stage wait, commit, issue floor) plus ~0.3
+// cycles per issued N column (the N/2 tensor rate, partly overlapped), with the same N splits as
+// issue_chunk; every work item adds OZ_ITEM_CYCLES (accumulator drain, pipeline restart).
+constexpr double OZ_ITEM_CYCLES = 8000.0;
 static double chunk_cycles(int w, int p0 = 0) {
-  double tensor = 60.0;
-  for (int p = p0 + 1; p <= OZ_S; ++p) {
-    const int N = oz_pad16((OZ_S + 1 - p) * w);
-    const int parts = (N + 255) / 256, step = oz_pad16((N + parts - 1) / parts);
-    for (int r0 = 0; r0 < N; r0 += step) tensor += std::max(80.0, std::min(step, N - r0) / 2.0);
-  }
-  return tensor;
+  double n_cols = 0.0;
+  for (int p = p0 + 1; p <= OZ_S; ++p) n_cols += oz_pad16((OZ_S + 1 - p) * w);
+  return 560.0 + 0.3 * n_cols;
 }
 
 // Work plan of one batched GEMM over the persistent CTAs (data-parallel waves + a stream-K
