@@ -257,6 +257,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
       // register, the tile's column exponents into shared memory (one global load per column
       // instead of one dependent L2 round trip per 8 columns inside the drain loop)
       const int ea = row < sh.m ? sh.eA[row] : 0;
+      const int zrow = row < sh.m && sh.perm ? sh.perm[row] : row;   // Z row in the reference order
       asm volatile("bar.sync 1, 256;\n" ::: "memory");   // previous item's readers of eb_sh are done
       if (half == 0 && rr < w) {
         const int n = tl.nt * w + rr;
@@ -297,7 +298,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
           if (part) {
             part[c * OZ_M + rr] = val;   // [column][row]: coalesced over the warp's rows
           } else if (ok) {
-            sh.Z[(size_t)(tl.nt * w + c) * sh.ld + row] = val;
+            sh.Z[(size_t)(tl.nt * w + c) * sh.ld + zrow] = val;
           }
         }
       }
@@ -328,7 +329,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
               }
 #pragma unroll
               for (int j = 0; j < FC; ++j)
-                if (c0 + j < nvalid) sh.Z[(size_t)(tl.nt * w + c0 + j) * sh.ld + row] = s[j];
+                if (c0 + j < nvalid) sh.Z[(size_t)(tl.nt * w + c0 + j) * sh.ld + zrow] = s[j];
             }
           }
           if (tid == 0) counters[tl.slot0] = 0;   // re-armed for the next launch
@@ -357,7 +358,8 @@ __device__ __forceinline__ void ozaki_write_digits(const OzSlice& o, int r, int 
 #pragma unroll
   for (int j = 0; j < 16; ++j) {
     const int k = gk * 16 + j;
-    const double x = (valid && k < o.kvalid) ? o.src[(size_t)r * o.ld + k] : 0.0;
+    const double x = (valid && k < o.kvalid) ? o.src[(size_t)(o.rperm ? o.rperm[r] : r) * o.ld + (o.kperm ? o.kperm[k] : k)]
+                                             : 0.0;
     long long V = llrint(ldexp(x, 8 * OZ_S - 2 - e));   // |V| <= 2^(8S-2)
 #pragma unroll
     for (int p = OZ_S - 1; p >= 0; --p) {                // balanced base-256 digits, least significant first
@@ -389,7 +391,7 @@ __global__ void __launch_bounds__(256) k_ozaki_slice_rows(const OzSlice* __restr
   const bool valid = r < o.rows;
   double mx = 0.0;
   if (valid) {
-    const double* src = o.src + (size_t)r * o.ld;
+    const double* src = o.src + (size_t)(o.rperm ? o.rperm[r] : r) * o.ld;   // the max is order-independent
     for (int k = threadIdx.x; k < o.kvalid; k += blockDim.x) mx = fmax(mx, fabs(src[k]));
   }
 #pragma unroll
@@ -462,6 +464,29 @@ int ozaki_launch(const OzPlan& p, cudaStream_t st) {
                                                             g_oz_prof, dbg);
   FMP_CHECK_LAUNCH();
   return 0;
+}
+
+// ---------------------------------------------------------------- row order
+std::vector<int> ozaki_row_order(int ex, int ey, int ez) {
+  struct Pt { uint64_t key; int row; };
+  std::vector<Pt> pts;
+  auto morton = [](uint64_t i, uint64_t j, uint64_t k) {
+    uint64_t c = 0;
+    for (int b = 0; b < 10; ++b) c |= (((i >> b) & 1) << (3 * b)) | (((j >> b) & 1) << (3 * b + 1)) | (((k >> b) & 1) << (3 * b + 2));
+    return c;
+  };
+  int row = 0;
+  for (int c = 0; c < 3; ++c)   // the reference's row order (ref:subdomain.py:183-194)
+    for (int k = 0; k < ez; ++k)
+      for (int j = 0; j < ey; ++j)
+        for (int i = 0; i < ex; ++i) {
+          const bool on = c == 0 ? (j == 0 || k == 0) : c == 1 ? (i == 0 || k == 0) : (i == 0 || j == 0);
+          if (on) pts.push_back(Pt{morton(i, j, k) * 4 + c, row++});
+        }
+  std::stable_sort(pts.begin(), pts.end(), [](const Pt& a, const Pt& b) { return a.key < b.key; });
+  std::vector<int> perm(pts.size());
+  for (size_t q = 0; q < pts.size(); ++q) perm[q] = pts[q].row;
+  return perm;
 }
 
 // ---------------------------------------------------------------- zero-slice skipping

@@ -19,6 +19,9 @@ struct OzShape {
   const uint16_t* klist;
   const uint8_t* kp0;
   const int* koff;
+  // Row/column order of the GEMM (ozaki_row_order): position i of the sliced C^-1 / of the K axis
+  // is correction row perm[i]; Z is written back through it.  null = identity.
+  const int* perm;
 };
 // Host copy of one shape's chunk lists (ozaki_chunk_lists -> ozaki_build).
 struct OzLists {
@@ -53,6 +56,8 @@ struct OzSlice {
   const double* src;
   int8_t* dst;
   int* exps;
+  const int* rperm;   // row r of the operand is source row rperm[r] (null = identity)
+  const int* kperm;   // K position k is source column kperm[k] (null = identity)
   int rows, ld, kvalid, kchunks, T, stacked;   // stacked = 1: slices stacked along N (B operand)
   int R;              // stacked: rows per K half of a (tile, kchunk) block (>= S * T, zero padding)
   int64_t row0, q0;   // prefix offsets of this operand in the batched exponent / digit grids
@@ -73,6 +78,12 @@ int ozaki_slice(const OzSlice* d_slices, int count, int64_t rows, int64_t padded
 // leading all-zero slice counts (FMP_OZ_DENSE=1: every chunk, no skipping); uploads the lists
 // into `plan` and points the shapes at them.  Returns 0 or -1.
 int ozaki_chunk_lists(std::vector<OzShape>& shapes, std::vector<OzLists>* lists, OzPlan* plan);
+// Locality order of the m correction rows of a box (ex, ey, ez): the rows (reference order:
+// component-major, ascending linear index) sorted by the Morton code of their point (i, j, k),
+// component last, so the points C^-1 couples strongly -- the same or nearby places, every
+// component -- share 128-row tiles and 32-column chunks, and fewer slice blocks are non-zero
+// (FMP_OZ_NOPERM=1: reference order).  Returns perm with position -> reference row.
+std::vector<int> ozaki_row_order(int ex, int ey, int ez);
 // Work items (column tiles x list segments) for the shapes (entries with n == 0 are skipped),
 // balanced over `sms` persistent CTAs, uploaded with the partial-slot workspace.  `plan` already
 // holds the chunk lists (ozaki_chunk_lists).  Returns 0 or -1.

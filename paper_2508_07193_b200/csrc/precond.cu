@@ -2170,7 +2170,7 @@ struct fmp_precond {
   bool use_cublas = false;
   bool use_ozaki = true;
   std::vector<int8_t*> oz_a, oz_b;
-  std::vector<int*> oz_ea, oz_eb;
+  std::vector<int*> oz_ea, oz_eb, oz_perm;
   OzPlan oz;                              // work items, schedule and split-K workspace
   OzSlice* d_ozslices = nullptr;          // per-apply slicing of Y, all shapes in two launches
   int n_ozslices = 0;
@@ -2230,6 +2230,7 @@ static void free_plan(fmp_precond* p) {
   for (auto* q : p->oz_a) cudaFree(q);
   for (auto* q : p->oz_b) cudaFree(q);
   for (auto* q : p->oz_ea) cudaFree(q);
+  for (auto* q : p->oz_perm) cudaFree(q);
   for (auto* q : p->oz_eb) cudaFree(q);
   ozaki_free(&p->oz);
   cudaFree(p->d_ozslices);
@@ -2538,9 +2539,23 @@ extern "C" int fmp_precond_create(const fmp_precond_desc* desc, fmp_precond** ou
       p->oz_b.push_back(b);
       p->oz_ea.push_back(ea);
       p->oz_eb.push_back(eb);
-      sa.push_back(OzSlice{p->cinv[s2], a, ea, m, (int)sh.ld, m, kc, ozaki_tile_m(), 0, 0, 0, 0, 0});
-      if (n > 0) sb.push_back(OzSlice{p->ymat[s2], b, eb, n, (int)sh.ld, m, kc, w, 1, ozaki_stack_rows(w), 0, 0, 0});
-      os.push_back(OzShape{a, ea, b, eb, p->zmat[s2], m, n, (int)sh.ld, kc, w, ozaki_stack_rows(w)});
+      // locality order of the correction rows (both C^-1 axes, Y's K axis, Z's rows)
+      int* perm = nullptr;
+      // (boxes with an extent < 24, 16^3-class subdomains: no gain, and the gathered Y slicing costs)
+      if (!getenv_flag("FMP_OZ_NOPERM") && std::max(sh.ext[0], std::max(sh.ext[1], sh.ext[2])) >= 24) {
+        const std::vector<int> h = ozaki_row_order((int)sh.ext[0], (int)sh.ext[1], (int)sh.ext[2]);
+        FMP_REQUIRE((int64_t)h.size() == m, "Ozaki row order: %zu rows for m = %d", h.size(), m);
+        if (upload(h, &perm)) {
+          free_plan(p);
+          return -1;
+        }
+        p->oz_perm.push_back(perm);
+      }
+      sa.push_back(OzSlice{p->cinv[s2], a, ea, perm, perm, m, (int)sh.ld, m, kc, ozaki_tile_m(), 0, 0, 0, 0, 0});
+      if (n > 0)
+        sb.push_back(OzSlice{p->ymat[s2], b, eb, nullptr, perm, n, (int)sh.ld, m, kc, w, 1, ozaki_stack_rows(w), 0, 0, 0});
+      os.push_back(OzShape{a, ea, b, eb, p->zmat[s2], m, n, (int)sh.ld, kc, w, ozaki_stack_rows(w), nullptr, nullptr,
+                           nullptr, perm});
     }
     int64_t ra = 0, qa = 0;
     ozaki_plan_slices(sa.data(), (int)sa.size(), &ra, &qa);

@@ -92,9 +92,10 @@ def test_ozaki_elementwise_vs_dgemm(gext, grid):
 
 @pytest.mark.parametrize("gext,grid", [((96, 96, 96), (3, 3, 3)), ((64, 64, 64), (4, 4, 4))])
 def test_zero_slice_skipping_is_exact(gext, grid, monkeypatch):
-    """Skipping the all-zero C^-1 slice blocks (and whole all-zero K chunks) changes no bit: with
-    whole-tile items (FMP_OZ_NOSPLIT, so no schedule-dependent K segments) the sparse GEMM equals
-    the dense one bitwise.  96^3/3^3 holds every 32^3 shape of the cfg4 census (rotation groups);
+    """Skipping the all-zero C^-1 slice blocks (and whole all-zero K chunks) and the locality row
+    order change no bit: with whole-tile items (FMP_OZ_NOSPLIT, so no schedule-dependent K
+    segments) the sparse GEMM equals the dense one, and the dense one in the reference row order,
+    bitwise.  96^3/3^3 holds every 32^3 shape of the cfg4 census (rotation groups);
     64^3/4^3 the 16^3 subdomains of config 5."""
     from paper_2508_07193_b200 import Box, RasPreconditioner, make_partition, make_transport
     part = make_partition(Box(*gext), grid, 1)
@@ -110,3 +111,7 @@ def test_zero_slice_skipping_is_exact(gext, grid, monkeypatch):
     z_sparse = prec.apply(r)
     assert torch.equal(z_dense, z_sparse)
     assert prec.plan.ozaki_kept_slices() < 0.9   # the skipping is active at these sizes
+    # the locality row order only permutes exact integer sums: reference order, dense, bit-identical
+    monkeypatch.setenv("FMP_OZ_NOPERM", "1")
+    monkeypatch.setenv("FMP_OZ_DENSE", "1")
+    assert torch.equal(RasPreconditioner(part, 0.25, tr).apply(r), z_dense)
