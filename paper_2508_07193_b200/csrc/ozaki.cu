@@ -351,15 +351,16 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
 // of tile height T.  A operand: [tile][kchunk][S][2 K halves][T/8][8 rows][16 B].  B operand
 // (stacked): [tile][kchunk][2 K halves][R rows][16 B] with slice p in rows [p T, (p+1) T) and
 // zero rows [S T, R) (T a multiple of 8, so every slice starts on an 8-row core matrix).
-__device__ __forceinline__ void ozaki_write_digits(const OzSlice& o, int r, int gk, int e, bool valid) {
+template <bool KPERM>
+__device__ __forceinline__ void ozaki_write_digits(const OzSlice& o, const double* srow, int r, int gk, int e,
+                                                   bool valid) {
   uint32_t w[OZ_S][4];
 #pragma unroll
   for (int p = 0; p < OZ_S; ++p) w[p][0] = w[p][1] = w[p][2] = w[p][3] = 0u;
 #pragma unroll
   for (int j = 0; j < 16; ++j) {
     const int k = gk * 16 + j;
-    const double x = (valid && k < o.kvalid) ? o.src[(size_t)(o.rperm ? o.rperm[r] : r) * o.ld + (o.kperm ? o.kperm[k] : k)]
-                                             : 0.0;
+    const double x = (valid && k < o.kvalid) ? srow[KPERM ? o.kperm[k] : k] : 0.0;
     long long V = llrint(ldexp(x, 8 * OZ_S - 2 - e));   // |V| <= 2^(8S-2)
 #pragma unroll
     for (int p = OZ_S - 1; p >= 0; --p) {                // balanced base-256 digits, least significant first
@@ -407,7 +408,11 @@ __global__ void __launch_bounds__(256) k_ozaki_slice_rows(const OzSlice* __restr
   }
   __syncthreads();
   const int e = e_sh, groups = o.kchunks * (OZ_KC / 16);
-  for (int gk = threadIdx.x; gk < groups; gk += blockDim.x) ozaki_write_digits(o, r, gk, e, valid);
+  const double* srow = o.src + (size_t)(valid ? (o.rperm ? o.rperm[r] : r) : 0) * o.ld;
+  if (o.kperm)
+    for (int gk = threadIdx.x; gk < groups; gk += blockDim.x) ozaki_write_digits<true>(o, srow, r, gk, e, valid);
+  else
+    for (int gk = threadIdx.x; gk < groups; gk += blockDim.x) ozaki_write_digits<false>(o, srow, r, gk, e, valid);
 }
 
 void ozaki_plan_slices(OzSlice* s, int count, int64_t* rows, int64_t* threads) {

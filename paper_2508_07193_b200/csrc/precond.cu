@@ -1790,6 +1790,8 @@ struct FaceArgs {
   int pmax;
   int max_ps;                  // largest padded plane stride of the plan
   const int* rowmap;           // shape row -> group row maps (fmp_shape::rowmap_off), may be null
+  const double* facepad;       // per distinct extent n: [U^T_n, V^T_n] zero-padded to FaceMat<NT> (N x S)
+  unsigned char pad_slot[80];  // extent n -> its slot in facepad
 };
 
 __device__ __forceinline__ int ext_of(const SubD& d, int a) { return a == 0 ? d.ex : (a == 1 ? d.ey : d.ez); }
@@ -1819,14 +1821,14 @@ __device__ __forceinline__ void face_mm(const double* A, const double* B, double
     C[(m0 + g) * S + n0 + 2 * t + 1] = d1;
   }
 }
-// zero-padded copy of the row-major n x n factor f into M (N x S)
+// the zero-padded N x S copy of the forward factor of component c on axis a (extent n): one
+// 16-byte vectorised copy of the plan's pre-padded matrix (no per-element index arithmetic)
 template <int NT>
-__device__ __forceinline__ void face_load_factor(double* M, const double* f, int n, int tid, int nth) {
-  constexpr int N = FaceMat<NT>::N, S = FaceMat<NT>::S;
-  for (int q = tid; q < N * S; q += nth) {
-    const int r = q / S, cc = q - r * S;
-    M[q] = (r < n && cc < n) ? __ldg(f + r * n + cc) : 0.0;
-  }
+__device__ __forceinline__ void face_load_factor(double* M, const FaceArgs& A, int c, int a, int n, int tid, int nth) {
+  constexpr int W2 = FaceMat<NT>::WORDS / 2;
+  const double2* f = reinterpret_cast<const double2*>(A.facepad + (size_t)(2 * A.pad_slot[n] + (a == c ? 0 : 1)) * FaceMat<NT>::WORDS);
+  double2* m2 = reinterpret_cast<double2*>(M);
+  for (int q = tid; q < W2; q += nth) m2[q] = __ldg(f + q);
 }
 
 // K5: Y[:, col] = e0 on the two faces per component, e0 = G^-1 y^ evaluated only there.
@@ -2063,8 +2065,8 @@ __global__ void __launch_bounds__(FACE_THREADS, NT <= 5 ? 3 : 1) k_faces(FaceArg
     const int ua = f == 0 ? fg.u1 : fg.u2, va = f == 0 ? fg.v1 : fg.v2;
     const int nu = ext[ua], nv_ = ext[va];
     double *sFu = sX, *sFv = sX + W, *sT = sX + 2 * W;
-    face_load_factor<NT>(sFu, fwd_factor(A.factors, sh, c, ua), nu, tid, FACE_THREADS);
-    face_load_factor<NT>(sFv, fwd_factor(A.factors, sh, c, va), nv_, tid, FACE_THREADS);
+    face_load_factor<NT>(sFu, A, c, ua, nu, tid, FACE_THREADS);
+    face_load_factor<NT>(sFv, A, c, va, nv_, tid, FACE_THREADS);
     __syncthreads();
     face_mm<NT, false, false>(f == 0 ? sA : sB, sFv, sT, warp, FACE_THREADS / 32, lane);   // T = Proj Fv
     __syncthreads();
@@ -2107,8 +2109,8 @@ __global__ void __launch_bounds__(FACE_THREADS) k_corr(FaceArgs A) {
     const int ua = f == 0 ? fg.u1 : fg.u2, va = f == 0 ? fg.v1 : fg.v2;
     const int nu = ext[ua], nv = ext[va];
     __syncthreads();   // previous face's result has been written out
-    face_load_factor<NT>(sFu, fwd_factor(A.factors, sh, c, ua), nu, tid, FACE_THREADS);
-    face_load_factor<NT>(sFv, fwd_factor(A.factors, sh, c, va), nv, tid, FACE_THREADS);
+    face_load_factor<NT>(sFu, A, c, ua, nu, tid, FACE_THREADS);
+    face_load_factor<NT>(sFv, A, c, va, nv, tid, FACE_THREADS);
     for (int q = tid; q < W; q += FACE_THREADS) {
       const int u = q / S, v = q - u * S;
       const int row = (u < nu && v < nv) ? face_row(c, f, u, v, ex, ey) : -1;
@@ -2124,6 +2126,20 @@ __global__ void __launch_bounds__(FACE_THREADS) k_corr(FaceArgs A) {
       const int tu = q / nv, tv = q - tu * nv;
       out[tu * pm + tv] = sO[tu * S + tv];
     }
+  }
+}
+
+// Padded forward factors for the face kernels: slot e holds [U^T_n, V^T_n] of extent n as
+// zero-padded N x S matrices (N = 8 NT, S = N + 4), built once per plan.
+__global__ void k_pad_factors(const double* __restrict__ factors, const int64_t* __restrict__ src_off,
+                              const int* __restrict__ ext, int nmat, int N, int S, double* __restrict__ out) {
+  const int mat = blockIdx.y, n = ext[mat];
+  if (mat >= nmat) return;
+  const double* f = factors + src_off[mat];
+  double* o = out + (size_t)mat * N * S;
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < N * S; q += gridDim.x * blockDim.x) {
+    const int r = q / S, cc = q - r * S;
+    o[q] = (r < n && cc < n) ? f[r * n + cc] : 0.0;
   }
 }
 
@@ -2171,6 +2187,8 @@ struct fmp_precond {
   bool use_ozaki = true;
   std::vector<int8_t*> oz_a, oz_b;
   std::vector<int*> oz_ea, oz_eb, oz_perm;
+  double* facepad = nullptr;            // padded forward factors of the face kernels (k_pad_factors)
+  unsigned char pad_slot[80] = {};
   OzPlan oz;                              // work items, schedule and split-K workspace
   OzSlice* d_ozslices = nullptr;          // per-apply slicing of Y, all shapes in two launches
   int n_ozslices = 0;
@@ -2231,6 +2249,7 @@ static void free_plan(fmp_precond* p) {
   for (auto* q : p->oz_b) cudaFree(q);
   for (auto* q : p->oz_ea) cudaFree(q);
   for (auto* q : p->oz_perm) cudaFree(q);
+  cudaFree(p->facepad);
   for (auto* q : p->oz_eb) cudaFree(q);
   ozaki_free(&p->oz);
   cudaFree(p->d_ozslices);
@@ -2511,6 +2530,36 @@ extern "C" int fmp_precond_create(const fmp_precond_desc* desc, fmp_precond** ou
       return -1;
     }
     for (int c = 0; c < 3; ++c) p->n_gtiles[c] = (int)gt[c].size();
+  }
+  {  // padded forward factors of the face kernels (k_faces / k_corr): [U^T_n, V^T_n] per extent
+    const int pm = (int)p->d.pmax, NTf = pm <= 24 ? 3 : (pm <= 40 ? 5 : 9), N = 8 * NTf, S = N + 4;
+    std::vector<int64_t> off;
+    std::vector<int> ext;
+    for (const auto& sh : p->shapes)
+      for (int a = 0; a < 3; ++a) {
+        const int n = (int)sh.ext[a];
+        FMP_REQUIRE(n > 0 && n < 80 && n <= N, "face factors: extent %d", n);
+        if (std::find(ext.begin(), ext.end(), n) != ext.end()) continue;
+        p->pad_slot[n] = (unsigned char)(ext.size() / 2);
+        ext.push_back(n);
+        off.push_back(sh.ut_off[a]);
+        ext.push_back(n);
+        off.push_back(sh.vt_off[a]);
+      }
+    int64_t* d_off = nullptr;
+    int* d_ext = nullptr;
+    if (cudaMalloc(&p->facepad, sizeof(double) * (size_t)N * S * ext.size()) != cudaSuccess || upload(off, &d_off) ||
+        upload(ext, &d_ext)) {
+      cudaFree(d_off);
+      cudaFree(d_ext);
+      free_plan(p);
+      FMP_REQUIRE(false, "face factor padding: allocation failed");
+    }
+    k_pad_factors<<<dim3(8, (unsigned)ext.size()), 256>>>(p->d.factors, d_off, d_ext, (int)ext.size(), N, S, p->facepad);
+    const cudaError_t e = cudaDeviceSynchronize();
+    cudaFree(d_off);
+    cudaFree(d_ext);
+    FMP_CHECK_CUDA(e);
   }
   bool have_cinv = desc->alpha != 0.0;
   for (const double* c : p->cinv) have_cinv = have_cinv && c != nullptr;
@@ -2891,7 +2940,8 @@ static int precond_apply(fmp_precond* p, const fmp_block* blk, int mode, int par
   mark(2);
   const int pm = (int)p->d.pmax;
   FaceArgs fa{p->d.subs, p->d.shapes, p->d.factors, wb, p->d.corr, p->d_ymat, p->d_zmat, pm, (p->max_p + 3) & ~3,
-              p->d.rowmap};
+              p->d.rowmap, p->facepad, {}};
+  memcpy(fa.pad_slot, p->pad_slot, sizeof(fa.pad_slot));
   if (mode != FMP_SOLVE_EXACT) {
     const dim3 fg(3, (unsigned)p->d.n_sub);
     const int slot = face_slot(fa.max_ps);
