@@ -106,6 +106,36 @@ __device__ __forceinline__ void issue_chunk_order(uint64_t da0, uint64_t db0, ui
     }
   }
 }
+// One asm block for a whole non-first chunk of a 72-column tile, p = 7 .. 1 (REV): a single elect,
+// every MMA predicated on p > p0, the descriptors and TMEM columns formed by immediate adds, so
+// ptxas moves da0 / db0 / tmem into uniform registers once per chunk instead of once per MMA.
+// (Generated from the same N splits as issue_chunk_order<72, true>.)
+__device__ __forceinline__ void issue_chunk72_rev(uint64_t da0, uint64_t db0, uint32_t tmem, int p0) {
+  asm volatile(
+      "{\n\t.reg .pred e, q, en;\n\t.reg .b32 d, id;\n\t.reg .b64 a, b;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 en, 1, 0;\n\t"
+      "setp.lt.s32 q, %3, 7;\n\tand.pred q, q, e;\n\tadd.s64 a, %1, 1536;\n\t"
+      "add.u32 d, %0, 432;\n\tadd.s64 b, %2, 0;\n\tmov.b32 id, 135529632;\n\t@q tcgen05.mma.cta_group::1.kind::i8 [d], a, b, id, en;\n\t"
+      "setp.lt.s32 q, %3, 6;\n\tand.pred q, q, e;\n\tadd.s64 a, %1, 1280;\n\t"
+      "add.u32 d, %0, 360;\n\tadd.s64 b, %2, 0;\n\tmov.b32 id, 136578208;\n\t@q tcgen05.mma.cta_group::1.kind::i8 [d], a, b, id, en;\n\t"
+      "setp.lt.s32 q, %3, 5;\n\tand.pred q, q, e;\n\tadd.s64 a, %1, 1024;\n\t"
+      "add.u32 d, %0, 288;\n\tadd.s64 b, %2, 0;\n\tmov.b32 id, 137888928;\n\t@q tcgen05.mma.cta_group::1.kind::i8 [d], a, b, id, en;\n\t"
+      "setp.lt.s32 q, %3, 4;\n\tand.pred q, q, e;\n\tadd.s64 a, %1, 768;\n\t"
+      "add.u32 d, %0, 216;\n\tadd.s64 b, %2, 0;\n\tmov.b32 id, 136578208;\n\t@q tcgen05.mma.cta_group::1.kind::i8 [d], a, b, id, en;\n\t"
+      "add.u32 d, %0, 360;\n\tadd.s64 b, %2, 144;\n\tmov.b32 id, 136578208;\n\t@q tcgen05.mma.cta_group::1.kind::i8 [d], a, b, id, en;\n\t"
+      "setp.lt.s32 q, %3, 3;\n\tand.pred q, q, e;\n\tadd.s64 a, %1, 512;\n\t"
+      "add.u32 d, %0, 144;\n\tadd.s64 b, %2, 0;\n\tmov.b32 id, 137364640;\n\t@q tcgen05.mma.cta_group::1.kind::i8 [d], a, b, id, en;\n\t"
+      "add.u32 d, %0, 336;\n\tadd.s64 b, %2, 192;\n\tmov.b32 id, 137102496;\n\t@q tcgen05.mma.cta_group::1.kind::i8 [d], a, b, id, en;\n\t"
+      "setp.lt.s32 q, %3, 2;\n\tand.pred q, q, e;\n\tadd.s64 a, %1, 256;\n\t"
+      "add.u32 d, %0, 72;\n\tadd.s64 b, %2, 0;\n\tmov.b32 id, 137888928;\n\t@q tcgen05.mma.cta_group::1.kind::i8 [d], a, b, id, en;\n\t"
+      "add.u32 d, %0, 296;\n\tadd.s64 b, %2, 224;\n\tmov.b32 id, 137626784;\n\t@q tcgen05.mma.cta_group::1.kind::i8 [d], a, b, id, en;\n\t"
+      "setp.lt.s32 q, %3, 1;\n\tand.pred q, q, e;\n\tadd.s64 a, %1, 0;\n\t"
+      "add.u32 d, %0, 0;\n\tadd.s64 b, %2, 0;\n\tmov.b32 id, 138413216;\n\t@q tcgen05.mma.cta_group::1.kind::i8 [d], a, b, id, en;\n\t"
+      "add.u32 d, %0, 256;\n\tadd.s64 b, %2, 256;\n\tmov.b32 id, 138413216;\n\t@q tcgen05.mma.cta_group::1.kind::i8 [d], a, b, id, en;\n\t"
+      "}\n"
+      :: "r"(tmem), "l"(da0), "l"(db0), "r"(p0));
+}
+
 // The first chunk of a tile runs p = 1 first (its acc = 0 MMA spans every level's columns); the
 // others run p = S .. 1, so the chunk ends on its widest MMAs and the tensor pipe still holds
 // ~256 cycles of work while the issuing warp commits, waits for the next stage and sets up.
@@ -229,7 +259,12 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
             case 48: issue_chunk<48>(da0, db0, tmem, first, rev, p0); break;
             case 56: issue_chunk<56>(da0, db0, tmem, first, rev, p0); break;
             case 64: issue_chunk<64>(da0, db0, tmem, first, rev, p0); break;
-            default: issue_chunk<72>(da0, db0, tmem, first, rev, p0); break;
+            default:
+              if (!first && rev && !(dbg & 32))   // FMP_OZ_DBG bit 5 (A/B): the per-MMA form
+                issue_chunk72_rev(da0, db0, tmem, p0);
+              else
+                issue_chunk<72>(da0, db0, tmem, first, rev, p0);
+              break;
           }
           umma_commit(&empty_bar[s]);                 // stage free once these MMAs retire
           if (j == tl.k1 - 1) umma_commit(&tfull_bar);   // accumulators complete
