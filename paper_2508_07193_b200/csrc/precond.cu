@@ -1950,7 +1950,7 @@ __device__ __forceinline__ void face_plane(const double* pl, int z, int rowstep,
 // FR rows per warp, FA columns per lane, NT 8-wide tiles per padded extent (register and
 // shared-memory footprints sized for the plan's extents)
 template <int FR, int FA, int NT>
-__global__ void __launch_bounds__(FACE_THREADS, NT <= 5 ? 3 : 1) k_faces(FaceArgs A) {
+__global__ void __launch_bounds__(FACE_THREADS, NT <= 3 ? 4 : (NT <= 5 ? 3 : 1)) k_faces(FaceArgs A) {
   extern __shared__ __align__(128) double smem[];
   __shared__ __align__(8) uint64_t full[FaceRing<NT>::NS], empty[FaceRing<NT>::NS];
   constexpr int S = FaceMat<NT>::S, W = FaceMat<NT>::WORDS, N = FaceMat<NT>::N;
