@@ -143,7 +143,7 @@ class ClockSampler:
 
 # ----------------------------------------------------------------------------------- ours
 INT8_PROBE_FILE = ROOT / "profiles" / "r01_umma_i8_rate.json"
-NCU_TRAFFIC_FILE = ROOT / "profiles" / "r02_v04_ncu_traffic.json"
+NCU_TRAFFIC_FILE = ROOT / "profiles" / "r02_v05_ncu_traffic.json"
 # bench stage -> ncu kernel name(s) whose DRAM bytes (one ncu --set full capture) it covers
 STAGE_KERNELS = {"plane_fwd": ["k_plane_fast<0, 5>"], "column_fwd": ["k_column_fast_db<0, 12, 5, 2>"],
                  "faces": ["k_faces<5, 2, 5>"], "slice_y": ["k_ozaki_slice_rows", "k_ozaki_exp", "k_ozaki_digits"], "gemm": ["k_ozaki"],
@@ -169,7 +169,7 @@ def dominant_roofline(stages: dict, peaks: dict) -> dict | None:
     """Roofline of the dominant single kernel of the step: the longest kernel of the
     preconditioner apply (the apply is ~2/3 of the step and every one of its kernels runs 8 times
     per step; since the Ozaki GEMM skips its all-zero C^-1 slice blocks that is the forward plane
-    pass k_plane_fast<0>, profiles/r02_v03_launches_step_summary.txt).  Algorithmic work per launch
+    pass k_plane_fast<0>, profiles/r02_v05_launches_step_summary.txt).  Algorithmic work per launch
     as in stage_rooflines; peak = the measured DMMA / HBM / INT8 rate (MEASURED_PEAKS.json and the
     committed probes)."""
     cand = {k: v for k, v in stages.items() if "frac" in v}
@@ -564,7 +564,7 @@ def run_reference(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="cfg4", choices=sorted(CONFIGS))
