@@ -417,8 +417,9 @@ __device__ __forceinline__ void ozaki_write_digits(const OzSlice& o, const doubl
 
 // One CTA per (padded) row: the row's exponent (max |x|), then its digits -- one launch, the row
 // re-read from L1/L2.  Padding rows of the last tile get zero digits.
-__global__ void __launch_bounds__(256) k_ozaki_slice_rows(const OzSlice* __restrict__ sl, int count) {
-  __shared__ double red[8];
+constexpr int OZ_SLICE_THREADS = 512;
+__global__ void __launch_bounds__(OZ_SLICE_THREADS) k_ozaki_slice_rows(const OzSlice* __restrict__ sl, int count) {
+  __shared__ double red[OZ_SLICE_THREADS / 32];
   __shared__ int e_sh;
   int si = 0;
   while (si + 1 < count && sl[si + 1].prow0 <= (int64_t)blockIdx.x) ++si;
@@ -467,7 +468,7 @@ void ozaki_plan_slices(OzSlice* s, int count, int64_t* rows, int64_t* threads) {
 
 int ozaki_slice(const OzSlice* d_slices, int count, int64_t rows, int64_t padded_rows, cudaStream_t st) {
   if (count <= 0 || rows <= 0) return 0;
-  k_ozaki_slice_rows<<<(unsigned)padded_rows, 256, 0, st>>>(d_slices, count);
+  k_ozaki_slice_rows<<<(unsigned)padded_rows, OZ_SLICE_THREADS, 0, st>>>(d_slices, count);
   FMP_CHECK_LAUNCH();
   return 0;
 }
