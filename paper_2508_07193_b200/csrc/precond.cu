@@ -2099,7 +2099,8 @@ __global__ void __launch_bounds__(FACE_THREADS) k_corr(FaceArgs A) {
   constexpr int S = FaceMat<NT>::S, W = FaceMat<NT>::WORDS;
   const SubD d = load_sub(A.subs + blockIdx.y);
   const fmp_shape& sh = A.shapes[d.shape];
-  const int c = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  // one CTA per (component, face, subdomain): blockIdx.x = 2 c + f
+  const int c = blockIdx.x >> 1, f = blockIdx.x & 1, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int ex = d.ex, ey = d.ey, ez = d.ez;
   const int ext[3] = {ex, ey, ez};
   const int pm = A.pmax;
@@ -2113,10 +2114,9 @@ __global__ void __launch_bounds__(FACE_THREADS) k_corr(FaceArgs A) {
   const int* rm = sh.rowmap_off >= 0 ? A.rowmap + sh.rowmap_off : nullptr;
   int base = 0;
   for (int q = 0; q < c; ++q) base += (int)sh.m_comp[q];
-  for (int f = 0; f < 2; ++f) {
+  {
     const int ua = f == 0 ? fg.u1 : fg.u2, va = f == 0 ? fg.v1 : fg.v2;
     const int nu = ext[ua], nv = ext[va];
-    __syncthreads();   // previous face's result has been written out
     face_load_factor<NT>(sFu, A, c, ua, nu, tid, FACE_THREADS);
     face_load_factor<NT>(sFv, A, c, va, nv, tid, FACE_THREADS);
     for (int q = tid; q < W; q += FACE_THREADS) {
@@ -2997,11 +2997,11 @@ static int precond_apply(fmp_precond* p, const fmp_block* blk, int mode, int par
     }
     mark(5);
     if (pm <= 24)
-      k_corr<3><<<dim3(3, (unsigned)p->d.n_sub), FACE_THREADS, 4 * FaceMat<3>::WORDS * sizeof(double), st>>>(fa);
+      k_corr<3><<<dim3(6, (unsigned)p->d.n_sub), FACE_THREADS, 4 * FaceMat<3>::WORDS * sizeof(double), st>>>(fa);
     else if (pm <= 40)
-      k_corr<5><<<dim3(3, (unsigned)p->d.n_sub), FACE_THREADS, 4 * FaceMat<5>::WORDS * sizeof(double), st>>>(fa);
+      k_corr<5><<<dim3(6, (unsigned)p->d.n_sub), FACE_THREADS, 4 * FaceMat<5>::WORDS * sizeof(double), st>>>(fa);
     else
-      k_corr<9><<<dim3(3, (unsigned)p->d.n_sub), FACE_THREADS, 4 * FaceMat<9>::WORDS * sizeof(double), st>>>(fa);
+      k_corr<9><<<dim3(6, (unsigned)p->d.n_sub), FACE_THREADS, 4 * FaceMat<9>::WORDS * sizeof(double), st>>>(fa);
     FMP_CHECK_LAUNCH();
   }
   mark(6);
