@@ -851,7 +851,7 @@ struct FastColArgs {
   int pmax;
   double alpha;
   ExtTable et;
-  int interleave;      // 1: warp gw takes items gw, gw + nw, ... (neighbouring warps read neighbouring columns)
+  int interleave;      // 1: warp gw takes items gw, gw + nw, ...; 2: CTA-contiguous ranges, warps interleaved inside
   const CUtensorMap* maps;   // k_column_fast_db: per-subdomain [3][ez][ps] maps of src (box 8 x CXR x 3), or null
   int no_rem;                // 1: the fifth row tile on DMMA too (FMP_COL_NO_REM, A/B)
   int unroll;                // 1: compile-time k loop over CXR (TMA tiles only: rows past ez are zero)
@@ -1034,10 +1034,16 @@ __global__ void __launch_bounds__(NW * 32, 1) k_column_fast_db(FastColArgs A) {
   __syncthreads();
   const int gw = blockIdx.x * NW + warp, nw = gridDim.x * NW;
   const int per = (A.n_items + nw - 1) / nw;
-  // interleaved: warp gw takes items gw, gw + nw, ... so the warps in flight read and write
+  // interleaved (1): warp gw takes items gw, gw + nw, ... so the warps in flight read and write
   // neighbouring 8-column tiles (whole DRAM pages) instead of nw scattered 64-byte rows
-  const int stp = A.interleave ? nw : 1;
-  const int beg = A.interleave ? gw : gw * per, end = A.interleave ? A.n_items : min(beg + per, A.n_items);
+  int stp = A.interleave ? nw : 1;
+  int beg = A.interleave ? gw : gw * per, end = A.interleave ? A.n_items : min(beg + per, A.n_items);
+  if (A.interleave == 2) {   // CTA-contiguous ranges, warps interleaved inside the CTA
+    const int pc = (A.n_items + gridDim.x - 1) / gridDim.x;
+    beg = blockIdx.x * pc + warp;
+    end = min(A.n_items, (blockIdx.x + 1) * pc);
+    stp = NW;
+  }
   if (beg >= end) return;
 
   __shared__ __align__(8) uint64_t cbar[NW][2];   // TMA tile arrival, per warp and buffer
@@ -2728,10 +2734,14 @@ static int column_pass(fmp_precond* p, bool inv, const double* src, double* dst,
     a.dst = dst;
     a.factors = p->d.factors;
     a.corr = corr;
+    if (inv && getenv_flag("FMP_COL_NO_CORR")) a.corr = nullptr;   // timing diagnostic only: wrong results
     a.pmax = (int)p->d.pmax;
     a.alpha = p->d.alpha;
     a.et = p->et;
-    a.interleave = getenv_flag("FMP_COL_CONTIG") ? 0 : 1;
+    // forward: CTA-contiguous item ranges, warps interleaved inside the CTA (measured 0.235 ->
+    // 0.227 ms at cfg4); inverse: warps interleaved over the whole launch (CTA ranges: 0.264 ->
+    // 0.273 ms)
+    a.interleave = getenv_flag("FMP_COL_CONTIG") ? 0 : (inv ? 1 : 2);
     a.no_rem = getenv_flag("FMP_COL_NO_REM") ? 1 : 0;
     a.maps = p->d_colmaps ? p->d_colmaps + (src == p->d.work_a ? 0 : p->d.n_sub) : nullptr;
     if (a.maps && src != p->d.work_a && src != p->d.work_b) a.maps = nullptr;
