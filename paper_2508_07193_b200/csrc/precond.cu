@@ -1806,6 +1806,7 @@ struct FaceArgs {
   const int* rowmap;           // shape row -> group row maps (fmp_shape::rowmap_off), may be null
   const double* facepad;       // per distinct extent n: [U^T_n, V^T_n] zero-padded to FaceMat<NT> (N x S)
   unsigned char pad_slot[80];  // extent n -> its slot in facepad
+  int bulk_factors;            // 1: k_faces loads the transform factors with bulk copies
 };
 
 __device__ __forceinline__ int ext_of(const SubD& d, int a) { return a == 0 ? d.ex : (a == 1 ? d.ey : d.ez); }
@@ -1958,7 +1959,7 @@ __device__ __forceinline__ void face_plane(const double* pl, int z, int rowstep,
 template <int FR, int FA, int NT>
 __global__ void __launch_bounds__(FACE_THREADS, NT <= 3 ? 4 : (NT <= 5 ? 3 : 1)) k_faces(FaceArgs A) {
   extern __shared__ __align__(128) double smem[];
-  __shared__ __align__(8) uint64_t full[FaceRing<NT>::NS], empty[FaceRing<NT>::NS];
+  __shared__ __align__(8) uint64_t full[FaceRing<NT>::NS], empty[FaceRing<NT>::NS], fbar;
   constexpr int S = FaceMat<NT>::S, W = FaceMat<NT>::WORDS, N = FaceMat<NT>::N;
   constexpr int NS = FaceRing<NT>::NS;
   const int SLOT = face_slot(A.max_ps);
@@ -1979,6 +1980,7 @@ __global__ void __launch_bounds__(FACE_THREADS, NT <= 3 ? 4 : (NT <= 5 ? 3 : 1))
       mbar_init(&full[q], 1);
       mbar_init(&empty[q], FACE_WARPS);
     }
+    mbar_init(&fbar, 1);
     fence_mbar_init();
   }
   // ring, weights and partials zeroed before the first bulk copy: the consumers' unpredicated
@@ -2079,14 +2081,29 @@ __global__ void __launch_bounds__(FACE_THREADS, NT <= 3 ? 4 : (NT <= 5 ? 3 : 1))
     const int ua = f == 0 ? fg.u1 : fg.u2, va = f == 0 ? fg.v1 : fg.v2;
     const int nu = ext[ua], nv_ = ext[va];
     double *sFu = sX, *sFv = sX + W, *sT = sX + 2 * W;
-    face_load_factor<NT>(sFu, A, c, ua, nu, tid, FACE_THREADS);
-    face_load_factor<NT>(sFv, A, c, va, nv_, tid, FACE_THREADS);
+    // the two padded factor matrices as two bulk copies (one round trip); face 1's are issued as
+    // soon as face 0's products are done, under its write-out
+    auto issue_factors = [&](int ff) {
+      const int fu = ff == 0 ? fg.u1 : fg.u2, fv = ff == 0 ? fg.v1 : fg.v2;
+      fence_proxy_async();   // the generic accesses of this region precede the async fill
+      mbar_expect_tx(&fbar, 2u * W * (uint32_t)sizeof(double));
+      bulk_g2s(sFu, A.facepad + (size_t)(2 * A.pad_slot[ext[fu]] + (fu == c ? 0 : 1)) * W, W * sizeof(double), &fbar);
+      bulk_g2s(sFv, A.facepad + (size_t)(2 * A.pad_slot[ext[fv]] + (fv == c ? 0 : 1)) * W, W * sizeof(double), &fbar);
+    };
+    if (A.bulk_factors) {
+      if (f == 0 && tid == 0) issue_factors(0);
+      mbar_wait(&fbar, (uint32_t)f);
+    } else {
+      face_load_factor<NT>(sFu, A, c, ua, nu, tid, FACE_THREADS);
+      face_load_factor<NT>(sFv, A, c, va, nv_, tid, FACE_THREADS);
+    }
     __syncthreads();
     face_mm<NT, false, false>(f == 0 ? sA : sB, sFv, sT, warp, FACE_THREADS / 32, lane);   // T = Proj Fv
     __syncthreads();
     double* E = f == 0 ? sA : sB;                                                  // E = Fu^T T
     face_mm<NT, true, false>(sFu, sT, E, warp, FACE_THREADS / 32, lane);
     __syncthreads();
+    if (A.bulk_factors && f == 0 && tid == 0) issue_factors(1);
     for (int q = tid; q < nu * nv_; q += FACE_THREADS) {
       const int u = q / nv_, vv = q - u * nv_;
       const int row = face_row(c, f, u, vv, ex, ey);
@@ -2960,6 +2977,7 @@ static int precond_apply(fmp_precond* p, const fmp_block* blk, int mode, int par
   const int pm = (int)p->d.pmax;
   FaceArgs fa{p->d.subs, p->d.shapes, p->d.factors, wb, p->d.corr, p->d_ymat, p->d_zmat, pm, (p->max_p + 3) & ~3,
               p->d.rowmap, p->facepad, {}};
+  fa.bulk_factors = getenv_flag("FMP_FACE_NO_BULK") ? 0 : 1;
   memcpy(fa.pad_slot, p->pad_slot, sizeof(fa.pad_slot));
   if (mode != FMP_SOLVE_EXACT) {
     const dim3 fg(3, (unsigned)p->d.n_sub);
