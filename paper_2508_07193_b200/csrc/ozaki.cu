@@ -675,9 +675,16 @@ int ozaki_chunk_lists(std::vector<OzShape>& shapes, std::vector<OzLists>* lists,
     shapes[s].kp0 = plan->kp0 + kl0[s];
     shapes[s].koff = plan->koff + ko0[s];
   }
-  if (getenv_flag("FMP_OZ_VERBOSE"))
-    fprintf(stderr, "ozaki chunk lists: %.3f of the C^-1 slice blocks, %.3f of the MMA work kept%s\n", plan->kept_slices,
-            plan->kept_mma, dense ? " (dense)" : "");
+  if (getenv_flag("FMP_OZ_VERBOSE")) {
+    size_t hist[OZ_S] = {}, pairs = 0;
+    for (uint8_t v : kp) {
+      ++hist[v & 7];
+      pairs += (v & OZ_KP0_PAIR) != 0;
+    }
+    fprintf(stderr, "ozaki chunk lists: %.3f of the C^-1 slice blocks, %.3f of the MMA work kept%s; %zu entries, "
+            "leading zero slices 0..6: %zu %zu %zu %zu %zu %zu %zu; %zu pairs\n", plan->kept_slices, plan->kept_mma,
+            dense ? " (dense)" : "", kp.size(), hist[0], hist[1], hist[2], hist[3], hist[4], hist[5], hist[6], pairs);
+  }
   return 0;
 }
 
