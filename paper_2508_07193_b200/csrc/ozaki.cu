@@ -40,8 +40,6 @@ constexpr int OZ_PART = OZ_MAX_K / OZ_KC;   // max K chunks of one segment
 constexpr int OZ_ABLK = OZ_M * OZ_KC;   // bytes of one A slice block
 constexpr int OZ_STAGE = OZ_S * OZ_ABLK + OZ_RMAX * OZ_KC;
 constexpr int OZ_STAGES = 5;
-constexpr int OZ_PAIR_P0 = 4;           // chunks with >= 4 leading zero slices share a stage in pairs
-constexpr int OZ_KP0_PAIR = 16;         // kp0 flag: this list entry and the next form a pair
 constexpr int OZ_EPI = 8;               // epilogue warps: two per TMEM lane quadrant, each half the column groups
 constexpr int OZ_THREADS = (OZ_EPI + 2) * 32;   // warps 0-7 epilogue, 8 producer, 9 MMA
 constexpr int OZ_TMEM_COLS = 512;
@@ -86,14 +84,13 @@ __device__ __forceinline__ void umma_i8(uint32_t tmem, uint64_t da, uint64_t db,
 // zero rows past the last one) and lands in columns >= 7 W, which no level uses.  W is a template
 // constant so every descriptor and TMEM offset folds to an immediate.
 template <int W, bool REV>
-__device__ __forceinline__ void issue_chunk_order(uint64_t da0, uint64_t db0, uint32_t tmem, bool first, int p0,
-                                                  int ashift = 0) {
+__device__ __forceinline__ void issue_chunk_order(uint64_t da0, uint64_t db0, uint32_t tmem, bool first, int p0) {
   constexpr uint32_t IDESC0 = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(OZ_M >> 4) << 24);
 #pragma unroll
   for (int pi = 1; pi <= OZ_S; ++pi) {
     const int p = REV ? OZ_S + 1 - pi : pi;
     if (p <= p0) continue;   // leading all-zero slices of this chunk: their products are zero
-    const uint64_t da = da0 + (uint64_t)(((p - 1 - ashift) * OZ_ABLK) >> 4);   // ashift: slices stored from p0
+    const uint64_t da = da0 + (uint64_t)(((p - 1) * OZ_ABLK) >> 4);
     const uint32_t acc = (first && p == 1) ? 0u : 1u;
     const int N = oz_pad16((OZ_S + 1 - p) * W);
     // N > 256 is split into near-equal parts (multiples of 16): an MMA costs max(N/2, ~50) cycles,
@@ -150,22 +147,6 @@ __device__ __forceinline__ void issue_chunk(uint64_t da0, uint64_t db0, uint32_t
     issue_chunk_order<W, true>(da0, db0, tmem, false, p0);
 }
 
-// Two sparse chunks in one stage (both with >= OZ_PAIR_P0 leading zero slices; stage layout in
-// the producer): slices P..S-1 of chunk a, then of chunk b, then each chunk's stacked B rows
-// [0, nB) of both 16-byte K halves (LBO nB * 16).  One commit covers both.
-template <int W>
-__device__ __forceinline__ void issue_pair(uint32_t sa, uint32_t tmem, int P) {
-  constexpr int S = OZ_S;
-  const uint32_t nb = (uint32_t)oz_pad16((S - P) * W);
-  const uint32_t abytes = (uint32_t)(S - P) * OZ_ABLK, bbytes = 2u * nb * 16u;
-#pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    const uint64_t da = umma_desc(sa + h * abytes, OZ_M * 16, 128);
-    const uint64_t db = umma_desc(sa + 2 * abytes + h * bbytes, nb * 16, 128);
-    issue_chunk_order<W, true>(da, db, tmem, false, P, P);
-  }
-}
-
 __device__ __forceinline__ void tmem_ld8(uint32_t addr, uint32_t (&v)[8]) {
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
                : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
@@ -182,7 +163,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
   __shared__ uint32_t tmem_base;
   __shared__ int last_flag;
   __shared__ int eb_sh[OZ_WMAX];   // column exponents (+4) of the epilogue's current item
-  __shared__ int stage_p0[OZ_STAGES];   // per stage (producer -> MMA warp): leading zero slices | pair << 4 | last << 5
+  __shared__ int stage_p0[OZ_STAGES];   // leading zero slices of the chunk in each stage (producer -> MMA warp)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(s_u32(&tmem_base)),
@@ -214,40 +195,26 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
         const uint32_t bblk = (uint32_t)sh.R * OZ_KC;
         const int8_t* b = sh.B + (size_t)tl.nt * sh.kchunks * bblk;
         const int base = sh.koff[tl.mt];
-        for (int j = tl.k0; j < tl.k1; ++it) {
-          // an item's first chunk zeroes every level (all slices, alone); later entries flagged as a
-          // pair head share one stage with the next entry of the item
-          const int kc = sh.klist[base + j], f = sh.kp0[base + j];
-          const bool pair = j > tl.k0 && (f & OZ_KP0_PAIR) && j + 1 < tl.k1;
-          const int kc2 = pair ? sh.klist[base + j + 1] : kc;
-          const int p0 = j == tl.k0 ? 0 : (pair ? min(f & 7, sh.kp0[base + j + 1] & 7) : (f & 7));
-          j += pair ? 2 : 1;
+        int kc_n = sh.klist[base + tl.k0], p0_n = sh.kp0[base + tl.k0];   // entry j, fetched one ahead
+        for (int j = tl.k0; j < tl.k1; ++j, ++it) {
+          const int kc = kc_n, p0 = j == tl.k0 ? 0 : p0_n;   // an item's first chunk zeroes every level: all slices
+          if (j + 1 < tl.k1) {
+            kc_n = sh.klist[base + j + 1];
+            p0_n = sh.kp0[base + j + 1];
+          }
           const int s = it % OZ_STAGES;
           const uint32_t ph = (it / OZ_STAGES) & 1;
           mbar_wait(&empty_bar[s], ph ^ 1);
-          stage_p0[s] = p0 | (pair ? 16 : 0) | (j >= tl.k1 ? 32 : 0);   // published by the full barrier's arrive
+          stage_p0[s] = p0;   // published to the MMA warp by the full barrier's arrive
           if (dbg & 1) {   // FMP_OZ_DBG=1 (timing diagnostics only, wrong results): no operand loads
             mbar_arrive(&full_bar[s]);
             continue;
           }
           uint8_t* st = osm + s * OZ_STAGE;
-          const uint32_t abytes = (uint32_t)(OZ_S - p0) * OZ_ABLK;   // slices p0 .. S-1
-          if (!pair) {   // slices land at their usual offsets, the whole stacked B block after them
-            mbar_expect_tx(&full_bar[s], abytes + bblk);
-            bulk_g2s(st + p0 * OZ_ABLK, a + ((size_t)kc * OZ_S + p0) * OZ_ABLK, abytes, &full_bar[s]);
-            bulk_g2s(st + OZ_S * OZ_ABLK, b + (size_t)kc * bblk, bblk, &full_bar[s]);
-          } else {       // issue_pair's layout: A of both chunks, then the B rows [0, nb) they use
-            const uint32_t nb = (uint32_t)oz_pad16((OZ_S - p0) * sh.w), hb = nb * 16u;
-            mbar_expect_tx(&full_bar[s], 2 * abytes + 4 * hb);
-            bulk_g2s(st, a + ((size_t)kc * OZ_S + p0) * OZ_ABLK, abytes, &full_bar[s]);
-            bulk_g2s(st + abytes, a + ((size_t)kc2 * OZ_S + p0) * OZ_ABLK, abytes, &full_bar[s]);
-            uint8_t* bs = st + 2 * abytes;
-            const uint32_t half = (uint32_t)sh.R * 16u;   // global distance of the two 16-byte K halves
-            bulk_g2s(bs, b + (size_t)kc * bblk, hb, &full_bar[s]);
-            bulk_g2s(bs + hb, b + (size_t)kc * bblk + half, hb, &full_bar[s]);
-            bulk_g2s(bs + 2 * hb, b + (size_t)kc2 * bblk, hb, &full_bar[s]);
-            bulk_g2s(bs + 3 * hb, b + (size_t)kc2 * bblk + half, hb, &full_bar[s]);
-          }
+          const uint32_t abytes = (uint32_t)(OZ_S - p0) * OZ_ABLK;   // slices p0 .. S-1 land at their usual offsets
+          mbar_expect_tx(&full_bar[s], abytes + bblk);
+          bulk_g2s(st + p0 * OZ_ABLK, a + ((size_t)kc * OZ_S + p0) * OZ_ABLK, abytes, &full_bar[s]);
+          bulk_g2s(st + OZ_S * OZ_ABLK, b + (size_t)kc * bblk, bblk, &full_bar[s]);
         }
       }
     }
@@ -266,7 +233,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
         if (prof) w_empty += clock64() - t1;
         asm volatile("tcgen05.fence::after_thread_sync;\n");
       }
-      for (bool first = true, last = false; !last; first = false, ++it) {
+      for (int j = tl.k0; j < tl.k1; ++j, ++it) {
         const int s = it % OZ_STAGES;
         const uint32_t ph = (it / OZ_STAGES) & 1;
         if (prof) t1 = clock64();
@@ -274,29 +241,16 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
         if (prof) {
           const long long dt = clock64() - t1;
           w_full += dt;
-          if (first) w_first += dt;
+          if (j == tl.k0) w_first += dt;
         }
         asm volatile("tcgen05.fence::after_thread_sync;\n");
         {
-          const int info = *reinterpret_cast<volatile int*>(&stage_p0[s]);
-          const int p0 = info & 15;
-          last = info & 32;
+          const int p0 = *reinterpret_cast<volatile int*>(&stage_p0[s]);
           const uint32_t sa = s_u32(osm + s * OZ_STAGE);
           const uint64_t da0 = umma_desc(sa, OZ_M * 16, 128);
           const uint64_t db0 = umma_desc(sa + OZ_S * OZ_ABLK, lbo_b, 128);
-          if (info & 16) {   // two sparse chunks in this stage
-            if (!(dbg & 2)) switch (w) {
-              case 8: issue_pair<8>(sa, tmem, p0); break;
-              case 16: issue_pair<16>(sa, tmem, p0); break;
-              case 24: issue_pair<24>(sa, tmem, p0); break;
-              case 32: issue_pair<32>(sa, tmem, p0); break;
-              case 40: issue_pair<40>(sa, tmem, p0); break;
-              case 48: issue_pair<48>(sa, tmem, p0); break;
-              case 56: issue_pair<56>(sa, tmem, p0); break;
-              case 64: issue_pair<64>(sa, tmem, p0); break;
-              default: issue_pair<72>(sa, tmem, p0); break;
-            }
-          } else if (!(dbg & 2)) switch (w) {   // FMP_OZ_DBG=2: no MMAs
+          const bool first = j == tl.k0;
+          if (!(dbg & 2)) switch (w) {   // FMP_OZ_DBG=2: no MMAs
             case 8: issue_chunk<8>(da0, db0, tmem, first, rev, p0); break;
             case 16: issue_chunk<16>(da0, db0, tmem, first, rev, p0); break;
             case 24: issue_chunk<24>(da0, db0, tmem, first, rev, p0); break;
@@ -313,7 +267,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
               break;
           }
           umma_commit(&empty_bar[s]);                 // stage free once these MMAs retire
-          if (last) umma_commit(&tfull_bar);          // accumulators complete
+          if (j == tl.k1 - 1) umma_commit(&tfull_bar);   // accumulators complete
         }
         __syncwarp();
       }
@@ -603,7 +557,7 @@ __global__ void k_ozaki_p0(const int8_t* __restrict__ A, int nchunks, uint8_t* _
 }
 
 int ozaki_chunk_lists(std::vector<OzShape>& shapes, std::vector<OzLists>* lists, OzPlan* plan) {
-  const bool dense = getenv_flag("FMP_OZ_DENSE"), nopair = getenv_flag("FMP_OZ_NOPAIR");
+  const bool dense = getenv_flag("FMP_OZ_DENSE");
   lists->assign(shapes.size(), OzLists{});
   std::vector<uint16_t> kl;
   std::vector<uint8_t> kp;
@@ -645,12 +599,6 @@ int ozaki_chunk_lists(std::vector<OzShape>& shapes, std::vector<OzLists>* lists,
         L.kp0.push_back(0);
         kept += OZ_S;
       }
-      // pair stages: consecutive entries that both skip >= OZ_PAIR_P0 slices share one stage (one
-      // wait, one commit); the kernel pairs a flagged entry with the next unless it starts or ends
-      // an item
-      if (!nopair)
-        for (size_t j = before; j + 1 < L.klist.size(); ++j)
-          if (L.kp0[j] >= OZ_PAIR_P0 && L.kp0[j + 1] >= OZ_PAIR_P0) L.kp0[j++] |= OZ_KP0_PAIR;
       L.koff.push_back((int)L.klist.size());
       total += (size_t)OZ_S * sh.kchunks;
     }
@@ -676,14 +624,11 @@ int ozaki_chunk_lists(std::vector<OzShape>& shapes, std::vector<OzLists>* lists,
     shapes[s].koff = plan->koff + ko0[s];
   }
   if (getenv_flag("FMP_OZ_VERBOSE")) {
-    size_t hist[OZ_S] = {}, pairs = 0;
-    for (uint8_t v : kp) {
-      ++hist[v & 7];
-      pairs += (v & OZ_KP0_PAIR) != 0;
-    }
+    size_t hist[OZ_S] = {};
+    for (uint8_t v : kp) ++hist[v];
     fprintf(stderr, "ozaki chunk lists: %.3f of the C^-1 slice blocks, %.3f of the MMA work kept%s; %zu entries, "
-            "leading zero slices 0..6: %zu %zu %zu %zu %zu %zu %zu; %zu pairs\n", plan->kept_slices, plan->kept_mma,
-            dense ? " (dense)" : "", kp.size(), hist[0], hist[1], hist[2], hist[3], hist[4], hist[5], hist[6], pairs);
+            "leading zero slices 0..6: %zu %zu %zu %zu %zu %zu %zu\n", plan->kept_slices, plan->kept_mma,
+            dense ? " (dense)" : "", kp.size(), hist[0], hist[1], hist[2], hist[3], hist[4], hist[5], hist[6]);
   }
   return 0;
 }
@@ -693,11 +638,11 @@ int ozaki_chunk_lists(std::vector<OzShape>& shapes, std::vector<OzLists>* lists,
 // probe (tools/umma_seq.cu): ~560 cycles per chunk (stage wait, commit, issue floor) plus ~0.3
 // cycles per issued N column (the N/2 tensor rate, partly overlapped), with the same N splits as
 // issue_chunk; every work item adds OZ_ITEM_CYCLES (accumulator drain, pipeline restart).
-constexpr double OZ_ITEM_CYCLES = 8000.0, OZ_CHUNK_FIXED = 560.0;
+constexpr double OZ_ITEM_CYCLES = 8000.0;
 static double chunk_cycles(int w, int p0 = 0) {
   double n_cols = 0.0;
   for (int p = p0 + 1; p <= OZ_S; ++p) n_cols += oz_pad16((OZ_S + 1 - p) * w);
-  return OZ_CHUNK_FIXED + 0.3 * n_cols;
+  return 560.0 + 0.3 * n_cols;
 }
 
 // Work plan of one batched GEMM over the persistent CTAs (data-parallel waves + a stream-K
@@ -722,12 +667,6 @@ int ozaki_build(const std::vector<OzShape>& shapes, const std::vector<OzLists>& 
   // per shape: modelled cycles of a chunk with p0 leading zero slices, and prefix sums of the
   // entry costs over the shape's concatenated lists
   std::vector<std::vector<double>> cyc(shapes.size()), pref(shapes.size());
-  // an entry's cost: the second chunk of a pair stage shares the first one's fixed cost
-  auto entry_cycles = [&](size_t s, size_t e) -> double {
-    const std::vector<uint8_t>& k = klists[s].kp0;
-    const bool tail = e > 0 && (k[e - 1] & OZ_KP0_PAIR);
-    return cyc[s][k[e] & 7] - (tail ? OZ_CHUNK_FIXED : 0.0);
-  };
   int n_tiles = 0;
   for (size_t s = 0; s < shapes.size(); ++s) {
     const OzShape& sh = shapes[s];
@@ -735,7 +674,7 @@ int ozaki_build(const std::vector<OzShape>& shapes, const std::vector<OzLists>& 
     const OzLists& L = klists[s];
     for (int q = 0; q <= OZ_S; ++q) cyc[s].push_back(chunk_cycles(sh.w, std::min(q, OZ_S)));
     pref[s].assign(L.klist.size() + 1, 0.0);
-    for (size_t e = 0; e < L.klist.size(); ++e) pref[s][e + 1] = pref[s][e] + entry_cycles(s, e);
+    for (size_t e = 0; e < L.klist.size(); ++e) pref[s][e + 1] = pref[s][e] + cyc[s][L.kp0[e]];
     const int nts = (sh.n + sh.w - 1) / sh.w;
     for (int mt = 0; mt * OZ_M < sh.m; ++mt) {
       const int ne = L.koff[mt + 1] - L.koff[mt];
@@ -754,7 +693,7 @@ int ozaki_build(const std::vector<OzShape>& shapes, const std::vector<OzLists>& 
     if (k1 <= k0) return 0.0;
     const std::vector<double>& P = pref[r.shape];
     const int base = klists[r.shape].koff[r.mt];
-    return P[base + k1] - P[base + k0] + cyc[r.shape][0] - entry_cycles(r.shape, base + k0);
+    return P[base + k1] - P[base + k0] + cyc[r.shape][0] - cyc[r.shape][klists[r.shape].kp0[base + k0]];
   };
   const int grid = std::min<int>(sms, (int)(shared.size() + solo.size()));
   // sibling teams: when every shared shape has the same number k of column tiles, the waves use
