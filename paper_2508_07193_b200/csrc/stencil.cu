@@ -188,6 +188,7 @@ struct BulkSpmvArgs {
   int64_t nlaunch;               // units handed out by this launch
   double alpha;
   int bnd, tiles_x, tiles_y, L, nzc, ghosts;
+  int wpf;   // modes 1-3: L2 prefetch distance (planes) of the w operand, 0 = off
 };
 
 template <int MODE, int SNSLOT>
@@ -357,6 +358,12 @@ __global__ void __launch_bounds__(STHREADS, SNSLOT <= 4 ? 3 : 2) k_spmv_bulk(con
         const double yx = id ? ex + A.alpha * tx : A.alpha * tx, yy = id ? ey + A.alpha * ty : A.alpha * ty,
                      yz = id ? ez + A.alpha * tz : A.alpha * tz;
         const int64_t oi = fidx(g, 0, k, j, i);
+        if (MODE >= 1 && A.wpf > 0 && k + A.wpf < g.bz) {   // w of a later plane of this column into L2
+          const double* wn = A.w + oi + (int64_t)A.wpf * g.bx * g.by;
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(wn));
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(wn + V));
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(wn + 2 * V));
+        }
         if (MODE == 3) {
           const double rx = A.w[oi] - yx, ry = A.w[oi + V] - yy, rz = A.w[oi + 2 * V] - yz;
           acc0 += rx * rx + ry * ry + rz * rz;
@@ -618,6 +625,10 @@ static int stencil_apply(const fmp_block* blk, double alpha, int boundary, int m
     a.tiles_y = (g.by + SY - 1) / SY;
     a.ghosts = 0;
     for (int q = 0; q < 6; ++q) a.ghosts |= g.ghost[q] != nullptr;
+    // the w operand of the fused dots / residual is read per point after the stencil, so its DRAM
+    // latency sits in every consumer step; prefetching the next plane's w into L2 hides it
+    // (bench.py: 2434 -> 2463 MDoF/s at cfg4; FMP_SPMV_WPF=0 turns it off)
+    a.wpf = getenv("FMP_SPMV_WPF") ? atoi(getenv("FMP_SPMV_WPF")) : 1;
     // [fetch, done] counter pairs of the unit scheduler, zero at rest (each launch re-arms its
     // own pair).  A ring of pairs, so launches in flight on different streams or devices of this
     // process never share one (per device: the ring is allocated on the current device).
