@@ -2104,10 +2104,26 @@ __global__ void __launch_bounds__(FACE_THREADS, NT <= 3 ? 4 : (NT <= 5 ? 3 : 1))
     face_mm<NT, true, false>(sFu, sT, E, warp, FACE_THREADS / 32, lane);
     __syncthreads();
     if (A.bulk_factors && f == 0 && tid == 0) issue_factors(1);
-    for (int q = tid; q < nu * nv_; q += FACE_THREADS) {
-      const int u = q / nv_, vv = q - u * nv_;
-      const int row = face_row(c, f, u, vv, ex, ey);
-      if (row >= 0) Y[rm ? rm[base + row] : base + row] = E[u * S + vv];
+    if (rm) {   // every row-map read of this thread first, then the stores (one round trip)
+      constexpr int GQ = (N * N + FACE_THREADS - 1) / FACE_THREADS;
+      int yi[GQ];
+#pragma unroll
+      for (int i = 0; i < GQ; ++i) {
+        const int q = tid + i * FACE_THREADS, u = q / nv_, vv = q - u * nv_;
+        const int row = q < nu * nv_ ? face_row(c, f, u, vv, ex, ey) : -1;
+        yi[i] = row < 0 ? -1 : rm[base + row];
+      }
+#pragma unroll
+      for (int i = 0; i < GQ; ++i) {
+        const int q = tid + i * FACE_THREADS, u = q / nv_, vv = q - u * nv_;
+        if (yi[i] >= 0) Y[yi[i]] = E[u * S + vv];
+      }
+    } else {
+      for (int q = tid; q < nu * nv_; q += FACE_THREADS) {
+        const int u = q / nv_, vv = q - u * nv_;
+        const int row = face_row(c, f, u, vv, ex, ey);
+        if (row >= 0) Y[base + row] = E[u * S + vv];
+      }
     }
     __syncthreads();
   }
@@ -2140,12 +2156,41 @@ __global__ void __launch_bounds__(FACE_THREADS) k_corr(FaceArgs A) {
   {
     const int ua = f == 0 ? fg.u1 : fg.u2, va = f == 0 ? fg.v1 : fg.v2;
     const int nu = ext[ua], nv = ext[va];
-    face_load_factor<NT>(sFu, A, c, ua, nu, tid, FACE_THREADS);
-    face_load_factor<NT>(sFv, A, c, va, nv, tid, FACE_THREADS);
-    for (int q = tid; q < W; q += FACE_THREADS) {
-      const int u = q / S, v = q - u * S;
-      const int row = (u < nu && v < nv) ? face_row(c, f, u, v, ex, ey) : -1;
-      sZ[q] = row < 0 ? 0.0 : Z[rm ? rm[base + row] : base + row];
+    if (A.bulk_factors) {   // both factors by bulk copy, in flight during the Z gather below
+      __shared__ __align__(8) uint64_t fbar;
+      if (tid == 0) {
+        mbar_init(&fbar, 1);
+        fence_mbar_init();
+        mbar_expect_tx(&fbar, 2u * W * (uint32_t)sizeof(double));
+        bulk_g2s(sFu, A.facepad + (size_t)(2 * A.pad_slot[nu] + (ua == c ? 0 : 1)) * W, W * sizeof(double), &fbar);
+        bulk_g2s(sFv, A.facepad + (size_t)(2 * A.pad_slot[nv] + (va == c ? 0 : 1)) * W, W * sizeof(double), &fbar);
+      }
+      // the face's Z values: every row-map read of this thread first, then every Z read (two
+      // round trips in all instead of two per element)
+      constexpr int GQ = (W + FACE_THREADS - 1) / FACE_THREADS;
+      int zi[GQ];
+#pragma unroll
+      for (int i = 0; i < GQ; ++i) {
+        const int q = tid + i * FACE_THREADS, u = q / S, v = q - u * S;
+        const int row = (q < W && u < nu && v < nv) ? face_row(c, f, u, v, ex, ey) : -1;
+        zi[i] = row < 0 ? -1 : (rm ? rm[base + row] : base + row);
+      }
+      double zv[GQ];
+#pragma unroll
+      for (int i = 0; i < GQ; ++i) zv[i] = zi[i] < 0 ? 0.0 : Z[zi[i]];
+#pragma unroll
+      for (int i = 0; i < GQ; ++i)
+        if (tid + i * FACE_THREADS < W) sZ[tid + i * FACE_THREADS] = zv[i];
+      __syncthreads();   // fbar's initialisation is visible before anyone waits on it
+      mbar_wait(&fbar, 0);
+    } else {
+      face_load_factor<NT>(sFu, A, c, ua, nu, tid, FACE_THREADS);
+      face_load_factor<NT>(sFv, A, c, va, nv, tid, FACE_THREADS);
+      for (int q = tid; q < W; q += FACE_THREADS) {
+        const int u = q / S, v = q - u * S;
+        const int row = (u < nu && v < nv) ? face_row(c, f, u, v, ex, ey) : -1;
+        sZ[q] = row < 0 ? 0.0 : Z[rm ? rm[base + row] : base + row];
+      }
     }
     __syncthreads();
     face_mm<NT, false, true>(sZ, sFv, sT, warp, FACE_THREADS / 32, lane);    // T[u][tv] = sum_v Z[u][v] Fv[tv][v]
