@@ -392,10 +392,28 @@ __device__ __forceinline__ void ozaki_write_digits(const OzSlice& o, const doubl
   uint32_t w[OZ_S][4];
 #pragma unroll
   for (int p = 0; p < OZ_S; ++p) w[p][0] = w[p][1] = w[p][2] = w[p][3] = 0u;
+  // the group's 16 values first (read-only loads: all in flight before the digit arithmetic)
+  double xs[16];
+  if (KPERM && valid && gk * 16 + 15 < o.kvalid) {
+    int kp[16];
+    const int4* k4 = reinterpret_cast<const int4*>(o.kperm + gk * 16);   // kperm is 64-byte aligned per group
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int4 t = __ldg(k4 + q);
+      kp[4 * q] = t.x; kp[4 * q + 1] = t.y; kp[4 * q + 2] = t.z; kp[4 * q + 3] = t.w;
+    }
+#pragma unroll
+    for (int j = 0; j < 16; ++j) xs[j] = __ldg(srow + kp[j]);
+  } else {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const int k = gk * 16 + j;
+      xs[j] = (valid && k < o.kvalid) ? __ldg(srow + (KPERM ? __ldg(o.kperm + k) : k)) : 0.0;
+    }
+  }
 #pragma unroll
   for (int j = 0; j < 16; ++j) {
-    const int k = gk * 16 + j;
-    const double x = (valid && k < o.kvalid) ? srow[KPERM ? o.kperm[k] : k] : 0.0;
+    const double x = xs[j];
     long long V = llrint(ldexp(x, 8 * OZ_S - 2 - e));   // |V| <= 2^(8S-2)
 #pragma unroll
     for (int p = OZ_S - 1; p >= 0; --p) {                // balanced base-256 digits, least significant first
@@ -429,7 +447,22 @@ __global__ void __launch_bounds__(OZ_SLICE_THREADS) k_ozaki_slice_rows(const OzS
   double mx = 0.0;
   if (valid) {
     const double* src = o.src + (size_t)(o.rperm ? o.rperm[r] : r) * o.ld;   // the max is order-independent
-    for (int k = threadIdx.x; k < o.kvalid; k += blockDim.x) mx = fmax(mx, fabs(src[k]));
+    // eight independent loads in flight per thread (the row is read once from DRAM here)
+    constexpr int U = 8;
+    double m8[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) m8[u] = 0.0;
+    int k = threadIdx.x;
+    for (; k + (U - 1) * OZ_SLICE_THREADS < o.kvalid; k += U * OZ_SLICE_THREADS) {
+      double v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) v[u] = src[k + u * OZ_SLICE_THREADS];
+#pragma unroll
+      for (int u = 0; u < U; ++u) m8[u] = fmax(m8[u], fabs(v[u]));
+    }
+    for (; k < o.kvalid; k += OZ_SLICE_THREADS) mx = fmax(mx, fabs(src[k]));
+#pragma unroll
+    for (int u = 0; u < U; ++u) mx = fmax(mx, m8[u]);
   }
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, off));
