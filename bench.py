@@ -197,10 +197,14 @@ def stage_rooflines(prec, x, z, specs, peaks, reps):
     kernels on the launching stream (fmp_precond_profile), averaged over `reps` applies, with
     each kernel's algorithmic work and roofline ("Kernels")."""
     from paper_2508_07193_b200.plan import correction_counts
+    import torch
     plan = prec.plan
     plan.profile(True)
     acc = {}
     for _ in range(reps):
+        # keep the GPU busy (~1 ms spin) while the host enqueues the apply: otherwise the first
+        # stage's interval (event 0 -> end of k_plane_fast<0>) also holds the host's launch latency
+        torch.cuda._sleep(2_000_000)
         prec.apply_into(x, z)
         for k, v in plan.stage_ms().items():
             acc[k] = acc.get(k, 0.0) + v / reps

@@ -1,6 +1,7 @@
 // Shared device helpers for libflashmp_b200 (sm_100a).
 #pragma once
 #include <atomic>
+#include <utility>
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
@@ -38,6 +39,39 @@ inline bool getenv_flag(const char* name) {
 }
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// ---------------------------------------------------------------- programmatic dependent launch
+// The hot-path kernels are launched with programmatic stream serialisation: a kernel may start
+// (its CTAs load their resident factor tables, initialise barriers, prefetch tensor maps) while
+// its predecessor on the stream is still finishing, and blocks in pdl_wait() until the
+// predecessor has completed and its writes are visible.  Every kernel launched by launch_pdl()
+// calls pdl_wait() in every CTA before touching data another kernel writes (and before its own
+// global writes), so completion stays transitively ordered along the stream.  pdl_trigger()
+// lets the successor launch once every CTA of this grid has started.  FMP_NO_PDL=1: ordinary
+// launches (A/B).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" :::); }
+
+inline bool pdl_on() {
+  static const bool on = !getenv_flag("FMP_NO_PDL");
+  return on;
+}
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args&&... args) {
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_on() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 constexpr int kNumSM = 148;
 // Fixed persistent-grid sizes keep every reduction's partial order independent of n.

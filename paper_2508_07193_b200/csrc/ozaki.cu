@@ -183,6 +183,8 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;\n");
   const uint32_t tmem = tmem_base;
+  pdl_trigger();
+  pdl_wait();   // TMEM and barriers are set up under the slicing kernel's tail; its Y slices are read below
 
   if (warp == OZ_EPI) {
     // ---------------- producer: two bulk copies per stage
@@ -439,6 +441,8 @@ constexpr int OZ_SLICE_THREADS = 512;
 __global__ void __launch_bounds__(OZ_SLICE_THREADS) k_ozaki_slice_rows(const OzSlice* __restrict__ sl, int count) {
   __shared__ double red[OZ_SLICE_THREADS / 32];
   __shared__ int e_sh;
+  pdl_trigger();
+  pdl_wait();   // Y is the faces kernel's output
   int si = 0;
   while (si + 1 < count && sl[si + 1].prow0 <= (int64_t)blockIdx.x) ++si;
   const OzSlice o = sl[si];
@@ -501,7 +505,7 @@ void ozaki_plan_slices(OzSlice* s, int count, int64_t* rows, int64_t* threads) {
 
 int ozaki_slice(const OzSlice* d_slices, int count, int64_t rows, int64_t padded_rows, cudaStream_t st) {
   if (count <= 0 || rows <= 0) return 0;
-  k_ozaki_slice_rows<<<(unsigned)padded_rows, OZ_SLICE_THREADS, 0, st>>>(d_slices, count);
+  FMP_CHECK_CUDA(launch_pdl(k_ozaki_slice_rows, (unsigned)padded_rows, OZ_SLICE_THREADS, 0, st, d_slices, count));
   FMP_CHECK_LAUNCH();
   return 0;
 }
@@ -534,8 +538,8 @@ int ozaki_launch(const OzPlan& p, cudaStream_t st) {
   if (p.grid <= 0) return 0;
   if (!g_oz_prof && getenv_flag("FMP_OZ_PROF")) FMP_CHECK_CUDA(cudaMalloc(&g_oz_prof, 4096 * 8 * sizeof(long long)));
   static const int dbg = getenv("FMP_OZ_DBG") ? atoi(getenv("FMP_OZ_DBG")) : 0;
-  k_ozaki<<<p.grid, OZ_THREADS, OZ_STAGES * OZ_STAGE, st>>>(p.shapes, p.items, p.offs, p.zpart, p.counters,
-                                                            g_oz_prof, dbg);
+  FMP_CHECK_CUDA(launch_pdl(k_ozaki, p.grid, OZ_THREADS, OZ_STAGES * OZ_STAGE, st, p.shapes, p.items, p.offs,
+                            p.zpart, p.counters, g_oz_prof, dbg));
   FMP_CHECK_LAUNCH();
   return 0;
 }

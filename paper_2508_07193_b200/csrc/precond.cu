@@ -685,6 +685,8 @@ __global__ void __launch_bounds__(PW_WARPS * 32, 1) k_plane_fast(const __grid_co
   uint32_t tphase = 0;
   // TMA destinations must be 128-byte aligned (RES_WORDS and PX_BUF keep the warp buffers so)
   const bool tma_ok = !INV && A.tma_rows > 0 && (s_u32(T) & 127) == 0;
+  pdl_trigger();
+  pdl_wait();   // factors are resident; the source field is the previous kernel's output
   __syncthreads();
   const int gw = blockIdx.x * PW_WARPS + warp, nw = gridDim.x * PW_WARPS;
   const int per = (A.n_items + nw - 1) / nw;
@@ -1031,6 +1033,8 @@ __global__ void __launch_bounds__(NW * 32, 1) k_column_fast_db(FastColArgs A) {
   load_resident(smem, A.et, A.factors, tid, blockDim.x);
   double* wbase = smem + RES_WORDS + warp * NB * CX_BUF;
   for (int q = lane; q < NB * CX_BUF; q += 32) wbase[q] = 0.0;
+  pdl_trigger();
+  pdl_wait();   // factors are resident; the source tiles are the previous kernel's output
   __syncthreads();
   const int gw = blockIdx.x * NW + warp, nw = gridDim.x * NW;
   const int per = (A.n_items + nw - 1) / nw;
@@ -1987,6 +1991,8 @@ __global__ void __launch_bounds__(FACE_THREADS, NT <= 3 ? 4 : (NT <= 5 ? 3 : 1))
   // loads of points outside a plane may reach past its slot (face_plane)
   for (int q = tid; q < NS * SLOT + 3 * N + FACE_WARPS * FZ * N; q += FACE_THREADS) ring[q] = 0.0;
   fence_proxy_async();   // these generic writes precede the async-proxy fills of the ring
+  pdl_trigger();
+  pdl_wait();   // y^ is the forward column pass's output
   const FaceGeo fg = face_geo(c);
   const bool zn = fg.n1 == 2, yn = fg.n1 == 1 || fg.n2 == 1, xn = fg.n2 == 0;
   double* sY = fg.n1 == 1 ? sA : sB;   // y-normal destination [z][a]
@@ -2151,6 +2157,7 @@ __global__ void __launch_bounds__(FACE_THREADS) k_corr(FaceArgs A) {
   const FaceGeo fg = face_geo(c);
   const double* Z = A.zmat[d.shape] + (int64_t)d.column * sh.ld;
   const int* rm = sh.rowmap_off >= 0 ? A.rowmap + sh.rowmap_off : nullptr;
+  pdl_trigger();
   int base = 0;
   for (int q = 0; q < c; ++q) base += (int)sh.m_comp[q];
   {
@@ -2175,6 +2182,7 @@ __global__ void __launch_bounds__(FACE_THREADS) k_corr(FaceArgs A) {
         const int row = (q < W && u < nu && v < nv) ? face_row(c, f, u, v, ex, ey) : -1;
         zi[i] = row < 0 ? -1 : (rm ? rm[base + row] : base + row);
       }
+      pdl_wait();   // factors and row map are constant; Z is the GEMM's output
       double zv[GQ];
 #pragma unroll
       for (int i = 0; i < GQ; ++i) zv[i] = zi[i] < 0 ? 0.0 : Z[zi[i]];
@@ -2184,6 +2192,7 @@ __global__ void __launch_bounds__(FACE_THREADS) k_corr(FaceArgs A) {
       __syncthreads();   // fbar's initialisation is visible before anyone waits on it
       mbar_wait(&fbar, 0);
     } else {
+      pdl_wait();
       face_load_factor<NT>(sFu, A, c, ua, nu, tid, FACE_THREADS);
       face_load_factor<NT>(sFv, A, c, va, nv, tid, FACE_THREADS);
       for (int q = tid; q < W; q += FACE_THREADS) {
@@ -2815,7 +2824,8 @@ static int column_pass(fmp_precond* p, bool inv, const double* src, double* dst,
       const bool small = std::max(p->max_ex, std::max(p->max_ey, p->max_ez)) <= 24;
       const int nwarp = inv ? CW_WARPS_INV : CW_WARPS_FWD;
       const int grid = std::min(p->sms, (p->n_fcol + nwarp - 1) / nwarp);
-#define FMP_COLF(I, S) k_column_fast_db<I, I ? CW_WARPS_INV : CW_WARPS_FWD, S><<<grid, nwarp * 32, col_db_smem(nwarp), st>>>(a);
+#define FMP_COLF(I, S) \
+  FMP_CHECK_CUDA(launch_pdl(k_column_fast_db<I, I ? CW_WARPS_INV : CW_WARPS_FWD, S>, grid, nwarp * 32, col_db_smem(nwarp), st, a));
       if (inv && small) { FMP_COLF(true, 3) }
       else if (inv) { FMP_COLF(true, 5) }
       else if (small) { FMP_COLF(false, 3) }
@@ -2923,13 +2933,13 @@ static int plane_pass(fmp_precond* p, const fmp_block* blk, bool inv, int mode, 
     const int grid = std::min(p->sms, (a.n_items + PW_WARPS - 1) / PW_WARPS);
     const bool small = std::max(p->max_ex, std::max(p->max_ey, p->max_ez)) <= 24;
     if (inv && small)
-      k_plane_fast<true, 3><<<grid, PW_WARPS * 32, kPlaneFastSmem, st>>>(tm, a);
+      FMP_CHECK_CUDA(launch_pdl(k_plane_fast<true, 3>, grid, PW_WARPS * 32, kPlaneFastSmem, st, tm, a));
     else if (inv)
-      k_plane_fast<true><<<grid, PW_WARPS * 32, kPlaneFastSmem, st>>>(tm, a);
+      FMP_CHECK_CUDA(launch_pdl(k_plane_fast<true>, grid, PW_WARPS * 32, kPlaneFastSmem, st, tm, a));
     else if (small)
-      k_plane_fast<false, 3><<<grid, PW_WARPS * 32, kPlaneFastSmem, st>>>(tm, a);
+      FMP_CHECK_CUDA(launch_pdl(k_plane_fast<false, 3>, grid, PW_WARPS * 32, kPlaneFastSmem, st, tm, a));
     else
-      k_plane_fast<false><<<grid, PW_WARPS * 32, kPlaneFastSmem, st>>>(tm, a);
+      FMP_CHECK_CUDA(launch_pdl(k_plane_fast<false>, grid, PW_WARPS * 32, kPlaneFastSmem, st, tm, a));
     FMP_CHECK_LAUNCH();
     return 0;
   }
@@ -3028,11 +3038,11 @@ static int precond_apply(fmp_precond* p, const fmp_block* blk, int mode, int par
     const dim3 fg(3, (unsigned)p->d.n_sub);
     const int slot = face_slot(fa.max_ps);
     if (pm <= 24)   // 16^3-class subdomains: 3 DMMA tiles per padded extent
-      k_faces<3, 1, 3><<<fg, FACE_THREADS, face_smem_bytes<3>(slot), st>>>(fa);
+      FMP_CHECK_CUDA(launch_pdl(k_faces<3, 1, 3>, fg, FACE_THREADS, face_smem_bytes<3>(slot), st, fa));
     else if (pm <= 40)
-      k_faces<5, 2, 5><<<fg, FACE_THREADS, face_smem_bytes<5>(slot), st>>>(fa);
+      FMP_CHECK_CUDA(launch_pdl(k_faces<5, 2, 5>, fg, FACE_THREADS, face_smem_bytes<5>(slot), st, fa));
     else
-      k_faces<9, 3, 9><<<fg, FACE_THREADS, face_smem_bytes<9>(slot), st>>>(fa);
+      FMP_CHECK_CUDA(launch_pdl(k_faces<9, 3, 9>, fg, FACE_THREADS, face_smem_bytes<9>(slot), st, fa));
     FMP_CHECK_LAUNCH();
   }
   mark(3);
@@ -3070,11 +3080,11 @@ static int precond_apply(fmp_precond* p, const fmp_block* blk, int mode, int par
     }
     mark(5);
     if (pm <= 24)
-      k_corr<3><<<dim3(6, (unsigned)p->d.n_sub), FACE_THREADS, 4 * FaceMat<3>::WORDS * sizeof(double), st>>>(fa);
+      FMP_CHECK_CUDA(launch_pdl(k_corr<3>, dim3(6, (unsigned)p->d.n_sub), FACE_THREADS, 4 * FaceMat<3>::WORDS * sizeof(double), st, fa));
     else if (pm <= 40)
-      k_corr<5><<<dim3(6, (unsigned)p->d.n_sub), FACE_THREADS, 4 * FaceMat<5>::WORDS * sizeof(double), st>>>(fa);
+      FMP_CHECK_CUDA(launch_pdl(k_corr<5>, dim3(6, (unsigned)p->d.n_sub), FACE_THREADS, 4 * FaceMat<5>::WORDS * sizeof(double), st, fa));
     else
-      k_corr<9><<<dim3(6, (unsigned)p->d.n_sub), FACE_THREADS, 4 * FaceMat<9>::WORDS * sizeof(double), st>>>(fa);
+      FMP_CHECK_CUDA(launch_pdl(k_corr<9>, dim3(6, (unsigned)p->d.n_sub), FACE_THREADS, 4 * FaceMat<9>::WORDS * sizeof(double), st, fa));
     FMP_CHECK_LAUNCH();
   }
   mark(6);

@@ -211,6 +211,8 @@ __global__ void __launch_bounds__(STHREADS, SNSLOT <= 4 ? 3 : 2) k_spmv_bulk(con
     }
     fence_mbar_init();
   }
+  pdl_trigger();
+  pdl_wait();   // x (and the scheduler counters) belong to the previous kernels on the stream
   __syncthreads();
   auto nplanes = [&](int64_t u) { return min(A.L, g.bz - (int)(u / ntiles) * A.L); };
 
@@ -452,6 +454,8 @@ __global__ void __launch_bounds__(CBX* CBY) k_curl(Geo g, const double* __restri
 // R = E + dt*curl_b(H) - alpha*(C_b C_f E), alpha = dt^2/4  (ref:cn_driver.py:54-59)
 __global__ void __launch_bounds__(CBX* CBY) k_cn_rhs(Geo gE, Geo gH, double dt, const double* __restrict__ E,
                                                     const double* __restrict__ H, double* __restrict__ R) {
+  pdl_trigger();
+  pdl_wait();
   const int i = blockIdx.x * CBX + threadIdx.x, j = blockIdx.y * CBY + threadIdx.y, k = blockIdx.z;
   if (i >= gE.bx || j >= gE.by) return;
   const double alpha = dt * dt / 4.0;
@@ -477,6 +481,8 @@ __global__ void __launch_bounds__(CBX* CBY) k_cn_rhs(Geo gE, Geo gH, double dt, 
 __global__ void __launch_bounds__(CBX* CBY) k_cn_h(Geo gN, Geo gO, double hdt, const double* __restrict__ H,
                                                   const double* __restrict__ En, const double* __restrict__ Eo,
                                                   double* __restrict__ Hn) {
+  pdl_trigger();
+  pdl_wait();
   const int i = blockIdx.x * CBX + threadIdx.x, j = blockIdx.y * CBY + threadIdx.y, k = blockIdx.z;
   if (i >= gN.bx || j >= gN.by) return;
   double ax, ay, az, bx, by, bz;
@@ -669,10 +675,10 @@ static int stencil_apply(const fmp_block* blk, double alpha, int boundary, int m
     if (int e = encode_tensor_map_f64(&tm, x, 4, dims, strides, box)) return e;
 #define FMP_SPMV_GO(N)                                                                                   \
   switch (mode) {                                                                                        \
-    case 0: k_spmv_bulk<0, N><<<grid, STHREADS, spmv_bulk_smem(N), st>>>(tm, a); break;                  \
-    case 1: k_spmv_bulk<1, N><<<grid, STHREADS, spmv_bulk_smem(N), st>>>(tm, a); break;                  \
-    case 2: k_spmv_bulk<2, N><<<grid, STHREADS, spmv_bulk_smem(N), st>>>(tm, a); break;                  \
-    case 3: k_spmv_bulk<3, N><<<grid, STHREADS, spmv_bulk_smem(N), st>>>(tm, a); break;                  \
+    case 0: FMP_CHECK_CUDA(launch_pdl(k_spmv_bulk<0, N>, grid, STHREADS, spmv_bulk_smem(N), st, tm, a)); break;                \
+    case 1: FMP_CHECK_CUDA(launch_pdl(k_spmv_bulk<1, N>, grid, STHREADS, spmv_bulk_smem(N), st, tm, a)); break;                \
+    case 2: FMP_CHECK_CUDA(launch_pdl(k_spmv_bulk<2, N>, grid, STHREADS, spmv_bulk_smem(N), st, tm, a)); break;                \
+    case 3: FMP_CHECK_CUDA(launch_pdl(k_spmv_bulk<3, N>, grid, STHREADS, spmv_bulk_smem(N), st, tm, a)); break;                \
   }
     if (ns == 4) {
       FMP_SPMV_GO(4)
@@ -722,7 +728,7 @@ extern "C" int fmp_cn_rhs(const fmp_block* blkE, const fmp_block* blkH, double d
   if (int e = check_block(blkE)) return e;
   const Geo gE = make_geo(blkE), gH = make_geo(blkH);
   const dim3 grid((gE.bx + CBX - 1) / CBX, (gE.by + CBY - 1) / CBY, gE.bz), block(CBX, CBY);
-  k_cn_rhs<<<grid, block, 0, as_stream(stream)>>>(gE, gH, dt, E, H, R);
+  FMP_CHECK_CUDA(launch_pdl(k_cn_rhs, grid, block, 0, as_stream(stream), gE, gH, dt, E, H, R));
   FMP_CHECK_LAUNCH();
   return 0;
 }
@@ -732,7 +738,7 @@ extern "C" int fmp_cn_h_update(const fmp_block* blkNew, const fmp_block* blkOld,
   if (int e = check_block(blkNew)) return e;
   const Geo gN = make_geo(blkNew), gO = make_geo(blkOld);
   const dim3 grid((gN.bx + CBX - 1) / CBX, (gN.by + CBY - 1) / CBY, gN.bz), block(CBX, CBY);
-  k_cn_h<<<grid, block, 0, as_stream(stream)>>>(gN, gO, 0.5 * dt, H, E_new, E_old, H_new);
+  FMP_CHECK_CUDA(launch_pdl(k_cn_h, grid, block, 0, as_stream(stream), gN, gO, 0.5 * dt, H, E_new, E_old, H_new));
   FMP_CHECK_LAUNCH();
   return 0;
 }

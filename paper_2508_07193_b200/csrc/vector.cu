@@ -24,6 +24,8 @@ void set_error(const char* fmt, ...) {
 // ---------------------------------------------------------------- reduction tail
 template <int ND>
 __global__ void __launch_bounds__(1024) k_finish(const double* __restrict__ partials, int count, double* out) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ double red[32];
 #pragma unroll
   for (int q = 0; q < ND; ++q) {
@@ -36,9 +38,9 @@ __global__ void __launch_bounds__(1024) k_finish(const double* __restrict__ part
 
 int finish_reduce(const double* partials, int count, int nd, double* out, cudaStream_t st) {
   if (nd == 1)
-    k_finish<1><<<1, 1024, 0, st>>>(partials, count, out);
+    FMP_CHECK_CUDA(launch_pdl(k_finish<1>, 1, 1024, 0, st, partials, count, out));
   else
-    k_finish<2><<<1, 1024, 0, st>>>(partials, count, out);
+    FMP_CHECK_CUDA(launch_pdl(k_finish<2>, 1, 1024, 0, st, partials, count, out));
   FMP_CHECK_LAUNCH();
   return 0;
 }
@@ -46,22 +48,30 @@ int finish_reduce(const double* partials, int count, int nd, double* out, cudaSt
 // ---------------------------------------------------------------- elementwise
 __global__ void k_lincomb(int64_t n, double a, const double* __restrict__ x, double b, const double* __restrict__ y,
                           double* __restrict__ out) {
+  pdl_trigger();
+  pdl_wait();
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x)
     out[q] = add_rn(mul_rn(a, x[q]), mul_rn(b, y[q]));
 }
 
 __global__ void k_axpy(int64_t n, double a, const double* __restrict__ x, double* __restrict__ y) {
+  pdl_trigger();
+  pdl_wait();
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x)
     y[q] = add_rn(y[q], mul_rn(a, x[q]));
 }
 
 __global__ void k_scale(int64_t n, double a, const double* __restrict__ x, double* __restrict__ out) {
+  pdl_trigger();
+  pdl_wait();
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x)
     out[q] = mul_rn(a, x[q]);
 }
 
 __global__ void __launch_bounds__(kVecThreads) k_dot(int64_t n, const double* __restrict__ x,
                                                      const double* __restrict__ y, double* __restrict__ partials) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ double red[kVecThreads / 32];
   double acc = 0.0;
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x)
@@ -73,6 +83,8 @@ __global__ void __launch_bounds__(kVecThreads) k_dot(int64_t n, const double* __
 // p = 1.0*r + beta*(1.0*p + (-omega)*v)     (ref:krylov.py:181-182)
 __global__ void k_bicg_p(int64_t n, const double* __restrict__ r, double* __restrict__ p,
                          const double* __restrict__ v, double beta, double momega) {
+  pdl_trigger();
+  pdl_wait();
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x) {
     const double p1 = add_rn(p[q], mul_rn(momega, v[q]));
     p[q] = add_rn(r[q], mul_rn(beta, p1));
@@ -88,6 +100,8 @@ __global__ void __launch_bounds__(kVecThreads) k_bicg_xr(int64_t n, double* __re
                                                          const double* __restrict__ t, double* __restrict__ r,
                                                          const double* __restrict__ rs, double alpha,
                                                          double omega, double* __restrict__ partials) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ double red[kVecThreads / 32];
   double acc = 0.0;
   const double momega = -omega;
@@ -107,6 +121,8 @@ __global__ void __launch_bounds__(kVecThreads) k_bicg_xr(int64_t n, double* __re
 __global__ void __launch_bounds__(kVecThreads) k_axpy_dot(int64_t n, double a, const double* __restrict__ x,
                                                           double* y, const double* z,
                                                           double* __restrict__ partials) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ double red[kVecThreads / 32];
   double acc = 0.0;
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x) {
@@ -129,6 +145,8 @@ struct CombineArgs {
 // x and out alias for every chunk after the first (fmp_vec_combine, k > kCombineMax): no
 // __restrict__ on them; each element is read before it is written by the same thread.
 __global__ void k_combine(int64_t n, const double* x, const CombineArgs A, double* out) {
+  pdl_trigger();
+  pdl_wait();
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x) {
     double t = x[q];
     for (int i = 0; i < A.k; ++i) t = add_rn(t, mul_rn(A.c[i], A.v[i][q]));
@@ -161,21 +179,21 @@ extern "C" int64_t fmp_launch_count(void) { return g_launches.load(); }
 extern "C" int fmp_vec_lincomb(int64_t n, double a, const double* x, double b, const double* y, double* out,
                                void* stream) {
   if (n <= 0) return 0;
-  k_lincomb<<<vec_grid(n), kVecThreads, 0, as_stream(stream)>>>(n, a, x, b, y, out);
+  FMP_CHECK_CUDA(launch_pdl(k_lincomb, vec_grid(n), kVecThreads, 0, as_stream(stream), n, a, x, b, y, out));
   FMP_CHECK_LAUNCH();
   return 0;
 }
 
 extern "C" int fmp_vec_axpy(int64_t n, double a, const double* x, double* y, void* stream) {
   if (n <= 0) return 0;
-  k_axpy<<<vec_grid(n), kVecThreads, 0, as_stream(stream)>>>(n, a, x, y);
+  FMP_CHECK_CUDA(launch_pdl(k_axpy, vec_grid(n), kVecThreads, 0, as_stream(stream), n, a, x, y));
   FMP_CHECK_LAUNCH();
   return 0;
 }
 
 extern "C" int fmp_vec_scale(int64_t n, double a, const double* x, double* out, void* stream) {
   if (n <= 0) return 0;
-  k_scale<<<vec_grid(n), kVecThreads, 0, as_stream(stream)>>>(n, a, x, out);
+  FMP_CHECK_CUDA(launch_pdl(k_scale, vec_grid(n), kVecThreads, 0, as_stream(stream), n, a, x, out));
   FMP_CHECK_LAUNCH();
   return 0;
 }
@@ -183,7 +201,7 @@ extern "C" int fmp_vec_scale(int64_t n, double a, const double* x, double* out, 
 extern "C" int fmp_vec_dot(int64_t n, const double* x, const double* y, double* out, double* scratch, void* stream) {
   const int grid = vec_grid(n);
   cudaStream_t st = as_stream(stream);
-  k_dot<<<grid, kVecThreads, 0, st>>>(n, x, y, scratch);
+  FMP_CHECK_CUDA(launch_pdl(k_dot, grid, kVecThreads, 0, st, n, x, y, scratch));
   FMP_CHECK_LAUNCH();
   return finish_reduce(scratch, grid, 1, out, st);
 }
@@ -192,7 +210,7 @@ extern "C" int fmp_vec_axpy_dot(int64_t n, double a, const double* x, double* y,
                                 double* scratch, void* stream) {
   const int grid = vec_grid(n);
   cudaStream_t st = as_stream(stream);
-  k_axpy_dot<<<grid, kVecThreads, 0, st>>>(n, a, x, y, z, scratch);
+  FMP_CHECK_CUDA(launch_pdl(k_axpy_dot, grid, kVecThreads, 0, st, n, a, x, y, z, scratch));
   FMP_CHECK_LAUNCH();
   return finish_reduce(scratch, grid, 1, dots, st);
 }
@@ -210,7 +228,7 @@ extern "C" int fmp_vec_combine(int64_t n, const double* x, int k, const double* 
       a.v[i] = v[i0 + i];
       a.c[i] = coef[i0 + i];
     }
-    k_combine<<<vec_grid(n), kVecThreads, 0, st>>>(n, src, a, out);
+    FMP_CHECK_CUDA(launch_pdl(k_combine, vec_grid(n), kVecThreads, 0, st, n, src, a, out));
     FMP_CHECK_LAUNCH();
     src = out;
     if (k == 0) break;
@@ -221,7 +239,7 @@ extern "C" int fmp_vec_combine(int64_t n, const double* x, int k, const double* 
 extern "C" int fmp_bicg_p(int64_t n, const double* r, double* p, const double* v, double beta, double omega,
                           void* stream) {
   if (n <= 0) return 0;
-  k_bicg_p<<<vec_grid(n), kVecThreads, 0, as_stream(stream)>>>(n, r, p, v, beta, -omega);
+  FMP_CHECK_CUDA(launch_pdl(k_bicg_p, vec_grid(n), kVecThreads, 0, as_stream(stream), n, r, p, v, beta, -omega));
   FMP_CHECK_LAUNCH();
   return 0;
 }
@@ -231,7 +249,7 @@ extern "C" int fmp_bicg_xr(int64_t n, double* x, const double* p_hat, const doub
                            double* dots, double* scratch, void* stream) {
   const int grid = vec_grid(n);
   cudaStream_t st = as_stream(stream);
-  k_bicg_xr<<<grid, kVecThreads, 0, st>>>(n, x, p_hat, s_hat, s, t, r, r_shadow, alpha, omega, scratch);
+  FMP_CHECK_CUDA(launch_pdl(k_bicg_xr, grid, kVecThreads, 0, st, n, x, p_hat, s_hat, s, t, r, r_shadow, alpha, omega, scratch));
   FMP_CHECK_LAUNCH();
   return finish_reduce(scratch, grid, 1, dots, st);
 }
