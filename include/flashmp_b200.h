@@ -212,6 +212,25 @@ int fmp_precond_apply(fmp_precond* p, const fmp_block* blk, int mode,
 int fmp_precond_apply_part(fmp_precond* p, const fmp_block* blk, int mode, int part,
                            const double* r, double* z, void* stream);
 
+/* BiCGSTAB's s = r + beta v followed by z = M s (ref: krylov.py:199-201, vec.lincomb(1.0, r,
+ * -alpha, v) then precond.apply(s)), as one apply: the forward plane pass forms s per point as
+ * each plane of r lands, applies the preconditioner to it and writes s (every owned point, so
+ * the whole block).  s and z are bit-identical to fmp_vec_lincomb(n, 1, r, beta, v, s) +
+ * fmp_precond_apply(p, blk, mode, s, z).  Blocks with ghosts, FACES mode and plans on the
+ * general / large kernels run exactly that two-pass form. */
+int fmp_precond_apply_lincomb(fmp_precond* p, const fmp_block* blk, int mode, const double* r,
+                              const double* v, double beta, double* s, double* z, void* stream);
+
+/* BiCGSTAB's direction update p_new = r + beta (p_old - omega v) followed by z = M p_new
+ * (ref: krylov.py:179-187, two vec.lincomb calls then precond.apply(p)) as one apply, the same
+ * way: the forward plane pass forms p_new per point from the landed plane of p_old and writes
+ * it.  p_new must be a separate buffer (other subdomains read p_old around the owned tiles while
+ * p_new is written).  Bit-identical to copying p_old to p_new, fmp_bicg_p on p_new, then
+ * fmp_precond_apply(p_new); blocks with ghosts etc. run exactly that. */
+int fmp_precond_apply_bicg_p(fmp_precond* p, const fmp_block* blk, int mode, const double* r,
+                             const double* p_old, const double* v, double beta, double omega,
+                             double* p_new, double* z, void* stream);
+
 /* ---------------------------------------------------------------- halo exchange (K10)
  * The ghost shell of fmp_block is filled in three phases -- 0: z faces, 1: y faces extended over
  * the z ghosts, 2: x faces extended over both (edges and corners without diagonal messages);

@@ -45,6 +45,8 @@ SIGNATURES = {
     "fmp_debug_ozaki_prof": (_i, [_p, _i]),
     "fmp_stencil_apply_part": (_i, [_p, _d, _i, _i, _i, _p, _p, _p, _p, _p, _p]),
     "fmp_precond_apply_part": (_i, [_p, _p, _i, _i, _p, _p, _p]),
+    "fmp_precond_apply_lincomb": (_i, [_p, _p, _i, _p, _p, _d, _p, _p, _p]),
+    "fmp_precond_apply_bicg_p": (_i, [_p, _p, _i, _p, _p, _p, _d, _d, _p, _p, _p]),
     "fmp_halo_slab_doubles": (_i64, [_p, _i]),
     "fmp_halo_pack": (_i, [_p, _i, _i, _p, _p, _d, _p]),
     "fmp_halo_unpack": (_i, [_p, _i, _i, _p, _d, _p, _p]),

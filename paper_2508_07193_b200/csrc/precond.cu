@@ -560,16 +560,87 @@ struct FastPlaneArgs {
   ExtTable et;
   int tma_rows;        // > 0: forward planes inside the block arrive as one TMA box of PXS x tma_rows
   int interleave;      // 1: warp gw takes items gw, gw + nw, ... (round-robin plane order)
+  // fused BiCGSTAB vector update (forward pass only; single block, no ghosts): the transformed
+  // input is formed per point from the landed plane X of src as
+  //   lc_kind 1 (fmp_precond_apply_lincomb): s = X + beta v                 (src = r)
+  //   lc_kind 2 (fmp_precond_apply_bicg_p):  p = r + beta (X + gamma v)      (src = p_old)
+  // and each owned point's value is written to lc_out, rounded exactly as the vector kernels
+  int lc_kind;         // 0: plain apply of src
+  int lc_prefetch;     // 1: L2 prefetch of the next item's operand rows (FMP_LC_PREFETCH=1, A/B)
+  const double* lc_r;
+  const double* lc_v;
+  double lc_beta, lc_gamma;
+  double* lc_out;
 };
 
-// K1 (INV=false): plane k of S_i r -> Fy X Fx^T -> work;  K4 (INV=true): work plane -> Fy^T X Fx -> owned z
-// Every warp owns whole plane items and never waits on another warp.  The step-1 result T
-// overwrites the plane buffer in place (rows m of T are written only after rows m of X were
-// consumed), so a warp needs one 36x36 buffer and 12 warps (3 per SM sub-partition) fit; the
-// other warps of a sub-partition hide each warp's load latency.  Row/column tiles are taken
-// two at a time (10 independent DMMA chains, 0.7 fragment loads per DMMA).
+// The fused vector update over one landed forward plane (X = the plane in shared memory, src
+// values), in place; owned points also go to A.lc_out.  Points outside the block stay zero (every
+// operand is zero there).  U points' loads in flight per lane; (j, i) walked without division.
+// Planes of subdomains inside the block take the unchecked path: one base pointer per operand,
+// a point at base + j bx + i.
+template <int KIND, bool INSIDE>
+__device__ __forceinline__ void plane_lincomb(double* X, const FastPlaneArgs& A, const SubD& d, int c, int z,
+                                              int lane) {
+  const int ex = d.ex, n = ex * d.ey, kz = d.lz + z, bx = A.g.bx;
+  if (!INSIDE && (unsigned)kz >= (unsigned)A.g.bz) return;
+  const bool zown = z >= d.oz && z < d.oz + d.wz;
+  const double beta = A.lc_beta, gamma = A.lc_gamma;
+  const int64_t o0 = fidx(A.g, c, kz, d.ly, d.lx);   // may point outside the block (!INSIDE): offsets only
+  const double* v0 = A.lc_v + o0;
+  const double* r0 = A.lc_r + o0;
+  double* s0 = A.lc_out + o0;
+  int j = 0, i = lane;
+  while (i >= ex) { i -= ex; ++j; }
+  constexpr int U = 8;
+  for (int q0 = 0; q0 < n; q0 += 32 * U) {
+    double v[U], r[U];
+    int jj[U], ii[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      jj[u] = j;
+      ii[u] = i;
+      bool ok = q0 + u * 32 + lane < n;
+      if (!INSIDE) ok = ok && (unsigned)(d.ly + j) < (unsigned)A.g.by && (unsigned)(d.lx + i) < (unsigned)bx;
+      const int64_t o = (int64_t)j * bx + i;
+      v[u] = ok ? v0[o] : 0.0;
+      if (KIND == 2) r[u] = ok ? r0[o] : 0.0;
+      i += 32;
+      while (i >= ex) { i -= ex; ++j; }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      bool ok = q0 + u * 32 + lane < n;
+      if (!INSIDE) ok = ok && (unsigned)(d.ly + jj[u]) < (unsigned)A.g.by && (unsigned)(d.lx + ii[u]) < (unsigned)bx;
+      if (ok) {
+        double* xp = X + jj[u] * PXS + ii[u];
+        double sv;
+        if (KIND == 1)   // ref:krylov.py:199, 126: s = 1.0 r + (-alpha) v
+          sv = __dadd_rn(*xp, __dmul_rn(beta, v[u]));
+        else             // ref:krylov.py:181-182 (k_bicg_p): p = 1.0 r + beta (1.0 p + (-omega) v)
+          sv = __dadd_rn(r[u], __dmul_rn(beta, __dadd_rn(*xp, __dmul_rn(gamma, v[u]))));
+        *xp = sv;
+        if (zown && (unsigned)(jj[u] - d.oy) < (unsigned)d.wy && (unsigned)(ii[u] - d.ox) < (unsigned)d.wx)
+          s0[(int64_t)jj[u] * bx + ii[u]] = sv;
+      }
+    }
+  }
+}
 
-// step 1 for NM consecutive 8-row tiles starting at m0: T[rows][a] = sum_i X[rows][i] Fx[a][i]
+// L2 prefetch of one forward plane's rows of field f (clipped to the block): one bulk prefetch
+// per row and lane
+__device__ __forceinline__ void prefetch_plane_l2(const double* f, const FastPlaneArgs& A, const SubD& d, int c,
+                                                  int z, int lane) {
+  const int kz = d.lz + z, x0 = max(d.lx, 0), x1 = min(d.lx + d.ex, A.g.bx);
+  if ((unsigned)kz >= (unsigned)A.g.bz || x1 <= x0) return;
+  for (int jj = lane; jj < d.ey; jj += 32) {
+    const int gy = d.ly + jj;
+    if ((unsigned)gy >= (unsigned)A.g.by) continue;
+    const uintptr_t s = (uintptr_t)(f + fidx(A.g, c, kz, gy, x0)) & ~(uintptr_t)15;
+    const uintptr_t e = ((uintptr_t)(f + fidx(A.g, c, kz, gy, x1)) + 15) & ~(uintptr_t)15;
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(s), "r"((unsigned)(e - s)) : "memory");
+  }
+}
+
 template <bool INV, int NM, int nt = 5>
 __device__ __forceinline__ void plane_step1(const double* X, double* T, const double* Fx, int m0, int k4, int g,
                                             int t, int coff = 0) {
@@ -786,6 +857,27 @@ __global__ void __launch_bounds__(PW_WARPS * 32, 1) k_plane_fast(const __grid_co
     const int4 w = w_cur;
     const SubD& d = d_cur;
     const int c = w.y;
+    if (!INV && A.lc_kind) {
+      if (A.lc_prefetch && it + stp < end) {   // the next item's operands into L2 (its record is an L1/L2 hit)
+        const SubD dn = w_nxt.x != w_cur.x ? load_sub(A.subs + w_nxt.x) : d_cur;
+        prefetch_plane_l2(A.lc_v, A, dn, w_nxt.y, w_nxt.z, lane);
+        if (A.lc_kind == 2) prefetch_plane_l2(A.lc_r, A, dn, w_nxt.y, w_nxt.z, lane);
+      }
+      const bool inside = d.lx >= 0 && d.ly >= 0 && d.lz >= 0 && d.lx + d.ex <= A.g.bx && d.ly + d.ey <= A.g.by &&
+                          d.lz + d.ez <= A.g.bz;
+      if (A.lc_kind == 1) {
+        if (inside)
+          plane_lincomb<1, true>(T + shift, A, d, c, w.z, lane);
+        else
+          plane_lincomb<1, false>(T + shift, A, d, c, w.z, lane);
+      } else {
+        if (inside)
+          plane_lincomb<2, true>(T + shift, A, d, c, w.z, lane);
+        else
+          plane_lincomb<2, false>(T + shift, A, d, c, w.z, lane);
+      }
+      __syncwarp();
+    }
     const double* Fx = res_factor(smem, A.et, c, 0, d.ex);
     const double* Fy = res_factor(smem, A.et, c, 1, d.ey);
     const double* X = T + shift;
@@ -2898,8 +2990,17 @@ static int column_pass(fmp_precond* p, bool inv, const double* src, double* dst,
   return 0;
 }
 
+// the fused Krylov vector update of the forward plane pass (FastPlaneArgs::lc_kind)
+struct LincombOp {
+  int kind = 0;
+  const double* r = nullptr;
+  const double* v = nullptr;
+  double beta = 0.0, gamma = 0.0;
+  double* out = nullptr;
+};
+
 static int plane_pass(fmp_precond* p, const fmp_block* blk, bool inv, int mode, const double* src, double* dst,
-                      cudaStream_t st, int part = FMP_PART_ALL) {
+                      cudaStream_t st, int part = FMP_PART_ALL, const LincombOp& lc = LincombOp()) {
   if (p->fast) {
     FastPlaneArgs a{};
     a.subs = p->d.subs;
@@ -2918,6 +3019,13 @@ static int plane_pass(fmp_precond* p, const fmp_block* blk, bool inv, int mode, 
     a.mode = mode;
     a.et = p->et;
     a.interleave = getenv_flag("FMP_PLANE_CONTIG") ? 0 : 1;   // round-robin planes (DRAM page locality)
+    a.lc_kind = inv ? 0 : lc.kind;
+    a.lc_prefetch = getenv_flag("FMP_LC_PREFETCH") ? 1 : 0;
+    a.lc_r = lc.r;
+    a.lc_v = lc.v;
+    a.lc_beta = lc.beta;
+    a.lc_gamma = lc.gamma;
+    a.lc_out = lc.out;
     CUtensorMap tm{};
     a.tma_rows = 0;
     if (!inv && mode != FMP_SOLVE_FACES && (blk->bx & 1) == 0 && ((uintptr_t)src & 15) == 0 &&
@@ -2995,7 +3103,15 @@ static int plane_pass(fmp_precond* p, const fmp_block* blk, bool inv, int mode, 
 }
 
 static int precond_apply(fmp_precond* p, const fmp_block* blk, int mode, int part, const double* r, double* z,
-                         void* stream);
+                         void* stream, const LincombOp& lc = LincombOp());
+
+// the fused forms need the fast kernels and a block without ghosts (ghost planes of the input
+// would have to be formed from the operands' ghosts); FACES mode reads compact fields
+static bool fusable(const fmp_precond* p, const fmp_block* blk, int mode) {
+  bool ghosts = false;
+  for (int q = 0; q < 6; ++q) ghosts |= blk->ghost[q] != nullptr;
+  return p->fast && !ghosts && mode != FMP_SOLVE_FACES && !getenv_flag("FMP_NO_FUSED_LINCOMB");
+}
 
 extern "C" int fmp_precond_apply(fmp_precond* p, const fmp_block* blk, int mode, const double* r, double* z,
                                  void* stream) {
@@ -3008,8 +3124,45 @@ extern "C" int fmp_precond_apply_part(fmp_precond* p, const fmp_block* blk, int 
   return precond_apply(p, blk, mode, part, r, z, stream);
 }
 
+extern "C" int fmp_precond_apply_lincomb(fmp_precond* p, const fmp_block* blk, int mode, const double* r,
+                                         const double* v, double beta, double* s, double* z, void* stream) {
+  FMP_REQUIRE(p && blk && r && v && s, "null argument");
+  if (!fusable(p, blk, mode)) {   // the two-pass form
+    const int64_t n = 3 * blk->bx * blk->by * blk->bz;
+    if (int e = fmp_vec_lincomb(n, 1.0, r, beta, v, s, stream)) return e;
+    return precond_apply(p, blk, mode, FMP_PART_ALL, s, z, stream);
+  }
+  LincombOp lc;
+  lc.kind = 1;
+  lc.v = v;
+  lc.beta = beta;
+  lc.out = s;
+  return precond_apply(p, blk, mode, FMP_PART_ALL, r, z, stream, lc);
+}
+
+extern "C" int fmp_precond_apply_bicg_p(fmp_precond* p, const fmp_block* blk, int mode, const double* r,
+                                        const double* p_old, const double* v, double beta, double omega,
+                                        double* p_new, double* z, void* stream) {
+  FMP_REQUIRE(p && blk && r && p_old && v && p_new, "null argument");
+  FMP_REQUIRE(p_new != p_old && p_new != r && p_new != v, "p_new must not alias an operand");
+  if (!fusable(p, blk, mode)) {   // the two-pass form (fmp_bicg_p updates in place: copy first)
+    const int64_t n = 3 * blk->bx * blk->by * blk->bz;
+    FMP_CHECK_CUDA(cudaMemcpyAsync(p_new, p_old, n * sizeof(double), cudaMemcpyDeviceToDevice, as_stream(stream)));
+    if (int e = fmp_bicg_p(n, r, p_new, v, beta, omega, stream)) return e;
+    return precond_apply(p, blk, mode, FMP_PART_ALL, p_new, z, stream);
+  }
+  LincombOp lc;
+  lc.kind = 2;
+  lc.r = r;
+  lc.v = v;
+  lc.beta = beta;
+  lc.gamma = -omega;
+  lc.out = p_new;
+  return precond_apply(p, blk, mode, FMP_PART_ALL, p_old, z, stream, lc);
+}
+
 static int precond_apply(fmp_precond* p, const fmp_block* blk, int mode, int part, const double* r, double* z,
-                         void* stream) {
+                         void* stream, const LincombOp& lc) {
   FMP_REQUIRE(p && blk, "null argument");
   FMP_REQUIRE(mode >= FMP_SOLVE_WOODBURY && mode <= FMP_SOLVE_FACES, "bad solve mode %d", mode);
   cudaStream_t st = as_stream(stream);
@@ -3025,7 +3178,7 @@ static int precond_apply(fmp_precond* p, const fmp_block* blk, int mode, int par
   const bool split = p->fast && mode != FMP_SOLVE_FACES;
   if (part != FMP_PART_BOUNDARY) mark(0);   // split: stage 0 spans interior pass, ghost wait, boundary pass
   if (part == FMP_PART_INTERIOR) return split ? plane_pass(p, blk, false, mode, r, wa, st, FMP_PART_INTERIOR) : 0;
-  if (int e = plane_pass(p, blk, false, mode, r, wa, st, split ? part : FMP_PART_ALL)) return e;
+  if (int e = plane_pass(p, blk, false, mode, r, wa, st, split ? part : FMP_PART_ALL, lc)) return e;
   mark(1);
   if (int e = column_pass(p, false, wa, wb, nullptr, st)) return e;
   mark(2);

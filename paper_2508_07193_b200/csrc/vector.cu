@@ -21,6 +21,12 @@ void set_error(const char* fmt, ...) {
   va_end(ap);
 }
 
+// the vector kernels' launches with programmatic serialisation (FMP_NO_PDL_VEC=1: ordinary, A/B)
+static bool vec_pdl() {
+  static const bool on = pdl_on() && !getenv_flag("FMP_NO_PDL_VEC");
+  return on;
+}
+
 // ---------------------------------------------------------------- reduction tail
 template <int ND>
 __global__ void __launch_bounds__(1024) k_finish(const double* __restrict__ partials, int count, double* out) {
@@ -38,9 +44,9 @@ __global__ void __launch_bounds__(1024) k_finish(const double* __restrict__ part
 
 int finish_reduce(const double* partials, int count, int nd, double* out, cudaStream_t st) {
   if (nd == 1)
-    FMP_CHECK_CUDA(launch_pdl(k_finish<1>, 1, 1024, 0, st, partials, count, out));
+    FMP_CHECK_CUDA(launch_k(vec_pdl(), k_finish<1>, 1, 1024, 0, st, partials, count, out));
   else
-    FMP_CHECK_CUDA(launch_pdl(k_finish<2>, 1, 1024, 0, st, partials, count, out));
+    FMP_CHECK_CUDA(launch_k(vec_pdl(), k_finish<2>, 1, 1024, 0, st, partials, count, out));
   FMP_CHECK_LAUNCH();
   return 0;
 }
@@ -179,21 +185,21 @@ extern "C" int64_t fmp_launch_count(void) { return g_launches.load(); }
 extern "C" int fmp_vec_lincomb(int64_t n, double a, const double* x, double b, const double* y, double* out,
                                void* stream) {
   if (n <= 0) return 0;
-  FMP_CHECK_CUDA(launch_pdl(k_lincomb, vec_grid(n), kVecThreads, 0, as_stream(stream), n, a, x, b, y, out));
+  FMP_CHECK_CUDA(launch_k(vec_pdl(), k_lincomb, vec_grid(n), kVecThreads, 0, as_stream(stream), n, a, x, b, y, out));
   FMP_CHECK_LAUNCH();
   return 0;
 }
 
 extern "C" int fmp_vec_axpy(int64_t n, double a, const double* x, double* y, void* stream) {
   if (n <= 0) return 0;
-  FMP_CHECK_CUDA(launch_pdl(k_axpy, vec_grid(n), kVecThreads, 0, as_stream(stream), n, a, x, y));
+  FMP_CHECK_CUDA(launch_k(vec_pdl(), k_axpy, vec_grid(n), kVecThreads, 0, as_stream(stream), n, a, x, y));
   FMP_CHECK_LAUNCH();
   return 0;
 }
 
 extern "C" int fmp_vec_scale(int64_t n, double a, const double* x, double* out, void* stream) {
   if (n <= 0) return 0;
-  FMP_CHECK_CUDA(launch_pdl(k_scale, vec_grid(n), kVecThreads, 0, as_stream(stream), n, a, x, out));
+  FMP_CHECK_CUDA(launch_k(vec_pdl(), k_scale, vec_grid(n), kVecThreads, 0, as_stream(stream), n, a, x, out));
   FMP_CHECK_LAUNCH();
   return 0;
 }
@@ -201,7 +207,7 @@ extern "C" int fmp_vec_scale(int64_t n, double a, const double* x, double* out, 
 extern "C" int fmp_vec_dot(int64_t n, const double* x, const double* y, double* out, double* scratch, void* stream) {
   const int grid = vec_grid(n);
   cudaStream_t st = as_stream(stream);
-  FMP_CHECK_CUDA(launch_pdl(k_dot, grid, kVecThreads, 0, st, n, x, y, scratch));
+  FMP_CHECK_CUDA(launch_k(vec_pdl(), k_dot, grid, kVecThreads, 0, st, n, x, y, scratch));
   FMP_CHECK_LAUNCH();
   return finish_reduce(scratch, grid, 1, out, st);
 }
@@ -210,7 +216,7 @@ extern "C" int fmp_vec_axpy_dot(int64_t n, double a, const double* x, double* y,
                                 double* scratch, void* stream) {
   const int grid = vec_grid(n);
   cudaStream_t st = as_stream(stream);
-  FMP_CHECK_CUDA(launch_pdl(k_axpy_dot, grid, kVecThreads, 0, st, n, a, x, y, z, scratch));
+  FMP_CHECK_CUDA(launch_k(vec_pdl(), k_axpy_dot, grid, kVecThreads, 0, st, n, a, x, y, z, scratch));
   FMP_CHECK_LAUNCH();
   return finish_reduce(scratch, grid, 1, dots, st);
 }
@@ -228,7 +234,7 @@ extern "C" int fmp_vec_combine(int64_t n, const double* x, int k, const double* 
       a.v[i] = v[i0 + i];
       a.c[i] = coef[i0 + i];
     }
-    FMP_CHECK_CUDA(launch_pdl(k_combine, vec_grid(n), kVecThreads, 0, st, n, src, a, out));
+    FMP_CHECK_CUDA(launch_k(vec_pdl(), k_combine, vec_grid(n), kVecThreads, 0, st, n, src, a, out));
     FMP_CHECK_LAUNCH();
     src = out;
     if (k == 0) break;
@@ -239,7 +245,7 @@ extern "C" int fmp_vec_combine(int64_t n, const double* x, int k, const double* 
 extern "C" int fmp_bicg_p(int64_t n, const double* r, double* p, const double* v, double beta, double omega,
                           void* stream) {
   if (n <= 0) return 0;
-  FMP_CHECK_CUDA(launch_pdl(k_bicg_p, vec_grid(n), kVecThreads, 0, as_stream(stream), n, r, p, v, beta, -omega));
+  FMP_CHECK_CUDA(launch_k(vec_pdl(), k_bicg_p, vec_grid(n), kVecThreads, 0, as_stream(stream), n, r, p, v, beta, -omega));
   FMP_CHECK_LAUNCH();
   return 0;
 }
@@ -249,7 +255,7 @@ extern "C" int fmp_bicg_xr(int64_t n, double* x, const double* p_hat, const doub
                            double* dots, double* scratch, void* stream) {
   const int grid = vec_grid(n);
   cudaStream_t st = as_stream(stream);
-  FMP_CHECK_CUDA(launch_pdl(k_bicg_xr, grid, kVecThreads, 0, st, n, x, p_hat, s_hat, s, t, r, r_shadow, alpha, omega, scratch));
+  FMP_CHECK_CUDA(launch_k(vec_pdl(), k_bicg_xr, grid, kVecThreads, 0, st, n, x, p_hat, s_hat, s, t, r, r_shadow, alpha, omega, scratch));
   FMP_CHECK_LAUNCH();
   return finish_reduce(scratch, grid, 1, dots, st);
 }

@@ -278,6 +278,22 @@ class SolvePlan:
                                                    _lib.stream())
         _lib.check(rc, "fmp_precond_apply")
 
+    def apply_lincomb(self, blk: _lib.FmpBlock, mode: int, r: torch.Tensor, v: torch.Tensor, beta: float,
+                      s: torch.Tensor, z: torch.Tensor) -> None:
+        """fmp_precond_apply_lincomb: s = r + beta v, z = M s in one apply (BiCGSTAB's s update
+        fused into the forward plane pass; bit-identical to the two-pass form)."""
+        rc = _lib.lib().fmp_precond_apply_lincomb(self._handle, C.byref(blk), mode, _lib.ptr(r), _lib.ptr(v),
+                                                  float(beta), _lib.ptr(s), _lib.ptr(z), _lib.stream())
+        _lib.check(rc, "fmp_precond_apply_lincomb")
+
+    def apply_bicg_p(self, blk: _lib.FmpBlock, mode: int, r: torch.Tensor, p_old: torch.Tensor, v: torch.Tensor,
+                     beta: float, omega: float, p_new: torch.Tensor, z: torch.Tensor) -> None:
+        """fmp_precond_apply_bicg_p: p_new = r + beta (p_old - omega v), z = M p_new in one apply."""
+        rc = _lib.lib().fmp_precond_apply_bicg_p(self._handle, C.byref(blk), mode, _lib.ptr(r), _lib.ptr(p_old),
+                                                 _lib.ptr(v), float(beta), float(omega), _lib.ptr(p_new),
+                                                 _lib.ptr(z), _lib.stream())
+        _lib.check(rc, "fmp_precond_apply_bicg_p")
+
     def path(self) -> str:
         """Transform kernel family of this plan: 'fast', 'large' or 'general' (fmp_precond_path)."""
         return {0: "general", 1: "fast", 2: "large"}[_lib.lib().fmp_precond_path(self._handle)]

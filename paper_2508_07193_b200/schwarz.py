@@ -676,6 +676,36 @@ class RasPreconditioner:
             self.plan.apply(blk, _lib.FMP_SOLVE_WOODBURY, r, z, part=_lib.FMP_PART_BOUNDARY)
         return z
 
+    def apply_lincomb_into(self, r: torch.Tensor, v: torch.Tensor, beta: float, s: torch.Tensor,
+                           z: torch.Tensor) -> torch.Tensor:
+        """s = r + beta v, then z = M s (ref:krylov.py:199-201).  On one GPU the update is formed
+        inside the apply's forward plane pass (fmp_precond_apply_lincomb, bit-identical); with
+        ghost exchanges it is the plain vector kernel followed by apply_into."""
+        if self.plan is None or self.exchanger.active:
+            _lib.call("fmp_vec_lincomb", r.numel(), 1.0, _lib.ptr(r), float(beta), _lib.ptr(v), _lib.ptr(s),
+                      _lib.stream())
+            return self.apply_into(s, z)
+        self.exchanger.check()
+        with self.timer.phase("fast_solve"):
+            self.plan.apply_lincomb(self.exchanger.block_struct(), _lib.FMP_SOLVE_WOODBURY, r, v, beta, s, z)
+        return z
+
+    def apply_bicg_p_into(self, r: torch.Tensor, p_old: torch.Tensor, v: torch.Tensor, beta: float, omega: float,
+                          p_new: torch.Tensor, z: torch.Tensor) -> torch.Tensor:
+        """p_new = r + beta (p_old - omega v), then z = M p_new (ref:krylov.py:179-187); fused into
+        the apply on one GPU (fmp_precond_apply_bicg_p, bit-identical), else the vector kernel on a
+        copy followed by apply_into."""
+        if self.plan is None or self.exchanger.active:
+            p_new.copy_(p_old)
+            _lib.call("fmp_bicg_p", r.numel(), _lib.ptr(r), _lib.ptr(p_new), _lib.ptr(v), float(beta), float(omega),
+                      _lib.stream())
+            return self.apply_into(p_new, z)
+        self.exchanger.check()
+        with self.timer.phase("fast_solve"):
+            self.plan.apply_bicg_p(self.exchanger.block_struct(), _lib.FMP_SOLVE_WOODBURY, r, p_old, v, beta, omega,
+                                   p_new, z)
+        return z
+
     def apply(self, r_dist):
         r, was_list = self.layout.as_block(r_dist)
         z = self.apply_into(r, torch.empty_like(r))

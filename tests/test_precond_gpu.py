@@ -250,3 +250,39 @@ def test_column_remainder_rows_match_dmma_tile(monkeypatch):
     monkeypatch.setenv("FMP_COL_NO_REM", "1")
     z1 = RasPreconditioner(part, 0.25, tr).apply(r)
     assert rel(z0.cpu().numpy(), z1.cpu().numpy()) <= 1e-14
+
+
+@pytest.mark.parametrize("n,grid,overlap", [(64, (2, 2, 2), 1), (96, (3, 3, 3), 1), (48, (3, 3, 3), 1),
+                                            (40, (2, 2, 2), 2)])
+def test_fused_lincomb_apply_is_bitwise_two_pass(n, grid, overlap):
+    """fmp_precond_apply_lincomb (BiCGSTAB's s = r - alpha v formed inside the forward plane pass)
+    gives exactly the s and z of fmp_vec_lincomb + fmp_precond_apply (ref:krylov.py:199-201):
+    interior subdomains (TMA planes), block-boundary ones (cp.async planes), rotated shapes,
+    16^3-class extents and overlap 2."""
+    from paper_2508_07193_b200 import Box, RasPreconditioner, make_partition, make_transport, _lib
+    part = make_partition(Box(n, n, n), grid, overlap)
+    prec = RasPreconditioner(part, 0.25, make_transport("cuda"))
+    gen = torch.Generator(device="cuda").manual_seed(7)
+    r = torch.rand(3, n, n, n, dtype=torch.float64, device="cuda", generator=gen) * 2 - 1
+    v = torch.rand(3, n, n, n, dtype=torch.float64, device="cuda", generator=gen) * 2 - 1
+    alpha = 0.731
+    s1, z1 = torch.full_like(r, float("nan")), torch.full_like(r, float("nan"))
+    prec.apply_lincomb_into(r, v, -alpha, s1, z1)
+    s2, z2 = torch.empty_like(r), torch.empty_like(r)
+    _lib.call("fmp_vec_lincomb", r.numel(), 1.0, _lib.ptr(r), -alpha, _lib.ptr(v), _lib.ptr(s2), _lib.stream())
+    prec.apply_into(s2, z2)
+    torch.cuda.synchronize()
+    assert torch.equal(s1, s2)
+    assert torch.equal(z1, z2)
+    assert prec.plan.path() == "fast"
+    # the direction update p_new = r + beta (p - omega v) fused into M p_new (ref:krylov.py:179-187)
+    p_old = torch.rand(3, n, n, n, dtype=torch.float64, device="cuda", generator=gen) * 2 - 1
+    beta, omega = 0.377, 1.19
+    p1, z1 = torch.full_like(r, float("nan")), torch.full_like(r, float("nan"))
+    prec.apply_bicg_p_into(r, p_old, v, beta, omega, p1, z1)
+    p2 = p_old.clone()
+    _lib.call("fmp_bicg_p", r.numel(), _lib.ptr(r), _lib.ptr(p2), _lib.ptr(v), beta, omega, _lib.stream())
+    prec.apply_into(p2, z2)
+    torch.cuda.synchronize()
+    assert torch.equal(p1, p2)
+    assert torch.equal(z1, z2)
