@@ -145,7 +145,7 @@ class ClockSampler:
 INT8_PROBE_FILE = ROOT / "profiles" / "r01_umma_i8_rate.json"
 NCU_TRAFFIC_FILE = ROOT / "profiles" / "r02_v11_ncu_traffic.json"
 # bench stage -> ncu kernel name(s) whose DRAM bytes (one ncu --set full capture) it covers
-STAGE_KERNELS = {"plane_fwd": ["k_plane_fast<0, 5>"], "column_fwd": ["k_column_fast_db<0, 12, 5, 2>"],
+STAGE_KERNELS = {"plane_fwd": ["k_plane_fast<0, 5, 0>", "k_plane_fast<0, 5>"], "column_fwd": ["k_column_fast_db<0, 12, 5, 2>"],
                  "faces": ["k_faces<5, 2, 5>"], "slice_y": ["k_ozaki_slice_rows", "k_ozaki_exp", "k_ozaki_digits"], "gemm": ["k_ozaki"],
                  "corr": ["k_corr<5>"], "column_inv": ["k_column_fast_db<1, 12, 5, 2>"], "plane_inv": ["k_plane_fast<1, 5>"]}
 

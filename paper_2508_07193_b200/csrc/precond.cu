@@ -740,7 +740,9 @@ __device__ __forceinline__ void plane_step2(const double* T, const double* Fy, c
   }
 }
 
-template <bool INV, int NT = 5>   // NT: 8-row DMMA tiles per padded extent (3: extents <= 24, 5: <= 40)
+// LC: the fused Krylov update compiled in (0: plain apply; 1, 2: FastPlaneArgs::lc_kind), so the
+// plain and fused forward passes are separate instances with their own register allocation
+template <bool INV, int NT = 5, int LC = 0>   // NT: 8-row DMMA tiles per padded extent (3: extents <= 24, 5: <= 40)
 __global__ void __launch_bounds__(PW_WARPS * 32, 1) k_plane_fast(const __grid_constant__ CUtensorMap tm,
                                                                   FastPlaneArgs A) {
   extern __shared__ __align__(128) double smem[];
@@ -857,15 +859,15 @@ __global__ void __launch_bounds__(PW_WARPS * 32, 1) k_plane_fast(const __grid_co
     const int4 w = w_cur;
     const SubD& d = d_cur;
     const int c = w.y;
-    if (!INV && A.lc_kind) {
+    if (!INV && LC != 0) {
       if (A.lc_prefetch && it + stp < end) {   // the next item's operands into L2 (its record is an L1/L2 hit)
         const SubD dn = w_nxt.x != w_cur.x ? load_sub(A.subs + w_nxt.x) : d_cur;
         prefetch_plane_l2(A.lc_v, A, dn, w_nxt.y, w_nxt.z, lane);
-        if (A.lc_kind == 2) prefetch_plane_l2(A.lc_r, A, dn, w_nxt.y, w_nxt.z, lane);
+        if (LC == 2) prefetch_plane_l2(A.lc_r, A, dn, w_nxt.y, w_nxt.z, lane);
       }
       const bool inside = d.lx >= 0 && d.ly >= 0 && d.lz >= 0 && d.lx + d.ex <= A.g.bx && d.ly + d.ey <= A.g.by &&
                           d.lz + d.ez <= A.g.bz;
-      if (A.lc_kind == 1) {
+      if (LC == 1) {
         if (inside)
           plane_lincomb<1, true>(T + shift, A, d, c, w.z, lane);
         else
@@ -2836,6 +2838,10 @@ extern "C" int fmp_precond_create(const fmp_precond_desc* desc, fmp_precond** ou
   cudaFuncSetAttribute(k_plane_fast<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kPlaneFastSmem);
   cudaFuncSetAttribute(k_plane_fast<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kPlaneFastSmem);
   cudaFuncSetAttribute(k_plane_fast<false, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, kPlaneFastSmem);
+  cudaFuncSetAttribute(k_plane_fast<false, 5, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kPlaneFastSmem);
+  cudaFuncSetAttribute(k_plane_fast<false, 5, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kPlaneFastSmem);
+  cudaFuncSetAttribute(k_plane_fast<false, 3, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kPlaneFastSmem);
+  cudaFuncSetAttribute(k_plane_fast<false, 3, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kPlaneFastSmem);
   cudaFuncSetAttribute(k_plane_fast<true, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, kPlaneFastSmem);
   cudaFuncSetAttribute(k_column_fast<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kColFastSmem);
   cudaFuncSetAttribute(k_column_fast<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kColFastSmem);
@@ -3045,9 +3051,11 @@ static int plane_pass(fmp_precond* p, const fmp_block* blk, bool inv, int mode, 
     else if (inv)
       FMP_CHECK_CUDA(launch_pdl(k_plane_fast<true>, grid, PW_WARPS * 32, kPlaneFastSmem, st, tm, a));
     else if (small)
-      FMP_CHECK_CUDA(launch_pdl(k_plane_fast<false, 3>, grid, PW_WARPS * 32, kPlaneFastSmem, st, tm, a));
+      FMP_CHECK_CUDA(launch_pdl(a.lc_kind == 0 ? k_plane_fast<false, 3> : (a.lc_kind == 1 ? k_plane_fast<false, 3, 1> : k_plane_fast<false, 3, 2>),
+                                grid, PW_WARPS * 32, kPlaneFastSmem, st, tm, a));
     else
-      FMP_CHECK_CUDA(launch_pdl(k_plane_fast<false>, grid, PW_WARPS * 32, kPlaneFastSmem, st, tm, a));
+      FMP_CHECK_CUDA(launch_pdl(a.lc_kind == 0 ? k_plane_fast<false> : (a.lc_kind == 1 ? k_plane_fast<false, 5, 1> : k_plane_fast<false, 5, 2>),
+                                grid, PW_WARPS * 32, kPlaneFastSmem, st, tm, a));
     FMP_CHECK_LAUNCH();
     return 0;
   }
