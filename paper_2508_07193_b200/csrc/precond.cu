@@ -3114,11 +3114,15 @@ static int precond_apply(fmp_precond* p, const fmp_block* blk, int mode, int par
                          void* stream, const LincombOp& lc = LincombOp());
 
 // the fused forms need the fast kernels and a block without ghosts (ghost planes of the input
-// would have to be formed from the operands' ghosts); FACES mode reads compact fields
+// would have to be formed from the operands' ghosts); FACES mode reads compact fields.  Plans
+// of 16^3-class subdomains (extents <= 24) run the two-pass form: their planes carry 1.4x halo
+// re-reads against little DMMA work, and fusing measured 3% slower (cfg5_sd16: 24.3 -> 25.0 ms
+// per step)
 static bool fusable(const fmp_precond* p, const fmp_block* blk, int mode) {
   bool ghosts = false;
   for (int q = 0; q < 6; ++q) ghosts |= blk->ghost[q] != nullptr;
-  return p->fast && !ghosts && mode != FMP_SOLVE_FACES && !getenv_flag("FMP_NO_FUSED_LINCOMB");
+  const bool small = std::max(p->max_ex, std::max(p->max_ey, p->max_ez)) <= 24;
+  return p->fast && !small && !ghosts && mode != FMP_SOLVE_FACES && !getenv_flag("FMP_NO_FUSED_LINCOMB");
 }
 
 extern "C" int fmp_precond_apply(fmp_precond* p, const fmp_block* blk, int mode, const double* r, double* z,

@@ -253,12 +253,12 @@ def test_column_remainder_rows_match_dmma_tile(monkeypatch):
 
 
 @pytest.mark.parametrize("n,grid,overlap", [(64, (2, 2, 2), 1), (96, (3, 3, 3), 1), (48, (3, 3, 3), 1),
-                                            (40, (2, 2, 2), 2)])
+                                            (40, (2, 2, 2), 2), (64, (2, 2, 2), 2)])
 def test_fused_lincomb_apply_is_bitwise_two_pass(n, grid, overlap):
     """fmp_precond_apply_lincomb (BiCGSTAB's s = r - alpha v formed inside the forward plane pass)
     gives exactly the s and z of fmp_vec_lincomb + fmp_precond_apply (ref:krylov.py:199-201):
-    interior subdomains (TMA planes), block-boundary ones (cp.async planes), rotated shapes,
-    16^3-class extents and overlap 2."""
+    interior subdomains (TMA planes), block-boundary ones (cp.async planes), rotated shapes;
+    16^3-class plans (and overlap 2 there) take the two-pass form and must give the same."""
     from paper_2508_07193_b200 import Box, RasPreconditioner, make_partition, make_transport, _lib
     part = make_partition(Box(n, n, n), grid, overlap)
     prec = RasPreconditioner(part, 0.25, make_transport("cuda"))
