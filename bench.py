@@ -254,6 +254,37 @@ def stage_rooflines(prec, x, z, specs, peaks, reps):
     return out
 
 
+def fused_update_rooflines(prec, x, specs, peaks, reps):
+    """The forward plane pass as it runs in 7 of the step's 8 applies: with BiCGSTAB's s update
+    (fmp_precond_apply_lincomb) or p update (fmp_precond_apply_bicg_p) fused in.  Times from the
+    same stage events as stage_rooflines; work = the plain pass's DMMA flops plus the update's
+    HBM bytes per owned DoF (s: v read + s written; p: r, v read + p written)."""
+    import torch
+    plan = prec.plan
+    if plan.path() != "fast" or max(max(sp.ext) for sp in specs) <= 24 or prec.exchanger.active:
+        return None   # plans / blocks that run the two-pass form
+    flops = sum(6 * int(np.prod(sp.ext)) * (sp.ext[0] + sp.ext[1]) for sp in specs)
+    dof = x.numel()
+    v, s, pn, z = (torch.empty_like(x) for _ in range(4))
+    v.copy_(x).mul_(0.5)
+    s.copy_(x)
+    out = {}
+    plan.profile(True)
+    for name, extra_b, fn in (("s_update", 16, lambda: prec.apply_lincomb_into(x, v, -0.3, s, z)),
+                              ("p_update", 24, lambda: prec.apply_bicg_p_into(x, s, v, 0.4, 1.1, pn, z))):
+        ms = 0.0
+        for _ in range(reps):
+            torch.cuda._sleep(2_000_000)
+            fn()
+            ms += plan.stage_ms()["plane_fwd"] / reps
+        a = flops / ms / 1e9
+        out[name] = {"kernel": f"k_plane_fast<0, 5, {1 if name == 's_update' else 2}>", "ms": round(ms, 4),
+                     "achieved_tflops": round(a, 2), "frac_dmma": round(a / peaks["fp64_tflops"], 3),
+                     "update_bytes_per_dof": extra_b, "update_gbs": round(extra_b * dof / ms / 1e6, 1)}
+    plan.profile(False)
+    return out
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -360,6 +391,7 @@ def run_ours(args):
     spmv_bytes = 48 * owned
     prec_tflops = flops_exec / t_prec / 1e12
     stages = stage_rooflines(prec, x, z, specs, peaks, reps)
+    fused_stages = fused_update_rooflines(prec, x, specs, peaks, reps)
 
     # ---- per-phase breakdown of one extra step (reference categories, ref:instrument.py:17-25)
     from paper_2508_07193_b200.instrument import PhaseTimer
@@ -432,6 +464,7 @@ def run_ours(args):
                           "flops_executed": flops_exec, "tflops_executed": round(prec_tflops, 2),
                           "tflops_reference_count": round(flops_ref / t_prec / 1e12, 2)},
         "precond_kernels": stages,
+        "plane_fwd_fused_update": fused_stages,
         "spmv": {"ms": round(t_spmv * 1e3, 4), "GB_per_s": round(spmv_bytes / t_spmv / 1e9, 1),
                  "algorithmic_bytes": spmv_bytes,
                  "traffic_bytes": ncu_traffic().get("k_spmv_bulk<0, 4>", {}).get("traffic_bytes"),
