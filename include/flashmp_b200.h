@@ -88,7 +88,8 @@ int fmp_stencil_apply_part(const fmp_block* blk, double alpha, int boundary, int
 int fmp_curl(const fmp_block* blk, int kind, const double* x, double* out, void* stream);
 
 /* CN right-hand side R = E + dt*curl_b(H) - (dt^2/4)*C_b C_f E    ref: cn_driver.py:54-59.
- * blkE / blkH carry the ghosts of E and H respectively. */
+ * blkE / blkH carry the ghosts of E and H respectively.  Runs on the SpMV's TMA z-march (E
+ * through the plane ring, H read per point); FMP_CN_RHS_POINT=1: thread-per-point kernel. */
 int fmp_cn_rhs(const fmp_block* blkE, const fmp_block* blkH, double dt,
                const double* E, const double* H, double* R, void* stream);
 

@@ -156,6 +156,21 @@ __global__ void __launch_bounds__(TX* TY) k_spmv(Geo g, double alpha, int bnd, c
   }
 }
 
+// curl at one point (used by the CN stencils and the CN right-hand side mode of the z-march)
+template <int KIND, bool GEN>  // 0 forward, 1 backward
+__device__ __forceinline__ void curl_at(const Loader<GEN>& L, int k, int j, int i, double& cx, double& cy,
+                                        double& cz) {
+  const double ex = L(0, k, j, i), ey = L(1, k, j, i), ez = L(2, k, j, i);
+  if (KIND == 0) {  // D^f u(i) = u(i+1) - u(i), zero beyond the high face (ref:operators.py:94-96)
+    cx = (L(2, k, j + 1, i) - ez) - (L(1, k + 1, j, i) - ey);
+    cy = (L(0, k + 1, j, i) - ex) - (L(2, k, j, i + 1) - ez);
+    cz = (L(1, k, j, i + 1) - ey) - (L(0, k, j + 1, i) - ex);
+  } else {  // D^b u(i) = u(i) - u(i-1), zero before the low face (ref:operators.py:97-99)
+    cx = (ez - L(2, k, j - 1, i)) - (ey - L(1, k - 1, j, i));
+    cy = (ex - L(0, k - 1, j, i)) - (ez - L(2, k, j, i - 1));
+    cz = (ey - L(1, k, j, i - 1)) - (ex - L(0, k, j - 1, i));
+  }
+}
 // ---------------------------------------------------------------- SpMV, TMA z-march (sm_100a)
 // Warp-specialised.  A producer warp streams each haloed plane of all three components
 // ([3][SY+2][SX+4] doubles, 16 KB) into a 4-slot shared-memory ring with ONE TMA box load per
@@ -189,6 +204,11 @@ struct BulkSpmvArgs {
   double alpha;
   int bnd, tiles_x, tiles_y, L, nzc, ghosts;
   int wpf;   // modes 1-3: L2 prefetch distance (planes) of the w operand, 0 = off
+  // mode 4 (CN right-hand side, fmp_cn_rhs): y = (x + dt curl_b(h)) - alpha C_b C_f x with x = E
+  // streamed through the ring, h = H read per point (its ghosts in gh), bnd = 0 (no Lambda)
+  Geo gh;
+  const double* h;
+  double dt;
 };
 
 template <int MODE, int SNSLOT>
@@ -360,13 +380,22 @@ __global__ void __launch_bounds__(STHREADS, SNSLOT <= 4 ? 3 : 2) k_spmv_bulk(con
         const double yx = id ? ex + A.alpha * tx : A.alpha * tx, yy = id ? ey + A.alpha * ty : A.alpha * ty,
                      yz = id ? ez + A.alpha * tz : A.alpha * tz;
         const int64_t oi = fidx(g, 0, k, j, i);
-        if (MODE >= 1 && A.wpf > 0 && k + A.wpf < g.bz) {   // w of a later plane of this column into L2
+        if (MODE >= 1 && MODE <= 3 && A.wpf > 0 && k + A.wpf < g.bz) {   // w of a later plane of this column into L2
           const double* wn = A.w + oi + (int64_t)A.wpf * g.bx * g.by;
           asm volatile("prefetch.global.L2 [%0];" ::"l"(wn));
           asm volatile("prefetch.global.L2 [%0];" ::"l"(wn + V));
           asm volatile("prefetch.global.L2 [%0];" ::"l"(wn + 2 * V));
         }
-        if (MODE == 3) {
+        if (MODE == 4) {   // ref:cn_driver.py:54-59, same evaluation order as k_cn_rhs
+          double hx, hy, hz;
+          if (i >= 1 && j >= 1 && k >= 1)
+            curl_at<1>(Loader<false>{A.gh, A.h}, k, j, i, hx, hy, hz);
+          else
+            curl_at<1>(Loader<true>{A.gh, A.h}, k, j, i, hx, hy, hz);
+          __stcs(A.y + oi, (ex + A.dt * hx) - A.alpha * tx);
+          __stcs(A.y + oi + V, (ey + A.dt * hy) - A.alpha * ty);
+          __stcs(A.y + oi + 2 * V, (ez + A.dt * hz) - A.alpha * tz);
+        } else if (MODE == 3) {
           const double rx = A.w[oi] - yx, ry = A.w[oi + V] - yy, rz = A.w[oi + 2 * V] - yz;
           acc0 += rx * rx + ry * ry + rz * rz;
         } else {
@@ -388,7 +417,7 @@ __global__ void __launch_bounds__(STHREADS, SNSLOT <= 4 ? 3 : 2) k_spmv_bulk(con
       }
     }
     qbase += np + 2;
-    if (MODE >= 1) {   // this unit's partial(s): consumer-only reduction (named barrier 1)
+    if (MODE >= 1 && MODE <= 3) {   // this unit's partial(s): consumer-only reduction (named barrier 1)
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
         acc0 += __shfl_xor_sync(0xffffffffu, acc0, o);
@@ -416,20 +445,6 @@ __global__ void __launch_bounds__(STHREADS, SNSLOT <= 4 ? 3 : 2) k_spmv_bulk(con
 // ---------------------------------------------------------------- curls and CN stencils
 // A point whose stencil stays inside the block reads with plain loads (Loader<false>); only the
 // block's surface layer goes through fetch() (global zero boundary, neighbour ghosts).
-template <int KIND, bool GEN>  // 0 forward, 1 backward
-__device__ __forceinline__ void curl_at(const Loader<GEN>& L, int k, int j, int i, double& cx, double& cy,
-                                        double& cz) {
-  const double ex = L(0, k, j, i), ey = L(1, k, j, i), ez = L(2, k, j, i);
-  if (KIND == 0) {  // D^f u(i) = u(i+1) - u(i), zero beyond the high face (ref:operators.py:94-96)
-    cx = (L(2, k, j + 1, i) - ez) - (L(1, k + 1, j, i) - ey);
-    cy = (L(0, k + 1, j, i) - ex) - (L(2, k, j, i + 1) - ez);
-    cz = (L(1, k, j, i + 1) - ey) - (L(0, k, j + 1, i) - ex);
-  } else {  // D^b u(i) = u(i) - u(i-1), zero before the low face (ref:operators.py:97-99)
-    cx = (ez - L(2, k, j - 1, i)) - (ey - L(1, k - 1, j, i));
-    cy = (ex - L(0, k - 1, j, i)) - (ez - L(2, k, j, i - 1));
-    cz = (ey - L(1, k, j, i - 1)) - (ex - L(0, k, j - 1, i));
-  }
-}
 __device__ __forceinline__ bool inner(const Geo& g, int k, int j, int i) {
   return i >= 1 && j >= 1 && k >= 1 && i + 1 < g.bx && j + 1 < g.by && k + 1 < g.bz;
 }
@@ -574,7 +589,8 @@ static int unit_list(const Geo& g, int tiles_x, int tiles_y, int L, int nzc, int
 }
 
 static int stencil_apply(const fmp_block* blk, double alpha, int boundary, int mode, int part, const double* x,
-                         double* y, const double* w, double* dots, double* scratch, void* stream);
+                         double* y, const double* w, double* dots, double* scratch, void* stream,
+                         const fmp_block* blkH = nullptr, const double* H = nullptr, double dt = 0.0);
 
 extern "C" int fmp_stencil_apply(const fmp_block* blk, double alpha, int boundary, int mode, const double* x,
                                  double* y, const double* w, double* dots, double* scratch, void* stream) {
@@ -589,11 +605,13 @@ extern "C" int fmp_stencil_apply_part(const fmp_block* blk, double alpha, int bo
 }
 
 static int stencil_apply(const fmp_block* blk, double alpha, int boundary, int mode, int part, const double* x,
-                         double* y, const double* w, double* dots, double* scratch, void* stream) {
+                         double* y, const double* w, double* dots, double* scratch, void* stream,
+                         const fmp_block* blkH, const double* H, double dt) {
   if (int e = check_block(blk)) return e;
-  FMP_REQUIRE(mode >= 0 && mode <= 3, "bad stencil mode %d", mode);
+  FMP_REQUIRE((mode >= 0 && mode <= 3) || (mode == 4 && blkH && H), "bad stencil mode %d", mode);
   FMP_REQUIRE(boundary >= 0 && boundary <= 3, "bad stencil boundary flags %d", boundary);
-  FMP_REQUIRE(mode == 0 || (w && dots && scratch), "mode %d needs w, dots and scratch", mode);
+  const bool reduces = mode >= 1 && mode <= 3;   // modes with fused dot products
+  FMP_REQUIRE(!reduces || (w && dots && scratch), "mode %d needs w, dots and scratch", mode);
   const Geo g = make_geo(blk);
   cudaStream_t st = as_stream(stream);
   if (bulk_ok(blk, x)) {
@@ -608,8 +626,8 @@ static int stencil_apply(const fmp_block* blk, double alpha, int boundary, int m
 #define FMP_SPMV_ATTR(M, N)                                                                            \
   FMP_CHECK_CUDA(cudaFuncSetAttribute(k_spmv_bulk<M, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                                       spmv_bulk_smem(N)));
-      FMP_SPMV_ATTR(0, 4) FMP_SPMV_ATTR(1, 4) FMP_SPMV_ATTR(2, 4) FMP_SPMV_ATTR(3, 4)
-      FMP_SPMV_ATTR(0, 6) FMP_SPMV_ATTR(1, 6) FMP_SPMV_ATTR(2, 6) FMP_SPMV_ATTR(3, 6)
+      FMP_SPMV_ATTR(0, 4) FMP_SPMV_ATTR(1, 4) FMP_SPMV_ATTR(2, 4) FMP_SPMV_ATTR(3, 4) FMP_SPMV_ATTR(4, 4)
+      FMP_SPMV_ATTR(0, 6) FMP_SPMV_ATTR(1, 6) FMP_SPMV_ATTR(2, 6) FMP_SPMV_ATTR(3, 6) FMP_SPMV_ATTR(4, 6)
 #undef FMP_SPMV_ATTR
       int r = 0;
       FMP_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r, k_spmv_bulk<0, 4>, STHREADS, spmv_bulk_smem(4)));
@@ -627,6 +645,11 @@ static int stencil_apply(const fmp_block* blk, double alpha, int boundary, int m
     a.partials = scratch;
     a.alpha = alpha;
     a.bnd = boundary;
+    if (mode == 4) {
+      a.gh = make_geo(blkH);
+      a.h = H;
+      a.dt = dt;
+    }
     a.tiles_x = (g.bx + SX - 1) / SX;
     a.tiles_y = (g.by + SY - 1) / SY;
     a.ghosts = 0;
@@ -654,13 +677,13 @@ static int stencil_apply(const fmp_block* blk, double alpha, int boundary, int m
     const int64_t ntiles = (int64_t)a.tiles_x * a.tiles_y;
     const int64_t resident = (int64_t)kNumSM * resident_per_sm;
     spmv_chunking(ntiles, g.bz, resident, &a.L, &a.nzc);
-    if (mode >= 1)   // one partial per unit (two in mode 2) must fit the scratch: longer chunks
+    if (reduces)   // one partial per unit (two in mode 2) must fit the scratch: longer chunks
       while (ntiles * a.nzc > kScratchDoubles / 2 && a.L < g.bz) {
         a.L = std::min(g.bz, 2 * a.L);
         a.nzc = (g.bz + a.L - 1) / a.L;
       }
     const int64_t units = ntiles * a.nzc;
-    FMP_REQUIRE(mode == 0 || units <= kScratchDoubles / 2, "block too large for the SpMV reduction scratch");
+    FMP_REQUIRE(!reduces || units <= kScratchDoubles / 2, "block too large for the SpMV reduction scratch");
     a.ulist = nullptr;
     a.nlaunch = units;
     if (part != FMP_PART_ALL) {
@@ -679,6 +702,7 @@ static int stencil_apply(const fmp_block* blk, double alpha, int boundary, int m
     case 1: FMP_CHECK_CUDA(launch_pdl(k_spmv_bulk<1, N>, grid, STHREADS, spmv_bulk_smem(N), st, tm, a)); break;                \
     case 2: FMP_CHECK_CUDA(launch_pdl(k_spmv_bulk<2, N>, grid, STHREADS, spmv_bulk_smem(N), st, tm, a)); break;                \
     case 3: FMP_CHECK_CUDA(launch_pdl(k_spmv_bulk<3, N>, grid, STHREADS, spmv_bulk_smem(N), st, tm, a)); break;                \
+    case 4: FMP_CHECK_CUDA(launch_pdl(k_spmv_bulk<4, N>, grid, STHREADS, spmv_bulk_smem(N), st, tm, a)); break;                \
   }
     if (ns == 4) {
       FMP_SPMV_GO(4)
@@ -690,9 +714,10 @@ static int stencil_apply(const fmp_block* blk, double alpha, int boundary, int m
     }
     // the interior part leaves its per-unit partials in scratch; the boundary part adds its own
     // and reduces all of them in the fixed unit order
-    if (mode >= 1 && part != FMP_PART_INTERIOR) return finish_reduce(scratch, (int)units, mode == 2 ? 2 : 1, dots, st);
+    if (reduces && part != FMP_PART_INTERIOR) return finish_reduce(scratch, (int)units, mode == 2 ? 2 : 1, dots, st);
     return 0;
   }
+  FMP_REQUIRE(mode != 4, "CN right-hand side mode needs the bulk path");
   if (part == FMP_PART_INTERIOR) return 0;   // the thread-per-point fallback runs whole in the boundary part
   const int tx = (g.bx + TX - 1) / TX, ty = (g.by + TY - 1) / TY;
   const int64_t units = (int64_t)tx * ty * g.bz;
@@ -726,6 +751,8 @@ extern "C" int fmp_curl(const fmp_block* blk, int kind, const double* x, double*
 extern "C" int fmp_cn_rhs(const fmp_block* blkE, const fmp_block* blkH, double dt, const double* E, const double* H,
                           double* R, void* stream) {
   if (int e = check_block(blkE)) return e;
+  if (bulk_ok(blkE, E) && !getenv_flag("FMP_CN_RHS_POINT"))   // E through the TMA z-march ring (mode 4)
+    return stencil_apply(blkE, dt * dt / 4.0, 0, 4, FMP_PART_ALL, E, R, nullptr, nullptr, nullptr, stream, blkH, H, dt);
   const Geo gE = make_geo(blkE), gH = make_geo(blkH);
   const dim3 grid((gE.bx + CBX - 1) / CBX, (gE.by + CBY - 1) / CBY, gE.bz), block(CBX, CBY);
   FMP_CHECK_CUDA(launch_pdl(k_cn_rhs, grid, block, 0, as_stream(stream), gE, gH, dt, E, H, R));

@@ -196,3 +196,27 @@ def test_stencil_full_256_block_matches_oracle():
     got = stencil_apply(dev(x, (n, n, n)), 0.25, True).cpu().numpy()
     want = O.apply_A(0.25, x, True)
     assert np.abs(got - want).max() <= 1e-14 * np.abs(want).max()
+
+
+@pytest.mark.parametrize("ext", [(64, 48, 40), (70, 33, 9), (8, 8, 8)])
+def test_cn_rhs_zmarch_matches_point_kernel(ext, monkeypatch):
+    """fmp_cn_rhs on the TMA z-march (SpMV mode 4: E through the plane ring, curl_b(H) per point)
+    against the thread-per-point k_cn_rhs (FMP_CN_RHS_POINT=1), ref:cn_driver.py:54-59 (the
+    reference-pinned CN tests in test_krylov_gpu.py run the z-march path).  The two kernels sum
+    the C_b C_f bracket in different orders, so they agree to rounding, not bitwise."""
+    from paper_2508_07193_b200 import _lib
+    from paper_2508_07193_b200.plan import block_struct
+    gen = torch.Generator(device="cuda").manual_seed(11)
+    E = torch.rand(3, ext[2], ext[1], ext[0], dtype=torch.float64, device="cuda", generator=gen) * 2 - 1
+    H = torch.rand(3, ext[2], ext[1], ext[0], dtype=torch.float64, device="cuda", generator=gen) * 2 - 1
+    blk = block_struct(*ext)
+    out = []
+    for flag in ("0", "1"):
+        monkeypatch.setenv("FMP_CN_RHS_POINT", flag)
+        R = torch.full_like(E, float("nan"))
+        _lib.call("fmp_cn_rhs", _lib.ref(blk), _lib.ref(blk), 0.7, _lib.ptr(E), _lib.ptr(H), _lib.ptr(R),
+                  _lib.stream())
+        torch.cuda.synchronize()
+        out.append(R.cpu().numpy())
+    assert np.isfinite(out[0]).all()
+    assert np.max(np.abs(out[0] - out[1])) <= 1e-14 * np.max(np.abs(out[1]))
