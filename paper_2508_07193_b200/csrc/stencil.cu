@@ -204,6 +204,7 @@ struct BulkSpmvArgs {
   double alpha;
   int bnd, tiles_x, tiles_y, L, nzc, ghosts;
   int wpf;   // modes 1-3: L2 prefetch distance (planes) of the w operand, 0 = off
+  int wlate; // modes 1-3: w read after the stencil (FMP_SPMV_WLATE=1, A/B)
   // mode 4 (CN right-hand side, fmp_cn_rhs): y = (x + dt curl_b(h)) - alpha C_b C_f x with x = E
   // streamed through the ring, h = H read per point (its ghosts in gh), bnd = 0 (no Lambda)
   Geo gh;
@@ -339,6 +340,19 @@ __global__ void __launch_bounds__(STHREADS, SNSLOT <= 4 ? 3 : 2) k_spmv_bulk(con
       const double* p0 = ring + ((q0 + 1) % SNSLOT) * SSLOT;
       const double* pp = ring + ((q0 + 2) % SNSLOT) * SSLOT;
       const int k = k0 + jz, j = j0 + ly;
+      // modes 1-3: this plane's w operand, loaded before the stencil so its latency overlaps the
+      // shared-memory reads and arithmetic (FMP_SPMV_WLATE=1: loaded after, A/B)
+      double wv[2][3];
+      if (MODE >= 1 && MODE <= 3 && !A.wlate) {
+#pragma unroll
+        for (int hx = 0; hx < 2; ++hx) {
+          const int i = i0 + lx + 32 * hx;
+          const bool in = i < g.bx && j < g.by;
+          const int64_t oi = in ? fidx(g, 0, k, j, i) : 0;
+#pragma unroll
+          for (int c = 0; c < 3; ++c) wv[hx][c] = in ? A.w[oi + c * V] : 0.0;
+        }
+      }
 #define EX(P, dj, di) P[0 * SPL + o + (dj) * SXR + (di)]
 #define EY(P, dj, di) P[1 * SPL + o + (dj) * SXR + (di)]
 #define EZ(P, dj, di) P[2 * SPL + o + (dj) * SXR + (di)]
@@ -396,13 +410,19 @@ __global__ void __launch_bounds__(STHREADS, SNSLOT <= 4 ? 3 : 2) k_spmv_bulk(con
           __stcs(A.y + oi + V, (ey + A.dt * hy) - A.alpha * ty);
           __stcs(A.y + oi + 2 * V, (ez + A.dt * hz) - A.alpha * tz);
         } else if (MODE == 3) {
-          const double rx = A.w[oi] - yx, ry = A.w[oi + V] - yy, rz = A.w[oi + 2 * V] - yz;
+          const double w0 = A.wlate ? A.w[oi] : wv[hx][0], w1 = A.wlate ? A.w[oi + V] : wv[hx][1],
+                       w2 = A.wlate ? A.w[oi + 2 * V] : wv[hx][2];
+          const double rx = w0 - yx, ry = w1 - yy, rz = w2 - yz;
           acc0 += rx * rx + ry * ry + rz * rz;
         } else {
           __stcs(A.y + oi, yx);   // streaming stores: keep L2 for the halo planes and rows
           __stcs(A.y + oi + V, yy);
           __stcs(A.y + oi + 2 * V, yz);
-          if (MODE >= 1) acc0 += yx * A.w[oi] + yy * A.w[oi + V] + yz * A.w[oi + 2 * V];
+          if (MODE >= 1) {
+            const double w0 = A.wlate ? A.w[oi] : wv[hx][0], w1 = A.wlate ? A.w[oi + V] : wv[hx][1],
+                         w2 = A.wlate ? A.w[oi + 2 * V] : wv[hx][2];
+            acc0 += yx * w0 + yy * w1 + yz * w2;
+          }
           if (MODE == 2) acc1 += yx * yx + yy * yy + yz * yz;
         }
       }
@@ -658,6 +678,7 @@ static int stencil_apply(const fmp_block* blk, double alpha, int boundary, int m
     // latency sits in every consumer step; prefetching the next plane's w into L2 hides it
     // (bench.py: 2434 -> 2463 MDoF/s at cfg4; FMP_SPMV_WPF=0 turns it off)
     a.wpf = getenv("FMP_SPMV_WPF") ? atoi(getenv("FMP_SPMV_WPF")) : 1;
+    a.wlate = getenv_flag("FMP_SPMV_WLATE") ? 1 : 0;
     // [fetch, done] counter pairs of the unit scheduler, zero at rest (each launch re-arms its
     // own pair).  A ring of pairs, so launches in flight on different streams or devices of this
     // process never share one (per device: the ring is allocated on the current device).
