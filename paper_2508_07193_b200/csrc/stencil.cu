@@ -343,6 +343,19 @@ __global__ void __launch_bounds__(STHREADS, SNSLOT <= 4 ? 3 : 2) k_spmv_bulk(con
       // modes 1-3: this plane's w operand, loaded before the stencil so its latency overlaps the
       // shared-memory reads and arithmetic (FMP_SPMV_WLATE=1: loaded after, A/B)
       double wv[2][3];
+      if (MODE == 4) {   // curl_b(H) of this plane's two points, ahead of the stencil likewise
+#pragma unroll
+        for (int hx = 0; hx < 2; ++hx) {
+          const int i = i0 + lx + 32 * hx;
+          wv[hx][0] = wv[hx][1] = wv[hx][2] = 0.0;
+          if (i < g.bx && j < g.by) {
+            if (i >= 1 && j >= 1 && k >= 1)
+              curl_at<1>(Loader<false>{A.gh, A.h}, k, j, i, wv[hx][0], wv[hx][1], wv[hx][2]);
+            else
+              curl_at<1>(Loader<true>{A.gh, A.h}, k, j, i, wv[hx][0], wv[hx][1], wv[hx][2]);
+          }
+        }
+      }
       if (MODE >= 1 && MODE <= 3 && !A.wlate) {
 #pragma unroll
         for (int hx = 0; hx < 2; ++hx) {
@@ -401,14 +414,9 @@ __global__ void __launch_bounds__(STHREADS, SNSLOT <= 4 ? 3 : 2) k_spmv_bulk(con
           asm volatile("prefetch.global.L2 [%0];" ::"l"(wn + 2 * V));
         }
         if (MODE == 4) {   // ref:cn_driver.py:54-59, same evaluation order as k_cn_rhs
-          double hx, hy, hz;
-          if (i >= 1 && j >= 1 && k >= 1)
-            curl_at<1>(Loader<false>{A.gh, A.h}, k, j, i, hx, hy, hz);
-          else
-            curl_at<1>(Loader<true>{A.gh, A.h}, k, j, i, hx, hy, hz);
-          __stcs(A.y + oi, (ex + A.dt * hx) - A.alpha * tx);
-          __stcs(A.y + oi + V, (ey + A.dt * hy) - A.alpha * ty);
-          __stcs(A.y + oi + 2 * V, (ez + A.dt * hz) - A.alpha * tz);
+          __stcs(A.y + oi, (ex + A.dt * wv[hx][0]) - A.alpha * tx);
+          __stcs(A.y + oi + V, (ey + A.dt * wv[hx][1]) - A.alpha * ty);
+          __stcs(A.y + oi + 2 * V, (ez + A.dt * wv[hx][2]) - A.alpha * tz);
         } else if (MODE == 3) {
           const double w0 = A.wlate ? A.w[oi] : wv[hx][0], w1 = A.wlate ? A.w[oi + V] : wv[hx][1],
                        w2 = A.wlate ? A.w[oi + 2 * V] : wv[hx][2];
