@@ -129,6 +129,11 @@ int fmp_bicg_p(int64_t n, const double* r, double* p, const double* v,
 int fmp_bicg_xr(int64_t n, double* x, const double* p_hat, const double* s_hat,
                 const double* s, const double* t, double* r, const double* r_shadow,
                 double alpha, double omega, double* dots, double* scratch, void* stream);
+/* The same for x = 0 on entry (BiCGSTAB's first iteration, ref: krylov.py:154 x = zeros_like(b)): x is
+ * written without being read, so it needs no zero fill; bit-identical to fmp_bicg_xr on a zeroed x. */
+int fmp_bicg_xr0(int64_t n, double* x, const double* p_hat, const double* s_hat,
+                 const double* s, const double* t, double* r, const double* r_shadow,
+                 double alpha, double omega, double* dots, double* scratch, void* stream);
 
 /* ---------------------------------------------------------------- subdomain solves (K1-K5)
  * A preconditioner plan batches every subdomain of one GPU block.  Subdomains are

@@ -34,6 +34,7 @@ SIGNATURES = {
     "fmp_vec_combine": (_i, [_i64, _p, _i, _p, _p, _p, _p]),
     "fmp_bicg_p": (_i, [_i64, _p, _p, _p, _d, _d, _p]),
     "fmp_bicg_xr": (_i, [_i64, _p, _p, _p, _p, _p, _p, _p, _d, _d, _p, _p, _p]),
+    "fmp_bicg_xr0": (_i, [_i64, _p, _p, _p, _p, _p, _p, _p, _d, _d, _p, _p, _p]),
     "fmp_precond_create": (_i, [_p, C.POINTER(_p)]),
     "fmp_precond_destroy": (_i, [_p]),
     "fmp_precond_apply": (_i, [_p, _p, _i, _p, _p, _p]),

@@ -98,7 +98,10 @@ __global__ void k_bicg_p(int64_t n, const double* __restrict__ r, double* __rest
 }
 
 // x += alpha*p_hat; x += omega*s_hat; r = 1.0*s + (-omega)*t; rho_next partial = (r_shadow, r)
-// (ref:krylov.py:213-215 and the next iteration's krylov.py:171)
+// (ref:krylov.py:213-215 and the next iteration's krylov.py:171).  XZERO: x is zero on entry (the
+// first iteration): the zero is a literal, so x is written without being read or pre-filled,
+// with the same rounding (0.0 + a == a, +0.0 for a == -0.0, as when a stored zero is read)
+template <bool XZERO>
 __global__ void __launch_bounds__(kVecThreads) k_bicg_xr(int64_t n, double* __restrict__ x,
                                                          const double* __restrict__ ph,
                                                          const double* __restrict__ sh,
@@ -112,7 +115,7 @@ __global__ void __launch_bounds__(kVecThreads) k_bicg_xr(int64_t n, double* __re
   double acc = 0.0;
   const double momega = -omega;
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x) {
-    double xv = add_rn(x[q], mul_rn(alpha, ph[q]));
+    double xv = add_rn(XZERO ? 0.0 : x[q], mul_rn(alpha, ph[q]));
     x[q] = add_rn(xv, mul_rn(omega, sh[q]));
     const double rv = add_rn(s[q], mul_rn(momega, t[q]));
     r[q] = rv;
@@ -250,12 +253,25 @@ extern "C" int fmp_bicg_p(int64_t n, const double* r, double* p, const double* v
   return 0;
 }
 
+static int bicg_xr(bool xzero, int64_t n, double* x, const double* p_hat, const double* s_hat, const double* s,
+                   const double* t, double* r, const double* r_shadow, double alpha, double omega, double* dots,
+                   double* scratch, void* stream) {
+  const int grid = vec_grid(n);
+  cudaStream_t st = as_stream(stream);
+  FMP_CHECK_CUDA(launch_k(vec_pdl(), xzero ? k_bicg_xr<true> : k_bicg_xr<false>, grid, kVecThreads, 0, st, n, x, p_hat,
+                          s_hat, s, t, r, r_shadow, alpha, omega, scratch));
+  FMP_CHECK_LAUNCH();
+  return finish_reduce(scratch, grid, 1, dots, st);
+}
+
 extern "C" int fmp_bicg_xr(int64_t n, double* x, const double* p_hat, const double* s_hat, const double* s,
                            const double* t, double* r, const double* r_shadow, double alpha, double omega,
                            double* dots, double* scratch, void* stream) {
-  const int grid = vec_grid(n);
-  cudaStream_t st = as_stream(stream);
-  FMP_CHECK_CUDA(launch_k(vec_pdl(), k_bicg_xr, grid, kVecThreads, 0, st, n, x, p_hat, s_hat, s, t, r, r_shadow, alpha, omega, scratch));
-  FMP_CHECK_LAUNCH();
-  return finish_reduce(scratch, grid, 1, dots, st);
+  return bicg_xr(false, n, x, p_hat, s_hat, s, t, r, r_shadow, alpha, omega, dots, scratch, stream);
+}
+
+extern "C" int fmp_bicg_xr0(int64_t n, double* x, const double* p_hat, const double* s_hat, const double* s,
+                            const double* t, double* r, const double* r_shadow, double alpha, double omega,
+                            double* dots, double* scratch, void* stream) {
+  return bicg_xr(true, n, x, p_hat, s_hat, s, t, r, r_shadow, alpha, omega, dots, scratch, stream);
 }

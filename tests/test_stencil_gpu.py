@@ -220,3 +220,28 @@ def test_cn_rhs_zmarch_matches_point_kernel(ext, monkeypatch):
         out.append(R.cpu().numpy())
     assert np.isfinite(out[0]).all()
     assert np.max(np.abs(out[0] - out[1])) <= 1e-14 * np.max(np.abs(out[1]))
+
+
+def test_bicg_xr0_is_bicg_xr_on_zero_x():
+    """fmp_bicg_xr0 (x = 0 on entry, written without being read) gives bit for bit the x, r and
+    next rho of fmp_bicg_xr on a zeroed x, signed zeros included (ref:krylov.py:154, 213-216)."""
+    from paper_2508_07193_b200 import _lib
+    n = 3 * 40 * 33 * 17
+    gen = torch.Generator(device="cuda").manual_seed(5)
+    ph, sh, s, t, rs = (torch.rand(n, dtype=torch.float64, device="cuda", generator=gen) * 2 - 1 for _ in range(5))
+    ph[::7] = -0.0
+    sh[::7] = 0.0
+    scratch = torch.zeros(int(_lib.lib().fmp_reduce_scratch_doubles()), dtype=torch.float64, device="cuda")
+    outs = []
+    for name in ("fmp_bicg_xr", "fmp_bicg_xr0"):
+        x = torch.zeros(n, dtype=torch.float64, device="cuda") if name == "fmp_bicg_xr" else \
+            torch.full((n,), float("nan"), dtype=torch.float64, device="cuda")
+        r = torch.empty_like(x)
+        dots = torch.zeros(2, dtype=torch.float64, device="cuda")
+        _lib.call(name, n, _lib.ptr(x), _lib.ptr(ph), _lib.ptr(sh), _lib.ptr(s), _lib.ptr(t), _lib.ptr(r),
+                  _lib.ptr(rs), 0.37, -1.3, _lib.ptr(dots), _lib.ptr(scratch), _lib.stream())
+        torch.cuda.synchronize()
+        outs.append((x.cpu().numpy(), r.cpu().numpy(), dots[0].item()))
+    (x0, r0, d0), (x1, r1, d1) = outs
+    assert np.array_equal(x0.view(np.int64), x1.view(np.int64))
+    assert np.array_equal(r0, r1) and d0 == d1
